@@ -1,0 +1,235 @@
+/*
+ * vxm.h — the C-ABI between the voxmap host library (C++, include/voxmap/)
+ * and the hand-written sm_100a kernels in paper_2112_13169_b200/csrc/.
+ *
+ * Plain C: pointers, sizes and PODs only; no torch or C++ types; no C++
+ * exceptions cross it. Every entry point that can fail returns an int status
+ * (VXM_OK == 0); the message is available from vxm_last_error() (per calling
+ * thread). The C++ wrapper rethrows VXM_EINVAL as std::invalid_argument, like
+ * the reference, and everything else as std::runtime_error.
+ *
+ * The reference interfaces each group replaces are cited next to it
+ * (paths relative to /root/reference).
+ *
+ * Threading: a vxm_ctx owns one cudaStream_t, its device buffers and a
+ * captured CUDA graph per frame shape; one caller at a time per context
+ * (proj/include/voxmap/pipeline.hpp:50-74 has the same single-caller rule,
+ * SPEC.md:387). Distinct contexts are independent and may be driven from
+ * different host threads / GPUs concurrently.
+ */
+#ifndef VXM_H_
+#define VXM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VXM_ABI_VERSION 1
+
+enum vxm_status {
+  VXM_OK = 0,
+  VXM_EINVAL = 1,   /* precondition violated (reference: std::invalid_argument) */
+  VXM_ECUDA = 2,    /* CUDA runtime / launch failure */
+  VXM_ENOMEM = 3,   /* device or pinned host allocation failed */
+  VXM_ENODEV = 4,   /* no sm_100 device visible */
+  VXM_ESTATE = 5    /* call not valid in the context's current state */
+};
+
+/* Voxel states, one byte per cell (proj/include/voxmap/voxel_state.hpp:9-17). */
+enum vxm_voxel_state {
+  VXM_UNKNOWN = 0,
+  VXM_FREE = 1,
+  VXM_OCCUPIED = 2,
+  VXM_UNKNOWN_TRACED = 3
+};
+
+/* Which tracer frees space (proj/include/voxmap/exec.hpp:13-16). */
+enum vxm_tracer_mode { VXM_TRACER_BUNDLED = 0, VXM_TRACER_PER_PIXEL = 1 };
+
+/* GridSpec (proj/include/voxmap/grid.hpp:27-35). Cells are stored flat,
+ * idx = x + y*dims[0] + z*dims[0]*dims[1] (grid.hpp:72-77). */
+typedef struct vxm_grid_spec {
+  double size[3];   /* grid_size_x/y/z, meters */
+  double vox_size;  /* meters */
+  int32_t dims[3];  /* lround(size / vox_size) per axis */
+  int32_t pad_;
+  double origin[3]; /* world position of the minimum corner */
+} vxm_grid_spec;
+
+/* CameraModel (proj/include/voxmap/geometry.hpp:60-72). */
+typedef struct vxm_camera {
+  double fov_x;     /* radians */
+  double fov_y;     /* radians */
+  int32_t width;
+  int32_t height;
+  double max_depth; /* meters */
+} vxm_camera;
+
+/* PipelineConfig (proj/include/voxmap/pipeline.hpp:11-22). ExecutionMode is
+ * not carried: the GPU path is always deterministic and equals the
+ * reference's Sequential mode bit for bit. */
+typedef struct vxm_config {
+  vxm_grid_spec grid;
+  vxm_camera camera;
+  int32_t vox_inf;      /* IntegratorConfig::vox_inf */
+  int32_t tracer_mode;  /* enum vxm_tracer_mode */
+  double depth;         /* clearing range, meters */
+} vxm_config;
+
+/* RigidTransform (geometry.hpp:16-40): p' = R p + t, R row-major. */
+typedef struct vxm_pose {
+  double rotation[9];
+  double translation[3];
+} vxm_pose;
+
+/* PipelineStats + TraceStats + PopulateStats (pipeline.hpp:30-41,
+ * raytracer.hpp:44-57, integrator.hpp:18-21). The *_us fields are device
+ * times of the stages measured with CUDA events only when the context was
+ * created with VXM_FLAG_STAGE_TIMING, else 0. */
+typedef struct vxm_stats {
+  uint64_t points_total;
+  uint64_t points_outside;
+  uint64_t rays_traced;
+  uint64_t voxels_freed;
+  uint64_t voxels_marked_unknown_traced;
+  uint64_t voxels_skipped_out_of_bounds;
+  uint64_t occupied_count;
+  uint64_t freed_count;
+  int32_t shifted;
+  int32_t shift_offset[3];
+  double origin[3];  /* local-grid origin after this frame */
+  double populate_us, trace_us, merge_us, shift_us;
+} vxm_stats;
+
+/* ------------------------------------------------------------------------ */
+/* Host-side helpers (pure host arithmetic, same formulas as the reference). */
+
+/* GridSpec::create / create_centered (proj/src/grid.cpp:17-52). */
+int vxm_grid_spec_create(double size_x, double size_y, double size_z, double vox_size,
+                         const double origin[3], vxm_grid_spec* out);
+int vxm_grid_spec_create_centered(double size_x, double size_y, double size_z,
+                                  double vox_size, const double center[3],
+                                  vxm_grid_spec* out);
+/* bundle_dimensions (proj/src/raytracer.cpp:8-21): out = {vox_depth, vox_width, vox_height}. */
+int vxm_bundle_dimensions(const vxm_camera* cam, double depth, double vox_size,
+                          int32_t out[3]);
+
+/* Thread-local message of the last failing call on this thread. */
+const char* vxm_last_error(void);
+/* "cuda-sm100a" plus build info. */
+const char* vxm_build_info(void);
+/* Number of visible CUDA devices of compute capability 10.x (0 when none). */
+int vxm_device_count(void);
+
+/* ------------------------------------------------------------------------ */
+/* Per-stream mapping contexts: MappingPipeline (pipeline.hpp:50-74;
+ * proj/src/pipeline.cpp:68-117) for n_streams independent sensor streams
+ * that share one configuration, processed as one batch per call.
+ * n_streams == 1 is the plain MappingPipeline. */
+
+typedef struct vxm_ctx vxm_ctx;
+
+#define VXM_FLAG_STAGE_TIMING 1u  /* record per-stage CUDA events (adds syncs) */
+#define VXM_FLAG_NO_GRAPH 2u      /* launch kernels directly instead of a CUDA graph */
+
+/* cfg->grid must already be placed (use vxm_grid_spec_create_centered to
+ * centre it on the first camera position, pipeline.cpp:71-72). Validates as
+ * PipelineConfig::validate (pipeline.cpp:33-42). */
+int vxm_create(const vxm_config* cfg, int32_t n_streams, int32_t device, uint32_t flags,
+               vxm_ctx** out);
+int vxm_destroy(vxm_ctx* ctx);
+int vxm_num_streams(const vxm_ctx* ctx);
+
+/* MappingPipeline::integrate for a depth frame:
+ * integrate(MeasurementFrame{depth_to_cloud(img, cam), t_wc}) with the
+ * back-projection fused into the first kernel (geometry.cpp:43-99).
+ * depth: n_streams * width * height floats, HOST memory, row-major per frame.
+ * poses: n_streams camera->world transforms. stats: n_streams outputs.
+ * Synchronous: copies in, runs, copies the stats back. */
+int vxm_integrate_depth(vxm_ctx* ctx, const float* depth, const vxm_pose* t_wc,
+                        vxm_stats* stats);
+
+/* Same, with the depth frames already in device memory (n_streams*W*H
+ * floats). Asynchronous on the context's stream: returns after enqueueing;
+ * read the stats with vxm_wait_stats(). */
+int vxm_integrate_depth_device(vxm_ctx* ctx, const float* depth_dev, const vxm_pose* t_wc);
+int vxm_wait_stats(vxm_ctx* ctx, vxm_stats* stats);
+
+/* MappingPipeline::integrate(MeasurementFrame{cloud, t_wc}) for n_streams == 1
+ * with an arbitrary camera-frame point cloud (double SoA, HOST memory). */
+int vxm_integrate_cloud(vxm_ctx* ctx, const double* xs, const double* ys, const double* zs,
+                        size_t n, const vxm_pose* t_wc, vxm_stats* stats);
+
+/* local_grid() (pipeline.hpp:67): copies stream `s`'s local grid (cell_count
+ * bytes) and its origin to HOST memory. */
+int vxm_download_local(vxm_ctx* ctx, int32_t s, uint8_t* cells, double origin[3]);
+/* Restores stream `s`'s local grid (checkpoint/resume, grid_io.cpp:14-63). */
+int vxm_upload_local(vxm_ctx* ctx, int32_t s, const uint8_t* cells, const double origin[3]);
+
+/* The context's CUDA stream (cudaStream_t) and the device time of the last
+ * integrate call's kernels in milliseconds (CUDA events on that stream). */
+void* vxm_cuda_stream(vxm_ctx* ctx);
+int vxm_last_frame_ms(vxm_ctx* ctx, float* ms);
+
+/* ------------------------------------------------------------------------ */
+/* Stage entry points on HOST grids (the free functions of the public API).
+ * Each uploads, runs the same kernels as the pipeline, and downloads. */
+
+typedef struct vxm_populate_stats { uint64_t points_total, points_outside; } vxm_populate_stats;
+typedef struct vxm_trace_stats {
+  uint64_t rays_traced, voxels_freed, voxels_marked_unknown_traced,
+      voxels_skipped_out_of_bounds;
+} vxm_trace_stats;
+
+/* populate_occupied (proj/include/voxmap/integrator.hpp:29-31,
+ * proj/src/integrator.cpp:45-103). ms: cell_count bytes, updated in place. */
+int vxm_populate_occupied(const vxm_grid_spec* grid, uint8_t* ms, const double* xs,
+                          const double* ys, const double* zs, size_t n,
+                          const vxm_pose* t_vc, int32_t vox_inf, vxm_populate_stats* st);
+
+/* trace_bundle (proj/include/voxmap/raytracer.hpp:127-132,
+ * proj/src/raytracer.cpp:98-118), Sequential semantics. bundle = {vd, vw, vh}. */
+int vxm_trace_bundle(const vxm_grid_spec* grid, uint8_t* ms, const int32_t bundle[3],
+                     const vxm_pose* t_vc, vxm_trace_stats* st);
+
+/* bresenham_trace_image (raytracer.hpp:196-202, raytracer.cpp:120-161), Sequential
+ * semantics (last writer in point order wins). */
+int vxm_trace_per_pixel(const vxm_grid_spec* grid, uint8_t* ms, const double* xs,
+                        const double* ys, const double* zs, size_t n, const vxm_pose* t_vc,
+                        vxm_trace_stats* st);
+
+/* merge_grids (proj/include/voxmap/pipeline.hpp:47-48, pipeline.cpp:44-61). */
+int vxm_merge_grids(uint8_t* local, const uint8_t* measurement, size_t n);
+
+/* shift_grid_by (proj/include/voxmap/grid.hpp:133, proj/src/grid.cpp:81-108):
+ * out[c] = in[c + offset] when in bounds, else Unknown. */
+int vxm_shift_grid(const int32_t dims[3], const uint8_t* in, uint8_t* out,
+                   const int32_t offset[3]);
+
+/* depth_to_cloud (proj/include/voxmap/geometry.hpp:131-132,
+ * proj/src/geometry.cpp:64-99): row-major compaction of valid pixels.
+ * xs/ys/zs must hold width*height doubles; *n_out receives the point count. */
+int vxm_depth_to_cloud(const vxm_camera* cam, const float* depth, double* xs, double* ys,
+                       double* zs, size_t* n_out);
+
+/* ------------------------------------------------------------------------ */
+/* KernelTable adapter (proj/include/voxmap/kernels/kernels.hpp:8-33): the
+ * exact MergeFn / TransformVoxelizeFn signatures, HOST pointers, void, no
+ * allocation visible to the caller, any alignment, any n (including 0).
+ * Errors abort with a message: the reference signature has no error channel.
+ * Useful for parity (each call pays H2D + D2H). */
+void vxm_kernel_merge(uint8_t* local, const uint8_t* measurement, size_t n);
+void vxm_kernel_transform_voxelize(const double* xs, const double* ys, const double* zs,
+                                   size_t n, const double* rotation,
+                                   const double* translation, double vox_size, int32_t* cx,
+                                   int32_t* cy, int32_t* cz);
+const char* vxm_kernel_isa(void); /* "cuda-sm100a" */
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VXM_H_ */
