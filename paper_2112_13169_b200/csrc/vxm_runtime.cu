@@ -1,0 +1,712 @@
+// C-ABI runtime (include/vxm.h): per-stream mapping contexts, the per-frame
+// CUDA graph, and the stand-alone stage entry points.
+//
+// Per-frame flow for a context of S streams (MappingPipeline::integrate,
+// proj/src/pipeline.cpp:74-117, batched over streams):
+//   host:  validate t_wc, T_vc = compose(T(-origin), t_wc), shift decision,
+//          epoch bump -> FrameParams[S] in pinned memory
+//   H2D:   FrameParams (and the depth frames for the host-buffer entry point)
+//   graph: memset counters | K1 populate | K2 dilate (vox_inf > 0) |
+//          K3 trace_bundle | K4 merge+shift+count | D2H counters
+// The measurement grid is never reset: epoch-tagged words (vxm_device.cuh).
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/vxm.h"
+#include "vxm_aux_kernels.cuh"
+#include "vxm_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+struct CudaError {
+  int code;
+};
+
+#define VXM_CK(call)                                                                      \
+  do {                                                                                    \
+    const cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess) {                                                              \
+      g_err = std::string(#call) + ": " + cudaGetErrorString(e_);                         \
+      throw CudaError{e_ == cudaErrorMemoryAllocation ? VXM_ENOMEM : VXM_ECUDA};          \
+    }                                                                                     \
+  } while (0)
+
+struct InvalidArg {
+  std::string what;
+};
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return VXM_OK;
+  } catch (const CudaError& e) {
+    return e.code;
+  } catch (const InvalidArg& e) {
+    return fail(VXM_EINVAL, e.what);
+  } catch (const std::bad_alloc&) {
+    return fail(VXM_ENOMEM, "host allocation failed");
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host arithmetic, operation for operation as the reference.
+// ---------------------------------------------------------------------------
+
+// GridSpec::create (proj/src/grid.cpp:17-42).
+void spec_create(double sx, double sy, double sz, double vs, const double origin[3],
+                 vxm_grid_spec* out) {
+  if (!(vs > 0.0)) throw InvalidArg{"vox_size must be positive"};
+  if (!(sx > 0.0) || !(sy > 0.0) || !(sz > 0.0)) throw InvalidArg{"grid sizes must be positive"};
+  for (int a = 0; a < 3; ++a)
+    if (!std::isfinite(origin[a])) throw InvalidArg{"grid origin must be finite"};
+  out->size[0] = sx;
+  out->size[1] = sy;
+  out->size[2] = sz;
+  out->vox_size = vs;
+  out->dims[0] = static_cast<int>(std::lround(sx / vs));
+  out->dims[1] = static_cast<int>(std::lround(sy / vs));
+  out->dims[2] = static_cast<int>(std::lround(sz / vs));
+  out->pad_ = 0;
+  for (int a = 0; a < 3; ++a) out->origin[a] = origin[a];
+  if (out->dims[0] < 1 || out->dims[1] < 1 || out->dims[2] < 1)
+    throw InvalidArg{"grid must be at least one voxel per axis"};
+}
+
+// GridSpec::half_extent (grid.hpp:56-60): integer halving, then * vox_size.
+double half_extent(const vxm_grid_spec& g, int a) {
+  return static_cast<double>(g.dims[a] / 2) * g.vox_size;
+}
+
+// CameraModel::validate (proj/src/geometry.cpp:28-41).
+void camera_validate(const vxm_camera& c) {
+  if (c.width <= 0 || c.height <= 0)
+    throw InvalidArg{"CameraModel: width and height must be positive"};
+  const double pi = 3.14159265358979323846;
+  if (!(c.fov_x > 0.0) || !(c.fov_x < pi) || !(c.fov_y > 0.0) || !(c.fov_y < pi))
+    throw InvalidArg{"CameraModel: FOV must lie in (0, pi)"};
+  if (!(c.max_depth > 0.0) || !std::isfinite(c.max_depth))
+    throw InvalidArg{"CameraModel: max_depth must be positive and finite"};
+}
+
+// bundle_dimensions (proj/src/raytracer.cpp:8-21).
+void bundle_dims(const vxm_camera& cam, double depth, double vs, int32_t out[3]) {
+  camera_validate(cam);
+  if (!(depth > 0.0) || !std::isfinite(depth))
+    throw InvalidArg{"bundle_dimensions: depth must be positive and finite"};
+  if (!(vs > 0.0) || !std::isfinite(vs))
+    throw InvalidArg{"bundle_dimensions: vox_size must be positive and finite"};
+  out[0] = std::max(1, static_cast<int>(std::lround(depth / vs)));
+  out[1] = 2 * static_cast<int>(std::lround(std::tan(cam.fov_x / 2.0) * out[0])) + 1;
+  out[2] = 2 * static_cast<int>(std::lround(std::tan(cam.fov_y / 2.0) * out[0])) + 1;
+}
+
+bool all_finite(const double* v, int n) {
+  for (int i = 0; i < n; ++i)
+    if (!std::isfinite(v[i])) return false;
+  return true;
+}
+
+// RigidTransform::is_valid (proj/src/geometry.cpp:17-22) with the Eigen
+// subset's arithmetic: gram = R^T R (left-to-right dot products), max |gram-I|,
+// determinant by cofactors of the first column.
+bool pose_valid(const vxm_pose& p, double tol) {
+  if (!all_finite(p.rotation, 9) || !all_finite(p.translation, 3)) return false;
+  auto R = [&](int i, int j) { return p.rotation[3 * i + j]; };
+  double worst = 0.0;
+  bool first = true;
+  for (int j = 0; j < 3; ++j) {
+    for (int i = 0; i < 3; ++i) {
+      double acc = R(0, i) * R(0, j);
+      acc = acc + R(1, i) * R(1, j);
+      acc = acc + R(2, i) * R(2, j);
+      double d = acc - (i == j ? 1.0 : 0.0);
+      d = d < 0.0 ? -d : d;
+      if (first || d > worst) worst = d;
+      first = false;
+    }
+  }
+  if (worst > tol) return false;
+  const double det = R(0, 0) * (R(1, 1) * R(2, 2) - R(2, 1) * R(1, 2)) -
+                     R(1, 0) * (R(0, 1) * R(2, 2) - R(2, 1) * R(0, 2)) +
+                     R(2, 0) * (R(0, 1) * R(1, 2) - R(1, 1) * R(0, 2));
+  return std::abs(det - 1.0) <= tol;
+}
+
+// camera_to_grid_transform = compose(T(-origin), t_wc) (pipeline.cpp:63-66,
+// geometry.cpp:24-26): R_vc = I * R_wc, t_vc = I * t_wc + (-origin), each
+// product a left-to-right dot product as in the Eigen subset.
+void camera_to_grid(const vxm_pose& t_wc, const double origin[3], double rot[9],
+                    double trans[3]) {
+  for (int i = 0; i < 3; ++i) {
+    for (int j = 0; j < 3; ++j) {
+      double acc = (i == 0 ? 1.0 : 0.0) * t_wc.rotation[0 * 3 + j];
+      acc = acc + (i == 1 ? 1.0 : 0.0) * t_wc.rotation[1 * 3 + j];
+      acc = acc + (i == 2 ? 1.0 : 0.0) * t_wc.rotation[2 * 3 + j];
+      rot[3 * i + j] = acc;
+    }
+    double acc = (i == 0 ? 1.0 : 0.0) * t_wc.translation[0];
+    acc = acc + (i == 1 ? 1.0 : 0.0) * t_wc.translation[1];
+    acc = acc + (i == 2 ? 1.0 : 0.0) * t_wc.translation[2];
+    trans[i] = acc + (-origin[i]);
+  }
+}
+
+// The recentring rule of MappingPipeline::integrate (pipeline.cpp:102-112)
+// and shift_offset_for_center (grid.cpp:110-117). Returns true when the grid
+// moves; `origin` is updated to the shifted grid's origin (grid.cpp:84).
+bool shift_decision(const vxm_grid_spec& g, double origin[3], const double t[3], int32_t off[3]) {
+  const double vs = g.vox_size;
+  bool drifted = false;
+  for (int a = 0; a < 3; ++a) {
+    const double center = origin[a] + half_extent(g, a);
+    double drift = t[a] - center;
+    drift = drift < 0.0 ? -drift : drift;
+    if (drift >= vs) drifted = true;
+  }
+  off[0] = off[1] = off[2] = 0;
+  if (!drifted) return false;
+  for (int a = 0; a < 3; ++a) {
+    const double ideal = t[a] - half_extent(g, a);
+    const double delta = (ideal - origin[a]) / vs;
+    off[a] = static_cast<int32_t>(std::lround(delta));
+  }
+  if (off[0] == 0 && off[1] == 0 && off[2] == 0) return false;
+  for (int a = 0; a < 3; ++a) origin[a] = origin[a] + static_cast<double>(off[a]) * vs;
+  return true;
+}
+
+int sm_count(int device) {
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+  return n > 0 ? n : 148;
+}
+
+void check_device(int device) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    g_err = "no CUDA device visible";
+    throw CudaError{VXM_ENODEV};
+  }
+  if (device < 0 || device >= count) throw InvalidArg{"device index out of range"};
+  cudaDeviceProp prop;
+  VXM_CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) {
+    g_err = std::string("device ") + prop.name + " is not sm_100 (this build targets sm_100a only)";
+    throw CudaError{VXM_ENODEV};
+  }
+}
+
+constexpr int kPopulateThreads = 256;
+constexpr int kTraceThreads = 128;
+constexpr int kMergeThreads = 256;
+
+}  // namespace
+
+void vxm_set_error(const char* msg) { g_err = msg ? msg : ""; }
+
+// ---------------------------------------------------------------------------
+// Context
+// ---------------------------------------------------------------------------
+struct vxm_ctx {
+  vxm_config cfg{};
+  int S = 1;
+  int device = 0;
+  uint32_t flags = 0;
+  int nsm = 148;
+  cudaStream_t stream = nullptr;
+  vxm::KParams kp{};
+  long long n = 0;
+  int32_t bundle[3] = {0, 0, 0};
+
+  // device buffers
+  uint32_t* msw = nullptr;
+  uint32_t* ctr = nullptr;
+  uint8_t* loc[2] = {nullptr, nullptr};
+  vxm::Counters* counters = nullptr;
+  vxm::FrameParams* frames_dev = nullptr;
+  float* depth_dev = nullptr;
+  double* cloud_dev = nullptr;
+  size_t cloud_cap = 0;
+
+  // pinned host mirrors
+  vxm::FrameParams* frames_host = nullptr;
+  vxm::Counters* counters_host = nullptr;
+
+  // host state per stream
+  std::vector<uint32_t> epoch;
+  std::vector<uint32_t> cur;
+  std::vector<double> origin;  // 3 per stream
+  std::vector<int32_t> last_off;
+  std::vector<int32_t> last_shifted;
+
+  cudaGraphExec_t graph_depth = nullptr;
+  cudaGraphExec_t graph_cloud = nullptr;
+  cudaEvent_t ev[6] = {};
+  bool pending = false;
+  float last_ms = 0.f;
+  double stage_us[4] = {0, 0, 0, 0};
+};
+
+namespace {
+
+void launch_frame(vxm_ctx* c, bool cloud, bool timed) {
+  const int S = c->S;
+  vxm::KParams kp = c->kp;
+  if (timed) VXM_CK(cudaEventRecord(c->ev[1], c->stream));
+  VXM_CK(cudaMemsetAsync(c->counters, 0, sizeof(vxm::Counters) * S, c->stream));
+  if (!cloud) {
+    const long long npix = static_cast<long long>(kp.W) * kp.H;
+    const long long quads = (npix + 3) / 4;
+    dim3 grid(static_cast<unsigned>((quads + kPopulateThreads - 1) / kPopulateThreads), S);
+    vxm::populate_depth_kernel<<<grid, kPopulateThreads, 0, c->stream>>>(kp);
+  } else {
+    dim3 grid(static_cast<unsigned>(c->nsm * 4), S);
+    vxm::populate_cloud_kernel<<<grid, kPopulateThreads, 0, c->stream>>>(kp);
+  }
+  VXM_CK(cudaGetLastError());
+  if (kp.vox_inf > 0) {
+    const int r = kp.vox_inf;
+    const int HX = vxm::kDilTX + 2 * r, HY = vxm::kDilTY + 2 * r, HZ = vxm::kDilTZ + 2 * r;
+    const size_t smem = static_cast<size_t>(HX) * HY * HZ + static_cast<size_t>(vxm::kDilTX) * HY * HZ +
+                        static_cast<size_t>(vxm::kDilTX) * vxm::kDilTY * HZ;
+    dim3 grid(static_cast<unsigned>(((kp.dx + vxm::kDilTX - 1) / vxm::kDilTX) *
+                                    ((kp.dy + vxm::kDilTY - 1) / vxm::kDilTY)),
+              static_cast<unsigned>((kp.dz + vxm::kDilTZ - 1) / vxm::kDilTZ), S);
+    vxm::dilate_kernel<<<grid, 256, smem, c->stream>>>(kp, r);
+    VXM_CK(cudaGetLastError());
+  }
+  if (timed) VXM_CK(cudaEventRecord(c->ev[2], c->stream));
+  {
+    const int tiles = kp.tiles_x * kp.tiles_y;
+    const int warps_per_block = kTraceThreads / 32;
+    dim3 grid(static_cast<unsigned>((tiles + warps_per_block - 1) / warps_per_block), S);
+    vxm::trace_bundle_kernel<<<grid, kTraceThreads, 0, c->stream>>>(kp);
+    VXM_CK(cudaGetLastError());
+  }
+  if (timed) VXM_CK(cudaEventRecord(c->ev[3], c->stream));
+  {
+    const long long quads = (c->n + 3) / 4;
+    const long long want = (quads + kMergeThreads - 1) / kMergeThreads;
+    const long long cap = static_cast<long long>(c->nsm) * 8;
+    dim3 grid(static_cast<unsigned>(std::max(1LL, std::min(want, cap))), S);
+    vxm::merge_shift_count_kernel<<<grid, kMergeThreads, 0, c->stream>>>(kp);
+    VXM_CK(cudaGetLastError());
+  }
+  if (timed) VXM_CK(cudaEventRecord(c->ev[4], c->stream));
+  VXM_CK(cudaMemcpyAsync(c->counters_host, c->counters, sizeof(vxm::Counters) * S,
+                         cudaMemcpyDeviceToHost, c->stream));
+}
+
+cudaGraphExec_t capture(vxm_ctx* c, bool cloud) {
+  cudaGraph_t g = nullptr;
+  VXM_CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    launch_frame(c, cloud, false);
+  } catch (...) {
+    cudaStreamEndCapture(c->stream, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  VXM_CK(cudaStreamEndCapture(c->stream, &g));
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
+  cudaGraphDestroy(g);
+  VXM_CK(e);
+  return exec;
+}
+
+// Host half of one frame for every stream: validation, T_vc, shift, epoch.
+void prepare_frames(vxm_ctx* c, const vxm_pose* poses, const float* depth_dev_base,
+                    size_t frame_elems) {
+  for (int s = 0; s < c->S; ++s) {
+    if (!pose_valid(poses[s], 1e-6)) throw InvalidArg{"MeasurementFrame: invalid transform"};
+  }
+  for (int s = 0; s < c->S; ++s) {
+    vxm::FrameParams& f = c->frames_host[s];
+    double* org = &c->origin[3 * s];
+    // the measurement grid takes the local grid's pre-shift origin (pipeline.cpp:84-85)
+    camera_to_grid(poses[s], org, f.rot, f.trans);
+    if (depth_dev_base) f.depth = depth_dev_base + frame_elems * s;
+    f.cur = c->cur[s];
+    int32_t off[3];
+    const bool moved = shift_decision(c->cfg.grid, org, poses[s].translation, off);
+    for (int a = 0; a < 3; ++a) {
+      f.off[a] = off[a];
+      c->last_off[3 * s + a] = off[a];
+    }
+    c->last_shifted[s] = moved ? 1 : 0;
+    // epoch-tagged words need no reset; wrap-around clears the words once
+    if (c->epoch[s] >= vxm::kMaxEpoch) {
+      VXM_CK(cudaMemsetAsync(c->msw + c->n * s, 0, sizeof(uint32_t) * c->n, c->stream));
+      if (c->ctr) VXM_CK(cudaMemsetAsync(c->ctr + c->n * s, 0, sizeof(uint32_t) * c->n, c->stream));
+      c->epoch[s] = 0;
+    }
+    c->epoch[s] += 1;
+    f.tag = c->epoch[s] << vxm::kEpochShift;
+  }
+  VXM_CK(cudaMemcpyAsync(c->frames_dev, c->frames_host, sizeof(vxm::FrameParams) * c->S,
+                         cudaMemcpyHostToDevice, c->stream));
+}
+
+void run_frame(vxm_ctx* c, bool cloud) {
+  const bool timed = (c->flags & VXM_FLAG_STAGE_TIMING) != 0;
+  VXM_CK(cudaEventRecord(c->ev[0], c->stream));
+  if (timed || (c->flags & VXM_FLAG_NO_GRAPH)) {
+    launch_frame(c, cloud, timed);
+  } else {
+    cudaGraphExec_t& g = cloud ? c->graph_cloud : c->graph_depth;
+    if (!g) g = capture(c, cloud);
+    VXM_CK(cudaGraphLaunch(g, c->stream));
+  }
+  VXM_CK(cudaEventRecord(c->ev[5], c->stream));
+  for (int s = 0; s < c->S; ++s) c->cur[s] ^= 1u;  // K4 wrote the other buffer
+  c->pending = true;
+}
+
+void collect_stats(vxm_ctx* c, vxm_stats* out) {
+  VXM_CK(cudaStreamSynchronize(c->stream));
+  if (c->pending) {
+    VXM_CK(cudaEventElapsedTime(&c->last_ms, c->ev[0], c->ev[5]));
+    if (c->flags & VXM_FLAG_STAGE_TIMING) {
+      float t[4] = {0, 0, 0, 0};
+      VXM_CK(cudaEventElapsedTime(&t[0], c->ev[1], c->ev[2]));
+      VXM_CK(cudaEventElapsedTime(&t[1], c->ev[2], c->ev[3]));
+      VXM_CK(cudaEventElapsedTime(&t[2], c->ev[3], c->ev[4]));
+      for (int i = 0; i < 3; ++i) c->stage_us[i] = t[i] * 1000.0;
+    }
+    c->pending = false;
+  }
+  if (!out) return;
+  for (int s = 0; s < c->S; ++s) {
+    const vxm::Counters& k = c->counters_host[s];
+    vxm_stats& o = out[s];
+    std::memset(&o, 0, sizeof(o));
+    o.points_total = k.points_total;
+    o.points_outside = k.points_outside;
+    o.rays_traced = k.rays_traced;
+    o.voxels_freed = k.voxels_freed;
+    o.voxels_marked_unknown_traced = k.voxels_traced;
+    o.voxels_skipped_out_of_bounds = k.voxels_skipped;
+    o.occupied_count = k.occupied;
+    o.freed_count = k.freed;
+    o.shifted = c->last_shifted[s];
+    for (int a = 0; a < 3; ++a) {
+      o.shift_offset[a] = c->last_off[3 * s + a];
+      o.origin[a] = c->origin[3 * s + a];
+    }
+    o.populate_us = c->stage_us[0];
+    o.trace_us = c->stage_us[1];
+    o.merge_us = c->stage_us[2];
+    o.shift_us = 0.0;  // fused into the merge kernel
+  }
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+void destroy_ctx(vxm_ctx* c) {
+  if (!c) return;
+  if (c->device >= 0) cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->graph_depth) cudaGraphExecDestroy(c->graph_depth);
+  if (c->graph_cloud) cudaGraphExecDestroy(c->graph_cloud);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  cudaFree(c->msw);
+  cudaFree(c->ctr);
+  cudaFree(c->loc[0]);
+  cudaFree(c->loc[1]);
+  cudaFree(c->counters);
+  cudaFree(c->frames_dev);
+  cudaFree(c->depth_dev);
+  cudaFree(c->cloud_dev);
+  cudaFreeHost(c->frames_host);
+  cudaFreeHost(c->counters_host);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+// PipelineConfig::validate (pipeline.cpp:33-42) + the GPU's own limits.
+void validate_config(const vxm_config& cfg) {
+  camera_validate(cfg.camera);
+  if (cfg.vox_inf < 0) throw InvalidArg{"IntegratorConfig: vox_inf must be non-negative"};
+  const vxm_grid_spec& g = cfg.grid;
+  if (g.dims[0] < 1 || g.dims[1] < 1 || g.dims[2] < 1)
+    throw InvalidArg{"PipelineConfig: empty grid"};
+  if (!(cfg.depth > 0.0) || cfg.depth > cfg.camera.max_depth)
+    throw InvalidArg{"PipelineConfig: depth must lie in (0, camera.max_depth]"};
+  if (!(g.vox_size > 0.0)) throw InvalidArg{"vox_size must be positive"};
+  if (static_cast<long long>(g.dims[0]) * g.dims[1] * g.dims[2] >= (1LL << 31))
+    throw InvalidArg{"grid larger than 2^31 cells is not supported"};
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* vxm_last_error(void) { return g_err.c_str(); }
+
+const char* vxm_build_info(void) {
+  return "cuda-sm100a voxmap kernels (fp64 IEEE, -fmad=false), ABI " "1";
+}
+
+int vxm_device_count(void) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  int n = 0;
+  for (int d = 0; d < count; ++d) {
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, d) == cudaSuccess && prop.major == 10) ++n;
+  }
+  return n;
+}
+
+int vxm_grid_spec_create(double sx, double sy, double sz, double vs, const double origin[3],
+                         vxm_grid_spec* out) {
+  const double zero[3] = {0, 0, 0};
+  return guarded([&] { spec_create(sx, sy, sz, vs, origin ? origin : zero, out); });
+}
+
+int vxm_grid_spec_create_centered(double sx, double sy, double sz, double vs,
+                                  const double center[3], vxm_grid_spec* out) {
+  return guarded([&] {
+    const double zero[3] = {0, 0, 0};
+    spec_create(sx, sy, sz, vs, zero, out);
+    for (int a = 0; a < 3; ++a) out->origin[a] = center[a] - half_extent(*out, a);
+    if (!all_finite(out->origin, 3)) throw InvalidArg{"grid center must be finite"};
+  });
+}
+
+int vxm_bundle_dimensions(const vxm_camera* cam, double depth, double vs, int32_t out[3]) {
+  return guarded([&] { bundle_dims(*cam, depth, vs, out); });
+}
+
+int vxm_create(const vxm_config* cfg, int32_t n_streams, int32_t device, uint32_t flags,
+               vxm_ctx** out) {
+  *out = nullptr;
+  vxm_ctx* c = nullptr;
+  const int rc = guarded([&] {
+    if (!cfg) throw InvalidArg{"null config"};
+    if (n_streams < 1) throw InvalidArg{"n_streams must be >= 1"};
+    validate_config(*cfg);
+    check_device(device);
+    VXM_CK(cudaSetDevice(device));
+    c = new vxm_ctx();
+    c->device = device;
+    c->cfg = *cfg;
+    c->S = n_streams;
+    c->flags = flags;
+    c->nsm = sm_count(device);
+    const vxm_grid_spec& g = cfg->grid;
+    c->n = static_cast<long long>(g.dims[0]) * g.dims[1] * g.dims[2];
+    bundle_dims(cfg->camera, cfg->depth, g.vox_size, c->bundle);
+    const long long rays = static_cast<long long>(c->bundle[1]) * c->bundle[2];
+    if (rays > static_cast<long long>(vxm::kMaxRays))
+      throw InvalidArg{"ray bundle exceeds " + std::to_string(vxm::kMaxRays) + " rays"};
+
+    VXM_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    for (auto& e : c->ev) VXM_CK(cudaEventCreate(&e));
+    const size_t S = static_cast<size_t>(n_streams);
+    const size_t npix = static_cast<size_t>(cfg->camera.width) * cfg->camera.height;
+    VXM_CK(cudaMalloc(&c->msw, sizeof(uint32_t) * c->n * S));
+    VXM_CK(cudaMemsetAsync(c->msw, 0, sizeof(uint32_t) * c->n * S, c->stream));
+    if (cfg->vox_inf > 0) {
+      VXM_CK(cudaMalloc(&c->ctr, sizeof(uint32_t) * c->n * S));
+      VXM_CK(cudaMemsetAsync(c->ctr, 0, sizeof(uint32_t) * c->n * S, c->stream));
+    }
+    for (int b = 0; b < 2; ++b) {
+      VXM_CK(cudaMalloc(&c->loc[b], c->n * S));
+      VXM_CK(cudaMemsetAsync(c->loc[b], 0, c->n * S, c->stream));
+    }
+    VXM_CK(cudaMalloc(&c->counters, sizeof(vxm::Counters) * S));
+    VXM_CK(cudaMalloc(&c->frames_dev, sizeof(vxm::FrameParams) * S));
+    VXM_CK(cudaMalloc(&c->depth_dev, sizeof(float) * npix * S));
+    VXM_CK(cudaMallocHost(&c->frames_host, sizeof(vxm::FrameParams) * S));
+    VXM_CK(cudaMallocHost(&c->counters_host, sizeof(vxm::Counters) * S));
+    std::memset(c->frames_host, 0, sizeof(vxm::FrameParams) * S);
+    std::memset(c->counters_host, 0, sizeof(vxm::Counters) * S);
+    c->epoch.assign(S, 0);
+    c->cur.assign(S, 0);
+    c->origin.resize(3 * S);
+    c->last_off.assign(3 * S, 0);
+    c->last_shifted.assign(S, 0);
+    for (size_t s = 0; s < S; ++s)
+      for (int a = 0; a < 3; ++a) c->origin[3 * s + a] = g.origin[a];
+
+    vxm::KParams& kp = c->kp;
+    kp.dx = g.dims[0];
+    kp.dy = g.dims[1];
+    kp.dz = g.dims[2];
+    kp.n = c->n;
+    kp.vs = g.vox_size;
+    kp.W = cfg->camera.width;
+    kp.H = cfg->camera.height;
+    // CameraModel::focal_x/y (geometry.hpp:67-68) and the principal point
+    // (geometry.cpp:50-51), computed once on the host with glibc tan.
+    kp.fx = (cfg->camera.width / 2.0) / std::tan(cfg->camera.fov_x / 2.0);
+    kp.fy = (cfg->camera.height / 2.0) / std::tan(cfg->camera.fov_y / 2.0);
+    kp.cx = cfg->camera.width / 2.0;
+    kp.cy = cfg->camera.height / 2.0;
+    kp.max_depth = cfg->camera.max_depth;
+    kp.vox_inf = cfg->vox_inf;
+    kp.vd = c->bundle[0];
+    kp.vw = c->bundle[1];
+    kp.vh = c->bundle[2];
+    kp.tiles_x = (kp.vw + 7) / 8;
+    kp.tiles_y = (kp.vh + 3) / 4;
+    kp.msw = c->msw;
+    kp.ctr = c->ctr;
+    kp.loc0 = c->loc[0];
+    kp.loc1 = c->loc[1];
+    kp.counters = c->counters;
+    kp.frames = c->frames_dev;
+    if (cfg->vox_inf > 0) {
+      const int r = cfg->vox_inf;
+      const size_t smem = static_cast<size_t>(vxm::kDilTX + 2 * r) * (vxm::kDilTY + 2 * r) * (vxm::kDilTZ + 2 * r) +
+                          static_cast<size_t>(vxm::kDilTX) * (vxm::kDilTY + 2 * r) * (vxm::kDilTZ + 2 * r) +
+                          static_cast<size_t>(vxm::kDilTX) * vxm::kDilTY * (vxm::kDilTZ + 2 * r);
+      if (smem > 200 * 1024) throw InvalidArg{"vox_inf too large for the dilation tile"};
+      VXM_CK(cudaFuncSetAttribute(vxm::dilate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    }
+    VXM_CK(cudaStreamSynchronize(c->stream));
+  });
+  if (rc != VXM_OK) {
+    destroy_ctx(c);
+    return rc;
+  }
+  *out = c;
+  return VXM_OK;
+}
+
+int vxm_destroy(vxm_ctx* ctx) {
+  destroy_ctx(ctx);
+  return VXM_OK;
+}
+
+int vxm_num_streams(const vxm_ctx* ctx) { return ctx ? ctx->S : 0; }
+
+void* vxm_cuda_stream(vxm_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+
+int vxm_last_frame_ms(vxm_ctx* ctx, float* ms) {
+  return guarded([&] {
+    collect_stats(ctx, nullptr);
+    *ms = ctx->last_ms;
+  });
+}
+
+int vxm_integrate_depth(vxm_ctx* ctx, const float* depth, const vxm_pose* t_wc, vxm_stats* stats) {
+  return guarded([&] {
+    if (!ctx || !depth || !t_wc) throw InvalidArg{"null argument"};
+    VXM_CK(cudaSetDevice(ctx->device));
+    const size_t frame = static_cast<size_t>(ctx->kp.W) * ctx->kp.H;
+    prepare_frames(ctx, t_wc, ctx->depth_dev, frame);
+    // pinned host buffers go straight to the copy engine; pageable ones are
+    // staged by the driver
+    VXM_CK(cudaMemcpyAsync(ctx->depth_dev, depth, sizeof(float) * frame * ctx->S,
+                           cudaMemcpyHostToDevice, ctx->stream));
+    run_frame(ctx, false);
+    collect_stats(ctx, stats);
+  });
+}
+
+int vxm_integrate_depth_device(vxm_ctx* ctx, const float* depth_dev, const vxm_pose* t_wc) {
+  return guarded([&] {
+    if (!ctx || !depth_dev || !t_wc) throw InvalidArg{"null argument"};
+    VXM_CK(cudaSetDevice(ctx->device));
+    const size_t frame = static_cast<size_t>(ctx->kp.W) * ctx->kp.H;
+    prepare_frames(ctx, t_wc, depth_dev, frame);
+    run_frame(ctx, false);
+  });
+}
+
+int vxm_wait_stats(vxm_ctx* ctx, vxm_stats* stats) {
+  return guarded([&] {
+    VXM_CK(cudaSetDevice(ctx->device));
+    collect_stats(ctx, stats);
+  });
+}
+
+int vxm_integrate_cloud(vxm_ctx* ctx, const double* xs, const double* ys, const double* zs,
+                        size_t n, const vxm_pose* t_wc, vxm_stats* stats) {
+  return guarded([&] {
+    if (!ctx || !t_wc) throw InvalidArg{"null argument"};
+    if (ctx->S != 1) throw InvalidArg{"vxm_integrate_cloud needs a single-stream context"};
+    if (n > 0 && (!xs || !ys || !zs)) throw InvalidArg{"null cloud arrays"};
+    VXM_CK(cudaSetDevice(ctx->device));
+    if (n > ctx->cloud_cap) {
+      cudaFree(ctx->cloud_dev);
+      ctx->cloud_dev = nullptr;
+      ctx->cloud_cap = 0;
+      VXM_CK(cudaMalloc(&ctx->cloud_dev, sizeof(double) * 3 * n));
+      ctx->cloud_cap = n;
+    }
+    vxm::FrameParams& f = ctx->frames_host[0];
+    f.xs = ctx->cloud_dev;
+    f.ys = ctx->cloud_dev + ctx->cloud_cap;
+    f.zs = ctx->cloud_dev + 2 * ctx->cloud_cap;
+    f.n_points = static_cast<long long>(n);
+    prepare_frames(ctx, t_wc, nullptr, 0);
+    if (n) {
+      VXM_CK(cudaMemcpyAsync(const_cast<double*>(f.xs), xs, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+      VXM_CK(cudaMemcpyAsync(const_cast<double*>(f.ys), ys, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+      VXM_CK(cudaMemcpyAsync(const_cast<double*>(f.zs), zs, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    run_frame(ctx, true);
+    collect_stats(ctx, stats);
+  });
+}
+
+int vxm_download_local(vxm_ctx* ctx, int32_t s, uint8_t* cells, double origin[3]) {
+  return guarded([&] {
+    if (!ctx || s < 0 || s >= ctx->S) throw InvalidArg{"stream index out of range"};
+    VXM_CK(cudaSetDevice(ctx->device));
+    collect_stats(ctx, nullptr);
+    if (cells)
+      VXM_CK(cudaMemcpy(cells, ctx->loc[ctx->cur[s]] + ctx->n * s, ctx->n, cudaMemcpyDeviceToHost));
+    if (origin)
+      for (int a = 0; a < 3; ++a) origin[a] = ctx->origin[3 * s + a];
+  });
+}
+
+int vxm_upload_local(vxm_ctx* ctx, int32_t s, const uint8_t* cells, const double origin[3]) {
+  return guarded([&] {
+    if (!ctx || s < 0 || s >= ctx->S) throw InvalidArg{"stream index out of range"};
+    if (origin && !all_finite(origin, 3)) throw InvalidArg{"grid origin must be finite"};
+    VXM_CK(cudaSetDevice(ctx->device));
+    collect_stats(ctx, nullptr);
+    if (cells)
+      VXM_CK(cudaMemcpy(ctx->loc[ctx->cur[s]] + ctx->n * s, cells, ctx->n, cudaMemcpyHostToDevice));
+    if (origin)
+      for (int a = 0; a < 3; ++a) ctx->origin[3 * s + a] = origin[a];
+  });
+}
+
+}  // extern "C"

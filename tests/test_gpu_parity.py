@@ -1,0 +1,294 @@
+"""Parity of the sm_100a path (through the C-ABI) with the reference's own
+Sequential implementation (oracle/_ref, or the C restatement). Bit-exact:
+grids byte for byte, every counter equal."""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from paper_2112_13169_b200 import voxmap as vm
+from tests import scenes
+from tests.oracle_api import have_ref, oracle_pipeline
+
+pytestmark = pytest.mark.gpu
+
+ref = pytest.importorskip("oracle.ref")
+if not have_ref():
+    pytest.skip("oracle/_ref not built", allow_module_level=True)
+
+DEG = math.pi / 180.0
+
+
+def random_rotation(rng):
+    axis = rng.uniform(-1, 1, 3)
+    while np.linalg.norm(axis) < 1e-3:
+        axis = rng.uniform(-1, 1, 3)
+    axis = axis / np.linalg.norm(axis)
+    ang = rng.uniform(-1, 1) * math.pi
+    K = np.array([[0, -axis[2], axis[1]], [axis[2], 0, -axis[0]], [-axis[1], axis[0], 0]])
+    return np.eye(3) + math.sin(ang) * K + (1 - math.cos(ang)) * (K @ K)
+
+
+# --- KernelTable adapter (proj/tests/test_kernels.cpp) ------------------------
+
+def test_kernel_isa(gpu_lib):
+    assert vm.kernel_isa() == "cuda-sm100a"
+
+
+def test_merge_table_all_16_cases(gpu_lib):
+    # proj/tests/test_kernels.cpp:12-21: m==0 keeps, m==3 -> 0, else m
+    loc = np.repeat(np.arange(4, dtype=np.uint8), 4)
+    ms = np.tile(np.arange(4, dtype=np.uint8), 4)
+    expect = np.where(ms == 0, loc, np.where(ms == 3, 0, ms)).astype(np.uint8)
+    got = loc.copy()
+    vm.kernel_merge(got, ms)
+    assert np.array_equal(got, expect)
+
+
+@pytest.mark.parametrize("n", [0, 1, 15, 16, 31, 32, 33, 100, 4097])
+@pytest.mark.parametrize("offset", [0, 1, 3])
+def test_merge_matches_reference_any_size_and_alignment(gpu_lib, n, offset):
+    rng = np.random.default_rng(n * 7 + offset)
+    buf_l = rng.integers(0, 4, n + offset, dtype=np.uint8)
+    buf_m = rng.integers(0, 4, n + offset, dtype=np.uint8)
+    loc, ms = buf_l[offset:], buf_m[offset:]
+    want = loc.copy()
+    ref.merge(want, ms.copy())
+    vm.kernel_merge(loc, ms)
+    assert np.array_equal(loc, want)
+
+
+def test_transform_voxelize_known_answers(gpu_lib):
+    # proj/tests/test_kernels.cpp:63-87: floor semantics and the +-1e9 clamp
+    xs = np.array([0.05, 0.15, -0.05, 1e12, -1e12, 0.0])
+    ys = np.array([0.0, 0.0, 0.0, 0.0, 0.0, 0.0])
+    zs = np.array([0.0, 0.25, 0.0, 0.0, 0.0, -0.0])
+    R = np.eye(3)
+    t = np.zeros(3)
+    got = vm.kernel_transform_voxelize(xs, ys, zs, R, t, 0.1)
+    want = ref.transform_voxelize(xs, ys, zs, R, t, 0.1)
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w)
+    assert list(got[0][:3]) == [0, 1, -1]
+    assert got[0][3] == 1_000_000_000 and got[0][4] == -1_000_000_000
+
+
+@pytest.mark.parametrize("n", [0, 1, 3, 4, 5, 33, 4097])
+def test_transform_voxelize_random_rotations(gpu_lib, n):
+    rng = np.random.default_rng(41 + n)
+    for _ in range(5):
+        xs, ys, zs = (rng.uniform(-20, 20, n) for _ in range(3))
+        R = random_rotation(rng)
+        t = rng.uniform(-5, 5, 3)
+        vs = float(rng.choice([0.05, 0.1, 0.15, 0.3]))
+        got = vm.kernel_transform_voxelize(xs, ys, zs, R, t, vs)
+        want = ref.transform_voxelize(xs, ys, zs, R, t, vs)
+        for g, w in zip(got, want):
+            assert np.array_equal(g, w)
+
+
+# --- populate_occupied (proj/tests/test_integrator.cpp, acceptance criterion 4) --
+
+@pytest.mark.parametrize("vox_inf", [0, 1, 2, 3])
+def test_populate_matches_reference(gpu_lib, vox_inf):
+    rng = np.random.default_rng(104 + vox_inf)
+    vox = 0.15
+    grid = vm.GridSpec.create(32 * vox, 32 * vox, 32 * vox, vox)
+    for n in (1, 500, 5000, 20000):
+        xs, ys, zs = (rng.uniform(-0.6, 32 * vox + 0.6, n) for _ in range(3))
+        pose = (random_rotation(rng), rng.uniform(-0.5, 0.5, 3))
+        ms_ref = np.zeros(grid.cell_count(), dtype=np.uint8)
+        ms_gpu = ms_ref.copy()
+        st_ref = ref.populate(grid.c, ms_ref, xs, ys, zs, pose, vox_inf)
+        st_gpu = vm.populate_occupied(grid, ms_gpu, xs, ys, zs, pose, vox_inf)
+        assert st_gpu == st_ref
+        assert np.array_equal(ms_gpu, ms_ref)
+
+
+def test_populate_never_clears_and_is_idempotent(gpu_lib):
+    # test_integrator.cpp:107-137
+    grid = vm.GridSpec.create(1.5, 1.5, 1.5, 0.15)
+    ms = np.zeros(grid.cell_count(), dtype=np.uint8)
+    ms[::7] = 1
+    ms[::11] = 3
+    before = ms.copy()
+    xs, ys, zs = np.array([0.7]), np.array([0.7]), np.array([0.7])
+    vm.populate_occupied(grid, ms, xs, ys, zs, vm.identity_pose(), 2)
+    again = ms.copy()
+    vm.populate_occupied(grid, again, xs, ys, zs, vm.identity_pose(), 2)
+    assert np.array_equal(ms, again)
+    untouched = ms != 2
+    assert np.array_equal(ms[untouched], before[untouched])
+    assert int((ms == 2).sum()) == 125
+
+
+# --- trace_bundle (acceptance criterion 3, test_raytracer.cpp) ------------------
+
+def _random_occupied(rng, grid, count):
+    ms = np.zeros(grid.cell_count(), dtype=np.uint8)
+    d = grid.dims
+    for _ in range(count):
+        x, y, z = rng.integers(0, d[0]), rng.integers(0, d[1]), rng.integers(0, d[2])
+        ms[x + y * d[0] + z * d[0] * d[1]] = 2
+    return ms
+
+
+def test_trace_bundle_matches_sequential_reference(gpu_lib):
+    vox = 0.15
+    grid = vm.GridSpec.create(32 * vox, 32 * vox, 32 * vox, vox)
+    rng = np.random.default_rng(103)
+    for scene in range(40):
+        ms = _random_occupied(rng, grid, int(rng.integers(50, 400)))
+        pose = (random_rotation(rng), rng.uniform(1.2, 3.6, 3))
+        bundle = (16, 13, 13)
+        ms_ref, ms_gpu = ms.copy(), ms.copy()
+        st_ref = ref.trace_bundle(grid.c, ms_ref, bundle, pose)
+        st_gpu = vm.trace_bundle(grid, ms_gpu, bundle, pose)
+        assert st_gpu == st_ref, scene
+        assert np.array_equal(ms_gpu, ms_ref), (scene, int((ms_gpu != ms_ref).sum()))
+
+
+def test_trace_bundle_camera_outside_grid_counts_skips(gpu_lib):
+    vox = 0.15
+    grid = vm.GridSpec.create(24 * vox, 24 * vox, 24 * vox, vox)
+    rng = np.random.default_rng(7)
+    for k in range(10):
+        ms = _random_occupied(rng, grid, 200)
+        pose = vm.look_along_x((-1.0 - 0.1 * k, 1.8, 1.8))
+        ms_ref, ms_gpu = ms.copy(), ms.copy()
+        st_ref = ref.trace_bundle(grid.c, ms_ref, (40, 31, 31), pose)
+        st_gpu = vm.trace_bundle(grid, ms_gpu, (40, 31, 31), pose)
+        assert st_ref["voxels_skipped_out_of_bounds"] > 0
+        assert st_gpu == st_ref
+        assert np.array_equal(ms_gpu, ms_ref)
+
+
+def test_trace_bundle_preexisting_free_and_traced(gpu_lib):
+    vox = 0.15
+    grid = vm.GridSpec.create(20 * vox, 20 * vox, 20 * vox, vox)
+    rng = np.random.default_rng(11)
+    ms = rng.integers(0, 4, grid.cell_count(), dtype=np.uint8)
+    pose = vm.look_along_x((0.3, 1.5, 1.5))
+    ms_ref, ms_gpu = ms.copy(), ms.copy()
+    assert vm.trace_bundle(grid, ms_gpu, (15, 11, 11), pose) == ref.trace_bundle(grid.c, ms_ref, (15, 11, 11), pose)
+    assert np.array_equal(ms_gpu, ms_ref)
+
+
+def test_trace_bundle_rejects_bad_bundle(gpu_lib):
+    grid = vm.GridSpec.create(1.5, 1.5, 1.5, 0.15)
+    ms = np.zeros(grid.cell_count(), dtype=np.uint8)
+    with pytest.raises(ValueError):
+        vm.trace_bundle(grid, ms, (10, 4, 5), vm.identity_pose())
+
+
+# --- shift and depth_to_cloud ----------------------------------------------------
+
+def test_shift_matches_reference(gpu_lib):
+    grid = vm.GridSpec.create(16 * 0.15, 14 * 0.15, 9 * 0.15, 0.15)
+    rng = np.random.default_rng(111)
+    for _ in range(50):
+        cells = rng.integers(0, 4, grid.cell_count(), dtype=np.uint8)
+        off = rng.integers(-20, 21, 3) if rng.random() < 0.3 else rng.integers(-5, 6, 3)
+        assert np.array_equal(vm.shift_grid_by(grid.dims, cells, off), ref.shift(grid.c, cells, off))
+
+
+def test_depth_to_cloud_matches_reference(gpu_lib):
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 97, 61, 5.0)
+    depth = scenes.stress_depth(cam, seed=3)
+    depth[0, :5] = [np.nan, np.inf, -1.0, 5.0, 5.0000005]
+    got = vm.depth_to_cloud(depth, cam)
+    want = ref.depth_to_cloud(cam.to_c(), depth)
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w)
+
+
+# --- the full per-frame pipeline ------------------------------------------------
+
+def _run_pair(cfg, frames):
+    gpu = vm.MappingPipeline(cfg)
+    orc = oracle_pipeline(cfg)
+    for k, (depth, pose) in enumerate(frames):
+        sg = gpu.integrate_depth(depth, pose)
+        sr = orc.integrate_depth(depth, pose)
+        for key in ("points_total", "points_outside", "rays_traced", "voxels_freed",
+                    "voxels_marked_unknown_traced", "voxels_skipped_out_of_bounds", "occupied_count",
+                    "freed_count", "shifted", "shift_offset", "origin"):
+            assert sg[key] == sr[key], (k, key, sg[key], sr[key])
+        cg, og = gpu.local_grid()
+        cr, orr = orc.local_grid()
+        assert np.array_equal(og, orr)
+        assert np.array_equal(cg, cr), (k, int((cg != cr).sum()))
+    return gpu
+
+
+@pytest.mark.parametrize("vox_inf", [0, 2])
+def test_pipeline_reference_default_config_moving(gpu_lib, vox_inf):
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 320, 240, 6.5)
+    grid = vm.GridSpec.create_centered(15.0, 15.0, 3.0, 0.15, (0.0, 0.0, 0.0))
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=vox_inf, depth=6.5)
+    boxes = scenes.box_field_boxes(1)
+    frames = []
+    for k in range(8):
+        pose = vm.look_along_x((0.05 * k, -0.6 + 0.17 * k, 0.02 * k))
+        frames.append((scenes.render(cam, pose, boxes), pose))
+    _run_pair(cfg, frames)
+
+
+@pytest.mark.parametrize("vox_inf,depth_m", [(0, 6.5), (2, 5.0)])
+def test_pipeline_cfg1_cfg2_640x480(gpu_lib, vox_inf, depth_m):
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 640, 480, depth_m)
+    grid = vm.GridSpec.create_centered(10.0, 10.0, 5.0, 0.1, (0.0, 0.0, 0.0))
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=vox_inf, depth=depth_m)
+    frames = []
+    for k in range(3):
+        pose = vm.look_along_x((0.0, 0.11 * k, 0.0))
+        frames.append((scenes.render(cam, pose, scenes.box_field_boxes(1 + k)), pose))
+    frames.append((scenes.stress_depth(cam, seed=1), vm.look_along_x((0.0, 0.35, 0.0))))
+    _run_pair(cfg, frames)
+
+
+def test_pipeline_cloud_entry_point(gpu_lib):
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 160, 120, 6.5)
+    grid = vm.GridSpec.create_centered(6.0, 6.0, 3.0, 0.15, (0.0, 0.0, 0.0))
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=1, depth=4.0)
+    gpu = vm.MappingPipeline(cfg)
+    orc = oracle_pipeline(cfg)
+    rng = np.random.default_rng(5)
+    for k in range(4):
+        n = int(rng.integers(0, 3000))
+        xs, ys, zs = rng.uniform(-3, 3, n), rng.uniform(-2, 2, n), rng.uniform(0.1, 6, n)
+        pose = (random_rotation(rng), rng.uniform(-0.3, 0.3, 3))
+        sg = gpu.integrate(xs, ys, zs, pose)
+        sr = orc.integrate(xs, ys, zs, pose)
+        for key in ("points_total", "points_outside", "rays_traced", "voxels_freed",
+                    "voxels_marked_unknown_traced", "occupied_count", "freed_count", "shifted"):
+            assert sg[key] == sr[key], (k, key)
+        assert np.array_equal(gpu.local_grid()[0], orc.local_grid()[0])
+
+
+def test_pipeline_rejects_invalid_transform(gpu_lib):
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 64, 48, 6.5)
+    grid = vm.GridSpec.create_centered(6.0, 6.0, 3.0, 0.15, (0.0, 0.0, 0.0))
+    gpu = vm.MappingPipeline(vm.PipelineConfig(grid, cam, vox_inf=0, depth=4.0))
+    with pytest.raises(ValueError, match="invalid transform"):
+        gpu.integrate_depth(np.ones((48, 64), np.float32), (2.0 * np.eye(3), np.zeros(3)))
+
+
+def test_batched_streams_equal_independent_pipelines(gpu_lib):
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 160, 120, 6.5)
+    grid = vm.GridSpec.create_centered(6.0, 6.0, 3.0, 0.15, (0.0, 0.0, 0.0))
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=2, depth=6.5)
+    S = 5
+    batch = vm.MappingPipeline(cfg, n_streams=S)
+    singles = [oracle_pipeline(cfg) for _ in range(S)]
+    for k in range(4):
+        poses = [vm.look_along_x((0.02 * s, 0.09 * k * (s + 1) - 0.2, 0.0)) for s in range(S)]
+        depth = np.stack([scenes.render(cam, poses[s], scenes.box_field_boxes(1 + s)) for s in range(S)])
+        stats = batch.integrate_depth(depth, poses)
+        for s in range(S):
+            sr = singles[s].integrate_depth(depth[s], poses[s])
+            assert stats[s]["occupied_count"] == sr["occupied_count"]
+            assert stats[s]["voxels_freed"] == sr["voxels_freed"]
+            assert np.array_equal(batch.local_grid(s)[0], singles[s].local_grid()[0]), (k, s)
