@@ -22,6 +22,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # proj/src/CMakeLists.txt:33-35); the kernels also spell every fp64 op with
 # _rn intrinsics.
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
+                  "-Xcompiler", "-ffp-contract=off",
                   "-Xcompiler", "-Wall", f"-I{ROOT / 'include'}"]
 
 CU_SOURCES = ["vxm_unity.cu"]

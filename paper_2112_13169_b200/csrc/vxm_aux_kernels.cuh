@@ -8,21 +8,25 @@
 
 namespace vxm {
 
-// Reference byte grid -> measurement words (see vxm_device.cuh): Occupied
-// becomes the epoch's maximum, pre-existing Free / UnknownTraced become the
-// lowest-priority ray keys so that any ray write overrides them.
-__global__ void encode_ms_kernel(const uint8_t* ms, uint32_t* msw, long long n, uint32_t tag) {
+// Reference byte grid -> (occ, key) of epoch e (see vxm_device.cuh):
+// Occupied becomes occ == e, pre-existing Free / UnknownTraced become the
+// lowest-priority keys so that any ray write overrides them.
+__global__ void encode_ms_kernel(const uint8_t* ms, uint8_t* occ, uint32_t* key, long long n,
+                                 uint32_t epoch) {
+  const uint32_t tag = key_tag(epoch);
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const uint8_t b = ms[i];
-    msw[i] = b == 2 ? occupied_word(tag) : b == 1 ? tag : b == 3 ? (tag | 1u) : 0u;
+    occ[i] = b == 2 ? static_cast<uint8_t>(epoch) : 0;
+    key[i] = b == 1 ? tag : b == 3 ? (tag | 1u) : 0u;
   }
 }
 
-__global__ void decode_ms_kernel(const uint32_t* msw, uint8_t* ms, long long n, uint32_t tag) {
+__global__ void decode_ms_kernel(const uint8_t* occ, const uint32_t* key, uint8_t* ms,
+                                 long long n, uint32_t epoch) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    ms[i] = static_cast<uint8_t>(decode_word(msw[i], tag));
+    ms[i] = static_cast<uint8_t>(decode_cell(occ[i], key[i], epoch));
   }
 }
 
@@ -60,6 +64,7 @@ __global__ void transform_voxelize_kernel(const double* xs, const double* ys, co
                                           long long n, const double* R, const double* t,
                                           double vs, int32_t* cx, int32_t* cy, int32_t* cz) {
   double Rr[9], tt[3];
+  const double inv_vs = __drcp_rn(vs);
 #pragma unroll
   for (int i = 0; i < 9; ++i) Rr[i] = R[i];
 #pragma unroll
@@ -67,7 +72,7 @@ __global__ void transform_voxelize_kernel(const double* xs, const double* ys, co
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     int c[3];
-    transform_voxelize(Rr, tt, xs[i], ys[i], zs[i], vs, c);
+    transform_voxelize(Rr, tt, xs[i], ys[i], zs[i], vs, inv_vs, c);
     cx[i] = c[0];
     cy[i] = c[1];
     cz[i] = c[2];

@@ -13,39 +13,41 @@
 namespace vxm {
 
 // ---------------------------------------------------------------------------
-// Measurement-grid words.
+// Measurement grid on the GPU.
 //
 // The reference measurement grid is one byte per cell, reset to Unknown every
 // frame (proj/src/pipeline.cpp:83), written Occupied by populate and Free /
 // UnknownTraced by the rays, with the highest-index ray winning a conflict in
-// Sequential mode (raytracer.cpp:98-104). On the GPU each cell
-// is one 32-bit word whose top bits carry a per-stream frame epoch:
+// Sequential mode (raytracer.cpp:98-104). The GPU splits it in
+// two arrays that are never reset, because every entry carries the frame's
+// epoch e (1..255, per stream):
 //
-//   word = epoch << 18 | low18
-//   low18 == 0x3FFFF                  Occupied
-//   low18 == (ray + 1) << 1 | traced  written by bundle ray `ray`
-//   low18 == 0 / 1                    Free / UnknownTraced carried in from a
-//                                     host grid (lowest priority)
-//   epoch != current epoch            Unknown (no per-frame reset needed)
+//   occ[c]  (uint8)   == e            Occupied this frame (populate / dilation)
+//   key[c]  (uint32)  == e << 18 | (ray + 1) << 1 | traced
+//                                      written by bundle ray `ray` this frame
+//                     == e << 18 | 0/1 Free / UnknownTraced carried in from a
+//                                      host grid (lowest priority)
+//   anything tagged with another epoch: Unknown.
 //
-// Populate stores the Occupied word with plain stores (idempotent, no
-// atomics). Rays resolve conflicts with a fire-and-forget atomicMax: a higher
-// ray index always wins, exactly the Sequential last-writer rule, and the
-// Occupied word is the maximum of its epoch so rays can never overwrite it.
+// Populate stores occ with plain idempotent byte stores (no atomics). During
+// the trace occ is read-only (read through the non-coherent path) and rays
+// resolve write conflicts with a fire-and-forget atomicMax on key: a higher
+// ray index always wins, exactly the Sequential last-writer rule. Occupied
+// cells are never written by rays, so occ wins over key when decoding.
 // ---------------------------------------------------------------------------
-constexpr uint32_t kEpochShift = 18;
-constexpr uint32_t kLowMask = (1u << kEpochShift) - 1u;  // 0x3FFFF
-constexpr uint32_t kMaxEpoch = (1u << (32 - kEpochShift)) - 1u;
-constexpr uint32_t kMaxRays = (kLowMask >> 1) - 1u;  // (ray+1)<<1|1 < 0x3FFFF
+constexpr uint32_t kKeyShift = 18;
+constexpr uint32_t kLowMask = (1u << kKeyShift) - 1u;  // 0x3FFFF
+constexpr uint32_t kMaxEpoch = 255u;                   // fits the occ byte
+constexpr uint32_t kMaxRays = (kLowMask >> 1) - 1u;    // (ray+1)<<1|1 <= 0x3FFFF
+constexpr int kMaxVoxInf = 16;
 
-__host__ __device__ constexpr uint32_t occupied_word(uint32_t tag) { return tag | kLowMask; }
+__host__ __device__ constexpr uint32_t key_tag(uint32_t epoch) { return epoch << kKeyShift; }
 
-// Word -> reference byte state (0 Unknown, 1 Free, 2 Occupied, 3 UnknownTraced).
-__device__ __forceinline__ uint32_t decode_word(uint32_t w, uint32_t tag) {
-  if ((w & ~kLowMask) != tag) return 0u;
-  const uint32_t low = w & kLowMask;
-  if (low == kLowMask) return 2u;
-  return (low & 1u) ? 3u : 1u;
+// (occ, key) -> reference byte state (0 Unknown, 1 Free, 2 Occupied, 3 UnknownTraced).
+__device__ __forceinline__ uint32_t decode_cell(uint32_t occ, uint32_t key, uint32_t epoch) {
+  if (occ == epoch) return 2u;
+  if ((key >> kKeyShift) != epoch) return 0u;
+  return (key & 1u) ? 3u : 1u;
 }
 
 // merge_scalar (proj/src/kernels/kernels_scalar.cpp:10-16): measurement 0
@@ -77,7 +79,7 @@ struct FrameParams {
   const double* zs;
   long long n_points;
   int32_t off[3];     // shift applied after the merge (0,0,0 = none)
-  uint32_t tag;       // epoch << 18
+  uint32_t epoch;     // 1..255
   uint32_t cur;       // which local buffer holds the current grid
   uint32_t pad_;
 };
@@ -88,17 +90,21 @@ struct KParams {
   int dx, dy, dz;
   long long n;        // cells per stream
   double vs;
-  // camera (host-computed with glibc tan, never recomputed on device)
+  double inv_vs;      // RN(1 / vs), fast-path divisor (see voxel_coord)
+  // camera
   int W, H;
-  double fx, fy, cx, cy, max_depth;
+  double max_depth;
+  const double* qx;   // ((u + 0.5) - cx) / fx per column (host glibc tan)
+  const double* qy;   // ((v + 0.5) - cy) / fy per row
   // populate
   int vox_inf;
   // bundle
   int vd, vw, vh;
   int tiles_x, tiles_y;  // 8x4 ray tiles per warp
   // buffers (stream s at offset s*n)
-  uint32_t* msw;       // measurement words (occupied / ray keys)
-  uint32_t* ctr;       // centre words when vox_inf > 0
+  uint8_t* occ;
+  uint8_t* ctr;        // centre bytes when vox_inf > 0
+  uint32_t* key;
   uint8_t* loc0;
   uint8_t* loc1;
   Counters* counters;
@@ -113,12 +119,27 @@ __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a,
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
 
+// floor(RN(acc / vs)) without the IEEE division whenever that is provably
+// the same value: q = RN(acc * RN(1/vs)) is within 2^-51 |q| of RN(acc/vs),
+// so if q is further than 2^-46 |q| from the nearest integer both quotients
+// lie strictly on the same side of it and have the same floor. Otherwise
+// (near an integer, zero, or extreme magnitudes) the exact division runs.
+__device__ __forceinline__ double floor_div(double acc, double vs, double inv_vs) {
+  const double q = dmul(acc, inv_vs);
+  const double aq = fabs(q);
+  if (aq > 0x1p-1000 && aq < 0x1p+1000) {
+    const double dist = fabs(dsub(q, rint(q)));
+    if (dist > dmul(aq, 0x1p-46)) return floor(q);
+  }
+  return floor(ddiv(acc, vs));
+}
+
 // floor(acc / vs), clamped to +-1e9 and truncated to int32, exactly as
 // transform_voxelize_scalar (proj/src/kernels/kernels_scalar.cpp:31-34):
 // f = std::min(std::max(f, -1e9), 1e9) keeps NaN, and x86's cvttsd2si turns
 // NaN into INT32_MIN, which the bounds test then rejects.
-__device__ __forceinline__ int voxel_coord(double acc, double vs) {
-  double f = floor(ddiv(acc, vs));
+__device__ __forceinline__ int voxel_coord(double acc, double vs, double inv_vs) {
+  double f = floor_div(acc, vs, inv_vs);
   f = (f < -1e9) ? -1e9 : f;
   f = (1e9 < f) ? 1e9 : f;
   if (f != f) return INT32_MIN;
@@ -127,22 +148,19 @@ __device__ __forceinline__ int voxel_coord(double acc, double vs) {
 
 // p_v[a] = ((t[a] + R[3a]x) + R[3a+1]y) + R[3a+2]z   (kernels_scalar.cpp:27-30)
 __device__ __forceinline__ void transform_voxelize(const double* R, const double* t, double x,
-                                                   double y, double z, double vs, int* c) {
+                                                   double y, double z, double vs,
+                                                   double inv_vs, int* c) {
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     double acc = t[a];
     acc = dadd(acc, dmul(R[3 * a + 0], x));
     acc = dadd(acc, dmul(R[3 * a + 1], y));
     acc = dadd(acc, dmul(R[3 * a + 2], z));
-    c[a] = voxel_coord(acc, vs);
+    c[a] = voxel_coord(acc, vs, inv_vs);
   }
 }
 
-__device__ __forceinline__ unsigned long long warp_sum(unsigned v) {
-  return __reduce_add_sync(0xffffffffu, v);
-}
-
-// Block-wide sums of up to 4 counters; thread 0 adds them to global memory.
+// Block-wide sums of NC counters; one atomic per counter per block.
 template <int NC>
 __device__ __forceinline__ void block_accumulate(unsigned (&v)[NC], unsigned long long* dst[NC]) {
   __shared__ unsigned long long partial[NC][32];

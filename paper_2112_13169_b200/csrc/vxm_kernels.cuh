@@ -1,6 +1,6 @@
 // The per-frame voxelization kernels (paper Alg. 1-3 + the local-grid shift).
-// One CUDA grid dimension (blockIdx.y) indexes independent sensor streams, so
-// a batch of S streams is one launch per stage.
+// The last CUDA grid dimension indexes independent sensor streams, so a batch
+// of S streams is one launch per stage.
 //
 //   K1 populate_depth / populate_cloud   depth -> point -> T_vc -> voxel -> Occupied
 //   K2 dilate                           vox_inf > 0: Chebyshev dilation of the centres
@@ -14,67 +14,56 @@ namespace vxm {
 
 // ---------------------------------------------------------------------------
 // K1: depth_to_cloud (proj/src/geometry.cpp:45-57) fused with
-// voxelize_points + mark_point for the centre voxel (proj/src/integrator.cpp:
-// 24-41, 62-85). Each thread owns 4 consecutive pixels (one 16-byte load).
-// Pixels never materialise as a point cloud.
+// voxelize_points + the centre store of mark_point (proj/src/integrator.cpp:
+// 24-41, 62-85). One pixel per thread: the chain is fp64-latency bound, so
+// the kernel wants threads, not work per thread. Pixels never materialise
+// as a point cloud; ((u + 0.5) - cx) / fx comes from a per-column table
+// computed once with the same IEEE operations.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void populate_point(const KParams& p, const FrameParams& f,
-                                               uint32_t* target, uint32_t occ, double x,
-                                               double y, double z, unsigned& outside) {
+__device__ __forceinline__ unsigned populate_point(const KParams& p, const double* R,
+                                                   const double* t, uint8_t* target,
+                                                   uint8_t mark, double x, double y, double z) {
   int c[3];
-  transform_voxelize(f.rot, f.trans, x, y, z, p.vs, c);
-  if (c[0] < 0 || c[1] < 0 || c[2] < 0 || c[0] >= p.dx || c[1] >= p.dy || c[2] >= p.dz) {
-    ++outside;
-    return;
+  transform_voxelize(R, t, x, y, z, p.vs, p.inv_vs, c);
+  if (static_cast<unsigned>(c[0]) >= static_cast<unsigned>(p.dx) ||
+      static_cast<unsigned>(c[1]) >= static_cast<unsigned>(p.dy) ||
+      static_cast<unsigned>(c[2]) >= static_cast<unsigned>(p.dz)) {
+    return 1u;  // counted in points_outside
   }
-  const long long idx = static_cast<long long>(c[0]) +
-                        static_cast<long long>(c[1]) * p.dx +
-                        static_cast<long long>(c[2]) * p.dx * p.dy;
-  target[idx] = occ;  // idempotent: every writer stores the same word
-}
-
-__device__ __forceinline__ void back_project(const KParams& p, int u, int v, double depth,
-                                             double& x, double& y) {
-  // x = (u + 0.5 - cx) / fx * depth  (geometry.cpp:55-56), left to right.
-  x = dmul(ddiv(dsub(dadd(static_cast<double>(u), 0.5), p.cx), p.fx), depth);
-  y = dmul(ddiv(dsub(dadd(static_cast<double>(v), 0.5), p.cy), p.fy), depth);
+  const uint32_t idx = static_cast<uint32_t>(c[0]) + static_cast<uint32_t>(c[1]) * p.dx +
+                       static_cast<uint32_t>(c[2]) * static_cast<uint32_t>(p.dx * p.dy);
+  target[idx] = mark;  // idempotent: every writer stores the same byte
+  return 0u;
 }
 
 __global__ void __launch_bounds__(256) populate_depth_kernel(KParams p) {
   const int s = blockIdx.y;
-  const FrameParams& f = p.frames[s];
-  uint32_t* target = (p.vox_inf > 0 ? p.ctr : p.msw) + static_cast<long long>(s) * p.n;
-  const uint32_t occ = occupied_word(f.tag);
-  const long long npix = static_cast<long long>(p.W) * p.H;
-  const long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const long long first = q * 4;
+  const FrameParams* fp = p.frames + s;
+  const uint8_t mark = static_cast<uint8_t>(fp->epoch);
+  uint8_t* target = (p.vox_inf > 0 ? p.ctr : p.occ) + static_cast<long long>(s) * p.n;
+  double R[9], t[3];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) R[i] = fp->rot[i];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) t[i] = fp->trans[i];
+  const float* depth = fp->depth;
 
+  const int npix = p.W * p.H;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned total = 0, outside = 0;
-  if (first < npix) {
-    float d[4];
-    if (first + 3 < npix && ((reinterpret_cast<uintptr_t>(f.depth) & 15u) == 0)) {
-      const float4 v = __ldcs(reinterpret_cast<const float4*>(f.depth) + q);
-      d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
-    } else {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) d[i] = first + i < npix ? f.depth[first + i] : 0.0f;
-    }
-    const int v0 = static_cast<int>(first / p.W);
-    const int u0 = static_cast<int>(first - static_cast<long long>(v0) * p.W);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      int u = u0 + i, v = v0;
-      if (u >= p.W) { u -= p.W; ++v; }
-      const float di = d[i];
-      // DepthImage::valid_depth (geometry.hpp:124): finite and > 0; then the
-      // max-depth cut on the promoted double (geometry.cpp:53-54).
-      if (!(isfinite(di) && di > 0.0f)) continue;
-      const double depth = static_cast<double>(di);
-      if (depth > p.max_depth) continue;
-      ++total;
-      double x, y;
-      back_project(p, u, v, depth, x, y);
-      populate_point(p, f, target, occ, x, y, depth, outside);
+  if (i < npix) {
+    const float d = __ldcs(depth + i);
+    // DepthImage::valid_depth (geometry.hpp:124): finite and > 0; then the
+    // max-depth cut on the promoted double (geometry.cpp:53-54).
+    if (isfinite(d) && d > 0.0f) {
+      const double D = static_cast<double>(d);
+      if (!(D > p.max_depth)) {
+        total = 1;
+        const int v = i / p.W;
+        const int u = i - v * p.W;
+        outside = populate_point(p, R, t, target, mark, dmul(__ldg(p.qx + u), D),
+                                 dmul(__ldg(p.qy + v), D), D);
+      }
     }
   }
   unsigned vals[2] = {total, outside};
@@ -87,16 +76,23 @@ __global__ void __launch_bounds__(256) populate_depth_kernel(KParams p) {
 // (proj/include/voxmap/geometry.hpp:84-89).
 __global__ void __launch_bounds__(256) populate_cloud_kernel(KParams p) {
   const int s = blockIdx.y;
-  const FrameParams& f = p.frames[s];
-  uint32_t* target = (p.vox_inf > 0 ? p.ctr : p.msw) + static_cast<long long>(s) * p.n;
-  const uint32_t occ = occupied_word(f.tag);
+  const FrameParams* fp = p.frames + s;
+  const uint8_t mark = static_cast<uint8_t>(fp->epoch);
+  uint8_t* target = (p.vox_inf > 0 ? p.ctr : p.occ) + static_cast<long long>(s) * p.n;
+  double R[9], t[3];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) R[i] = fp->rot[i];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) t[i] = fp->trans[i];
+  const long long n = fp->n_points;
+  const double *xs = fp->xs, *ys = fp->ys, *zs = fp->zs;
   unsigned total = 0, outside = 0;
-  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-       i < f.n_points; i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const double x = f.xs[i], y = f.ys[i], z = f.zs[i];
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double x = xs[i], y = ys[i], z = zs[i];
     if (!(isfinite(x) && isfinite(y) && isfinite(z))) continue;
     ++total;
-    populate_point(p, f, target, occ, x, y, z, outside);
+    outside += populate_point(p, R, t, target, mark, x, y, z);
   }
   unsigned vals[2] = {total, outside};
   unsigned long long* dst[2] = {&p.counters[s].points_total, &p.counters[s].points_outside};
@@ -105,68 +101,79 @@ __global__ void __launch_bounds__(256) populate_cloud_kernel(KParams p) {
 
 // ---------------------------------------------------------------------------
 // K2: obstacle inflation. mark_point writes the (2r+1)^3 cube around every
-// in-bounds centre, clipped to the grid (integrator.cpp:70-83); that is a
-// Chebyshev dilation of the centre set restricted to the grid, which is
-// separable: three 1-D max filters. One block produces a 32x8x8 tile from a
-// shared-memory copy of the tile plus an r-voxel halo.
+// in-bounds centre, clipped to the grid (integrator.cpp:70-83): a Chebyshev
+// dilation of the centre set restricted to the grid, which is separable.
+// A block owns an 8x8 (y,z) tile of full x-rows. The rows plus an r-row halo
+// are packed into bitmasks with warp ballots, dilated along x with shifts,
+// then along y and z with ORs, all in shared memory; set bits are written
+// back as Occupied bytes.
 // ---------------------------------------------------------------------------
-constexpr int kDilTX = 32, kDilTY = 8, kDilTZ = 8;
+constexpr int kDilT = 8;
+
+__host__ __device__ constexpr size_t dilate_smem_bytes(int r, int words) {
+  return sizeof(uint32_t) * static_cast<size_t>(words) *
+         (2u * (kDilT + 2 * r) * (kDilT + 2 * r) + static_cast<size_t>(kDilT) * (kDilT + 2 * r));
+}
 
 __global__ void __launch_bounds__(256) dilate_kernel(KParams p, int r) {
-  extern __shared__ uint8_t smem[];
+  extern __shared__ uint32_t bits[];
   const int s = blockIdx.z;
-  const FrameParams& f = p.frames[s];
-  const uint32_t occ = occupied_word(f.tag);
-  const uint32_t* ctr = p.ctr + static_cast<long long>(s) * p.n;
-  uint32_t* msw = p.msw + static_cast<long long>(s) * p.n;
+  const uint32_t e = p.frames[s].epoch;
+  const uint8_t* ctr = p.ctr + static_cast<long long>(s) * p.n;
+  uint8_t* occ = p.occ + static_cast<long long>(s) * p.n;
+  const int W = (p.dx + 31) >> 5;
+  const int H = kDilT + 2 * r;
+  const int y0 = blockIdx.x * kDilT, z0 = blockIdx.y * kDilT;
+  const uint32_t dxy = static_cast<uint32_t>(p.dx) * p.dy;
+  uint32_t* in = bits;                  // [H z][H y][W]
+  uint32_t* bx = in + H * H * W;        // x-dilated
+  uint32_t* by = bx + H * H * W;        // [H z][kDilT y][W], y-dilated
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
 
-  const int tiles_x = (p.dx + kDilTX - 1) / kDilTX;
-  const int x0 = (blockIdx.x % tiles_x) * kDilTX;
-  const int y0 = (blockIdx.x / tiles_x) * kDilTY;
-  const int z0 = blockIdx.y * kDilTZ;
-  const int HX = kDilTX + 2 * r, HY = kDilTY + 2 * r, HZ = kDilTZ + 2 * r;
-  uint8_t* in = smem;                       // HZ x HY x HX
-  uint8_t* tx = in + HX * HY * HZ;          // HZ x HY x TX
-  uint8_t* ty = tx + kDilTX * HY * HZ;      // HZ x TY x TX
-  const int tid = threadIdx.x;
-
-  for (int i = tid; i < HX * HY * HZ; i += blockDim.x) {
-    const int hx = i % HX, hy = (i / HX) % HY, hz = i / (HX * HY);
-    const int x = x0 - r + hx, y = y0 - r + hy, z = z0 - r + hz;
-    uint8_t c = 0;
-    if (x >= 0 && y >= 0 && z >= 0 && x < p.dx && y < p.dy && z < p.dz) {
-      const long long idx = x + static_cast<long long>(y) * p.dx +
-                            static_cast<long long>(z) * p.dx * p.dy;
-      c = ctr[idx] == occ;
+  for (int row = warp; row < H * H; row += nw) {
+    const int hy = row % H, hz = row / H;
+    const int y = y0 - r + hy, z = z0 - r + hz;
+    const bool ok = y >= 0 && y < p.dy && z >= 0 && z < p.dz;
+    for (int w = 0; w < W; ++w) {
+      const int x = (w << 5) + lane;
+      bool c = false;
+      if (ok && x < p.dx) c = ctr[static_cast<uint32_t>(x) + static_cast<uint32_t>(y) * p.dx + static_cast<uint32_t>(z) * dxy] == e;
+      const uint32_t m = __ballot_sync(0xffffffffu, c);
+      if (lane == 0) in[row * W + w] = m;
     }
-    in[i] = c;
   }
   __syncthreads();
-  for (int i = tid; i < kDilTX * HY * HZ; i += blockDim.x) {
-    const int x = i % kDilTX, yz = i / kDilTX;
-    const uint8_t* row = in + yz * HX + x;
-    uint8_t m = 0;
-    for (int k = 0; k <= 2 * r; ++k) m |= row[k];
-    tx[i] = m;
+  for (int i = threadIdx.x; i < H * H * W; i += blockDim.x) {
+    const int w = i % W;
+    const uint32_t m = in[i];
+    const uint32_t prev = w > 0 ? in[i - 1] : 0u;
+    const uint32_t next = w + 1 < W ? in[i + 1] : 0u;
+    uint32_t d = m;
+    for (int k = 1; k <= r; ++k) {
+      d |= (m << k) | (prev >> (32 - k)) | (m >> k) | (next << (32 - k));
+    }
+    bx[i] = d;
   }
   __syncthreads();
-  for (int i = tid; i < kDilTX * kDilTY * HZ; i += blockDim.x) {
-    const int x = i % kDilTX, y = (i / kDilTX) % kDilTY, z = i / (kDilTX * kDilTY);
-    const uint8_t* col = tx + (z * HY + y) * kDilTX + x;
-    uint8_t m = 0;
-    for (int k = 0; k <= 2 * r; ++k) m |= col[k * kDilTX];
-    ty[i] = m;
+  for (int i = threadIdx.x; i < H * kDilT * W; i += blockDim.x) {
+    const int w = i % W, y = (i / W) % kDilT, hz = i / (W * kDilT);
+    uint32_t d = 0;
+    for (int k = 0; k <= 2 * r; ++k) d |= bx[(hz * H + y + k) * W + w];
+    by[i] = d;
   }
   __syncthreads();
-  for (int i = tid; i < kDilTX * kDilTY * kDilTZ; i += blockDim.x) {
-    const int x = i % kDilTX, y = (i / kDilTX) % kDilTY, z = i / (kDilTX * kDilTY);
-    const int gx = x0 + x, gy = y0 + y, gz = z0 + z;
-    if (gx >= p.dx || gy >= p.dy || gz >= p.dz) continue;
-    const uint8_t* col = ty + z * kDilTY * kDilTX + y * kDilTX + x;
-    uint8_t m = 0;
-    for (int k = 0; k <= 2 * r; ++k) m |= col[k * kDilTY * kDilTX];
-    if (m) {
-      msw[gx + static_cast<long long>(gy) * p.dx + static_cast<long long>(gz) * p.dx * p.dy] = occ;
+  for (int row = warp; row < kDilT * kDilT; row += nw) {
+    const int y = row % kDilT, z = row / kDilT;
+    const int gy = y0 + y, gz = z0 + z;
+    if (gy >= p.dy || gz >= p.dz) continue;
+    for (int w = 0; w < W; ++w) {
+      uint32_t d = 0;
+      for (int k = 0; k <= 2 * r; ++k) d |= by[((z + k) * kDilT + y) * W + w];
+      const int x = (w << 5) + lane;
+      if (x < p.dx && ((d >> lane) & 1u)) {
+        occ[static_cast<uint32_t>(x) + static_cast<uint32_t>(gy) * p.dx + static_cast<uint32_t>(gz) * dxy] =
+            static_cast<uint8_t>(e);
+      }
     }
   }
 }
@@ -176,11 +183,16 @@ __global__ void __launch_bounds__(256) dilate_kernel(KParams p, int r) {
 // (proj/src/raytracer.cpp:35-61) + walk_ray (proj/include/voxmap/raytracer.hpp:
 // 76-118) + traverse_ray (raytracer.cpp:63-96). One thread per ray; a warp
 // owns an 8x4 tile of end-plane targets so that its rays stay spatially
-// coherent. The Sequential last-writer rule becomes atomicMax on the cell
-// word (see vxm_device.cuh); before issuing it a lane drops its write when
-// lane+1 or lane+8 (both higher ray indices) writes the same cell in the same
-// step, which removes most same-address traffic near the camera.
+// coherent. The walk runs in chunks of kChunk DDA steps: the cell indices of
+// a chunk are computed first (they do not depend on grid contents), their
+// occupancy bytes are loaded together through the read-only path, then the
+// chunk is resolved in order. The Sequential last-writer rule is an
+// atomicMax on the cell key; before issuing it a lane drops its write when
+// lane+1 or lane+8 (both higher ray indices) writes the same cell in the
+// same step, which removes most same-address traffic near the camera.
 // ---------------------------------------------------------------------------
+constexpr int kChunk = 4;
+
 struct RayState {
   int cur[3];
   int step[3];
@@ -229,11 +241,39 @@ __device__ __forceinline__ void ray_setup(const double* R, const double* start, 
   }
 }
 
+// Advances the DDA by one cell (walk_ray's loop body, raytracer.hpp:103-116):
+// ties step x, then y, then z; returns false when the next crossing lies at
+// or beyond max_dist - 1e-10.
+__device__ __forceinline__ bool ray_advance(RayState& st) {
+  const bool x_first = st.tmax[0] <= st.tmax[1] && st.tmax[0] <= st.tmax[2];
+  const bool y_first = !x_first && st.tmax[1] <= st.tmax[2];
+  const double tm = x_first ? st.tmax[0] : (y_first ? st.tmax[1] : st.tmax[2]);
+  if (tm >= st.stop) return false;
+  if (x_first) {
+    st.cur[0] += st.step[0];
+    st.tmax[0] = dadd(st.tmax[0], st.tdelta[0]);
+  } else if (y_first) {
+    st.cur[1] += st.step[1];
+    st.tmax[1] = dadd(st.tmax[1], st.tdelta[1]);
+  } else {
+    st.cur[2] += st.step[2];
+    st.tmax[2] = dadd(st.tmax[2], st.tdelta[2]);
+  }
+  return true;
+}
+
 __global__ void __launch_bounds__(128) trace_bundle_kernel(KParams p) {
   const int s = blockIdx.y;
-  const FrameParams& f = p.frames[s];
-  uint32_t* msw = p.msw + static_cast<long long>(s) * p.n;
-  const uint32_t occ = occupied_word(f.tag);
+  const FrameParams* fp = p.frames + s;
+  const uint32_t epoch = fp->epoch;
+  const uint32_t tag = key_tag(epoch);
+  uint32_t* key = p.key + static_cast<long long>(s) * p.n;
+  const uint8_t* occ = p.occ + static_cast<long long>(s) * p.n;
+  double R[9], start[3];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) R[i] = fp->rot[i];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) start[i] = fp->trans[i];
 
   const int lane = threadIdx.x & 31;
   const int tile = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -241,64 +281,62 @@ __global__ void __launch_bounds__(128) trace_bundle_kernel(KParams p) {
   const int xi_idx = tx * 8 + (lane & 7);
   const int yi_idx = ty * 4 + (lane >> 3);
   const bool active = ty < p.tiles_y && xi_idx < p.vw && yi_idx < p.vh;
-
-  const int hw = (p.vw - 1) / 2, hh = (p.vh - 1) / 2;
   const uint32_t ray = static_cast<uint32_t>(yi_idx) * p.vw + xi_idx;  // row-major, y outer
-  RayState st;
-  ray_setup(f.rot, f.trans, p.vs, xi_idx - hw, yi_idx - hh, p.vd, st);
+  const uint32_t ray_key = tag | ((ray + 1u) << 1);
 
-  bool alive = active;
+  RayState st;
+  ray_setup(R, start, p.vs, xi_idx - (p.vw - 1) / 2, yi_idx - (p.vh - 1) / 2, p.vd, st);
+
+  const unsigned dx = p.dx, dy = p.dy, dz = p.dz;
+  const uint32_t dxy = dx * dy;
+  bool walking = active;
   bool entered = false;
   uint32_t traced_bit = 0;
   unsigned freed = 0, traced = 0, skipped = 0;
-  const long long dxy = static_cast<long long>(p.dx) * p.dy;
 
-  while (__any_sync(0xffffffffu, alive)) {
-    bool write = false;
-    uint32_t idx = 0xffffffffu - lane;  // unique non-cell sentinel for idle lanes
-    if (alive) {
-      const int x = st.cur[0], y = st.cur[1], z = st.cur[2];
-      if (x < 0 || y < 0 || z < 0 || x >= p.dx || y >= p.dy || z >= p.dz) {
-        if (entered) {
-          alive = false;  // a line leaves a convex grid exactly once
-        } else {
+  while (__any_sync(0xffffffffu, walking)) {
+    uint32_t cell[kChunk];
+    bool valid[kChunk];
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j) {
+      valid[j] = false;
+      cell[j] = 0;
+      if (walking) {
+        const unsigned x = st.cur[0], y = st.cur[1], z = st.cur[2];
+        if (x >= dx || y >= dy || z >= dz) {
+          if (entered) {
+            walking = false;  // a line leaves a convex grid exactly once
+            continue;
+          }
           ++skipped;
+        } else {
+          entered = true;
+          valid[j] = true;
+          cell[j] = x + y * dx + z * dxy;
         }
-      } else {
-        entered = true;
-        const uint32_t cell = static_cast<uint32_t>(x + y * p.dx + z * dxy);
-        if (msw[cell] == occ) {
+        walking = ray_advance(st);
+      }
+    }
+    uint32_t o[kChunk];
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j) o[j] = valid[j] ? __ldg(occ + cell[j]) : 0u;
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j) {
+      bool write = false;
+      uint32_t idx = 0xffffffffu - lane;  // unique non-cell sentinel for idle lanes
+      if (valid[j]) {
+        if (o[j] == epoch) {
           traced_bit = 1;
         } else {
           write = true;
-          idx = cell;
+          idx = cell[j];
           if (traced_bit) ++traced; else ++freed;
         }
       }
-    }
-    const uint32_t right = __shfl_down_sync(0xffffffffu, idx, 1);
-    const uint32_t below = __shfl_down_sync(0xffffffffu, idx, 8);
-    const bool dominated = (lane < 31 && right == idx) || (lane < 24 && below == idx);
-    if (write && !dominated) {
-      atomicMax(msw + idx, f.tag | ((ray + 1u) << 1) | traced_bit);
-    }
-    if (alive) {
-      int axis;
-      if (st.tmax[0] <= st.tmax[1] && st.tmax[0] <= st.tmax[2]) {
-        axis = 0;
-      } else if (st.tmax[1] <= st.tmax[2]) {
-        axis = 1;
-      } else {
-        axis = 2;
-      }
-      const double tm = axis == 0 ? st.tmax[0] : (axis == 1 ? st.tmax[1] : st.tmax[2]);
-      if (tm >= st.stop) {
-        alive = false;
-      } else {
-        if (axis == 0) { st.cur[0] += st.step[0]; st.tmax[0] = dadd(st.tmax[0], st.tdelta[0]); }
-        else if (axis == 1) { st.cur[1] += st.step[1]; st.tmax[1] = dadd(st.tmax[1], st.tdelta[1]); }
-        else { st.cur[2] += st.step[2]; st.tmax[2] = dadd(st.tmax[2], st.tdelta[2]); }
-      }
+      const uint32_t right = __shfl_down_sync(0xffffffffu, idx, 1);
+      const uint32_t below = __shfl_down_sync(0xffffffffu, idx, 8);
+      const bool dominated = (lane < 31 && right == idx) || (lane < 24 && below == idx);
+      if (write && !dominated) atomicMax(key + idx, ray_key | traced_bit);
     }
   }
   unsigned vals[4] = {active ? 1u : 0u, freed, traced, skipped};
@@ -312,45 +350,54 @@ __global__ void __launch_bounds__(128) trace_bundle_kernel(KParams p) {
 // (proj/src/grid.cpp:81-108) + the two VoxelGrid::count passes
 // (pipeline.cpp:114-115) in one gather: destination cell c takes
 // merge(loc[c+off], ms[c+off]) when c+off is inside the grid, else Unknown.
-// Reads the current local buffer, writes the other (ping-pong). Each thread
-// produces 4 consecutive cells (one 32-bit store).
+// Reads the current local buffer, writes the other (ping-pong). One warp per
+// x-row; each lane produces 4 consecutive cells.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p) {
   const int s = blockIdx.y;
-  const FrameParams& f = p.frames[s];
+  const FrameParams* fp = p.frames + s;
+  const uint32_t epoch = fp->epoch;
+  const uint32_t cur = fp->cur;
+  const int ox = fp->off[0], oy = fp->off[1], oz = fp->off[2];
   const long long base = static_cast<long long>(s) * p.n;
-  const uint32_t* msw = p.msw + base;
-  const uint8_t* src = (f.cur ? p.loc1 : p.loc0) + base;
-  uint8_t* dst = (f.cur ? p.loc0 : p.loc1) + base;
-  const long long dxy = static_cast<long long>(p.dx) * p.dy;
-  const long long dshift = f.off[0] + f.off[1] * static_cast<long long>(p.dx) + f.off[2] * dxy;
+  const uint8_t* occ = p.occ + base;
+  const uint32_t* key = p.key + base;
+  const uint8_t* src = (cur ? p.loc1 : p.loc0) + base;
+  uint8_t* dst = (cur ? p.loc0 : p.loc1) + base;
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int rows = p.dy * p.dz;
+  const uint32_t dxy = static_cast<uint32_t>(p.dx) * p.dy;
 
   unsigned occ_n = 0, free_n = 0;
-  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x * 4;
-  for (long long c0 = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
-       c0 < p.n; c0 += stride) {
-    uint32_t out = 0;
-    const int nc = p.n - c0 < 4 ? static_cast<int>(p.n - c0) : 4;
-    for (int i = 0; i < nc; ++i) {
-      const long long c = c0 + i;
-      const int z = static_cast<int>(c / dxy);
-      const long long rem = c - z * dxy;
-      const int y = static_cast<int>(rem / p.dx);
-      const int x = static_cast<int>(rem - static_cast<long long>(y) * p.dx);
-      const int sx = x + f.off[0], sy = y + f.off[1], sz = z + f.off[2];
-      uint32_t v = 0;
-      if (sx >= 0 && sy >= 0 && sz >= 0 && sx < p.dx && sy < p.dy && sz < p.dz) {
-        const long long sc = c + dshift;
-        v = merge_cell(src[sc], decode_word(msw[sc], f.tag));
+  if (row < rows) {
+    const int z = row / p.dy;
+    const int y = row - z * p.dy;
+    const int sy = y + oy, sz = z + oz;
+    const bool row_ok = sy >= 0 && sy < p.dy && sz >= 0 && sz < p.dz;
+    const uint32_t drow = static_cast<uint32_t>(y) * p.dx + static_cast<uint32_t>(z) * dxy;
+    const long long srow = static_cast<long long>(sy) * p.dx + static_cast<long long>(sz) * dxy;
+    const bool vec = (p.dx & 3) == 0;
+    for (int x0 = lane * 4; x0 < p.dx; x0 += 128) {
+      uint32_t out = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int x = x0 + i;
+        const int sx = x + ox;
+        uint32_t v = 0;
+        if (row_ok && x < p.dx && sx >= 0 && sx < p.dx) {
+          const long long sc = srow + sx;
+          v = merge_cell(src[sc], decode_cell(occ[sc], key[sc], epoch));
+        }
+        occ_n += v == 2u;
+        free_n += v == 1u;
+        out |= v << (8 * i);
       }
-      occ_n += v == 2u;
-      free_n += v == 1u;
-      out |= v << (8 * i);
-    }
-    if (nc == 4 && ((reinterpret_cast<uintptr_t>(dst + c0) & 3u) == 0)) {
-      *reinterpret_cast<uint32_t*>(dst + c0) = out;
-    } else {
-      for (int i = 0; i < nc; ++i) dst[c0 + i] = static_cast<uint8_t>(out >> (8 * i));
+      if (vec) {
+        *reinterpret_cast<uint32_t*>(dst + drow + x0) = out;
+      } else {
+        for (int i = 0; i < 4 && x0 + i < p.dx; ++i) dst[drow + x0 + i] = static_cast<uint8_t>(out >> (8 * i));
+      }
     }
   }
   unsigned vals[2] = {occ_n, free_n};

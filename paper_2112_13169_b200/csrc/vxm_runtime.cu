@@ -237,9 +237,11 @@ struct vxm_ctx {
   int32_t bundle[3] = {0, 0, 0};
 
   // device buffers
-  uint32_t* msw = nullptr;
-  uint32_t* ctr = nullptr;
+  uint8_t* occ = nullptr;
+  uint8_t* ctr = nullptr;
+  uint32_t* key = nullptr;
   uint8_t* loc[2] = {nullptr, nullptr};
+  double* qtab = nullptr;  // W column + H row back-projection factors
   vxm::Counters* counters = nullptr;
   vxm::FrameParams* frames_dev = nullptr;
   float* depth_dev = nullptr;
@@ -274,8 +276,7 @@ void launch_frame(vxm_ctx* c, bool cloud, bool timed) {
   VXM_CK(cudaMemsetAsync(c->counters, 0, sizeof(vxm::Counters) * S, c->stream));
   if (!cloud) {
     const long long npix = static_cast<long long>(kp.W) * kp.H;
-    const long long quads = (npix + 3) / 4;
-    dim3 grid(static_cast<unsigned>((quads + kPopulateThreads - 1) / kPopulateThreads), S);
+    dim3 grid(static_cast<unsigned>((npix + kPopulateThreads - 1) / kPopulateThreads), S);
     vxm::populate_depth_kernel<<<grid, kPopulateThreads, 0, c->stream>>>(kp);
   } else {
     dim3 grid(static_cast<unsigned>(c->nsm * 4), S);
@@ -284,12 +285,9 @@ void launch_frame(vxm_ctx* c, bool cloud, bool timed) {
   VXM_CK(cudaGetLastError());
   if (kp.vox_inf > 0) {
     const int r = kp.vox_inf;
-    const int HX = vxm::kDilTX + 2 * r, HY = vxm::kDilTY + 2 * r, HZ = vxm::kDilTZ + 2 * r;
-    const size_t smem = static_cast<size_t>(HX) * HY * HZ + static_cast<size_t>(vxm::kDilTX) * HY * HZ +
-                        static_cast<size_t>(vxm::kDilTX) * vxm::kDilTY * HZ;
-    dim3 grid(static_cast<unsigned>(((kp.dx + vxm::kDilTX - 1) / vxm::kDilTX) *
-                                    ((kp.dy + vxm::kDilTY - 1) / vxm::kDilTY)),
-              static_cast<unsigned>((kp.dz + vxm::kDilTZ - 1) / vxm::kDilTZ), S);
+    const size_t smem = vxm::dilate_smem_bytes(r, (kp.dx + 31) / 32);
+    dim3 grid(static_cast<unsigned>((kp.dy + vxm::kDilT - 1) / vxm::kDilT),
+              static_cast<unsigned>((kp.dz + vxm::kDilT - 1) / vxm::kDilT), S);
     vxm::dilate_kernel<<<grid, 256, smem, c->stream>>>(kp, r);
     VXM_CK(cudaGetLastError());
   }
@@ -303,10 +301,9 @@ void launch_frame(vxm_ctx* c, bool cloud, bool timed) {
   }
   if (timed) VXM_CK(cudaEventRecord(c->ev[3], c->stream));
   {
-    const long long quads = (c->n + 3) / 4;
-    const long long want = (quads + kMergeThreads - 1) / kMergeThreads;
-    const long long cap = static_cast<long long>(c->nsm) * 8;
-    dim3 grid(static_cast<unsigned>(std::max(1LL, std::min(want, cap))), S);
+    const long long rows = static_cast<long long>(kp.dy) * kp.dz;
+    const int rows_per_block = kMergeThreads / 32;
+    dim3 grid(static_cast<unsigned>((rows + rows_per_block - 1) / rows_per_block), S);
     vxm::merge_shift_count_kernel<<<grid, kMergeThreads, 0, c->stream>>>(kp);
     VXM_CK(cudaGetLastError());
   }
@@ -353,14 +350,16 @@ void prepare_frames(vxm_ctx* c, const vxm_pose* poses, const float* depth_dev_ba
       c->last_off[3 * s + a] = off[a];
     }
     c->last_shifted[s] = moved ? 1 : 0;
-    // epoch-tagged words need no reset; wrap-around clears the words once
+    // epoch-tagged cells need no per-frame reset; the 8-bit epoch wraps
+    // every 255 frames, when this stream's arrays are cleared once
     if (c->epoch[s] >= vxm::kMaxEpoch) {
-      VXM_CK(cudaMemsetAsync(c->msw + c->n * s, 0, sizeof(uint32_t) * c->n, c->stream));
-      if (c->ctr) VXM_CK(cudaMemsetAsync(c->ctr + c->n * s, 0, sizeof(uint32_t) * c->n, c->stream));
+      VXM_CK(cudaMemsetAsync(c->occ + c->n * s, 0, c->n, c->stream));
+      if (c->ctr) VXM_CK(cudaMemsetAsync(c->ctr + c->n * s, 0, c->n, c->stream));
+      VXM_CK(cudaMemsetAsync(c->key + c->n * s, 0, sizeof(uint32_t) * c->n, c->stream));
       c->epoch[s] = 0;
     }
     c->epoch[s] += 1;
-    f.tag = c->epoch[s] << vxm::kEpochShift;
+    f.epoch = c->epoch[s];
   }
   VXM_CK(cudaMemcpyAsync(c->frames_dev, c->frames_host, sizeof(vxm::FrameParams) * c->S,
                          cudaMemcpyHostToDevice, c->stream));
@@ -436,8 +435,10 @@ void destroy_ctx(vxm_ctx* c) {
   if (c->graph_cloud) cudaGraphExecDestroy(c->graph_cloud);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
-  cudaFree(c->msw);
+  cudaFree(c->occ);
   cudaFree(c->ctr);
+  cudaFree(c->key);
+  cudaFree(c->qtab);
   cudaFree(c->loc[0]);
   cudaFree(c->loc[1]);
   cudaFree(c->counters);
@@ -535,11 +536,13 @@ int vxm_create(const vxm_config* cfg, int32_t n_streams, int32_t device, uint32_
     for (auto& e : c->ev) VXM_CK(cudaEventCreate(&e));
     const size_t S = static_cast<size_t>(n_streams);
     const size_t npix = static_cast<size_t>(cfg->camera.width) * cfg->camera.height;
-    VXM_CK(cudaMalloc(&c->msw, sizeof(uint32_t) * c->n * S));
-    VXM_CK(cudaMemsetAsync(c->msw, 0, sizeof(uint32_t) * c->n * S, c->stream));
+    VXM_CK(cudaMalloc(&c->occ, c->n * S));
+    VXM_CK(cudaMemsetAsync(c->occ, 0, c->n * S, c->stream));
+    VXM_CK(cudaMalloc(&c->key, sizeof(uint32_t) * c->n * S));
+    VXM_CK(cudaMemsetAsync(c->key, 0, sizeof(uint32_t) * c->n * S, c->stream));
     if (cfg->vox_inf > 0) {
-      VXM_CK(cudaMalloc(&c->ctr, sizeof(uint32_t) * c->n * S));
-      VXM_CK(cudaMemsetAsync(c->ctr, 0, sizeof(uint32_t) * c->n * S, c->stream));
+      VXM_CK(cudaMalloc(&c->ctr, c->n * S));
+      VXM_CK(cudaMemsetAsync(c->ctr, 0, c->n * S, c->stream));
     }
     for (int b = 0; b < 2; ++b) {
       VXM_CK(cudaMalloc(&c->loc[b], c->n * S));
@@ -569,11 +572,23 @@ int vxm_create(const vxm_config* cfg, int32_t n_streams, int32_t device, uint32_
     kp.W = cfg->camera.width;
     kp.H = cfg->camera.height;
     // CameraModel::focal_x/y (geometry.hpp:67-68) and the principal point
-    // (geometry.cpp:50-51), computed once on the host with glibc tan.
-    kp.fx = (cfg->camera.width / 2.0) / std::tan(cfg->camera.fov_x / 2.0);
-    kp.fy = (cfg->camera.height / 2.0) / std::tan(cfg->camera.fov_y / 2.0);
-    kp.cx = cfg->camera.width / 2.0;
-    kp.cy = cfg->camera.height / 2.0;
+    // (geometry.cpp:50-51), computed once on the host with glibc tan; the
+    // per-column / per-row factors ((u + 0.5) - cx) / fx of back_project_rows
+    // (geometry.cpp:55-56) are tabulated with the same IEEE operations.
+    {
+      const double fx = (cfg->camera.width / 2.0) / std::tan(cfg->camera.fov_x / 2.0);
+      const double fy = (cfg->camera.height / 2.0) / std::tan(cfg->camera.fov_y / 2.0);
+      const double cx = cfg->camera.width / 2.0;
+      const double cy = cfg->camera.height / 2.0;
+      std::vector<double> q(static_cast<size_t>(kp.W) + kp.H);
+      for (int u = 0; u < kp.W; ++u) q[u] = ((u + 0.5) - cx) / fx;
+      for (int v = 0; v < kp.H; ++v) q[kp.W + v] = ((v + 0.5) - cy) / fy;
+      VXM_CK(cudaMalloc(&c->qtab, sizeof(double) * q.size()));
+      VXM_CK(cudaMemcpy(c->qtab, q.data(), sizeof(double) * q.size(), cudaMemcpyHostToDevice));
+      kp.qx = c->qtab;
+      kp.qy = c->qtab + kp.W;
+    }
+    kp.inv_vs = 1.0 / g.vox_size;
     kp.max_depth = cfg->camera.max_depth;
     kp.vox_inf = cfg->vox_inf;
     kp.vd = c->bundle[0];
@@ -581,18 +596,18 @@ int vxm_create(const vxm_config* cfg, int32_t n_streams, int32_t device, uint32_
     kp.vh = c->bundle[2];
     kp.tiles_x = (kp.vw + 7) / 8;
     kp.tiles_y = (kp.vh + 3) / 4;
-    kp.msw = c->msw;
+    kp.occ = c->occ;
     kp.ctr = c->ctr;
+    kp.key = c->key;
     kp.loc0 = c->loc[0];
     kp.loc1 = c->loc[1];
     kp.counters = c->counters;
     kp.frames = c->frames_dev;
     if (cfg->vox_inf > 0) {
-      const int r = cfg->vox_inf;
-      const size_t smem = static_cast<size_t>(vxm::kDilTX + 2 * r) * (vxm::kDilTY + 2 * r) * (vxm::kDilTZ + 2 * r) +
-                          static_cast<size_t>(vxm::kDilTX) * (vxm::kDilTY + 2 * r) * (vxm::kDilTZ + 2 * r) +
-                          static_cast<size_t>(vxm::kDilTX) * vxm::kDilTY * (vxm::kDilTZ + 2 * r);
-      if (smem > 200 * 1024) throw InvalidArg{"vox_inf too large for the dilation tile"};
+      const size_t smem = vxm::dilate_smem_bytes(cfg->vox_inf, (kp.dx + 31) / 32);
+      if (cfg->vox_inf > vxm::kMaxVoxInf || smem > 200 * 1024)
+        throw InvalidArg{"vox_inf " + std::to_string(cfg->vox_inf) + " exceeds the dilation tile limit (" +
+                         std::to_string(vxm::kMaxVoxInf) + ")"};
       VXM_CK(cudaFuncSetAttribute(vxm::dilate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     }

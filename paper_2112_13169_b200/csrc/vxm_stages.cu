@@ -75,7 +75,7 @@ unsigned blocks_for(long long n, int threads, int cap = 148 * 16) {
   return static_cast<unsigned>(b);
 }
 
-constexpr uint32_t kTag = 1u << vxm::kEpochShift;
+constexpr uint32_t kEpoch = 1u;
 
 // One-stream kernel parameters for a grid (no camera, no bundle).
 vxm::KParams grid_params(const vxm_grid_spec& g) {
@@ -85,6 +85,7 @@ vxm::KParams grid_params(const vxm_grid_spec& g) {
   kp.dz = g.dims[2];
   kp.n = static_cast<long long>(g.dims[0]) * g.dims[1] * g.dims[2];
   kp.vs = g.vox_size;
+  kp.inv_vs = 1.0 / g.vox_size;
   return kp;
 }
 
@@ -113,8 +114,8 @@ int vxm_populate_occupied(const vxm_grid_spec* grid, uint8_t* ms, const double* 
     if (!ms || !t_vc || (n && (!xs || !ys || !zs))) throw StageError{VXM_EINVAL, "null argument"};
     vxm::KParams kp = grid_params(*grid);
     const long long N = kp.n;
-    DevBuf<uint8_t> d_ms(N);
-    DevBuf<uint32_t> d_msw(N), d_ctr(vox_inf > 0 ? N : 0);
+    DevBuf<uint8_t> d_ms(N), d_occ(N), d_ctr(vox_inf > 0 ? N : 0);
+    DevBuf<uint32_t> d_key(N);
     DevBuf<double> d_pts(3 * n + 1);
     DevBuf<vxm::Counters> d_cnt(1);
     DevBuf<vxm::FrameParams> d_frame(1);
@@ -124,7 +125,7 @@ int vxm_populate_occupied(const vxm_grid_spec* grid, uint8_t* ms, const double* 
     f.ys = d_pts.p + n;
     f.zs = d_pts.p + 2 * n;
     f.n_points = static_cast<long long>(n);
-    f.tag = kTag;
+    f.epoch = kEpoch;
     VXM_SCK(cudaMemcpy(d_frame.p, &f, sizeof(f), cudaMemcpyHostToDevice));
     if (n) {
       VXM_SCK(cudaMemcpy(d_pts.p, xs, sizeof(double) * n, cudaMemcpyHostToDevice));
@@ -133,9 +134,10 @@ int vxm_populate_occupied(const vxm_grid_spec* grid, uint8_t* ms, const double* 
     }
     VXM_SCK(cudaMemcpy(d_ms.p, ms, N, cudaMemcpyHostToDevice));
     VXM_SCK(cudaMemset(d_cnt.p, 0, sizeof(vxm::Counters)));
-    if (d_ctr.p) VXM_SCK(cudaMemset(d_ctr.p, 0, sizeof(uint32_t) * N));
-    vxm::encode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_ms.p, d_msw.p, N, kTag);
-    kp.msw = d_msw.p;
+    if (d_ctr.p) VXM_SCK(cudaMemset(d_ctr.p, 0, N));
+    vxm::encode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_ms.p, d_occ.p, d_key.p, N, kEpoch);
+    kp.occ = d_occ.p;
+    kp.key = d_key.p;
     kp.ctr = d_ctr.p;
     kp.vox_inf = vox_inf;
     kp.counters = d_cnt.p;
@@ -144,19 +146,17 @@ int vxm_populate_occupied(const vxm_grid_spec* grid, uint8_t* ms, const double* 
     VXM_SCK(cudaGetLastError());
     if (vox_inf > 0) {
       const int r = vox_inf;
-      const size_t smem = static_cast<size_t>(vxm::kDilTX + 2 * r) * (vxm::kDilTY + 2 * r) * (vxm::kDilTZ + 2 * r) +
-                          static_cast<size_t>(vxm::kDilTX) * (vxm::kDilTY + 2 * r) * (vxm::kDilTZ + 2 * r) +
-                          static_cast<size_t>(vxm::kDilTX) * vxm::kDilTY * (vxm::kDilTZ + 2 * r);
-      if (smem > 200 * 1024) throw StageError{VXM_EINVAL, "vox_inf too large for the dilation tile"};
+      const size_t smem = vxm::dilate_smem_bytes(r, (kp.dx + 31) / 32);
+      if (r > vxm::kMaxVoxInf || smem > 200 * 1024)
+        throw StageError{VXM_EINVAL, "vox_inf exceeds the dilation tile limit"};
       VXM_SCK(cudaFuncSetAttribute(vxm::dilate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
-      dim3 g3(static_cast<unsigned>(((kp.dx + vxm::kDilTX - 1) / vxm::kDilTX) *
-                                    ((kp.dy + vxm::kDilTY - 1) / vxm::kDilTY)),
-              static_cast<unsigned>((kp.dz + vxm::kDilTZ - 1) / vxm::kDilTZ), 1);
+      dim3 g3(static_cast<unsigned>((kp.dy + vxm::kDilT - 1) / vxm::kDilT),
+              static_cast<unsigned>((kp.dz + vxm::kDilT - 1) / vxm::kDilT), 1);
       vxm::dilate_kernel<<<g3, 256, smem>>>(kp, r);
       VXM_SCK(cudaGetLastError());
     }
-    vxm::decode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_msw.p, d_ms.p, N, kTag);
+    vxm::decode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_occ.p, d_key.p, d_ms.p, N, kEpoch);
     VXM_SCK(cudaGetLastError());
     vxm::Counters cnt{};
     VXM_SCK(cudaMemcpy(&cnt, d_cnt.p, sizeof(cnt), cudaMemcpyDeviceToHost));
@@ -205,24 +205,25 @@ int vxm_trace_bundle(const vxm_grid_spec* grid, uint8_t* ms, const int32_t bundl
     kp.vh = bundle[2];
     kp.tiles_x = (kp.vw + 7) / 8;
     kp.tiles_y = (kp.vh + 3) / 4;
-    DevBuf<uint8_t> d_ms(N);
-    DevBuf<uint32_t> d_msw(N);
+    DevBuf<uint8_t> d_ms(N), d_occ(N);
+    DevBuf<uint32_t> d_key(N);
     DevBuf<vxm::Counters> d_cnt(1);
     DevBuf<vxm::FrameParams> d_frame(1);
     vxm::FrameParams f{};
     fill_pose(f, *t_vc);
-    f.tag = kTag;
+    f.epoch = kEpoch;
     VXM_SCK(cudaMemcpy(d_frame.p, &f, sizeof(f), cudaMemcpyHostToDevice));
     VXM_SCK(cudaMemcpy(d_ms.p, ms, N, cudaMemcpyHostToDevice));
     VXM_SCK(cudaMemset(d_cnt.p, 0, sizeof(vxm::Counters)));
-    vxm::encode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_ms.p, d_msw.p, N, kTag);
-    kp.msw = d_msw.p;
+    vxm::encode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_ms.p, d_occ.p, d_key.p, N, kEpoch);
+    kp.occ = d_occ.p;
+    kp.key = d_key.p;
     kp.counters = d_cnt.p;
     kp.frames = d_frame.p;
     const int tiles = kp.tiles_x * kp.tiles_y;
     vxm::trace_bundle_kernel<<<dim3((tiles + 3) / 4, 1), 128>>>(kp);
     VXM_SCK(cudaGetLastError());
-    vxm::decode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_msw.p, d_ms.p, N, kTag);
+    vxm::decode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_occ.p, d_key.p, d_ms.p, N, kEpoch);
     VXM_SCK(cudaGetLastError());
     vxm::Counters cnt{};
     VXM_SCK(cudaMemcpy(&cnt, d_cnt.p, sizeof(cnt), cudaMemcpyDeviceToHost));

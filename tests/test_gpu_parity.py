@@ -292,3 +292,27 @@ def test_batched_streams_equal_independent_pipelines(gpu_lib):
             assert stats[s]["occupied_count"] == sr["occupied_count"]
             assert stats[s]["voxels_freed"] == sr["voxels_freed"]
             assert np.array_equal(batch.local_grid(s)[0], singles[s].local_grid()[0]), (k, s)
+
+
+def test_pipeline_long_trajectory_wraps_epochs(gpu_lib):
+    """cfg4-style moving robot over more frames than the 8-bit epoch holds
+    (255), shifting by about one voxel per frame."""
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 64, 48, 6.5)
+    grid = vm.GridSpec.create_centered(6.0, 6.0, 3.0, 0.1, (0.0, -8.0, 0.0))
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=1, depth=6.5)
+    boxes = scenes.corridor_boxes(-12.0, 25.0)
+    gpu = vm.MappingPipeline(cfg)
+    orc = oracle_pipeline(cfg)
+    shifts = 0
+    for k in range(300):
+        pose = vm.look_along_x((0.0, -8.0 + 0.1001 * k, 0.0))
+        depth = scenes.render(cam, pose, boxes)
+        sg = gpu.integrate_depth(depth, pose)
+        sr = orc.integrate_depth(depth, pose)
+        shifts += sr["shifted"]
+        for key in ("occupied_count", "freed_count", "voxels_freed", "voxels_marked_unknown_traced",
+                    "shifted", "shift_offset", "origin", "points_outside"):
+            assert sg[key] == sr[key], (k, key, sg[key], sr[key])
+        if k % 50 == 49 or k == 299:
+            assert np.array_equal(gpu.local_grid()[0], orc.local_grid()[0]), k
+    assert shifts > 250
