@@ -5,6 +5,7 @@
 #pragma once
 
 #include "vxm_device.cuh"
+#include "vxm_kernels.cuh"
 
 namespace vxm {
 
@@ -168,5 +169,8 @@ __global__ void __launch_bounds__(256) cloud_write_rows_kernel(const float* dept
     __syncthreads();
   }
 }
+
+// Stand-alone trace: fold K3's slots (K4 does this in the per-frame graph).
+__global__ void fold_trace_slots_kernel(Counters* c) { fold_trace_slots(*c); }
 
 }  // namespace vxm

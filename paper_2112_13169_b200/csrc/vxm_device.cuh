@@ -66,6 +66,7 @@ struct Counters {
   unsigned long long voxels_skipped;
   unsigned long long occupied;
   unsigned long long freed;
+  unsigned long long trace_slots[32][4];  // K3 partials, folded by K4
 };
 
 // Per-stream, per-frame parameters: uploaded each frame as one small H2D

@@ -110,9 +110,11 @@ __global__ void __launch_bounds__(256) populate_cloud_kernel(KParams p) {
 // ---------------------------------------------------------------------------
 constexpr int kDilT = 8;
 
-__host__ __device__ constexpr size_t dilate_smem_bytes(int r, int words) {
-  return sizeof(uint32_t) * static_cast<size_t>(words) *
-         (2u * (kDilT + 2 * r) * (kDilT + 2 * r) + static_cast<size_t>(kDilT) * (kDilT + 2 * r));
+// Shared memory: bit planes (in, bx, by) plus the staged centre bytes.
+__host__ __device__ constexpr size_t dilate_smem_bytes(int r, int dx) {
+  return sizeof(uint32_t) * static_cast<size_t>((dx + 31) / 32) *
+             (2u * (kDilT + 2 * r) * (kDilT + 2 * r) + static_cast<size_t>(kDilT) * (kDilT + 2 * r)) +
+         static_cast<size_t>((dx + 3) & ~3) * (kDilT + 2 * r) * (kDilT + 2 * r);
 }
 
 __global__ void __launch_bounds__(256) dilate_kernel(KParams p, int r) {
@@ -130,14 +132,34 @@ __global__ void __launch_bounds__(256) dilate_kernel(KParams p, int r) {
   uint32_t* by = bx + H * H * W;        // [H z][kDilT y][W], y-dilated
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
 
-  for (int row = warp; row < H * H; row += nw) {
+  // Stage the halo rows' centre bytes in shared memory with independent
+  // 4-byte loads (the whole block's loads are in flight together), then pack
+  // them into bitmasks with ballots.
+  uint8_t* raw = reinterpret_cast<uint8_t*>(by + H * kDilT * W);  // [H*H][dx4]
+  const int dx4 = (p.dx + 3) & ~3;
+  const int words_per_row = dx4 >> 2;
+  const bool vec = (p.dx & 3) == 0;
+#pragma unroll 4
+  for (int i = threadIdx.x; i < H * H * words_per_row; i += blockDim.x) {
+    const int row = i / words_per_row, wd = i - row * words_per_row;
     const int hy = row % H, hz = row / H;
     const int y = y0 - r + hy, z = z0 - r + hz;
-    const bool ok = y >= 0 && y < p.dy && z >= 0 && z < p.dz;
+    uint32_t v = 0;
+    if (y >= 0 && y < p.dy && z >= 0 && z < p.dz) {
+      const uint8_t* src = ctr + static_cast<uint32_t>(y) * p.dx + static_cast<uint32_t>(z) * dxy + 4 * wd;
+      if (vec) {
+        v = __ldg(reinterpret_cast<const uint32_t*>(src));
+      } else {
+        for (int b = 0; b < 4 && 4 * wd + b < p.dx; ++b) v |= static_cast<uint32_t>(src[b]) << (8 * b);
+      }
+    }
+    reinterpret_cast<uint32_t*>(raw)[i] = v;
+  }
+  __syncthreads();
+  for (int row = warp; row < H * H; row += nw) {
     for (int w = 0; w < W; ++w) {
       const int x = (w << 5) + lane;
-      bool c = false;
-      if (ok && x < p.dx) c = ctr[static_cast<uint32_t>(x) + static_cast<uint32_t>(y) * p.dx + static_cast<uint32_t>(z) * dxy] == e;
+      const bool c = x < p.dx && raw[row * dx4 + x] == e;
       const uint32_t m = __ballot_sync(0xffffffffu, c);
       if (lane == 0) in[row * W + w] = m;
     }
@@ -183,15 +205,20 @@ __global__ void __launch_bounds__(256) dilate_kernel(KParams p, int r) {
 // (proj/src/raytracer.cpp:35-61) + walk_ray (proj/include/voxmap/raytracer.hpp:
 // 76-118) + traverse_ray (raytracer.cpp:63-96). One thread per ray; a warp
 // owns an 8x4 tile of end-plane targets so that its rays stay spatially
-// coherent. The walk runs in chunks of kChunk DDA steps: the cell indices of
-// a chunk are computed first (they do not depend on grid contents), their
-// occupancy bytes are loaded together through the read-only path, then the
-// chunk is resolved in order. The Sequential last-writer rule is an
-// atomicMax on the cell key; before issuing it a lane drops its write when
-// lane+1 or lane+8 (both higher ray indices) writes the same cell in the
-// same step, which removes most same-address traffic near the camera.
+// coherent, and a block is one warp so no warp waits on another.
+//
+// The walk runs in chunks of kChunk DDA steps, written without divergent
+// branches: (A) the chunk's cell indices are computed (they do not depend on
+// grid contents), (B) their occupancy bytes are loaded together through the
+// read-only path, (C) the chunk is resolved in order. The Sequential
+// last-writer rule is an atomicMax on the cell key; before issuing it a lane
+// drops its write when lane+1 or lane+8 (both higher ray indices) writes the
+// same cell in the same step, which removes most same-address traffic near
+// the camera. Counters go to 32 per-stream slots (one RED per warp each),
+// summed by K4.
 // ---------------------------------------------------------------------------
-constexpr int kChunk = 4;
+constexpr int kChunk = 8;
+constexpr int kTraceSlots = 32;
 
 struct RayState {
   int cur[3];
@@ -241,32 +268,10 @@ __device__ __forceinline__ void ray_setup(const double* R, const double* start, 
   }
 }
 
-// Advances the DDA by one cell (walk_ray's loop body, raytracer.hpp:103-116):
-// ties step x, then y, then z; returns false when the next crossing lies at
-// or beyond max_dist - 1e-10.
-__device__ __forceinline__ bool ray_advance(RayState& st) {
-  const bool x_first = st.tmax[0] <= st.tmax[1] && st.tmax[0] <= st.tmax[2];
-  const bool y_first = !x_first && st.tmax[1] <= st.tmax[2];
-  const double tm = x_first ? st.tmax[0] : (y_first ? st.tmax[1] : st.tmax[2]);
-  if (tm >= st.stop) return false;
-  if (x_first) {
-    st.cur[0] += st.step[0];
-    st.tmax[0] = dadd(st.tmax[0], st.tdelta[0]);
-  } else if (y_first) {
-    st.cur[1] += st.step[1];
-    st.tmax[1] = dadd(st.tmax[1], st.tdelta[1]);
-  } else {
-    st.cur[2] += st.step[2];
-    st.tmax[2] = dadd(st.tmax[2], st.tdelta[2]);
-  }
-  return true;
-}
-
-__global__ void __launch_bounds__(128) trace_bundle_kernel(KParams p) {
+__global__ void __launch_bounds__(32) trace_bundle_kernel(KParams p) {
   const int s = blockIdx.y;
   const FrameParams* fp = p.frames + s;
   const uint32_t epoch = fp->epoch;
-  const uint32_t tag = key_tag(epoch);
   uint32_t* key = p.key + static_cast<long long>(s) * p.n;
   const uint8_t* occ = p.occ + static_cast<long long>(s) * p.n;
   double R[9], start[3];
@@ -275,20 +280,27 @@ __global__ void __launch_bounds__(128) trace_bundle_kernel(KParams p) {
 #pragma unroll
   for (int i = 0; i < 3; ++i) start[i] = fp->trans[i];
 
-  const int lane = threadIdx.x & 31;
-  const int tile = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x;
+  const int tile = blockIdx.x;
   const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
   const int xi_idx = tx * 8 + (lane & 7);
   const int yi_idx = ty * 4 + (lane >> 3);
   const bool active = ty < p.tiles_y && xi_idx < p.vw && yi_idx < p.vh;
   const uint32_t ray = static_cast<uint32_t>(yi_idx) * p.vw + xi_idx;  // row-major, y outer
-  const uint32_t ray_key = tag | ((ray + 1u) << 1);
+  const uint32_t ray_key = key_tag(epoch) | ((ray + 1u) << 1);
 
   RayState st;
   ray_setup(R, start, p.vs, xi_idx - (p.vw - 1) / 2, yi_idx - (p.vh - 1) / 2, p.vd, st);
 
   const unsigned dx = p.dx, dy = p.dy, dz = p.dz;
-  const uint32_t dxy = dx * dy;
+  const int dxy = p.dx * p.dy;
+  // linear-index increment of one step along each axis
+  const int lin0 = st.step[0], lin1 = st.step[1] * p.dx, lin2 = st.step[2] * dxy;
+  unsigned x = st.cur[0], y = st.cur[1], z = st.cur[2];
+  int idx = st.cur[0] + st.cur[1] * p.dx + st.cur[2] * dxy;
+  double t0 = st.tmax[0], t1 = st.tmax[1], t2 = st.tmax[2];
+  const double stop = st.stop;
+
   bool walking = active;
   bool entered = false;
   uint32_t traced_bit = 0;
@@ -296,53 +308,83 @@ __global__ void __launch_bounds__(128) trace_bundle_kernel(KParams p) {
 
   while (__any_sync(0xffffffffu, walking)) {
     uint32_t cell[kChunk];
-    bool valid[kChunk];
 #pragma unroll
     for (int j = 0; j < kChunk; ++j) {
-      valid[j] = false;
-      cell[j] = 0;
+      const bool inb = x < dx && y < dy && z < dz;
+      const bool visit = walking && inb;
+      skipped += (walking && !inb && !entered) ? 1u : 0u;
+      walking = walking && (inb || !entered);  // a line leaves a convex grid exactly once
+      entered = entered || visit;
+      cell[j] = visit ? static_cast<uint32_t>(idx) : 0xffffffffu;
+      // walk_ray's step (raytracer.hpp:103-116): ties step x, then y, then z
+      const bool bx = t0 <= t1 && t0 <= t2;
+      const bool by = !bx && t1 <= t2;
+      const double tm = bx ? t0 : (by ? t1 : t2);
+      walking = walking && !(tm >= stop);
       if (walking) {
-        const unsigned x = st.cur[0], y = st.cur[1], z = st.cur[2];
-        if (x >= dx || y >= dy || z >= dz) {
-          if (entered) {
-            walking = false;  // a line leaves a convex grid exactly once
-            continue;
-          }
-          ++skipped;
+        if (bx) {
+          t0 = dadd(t0, st.tdelta[0]);
+          x += st.step[0];
+          idx += lin0;
+        } else if (by) {
+          t1 = dadd(t1, st.tdelta[1]);
+          y += st.step[1];
+          idx += lin1;
         } else {
-          entered = true;
-          valid[j] = true;
-          cell[j] = x + y * dx + z * dxy;
+          t2 = dadd(t2, st.tdelta[2]);
+          z += st.step[2];
+          idx += lin2;
         }
-        walking = ray_advance(st);
       }
     }
     uint32_t o[kChunk];
 #pragma unroll
-    for (int j = 0; j < kChunk; ++j) o[j] = valid[j] ? __ldg(occ + cell[j]) : 0u;
+    for (int j = 0; j < kChunk; ++j) o[j] = cell[j] != 0xffffffffu ? __ldg(occ + cell[j]) : 0u;
 #pragma unroll
     for (int j = 0; j < kChunk; ++j) {
-      bool write = false;
-      uint32_t idx = 0xffffffffu - lane;  // unique non-cell sentinel for idle lanes
-      if (valid[j]) {
-        if (o[j] == epoch) {
-          traced_bit = 1;
-        } else {
-          write = true;
-          idx = cell[j];
-          if (traced_bit) ++traced; else ++freed;
-        }
-      }
-      const uint32_t right = __shfl_down_sync(0xffffffffu, idx, 1);
-      const uint32_t below = __shfl_down_sync(0xffffffffu, idx, 8);
-      const bool dominated = (lane < 31 && right == idx) || (lane < 24 && below == idx);
-      if (write && !dominated) atomicMax(key + idx, ray_key | traced_bit);
+      const bool valid = cell[j] != 0xffffffffu;
+      const bool is_occ = valid && o[j] == epoch;
+      const bool write = valid && !is_occ;
+      traced += (write && traced_bit) ? 1u : 0u;
+      freed += (write && !traced_bit) ? 1u : 0u;
+      const uint32_t kval = ray_key | traced_bit;
+      traced_bit |= is_occ ? 1u : 0u;
+      const uint32_t id = write ? cell[j] : (0xfffffff0u - lane);  // idle lanes never match
+      const uint32_t right = __shfl_down_sync(0xffffffffu, id, 1);
+      const uint32_t below = __shfl_down_sync(0xffffffffu, id, 8);
+      const bool dominated = (lane < 31 && right == id) || (lane < 24 && below == id);
+      if (write && !dominated) atomicMax(key + cell[j], kval);
     }
   }
-  unsigned vals[4] = {active ? 1u : 0u, freed, traced, skipped};
-  unsigned long long* dst[4] = {&p.counters[s].rays_traced, &p.counters[s].voxels_freed,
-                                &p.counters[s].voxels_traced, &p.counters[s].voxels_skipped};
-  block_accumulate<4>(vals, dst);
+  unsigned long long* slot = &p.counters[s].trace_slots[tile % kTraceSlots][0];
+  const unsigned r_n = __reduce_add_sync(0xffffffffu, active ? 1u : 0u);
+  const unsigned f_n = __reduce_add_sync(0xffffffffu, freed);
+  const unsigned t_n = __reduce_add_sync(0xffffffffu, traced);
+  const unsigned k_n = __reduce_add_sync(0xffffffffu, skipped);
+  if (lane == 0) {
+    if (r_n) atomicAdd(slot + 0, r_n);
+    if (f_n) atomicAdd(slot + 1, f_n);
+    if (t_n) atomicAdd(slot + 2, t_n);
+    if (k_n) atomicAdd(slot + 3, k_n);
+  }
+}
+
+// Sums K3's per-slot counters into the stream's totals (one warp).
+__device__ __forceinline__ void fold_trace_slots(Counters& c) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long v[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    v[i] = c.trace_slots[lane][i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_down_sync(0xffffffffu, v[i], o);
+  }
+  if (lane == 0) {
+    c.rays_traced = v[0];
+    c.voxels_freed = v[1];
+    c.voxels_traced = v[2];
+    c.voxels_skipped = v[3];
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -368,6 +410,8 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p) {
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int rows = p.dy * p.dz;
   const uint32_t dxy = static_cast<uint32_t>(p.dx) * p.dy;
+
+  if (blockIdx.x == 0 && threadIdx.x < 32) fold_trace_slots(p.counters[s]);
 
   unsigned occ_n = 0, free_n = 0;
   if (row < rows) {

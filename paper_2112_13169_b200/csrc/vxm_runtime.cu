@@ -215,7 +215,6 @@ void check_device(int device) {
 }
 
 constexpr int kPopulateThreads = 256;
-constexpr int kTraceThreads = 128;
 constexpr int kMergeThreads = 256;
 
 }  // namespace
@@ -285,7 +284,7 @@ void launch_frame(vxm_ctx* c, bool cloud, bool timed) {
   VXM_CK(cudaGetLastError());
   if (kp.vox_inf > 0) {
     const int r = kp.vox_inf;
-    const size_t smem = vxm::dilate_smem_bytes(r, (kp.dx + 31) / 32);
+    const size_t smem = vxm::dilate_smem_bytes(r, kp.dx);
     dim3 grid(static_cast<unsigned>((kp.dy + vxm::kDilT - 1) / vxm::kDilT),
               static_cast<unsigned>((kp.dz + vxm::kDilT - 1) / vxm::kDilT), S);
     vxm::dilate_kernel<<<grid, 256, smem, c->stream>>>(kp, r);
@@ -293,10 +292,8 @@ void launch_frame(vxm_ctx* c, bool cloud, bool timed) {
   }
   if (timed) VXM_CK(cudaEventRecord(c->ev[2], c->stream));
   {
-    const int tiles = kp.tiles_x * kp.tiles_y;
-    const int warps_per_block = kTraceThreads / 32;
-    dim3 grid(static_cast<unsigned>((tiles + warps_per_block - 1) / warps_per_block), S);
-    vxm::trace_bundle_kernel<<<grid, kTraceThreads, 0, c->stream>>>(kp);
+    dim3 grid(static_cast<unsigned>(kp.tiles_x * kp.tiles_y), S);
+    vxm::trace_bundle_kernel<<<grid, 32, 0, c->stream>>>(kp);
     VXM_CK(cudaGetLastError());
   }
   if (timed) VXM_CK(cudaEventRecord(c->ev[3], c->stream));
@@ -604,7 +601,7 @@ int vxm_create(const vxm_config* cfg, int32_t n_streams, int32_t device, uint32_
     kp.counters = c->counters;
     kp.frames = c->frames_dev;
     if (cfg->vox_inf > 0) {
-      const size_t smem = vxm::dilate_smem_bytes(cfg->vox_inf, (kp.dx + 31) / 32);
+      const size_t smem = vxm::dilate_smem_bytes(cfg->vox_inf, kp.dx);
       if (cfg->vox_inf > vxm::kMaxVoxInf || smem > 200 * 1024)
         throw InvalidArg{"vox_inf " + std::to_string(cfg->vox_inf) + " exceeds the dilation tile limit (" +
                          std::to_string(vxm::kMaxVoxInf) + ")"};

@@ -146,7 +146,7 @@ int vxm_populate_occupied(const vxm_grid_spec* grid, uint8_t* ms, const double* 
     VXM_SCK(cudaGetLastError());
     if (vox_inf > 0) {
       const int r = vox_inf;
-      const size_t smem = vxm::dilate_smem_bytes(r, (kp.dx + 31) / 32);
+      const size_t smem = vxm::dilate_smem_bytes(r, kp.dx);
       if (r > vxm::kMaxVoxInf || smem > 200 * 1024)
         throw StageError{VXM_EINVAL, "vox_inf exceeds the dilation tile limit"};
       VXM_SCK(cudaFuncSetAttribute(vxm::dilate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -220,9 +220,9 @@ int vxm_trace_bundle(const vxm_grid_spec* grid, uint8_t* ms, const int32_t bundl
     kp.key = d_key.p;
     kp.counters = d_cnt.p;
     kp.frames = d_frame.p;
-    const int tiles = kp.tiles_x * kp.tiles_y;
-    vxm::trace_bundle_kernel<<<dim3((tiles + 3) / 4, 1), 128>>>(kp);
+    vxm::trace_bundle_kernel<<<dim3(kp.tiles_x * kp.tiles_y, 1), 32>>>(kp);
     VXM_SCK(cudaGetLastError());
+    vxm::fold_trace_slots_kernel<<<1, 32>>>(d_cnt.p);
     vxm::decode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_occ.p, d_key.p, d_ms.p, N, kEpoch);
     VXM_SCK(cudaGetLastError());
     vxm::Counters cnt{};
