@@ -120,31 +120,40 @@ __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a,
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
 
-// floor(RN(acc / vs)) without the IEEE division whenever that is provably
-// the same value: q = RN(acc * RN(1/vs)) is within 2^-51 |q| of RN(acc/vs),
-// so if q is further than 2^-46 |q| from the nearest integer both quotients
-// lie strictly on the same side of it and have the same floor. Otherwise
-// (near an integer, zero, or extreme magnitudes) the exact division runs.
-__device__ __forceinline__ double floor_div(double acc, double vs, double inv_vs) {
-  const double q = dmul(acc, inv_vs);
-  const double aq = fabs(q);
-  if (aq > 0x1p-1000 && aq < 0x1p+1000) {
-    const double dist = fabs(dsub(q, rint(q)));
-    if (dist > dmul(aq, 0x1p-46)) return floor(q);
-  }
-  return floor(ddiv(acc, vs));
-}
-
 // floor(acc / vs), clamped to +-1e9 and truncated to int32, exactly as
 // transform_voxelize_scalar (proj/src/kernels/kernels_scalar.cpp:31-34):
 // f = std::min(std::max(f, -1e9), 1e9) keeps NaN, and x86's cvttsd2si turns
 // NaN into INT32_MIN, which the bounds test then rejects.
-__device__ __forceinline__ int voxel_coord(double acc, double vs, double inv_vs) {
-  double f = floor_div(acc, vs, inv_vs);
+__device__ __noinline__ int voxel_coord_exact(double acc, double vs) {
+  double f = floor(ddiv(acc, vs));
   f = (f < -1e9) ? -1e9 : f;
   f = (1e9 < f) ? 1e9 : f;
   if (f != f) return INT32_MIN;
   return static_cast<int>(f);
+}
+
+// Same value without the IEEE division whenever that is provable:
+// q = RN(acc * RN(1/vs)) is within 2^-51 |q| of RN(acc/vs), so when q is
+// further than 2^-46 |q| from its nearest integer both quotients lie strictly
+// on the same side of every integer and share their floor. The nearest
+// integer comes from the 1.5*2^52 rounding trick (two adds on the fp64 pipe,
+// integer read from the low word), so the fast path needs no conversion
+// instructions. Near an integer, at zero, or beyond 2^30 (where the +-1e9
+// clamp may apply) the exact division runs.
+__device__ __forceinline__ int voxel_coord(double acc, double vs, double inv_vs) {
+  constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+  const double q = dmul(acc, inv_vs);
+  const double aq = fabs(q);
+  if (aq > 0x1p-1000 && aq < 0x1p+30) {
+    const double t = dadd(q, kMagic);
+    const double n = dsub(t, kMagic);        // rint(q)
+    const double dist = fabs(dsub(q, n));
+    if (dist > dmul(aq, 0x1p-46)) {
+      const int ni = __double2loint(t);      // n as int32
+      return n > q ? ni - 1 : ni;
+    }
+  }
+  return voxel_coord_exact(acc, vs);
 }
 
 // p_v[a] = ((t[a] + R[3a]x) + R[3a+1]y) + R[3a+2]z   (kernels_scalar.cpp:27-30)

@@ -15,10 +15,10 @@ namespace vxm {
 // ---------------------------------------------------------------------------
 // K1: depth_to_cloud (proj/src/geometry.cpp:45-57) fused with
 // voxelize_points + the centre store of mark_point (proj/src/integrator.cpp:
-// 24-41, 62-85). One pixel per thread: the chain is fp64-latency bound, so
-// the kernel wants threads, not work per thread. Pixels never materialise
-// as a point cloud; ((u + 0.5) - cx) / fx comes from a per-column table
-// computed once with the same IEEE operations.
+// 24-41, 62-85). Pixels never materialise as a point cloud;
+// ((u + 0.5) - cx) / fx comes from a per-column table computed once with the
+// same IEEE operations, and floor(acc / vs) avoids the fp64 division when
+// provably exact (voxel_coord).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ unsigned populate_point(const KParams& p, const double* R,
                                                    const double* t, uint8_t* target,
@@ -48,22 +48,35 @@ __global__ void __launch_bounds__(256) populate_depth_kernel(KParams p) {
   for (int i = 0; i < 3; ++i) t[i] = fp->trans[i];
   const float* depth = fp->depth;
 
+  // Each thread owns 4 consecutive pixels: one 16-byte streaming load keeps
+  // enough bytes in flight for HBM when many streams are batched, and the 4
+  // independent fp64 chains give the scheduler ILP.
   const int npix = p.W * p.H;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int first = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   unsigned total = 0, outside = 0;
-  if (i < npix) {
-    const float d = __ldcs(depth + i);
-    // DepthImage::valid_depth (geometry.hpp:124): finite and > 0; then the
-    // max-depth cut on the promoted double (geometry.cpp:53-54).
-    if (isfinite(d) && d > 0.0f) {
-      const double D = static_cast<double>(d);
-      if (!(D > p.max_depth)) {
-        total = 1;
-        const int v = i / p.W;
-        const int u = i - v * p.W;
-        outside = populate_point(p, R, t, target, mark, dmul(__ldg(p.qx + u), D),
-                                 dmul(__ldg(p.qy + v), D), D);
-      }
+  if (first < npix) {
+    float d[4];
+    if (first + 3 < npix && (reinterpret_cast<uintptr_t>(depth + first) & 15u) == 0) {
+      const float4 v4 = __ldcs(reinterpret_cast<const float4*>(depth + first));
+      d[0] = v4.x; d[1] = v4.y; d[2] = v4.z; d[3] = v4.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) d[k] = first + k < npix ? depth[first + k] : 0.0f;
+    }
+    const int v0 = first / p.W;
+    const int u0 = first - v0 * p.W;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int u = u0 + k, v = v0;
+      if (u >= p.W) { u -= p.W; ++v; }  // a row boundary inside the quad
+      // DepthImage::valid_depth (geometry.hpp:124): finite and > 0; then the
+      // max-depth cut on the promoted double (geometry.cpp:53-54).
+      if (!(isfinite(d[k]) && d[k] > 0.0f)) continue;
+      const double D = static_cast<double>(d[k]);
+      if (D > p.max_depth) continue;
+      ++total;
+      outside += populate_point(p, R, t, target, mark, dmul(__ldg(p.qx + u), D),
+                                dmul(__ldg(p.qy + v), D), D);
     }
   }
   unsigned vals[2] = {total, outside};
@@ -103,18 +116,17 @@ __global__ void __launch_bounds__(256) populate_cloud_kernel(KParams p) {
 // K2: obstacle inflation. mark_point writes the (2r+1)^3 cube around every
 // in-bounds centre, clipped to the grid (integrator.cpp:70-83): a Chebyshev
 // dilation of the centre set restricted to the grid, which is separable.
-// A block owns an 8x8 (y,z) tile of full x-rows. The rows plus an r-row halo
-// are packed into bitmasks with warp ballots, dilated along x with shifts,
-// then along y and z with ORs, all in shared memory; set bits are written
-// back as Occupied bytes.
+// A block owns an 8x8 (y,z) tile of full x-rows. Its rows plus an r-row halo
+// are loaded with coalesced 4-byte loads and packed into bitmasks (one warp
+// per row), dilated along x with shifts, then along y and z with ORs, all in
+// shared memory; set bits are written back as Occupied bytes.
 // ---------------------------------------------------------------------------
 constexpr int kDilT = 8;
 
-// Shared memory: bit planes (in, bx, by) plus the staged centre bytes.
+// Shared memory: three bit planes (in, x-dilated, y-dilated).
 __host__ __device__ constexpr size_t dilate_smem_bytes(int r, int dx) {
   return sizeof(uint32_t) * static_cast<size_t>((dx + 31) / 32) *
-             (2u * (kDilT + 2 * r) * (kDilT + 2 * r) + static_cast<size_t>(kDilT) * (kDilT + 2 * r)) +
-         static_cast<size_t>((dx + 3) & ~3) * (kDilT + 2 * r) * (kDilT + 2 * r);
+         (2u * (kDilT + 2 * r) * (kDilT + 2 * r) + static_cast<size_t>(kDilT) * (kDilT + 2 * r));
 }
 
 __global__ void __launch_bounds__(256) dilate_kernel(KParams p, int r) {
@@ -131,71 +143,72 @@ __global__ void __launch_bounds__(256) dilate_kernel(KParams p, int r) {
   uint32_t* bx = in + H * H * W;        // x-dilated
   uint32_t* by = bx + H * H * W;        // [H z][kDilT y][W], y-dilated
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-
-  // Stage the halo rows' centre bytes in shared memory with independent
-  // 4-byte loads (the whole block's loads are in flight together), then pack
-  // them into bitmasks with ballots.
-  uint8_t* raw = reinterpret_cast<uint8_t*>(by + H * kDilT * W);  // [H*H][dx4]
-  const int dx4 = (p.dx + 3) & ~3;
-  const int words_per_row = dx4 >> 2;
   const bool vec = (p.dx & 3) == 0;
-#pragma unroll 4
-  for (int i = threadIdx.x; i < H * H * words_per_row; i += blockDim.x) {
-    const int row = i / words_per_row, wd = i - row * words_per_row;
-    const int hy = row % H, hz = row / H;
+  const uint32_t ee = e * 0x01010101u;  // the epoch byte in every lane of a word
+
+  // Pack: lane l reads cells 4l..4l+3 of each 128-cell segment of the row;
+  // word j of the segment is the OR of lanes 8j..8j+7's nibbles.
+  for (int row = warp; row < H * H; row += nw) {
+    const int hz = row / H, hy = row - hz * H;
     const int y = y0 - r + hy, z = z0 - r + hz;
-    uint32_t v = 0;
-    if (y >= 0 && y < p.dy && z >= 0 && z < p.dz) {
-      const uint8_t* src = ctr + static_cast<uint32_t>(y) * p.dx + static_cast<uint32_t>(z) * dxy + 4 * wd;
-      if (vec) {
-        v = __ldg(reinterpret_cast<const uint32_t*>(src));
-      } else {
-        for (int b = 0; b < 4 && 4 * wd + b < p.dx; ++b) v |= static_cast<uint32_t>(src[b]) << (8 * b);
+    const bool ok = y >= 0 && y < p.dy && z >= 0 && z < p.dz;
+    const uint8_t* src = ctr + (ok ? static_cast<uint32_t>(y) * p.dx + static_cast<uint32_t>(z) * dxy : 0u);
+    for (int seg = 0; seg < W; seg += 4) {
+      const int x = (seg << 5) + 4 * lane;
+      uint32_t nib = 0;
+      if (ok && x < p.dx) {
+        uint32_t v;
+        if (vec) {
+          v = __ldg(reinterpret_cast<const uint32_t*>(src + x));
+        } else {
+          v = 0;
+          for (int b = 0; b < 4 && x + b < p.dx; ++b) v |= static_cast<uint32_t>(src[x + b]) << (8 * b);
+        }
+        const uint32_t eq = __vcmpeq4(v, ee);  // 0xff per matching byte
+        nib = (eq & 1u) | ((eq >> 7) & 2u) | ((eq >> 14) & 4u) | ((eq >> 21) & 8u);
+        if (!vec) nib &= (1u << min(4, p.dx - x)) - 1u;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t m = __reduce_or_sync(0xffffffffu, (lane >> 3) == j ? nib << (4 * (lane & 7)) : 0u);
+        if (lane == j && seg + j < W) in[row * W + seg + j] = m;
       }
     }
-    reinterpret_cast<uint32_t*>(raw)[i] = v;
   }
   __syncthreads();
-  for (int row = warp; row < H * H; row += nw) {
-    for (int w = 0; w < W; ++w) {
-      const int x = (w << 5) + lane;
-      const bool c = x < p.dx && raw[row * dx4 + x] == e;
-      const uint32_t m = __ballot_sync(0xffffffffu, c);
-      if (lane == 0) in[row * W + w] = m;
-    }
-  }
-  __syncthreads();
+  // x: bit x of the dilated row = OR of bits x-r .. x+r (r <= 31)
   for (int i = threadIdx.x; i < H * H * W; i += blockDim.x) {
     const int w = i % W;
     const uint32_t m = in[i];
     const uint32_t prev = w > 0 ? in[i - 1] : 0u;
     const uint32_t next = w + 1 < W ? in[i + 1] : 0u;
     uint32_t d = m;
-    for (int k = 1; k <= r; ++k) {
-      d |= (m << k) | (prev >> (32 - k)) | (m >> k) | (next << (32 - k));
-    }
+    for (int k = 1; k <= r; ++k) d |= (m << k) | (prev >> (32 - k)) | (m >> k) | (next << (32 - k));
     bx[i] = d;
   }
   __syncthreads();
+  // y
   for (int i = threadIdx.x; i < H * kDilT * W; i += blockDim.x) {
-    const int w = i % W, y = (i / W) % kDilT, hz = i / (W * kDilT);
+    const int w = i % W, yz = i / W;
+    const int y = yz % kDilT, hz = yz / kDilT;
     uint32_t d = 0;
-    for (int k = 0; k <= 2 * r; ++k) d |= bx[(hz * H + y + k) * W + w];
+    const uint32_t* col = bx + (hz * H + y) * W + w;
+    for (int k = 0; k <= 2 * r; ++k) d |= col[k * W];
     by[i] = d;
   }
   __syncthreads();
+  // z, then one byte store per set bit (a warp covers 32 consecutive cells)
   for (int row = warp; row < kDilT * kDilT; row += nw) {
-    const int y = row % kDilT, z = row / kDilT;
+    const int z = row / kDilT, y = row - z * kDilT;
     const int gy = y0 + y, gz = z0 + z;
     if (gy >= p.dy || gz >= p.dz) continue;
+    uint8_t* dst = occ + static_cast<uint32_t>(gy) * p.dx + static_cast<uint32_t>(gz) * dxy;
     for (int w = 0; w < W; ++w) {
       uint32_t d = 0;
-      for (int k = 0; k <= 2 * r; ++k) d |= by[((z + k) * kDilT + y) * W + w];
+      const uint32_t* col = by + (z * kDilT + y) * W + w;
+      for (int k = 0; k <= 2 * r; ++k) d |= col[k * kDilT * W];
       const int x = (w << 5) + lane;
-      if (x < p.dx && ((d >> lane) & 1u)) {
-        occ[static_cast<uint32_t>(x) + static_cast<uint32_t>(gy) * p.dx + static_cast<uint32_t>(gz) * dxy] =
-            static_cast<uint8_t>(e);
-      }
+      if (x < p.dx && ((d >> lane) & 1u)) dst[x] = static_cast<uint8_t>(e);
     }
   }
 }
@@ -422,6 +435,31 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p) {
     const uint32_t drow = static_cast<uint32_t>(y) * p.dx + static_cast<uint32_t>(z) * dxy;
     const long long srow = static_cast<long long>(sy) * p.dx + static_cast<long long>(sz) * dxy;
     const bool vec = (p.dx & 3) == 0;
+    if (vec && (ox & 3) == 0) {
+      // 4-aligned source and destination: 4-byte loads of loc/occ and one
+      // 16-byte load of the 4 keys; the 4 cells are all in or all out of
+      // the grid along x because dx and ox are multiples of 4.
+      for (int x0 = lane * 4; x0 < p.dx; x0 += 128) {
+        const int sx = x0 + ox;
+        uint32_t out = 0;
+        if (row_ok && sx >= 0 && sx < p.dx) {
+          const long long sc = srow + sx;
+          const uint32_t l4 = *reinterpret_cast<const uint32_t*>(src + sc);
+          const uint32_t o4 = *reinterpret_cast<const uint32_t*>(occ + sc);
+          const uint4 k4 = *reinterpret_cast<const uint4*>(key + sc);
+          const uint32_t kk[4] = {k4.x, k4.y, k4.z, k4.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint32_t v = merge_cell((l4 >> (8 * i)) & 0xffu,
+                                          decode_cell((o4 >> (8 * i)) & 0xffu, kk[i], epoch));
+            occ_n += v == 2u;
+            free_n += v == 1u;
+            out |= v << (8 * i);
+          }
+        }
+        *reinterpret_cast<uint32_t*>(dst + drow + x0) = out;
+      }
+    } else
     for (int x0 = lane * 4; x0 < p.dx; x0 += 128) {
       uint32_t out = 0;
 #pragma unroll

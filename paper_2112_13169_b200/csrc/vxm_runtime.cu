@@ -275,7 +275,7 @@ void launch_frame(vxm_ctx* c, bool cloud, bool timed) {
   VXM_CK(cudaMemsetAsync(c->counters, 0, sizeof(vxm::Counters) * S, c->stream));
   if (!cloud) {
     const long long npix = static_cast<long long>(kp.W) * kp.H;
-    dim3 grid(static_cast<unsigned>((npix + kPopulateThreads - 1) / kPopulateThreads), S);
+    dim3 grid(static_cast<unsigned>(((npix + 3) / 4 + kPopulateThreads - 1) / kPopulateThreads), S);
     vxm::populate_depth_kernel<<<grid, kPopulateThreads, 0, c->stream>>>(kp);
   } else {
     dim3 grid(static_cast<unsigned>(c->nsm * 4), S);

@@ -2,7 +2,8 @@
 import csv, subprocess, sys
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
-det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
+kf = ["-k", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
+det = subprocess.run(["ncu", "-i", rep, *kf, "--page", "details", "--csv"], capture_output=True, text=True).stdout
 keep = ("Duration", "Elapsed Cycles", "SM Active Cycles", "DRAM Throughput", "L2 Cache Throughput", "L1/TEX Hit Rate",
         "L2 Hit Rate", "Achieved Occupancy", "Registers Per Thread", "Warp Cycles Per Issued Instruction",
         "Executed Instructions", "Issued Warp Per Scheduler", "Memory Throughput", "Theoretical Occupancy",
@@ -10,7 +11,7 @@ keep = ("Duration", "Elapsed Cycles", "SM Active Cycles", "DRAM Throughput", "L2
 for r in csv.reader(det.splitlines()):
     if len(r) > 4 and r[-4] in keep:
         print(f"  {r[-4]:40s} {r[-2]:>14s} {r[-3]}")
-src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True, text=True).stdout
+src = subprocess.run(["ncu", "-i", rep, *kf, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True, text=True).stdout
 rows = list(csv.reader(src.splitlines()))
 hdr = rows[1]; data = rows[2:]
 i_s = hdr.index("Warp Stall Sampling (All Samples)"); i_e = hdr.index("Instructions Executed")
