@@ -87,8 +87,9 @@ typedef struct vxm_pose {
 
 /* PipelineStats + TraceStats + PopulateStats (pipeline.hpp:30-41,
  * raytracer.hpp:44-57, integrator.hpp:18-21). The *_us fields are device
- * times of the stages measured with CUDA events only when the context was
- * created with VXM_FLAG_STAGE_TIMING, else 0. */
+ * times of the stages from CUDA events recorded inside the frame
+ * (populate_us includes the dilation; shift_us is 0 because the shift is
+ * fused into the merge kernel). */
 typedef struct vxm_stats {
   uint64_t points_total;
   uint64_t points_outside;
@@ -132,7 +133,7 @@ int vxm_device_count(void);
 
 typedef struct vxm_ctx vxm_ctx;
 
-#define VXM_FLAG_STAGE_TIMING 1u  /* record per-stage CUDA events (adds syncs) */
+#define VXM_FLAG_STAGE_TIMING 1u  /* launch stages directly (no graph), events between them */
 #define VXM_FLAG_NO_GRAPH 2u      /* launch kernels directly instead of a CUDA graph */
 
 /* cfg->grid must already be placed (use vxm_grid_spec_create_centered to
@@ -173,6 +174,13 @@ int vxm_upload_local(vxm_ctx* ctx, int32_t s, const uint8_t* cells, const double
  * integrate call's kernels in milliseconds (CUDA events on that stream). */
 void* vxm_cuda_stream(vxm_ctx* ctx);
 int vxm_last_frame_ms(vxm_ctx* ctx, float* ms);
+
+/* Redirects the four stage-boundary events recorded inside every following
+ * frame (cudaEvent_t: before populate, before trace, after trace, after
+ * merge) to the caller's events, so per-kernel device times can be read for
+ * many queued frames without synchronizing; NULL restores the context's own
+ * (whose stage times fill vxm_stats::*_us). */
+int vxm_set_stage_events(vxm_ctx* ctx, void* const events[4]);
 
 /* ------------------------------------------------------------------------ */
 /* Stage entry points on HOST grids (the free functions of the public API).

@@ -82,6 +82,7 @@ SIGNATURES = {
     "vxm_upload_local": (C.c_int, [C.c_void_p, C.c_int32, _u8p, _f64p]),
     "vxm_cuda_stream": (C.c_void_p, [C.c_void_p]),
     "vxm_last_frame_ms": (C.c_int, [C.c_void_p, P(C.c_float)]),
+    "vxm_set_stage_events": (C.c_int, [C.c_void_p, P(C.c_void_p)]),
     "vxm_populate_occupied": (C.c_int, [P(GridSpecC), _u8p, _f64p, _f64p, _f64p, C.c_size_t, P(PoseC), C.c_int32, P(PopulateStatsC)]),
     "vxm_trace_bundle": (C.c_int, [P(GridSpecC), _u8p, _i32p, P(PoseC), P(TraceStatsC)]),
     "vxm_trace_per_pixel": (C.c_int, [P(GridSpecC), _u8p, _f64p, _f64p, _f64p, C.c_size_t, P(PoseC), P(TraceStatsC)]),

@@ -146,33 +146,46 @@ __global__ void __launch_bounds__(256) dilate_kernel(KParams p, int r) {
   const bool vec = (p.dx & 3) == 0;
   const uint32_t ee = e * 0x01010101u;  // the epoch byte in every lane of a word
 
-  // Pack: lane l reads cells 4l..4l+3 of each 128-cell segment of the row;
-  // word j of the segment is the OR of lanes 8j..8j+7's nibbles.
-  for (int row = warp; row < H * H; row += nw) {
-    const int hz = row / H, hy = row - hz * H;
-    const int y = y0 - r + hy, z = z0 - r + hz;
-    const bool ok = y >= 0 && y < p.dy && z >= 0 && z < p.dz;
-    const uint8_t* src = ctr + (ok ? static_cast<uint32_t>(y) * p.dx + static_cast<uint32_t>(z) * dxy : 0u);
-    for (int seg = 0; seg < W; seg += 4) {
-      const int x = (seg << 5) + 4 * lane;
-      uint32_t nib = 0;
-      if (ok && x < p.dx) {
-        uint32_t v;
-        if (vec) {
-          v = __ldg(reinterpret_cast<const uint32_t*>(src + x));
-        } else {
-          v = 0;
-          for (int b = 0; b < 4 && x + b < p.dx; ++b) v |= static_cast<uint32_t>(src[x + b]) << (8 * b);
-        }
-        const uint32_t eq = __vcmpeq4(v, ee);  // 0xff per matching byte
-        nib = (eq & 1u) | ((eq >> 7) & 2u) | ((eq >> 14) & 4u) | ((eq >> 21) & 8u);
-        if (!vec) nib &= (1u << min(4, p.dx - x)) - 1u;
-      }
+  // Pack: lane l reads cells 4l..4l+3 of each 128-cell segment of a row;
+  // word j of the segment is the OR of lanes 8j..8j+7's nibbles. A warp
+  // issues the loads of kBatch rows before packing any of them, so their
+  // latencies overlap.
+  constexpr int kBatch = 6;
+  const int segs = (W + 3) >> 2;
+  for (int task0 = warp * kBatch; task0 < H * H * segs; task0 += nw * kBatch) {
+    uint32_t v[kBatch];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t m = __reduce_or_sync(0xffffffffu, (lane >> 3) == j ? nib << (4 * (lane & 7)) : 0u);
-        if (lane == j && seg + j < W) in[row * W + seg + j] = m;
+    for (int b = 0; b < kBatch; ++b) {
+      const int task = task0 + b;
+      const int row = task / segs, seg = task - row * segs;
+      const int hz = row / H, hy = row - hz * H;
+      const int y = y0 - r + hy, z = z0 - r + hz;
+      const int x = (seg << 7) + 4 * lane;
+      v[b] = 0;
+      if (task < H * H * segs && y >= 0 && y < p.dy && z >= 0 && z < p.dz && x < p.dx) {
+        const uint8_t* src = ctr + static_cast<uint32_t>(y) * p.dx + static_cast<uint32_t>(z) * dxy + x;
+        if (vec) {
+          v[b] = __ldg(reinterpret_cast<const uint32_t*>(src));
+        } else {
+          // bytes past the row end stay 0, which never equals an epoch (>= 1)
+          for (int k = 0; k < 4 && x + k < p.dx; ++k) v[b] |= static_cast<uint32_t>(src[k]) << (8 * k);
+        }
       }
+    }
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b) {
+      const int task = task0 + b;
+      if (task >= H * H * segs) break;  // warp-uniform
+      const int row = task / segs, seg = task - row * segs;
+      const uint32_t eq = __vcmpeq4(v[b], ee);  // 0xff per matching byte
+      const uint32_t nib = (eq & 1u) | ((eq >> 7) & 2u) | ((eq >> 14) & 4u) | ((eq >> 21) & 8u);
+      // gather the 4 words of this segment: word j = nibbles of lanes 8j..8j+7
+      uint32_t m = nib << (4 * (lane & 7));
+      m |= __shfl_xor_sync(0xffffffffu, m, 1);
+      m |= __shfl_xor_sync(0xffffffffu, m, 2);
+      m |= __shfl_xor_sync(0xffffffffu, m, 4);
+      const int w = (seg << 2) + (lane >> 3);
+      if ((lane & 7) == 0 && w < W) in[row * W + w] = m;
     }
   }
   __syncthreads();
@@ -230,7 +243,7 @@ __global__ void __launch_bounds__(256) dilate_kernel(KParams p, int r) {
 // the camera. Counters go to 32 per-stream slots (one RED per warp each),
 // summed by K4.
 // ---------------------------------------------------------------------------
-constexpr int kChunk = 8;
+constexpr int kChunk = 8;  // default chunk (variants below for tuning)
 constexpr int kTraceSlots = 32;
 
 struct RayState {
@@ -281,6 +294,7 @@ __device__ __forceinline__ void ray_setup(const double* R, const double* start, 
   }
 }
 
+template <int kChunk, bool kDedup>
 __global__ void __launch_bounds__(32) trace_bundle_kernel(KParams p) {
   const int s = blockIdx.y;
   const FrameParams* fp = p.frames + s;
@@ -362,10 +376,13 @@ __global__ void __launch_bounds__(32) trace_bundle_kernel(KParams p) {
       freed += (write && !traced_bit) ? 1u : 0u;
       const uint32_t kval = ray_key | traced_bit;
       traced_bit |= is_occ ? 1u : 0u;
-      const uint32_t id = write ? cell[j] : (0xfffffff0u - lane);  // idle lanes never match
-      const uint32_t right = __shfl_down_sync(0xffffffffu, id, 1);
-      const uint32_t below = __shfl_down_sync(0xffffffffu, id, 8);
-      const bool dominated = (lane < 31 && right == id) || (lane < 24 && below == id);
+      bool dominated = false;
+      if constexpr (kDedup) {
+        const uint32_t id = write ? cell[j] : (0xfffffff0u - lane);  // idle lanes never match
+        const uint32_t right = __shfl_down_sync(0xffffffffu, id, 1);
+        const uint32_t below = __shfl_down_sync(0xffffffffu, id, 8);
+        dominated = (lane < 31 && right == id) || (lane < 24 && below == id);
+      }
       if (write && !dominated) atomicMax(key + cell[j], kval);
     }
   }

@@ -247,8 +247,13 @@ struct vxm_ctx {
   double* cloud_dev = nullptr;
   size_t cloud_cap = 0;
 
-  // pinned host mirrors
-  vxm::FrameParams* frames_host = nullptr;
+  // pinned host mirrors; FrameParams go through a ring so that a frame can be
+  // prepared while earlier ones are still queued
+  static constexpr int kRing = 4;
+  vxm::FrameParams* frames_ring = nullptr;  // kRing * S
+  cudaEvent_t ring_ev[kRing] = {};
+  int ring_slot = 0;
+  vxm::FrameParams* frames_host = nullptr;  // current ring slot
   vxm::Counters* counters_host = nullptr;
 
   // host state per stream
@@ -260,18 +265,31 @@ struct vxm_ctx {
 
   cudaGraphExec_t graph_depth = nullptr;
   cudaGraphExec_t graph_cloud = nullptr;
+  cudaGraph_t graph_tmpl[2] = {nullptr, nullptr};          // kept for node updates
+  cudaGraphNode_t stage_nodes[2][4] = {};                  // event-record nodes per graph
+  void* user_stage_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // ev[0] / ev[5] bracket the frame outside the graph; ev[1..4] are the
+  // stage boundaries recorded inside it (before populate, before trace,
+  // after trace, after merge)
   cudaEvent_t ev[6] = {};
   bool pending = false;
+  int trace_variant = 0;  // VXM_TRACE_VARIANT (tuning experiments only)
   float last_ms = 0.f;
   double stage_us[4] = {0, 0, 0, 0};
 };
 
 namespace {
 
-void launch_frame(vxm_ctx* c, bool cloud, bool timed) {
+// capturing: inside stream capture the stage events must be recorded as
+// external event-record nodes (a plain record only adds a dependency edge).
+void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
   const int S = c->S;
   vxm::KParams kp = c->kp;
-  if (timed) VXM_CK(cudaEventRecord(c->ev[1], c->stream));
+  auto mark = [&](cudaEvent_t e) {
+    VXM_CK(capturing ? cudaEventRecordWithFlags(e, c->stream, cudaEventRecordExternal)
+                     : cudaEventRecord(e, c->stream));
+  };
+  mark(c->ev[1]);
   VXM_CK(cudaMemsetAsync(c->counters, 0, sizeof(vxm::Counters) * S, c->stream));
   if (!cloud) {
     const long long npix = static_cast<long long>(kp.W) * kp.H;
@@ -290,13 +308,19 @@ void launch_frame(vxm_ctx* c, bool cloud, bool timed) {
     vxm::dilate_kernel<<<grid, 256, smem, c->stream>>>(kp, r);
     VXM_CK(cudaGetLastError());
   }
-  if (timed) VXM_CK(cudaEventRecord(c->ev[2], c->stream));
+  mark(c->ev[2]);
   {
     dim3 grid(static_cast<unsigned>(kp.tiles_x * kp.tiles_y), S);
-    vxm::trace_bundle_kernel<<<grid, 32, 0, c->stream>>>(kp);
+    switch (c->trace_variant) {
+      case 1: vxm::trace_bundle_kernel<8, false><<<grid, 32, 0, c->stream>>>(kp); break;
+      case 2: vxm::trace_bundle_kernel<4, true><<<grid, 32, 0, c->stream>>>(kp); break;
+      case 3: vxm::trace_bundle_kernel<16, true><<<grid, 32, 0, c->stream>>>(kp); break;
+      case 4: vxm::trace_bundle_kernel<4, false><<<grid, 32, 0, c->stream>>>(kp); break;
+      default: vxm::trace_bundle_kernel<8, true><<<grid, 32, 0, c->stream>>>(kp); break;
+    }
     VXM_CK(cudaGetLastError());
   }
-  if (timed) VXM_CK(cudaEventRecord(c->ev[3], c->stream));
+  mark(c->ev[3]);
   {
     const long long rows = static_cast<long long>(kp.dy) * kp.dz;
     const int rows_per_block = kMergeThreads / 32;
@@ -304,7 +328,7 @@ void launch_frame(vxm_ctx* c, bool cloud, bool timed) {
     vxm::merge_shift_count_kernel<<<grid, kMergeThreads, 0, c->stream>>>(kp);
     VXM_CK(cudaGetLastError());
   }
-  if (timed) VXM_CK(cudaEventRecord(c->ev[4], c->stream));
+  mark(c->ev[4]);
   VXM_CK(cudaMemcpyAsync(c->counters_host, c->counters, sizeof(vxm::Counters) * S,
                          cudaMemcpyDeviceToHost, c->stream));
 }
@@ -313,21 +337,53 @@ cudaGraphExec_t capture(vxm_ctx* c, bool cloud) {
   cudaGraph_t g = nullptr;
   VXM_CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   try {
-    launch_frame(c, cloud, false);
+    launch_frame(c, cloud, true);
   } catch (...) {
     cudaStreamEndCapture(c->stream, &g);
     if (g) cudaGraphDestroy(g);
     throw;
   }
   VXM_CK(cudaStreamEndCapture(c->stream, &g));
+  const int gi = cloud ? 1 : 0;
+  c->graph_tmpl[gi] = g;
+  // locate the stage event-record nodes so callers can redirect them
+  size_t nn = 0;
+  VXM_CK(cudaGraphGetNodes(g, nullptr, &nn));
+  std::vector<cudaGraphNode_t> nodes(nn);
+  VXM_CK(cudaGraphGetNodes(g, nodes.data(), &nn));
+  for (cudaGraphNode_t node : nodes) {
+    cudaGraphNodeType type;
+    VXM_CK(cudaGraphNodeGetType(node, &type));
+    if (type != cudaGraphNodeTypeEventRecord) continue;
+    cudaEvent_t e = nullptr;
+    VXM_CK(cudaGraphEventRecordNodeGetEvent(node, &e));
+    for (int i = 0; i < 4; ++i)
+      if (e == c->ev[1 + i]) c->stage_nodes[gi][i] = node;
+  }
   cudaGraphExec_t exec = nullptr;
-  const cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
-  cudaGraphDestroy(g);
-  VXM_CK(e);
+  VXM_CK(cudaGraphInstantiate(&exec, g, 0));
   return exec;
 }
 
+// Points the graph's stage event-record nodes at the caller's events (or
+// back at the context's own).
+void apply_stage_events(vxm_ctx* c, cudaGraphExec_t exec, int gi) {
+  for (int i = 0; i < 4; ++i) {
+    if (!c->stage_nodes[gi][i]) continue;
+    cudaEvent_t e = c->user_stage_ev[i] ? static_cast<cudaEvent_t>(c->user_stage_ev[i]) : c->ev[1 + i];
+    VXM_CK(cudaGraphExecEventRecordNodeSetEvent(exec, c->stage_nodes[gi][i], e));
+  }
+}
+
 // Host half of one frame for every stream: validation, T_vc, shift, epoch.
+// Claims the next FrameParams ring slot (waiting until the copy that last
+// used it has executed).
+void next_slot(vxm_ctx* c) {
+  c->ring_slot = (c->ring_slot + 1) % vxm_ctx::kRing;
+  VXM_CK(cudaEventSynchronize(c->ring_ev[c->ring_slot]));
+  c->frames_host = c->frames_ring + static_cast<size_t>(c->ring_slot) * c->S;
+}
+
 void prepare_frames(vxm_ctx* c, const vxm_pose* poses, const float* depth_dev_base,
                     size_t frame_elems) {
   for (int s = 0; s < c->S; ++s) {
@@ -360,16 +416,18 @@ void prepare_frames(vxm_ctx* c, const vxm_pose* poses, const float* depth_dev_ba
   }
   VXM_CK(cudaMemcpyAsync(c->frames_dev, c->frames_host, sizeof(vxm::FrameParams) * c->S,
                          cudaMemcpyHostToDevice, c->stream));
+  VXM_CK(cudaEventRecord(c->ring_ev[c->ring_slot], c->stream));
 }
 
 void run_frame(vxm_ctx* c, bool cloud) {
   const bool timed = (c->flags & VXM_FLAG_STAGE_TIMING) != 0;
   VXM_CK(cudaEventRecord(c->ev[0], c->stream));
   if (timed || (c->flags & VXM_FLAG_NO_GRAPH)) {
-    launch_frame(c, cloud, timed);
+    launch_frame(c, cloud, false);
   } else {
     cudaGraphExec_t& g = cloud ? c->graph_cloud : c->graph_depth;
     if (!g) g = capture(c, cloud);
+    apply_stage_events(c, g, cloud ? 1 : 0);
     VXM_CK(cudaGraphLaunch(g, c->stream));
   }
   VXM_CK(cudaEventRecord(c->ev[5], c->stream));
@@ -381,8 +439,10 @@ void collect_stats(vxm_ctx* c, vxm_stats* out) {
   VXM_CK(cudaStreamSynchronize(c->stream));
   if (c->pending) {
     VXM_CK(cudaEventElapsedTime(&c->last_ms, c->ev[0], c->ev[5]));
-    if (c->flags & VXM_FLAG_STAGE_TIMING) {
-      float t[4] = {0, 0, 0, 0};
+    const bool own = !c->user_stage_ev[0] && !c->user_stage_ev[1] && !c->user_stage_ev[2] &&
+                     !c->user_stage_ev[3];
+    if (own) {
+      float t[3] = {0, 0, 0};
       VXM_CK(cudaEventElapsedTime(&t[0], c->ev[1], c->ev[2]));
       VXM_CK(cudaEventElapsedTime(&t[1], c->ev[2], c->ev[3]));
       VXM_CK(cudaEventElapsedTime(&t[2], c->ev[3], c->ev[4]));
@@ -430,7 +490,11 @@ void destroy_ctx(vxm_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->graph_depth) cudaGraphExecDestroy(c->graph_depth);
   if (c->graph_cloud) cudaGraphExecDestroy(c->graph_cloud);
+  for (auto& g : c->graph_tmpl)
+    if (g) cudaGraphDestroy(g);
   for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : c->ring_ev)
     if (e) cudaEventDestroy(e);
   cudaFree(c->occ);
   cudaFree(c->ctr);
@@ -442,7 +506,7 @@ void destroy_ctx(vxm_ctx* c) {
   cudaFree(c->frames_dev);
   cudaFree(c->depth_dev);
   cudaFree(c->cloud_dev);
-  cudaFreeHost(c->frames_host);
+  cudaFreeHost(c->frames_ring);
   cudaFreeHost(c->counters_host);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -522,6 +586,7 @@ int vxm_create(const vxm_config* cfg, int32_t n_streams, int32_t device, uint32_
     c->S = n_streams;
     c->flags = flags;
     c->nsm = sm_count(device);
+    if (const char* tv = std::getenv("VXM_TRACE_VARIANT")) c->trace_variant = std::atoi(tv);
     const vxm_grid_spec& g = cfg->grid;
     c->n = static_cast<long long>(g.dims[0]) * g.dims[1] * g.dims[2];
     bundle_dims(cfg->camera, cfg->depth, g.vox_size, c->bundle);
@@ -548,9 +613,11 @@ int vxm_create(const vxm_config* cfg, int32_t n_streams, int32_t device, uint32_
     VXM_CK(cudaMalloc(&c->counters, sizeof(vxm::Counters) * S));
     VXM_CK(cudaMalloc(&c->frames_dev, sizeof(vxm::FrameParams) * S));
     VXM_CK(cudaMalloc(&c->depth_dev, sizeof(float) * npix * S));
-    VXM_CK(cudaMallocHost(&c->frames_host, sizeof(vxm::FrameParams) * S));
+    VXM_CK(cudaMallocHost(&c->frames_ring, sizeof(vxm::FrameParams) * S * vxm_ctx::kRing));
+    std::memset(c->frames_ring, 0, sizeof(vxm::FrameParams) * S * vxm_ctx::kRing);
+    for (auto& e : c->ring_ev) VXM_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->frames_host = c->frames_ring;
     VXM_CK(cudaMallocHost(&c->counters_host, sizeof(vxm::Counters) * S));
-    std::memset(c->frames_host, 0, sizeof(vxm::FrameParams) * S);
     std::memset(c->counters_host, 0, sizeof(vxm::Counters) * S);
     c->epoch.assign(S, 0);
     c->cur.assign(S, 0);
@@ -639,6 +706,7 @@ int vxm_integrate_depth(vxm_ctx* ctx, const float* depth, const vxm_pose* t_wc, 
     if (!ctx || !depth || !t_wc) throw InvalidArg{"null argument"};
     VXM_CK(cudaSetDevice(ctx->device));
     const size_t frame = static_cast<size_t>(ctx->kp.W) * ctx->kp.H;
+    next_slot(ctx);
     prepare_frames(ctx, t_wc, ctx->depth_dev, frame);
     // pinned host buffers go straight to the copy engine; pageable ones are
     // staged by the driver
@@ -654,8 +722,16 @@ int vxm_integrate_depth_device(vxm_ctx* ctx, const float* depth_dev, const vxm_p
     if (!ctx || !depth_dev || !t_wc) throw InvalidArg{"null argument"};
     VXM_CK(cudaSetDevice(ctx->device));
     const size_t frame = static_cast<size_t>(ctx->kp.W) * ctx->kp.H;
+    next_slot(ctx);
     prepare_frames(ctx, t_wc, depth_dev, frame);
     run_frame(ctx, false);
+  });
+}
+
+int vxm_set_stage_events(vxm_ctx* ctx, void* const events[4]) {
+  return guarded([&] {
+    if (!ctx) throw InvalidArg{"null context"};
+    for (int i = 0; i < 4; ++i) ctx->user_stage_ev[i] = events ? events[i] : nullptr;
   });
 }
 
@@ -680,6 +756,7 @@ int vxm_integrate_cloud(vxm_ctx* ctx, const double* xs, const double* ys, const 
       VXM_CK(cudaMalloc(&ctx->cloud_dev, sizeof(double) * 3 * n));
       ctx->cloud_cap = n;
     }
+    next_slot(ctx);
     vxm::FrameParams& f = ctx->frames_host[0];
     f.xs = ctx->cloud_dev;
     f.ys = ctx->cloud_dev + ctx->cloud_cap;

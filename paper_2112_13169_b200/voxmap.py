@@ -226,6 +226,18 @@ class MappingPipeline:
         origin = np.ascontiguousarray(origin, dtype=np.float64)
         N.check(self._lib.vxm_upload_local(self._ctx, s, _u8(cells), _f64(origin)))
 
+    def set_origin(self, origin, s=0):
+        """Places stream s's (empty) local grid, e.g. centred on that stream's
+        first camera position (pipeline.hpp:63)."""
+        origin = np.ascontiguousarray(origin, dtype=np.float64)
+        N.check(self._lib.vxm_upload_local(self._ctx, s, None, _f64(origin)))
+
+    def set_stage_events(self, events):
+        """events: 4 cudaEvent_t handles (ints) recorded at the stage
+        boundaries of following frames, or None to restore the context's."""
+        arr = (C.c_void_p * 4)(*(events or [None] * 4))
+        N.check(self._lib.vxm_set_stage_events(self._ctx, arr if events else None))
+
     def last_frame_ms(self):
         v = C.c_float()
         N.check(self._lib.vxm_last_frame_ms(self._ctx, C.byref(v)))
