@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(256) dilate_kernel(KParams p, int r) {
 // the camera. Counters go to 32 per-stream slots (one RED per warp each),
 // summed by K4.
 // ---------------------------------------------------------------------------
-constexpr int kChunk = 8;  // default chunk (variants below for tuning)
+constexpr int kChunk = 8;  // 4 and 16 measured equal; without kDedup 2-3x slower
 constexpr int kTraceSlots = 32;
 
 struct RayState {
@@ -294,7 +294,7 @@ __device__ __forceinline__ void ray_setup(const double* R, const double* start, 
   }
 }
 
-template <int kChunk, bool kDedup>
+template <bool kDedup>
 __global__ void __launch_bounds__(32) trace_bundle_kernel(KParams p) {
   const int s = blockIdx.y;
   const FrameParams* fp = p.frames + s;
@@ -415,6 +415,120 @@ __device__ __forceinline__ void fold_trace_slots(Counters& c) {
     c.voxels_traced = v[2];
     c.voxels_skipped = v[3];
   }
+}
+
+// ---------------------------------------------------------------------------
+// K3b: the per-pixel comparison tracer (TracerMode::PerPixelBaseline, paper
+// §V-D): bresenham_trace_image (proj/src/raytracer.cpp:120-161) with
+// bresenham_line (proj/include/voxmap/raytracer.hpp:136-194). One thread per
+// cloud point (or per depth pixel, back-projected again exactly as K1 does).
+// Every write stores Free and occupancy is frozen during the trace, so the
+// Sequential result is order independent: plain stores, no atomics. Free is
+// written as a key with ray index 0 (decodes to Free).
+// ---------------------------------------------------------------------------
+struct PerPixelAcc {
+  unsigned rays, freed, skipped;
+};
+
+__device__ __forceinline__ void pp_visit(const KParams& p, const int* c, const int* end,
+                                         const uint8_t* occ, uint32_t* key, uint32_t epoch,
+                                         PerPixelAcc& acc) {
+  if (c[0] == end[0] && c[1] == end[1] && c[2] == end[2]) return;  // the endpoint holds the obstacle
+  if (static_cast<unsigned>(c[0]) >= static_cast<unsigned>(p.dx) ||
+      static_cast<unsigned>(c[1]) >= static_cast<unsigned>(p.dy) ||
+      static_cast<unsigned>(c[2]) >= static_cast<unsigned>(p.dz)) {
+    ++acc.skipped;
+    return;
+  }
+  const uint32_t idx = static_cast<uint32_t>(c[0]) + static_cast<uint32_t>(c[1]) * p.dx +
+                       static_cast<uint32_t>(c[2]) * static_cast<uint32_t>(p.dx * p.dy);
+  if (occ[idx] != epoch) {
+    key[idx] = key_tag(epoch) | 2u;
+    ++acc.freed;
+  }
+}
+
+__device__ __forceinline__ void pp_trace_point(const KParams& p, const double* R, const double* t,
+                                               const int* cam, double x, double y, double z,
+                                               const uint8_t* occ, uint32_t* key, uint32_t epoch,
+                                               PerPixelAcc& acc) {
+  // world_to_voxel(t_vc.apply(point)) (grid.cpp:54-62, geometry.cpp:10-15):
+  // ((R p) + t) / vs, rows left to right, floor, int
+  int end[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double w = dadd(dadd(dadd(dmul(R[3 * a], x), dmul(R[3 * a + 1], y)), dmul(R[3 * a + 2], z)), t[a]);
+    end[a] = static_cast<int>(floor(ddiv(w, p.vs)));
+  }
+  ++acc.rays;
+  int q[3] = {cam[0], cam[1], cam[2]};
+  int d[3], sg[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    d[a] = abs(end[a] - q[a]);
+    sg[a] = end[a] > q[a] ? 1 : -1;
+  }
+  int drive, o1, o2;
+  if (d[0] >= d[1] && d[0] >= d[2]) {
+    drive = 0; o1 = 1; o2 = 2;
+  } else if (d[1] >= d[0] && d[1] >= d[2]) {
+    drive = 1; o1 = 0; o2 = 2;
+  } else {
+    drive = 2; o1 = 1; o2 = 0;
+  }
+  int p1 = 2 * d[o1] - d[drive], p2 = 2 * d[o2] - d[drive];
+  while (q[drive] != end[drive]) {
+    pp_visit(p, q, end, occ, key, epoch, acc);
+    if (p1 >= 0) { q[o1] += sg[o1]; p1 -= 2 * d[drive]; }
+    if (p2 >= 0) { q[o2] += sg[o2]; p2 -= 2 * d[drive]; }
+    p1 += 2 * d[o1];
+    p2 += 2 * d[o2];
+    q[drive] += sg[drive];
+  }
+  // the final visit(to) of bresenham_line is the endpoint: skipped by pp_visit
+}
+
+// from_depth: pixels of fp->depth (back-projected as K1), else fp->xs/ys/zs.
+__global__ void __launch_bounds__(256) trace_per_pixel_kernel(KParams p, int from_depth) {
+  const int s = blockIdx.y;
+  const FrameParams* fp = p.frames + s;
+  const uint32_t epoch = fp->epoch;
+  uint32_t* key = p.key + static_cast<long long>(s) * p.n;
+  const uint8_t* occ = p.occ + static_cast<long long>(s) * p.n;
+  double R[9], t[3];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) R[i] = fp->rot[i];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) t[i] = fp->trans[i];
+  int cam[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) cam[a] = static_cast<int>(floor(ddiv(t[a], p.vs)));
+  PerPixelAcc acc{0, 0, 0};
+  const long long n = from_depth ? static_cast<long long>(p.W) * p.H : fp->n_points;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    double x, y, z;
+    if (from_depth) {
+      const float d = fp->depth[i];
+      if (!(isfinite(d) && d > 0.0f)) continue;
+      z = static_cast<double>(d);
+      if (z > p.max_depth) continue;
+      const int v = static_cast<int>(i / p.W), u = static_cast<int>(i - static_cast<long long>(v) * p.W);
+      x = dmul(__ldg(p.qx + u), z);
+      y = dmul(__ldg(p.qy + v), z);
+    } else {
+      x = fp->xs[i];
+      y = fp->ys[i];
+      z = fp->zs[i];
+      if (!(isfinite(x) && isfinite(y) && isfinite(z))) continue;
+    }
+    pp_trace_point(p, R, t, cam, x, y, z, occ, key, epoch, acc);
+  }
+  unsigned vals[3] = {acc.rays, acc.freed, acc.skipped};
+  unsigned long long* dst[3] = {&p.counters[s].trace_slots[blockIdx.x % 32][0],
+                                &p.counters[s].trace_slots[blockIdx.x % 32][1],
+                                &p.counters[s].trace_slots[blockIdx.x % 32][3]};
+  block_accumulate<3>(vals, dst);
 }
 
 // ---------------------------------------------------------------------------

@@ -273,7 +273,6 @@ struct vxm_ctx {
   // after trace, after merge)
   cudaEvent_t ev[6] = {};
   bool pending = false;
-  int trace_variant = 0;  // VXM_TRACE_VARIANT (tuning experiments only)
   float last_ms = 0.f;
   double stage_us[4] = {0, 0, 0, 0};
 };
@@ -310,13 +309,14 @@ void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
   }
   mark(c->ev[2]);
   {
-    dim3 grid(static_cast<unsigned>(kp.tiles_x * kp.tiles_y), S);
-    switch (c->trace_variant) {
-      case 1: vxm::trace_bundle_kernel<8, false><<<grid, 32, 0, c->stream>>>(kp); break;
-      case 2: vxm::trace_bundle_kernel<4, true><<<grid, 32, 0, c->stream>>>(kp); break;
-      case 3: vxm::trace_bundle_kernel<16, true><<<grid, 32, 0, c->stream>>>(kp); break;
-      case 4: vxm::trace_bundle_kernel<4, false><<<grid, 32, 0, c->stream>>>(kp); break;
-      default: vxm::trace_bundle_kernel<8, true><<<grid, 32, 0, c->stream>>>(kp); break;
+    if (c->cfg.tracer_mode == VXM_TRACER_PER_PIXEL) {
+      const long long n = cloud ? static_cast<long long>(c->nsm) * 4 * kPopulateThreads
+                                : static_cast<long long>(kp.W) * kp.H;
+      dim3 grid(static_cast<unsigned>(std::min<long long>((n + 255) / 256, c->nsm * 8)), S);
+      vxm::trace_per_pixel_kernel<<<grid, 256, 0, c->stream>>>(kp, cloud ? 0 : 1);
+    } else {
+      dim3 grid(static_cast<unsigned>(kp.tiles_x * kp.tiles_y), S);
+      vxm::trace_bundle_kernel<true><<<grid, 32, 0, c->stream>>>(kp);
     }
     VXM_CK(cudaGetLastError());
   }
@@ -586,7 +586,6 @@ int vxm_create(const vxm_config* cfg, int32_t n_streams, int32_t device, uint32_
     c->S = n_streams;
     c->flags = flags;
     c->nsm = sm_count(device);
-    if (const char* tv = std::getenv("VXM_TRACE_VARIANT")) c->trace_variant = std::atoi(tv);
     const vxm_grid_spec& g = cfg->grid;
     c->n = static_cast<long long>(g.dims[0]) * g.dims[1] * g.dims[2];
     bundle_dims(cfg->camera, cfg->depth, g.vox_size, c->bundle);

@@ -220,7 +220,7 @@ int vxm_trace_bundle(const vxm_grid_spec* grid, uint8_t* ms, const int32_t bundl
     kp.key = d_key.p;
     kp.counters = d_cnt.p;
     kp.frames = d_frame.p;
-    vxm::trace_bundle_kernel<vxm::kChunk, true><<<dim3(kp.tiles_x * kp.tiles_y, 1), 32>>>(kp);
+    vxm::trace_bundle_kernel<true><<<dim3(kp.tiles_x * kp.tiles_y, 1), 32>>>(kp);
     VXM_SCK(cudaGetLastError());
     vxm::fold_trace_slots_kernel<<<1, 32>>>(d_cnt.p);
     vxm::decode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_occ.p, d_key.p, d_ms.p, N, kEpoch);
@@ -341,10 +341,58 @@ void vxm_kernel_transform_voxelize(const double* xs, const double* ys, const dou
 
 const char* vxm_kernel_isa(void) { return "cuda-sm100a"; }
 
-int vxm_trace_per_pixel(const vxm_grid_spec*, uint8_t*, const double*, const double*,
-                        const double*, size_t, const vxm_pose*, vxm_trace_stats*) {
-  vxm_set_error("vxm_trace_per_pixel: not built yet");
-  return VXM_ESTATE;
+int vxm_trace_per_pixel(const vxm_grid_spec* grid, uint8_t* ms, const double* xs,
+                        const double* ys, const double* zs, size_t n, const vxm_pose* t_vc,
+                        vxm_trace_stats* st) {
+  return stage_guard([&] {
+    check_grid(grid);
+    if (!ms || !t_vc || (n && (!xs || !ys || !zs))) throw StageError{VXM_EINVAL, "null argument"};
+    // world_to_voxel of the camera centre throws on non-finite input (grid.cpp:54-57)
+    for (int a = 0; a < 3; ++a)
+      if (!std::isfinite(t_vc->translation[a]))
+        throw StageError{VXM_EINVAL, "world_to_voxel: non-finite point"};
+    vxm::KParams kp = grid_params(*grid);
+    const long long N = kp.n;
+    DevBuf<uint8_t> d_ms(N), d_occ(N);
+    DevBuf<uint32_t> d_key(N);
+    DevBuf<double> d_pts(3 * n + 1);
+    DevBuf<vxm::Counters> d_cnt(1);
+    DevBuf<vxm::FrameParams> d_frame(1);
+    vxm::FrameParams f{};
+    fill_pose(f, *t_vc);
+    f.xs = d_pts.p;
+    f.ys = d_pts.p + n;
+    f.zs = d_pts.p + 2 * n;
+    f.n_points = static_cast<long long>(n);
+    f.epoch = kEpoch;
+    VXM_SCK(cudaMemcpy(d_frame.p, &f, sizeof(f), cudaMemcpyHostToDevice));
+    if (n) {
+      VXM_SCK(cudaMemcpy(d_pts.p, xs, sizeof(double) * n, cudaMemcpyHostToDevice));
+      VXM_SCK(cudaMemcpy(d_pts.p + n, ys, sizeof(double) * n, cudaMemcpyHostToDevice));
+      VXM_SCK(cudaMemcpy(d_pts.p + 2 * n, zs, sizeof(double) * n, cudaMemcpyHostToDevice));
+    }
+    VXM_SCK(cudaMemcpy(d_ms.p, ms, N, cudaMemcpyHostToDevice));
+    VXM_SCK(cudaMemset(d_cnt.p, 0, sizeof(vxm::Counters)));
+    vxm::encode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_ms.p, d_occ.p, d_key.p, N, kEpoch);
+    kp.occ = d_occ.p;
+    kp.key = d_key.p;
+    kp.counters = d_cnt.p;
+    kp.frames = d_frame.p;
+    vxm::trace_per_pixel_kernel<<<dim3(blocks_for(static_cast<long long>(n), 256), 1), 256>>>(kp, 0);
+    VXM_SCK(cudaGetLastError());
+    vxm::fold_trace_slots_kernel<<<1, 32>>>(d_cnt.p);
+    vxm::decode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_occ.p, d_key.p, d_ms.p, N, kEpoch);
+    VXM_SCK(cudaGetLastError());
+    vxm::Counters cnt{};
+    VXM_SCK(cudaMemcpy(&cnt, d_cnt.p, sizeof(cnt), cudaMemcpyDeviceToHost));
+    VXM_SCK(cudaMemcpy(ms, d_ms.p, N, cudaMemcpyDeviceToHost));
+    if (st) {
+      st->rays_traced = cnt.rays_traced;
+      st->voxels_freed = cnt.voxels_freed;
+      st->voxels_marked_unknown_traced = cnt.voxels_traced;
+      st->voxels_skipped_out_of_bounds = cnt.voxels_skipped;
+    }
+  });
 }
 
 }  // extern "C"
