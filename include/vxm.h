@@ -199,9 +199,11 @@ int vxm_populate_occupied(const vxm_grid_spec* grid, uint8_t* ms, const double* 
                           const vxm_pose* t_vc, int32_t vox_inf, vxm_populate_stats* st);
 
 /* trace_bundle (proj/include/voxmap/raytracer.hpp:127-132,
- * proj/src/raytracer.cpp:98-118), Sequential semantics. bundle = {vd, vw, vh}. */
+ * proj/src/raytracer.cpp:98-118), Sequential semantics. bundle = {vd, vw, vh};
+ * ray_vox_size is trace_bundle's vox_size argument (ray directions and
+ * lengths), the walk uses grid->vox_size, as the reference does. */
 int vxm_trace_bundle(const vxm_grid_spec* grid, uint8_t* ms, const int32_t bundle[3],
-                     const vxm_pose* t_vc, vxm_trace_stats* st);
+                     const vxm_pose* t_vc, double ray_vox_size, vxm_trace_stats* st);
 
 /* bresenham_trace_image (raytracer.hpp:196-202, raytracer.cpp:120-161), Sequential
  * semantics (last writer in point order wins). */

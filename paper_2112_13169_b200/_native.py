@@ -84,7 +84,7 @@ SIGNATURES = {
     "vxm_last_frame_ms": (C.c_int, [C.c_void_p, P(C.c_float)]),
     "vxm_set_stage_events": (C.c_int, [C.c_void_p, P(C.c_void_p)]),
     "vxm_populate_occupied": (C.c_int, [P(GridSpecC), _u8p, _f64p, _f64p, _f64p, C.c_size_t, P(PoseC), C.c_int32, P(PopulateStatsC)]),
-    "vxm_trace_bundle": (C.c_int, [P(GridSpecC), _u8p, _i32p, P(PoseC), P(TraceStatsC)]),
+    "vxm_trace_bundle": (C.c_int, [P(GridSpecC), _u8p, _i32p, P(PoseC), C.c_double, P(TraceStatsC)]),
     "vxm_trace_per_pixel": (C.c_int, [P(GridSpecC), _u8p, _f64p, _f64p, _f64p, C.c_size_t, P(PoseC), P(TraceStatsC)]),
     "vxm_merge_grids": (C.c_int, [_u8p, _u8p, C.c_size_t]),
     "vxm_shift_grid": (C.c_int, [_i32p, _u8p, _u8p, _i32p]),

@@ -61,6 +61,27 @@ def build_libvxm(force=False) -> Path:
     return out
 
 
+HOST_CXX = ["g++", "-std=c++20", "-O2", "-fPIC", "-Wall", "-ffp-contract=off",
+            f"-I{ROOT / 'include'}", f"-I{ROOT / 'third_party' / 'eigen_subset'}"]
+
+
+def build_dropin(force=False):
+    """libvoxmap_b200.so: the C++ voxmap API (include/voxmap/) over libvxm.so,
+    plus the C++ test driver tests/cpp/build/test_dropin."""
+    lib = LIBDIR / "libvoxmap_b200.so"
+    src = CSRC / "host" / "voxmap_api.cpp"
+    hdrs = list((ROOT / "include" / "voxmap").rglob("*.hpp")) + [ROOT / "include" / "vxm.h"]
+    if force or _stale(lib, [src, LIBDIR / "libvxm.so", *hdrs]):
+        _run([*HOST_CXX, "-shared", str(src), f"-L{LIBDIR}", "-lvxm", "-Wl,-rpath,$ORIGIN", "-o", str(lib)])
+    test_src = ROOT / "tests" / "cpp" / "test_dropin.cpp"
+    test_bin = ROOT / "tests" / "cpp" / "build" / "test_dropin"
+    if test_src.exists() and (force or _stale(test_bin, [test_src, lib, *hdrs])):
+        test_bin.parent.mkdir(exist_ok=True)
+        _run([*HOST_CXX, str(test_src), f"-L{LIBDIR}", "-lvoxmap_b200", "-lvxm",
+              "-Wl,-rpath,$ORIGIN/../../../paper_2112_13169_b200/lib", "-o", str(test_bin)])
+    return lib
+
+
 def build_oracle(force=False):
     """oracle/_ref (reference sources) when /root/reference is present, and
     the plain-C restatement oracle/build/liboracle.so. Test infrastructure."""
@@ -81,8 +102,9 @@ def build_oracle(force=False):
 
 def build_all(force=False):
     lib = build_libvxm(force)
+    dropin = build_dropin(force)
     oracle = build_oracle(force)
-    return [lib, *oracle]
+    return [lib, dropin, *oracle]
 
 
 if __name__ == "__main__":

@@ -91,6 +91,7 @@ struct KParams {
   int dx, dy, dz;
   long long n;        // cells per stream
   double vs;
+  double ray_vs;      // vox_size given to generate_rays (== vs on the pipeline path)
   double inv_vs;      // RN(1 / vs), fast-path divisor (see voxel_coord)
   // camera
   int W, H;

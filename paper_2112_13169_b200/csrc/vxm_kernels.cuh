@@ -258,11 +258,13 @@ struct RayState {
 // dir = R * (xi*vs, yi*vs, vd*vs) with left-to-right row sums (the Eigen
 // subset's order; every order agrees for the axis-aligned poses used by the
 // golden vectors), |dir|^2 = (d0^2 + d1^2) + d2^2 (Eigen's vectorized redux).
+// gvs is generate_rays' vox_size (direction and max_dist), vs the grid's
+// (the walk): trace_bundle passes both (raytracer.cpp:100, 63-72).
 __device__ __forceinline__ void ray_setup(const double* R, const double* start, double vs,
-                                          int xi, int yi, int vd, RayState& st) {
-  const double v0 = dmul(static_cast<double>(xi), vs);
-  const double v1 = dmul(static_cast<double>(yi), vs);
-  const double v2 = dmul(static_cast<double>(vd), vs);
+                                          double gvs, int xi, int yi, int vd, RayState& st) {
+  const double v0 = dmul(static_cast<double>(xi), gvs);
+  const double v1 = dmul(static_cast<double>(yi), gvs);
+  const double v2 = dmul(static_cast<double>(vd), gvs);
   double d[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
@@ -270,7 +272,7 @@ __device__ __forceinline__ void ray_setup(const double* R, const double* start, 
   }
   const double xs = static_cast<double>(xi), ys = static_cast<double>(yi),
                ds = static_cast<double>(vd);
-  const double max_dist = dmul(vs, __dsqrt_rn(dadd(dadd(dmul(xs, xs), dmul(ys, ys)), dmul(ds, ds))));
+  const double max_dist = dmul(gvs, __dsqrt_rn(dadd(dadd(dmul(xs, xs), dmul(ys, ys)), dmul(ds, ds))));
   st.stop = dsub(max_dist, 1e-10);
   const double n2 = dadd(dadd(dmul(d[0], d[0]), dmul(d[1], d[1])), dmul(d[2], d[2]));
   const double nrm = __dsqrt_rn(n2);
@@ -317,7 +319,7 @@ __global__ void __launch_bounds__(32) trace_bundle_kernel(KParams p) {
   const uint32_t ray_key = key_tag(epoch) | ((ray + 1u) << 1);
 
   RayState st;
-  ray_setup(R, start, p.vs, xi_idx - (p.vw - 1) / 2, yi_idx - (p.vh - 1) / 2, p.vd, st);
+  ray_setup(R, start, p.vs, p.ray_vs, xi_idx - (p.vw - 1) / 2, yi_idx - (p.vh - 1) / 2, p.vd, st);
 
   const unsigned dx = p.dx, dy = p.dy, dz = p.dz;
   const int dxy = p.dx * p.dy;

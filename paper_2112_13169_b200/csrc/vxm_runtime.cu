@@ -652,6 +652,7 @@ int vxm_create(const vxm_config* cfg, int32_t n_streams, int32_t device, uint32_
       kp.qy = c->qtab + kp.W;
     }
     kp.inv_vs = 1.0 / g.vox_size;
+    kp.ray_vs = g.vox_size;
     kp.max_depth = cfg->camera.max_depth;
     kp.vox_inf = cfg->vox_inf;
     kp.vd = c->bundle[0];

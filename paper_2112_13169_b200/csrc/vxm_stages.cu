@@ -86,6 +86,7 @@ vxm::KParams grid_params(const vxm_grid_spec& g) {
   kp.n = static_cast<long long>(g.dims[0]) * g.dims[1] * g.dims[2];
   kp.vs = g.vox_size;
   kp.inv_vs = 1.0 / g.vox_size;
+  kp.ray_vs = g.vox_size;
   return kp;
 }
 
@@ -169,18 +170,19 @@ int vxm_populate_occupied(const vxm_grid_spec* grid, uint8_t* ms, const double* 
 }
 
 int vxm_trace_bundle(const vxm_grid_spec* grid, uint8_t* ms, const int32_t bundle[3],
-                     const vxm_pose* t_vc, vxm_trace_stats* st) {
+                     const vxm_pose* t_vc, double ray_vox_size, vxm_trace_stats* st) {
   return stage_guard([&] {
     check_grid(grid);
     if (!ms || !bundle || !t_vc) throw StageError{VXM_EINVAL, "null argument"};
     // generate_rays preconditions (raytracer.cpp:37-44)
     if (bundle[0] < 1 || bundle[1] < 1 || bundle[2] < 1 || bundle[1] % 2 == 0 || bundle[2] % 2 == 0)
       throw StageError{VXM_EINVAL, "generate_rays: bundle dimensions must be positive and odd"};
+    if (!(ray_vox_size > 0.0)) throw StageError{VXM_EINVAL, "generate_rays: vox_size must be positive"};
     const long long rays = static_cast<long long>(bundle[1]) * bundle[2];
     if (rays > static_cast<long long>(vxm::kMaxRays))
       throw StageError{VXM_EINVAL, "ray bundle exceeds the 17-bit ray key"};
     // validate_ray (raytracer.cpp:23-33) for every ray, before any write.
-    const double vs = grid->vox_size;
+    const double vs = ray_vox_size;
     for (int a = 0; a < 3; ++a)
       if (!std::isfinite(t_vc->translation[a])) throw StageError{VXM_EINVAL, "Ray: non-finite field"};
     const int hw = (bundle[1] - 1) / 2, hh = (bundle[2] - 1) / 2;
@@ -200,6 +202,7 @@ int vxm_trace_bundle(const vxm_grid_spec* grid, uint8_t* ms, const int32_t bundl
     }
     vxm::KParams kp = grid_params(*grid);
     const long long N = kp.n;
+    kp.ray_vs = ray_vox_size;
     kp.vd = bundle[0];
     kp.vw = bundle[1];
     kp.vh = bundle[2];

@@ -263,11 +263,14 @@ def _trace_dict(st):
     return {k: getattr(st, k) for k, _ in N.TraceStatsC._fields_}
 
 
-def trace_bundle(grid: GridSpec, ms, bundle, t_vc):
-    """trace_bundle (raytracer.hpp:130-132), Sequential semantics."""
+def trace_bundle(grid: GridSpec, ms, bundle, t_vc, vox_size=None):
+    """trace_bundle (raytracer.hpp:130-132), Sequential semantics; vox_size
+    defaults to the grid's."""
     b = np.asarray(bundle, dtype=np.int32)
     st = N.TraceStatsC()
-    N.check(N.load().vxm_trace_bundle(C.byref(grid.c), _u8(ms), _i32(b), C.byref(pose_c(t_vc)), C.byref(st)))
+    vs = grid.vox_size if vox_size is None else vox_size
+    N.check(N.load().vxm_trace_bundle(C.byref(grid.c), _u8(ms), _i32(b), C.byref(pose_c(t_vc)), vs,
+                                      C.byref(st)))
     return _trace_dict(st)
 
 
