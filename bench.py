@@ -67,10 +67,8 @@ def parse():
 
 
 def dist_env():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
+    from paper_2112_13169_b200 import multi
+    return multi.env()
 
 
 def host_cores():
@@ -233,6 +231,7 @@ def our_arm(args, world, rank, local):
     import numpy as np
     import torch
 
+    from paper_2112_13169_b200 import multi
     from paper_2112_13169_b200 import voxmap as vm
     from tests import scenes
 
@@ -251,23 +250,25 @@ def our_arm(args, world, rank, local):
     pool = np.stack([scenes.render(cam, poses[j], boxes) for j in range(POOL)])  # (P, H, W)
     npix = c["width"] * c["height"]
 
-    # device input slots: slot q holds, for every stream s, pool frame (s + q) mod P
+    # this rank's streams (global ids); slot q holds, for every stream g,
+    # pool frame (g + q) mod P
+    gids = list(multi.stream_range(S, rank))
     pool_dev = torch.from_numpy(pool).to(dev)
     slots = torch.empty((POOL, S, c["height"], c["width"]), dtype=torch.float32, device=dev)
     for q in range(POOL):
-        idx = torch.tensor([(s + q) % POOL for s in range(S)], device=dev)
+        idx = torch.tensor([(g + q) % POOL for g in gids], device=dev)
         slots[q] = pool_dev[idx]
     torch.cuda.synchronize()
 
     def step_poses(k):
-        return [poses[(s + k) % POOL] for s in range(S)]
+        return [poses[(g + k) % POOL] for g in gids]
 
     def new_pipeline(streams, flags=0):
         g0 = vm.GridSpec.create_centered(*c["grid"], c["vox"], poses[0][1])
         p = vm.MappingPipeline(vm.PipelineConfig(g0, cam, vox_inf=c["vox_inf"], depth=c["depth"]),
                                n_streams=streams, device=local, flags=flags)
         for s in range(streams):
-            p.set_origin(vm.GridSpec.create_centered(*c["grid"], c["vox"], poses[s % POOL][1]).origin, s)
+            p.set_origin(vm.GridSpec.create_centered(*c["grid"], c["vox"], poses[gids[s] % POOL][1]).origin, s)
         return p
 
     # ---- device-resident throughput (value) + live trace-kernel timing
@@ -299,18 +300,15 @@ def our_arm(args, world, rank, local):
     stage_ms = {"populate_dilate": statistics.mean(e4[0].elapsed_time(e4[1]) for e4 in ev),
                 "trace": statistics.mean(trace_ms),
                 "merge_shift_count": statistics.mean(e4[2].elapsed_time(e4[3]) for e4 in ev)}
-    if dist:
-        t = torch.tensor([ms], device=dev)
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        ms = float(t.item())
-    value = S * K * world / (ms / 1000.0)
+    ms = multi.max_over_ranks(ms, dev)
+    value = multi.job_throughput(S * K, world, ms / 1000.0)
     kernels_per_step = 4 if c["vox_inf"] > 0 else 3
 
     # ---- end to end through the C-ABI host-buffer call
     pinned = torch.empty((POOL, S, c["height"], c["width"]), dtype=torch.float32).pin_memory()
     pool_cpu = torch.from_numpy(pool)
     for q in range(POOL):
-        pinned[q].copy_(pool_cpu[torch.tensor([(s + q) % POOL for s in range(S)])])
+        pinned[q].copy_(pool_cpu[torch.tensor([(g + q) % POOL for g in gids])])
     e2e_pipe = new_pipeline(S)
     for k in range(WU):
         e2e_pipe.integrate_depth_ptr(pinned[k % POOL].data_ptr(), step_poses(k))
@@ -321,11 +319,8 @@ def our_arm(args, world, rank, local):
     for k in range(K):
         e2e_pipe.integrate_depth_ptr(pinned[(WU + k) % POOL].data_ptr(), step_poses(WU + k))
     e2e_s = time.perf_counter() - t0
-    if dist:
-        t = torch.tensor([e2e_s], device=dev)
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e_value = S * K * world / e2e_s
+    e2e_s = multi.max_over_ranks(e2e_s, dev)
+    e2e_value = multi.job_throughput(S * K, world, e2e_s)
     h2d = S * npix * 4 + S * 160  # depth frames + per-stream FrameParams
     d2h = S * 1088                # per-stream counters
     e2e_pipe.close()

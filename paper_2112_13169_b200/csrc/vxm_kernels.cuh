@@ -123,107 +123,160 @@ __global__ void __launch_bounds__(256) populate_cloud_kernel(KParams p) {
 // ---------------------------------------------------------------------------
 constexpr int kDilT = 8;
 
+// Word stride of a bit row: ceil(dx/32) rounded up to a power of two, so the
+// smem index arithmetic is shifts and masks.
+__host__ __device__ constexpr int dilate_row_words(int dx) {
+  int w = 1;
+  while (w * 32 < dx) w <<= 1;
+  return w;
+}
+
 // Shared memory: three bit planes (in, x-dilated, y-dilated).
 __host__ __device__ constexpr size_t dilate_smem_bytes(int r, int dx) {
-  return sizeof(uint32_t) * static_cast<size_t>((dx + 31) / 32) *
+  return sizeof(uint32_t) * static_cast<size_t>(dilate_row_words(dx)) *
          (2u * (kDilT + 2 * r) * (kDilT + 2 * r) + static_cast<size_t>(kDilT) * (kDilT + 2 * r));
 }
 
-__global__ void __launch_bounds__(256) dilate_kernel(KParams p, int r) {
+// kR > 0: radius fixed at compile time (loops unrolled, constant divisors);
+// kR == 0: radius r at run time.
+template <int kR>
+__global__ void __launch_bounds__(256) dilate_kernel(KParams p, int r_rt) {
   extern __shared__ uint32_t bits[];
+  const int r = kR > 0 ? kR : r_rt;
   const int s = blockIdx.z;
   const uint32_t e = p.frames[s].epoch;
   const uint8_t* ctr = p.ctr + static_cast<long long>(s) * p.n;
   uint8_t* occ = p.occ + static_cast<long long>(s) * p.n;
-  const int W = (p.dx + 31) >> 5;
+  const int W = (p.dx + 31) >> 5;                 // words holding cells
+  const int WP = dilate_row_words(p.dx);          // word stride (power of 2)
+  const int lg = __ffs(WP) - 1;
   const int H = kDilT + 2 * r;
   const int y0 = blockIdx.x * kDilT, z0 = blockIdx.y * kDilT;
   const uint32_t dxy = static_cast<uint32_t>(p.dx) * p.dy;
-  uint32_t* in = bits;                  // [H z][H y][W]
-  uint32_t* bx = in + H * H * W;        // x-dilated
-  uint32_t* by = bx + H * H * W;        // [H z][kDilT y][W], y-dilated
+  uint32_t* in = bits;                  // [H z][H y][WP]
+  uint32_t* bx = in + H * H * WP;       // x-dilated
+  uint32_t* by = bx + H * H * WP;       // [H z][kDilT y][WP], y-dilated
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const bool vec = (p.dx & 3) == 0;
   const uint32_t ee = e * 0x01010101u;  // the epoch byte in every lane of a word
 
-  // Pack: lane l reads cells 4l..4l+3 of each 128-cell segment of a row;
-  // word j of the segment is the OR of lanes 8j..8j+7's nibbles. A warp
-  // issues the loads of kBatch rows before packing any of them, so their
-  // latencies overlap.
-  constexpr int kBatch = 6;
+  // Pack: one warp per halo row; lane l reads cells 4l..4l+3 of each
+  // 128-cell segment; word j of a segment is the OR of lanes 8j..8j+7's
+  // nibbles. The loads of kBatch rows are issued before any is packed.
+  constexpr int kBatch = 4;
   const int segs = (W + 3) >> 2;
-  for (int task0 = warp * kBatch; task0 < H * H * segs; task0 += nw * kBatch) {
-    uint32_t v[kBatch];
-#pragma unroll
-    for (int b = 0; b < kBatch; ++b) {
-      const int task = task0 + b;
-      const int row = task / segs, seg = task - row * segs;
-      const int hz = row / H, hy = row - hz * H;
-      const int y = y0 - r + hy, z = z0 - r + hz;
+  for (int row0 = warp; row0 < H * H; row0 += nw * kBatch) {
+    for (int seg = 0; seg < segs; ++seg) {
+      uint32_t v[kBatch];
       const int x = (seg << 7) + 4 * lane;
-      v[b] = 0;
-      if (task < H * H * segs && y >= 0 && y < p.dy && z >= 0 && z < p.dz && x < p.dx) {
-        const uint8_t* src = ctr + static_cast<uint32_t>(y) * p.dx + static_cast<uint32_t>(z) * dxy + x;
-        if (vec) {
-          v[b] = __ldg(reinterpret_cast<const uint32_t*>(src));
-        } else {
-          // bytes past the row end stay 0, which never equals an epoch (>= 1)
-          for (int k = 0; k < 4 && x + k < p.dx; ++k) v[b] |= static_cast<uint32_t>(src[k]) << (8 * k);
+#pragma unroll
+      for (int b = 0; b < kBatch; ++b) {
+        const int row = row0 + b * nw;
+        const int hz = row / H, hy = row - hz * H;
+        const int y = y0 - r + hy, z = z0 - r + hz;
+        v[b] = 0;
+        if (row < H * H && y >= 0 && y < p.dy && z >= 0 && z < p.dz && x < p.dx) {
+          const uint8_t* src = ctr + static_cast<uint32_t>(y) * p.dx + static_cast<uint32_t>(z) * dxy + x;
+          if (vec) {
+            v[b] = __ldg(reinterpret_cast<const uint32_t*>(src));
+          } else {
+            // bytes past the row end stay 0, which never equals an epoch (>= 1)
+            for (int k = 0; k < 4 && x + k < p.dx; ++k) v[b] |= static_cast<uint32_t>(src[k]) << (8 * k);
+          }
         }
       }
-    }
 #pragma unroll
-    for (int b = 0; b < kBatch; ++b) {
-      const int task = task0 + b;
-      if (task >= H * H * segs) break;  // warp-uniform
-      const int row = task / segs, seg = task - row * segs;
-      const uint32_t eq = __vcmpeq4(v[b], ee);  // 0xff per matching byte
-      const uint32_t nib = (eq & 1u) | ((eq >> 7) & 2u) | ((eq >> 14) & 4u) | ((eq >> 21) & 8u);
-      // gather the 4 words of this segment: word j = nibbles of lanes 8j..8j+7
-      uint32_t m = nib << (4 * (lane & 7));
-      m |= __shfl_xor_sync(0xffffffffu, m, 1);
-      m |= __shfl_xor_sync(0xffffffffu, m, 2);
-      m |= __shfl_xor_sync(0xffffffffu, m, 4);
-      const int w = (seg << 2) + (lane >> 3);
-      if ((lane & 7) == 0 && w < W) in[row * W + w] = m;
+      for (int b = 0; b < kBatch; ++b) {
+        const int row = row0 + b * nw;
+        if (row >= H * H) break;  // warp-uniform
+        const uint32_t eq = __vcmpeq4(v[b], ee);  // 0xff per matching byte
+        uint32_t m = ((eq & 1u) | ((eq >> 7) & 2u) | ((eq >> 14) & 4u) | ((eq >> 21) & 8u)) << (4 * (lane & 7));
+        m |= __shfl_xor_sync(0xffffffffu, m, 1);
+        m |= __shfl_xor_sync(0xffffffffu, m, 2);
+        m |= __shfl_xor_sync(0xffffffffu, m, 4);
+        const int w = (seg << 2) + (lane >> 3);
+        if ((lane & 7) == 0 && w < WP) in[(row << lg) + w] = w < W ? m : 0u;
+      }
+    }
+    if (segs * 4 < WP && lane < WP - segs * 4) {  // zero the padding words
+      for (int b = 0; b < kBatch; ++b) {
+        const int row = row0 + b * nw;
+        if (row < H * H) in[(row << lg) + segs * 4 + lane] = 0u;
+      }
     }
   }
   __syncthreads();
   // x: bit x of the dilated row = OR of bits x-r .. x+r (r <= 31)
-  for (int i = threadIdx.x; i < H * H * W; i += blockDim.x) {
-    const int w = i % W;
+  for (int i = threadIdx.x; i < (H * H) << lg; i += blockDim.x) {
+    const int w = i & (WP - 1);
     const uint32_t m = in[i];
     const uint32_t prev = w > 0 ? in[i - 1] : 0u;
-    const uint32_t next = w + 1 < W ? in[i + 1] : 0u;
+    const uint32_t next = w + 1 < WP ? in[i + 1] : 0u;
     uint32_t d = m;
-    for (int k = 1; k <= r; ++k) d |= (m << k) | (prev >> (32 - k)) | (m >> k) | (next << (32 - k));
+#pragma unroll
+    for (int k = 1; k <= (kR > 0 ? kR : 31); ++k) {
+      if (kR == 0 && k > r) break;
+      d |= (m << k) | (prev >> (32 - k)) | (m >> k) | (next << (32 - k));
+    }
     bx[i] = d;
   }
   __syncthreads();
-  // y
-  for (int i = threadIdx.x; i < H * kDilT * W; i += blockDim.x) {
-    const int w = i % W, yz = i / W;
-    const int y = yz % kDilT, hz = yz / kDilT;
+  // y: by[hz][y][w] = OR_k bx[hz][y + k][w]
+  for (int i = threadIdx.x; i < (H * kDilT) << lg; i += blockDim.x) {
+    const int w = i & (WP - 1), yz = i >> lg;
+    const int y = yz & (kDilT - 1), hz = yz / kDilT;
+    const uint32_t* col = bx + ((hz * H + y) << lg) + w;
     uint32_t d = 0;
-    const uint32_t* col = bx + (hz * H + y) * W + w;
-    for (int k = 0; k <= 2 * r; ++k) d |= col[k * W];
+#pragma unroll
+    for (int k = 0; k <= 2 * (kR > 0 ? kR : 16); ++k) {
+      if (kR == 0 && k > 2 * r) break;
+      d |= col[k << lg];
+    }
     by[i] = d;
   }
   __syncthreads();
   // z, then one byte store per set bit (a warp covers 32 consecutive cells)
   for (int row = warp; row < kDilT * kDilT; row += nw) {
-    const int z = row / kDilT, y = row - z * kDilT;
+    const int z = row / kDilT, y = row & (kDilT - 1);
     const int gy = y0 + y, gz = z0 + z;
     if (gy >= p.dy || gz >= p.dz) continue;
     uint8_t* dst = occ + static_cast<uint32_t>(gy) * p.dx + static_cast<uint32_t>(gz) * dxy;
     for (int w = 0; w < W; ++w) {
+      const uint32_t* col = by + ((z * kDilT + y) << lg) + w;
       uint32_t d = 0;
-      const uint32_t* col = by + (z * kDilT + y) * W + w;
-      for (int k = 0; k <= 2 * r; ++k) d |= col[k * kDilT * W];
+#pragma unroll
+      for (int k = 0; k <= 2 * (kR > 0 ? kR : 16); ++k) {
+        if (kR == 0 && k > 2 * r) break;
+        d |= col[(k * kDilT) << lg];
+      }
       const int x = (w << 5) + lane;
       if (x < p.dx && ((d >> lane) & 1u)) dst[x] = static_cast<uint8_t>(e);
     }
   }
+}
+
+// Launches the radius-specialised instance (1..4) or the generic one.
+inline void launch_dilate(const KParams& kp, int r, dim3 grid, size_t smem, cudaStream_t st) {
+  switch (r) {
+    case 1: dilate_kernel<1><<<grid, 256, smem, st>>>(kp, r); break;
+    case 2: dilate_kernel<2><<<grid, 256, smem, st>>>(kp, r); break;
+    case 3: dilate_kernel<3><<<grid, 256, smem, st>>>(kp, r); break;
+    case 4: dilate_kernel<4><<<grid, 256, smem, st>>>(kp, r); break;
+    default: dilate_kernel<0><<<grid, 256, smem, st>>>(kp, r); break;
+  }
+}
+
+// Opt-in to large dynamic shared memory for every instance.
+inline cudaError_t dilate_set_smem(int bytes) {
+  cudaError_t e = cudaSuccess;
+  const void* fns[5] = {reinterpret_cast<const void*>(dilate_kernel<0>), reinterpret_cast<const void*>(dilate_kernel<1>),
+                        reinterpret_cast<const void*>(dilate_kernel<2>), reinterpret_cast<const void*>(dilate_kernel<3>),
+                        reinterpret_cast<const void*>(dilate_kernel<4>)};
+  for (const void* f : fns) {
+    const cudaError_t x = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (x != cudaSuccess) e = x;
+  }
+  return e;
 }
 
 // ---------------------------------------------------------------------------

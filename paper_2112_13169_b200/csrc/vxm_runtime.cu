@@ -304,7 +304,7 @@ void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
     const size_t smem = vxm::dilate_smem_bytes(r, kp.dx);
     dim3 grid(static_cast<unsigned>((kp.dy + vxm::kDilT - 1) / vxm::kDilT),
               static_cast<unsigned>((kp.dz + vxm::kDilT - 1) / vxm::kDilT), S);
-    vxm::dilate_kernel<<<grid, 256, smem, c->stream>>>(kp, r);
+    vxm::launch_dilate(kp, r, grid, smem, c->stream);
     VXM_CK(cudaGetLastError());
   }
   mark(c->ev[2]);
@@ -672,8 +672,7 @@ int vxm_create(const vxm_config* cfg, int32_t n_streams, int32_t device, uint32_
       if (cfg->vox_inf > vxm::kMaxVoxInf || smem > 200 * 1024)
         throw InvalidArg{"vox_inf " + std::to_string(cfg->vox_inf) + " exceeds the dilation tile limit (" +
                          std::to_string(vxm::kMaxVoxInf) + ")"};
-      VXM_CK(cudaFuncSetAttribute(vxm::dilate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
+      VXM_CK(vxm::dilate_set_smem(static_cast<int>(smem)));
     }
     VXM_CK(cudaStreamSynchronize(c->stream));
   });

@@ -150,11 +150,10 @@ int vxm_populate_occupied(const vxm_grid_spec* grid, uint8_t* ms, const double* 
       const size_t smem = vxm::dilate_smem_bytes(r, kp.dx);
       if (r > vxm::kMaxVoxInf || smem > 200 * 1024)
         throw StageError{VXM_EINVAL, "vox_inf exceeds the dilation tile limit"};
-      VXM_SCK(cudaFuncSetAttribute(vxm::dilate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
+      VXM_SCK(vxm::dilate_set_smem(static_cast<int>(smem)));
       dim3 g3(static_cast<unsigned>((kp.dy + vxm::kDilT - 1) / vxm::kDilT),
               static_cast<unsigned>((kp.dz + vxm::kDilT - 1) / vxm::kDilT), 1);
-      vxm::dilate_kernel<<<g3, 256, smem>>>(kp, r);
+      vxm::launch_dilate(kp, r, g3, smem, 0);
       VXM_SCK(cudaGetLastError());
     }
     vxm::decode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_occ.p, d_key.p, d_ms.p, N, kEpoch);

@@ -91,7 +91,7 @@ def test_transform_voxelize_random_rotations(gpu_lib, n):
 
 # --- populate_occupied (proj/tests/test_integrator.cpp, acceptance criterion 4) --
 
-@pytest.mark.parametrize("vox_inf", [0, 1, 2, 3])
+@pytest.mark.parametrize("vox_inf", [0, 1, 2, 3, 4, 5, 8])
 def test_populate_matches_reference(gpu_lib, vox_inf):
     rng = np.random.default_rng(104 + vox_inf)
     vox = 0.15

@@ -15,5 +15,5 @@ for name, vox_inf, dm, S in (("cfg1", 0, 6.5, 1), ("cfg2", 2, 5.0, 1), ("cfg2x64
     pose = vm.look_along_x((0, 0, 0))
     d = scenes.render(cam, pose, scenes.box_field_boxes(1))
     dev = torch.from_numpy(np.stack([d] * S)).cuda()
-    for _ in range(3):
+    for _ in range(6):
         p.integrate_depth_device(dev.data_ptr(), [pose] * S); p.wait_stats()

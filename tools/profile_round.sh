@@ -1,0 +1,15 @@
+#!/bin/bash
+# Profiling recipe for the committed evidence under profiles/ (run under gpurun).
+#  1. launch list of the bench command (serialised, cold-cache: compare shares)
+#  2. one ncu --set full capture of each kernel of a batched cfg2 step
+set -x
+mkdir -p gpurun_out
+TAG=${1:-r01}
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
+    --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 3 --latency-frames 5 --no-cpu-baseline \
+    > gpurun_out/${TAG}_bench_under_ncu.log 2>&1
+for k in trace_bundle populate_depth dilate merge_shift; do
+  ncu --set full --clock-control none --import-source on -k regex:$k -s 4 -c 1 -o gpurun_out/${TAG}_$k \
+      python tools/prof_frames.py cfg2x64 > gpurun_out/${TAG}_$k.log 2>&1
+done
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem --format=csv > gpurun_out/${TAG}_gpu.txt
