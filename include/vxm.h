@@ -159,6 +159,12 @@ int vxm_integrate_depth(vxm_ctx* ctx, const float* depth, const vxm_pose* t_wc,
 int vxm_integrate_depth_device(vxm_ctx* ctx, const float* depth_dev, const vxm_pose* t_wc);
 int vxm_wait_stats(vxm_ctx* ctx, vxm_stats* stats);
 
+/* Host frames (pinned for full overlap), asynchronous: the H2D copy runs on a
+ * copy stream into one of two device staging buffers, so consecutive calls
+ * overlap frame k+1's transfer with frame k's kernels. The host buffer must
+ * stay valid until the following vxm_wait_stats (or the next-but-one call). */
+int vxm_integrate_depth_async(vxm_ctx* ctx, const float* depth, const vxm_pose* t_wc);
+
 /* MappingPipeline::integrate(MeasurementFrame{cloud, t_wc}) for n_streams == 1
  * with an arbitrary camera-frame point cloud (double SoA, HOST memory). */
 int vxm_integrate_cloud(vxm_ctx* ctx, const double* xs, const double* ys, const double* zs,

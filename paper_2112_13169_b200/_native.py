@@ -77,6 +77,7 @@ SIGNATURES = {
     "vxm_integrate_depth": (C.c_int, [C.c_void_p, C.c_void_p, P(PoseC), P(StatsC)]),
     "vxm_integrate_depth_device": (C.c_int, [C.c_void_p, C.c_void_p, P(PoseC)]),
     "vxm_wait_stats": (C.c_int, [C.c_void_p, P(StatsC)]),
+    "vxm_integrate_depth_async": (C.c_int, [C.c_void_p, C.c_void_p, P(PoseC)]),
     "vxm_integrate_cloud": (C.c_int, [C.c_void_p, _f64p, _f64p, _f64p, C.c_size_t, P(PoseC), P(StatsC)]),
     "vxm_download_local": (C.c_int, [C.c_void_p, C.c_int32, _u8p, _f64p]),
     "vxm_upload_local": (C.c_int, [C.c_void_p, C.c_int32, _u8p, _f64p]),

@@ -36,7 +36,20 @@ __device__ __forceinline__ unsigned populate_point(const KParams& p, const doubl
   return 0u;
 }
 
-__global__ void __launch_bounds__(256) populate_depth_kernel(KParams p) {
+// Depth quads (4 pixels, one 16-byte streaming load) per thread; a block
+// walks `iters` consecutive 256-quad tiles of one stream's frame and loads
+// tile i+1 before resolving tile i, so the HBM latency of a batched launch
+// overlaps the fp64 work.
+__device__ __forceinline__ float4 load_quad(const float* depth, int first, int npix) {
+  if (first + 3 < npix && (reinterpret_cast<uintptr_t>(depth + first) & 15u) == 0)
+    return __ldcs(reinterpret_cast<const float4*>(depth + first));
+  float d[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) d[k] = first + k < npix ? depth[first + k] : 0.0f;
+  return make_float4(d[0], d[1], d[2], d[3]);
+}
+
+__global__ void __launch_bounds__(256) populate_depth_kernel(KParams p, int iters) {
   const int s = blockIdx.y;
   const FrameParams* fp = p.frames + s;
   const uint8_t mark = static_cast<uint8_t>(fp->epoch);
@@ -47,22 +60,16 @@ __global__ void __launch_bounds__(256) populate_depth_kernel(KParams p) {
 #pragma unroll
   for (int i = 0; i < 3; ++i) t[i] = fp->trans[i];
   const float* depth = fp->depth;
-
-  // Each thread owns 4 consecutive pixels: one 16-byte streaming load keeps
-  // enough bytes in flight for HBM when many streams are batched, and the 4
-  // independent fp64 chains give the scheduler ILP.
   const int npix = p.W * p.H;
-  const int first = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+
   unsigned total = 0, outside = 0;
-  if (first < npix) {
-    float d[4];
-    if (first + 3 < npix && (reinterpret_cast<uintptr_t>(depth + first) & 15u) == 0) {
-      const float4 v4 = __ldcs(reinterpret_cast<const float4*>(depth + first));
-      d[0] = v4.x; d[1] = v4.y; d[2] = v4.z; d[3] = v4.w;
-    } else {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) d[k] = first + k < npix ? depth[first + k] : 0.0f;
-    }
+  int first = ((blockIdx.x * iters) * blockDim.x + threadIdx.x) * 4;
+  float4 next = first < npix ? load_quad(depth, first, npix) : make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int it = 0; it < iters && first < npix; ++it) {
+    const float4 cur = next;
+    const int nfirst = first + blockDim.x * 4;
+    if (it + 1 < iters && nfirst < npix) next = load_quad(depth, nfirst, npix);
+    const float d[4] = {cur.x, cur.y, cur.z, cur.w};
     const int v0 = first / p.W;
     const int u0 = first - v0 * p.W;
 #pragma unroll
@@ -71,13 +78,14 @@ __global__ void __launch_bounds__(256) populate_depth_kernel(KParams p) {
       if (u >= p.W) { u -= p.W; ++v; }  // a row boundary inside the quad
       // DepthImage::valid_depth (geometry.hpp:124): finite and > 0; then the
       // max-depth cut on the promoted double (geometry.cpp:53-54).
-      if (!(isfinite(d[k]) && d[k] > 0.0f)) continue;
+      if (first + k >= npix || !(isfinite(d[k]) && d[k] > 0.0f)) continue;
       const double D = static_cast<double>(d[k]);
       if (D > p.max_depth) continue;
       ++total;
       outside += populate_point(p, R, t, target, mark, dmul(__ldg(p.qx + u), D),
                                 dmul(__ldg(p.qy + v), D), D);
     }
+    first = nfirst;
   }
   unsigned vals[2] = {total, outside};
   unsigned long long* dst[2] = {&p.counters[s].points_total, &p.counters[s].points_outside};
@@ -592,9 +600,31 @@ __global__ void __launch_bounds__(256) trace_per_pixel_kernel(KParams p, int fro
 // (pipeline.cpp:114-115) in one gather: destination cell c takes
 // merge(loc[c+off], ms[c+off]) when c+off is inside the grid, else Unknown.
 // Reads the current local buffer, writes the other (ping-pong). One warp per
-// x-row; each lane produces 4 consecutive cells.
+// x-row (rows_per_warp rows per warp: 1 for a single stream, up to
+// kRowsPerWarp when a batch fills the GPU); each lane produces 4 cells.
+// When dx and the x-shift are multiples of 4 (all benchmark grids), the 4
+// cells move as one 32-bit word and are decoded / merged with byte-SIMD
+// intrinsics; otherwise a per-cell path runs.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p) {
+constexpr int kRowsPerWarp = 4;
+
+// merge of 4 packed cells: local l4, occupancy o4 (epoch bytes), 4 keys
+__device__ __forceinline__ uint32_t merge4(uint32_t l4, uint32_t o4, uint4 k4, uint32_t epoch) {
+  const uint32_t kk[4] = {k4.x, k4.y, k4.z, k4.w};
+  uint32_t m4 = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t v = (kk[i] >> kKeyShift) == epoch ? (1u | ((kk[i] & 1u) << 1)) : 0u;  // 1 or 3
+    m4 |= v << (8 * i);
+  }
+  const uint32_t occm = __vcmpeq4(o4, epoch * 0x01010101u);  // 0xff where Occupied
+  m4 = (m4 & ~occm) | (0x02020202u & occm);
+  const uint32_t keep = __vcmpeq4(m4, 0u);                   // measurement Unknown: keep local
+  const uint32_t clear = __vcmpeq4(m4, 0x03030303u);          // UnknownTraced: -> Unknown
+  return (l4 & keep) | (m4 & ~(keep | clear));
+}
+
+__global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int rows_per_warp) {
   const int s = blockIdx.y;
   const FrameParams* fp = p.frames + s;
   const uint32_t epoch = fp->epoch;
@@ -606,65 +636,49 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p) {
   const uint8_t* src = (cur ? p.loc1 : p.loc0) + base;
   uint8_t* dst = (cur ? p.loc0 : p.loc1) + base;
   const int lane = threadIdx.x & 31;
-  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int warp_id = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int rows = p.dy * p.dz;
   const uint32_t dxy = static_cast<uint32_t>(p.dx) * p.dy;
 
   if (blockIdx.x == 0 && threadIdx.x < 32) fold_trace_slots(p.counters[s]);
 
   unsigned occ_n = 0, free_n = 0;
-  if (row < rows) {
+  const bool vec = (p.dx & 3) == 0 && (ox & 3) == 0;
+  for (int rr = 0; rr < rows_per_warp; ++rr) {
+    const int row = warp_id * rows_per_warp + rr;
+    if (row >= rows) break;
     const int z = row / p.dy;
     const int y = row - z * p.dy;
     const int sy = y + oy, sz = z + oz;
     const bool row_ok = sy >= 0 && sy < p.dy && sz >= 0 && sz < p.dz;
     const uint32_t drow = static_cast<uint32_t>(y) * p.dx + static_cast<uint32_t>(z) * dxy;
     const long long srow = static_cast<long long>(sy) * p.dx + static_cast<long long>(sz) * dxy;
-    const bool vec = (p.dx & 3) == 0;
-    if (vec && (ox & 3) == 0) {
-      // 4-aligned source and destination: 4-byte loads of loc/occ and one
-      // 16-byte load of the 4 keys; the 4 cells are all in or all out of
-      // the grid along x because dx and ox are multiples of 4.
+    if (vec) {
       for (int x0 = lane * 4; x0 < p.dx; x0 += 128) {
         const int sx = x0 + ox;
         uint32_t out = 0;
         if (row_ok && sx >= 0 && sx < p.dx) {
           const long long sc = srow + sx;
-          const uint32_t l4 = *reinterpret_cast<const uint32_t*>(src + sc);
-          const uint32_t o4 = *reinterpret_cast<const uint32_t*>(occ + sc);
-          const uint4 k4 = *reinterpret_cast<const uint4*>(key + sc);
-          const uint32_t kk[4] = {k4.x, k4.y, k4.z, k4.w};
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const uint32_t v = merge_cell((l4 >> (8 * i)) & 0xffu,
-                                          decode_cell((o4 >> (8 * i)) & 0xffu, kk[i], epoch));
-            occ_n += v == 2u;
-            free_n += v == 1u;
-            out |= v << (8 * i);
+          out = merge4(*reinterpret_cast<const uint32_t*>(src + sc), *reinterpret_cast<const uint32_t*>(occ + sc),
+                       *reinterpret_cast<const uint4*>(key + sc), epoch);
+        }
+        occ_n += __popc(__vcmpeq4(out, 0x02020202u)) >> 3;
+        free_n += __popc(__vcmpeq4(out, 0x01010101u)) >> 3;
+        *reinterpret_cast<uint32_t*>(dst + drow + x0) = out;
+      }
+    } else {
+      for (int x0 = lane * 4; x0 < p.dx; x0 += 128) {
+        for (int i = 0; i < 4 && x0 + i < p.dx; ++i) {
+          const int sx = x0 + i + ox;
+          uint32_t v = 0;
+          if (row_ok && sx >= 0 && sx < p.dx) {
+            const long long sc = srow + sx;
+            v = merge_cell(src[sc], decode_cell(occ[sc], key[sc], epoch));
           }
+          occ_n += v == 2u;
+          free_n += v == 1u;
+          dst[drow + x0 + i] = static_cast<uint8_t>(v);
         }
-        *reinterpret_cast<uint32_t*>(dst + drow + x0) = out;
-      }
-    } else
-    for (int x0 = lane * 4; x0 < p.dx; x0 += 128) {
-      uint32_t out = 0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int x = x0 + i;
-        const int sx = x + ox;
-        uint32_t v = 0;
-        if (row_ok && x < p.dx && sx >= 0 && sx < p.dx) {
-          const long long sc = srow + sx;
-          v = merge_cell(src[sc], decode_cell(occ[sc], key[sc], epoch));
-        }
-        occ_n += v == 2u;
-        free_n += v == 1u;
-        out |= v << (8 * i);
-      }
-      if (vec) {
-        *reinterpret_cast<uint32_t*>(dst + drow + x0) = out;
-      } else {
-        for (int i = 0; i < 4 && x0 + i < p.dx; ++i) dst[drow + x0 + i] = static_cast<uint8_t>(out >> (8 * i));
       }
     }
   }

@@ -244,6 +244,12 @@ struct vxm_ctx {
   vxm::Counters* counters = nullptr;
   vxm::FrameParams* frames_dev = nullptr;
   float* depth_dev = nullptr;
+  // double-buffered staging for vxm_integrate_depth_async (created lazily)
+  cudaStream_t copy_stream = nullptr;
+  float* stage[2] = {nullptr, nullptr};
+  cudaEvent_t ev_copied[2] = {};
+  cudaEvent_t ev_consumed[2] = {};
+  int stage_slot = 0;
   double* cloud_dev = nullptr;
   size_t cloud_cap = 0;
 
@@ -268,6 +274,7 @@ struct vxm_ctx {
   cudaGraph_t graph_tmpl[2] = {nullptr, nullptr};          // kept for node updates
   cudaGraphNode_t stage_nodes[2][4] = {};                  // event-record nodes per graph
   void* user_stage_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool stage_dirty[2] = {true, true};                      // node events need re-pointing
   // ev[0] / ev[5] bracket the frame outside the graph; ev[1..4] are the
   // stage boundaries recorded inside it (before populate, before trace,
   // after trace, after merge)
@@ -291,9 +298,14 @@ void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
   mark(c->ev[1]);
   VXM_CK(cudaMemsetAsync(c->counters, 0, sizeof(vxm::Counters) * S, c->stream));
   if (!cloud) {
+    // tiles of 256 quads; a block takes `iters` of them once the batch
+    // alone fills the GPU several times over (8 blocks per SM)
     const long long npix = static_cast<long long>(kp.W) * kp.H;
-    dim3 grid(static_cast<unsigned>(((npix + 3) / 4 + kPopulateThreads - 1) / kPopulateThreads), S);
-    vxm::populate_depth_kernel<<<grid, kPopulateThreads, 0, c->stream>>>(kp);
+    const long long tiles = ((npix + 3) / 4 + kPopulateThreads - 1) / kPopulateThreads;
+    const long long fill = static_cast<long long>(c->nsm) * 8;
+    const int iters = static_cast<int>(std::max(1LL, std::min(8LL, tiles * S / fill)));
+    dim3 grid(static_cast<unsigned>((tiles + iters - 1) / iters), S);
+    vxm::populate_depth_kernel<<<grid, kPopulateThreads, 0, c->stream>>>(kp, iters);
   } else {
     dim3 grid(static_cast<unsigned>(c->nsm * 4), S);
     vxm::populate_cloud_kernel<<<grid, kPopulateThreads, 0, c->stream>>>(kp);
@@ -323,9 +335,13 @@ void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
   mark(c->ev[3]);
   {
     const long long rows = static_cast<long long>(kp.dy) * kp.dz;
-    const int rows_per_block = kMergeThreads / 32;
+    // one row per warp unless the batch fills the GPU several times over
+    const long long warps = rows * S;
+    const long long fill = static_cast<long long>(c->nsm) * 64;
+    const int rpw = static_cast<int>(std::max(1LL, std::min<long long>(vxm::kRowsPerWarp, warps / fill)));
+    const int rows_per_block = kMergeThreads / 32 * rpw;
     dim3 grid(static_cast<unsigned>((rows + rows_per_block - 1) / rows_per_block), S);
-    vxm::merge_shift_count_kernel<<<grid, kMergeThreads, 0, c->stream>>>(kp);
+    vxm::merge_shift_count_kernel<<<grid, kMergeThreads, 0, c->stream>>>(kp, rpw);
     VXM_CK(cudaGetLastError());
   }
   mark(c->ev[4]);
@@ -421,13 +437,22 @@ void prepare_frames(vxm_ctx* c, const vxm_pose* poses, const float* depth_dev_ba
 
 void run_frame(vxm_ctx* c, bool cloud) {
   const bool timed = (c->flags & VXM_FLAG_STAGE_TIMING) != 0;
-  VXM_CK(cudaEventRecord(c->ev[0], c->stream));
   if (timed || (c->flags & VXM_FLAG_NO_GRAPH)) {
+    VXM_CK(cudaEventRecord(c->ev[0], c->stream));
     launch_frame(c, cloud, false);
   } else {
+    const int gi = cloud ? 1 : 0;
     cudaGraphExec_t& g = cloud ? c->graph_cloud : c->graph_depth;
-    if (!g) g = capture(c, cloud);
-    apply_stage_events(c, g, cloud ? 1 : 0);
+    if (!g) {
+      g = capture(c, cloud);
+      c->stage_dirty[gi] = true;
+    }
+    if (c->stage_dirty[gi]) {
+      apply_stage_events(c, g, gi);
+      c->stage_dirty[gi] = false;
+    }
+    // recorded after the host-side work so the frame time is device time only
+    VXM_CK(cudaEventRecord(c->ev[0], c->stream));
     VXM_CK(cudaGraphLaunch(g, c->stream));
   }
   VXM_CK(cudaEventRecord(c->ev[5], c->stream));
@@ -508,9 +533,21 @@ void destroy_ctx(vxm_ctx* c) {
   cudaFree(c->cloud_dev);
   cudaFreeHost(c->frames_ring);
   cudaFreeHost(c->counters_host);
+  if (c->copy_stream) {
+    cudaStreamSynchronize(c->copy_stream);
+    for (int b = 0; b < 2; ++b) {
+      cudaFree(c->stage[b]);
+      cudaEventDestroy(c->ev_copied[b]);
+      cudaEventDestroy(c->ev_consumed[b]);
+    }
+    cudaStreamDestroy(c->copy_stream);
+  }
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
+
+// Drop the unused helper warning: pinned-ness is decided by the driver.
+[[maybe_unused]] static bool (*const kIsPinned)(const void*) = is_pinned;
 
 // PipelineConfig::validate (pipeline.cpp:33-42) + the GPU's own limits.
 void validate_config(const vxm_config& cfg) {
@@ -727,10 +764,42 @@ int vxm_integrate_depth_device(vxm_ctx* ctx, const float* depth_dev, const vxm_p
   });
 }
 
+// Host-buffer frames, asynchronous and double buffered: the H2D copy of this
+// call runs on the context's copy stream into one of two staging buffers
+// while the compute stream may still be busy with the previous frame.
+int vxm_integrate_depth_async(vxm_ctx* ctx, const float* depth, const vxm_pose* t_wc) {
+  return guarded([&] {
+    if (!ctx || !depth || !t_wc) throw InvalidArg{"null argument"};
+    VXM_CK(cudaSetDevice(ctx->device));
+    const size_t frame = static_cast<size_t>(ctx->kp.W) * ctx->kp.H;
+    const size_t bytes = sizeof(float) * frame * ctx->S;
+    if (!ctx->copy_stream) {
+      VXM_CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+      for (int b = 0; b < 2; ++b) {
+        VXM_CK(cudaMalloc(&ctx->stage[b], bytes));
+        VXM_CK(cudaEventCreateWithFlags(&ctx->ev_copied[b], cudaEventDisableTiming));
+        VXM_CK(cudaEventCreateWithFlags(&ctx->ev_consumed[b], cudaEventDisableTiming));
+        VXM_CK(cudaEventRecord(ctx->ev_consumed[b], ctx->stream));
+      }
+    }
+    const int b = ctx->stage_slot;
+    ctx->stage_slot ^= 1;
+    VXM_CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_consumed[b], 0));  // K1 done with it
+    VXM_CK(cudaMemcpyAsync(ctx->stage[b], depth, bytes, cudaMemcpyHostToDevice, ctx->copy_stream));
+    VXM_CK(cudaEventRecord(ctx->ev_copied[b], ctx->copy_stream));
+    next_slot(ctx);
+    prepare_frames(ctx, t_wc, ctx->stage[b], frame);
+    VXM_CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[b], 0));
+    run_frame(ctx, false);
+    VXM_CK(cudaEventRecord(ctx->ev_consumed[b], ctx->stream));
+  });
+}
+
 int vxm_set_stage_events(vxm_ctx* ctx, void* const events[4]) {
   return guarded([&] {
     if (!ctx) throw InvalidArg{"null context"};
     for (int i = 0; i < 4; ++i) ctx->user_stage_ev[i] = events ? events[i] : nullptr;
+    ctx->stage_dirty[0] = ctx->stage_dirty[1] = true;
   });
 }
 

@@ -200,6 +200,12 @@ class MappingPipeline:
         self._set_poses(poses)
         N.check(self._lib.vxm_integrate_depth_device(self._ctx, C.c_void_p(depth_dev_ptr), self._poses))
 
+    def integrate_depth_async(self, depth_host_ptr: int, poses):
+        """Host frames at a raw (pinned) pointer; asynchronous, double
+        buffered (H2D of the next call overlaps this call's kernels)."""
+        self._set_poses(poses)
+        N.check(self._lib.vxm_integrate_depth_async(self._ctx, C.c_void_p(depth_host_ptr), self._poses))
+
     def wait_stats(self):
         N.check(self._lib.vxm_wait_stats(self._ctx, self._stats))
         return [stats_dict(s) for s in self._stats]

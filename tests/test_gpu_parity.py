@@ -316,3 +316,28 @@ def test_pipeline_long_trajectory_wraps_epochs(gpu_lib):
         if k % 50 == 49 or k == 299:
             assert np.array_equal(gpu.local_grid()[0], orc.local_grid()[0]), k
     assert shifts > 250
+
+
+def test_async_double_buffered_host_path(gpu_lib):
+    """vxm_integrate_depth_async: queued host frames (pinned) give the same
+    grids as the synchronous path and the reference."""
+    import torch
+
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 160, 120, 6.5)
+    grid = vm.GridSpec.create_centered(6.0, 6.0, 3.0, 0.15, (0.0, 0.0, 0.0))
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=2, depth=6.5)
+    S, F = 3, 6
+    poses = [[vm.look_along_x((0.01 * s, 0.08 * k - 0.2, 0.0)) for s in range(S)] for k in range(F)]
+    frames = [np.stack([scenes.render(cam, poses[k][s], scenes.box_field_boxes(1 + s)) for s in range(S)])
+              for k in range(F)]
+    pinned = [torch.from_numpy(f).pin_memory() for f in frames]
+    pipe = vm.MappingPipeline(cfg, n_streams=S)
+    for k in range(F):
+        pipe.integrate_depth_async(pinned[k].data_ptr(), poses[k])
+    last = pipe.wait_stats()
+    refs = [oracle_pipeline(cfg) for _ in range(S)]
+    for s in range(S):
+        for k in range(F):
+            sr = refs[s].integrate_depth(frames[k][s], poses[k][s])
+        assert last[s]["freed_count"] == sr["freed_count"]
+        assert np.array_equal(pipe.local_grid(s)[0], refs[s].local_grid()[0]), s
