@@ -124,112 +124,104 @@ __global__ void __launch_bounds__(256) populate_cloud_kernel(KParams p) {
 // K2: obstacle inflation. mark_point writes the (2r+1)^3 cube around every
 // in-bounds centre, clipped to the grid (integrator.cpp:70-83): a Chebyshev
 // dilation of the centre set restricted to the grid, which is separable.
-// A block owns an 8x8 (y,z) tile of full x-rows. Its rows plus an r-row halo
-// are loaded with coalesced 4-byte loads and packed into bitmasks (one warp
-// per row), dilated along x with shifts, then along y and z with ORs, all in
-// shared memory; set bits are written back as Occupied bytes.
+// Two kernels: K2a packs and x-dilates every row once into a bit plane; K2b
+// dilates 8x8 tiles of bit rows along y and z in shared memory and writes the
+// Occupied bytes.
 // ---------------------------------------------------------------------------
 constexpr int kDilT = 8;
 
 // Word stride of a bit row: ceil(dx/32) rounded up to a power of two, so the
-// smem index arithmetic is shifts and masks.
+// index arithmetic is shifts and masks.
 __host__ __device__ constexpr int dilate_row_words(int dx) {
   int w = 1;
   while (w * 32 < dx) w <<= 1;
   return w;
 }
 
-// Shared memory: three bit planes (in, x-dilated, y-dilated).
-__host__ __device__ constexpr size_t dilate_smem_bytes(int r, int dx) {
-  return sizeof(uint32_t) * static_cast<size_t>(dilate_row_words(dx)) *
-         (2u * (kDilT + 2 * r) * (kDilT + 2 * r) + static_cast<size_t>(kDilT) * (kDilT + 2 * r));
+// K2a: one warp per x-row: the row's centre bytes become a bit row (one
+// ballot per 32 cells, coalesced byte loads), dilated along x by r with
+// shuffles between the lanes holding neighbouring words, and stored to the
+// per-stream bit plane `dbits` [dy*dz rows][WP words]. Each row is packed
+// exactly once (the tile kernel below reads bits, never bytes).
+constexpr int kDilRowsPerWarp = 4;
+
+__global__ void __launch_bounds__(256) dilate_rows_kernel(KParams p, int r) {
+  const int s = blockIdx.y;
+  const uint32_t e = p.frames[s].epoch;
+  const int lane = threadIdx.x & 31;
+  const int row0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * kDilRowsPerWarp;
+  const int rows = p.dy * p.dz;
+  const int W = (p.dx + 31) >> 5;
+  const int WP = dilate_row_words(p.dx);
+  const uint8_t* ctr = p.ctr + static_cast<long long>(s) * p.n;
+  uint32_t* plane = p.dbits + static_cast<long long>(s) * rows * WP;
+  for (int row = row0; row < row0 + kDilRowsPerWarp && row < rows; ++row) {
+    const uint8_t* src = ctr + static_cast<uint32_t>(row) * p.dx;
+    uint32_t mine = 0;  // lane w keeps word w
+    for (int w0 = 0; w0 < W; w0 += 4) {
+      uint32_t c[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int x = ((w0 + j) << 5) + lane;
+        c[j] = x < p.dx ? __ldg(src + x) : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t m = __ballot_sync(0xffffffffu, c[j] == e);
+        if (lane == w0 + j) mine = m;
+      }
+    }
+    uint32_t d = mine;
+    if (__any_sync(0xffffffffu, mine != 0u)) {
+      const uint32_t prev = __shfl_up_sync(0xffffffffu, mine, 1);
+      const uint32_t next = __shfl_down_sync(0xffffffffu, mine, 1);
+      const uint32_t pv = lane > 0 ? prev : 0u;
+      const uint32_t nx = lane + 1 < W ? next : 0u;
+      for (int k = 1; k <= r; ++k) d |= (mine << k) | (pv >> (32 - k)) | (mine >> k) | (nx << (32 - k));
+    }
+    if (lane < WP) plane[static_cast<uint32_t>(row) * WP + lane] = lane < W ? d : 0u;
+  }
 }
 
-// kR > 0: radius fixed at compile time (loops unrolled, constant divisors);
-// kR == 0: radius r at run time.
+// Shared memory of K2b: the (8+2r)^2 halo bit rows and the y-dilated rows.
+__host__ __device__ constexpr size_t dilate_smem_bytes(int r, int dx) {
+  return sizeof(uint32_t) * static_cast<size_t>(dilate_row_words(dx)) *
+         (static_cast<size_t>(kDilT + 2 * r) * (kDilT + 2 * r) + static_cast<size_t>(kDilT) * (kDilT + 2 * r));
+}
+
+// K2b: a block owns an 8x8 (y,z) tile of x-dilated bit rows, loads them with
+// an r-row halo into shared memory, ORs along y then z, and writes one
+// Occupied byte per set bit (a warp covers 32 consecutive cells).
+// kR > 0: radius fixed at compile time; kR == 0: radius at run time.
 template <int kR>
-__global__ void __launch_bounds__(256) dilate_kernel(KParams p, int r_rt) {
+__global__ void __launch_bounds__(256) dilate_tiles_kernel(KParams p, int r_rt) {
   extern __shared__ uint32_t bits[];
   const int r = kR > 0 ? kR : r_rt;
   const int s = blockIdx.z;
   const uint32_t e = p.frames[s].epoch;
-  const uint8_t* ctr = p.ctr + static_cast<long long>(s) * p.n;
   uint8_t* occ = p.occ + static_cast<long long>(s) * p.n;
-  const int W = (p.dx + 31) >> 5;                 // words holding cells
-  const int WP = dilate_row_words(p.dx);          // word stride (power of 2)
+  const int W = (p.dx + 31) >> 5;
+  const int WP = dilate_row_words(p.dx);
   const int lg = __ffs(WP) - 1;
   const int H = kDilT + 2 * r;
   const int y0 = blockIdx.x * kDilT, z0 = blockIdx.y * kDilT;
   const uint32_t dxy = static_cast<uint32_t>(p.dx) * p.dy;
-  uint32_t* in = bits;                  // [H z][H y][WP]
-  uint32_t* bx = in + H * H * WP;       // x-dilated
-  uint32_t* by = bx + H * H * WP;       // [H z][kDilT y][WP], y-dilated
+  const uint32_t* plane = p.dbits + static_cast<long long>(s) * p.dy * p.dz * WP;
+  uint32_t* bx = bits;                  // [H z][H y][WP]
+  uint32_t* by = bx + (H * H << lg);    // [H z][kDilT y][WP], y-dilated
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const bool vec = (p.dx & 3) == 0;
-  const uint32_t ee = e * 0x01010101u;  // the epoch byte in every lane of a word
 
-  // Pack: one warp per halo row; lane l reads cells 4l..4l+3 of each
-  // 128-cell segment; word j of a segment is the OR of lanes 8j..8j+7's
-  // nibbles. The loads of kBatch rows are issued before any is packed.
-  constexpr int kBatch = 4;
-  const int segs = (W + 3) >> 2;
-  for (int row0 = warp; row0 < H * H; row0 += nw * kBatch) {
-    for (int seg = 0; seg < segs; ++seg) {
-      uint32_t v[kBatch];
-      const int x = (seg << 7) + 4 * lane;
-#pragma unroll
-      for (int b = 0; b < kBatch; ++b) {
-        const int row = row0 + b * nw;
-        const int hz = row / H, hy = row - hz * H;
-        const int y = y0 - r + hy, z = z0 - r + hz;
-        v[b] = 0;
-        if (row < H * H && y >= 0 && y < p.dy && z >= 0 && z < p.dz && x < p.dx) {
-          const uint8_t* src = ctr + static_cast<uint32_t>(y) * p.dx + static_cast<uint32_t>(z) * dxy + x;
-          if (vec) {
-            v[b] = __ldg(reinterpret_cast<const uint32_t*>(src));
-          } else {
-            // bytes past the row end stay 0, which never equals an epoch (>= 1)
-            for (int k = 0; k < 4 && x + k < p.dx; ++k) v[b] |= static_cast<uint32_t>(src[k]) << (8 * k);
-          }
-        }
-      }
-#pragma unroll
-      for (int b = 0; b < kBatch; ++b) {
-        const int row = row0 + b * nw;
-        if (row >= H * H) break;  // warp-uniform
-        const uint32_t eq = __vcmpeq4(v[b], ee);  // 0xff per matching byte
-        uint32_t m = ((eq & 1u) | ((eq >> 7) & 2u) | ((eq >> 14) & 4u) | ((eq >> 21) & 8u)) << (4 * (lane & 7));
-        m |= __shfl_xor_sync(0xffffffffu, m, 1);
-        m |= __shfl_xor_sync(0xffffffffu, m, 2);
-        m |= __shfl_xor_sync(0xffffffffu, m, 4);
-        const int w = (seg << 2) + (lane >> 3);
-        if ((lane & 7) == 0 && w < WP) in[(row << lg) + w] = w < W ? m : 0u;
-      }
-    }
-    if (segs * 4 < WP && lane < WP - segs * 4) {  // zero the padding words
-      for (int b = 0; b < kBatch; ++b) {
-        const int row = row0 + b * nw;
-        if (row < H * H) in[(row << lg) + segs * 4 + lane] = 0u;
-      }
-    }
-  }
-  __syncthreads();
-  // x: bit x of the dilated row = OR of bits x-r .. x+r (r <= 31)
+  uint32_t any = 0;
   for (int i = threadIdx.x; i < (H * H) << lg; i += blockDim.x) {
-    const int w = i & (WP - 1);
-    const uint32_t m = in[i];
-    const uint32_t prev = w > 0 ? in[i - 1] : 0u;
-    const uint32_t next = w + 1 < WP ? in[i + 1] : 0u;
-    uint32_t d = m;
-#pragma unroll
-    for (int k = 1; k <= (kR > 0 ? kR : 31); ++k) {
-      if (kR == 0 && k > r) break;
-      d |= (m << k) | (prev >> (32 - k)) | (m >> k) | (next << (32 - k));
-    }
-    bx[i] = d;
+    const int w = i & (WP - 1), row = i >> lg;
+    const int hz = row / H, hy = row - hz * H;
+    const int y = y0 - r + hy, z = z0 - r + hz;
+    const uint32_t v = (y >= 0 && y < p.dy && z >= 0 && z < p.dz) ? __ldg(plane + ((z * p.dy + y) << lg) + w) : 0u;
+    bx[i] = v;
+    any |= v;
   }
-  __syncthreads();
-  // y: by[hz][y][w] = OR_k bx[hz][y + k][w]
+  // surfaces are sparse in 3-D: a tile with no centre within r writes nothing
+  if (!__syncthreads_or(any != 0u)) return;
   for (int i = threadIdx.x; i < (H * kDilT) << lg; i += blockDim.x) {
     const int w = i & (WP - 1), yz = i >> lg;
     const int y = yz & (kDilT - 1), hz = yz / kDilT;
@@ -243,7 +235,6 @@ __global__ void __launch_bounds__(256) dilate_kernel(KParams p, int r_rt) {
     by[i] = d;
   }
   __syncthreads();
-  // z, then one byte store per set bit (a warp covers 32 consecutive cells)
   for (int row = warp; row < kDilT * kDilT; row += nw) {
     const int z = row / kDilT, y = row & (kDilT - 1);
     const int gy = y0 + y, gz = z0 + z;
@@ -263,23 +254,31 @@ __global__ void __launch_bounds__(256) dilate_kernel(KParams p, int r_rt) {
   }
 }
 
-// Launches the radius-specialised instance (1..4) or the generic one.
-inline void launch_dilate(const KParams& kp, int r, dim3 grid, size_t smem, cudaStream_t st) {
+// Launches K2a and the radius-specialised K2b (1..4) or the generic one.
+inline void launch_dilate(const KParams& kp, int r, int streams, size_t smem, cudaStream_t st) {
+  const int rows = kp.dy * kp.dz;
+  // a single stream gets one row per warp-step of parallelism anyway; batches
+  // amortise the per-warp setup over kDilRowsPerWarp rows
+  const int per_block = 8 * kDilRowsPerWarp;
+  dilate_rows_kernel<<<dim3((rows + per_block - 1) / per_block, streams), 256, 0, st>>>(kp, r);
+  const dim3 grid((kp.dy + kDilT - 1) / kDilT, (kp.dz + kDilT - 1) / kDilT, streams);
   switch (r) {
-    case 1: dilate_kernel<1><<<grid, 256, smem, st>>>(kp, r); break;
-    case 2: dilate_kernel<2><<<grid, 256, smem, st>>>(kp, r); break;
-    case 3: dilate_kernel<3><<<grid, 256, smem, st>>>(kp, r); break;
-    case 4: dilate_kernel<4><<<grid, 256, smem, st>>>(kp, r); break;
-    default: dilate_kernel<0><<<grid, 256, smem, st>>>(kp, r); break;
+    case 1: dilate_tiles_kernel<1><<<grid, 256, smem, st>>>(kp, r); break;
+    case 2: dilate_tiles_kernel<2><<<grid, 256, smem, st>>>(kp, r); break;
+    case 3: dilate_tiles_kernel<3><<<grid, 256, smem, st>>>(kp, r); break;
+    case 4: dilate_tiles_kernel<4><<<grid, 256, smem, st>>>(kp, r); break;
+    default: dilate_tiles_kernel<0><<<grid, 256, smem, st>>>(kp, r); break;
   }
 }
 
-// Opt-in to large dynamic shared memory for every instance.
+// Opt-in to large dynamic shared memory for every K2b instance.
 inline cudaError_t dilate_set_smem(int bytes) {
   cudaError_t e = cudaSuccess;
-  const void* fns[5] = {reinterpret_cast<const void*>(dilate_kernel<0>), reinterpret_cast<const void*>(dilate_kernel<1>),
-                        reinterpret_cast<const void*>(dilate_kernel<2>), reinterpret_cast<const void*>(dilate_kernel<3>),
-                        reinterpret_cast<const void*>(dilate_kernel<4>)};
+  const void* fns[5] = {reinterpret_cast<const void*>(dilate_tiles_kernel<0>),
+                        reinterpret_cast<const void*>(dilate_tiles_kernel<1>),
+                        reinterpret_cast<const void*>(dilate_tiles_kernel<2>),
+                        reinterpret_cast<const void*>(dilate_tiles_kernel<3>),
+                        reinterpret_cast<const void*>(dilate_tiles_kernel<4>)};
   for (const void* f : fns) {
     const cudaError_t x = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (x != cudaSuccess) e = x;
@@ -608,7 +607,15 @@ __global__ void __launch_bounds__(256) trace_per_pixel_kernel(KParams p, int fro
 // ---------------------------------------------------------------------------
 constexpr int kRowsPerWarp = 4;
 
-// merge of 4 packed cells: local l4, occupancy o4 (epoch bytes), 4 keys
+// 0xff in every byte of x that is zero, 0x00 elsewhere (exact, no carries
+// across bytes: each byte's low 7 bits + 0x7f stays within the byte).
+__device__ __forceinline__ uint32_t zero_bytes(uint32_t x) {
+  const uint32_t nonzero = (((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x) & 0x80808080u;
+  return ((nonzero ^ 0x80808080u) >> 7) * 0xffu;
+}
+
+// merge of 4 packed cells: local l4, occupancy o4 (epoch bytes), 4 keys.
+// States are 0..3 per byte, so "== 0" and "== 3" are two-bit tests.
 __device__ __forceinline__ uint32_t merge4(uint32_t l4, uint32_t o4, uint4 k4, uint32_t epoch) {
   const uint32_t kk[4] = {k4.x, k4.y, k4.z, k4.w};
   uint32_t m4 = 0;
@@ -617,12 +624,16 @@ __device__ __forceinline__ uint32_t merge4(uint32_t l4, uint32_t o4, uint4 k4, u
     const uint32_t v = (kk[i] >> kKeyShift) == epoch ? (1u | ((kk[i] & 1u) << 1)) : 0u;  // 1 or 3
     m4 |= v << (8 * i);
   }
-  const uint32_t occm = __vcmpeq4(o4, epoch * 0x01010101u);  // 0xff where Occupied
+  const uint32_t occm = zero_bytes(o4 ^ (epoch * 0x01010101u));  // 0xff where Occupied
   m4 = (m4 & ~occm) | (0x02020202u & occm);
-  const uint32_t keep = __vcmpeq4(m4, 0u);                   // measurement Unknown: keep local
-  const uint32_t clear = __vcmpeq4(m4, 0x03030303u);          // UnknownTraced: -> Unknown
+  const uint32_t keep = (((m4 | (m4 >> 1)) & 0x01010101u) ^ 0x01010101u) * 0xffu;  // m == 0
+  const uint32_t clear = (m4 & (m4 >> 1) & 0x01010101u) * 0xffu;                   // m == 3
   return (l4 & keep) | (m4 & ~(keep | clear));
 }
+
+// number of bytes of x (states 0..3) equal to 2 / to 1
+__device__ __forceinline__ unsigned count_occupied4(uint32_t x) { return __popc((x >> 1) & ~x & 0x01010101u); }
+__device__ __forceinline__ unsigned count_free4(uint32_t x) { return __popc(x & ~(x >> 1) & 0x01010101u); }
 
 __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int rows_per_warp) {
   const int s = blockIdx.y;
@@ -662,8 +673,8 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int r
           out = merge4(*reinterpret_cast<const uint32_t*>(src + sc), *reinterpret_cast<const uint32_t*>(occ + sc),
                        *reinterpret_cast<const uint4*>(key + sc), epoch);
         }
-        occ_n += __popc(__vcmpeq4(out, 0x02020202u)) >> 3;
-        free_n += __popc(__vcmpeq4(out, 0x01010101u)) >> 3;
+        occ_n += count_occupied4(out);
+        free_n += count_free4(out);
         *reinterpret_cast<uint32_t*>(dst + drow + x0) = out;
       }
     } else {

@@ -241,6 +241,7 @@ struct vxm_ctx {
   uint32_t* key = nullptr;
   uint8_t* loc[2] = {nullptr, nullptr};
   double* qtab = nullptr;  // W column + H row back-projection factors
+  uint32_t* dbits = nullptr;  // x-dilated centre bit rows (vox_inf > 0)
   vxm::Counters* counters = nullptr;
   vxm::FrameParams* frames_dev = nullptr;
   float* depth_dev = nullptr;
@@ -313,10 +314,7 @@ void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
   VXM_CK(cudaGetLastError());
   if (kp.vox_inf > 0) {
     const int r = kp.vox_inf;
-    const size_t smem = vxm::dilate_smem_bytes(r, kp.dx);
-    dim3 grid(static_cast<unsigned>((kp.dy + vxm::kDilT - 1) / vxm::kDilT),
-              static_cast<unsigned>((kp.dz + vxm::kDilT - 1) / vxm::kDilT), S);
-    vxm::launch_dilate(kp, r, grid, smem, c->stream);
+    vxm::launch_dilate(kp, r, S, vxm::dilate_smem_bytes(r, kp.dx), c->stream);
     VXM_CK(cudaGetLastError());
   }
   mark(c->ev[2]);
@@ -525,6 +523,7 @@ void destroy_ctx(vxm_ctx* c) {
   cudaFree(c->ctr);
   cudaFree(c->key);
   cudaFree(c->qtab);
+  cudaFree(c->dbits);
   cudaFree(c->loc[0]);
   cudaFree(c->loc[1]);
   cudaFree(c->counters);
@@ -706,9 +705,13 @@ int vxm_create(const vxm_config* cfg, int32_t n_streams, int32_t device, uint32_
     kp.frames = c->frames_dev;
     if (cfg->vox_inf > 0) {
       const size_t smem = vxm::dilate_smem_bytes(cfg->vox_inf, kp.dx);
-      if (cfg->vox_inf > vxm::kMaxVoxInf || smem > 200 * 1024)
-        throw InvalidArg{"vox_inf " + std::to_string(cfg->vox_inf) + " exceeds the dilation tile limit (" +
-                         std::to_string(vxm::kMaxVoxInf) + ")"};
+      if (cfg->vox_inf > vxm::kMaxVoxInf || smem > 200 * 1024 || kp.dx > 1024)
+        throw InvalidArg{"vox_inf " + std::to_string(cfg->vox_inf) + " / dims_x " + std::to_string(kp.dx) +
+                         " exceed the dilation limits (vox_inf <= " + std::to_string(vxm::kMaxVoxInf) +
+                         ", dims_x <= 1024)"};
+      const size_t words = static_cast<size_t>(vxm::dilate_row_words(kp.dx)) * kp.dy * kp.dz * S;
+      VXM_CK(cudaMalloc(&c->dbits, sizeof(uint32_t) * words));
+      kp.dbits = c->dbits;
       VXM_CK(vxm::dilate_set_smem(static_cast<int>(smem)));
     }
     VXM_CK(cudaStreamSynchronize(c->stream));

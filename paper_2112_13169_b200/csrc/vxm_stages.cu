@@ -145,15 +145,15 @@ int vxm_populate_occupied(const vxm_grid_spec* grid, uint8_t* ms, const double* 
     kp.frames = d_frame.p;
     vxm::populate_cloud_kernel<<<dim3(blocks_for(static_cast<long long>(n), 256), 1), 256>>>(kp);
     VXM_SCK(cudaGetLastError());
+    DevBuf<uint32_t> d_bits(vox_inf > 0 ? static_cast<size_t>(vxm::dilate_row_words(kp.dx)) * kp.dy * kp.dz : 0);
     if (vox_inf > 0) {
       const int r = vox_inf;
       const size_t smem = vxm::dilate_smem_bytes(r, kp.dx);
-      if (r > vxm::kMaxVoxInf || smem > 200 * 1024)
-        throw StageError{VXM_EINVAL, "vox_inf exceeds the dilation tile limit"};
+      if (r > vxm::kMaxVoxInf || smem > 200 * 1024 || kp.dx > 1024)
+        throw StageError{VXM_EINVAL, "vox_inf / dims_x exceed the dilation limits (16 / 1024)"};
       VXM_SCK(vxm::dilate_set_smem(static_cast<int>(smem)));
-      dim3 g3(static_cast<unsigned>((kp.dy + vxm::kDilT - 1) / vxm::kDilT),
-              static_cast<unsigned>((kp.dz + vxm::kDilT - 1) / vxm::kDilT), 1);
-      vxm::launch_dilate(kp, r, g3, smem, 0);
+      kp.dbits = d_bits.p;
+      vxm::launch_dilate(kp, r, 1, smem, 0);
       VXM_SCK(cudaGetLastError());
     }
     vxm::decode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_occ.p, d_key.p, d_ms.p, N, kEpoch);
