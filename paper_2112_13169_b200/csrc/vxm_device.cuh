@@ -79,6 +79,10 @@ struct FrameParams {
   const double* ys;
   const double* zs;
   long long n_points;
+  // this stream's occupancy bytes and ray keys (base + s*n); read from memory
+  // so the tracer keeps them in registers instead of rebuilding each address
+  const uint8_t* occ_s;
+  uint32_t* key_s;
   int32_t off[3];     // shift applied after the merge (0,0,0 = none)
   uint32_t epoch;     // 1..255
   uint32_t cur;       // which local buffer holds the current grid

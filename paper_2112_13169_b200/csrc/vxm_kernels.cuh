@@ -361,8 +361,8 @@ __global__ void __launch_bounds__(32) trace_bundle_kernel(KParams p) {
   const int s = blockIdx.y;
   const FrameParams* fp = p.frames + s;
   const uint32_t epoch = fp->epoch;
-  uint32_t* key = p.key + static_cast<long long>(s) * p.n;
-  const uint8_t* occ = p.occ + static_cast<long long>(s) * p.n;
+  uint32_t* const key = fp->key_s;
+  const uint8_t* const occ = fp->occ_s;
   double R[9], start[3];
 #pragma unroll
   for (int i = 0; i < 9; ++i) R[i] = fp->rot[i];
@@ -395,6 +395,62 @@ __global__ void __launch_bounds__(32) trace_bundle_kernel(KParams p) {
   uint32_t traced_bit = 0;
   unsigned freed = 0, traced = 0, skipped = 0;
 
+  // Phase B + C of a chunk: occupancy loads, then the writes in order.
+  auto resolve = [&](const uint32_t (&cell)[kChunk]) {
+    uint32_t o[kChunk];
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j) o[j] = cell[j] != 0xffffffffu ? __ldg(occ + cell[j]) : 0u;
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j) {
+      const bool valid = cell[j] != 0xffffffffu;
+      const bool is_occ = valid && o[j] == epoch;
+      const bool write = valid && !is_occ;
+      traced += (write && traced_bit) ? 1u : 0u;
+      freed += (write && !traced_bit) ? 1u : 0u;
+      const uint32_t kval = ray_key | traced_bit;
+      traced_bit |= is_occ ? 1u : 0u;
+      bool dominated = false;
+      if constexpr (kDedup) {
+        const uint32_t id = write ? cell[j] : (0xfffffff0u - lane);  // idle lanes never match
+        const uint32_t right = __shfl_down_sync(0xffffffffu, id, 1);
+        const uint32_t below = __shfl_down_sync(0xffffffffu, id, 8);
+        dominated = (lane < 31 && right == id) || (lane < 24 && below == id);
+      }
+      if (write && !dominated) atomicMax(key + cell[j], kval);
+    }
+  };
+
+  // The camera (every ray's start) is shared by the whole frame, so this
+  // branch is uniform. Inside the grid the walk needs no per-cell bounds
+  // test: it ends on the first step along an axis whose remaining in-grid
+  // steps are used up.
+  if (x < dx && y < dy && z < dz) {
+    int rem0 = st.step[0] > 0 ? static_cast<int>(dx - 1 - x) : (st.step[0] < 0 ? static_cast<int>(x) : INT_MAX);
+    int rem1 = st.step[1] > 0 ? static_cast<int>(dy - 1 - y) : (st.step[1] < 0 ? static_cast<int>(y) : INT_MAX);
+    int rem2 = st.step[2] > 0 ? static_cast<int>(dz - 1 - z) : (st.step[2] < 0 ? static_cast<int>(z) : INT_MAX);
+    const double d0 = st.tdelta[0], d1 = st.tdelta[1], d2 = st.tdelta[2];
+    while (__any_sync(0xffffffffu, walking)) {
+      uint32_t cell[kChunk];
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) {
+        cell[j] = walking ? static_cast<uint32_t>(idx) : 0xffffffffu;
+        const bool bx = t0 <= t1 && t0 <= t2;
+        const bool by = !bx && t1 <= t2;
+        const double tm = bx ? t0 : (by ? t1 : t2);
+        const int rsel = bx ? rem0 : (by ? rem1 : rem2);
+        walking = walking && !(tm >= stop) && rsel != 0;
+        const bool ax = walking && bx, ay = walking && by, az = walking && !bx && !by;
+        t0 = ax ? dadd(t0, d0) : t0;
+        t1 = ay ? dadd(t1, d1) : t1;
+        t2 = az ? dadd(t2, d2) : t2;
+        idx += ax ? lin0 : (ay ? lin1 : (az ? lin2 : 0));
+        rem0 -= ax ? 1 : 0;
+        rem1 -= ay ? 1 : 0;
+        rem2 -= az ? 1 : 0;
+      }
+      resolve(cell);
+    }
+  } else
   while (__any_sync(0xffffffffu, walking)) {
     uint32_t cell[kChunk];
 #pragma unroll
@@ -426,27 +482,7 @@ __global__ void __launch_bounds__(32) trace_bundle_kernel(KParams p) {
         }
       }
     }
-    uint32_t o[kChunk];
-#pragma unroll
-    for (int j = 0; j < kChunk; ++j) o[j] = cell[j] != 0xffffffffu ? __ldg(occ + cell[j]) : 0u;
-#pragma unroll
-    for (int j = 0; j < kChunk; ++j) {
-      const bool valid = cell[j] != 0xffffffffu;
-      const bool is_occ = valid && o[j] == epoch;
-      const bool write = valid && !is_occ;
-      traced += (write && traced_bit) ? 1u : 0u;
-      freed += (write && !traced_bit) ? 1u : 0u;
-      const uint32_t kval = ray_key | traced_bit;
-      traced_bit |= is_occ ? 1u : 0u;
-      bool dominated = false;
-      if constexpr (kDedup) {
-        const uint32_t id = write ? cell[j] : (0xfffffff0u - lane);  // idle lanes never match
-        const uint32_t right = __shfl_down_sync(0xffffffffu, id, 1);
-        const uint32_t below = __shfl_down_sync(0xffffffffu, id, 8);
-        dominated = (lane < 31 && right == id) || (lane < 24 && below == id);
-      }
-      if (write && !dominated) atomicMax(key + cell[j], kval);
-    }
+    resolve(cell);
   }
   unsigned long long* slot = &p.counters[s].trace_slots[tile % kTraceSlots][0];
   const unsigned r_n = __reduce_add_sync(0xffffffffu, active ? 1u : 0u);

@@ -410,6 +410,8 @@ void prepare_frames(vxm_ctx* c, const vxm_pose* poses, const float* depth_dev_ba
     camera_to_grid(poses[s], org, f.rot, f.trans);
     if (depth_dev_base) f.depth = depth_dev_base + frame_elems * s;
     f.cur = c->cur[s];
+    f.occ_s = c->occ + c->n * s;
+    f.key_s = c->key + c->n * s;
     int32_t off[3];
     const bool moved = shift_decision(c->cfg.grid, org, poses[s].translation, off);
     for (int a = 0; a < 3; ++a) {

@@ -214,6 +214,8 @@ int vxm_trace_bundle(const vxm_grid_spec* grid, uint8_t* ms, const int32_t bundl
     vxm::FrameParams f{};
     fill_pose(f, *t_vc);
     f.epoch = kEpoch;
+    f.occ_s = d_occ.p;
+    f.key_s = d_key.p;
     VXM_SCK(cudaMemcpy(d_frame.p, &f, sizeof(f), cudaMemcpyHostToDevice));
     VXM_SCK(cudaMemcpy(d_ms.p, ms, N, cudaMemcpyHostToDevice));
     VXM_SCK(cudaMemset(d_cnt.p, 0, sizeof(vxm::Counters)));
