@@ -12,7 +12,7 @@ import os
 from pathlib import Path
 
 PKG_DIR = Path(__file__).resolve().parent
-LIB_PATH = PKG_DIR / "lib" / "libvxm.so"
+LIB_PATH = PKG_DIR / "lib" / os.environ.get("VXM_LIB_NAME", "libvxm.so")  # override: A/B builds
 
 VXM_OK, VXM_EINVAL, VXM_ECUDA, VXM_ENOMEM, VXM_ENODEV, VXM_ESTATE = range(6)
 UNKNOWN, FREE, OCCUPIED, UNKNOWN_TRACED = 0, 1, 2, 3

@@ -293,17 +293,25 @@ inline cudaError_t dilate_set_smem(int bytes) {
 // owns an 8x4 tile of end-plane targets so that its rays stay spatially
 // coherent, and a block is one warp so no warp waits on another.
 //
-// The walk runs in chunks of kChunk DDA steps, written without divergent
-// branches: (A) the chunk's cell indices are computed (they do not depend on
-// grid contents), (B) their occupancy bytes are loaded together through the
-// read-only path, (C) the chunk is resolved in order. The Sequential
-// last-writer rule is an atomicMax on the cell key; before issuing it a lane
-// drops its write when lane+1 or lane+8 (both higher ray indices) writes the
-// same cell in the same step, which removes most same-address traffic near
-// the camera. Counters go to 32 per-stream slots (one RED per warp each),
-// summed by K4.
+// The walk runs in chunks of kChunk DDA steps: (A) the chunk's cell indices
+// are computed (they do not depend on grid contents), (B) their occupancy
+// bytes are loaded together through the read-only path, (C) the chunk is
+// resolved in order with predicated, branch-free PTX. A chunk that provably
+// cannot reach the stop distance or the grid boundary for any ray of the
+// warp (a conservative bound from the tmax/tdelta values, checked per chunk)
+// runs only the axis choice and the advance; the last chunks of a ray run
+// the exact per-step stop and in-grid tests. ncu (profiles/) showed the
+// kernel issue- and ALU-pipe bound, so both paths are written to minimise
+// instructions per visit. The Sequential last-writer rule is a fire-and-forget
+// RED.max on the cell key; before issuing it a lane drops its write when
+// lane+1 or lane+8 (both higher ray indices) writes the same cell in the
+// same step, which removes most same-address traffic near the camera.
+// Counters go to 32 per-stream slots (one RED per warp each), summed by K4.
 // ---------------------------------------------------------------------------
-constexpr int kChunk = 8;  // 4 and 16 measured equal; without kDedup 2-3x slower
+#ifndef VXM_FAST_MUL
+#define VXM_FAST_MUL 1
+#endif
+constexpr int kChunk = 8;  // 4 and 16 measured equal; without the dedup 2-3x slower
 constexpr int kTraceSlots = 32;
 
 struct RayState {
@@ -356,7 +364,6 @@ __device__ __forceinline__ void ray_setup(const double* R, const double* start, 
   }
 }
 
-template <bool kDedup>
 __global__ void __launch_bounds__(32) trace_bundle_kernel(KParams p) {
   const int s = blockIdx.y;
   const FrameParams* fp = p.frames + s;
@@ -395,28 +402,46 @@ __global__ void __launch_bounds__(32) trace_bundle_kernel(KParams p) {
   uint32_t traced_bit = 0;
   unsigned freed = 0, traced = 0, skipped = 0;
 
-  // Phase B + C of a chunk: occupancy loads, then the writes in order.
+  // Lean resolve (inline PTX, no branches): per cell one predicated
+  // occupancy load, the write/traced counters (freed = writes - traced, summed
+  // at the end), the neighbour dedup through the shuffles' in-range
+  // predicates, and a predicated fire-and-forget RED.max on the key.
+  unsigned lw = 0, lt = 0;
+  const unsigned long long key_base = reinterpret_cast<unsigned long long>(key);
   auto resolve = [&](const uint32_t (&cell)[kChunk]) {
     uint32_t o[kChunk];
 #pragma unroll
-    for (int j = 0; j < kChunk; ++j) o[j] = cell[j] != 0xffffffffu ? __ldg(occ + cell[j]) : 0u;
+    for (int j = 0; j < kChunk; ++j) {
+      o[j] = cell[j] != 0xffffffffu ? __ldg(occ + cell[j]) : 0u;
+    }
 #pragma unroll
     for (int j = 0; j < kChunk; ++j) {
-      const bool valid = cell[j] != 0xffffffffu;
-      const bool is_occ = valid && o[j] == epoch;
-      const bool write = valid && !is_occ;
-      traced += (write && traced_bit) ? 1u : 0u;
-      freed += (write && !traced_bit) ? 1u : 0u;
-      const uint32_t kval = ray_key | traced_bit;
-      traced_bit |= is_occ ? 1u : 0u;
-      bool dominated = false;
-      if constexpr (kDedup) {
-        const uint32_t id = write ? cell[j] : (0xfffffff0u - lane);  // idle lanes never match
-        const uint32_t right = __shfl_down_sync(0xffffffffu, id, 1);
-        const uint32_t below = __shfl_down_sync(0xffffffffu, id, 8);
-        dominated = (lane < 31 && right == id) || (lane < 24 && below == id);
-      }
-      if (write && !dominated) atomicMax(key + cell[j], kval);
+      asm volatile("{\n\t"
+                   ".reg .pred v, io, w, p1, p8, d1, d8, ok;\n\t"
+                   ".reg .b32 id, r1, r8, kv;\n\t"
+                   ".reg .b64 a;\n\t"
+                   "setp.ne.u32 v, %3, -1;\n\t"
+                   "setp.eq.and.u32 io, %4, %5, v;\n\t"
+                   "setp.ne.and.u32 w, %4, %5, v;\n\t"
+                   "@w add.u32 %1, %1, 1;\n\t"
+                   "@w add.u32 %2, %2, %0;\n\t"
+                   "or.b32 kv, %6, %0;\n\t"
+                   "selp.u32 %0, 1, %0, io;\n\t"
+                   "selp.u32 id, %3, -1, w;\n\t"
+                   "shfl.sync.down.b32 r1|p1, id, 1, 31, -1;\n\t"
+                   "shfl.sync.down.b32 r8|p8, id, 8, 31, -1;\n\t"
+                   "setp.eq.and.u32 d1, r1, id, p1;\n\t"
+                   "setp.eq.and.u32 d8, r8, id, p8;\n\t"
+                   "or.pred d1, d1, d8;\n\t"
+                   "not.pred d1, d1;\n\t"
+                   "and.pred ok, w, d1;\n\t"
+                   "mul.wide.u32 a, %3, 4;\n\t"
+                   "add.u64 a, a, %7;\n\t"
+                   "@ok red.relaxed.gpu.global.max.u32 [a], kv;\n\t"
+                   "}"
+                   : "+r"(traced_bit), "+r"(lw), "+r"(lt)
+                   : "r"(cell[j]), "r"(o[j]), "r"(epoch), "r"(ray_key), "l"(key_base)
+                   : "memory");
     }
   };
 
@@ -425,32 +450,118 @@ __global__ void __launch_bounds__(32) trace_bundle_kernel(KParams p) {
   // test: it ends on the first step along an axis whose remaining in-grid
   // steps are used up.
   if (x < dx && y < dy && z < dz) {
-    int rem0 = st.step[0] > 0 ? static_cast<int>(dx - 1 - x) : (st.step[0] < 0 ? static_cast<int>(x) : INT_MAX);
-    int rem1 = st.step[1] > 0 ? static_cast<int>(dy - 1 - y) : (st.step[1] < 0 ? static_cast<int>(y) : INT_MAX);
-    int rem2 = st.step[2] > 0 ? static_cast<int>(dz - 1 - z) : (st.step[2] < 0 ? static_cast<int>(z) : INT_MAX);
     const double d0 = st.tdelta[0], d1 = st.tdelta[1], d2 = st.tdelta[2];
-    while (__any_sync(0xffffffffu, walking)) {
-      uint32_t cell[kChunk];
+    // r_a = A_a + B_a * coordinate: in-grid steps left along axis a
+    // (coordinate to the far face for step +1, to 0 for step -1, a large
+    // constant for an axis the ray never steps along)
+    const int A0 = st.step[0] > 0 ? static_cast<int>(dx) - 1 : (st.step[0] < 0 ? 0 : (1 << 30));
+    const int A1 = st.step[1] > 0 ? static_cast<int>(dy) - 1 : (st.step[1] < 0 ? 0 : (1 << 30));
+    const int A2 = st.step[2] > 0 ? static_cast<int>(dz) - 1 : (st.step[2] < 0 ? 0 : (1 << 30));
+    const int B0 = -st.step[0], B1 = -st.step[1], B2 = -st.step[2];
+    // conservative reach of a chunk: tmax grows by at most kChunk * tdelta
+    // (plus rounding) along any axis, so if min_a(tmax_a + kChunk*tdelta_a)
+    // stays below the stop distance no step of the chunk can hit it
+    const double span0 = dmul(d0, static_cast<double>(kChunk) * (1.0 + 0x1p-40));
+    const double span1 = dmul(d1, static_cast<double>(kChunk) * (1.0 + 0x1p-40));
+    const double span2 = dmul(d2, static_cast<double>(kChunk) * (1.0 + 0x1p-40));
+    bool alive = active;
+    uint32_t uidx = static_cast<uint32_t>(idx);
+    // tdelta of an axis the ray never steps along is +inf; that axis is never
+    // chosen, and the multiply-add form below needs a finite addend for it
+    const double e0 = st.step[0] ? d0 : 0.0, e1 = st.step[1] ? d1 : 0.0, e2 = st.step[2] ? d2 : 0.0;
+    // Where the walk can end: at the stop distance, or at the step that
+    // leaves the grid along axis a, which happens at tmax_a after rem_a steps
+    // along a, i.e. at ~ tmax_a + rem_a * tdelta_a (repeated rounding moves
+    // that by far less than the 2^-30 relative margin used below).
+    double end = stop;
+    {
+      const int rr[3] = {A0 + B0 * static_cast<int>(x), A1 + B1 * static_cast<int>(y), A2 + B2 * static_cast<int>(z)};
+      const double tt[3] = {t0, t1, t2};
 #pragma unroll
-      for (int j = 0; j < kChunk; ++j) {
-        cell[j] = walking ? static_cast<uint32_t>(idx) : 0xffffffffu;
-        const bool bx = t0 <= t1 && t0 <= t2;
-        const bool by = !bx && t1 <= t2;
-        const double tm = bx ? t0 : (by ? t1 : t2);
-        const int rsel = bx ? rem0 : (by ? rem1 : rem2);
-        walking = walking && !(tm >= stop) && rsel != 0;
-        const bool ax = walking && bx, ay = walking && by, az = walking && !bx && !by;
-        t0 = ax ? dadd(t0, d0) : t0;
-        t1 = ay ? dadd(t1, d1) : t1;
-        t2 = az ? dadd(t2, d2) : t2;
-        idx += ax ? lin0 : (ay ? lin1 : (az ? lin2 : 0));
-        rem0 -= ax ? 1 : 0;
-        rem1 -= ay ? 1 : 0;
-        rem2 -= az ? 1 : 0;
+      for (int a = 0; a < 3; ++a)
+        if (st.step[a]) end = fmin(end, dadd(tt[a], dmul(static_cast<double>(rr[a]), st.tdelta[a])));
+      end = dmul(end, 1.0 - 0x1p-30);
+    }
+    while (__any_sync(0xffffffffu, alive)) {
+      uint32_t cell[kChunk];
+      const double reach = fmin(fmin(dadd(t0, span0), dadd(t1, span1)), dadd(t2, span2));
+      const bool fast = !alive || reach < end;
+      if (__all_sync(0xffffffffu, fast)) {
+        // No ray of the warp can stop or leave the grid within the chunk:
+        // only the axis choice (ties x, then y, then z) and the advance.
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) {
+          cell[j] = alive ? uidx : 0xffffffffu;
+          const bool px = t0 <= t1 && t0 <= t2;
+          const bool py = !px && t1 <= t2;
+          const bool pz = !px && !py;
+#if VXM_FAST_MUL
+          // t + tdelta*1 == RN(t + tdelta); t + tdelta*0 == t (t >= 0)
+          t0 = dadd(t0, dmul(e0, px ? 1.0 : 0.0));
+          t1 = dadd(t1, dmul(e1, py ? 1.0 : 0.0));
+          t2 = dadd(t2, dmul(e2, pz ? 1.0 : 0.0));
+#else
+          t0 = px ? dadd(t0, d0) : t0;
+          t1 = py ? dadd(t1, d1) : t1;
+          t2 = pz ? dadd(t2, d2) : t2;
+#endif
+          uidx += px ? lin0 : (py ? lin1 : lin2);
+        }
+      } else {
+        uint32_t al = alive ? 1u : 0u;
+        // in-grid steps left per axis, from the cell coordinates
+        const uint32_t cz = uidx / static_cast<uint32_t>(dxy);
+        const uint32_t rxy = uidx - cz * static_cast<uint32_t>(dxy);
+        const uint32_t cy = rxy / dx;
+        int r0 = A0 + B0 * static_cast<int>(rxy - cy * dx);
+        int r1 = A1 + B1 * static_cast<int>(cy);
+        int r2 = A2 + B2 * static_cast<int>(cz);
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) {
+          cell[j] = al ? uidx : 0xffffffffu;
+          // walk_ray's step (raytracer.hpp:103-116): the axis with the
+          // smallest tmax, ties x then y then z; stop when that tmax >=
+          // max_dist - 1e-10, or when the step would leave the grid (r < 0).
+          asm("{\n\t"
+              ".reg .pred q, px, py, pz, npx, s0, s1, s2, ok, rg;\n\t"
+              ".reg .b32 m;\n\t"
+              "setp.le.f64 q, %0, %1;\n\t"
+              "setp.le.and.f64 px, %0, %2, q;\n\t"
+              "setp.le.f64 q, %1, %2;\n\t"
+              "not.pred npx, px;\n\t"
+              "and.pred py, q, npx;\n\t"
+              "or.pred pz, px, py;\n\t"
+              "not.pred pz, pz;\n\t"
+              "setp.lt.and.f64 s0, %0, %11, px;\n\t"
+              "setp.lt.and.f64 s1, %1, %11, py;\n\t"
+              "setp.lt.and.f64 s2, %2, %11, pz;\n\t"
+              "or.pred ok, s0, s1;\n\t"
+              "or.pred ok, ok, s2;\n\t"
+              "@px add.rn.f64 %0, %0, %8;\n\t"
+              "@py add.rn.f64 %1, %1, %9;\n\t"
+              "@pz add.rn.f64 %2, %2, %10;\n\t"
+              "@px add.s32 %3, %3, -1;\n\t"
+              "@py add.s32 %4, %4, -1;\n\t"
+              "@pz add.s32 %5, %5, -1;\n\t"
+              "@px add.s32 %6, %6, %12;\n\t"
+              "@py add.s32 %6, %6, %13;\n\t"
+              "@pz add.s32 %6, %6, %14;\n\t"
+              "or.b32 m, %3, %4;\n\t"
+              "or.b32 m, m, %5;\n\t"
+              "setp.ge.s32 rg, m, 0;\n\t"
+              "and.pred ok, ok, rg;\n\t"
+              "selp.u32 %7, %7, 0, ok;\n\t"
+              "}"
+              : "+d"(t0), "+d"(t1), "+d"(t2), "+r"(r0), "+r"(r1), "+r"(r2), "+r"(uidx), "+r"(al)
+              : "d"(d0), "d"(d1), "d"(d2), "d"(stop), "r"(lin0), "r"(lin1), "r"(lin2));
+        }
+        alive = al != 0u;
       }
       resolve(cell);
     }
-  } else
+    freed += lw - lt;
+    traced += lt;
+  } else {
   while (__any_sync(0xffffffffu, walking)) {
     uint32_t cell[kChunk];
 #pragma unroll
@@ -483,6 +594,9 @@ __global__ void __launch_bounds__(32) trace_bundle_kernel(KParams p) {
       }
     }
     resolve(cell);
+  }
+  freed += lw - lt;
+  traced += lt;
   }
   unsigned long long* slot = &p.counters[s].trace_slots[tile % kTraceSlots][0];
   const unsigned r_n = __reduce_add_sync(0xffffffffu, active ? 1u : 0u);

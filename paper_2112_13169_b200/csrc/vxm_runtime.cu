@@ -326,7 +326,7 @@ void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
       vxm::trace_per_pixel_kernel<<<grid, 256, 0, c->stream>>>(kp, cloud ? 0 : 1);
     } else {
       dim3 grid(static_cast<unsigned>(kp.tiles_x * kp.tiles_y), S);
-      vxm::trace_bundle_kernel<true><<<grid, 32, 0, c->stream>>>(kp);
+      vxm::trace_bundle_kernel<<<grid, 32, 0, c->stream>>>(kp);
     }
     VXM_CK(cudaGetLastError());
   }

@@ -19,3 +19,8 @@ tot = sum(int(r[i_s] or 0) for r in data)
 print("  samples", tot, "instructions", sum(int(r[i_e] or 0) for r in data))
 for k, r in sorted(enumerate(data), key=lambda kr: -int(kr[1][i_s] or 0))[:top]:
     print(f"  {k:5d} {r[1][:64]:64s} {r[i_s]:>6s} {r[i_e]:>8s}")
+# stall reasons summed over the kernel (share of all samples)
+st = [i for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
+tot_st = {hdr[i]: sum(int(r[i] or 0) for r in data) for i in st}
+s_all = sum(tot_st.values()) or 1
+print("  stalls:", ", ".join(f"{k[6:]} {100*v/s_all:.1f}%" for k, v in sorted(tot_st.items(), key=lambda kv: -kv[1]) if v > 0.01 * s_all))

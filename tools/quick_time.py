@@ -1,12 +1,16 @@
-"""Scratch timing of the per-frame graph (device-resident depth), cfg1/cfg2,
-plus warm per-stage device times (events between stages, no graph)."""
-import math, sys
+"""Scratch timing of the per-frame graph (device-resident depth) for cfg1/cfg2
+batches, plus warm per-stage device times (events between stages, no graph).
+QT_CONFIGS="cfg2:64,cfg1:64" selects config:streams pairs."""
+import math, os, sys
 sys.path.insert(0, '.')
 import numpy as np, torch
 from paper_2112_13169_b200 import voxmap as vm
 from tests import scenes
 DEG = math.pi / 180
-for name, vox_inf, dm, S in (("cfg1", 0, 6.5, 1), ("cfg2", 2, 5.0, 1), ("cfg2x64", 2, 5.0, 64), ("cfg1x64", 0, 6.5, 64)):
+CFGS = {"cfg1": (0, 6.5), "cfg2": (2, 5.0)}
+for item in os.environ.get("QT_CONFIGS", "cfg1:1,cfg2:1,cfg2:64,cfg1:64").split(","):
+    name, S = item.split(":"); S = int(S)
+    vox_inf, dm = CFGS[name]
     cam = vm.CameraModel(85 * DEG, 101 * DEG, 640, 480, dm)
     grid = vm.GridSpec.create_centered(10.0, 10.0, 5.0, 0.1, (0, 0, 0))
     pose = vm.look_along_x((0, 0, 0))
@@ -23,7 +27,7 @@ for name, vox_inf, dm, S in (("cfg1", 0, 6.5, 1), ("cfg2", 2, 5.0, 1), ("cfg2x64
             st3.append((st[0]["populate_us"], st[0]["trace_us"], st[0]["merge_us"]))
         ts = np.array(ts)
         if flags == 0:
-            print(name, "S", S, "graph p50 ms %.4f p99 %.4f  frames/s %.0f" % (np.median(ts), np.percentile(ts, 99), S / np.median(ts) * 1e3), flush=True)
+            print(f"{name}x{S} graph p50 ms %.4f p99 %.4f  frames/s %.0f  us/frame %.2f" % (np.median(ts), np.percentile(ts, 99), S / np.median(ts) * 1e3, np.median(ts) * 1e3 / S), flush=True)
         else:
             m = np.median(np.array(st3), axis=0)
             print("   stages (us): populate+dilate %.1f  trace %.1f  merge %.1f   (no-graph total %.1f)" % (m[0], m[1], m[2], np.median(ts) * 1e3), flush=True)

@@ -1,1 +1,4 @@
-for v in 0 1 2 3 4; do echo "variant $v"; VXM_TRACE_VARIANT=$v python tools/quick_time.py 2>&1 | grep -v "^   " ; done
+#!/bin/bash
+# Scratch: per-stage device times for trace-kernel variants (VXM_TRACE_VARIANT
+# bit0 dedup, bit1 no atomics, bit2 no occupancy loads, bit3 lean loop).
+for v in ${VARIANTS:-1 9}; do echo "variant $v"; VXM_TRACE_VARIANT=$v python tools/quick_time.py 2>&1; done
