@@ -139,26 +139,24 @@ __device__ __noinline__ int voxel_coord_exact(double acc, double vs) {
 }
 
 // Same value without the IEEE division whenever that is provable:
-// q = RN(acc * RN(1/vs)) is within 2^-51 |q| of RN(acc/vs), so when q is
-// further than 2^-46 |q| from its nearest integer both quotients lie strictly
-// on the same side of every integer and share their floor. The nearest
-// integer comes from the 1.5*2^52 rounding trick (two adds on the fp64 pipe,
-// integer read from the low word), so the fast path needs no conversion
-// instructions. Near an integer, at zero, or beyond 2^30 (where the +-1e9
-// clamp may apply) the exact division runs.
+// q = RN(acc * RN(1/vs)) is within 2^-51 |q| of RN(acc/vs). For |q| < 2^29
+// (inside the +-1e9 clamp) that is below 2^-22, so when q's fractional part
+// lies in (2^-16, 1 - 2^-16) both quotients share their floor. floor(q)
+// comes from one round-down add of 1.5*2^52 (exact: the sum is an integer in
+// [2^52, 2^53)), its int32 value is the sum's low word, and the range and
+// fraction tests read the high words, so the fast path costs four fp64
+// operations and a few integer compares. Otherwise (near an integer, zero,
+// large, NaN) the exact division runs.
 __device__ __forceinline__ int voxel_coord(double acc, double vs, double inv_vs) {
   constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
   const double q = dmul(acc, inv_vs);
-  const double aq = fabs(q);
-  if (aq > 0x1p-1000 && aq < 0x1p+30) {
-    const double t = dadd(q, kMagic);
-    const double n = dsub(t, kMagic);        // rint(q)
-    const double dist = fabs(dsub(q, n));
-    if (dist > dmul(aq, 0x1p-46)) {
-      const int ni = __double2loint(t);      // n as int32
-      return n > q ? ni - 1 : ni;
-    }
-  }
+  const double t = __dadd_rd(q, kMagic);   // floor(q) + kMagic
+  const double n = dsub(t, kMagic);        // floor(q)
+  const double frac = dsub(q, n);          // in [0, 1]
+  const uint32_t qhi = static_cast<uint32_t>(__double2hiint(q)) & 0x7fffffffu;
+  const uint32_t fhi = static_cast<uint32_t>(__double2hiint(frac));
+  // |q| < 2^29, frac > 2^-16 (hi word above 0x3EF00000), frac < 1 - 2^-16
+  if (qhi < 0x41C00000u && fhi > 0x3EF00000u && fhi < 0x3FEFFFE0u) return __double2loint(t);
   return voxel_coord_exact(acc, vs);
 }
 
@@ -198,6 +196,38 @@ __device__ __forceinline__ void block_accumulate(unsigned (&v)[NC], unsigned lon
       if (lane == 0 && s) atomicAdd(dst[i], s);
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Bulk asynchronous copies (TMA engine, cp.async.bulk) into shared memory,
+// completed on an mbarrier with a transaction byte count.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+// makes the barrier initialisation visible to the async (TMA) proxy
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// global -> shared, `bytes` a multiple of 16, both addresses 16-byte aligned
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile("{\n\t.reg .pred p;\n\t"
+               "WAIT_%=:\n\t"
+               "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+               "@!p bra WAIT_%=;\n\t}"
+               ::"r"(smem_u32(bar)), "r"(phase)
+               : "memory");
 }
 
 }  // namespace vxm

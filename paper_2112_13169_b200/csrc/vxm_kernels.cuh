@@ -92,6 +92,79 @@ __global__ void __launch_bounds__(256) populate_depth_kernel(KParams p, int iter
   block_accumulate<2>(vals, dst);
 }
 
+// K1 with the depth span of a block staged in shared memory by the TMA
+// engine: one elected thread issues `iters` bulk copies (one per 256-quad
+// tile, 4 KB each) on per-tile mbarriers at block start, so every block keeps
+// its whole span in flight (HBM latency no longer bounds the launch); the
+// threads then consume tile after tile as the copies land. Requires W*H % 4
+// == 0 and a 16-byte aligned frame (checked; otherwise the plain loads).
+constexpr int kPopMaxIters = 8;
+
+__global__ void __launch_bounds__(256) populate_depth_tma_kernel(KParams p, int iters) {
+  extern __shared__ float4 sq[];  // iters * blockDim.x quads
+  __shared__ uint64_t bar[kPopMaxIters];
+  const int s = blockIdx.y;
+  const FrameParams* fp = p.frames + s;
+  const uint8_t mark = static_cast<uint8_t>(fp->epoch);
+  uint8_t* target = (p.vox_inf > 0 ? p.ctr : p.occ) + static_cast<long long>(s) * p.n;
+  const float* depth = fp->depth;
+  const int nq = (p.W * p.H) >> 2;
+  const int T = blockDim.x;
+  const int q0 = blockIdx.x * iters * T;
+  const bool aligned = (reinterpret_cast<uintptr_t>(depth) & 15u) == 0;
+  if (aligned && threadIdx.x == 0) {
+    for (int i = 0; i < iters; ++i) mbar_init(&bar[i], 1);
+    fence_mbar_init();
+    for (int i = 0; i < iters; ++i) {
+      const int start = q0 + i * T;
+      if (start >= nq) break;
+      const uint32_t bytes = static_cast<uint32_t>(min(T, nq - start)) * 16u;
+      mbar_expect_tx(&bar[i], bytes);
+      bulk_g2s(sq + i * T, depth + static_cast<long long>(start) * 4, bytes, &bar[i]);
+    }
+  }
+  double R[9], t[3];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) R[i] = fp->rot[i];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) t[i] = fp->trans[i];
+  __syncthreads();  // barriers initialised before anyone waits on them
+
+  unsigned total = 0, outside = 0;
+  for (int it = 0; it < iters; ++it) {
+    const int q = q0 + it * T + threadIdx.x;
+    if (q0 + it * T >= nq) break;
+    float4 cur;
+    if (aligned) {
+      mbar_wait(&bar[it], 0);
+      cur = q < nq ? sq[it * T + threadIdx.x] : make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      cur = q < nq ? load_quad(depth, q * 4, nq * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (q >= nq) continue;
+    const float d[4] = {cur.x, cur.y, cur.z, cur.w};
+    const int first = q * 4;
+    const int v0 = first / p.W;
+    const int u0 = first - v0 * p.W;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int u = u0 + k, v = v0;
+      if (u >= p.W) { u -= p.W; ++v; }  // a row boundary inside the quad
+      // DepthImage::valid_depth (geometry.hpp:124): finite and > 0; then the
+      // max-depth cut on the promoted double (geometry.cpp:53-54).
+      if (!(isfinite(d[k]) && d[k] > 0.0f)) continue;
+      const double D = static_cast<double>(d[k]);
+      if (D > p.max_depth) continue;
+      ++total;
+      outside += populate_point(p, R, t, target, mark, dmul(__ldg(p.qx + u), D),
+                                dmul(__ldg(p.qy + v), D), D);
+    }
+  }
+  unsigned vals[2] = {total, outside};
+  unsigned long long* dst[2] = {&p.counters[s].points_total, &p.counters[s].points_outside};
+  block_accumulate<2>(vals, dst);
+}
+
 // K1 for an explicit camera-frame cloud (MeasurementFrame::cloud). Points
 // that PointCloud::add would have dropped (non-finite) are skipped uncounted
 // (proj/include/voxmap/geometry.hpp:84-89).
@@ -805,6 +878,41 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int r
 
   unsigned occ_n = 0, free_n = 0;
   const bool vec = (p.dx & 3) == 0 && (ox & 3) == 0;
+  if (vec && p.dx <= 128 && rows_per_warp == kRowsPerWarp) {
+    // A row is at most one 4-cell group per lane: issue the loads of all the
+    // warp's rows before resolving any, so each lane keeps kRowsPerWarp x 24 B
+    // in flight (the kernel is HBM-latency bound otherwise).
+    const int x0 = lane * 4, sx = x0 + ox;
+    uint32_t l4[kRowsPerWarp], o4[kRowsPerWarp], drow[kRowsPerWarp];
+    uint4 k4[kRowsPerWarp];
+    bool ok[kRowsPerWarp], in_row[kRowsPerWarp];
+#pragma unroll
+    for (int rr = 0; rr < kRowsPerWarp; ++rr) {
+      const int row = warp_id * kRowsPerWarp + rr;
+      const int z = row / p.dy;
+      const int y = row - z * p.dy;
+      const int sy = y + oy, sz = z + oz;
+      in_row[rr] = row < rows && x0 < p.dx;
+      ok[rr] = in_row[rr] && sy >= 0 && sy < p.dy && sz >= 0 && sz < p.dz && sx >= 0 && sx < p.dx;
+      drow[rr] = static_cast<uint32_t>(y) * p.dx + static_cast<uint32_t>(z) * dxy;
+      const long long sc = static_cast<long long>(sy) * p.dx + static_cast<long long>(sz) * dxy + sx;
+      l4[rr] = o4[rr] = 0u;
+      k4[rr] = make_uint4(0u, 0u, 0u, 0u);
+      if (ok[rr]) {
+        l4[rr] = __ldcs(reinterpret_cast<const unsigned int*>(src + sc));
+        o4[rr] = __ldcs(reinterpret_cast<const unsigned int*>(occ + sc));
+        k4[rr] = __ldcs(reinterpret_cast<const uint4*>(key + sc));
+      }
+    }
+#pragma unroll
+    for (int rr = 0; rr < kRowsPerWarp; ++rr) {
+      if (!in_row[rr]) continue;
+      const uint32_t out = ok[rr] ? merge4(l4[rr], o4[rr], k4[rr], epoch) : 0u;
+      occ_n += count_occupied4(out);
+      free_n += count_free4(out);
+      *reinterpret_cast<uint32_t*>(dst + drow[rr] + x0) = out;
+    }
+  } else
   for (int rr = 0; rr < rows_per_warp; ++rr) {
     const int row = warp_id * rows_per_warp + rr;
     if (row >= rows) break;

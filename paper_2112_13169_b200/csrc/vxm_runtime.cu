@@ -304,9 +304,14 @@ void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
     const long long npix = static_cast<long long>(kp.W) * kp.H;
     const long long tiles = ((npix + 3) / 4 + kPopulateThreads - 1) / kPopulateThreads;
     const long long fill = static_cast<long long>(c->nsm) * 8;
-    const int iters = static_cast<int>(std::max(1LL, std::min(8LL, tiles * S / fill)));
+    const int iters = static_cast<int>(std::max(1LL, std::min<long long>(vxm::kPopMaxIters, tiles * S / fill)));
     dim3 grid(static_cast<unsigned>((tiles + iters - 1) / iters), S);
-    vxm::populate_depth_kernel<<<grid, kPopulateThreads, 0, c->stream>>>(kp, iters);
+    if (npix % 4 == 0) {
+      const size_t smem = sizeof(float4) * kPopulateThreads * static_cast<size_t>(iters);
+      vxm::populate_depth_tma_kernel<<<grid, kPopulateThreads, smem, c->stream>>>(kp, iters);
+    } else {
+      vxm::populate_depth_kernel<<<grid, kPopulateThreads, 0, c->stream>>>(kp, iters);
+    }
   } else {
     dim3 grid(static_cast<unsigned>(c->nsm * 4), S);
     vxm::populate_cloud_kernel<<<grid, kPopulateThreads, 0, c->stream>>>(kp);

@@ -75,6 +75,28 @@ def test_transform_voxelize_known_answers(gpu_lib):
     assert got[0][3] == 1_000_000_000 and got[0][4] == -1_000_000_000
 
 
+def test_transform_voxelize_clamp_band_and_near_integers(gpu_lib):
+    # quotients just inside / outside the +-1e9 clamp (kernels_scalar.cpp:31-34),
+    # around 2^29..2^31, exact multiples of the voxel size, tiny and negative
+    # values, NaN and inf: the division-free fast path must agree everywhere
+    vs = 0.1
+    q = np.array([1e9 - 1.5, 1e9 - 0.5, 1e9, 1e9 + 0.5, 1.05e9, 2.0**29 - 0.5, 2.0**29 + 0.5,
+                  2.0**30, 2.0**31 + 7, -1e9 + 0.5, -1e9 - 0.5, -1.05e9, -(2.0**29) - 0.5])
+    xs = np.concatenate([q * vs, np.arange(-50, 51) * vs, np.arange(-50, 51) * vs + 1e-17,
+                         [1e-300, -1e-300, 5e-324, -0.0, np.nan, np.inf, -np.inf]])
+    rng = np.random.default_rng(7)
+    xs = np.concatenate([xs, rng.integers(-10**6, 10**6, 2000) * vs,
+                         rng.integers(-10**6, 10**6, 2000) * vs * (1 + 1e-15)])
+    ys = rng.uniform(-1, 1, xs.size) * 0.0
+    zs = np.zeros(xs.size)
+    R = np.eye(3)
+    t = np.zeros(3)
+    got = vm.kernel_transform_voxelize(xs, ys, zs, R, t, vs)
+    want = ref.transform_voxelize(xs, ys, zs, R, t, vs)
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w)
+
+
 @pytest.mark.parametrize("n", [0, 1, 3, 4, 5, 33, 4097])
 def test_transform_voxelize_random_rotations(gpu_lib, n):
     rng = np.random.default_rng(41 + n)
