@@ -198,6 +198,13 @@ __device__ __forceinline__ void block_accumulate(unsigned (&v)[NC], unsigned lon
   }
 }
 
+// 0xff in every byte of x that is zero, 0x00 elsewhere (exact, no carries
+// across bytes: each byte's low 7 bits + 0x7f stays within the byte).
+__device__ __forceinline__ uint32_t zero_bytes(uint32_t x) {
+  const uint32_t nonzero = (((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x) & 0x80808080u;
+  return ((nonzero ^ 0x80808080u) >> 7) * 0xffu;
+}
+
 // ---------------------------------------------------------------------------
 // Bulk asynchronous copies (TMA engine, cp.async.bulk) into shared memory,
 // completed on an mbarrier with a transaction byte count.

@@ -256,6 +256,71 @@ __global__ void __launch_bounds__(256) dilate_rows_kernel(KParams p, int r) {
   }
 }
 
+// K2a, vector form: a warp packs a group of G consecutive rows whose bytes
+// (G*dx) form whole 16-byte vectors (one 16-byte streaming load per lane,
+// G*dx <= 512). Each lane turns its 16 bytes into a 16-bit mask; lane o < G*WP
+// then assembles word (o & (WP-1)) of row (o / WP) from the masks of the
+// (at most) three lanes covering it, clears the bits past dx, dilates along x
+// with its neighbouring words, and stores it. Used when the stream size and
+// G*dx are multiples of 16 (all benchmark grids); else the per-row kernel.
+__host__ __device__ constexpr int dilate_rows_group(int dx) {
+  // smallest G with G*dx % 16 == 0 (1, 2, 4, 8, 16)
+  int g = 1;
+  while ((g * dx) % 16 != 0) g <<= 1;
+  return g;
+}
+
+__global__ void __launch_bounds__(256) dilate_rows_vec_kernel(KParams p, int r) {
+  const int s = blockIdx.y;
+  const uint32_t e = p.frames[s].epoch;
+  const int lane = threadIdx.x & 31;
+  const int G = dilate_rows_group(p.dx);
+  const int WP = dilate_row_words(p.dx);
+  const int lg = __ffs(WP) - 1;
+  const int W = (p.dx + 31) >> 5;
+  const int rows = p.dy * p.dz;
+  const int row0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * G;
+  if (row0 >= rows) return;
+  const int span = min(G, rows - row0) * p.dx;  // bytes of this group
+  const uint8_t* src = p.ctr + static_cast<long long>(s) * p.n + static_cast<long long>(row0) * p.dx;
+  uint32_t m = 0;  // bit i: byte 16*lane + i holds a centre
+  if (lane * 16 < span) {
+    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(src) + lane);
+    const uint32_t ee = e * 0x01010101u;
+    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t hit = zero_bytes(w4[i] ^ ee) & 0x80808080u;  // 0x80 per matching byte
+      m |= ((hit * 0x00204081u) >> 28) << (4 * i);
+    }
+  }
+  // word j of row k covers group bytes [k*dx + 32j, +32)
+  const int k = lane >> lg, j = lane & (WP - 1);
+  const int b0 = k * p.dx + 32 * j;
+  const int L0 = b0 >> 4, off = b0 & 15;
+  const uint32_t m0 = __shfl_sync(0xffffffffu, m, L0 & 31);
+  const uint32_t m1 = __shfl_sync(0xffffffffu, m, (L0 + 1) & 31);
+  const uint32_t m2 = __shfl_sync(0xffffffffu, m, (L0 + 2) & 31);
+  const unsigned long long win = static_cast<unsigned long long>(m0) | (static_cast<unsigned long long>(m1) << 16) |
+                                 (static_cast<unsigned long long>(m2) << 32);
+  const int valid = min(32, p.dx - 32 * j);  // cells of this word inside the row
+  uint32_t w = j < W ? static_cast<uint32_t>(win >> off) : 0u;
+  if (valid < 32) w &= valid > 0 ? (1u << valid) - 1u : 0u;
+  uint32_t d = w;
+  if (__any_sync(0xffffffffu, w != 0u)) {
+    const uint32_t prev = __shfl_up_sync(0xffffffffu, w, 1);
+    const uint32_t next = __shfl_down_sync(0xffffffffu, w, 1);
+    const uint32_t pv = j > 0 ? prev : 0u;
+    const uint32_t nx = j + 1 < WP ? next : 0u;
+    for (int q = 1; q <= r; ++q) d |= (w << q) | (pv >> (32 - q)) | (w >> q) | (nx << (32 - q));
+    if (valid < 32) d &= valid > 0 ? (1u << valid) - 1u : 0u;
+  }
+  if (k < G && row0 + k < rows) {
+    uint32_t* plane = p.dbits + static_cast<long long>(s) * rows * WP;
+    plane[static_cast<uint32_t>(row0 + k) * WP + j] = d;
+  }
+}
+
 // Shared memory of K2b: the (8+2r)^2 halo bit rows and the y-dilated rows.
 __host__ __device__ constexpr size_t dilate_smem_bytes(int r, int dx) {
   return sizeof(uint32_t) * static_cast<size_t>(dilate_row_words(dx)) *
@@ -332,8 +397,14 @@ inline void launch_dilate(const KParams& kp, int r, int streams, size_t smem, cu
   const int rows = kp.dy * kp.dz;
   // a single stream gets one row per warp-step of parallelism anyway; batches
   // amortise the per-warp setup over kDilRowsPerWarp rows
-  const int per_block = 8 * kDilRowsPerWarp;
-  dilate_rows_kernel<<<dim3((rows + per_block - 1) / per_block, streams), 256, 0, st>>>(kp, r);
+  const int G = dilate_rows_group(kp.dx);
+  if (kp.n % 16 == 0 && G * kp.dx <= 512 && G * dilate_row_words(kp.dx) <= 32) {
+    const int per_block = 8 * G;
+    dilate_rows_vec_kernel<<<dim3((rows + per_block - 1) / per_block, streams), 256, 0, st>>>(kp, r);
+  } else {
+    const int per_block = 8 * kDilRowsPerWarp;
+    dilate_rows_kernel<<<dim3((rows + per_block - 1) / per_block, streams), 256, 0, st>>>(kp, r);
+  }
   const dim3 grid((kp.dy + kDilT - 1) / kDilT, (kp.dz + kDilT - 1) / kDilT, streams);
   switch (r) {
     case 1: dilate_tiles_kernel<1><<<grid, 256, smem, st>>>(kp, r); break;
@@ -829,13 +900,6 @@ __global__ void __launch_bounds__(256) trace_per_pixel_kernel(KParams p, int fro
 // intrinsics; otherwise a per-cell path runs.
 // ---------------------------------------------------------------------------
 constexpr int kRowsPerWarp = 4;
-
-// 0xff in every byte of x that is zero, 0x00 elsewhere (exact, no carries
-// across bytes: each byte's low 7 bits + 0x7f stays within the byte).
-__device__ __forceinline__ uint32_t zero_bytes(uint32_t x) {
-  const uint32_t nonzero = (((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x) & 0x80808080u;
-  return ((nonzero ^ 0x80808080u) >> 7) * 0xffu;
-}
 
 // merge of 4 packed cells: local l4, occupancy o4 (epoch bytes), 4 keys.
 // States are 0..3 per byte, so "== 0" and "== 3" are two-bit tests.

@@ -129,6 +129,27 @@ def test_populate_matches_reference(gpu_lib, vox_inf):
         assert np.array_equal(ms_gpu, ms_ref)
 
 
+@pytest.mark.parametrize("dims", [(100, 20, 10), (200, 8, 6), (20, 30, 12), (36, 10, 9), (33, 12, 7),
+                                  (64, 5, 5), (96, 7, 3), (8, 9, 10), (4, 4, 4)])
+@pytest.mark.parametrize("vox_inf", [1, 2, 5])
+def test_populate_dilation_row_layouts(gpu_lib, dims, vox_inf):
+    # row lengths that take the vector row-packing path (G*dx a multiple of 16,
+    # 1..8 words per row) and ones that fall back to the per-row kernel
+    rng = np.random.default_rng(sum(dims) + vox_inf)
+    vox = 0.1
+    grid = vm.GridSpec.create(dims[0] * vox, dims[1] * vox, dims[2] * vox, vox)
+    assert tuple(grid.dims) == dims
+    for n in (1, 50, 3000):
+        xs, ys, zs = (rng.uniform(-0.3, d * vox + 0.3, n) for d in dims)
+        pose = vm.identity_pose()
+        ms_ref = np.zeros(grid.cell_count(), dtype=np.uint8)
+        ms_gpu = ms_ref.copy()
+        st_ref = ref.populate(grid.c, ms_ref, xs, ys, zs, pose, vox_inf)
+        st_gpu = vm.populate_occupied(grid, ms_gpu, xs, ys, zs, pose, vox_inf)
+        assert st_gpu == st_ref
+        assert np.array_equal(ms_gpu, ms_ref)
+
+
 def test_populate_never_clears_and_is_idempotent(gpu_lib):
     # test_integrator.cpp:107-137
     grid = vm.GridSpec.create(1.5, 1.5, 1.5, 0.15)
