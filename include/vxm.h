@@ -141,8 +141,19 @@ typedef struct vxm_ctx vxm_ctx;
  * PipelineConfig::validate (pipeline.cpp:33-42). */
 int vxm_create(const vxm_config* cfg, int32_t n_streams, int32_t device, uint32_t flags,
                vxm_ctx** out);
+/* Multi-frame pipelining (no reference counterpart; SURVEY.md §8f "next" #1):
+ * each call takes frames_per_call (F, 1..64) CONSECUTIVE frames of every
+ * stream, stream-major (frame k of stream s at index s*F + k, for depth
+ * frames, poses and stats alike). Results equal F successive integrate
+ * calls bit for bit: the measurement grid origins depend only on the poses
+ * (pipeline.cpp:84,102-112), so populate and the ray casts of all F frames
+ * run as independent slots, and one chain kernel folds the F merges and
+ * shifts in order, producing every frame's counts. vxm_create == F = 1. */
+int vxm_create_multi(const vxm_config* cfg, int32_t n_streams, int32_t frames_per_call,
+                     int32_t device, uint32_t flags, vxm_ctx** out);
 int vxm_destroy(vxm_ctx* ctx);
 int vxm_num_streams(const vxm_ctx* ctx);
+int vxm_frames_per_call(const vxm_ctx* ctx);
 
 /* MappingPipeline::integrate for a depth frame:
  * integrate(MeasurementFrame{depth_to_cloud(img, cam), t_wc}) with the

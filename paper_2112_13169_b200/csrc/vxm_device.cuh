@@ -86,6 +86,11 @@ struct FrameParams {
   int32_t off[3];     // shift applied after the merge (0,0,0 = none)
   uint32_t epoch;     // 1..255
   uint32_t cur;       // which local buffer holds the current grid
+  // multi-frame calls (frames_per_call > 1), first slot of a stream only:
+  // the box of chain coordinates g = cell + P_k (P_k = sum of the shifts of
+  // frames 0..k) that some frame's grid covers (merge_sequence_kernel)
+  int32_t box_lo[3];
+  int32_t box_ext[3];
   uint32_t pad_;
 };
 

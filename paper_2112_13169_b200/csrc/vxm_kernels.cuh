@@ -1020,4 +1020,121 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int r
   block_accumulate<2>(vals, dsts);
 }
 
+
+// ---------------------------------------------------------------------------
+// K4 for F > 1 consecutive frames of each stream in one call (SURVEY §8f
+// "next" #1: populate and trace of all F frames run as F independent slots,
+// only the merge + shift is a chain). Frame k merges its measurement grid
+// into the local grid and then shifts it by off_k (pipeline.cpp:99-112), so
+// the value that ends at cell c_k after frame k came from c_{k-1} = c_k +
+// off_k: along such a chain g = c_k + P_k (P_k = off_0 + ... + off_k,
+// P_{-1} = 0) is invariant. Every (frame, cell) lies on exactly one chain, so
+// one thread per chain folds the F merges in order, exactly as F K4 launches
+// would, without materialising the intermediate grids:
+//   v_k(c_k) = inb(c_{k-1}) ? merge(v_{k-1}(c_{k-1}), ms_k(c_{k-1})) : Unknown
+// and counts Occupied / Free of every intermediate grid (the per-frame
+// PipelineStats counts, pipeline.cpp:114-115). The chains of a stream span
+// the box [min P, max P + dims) (host-computed, FrameParams::box_*); a
+// grid-stride loop covers it, so the captured launch shape never changes.
+// ---------------------------------------------------------------------------
+constexpr int kMaxFramesPerCall = 64;
+
+__global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
+  constexpr int U = 4;  // frames whose loads are issued together
+  __shared__ unsigned long long cnt[kMaxFramesPerCall];     // occupied | freed << 32
+  __shared__ int Pc[kMaxFramesPerCall + U][3];              // P_{k-1} at index k
+  __shared__ uint32_t ep[kMaxFramesPerCall];
+  const int s = blockIdx.y;  // stream
+  const FrameParams* f0 = p.frames + static_cast<long long>(s) * F;
+  const int lane = threadIdx.x & 31;
+  for (int k = threadIdx.x; k < kMaxFramesPerCall; k += blockDim.x) cnt[k] = 0ull;
+  if (threadIdx.x == 0) {
+    int P[3] = {0, 0, 0};
+    for (int k = 0; k <= F; ++k) {
+      for (int a = 0; a < 3; ++a) Pc[k][a] = P[a];
+      if (k < F) {
+        for (int a = 0; a < 3; ++a) P[a] += f0[k].off[a];
+        ep[k] = f0[k].epoch;
+      }
+    }
+  }
+  if (blockIdx.x == 0) {
+    // fold the trace counters of every frame slot of this stream (one warp each)
+    for (int k = threadIdx.x >> 5; k < F; k += blockDim.x >> 5) fold_trace_slots(p.counters[static_cast<long long>(s) * F + k]);
+  }
+  __syncthreads();
+  const int dx = p.dx, dy = p.dy, dz = p.dz;
+  const int dxy = dx * dy;
+  const int bx = f0->box_lo[0], by = f0->box_lo[1], bz = f0->box_lo[2];
+  const int ex = f0->box_ext[0], ey = f0->box_ext[1], ez = f0->box_ext[2];
+  const long long nchain = static_cast<long long>(ex) * ey * ez;
+  const uint32_t cur = f0->cur;
+  const uint8_t* src = (cur ? p.loc1 : p.loc0) + static_cast<long long>(s) * p.n;
+  uint8_t* dst = (cur ? p.loc0 : p.loc1) + static_cast<long long>(s) * p.n;
+  const uint8_t* occ0 = p.occ + static_cast<long long>(s) * F * p.n;
+  const uint32_t* key0 = p.key + static_cast<long long>(s) * F * p.n;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long base = static_cast<long long>(blockIdx.x) * blockDim.x; base < nchain; base += stride) {
+    const long long i = base + threadIdx.x;
+    const bool active = i < nchain;
+    const int iz = static_cast<int>(i / (static_cast<long long>(ex) * ey));
+    const int rem = static_cast<int>(i - static_cast<long long>(iz) * ex * ey);
+    const int iy = rem / ex;
+    const int gx = bx + rem - iy * ex, gy = by + iy, gz = bz + iz;
+    auto cell_of = [&](int k, bool& in) {  // c_{k-1} = g - P_{k-1}
+      const int cx = gx - Pc[k][0], cy = gy - Pc[k][1], cz = gz - Pc[k][2];
+      in = active && static_cast<unsigned>(cx) < static_cast<unsigned>(dx) &&
+           static_cast<unsigned>(cy) < static_cast<unsigned>(dy) && static_cast<unsigned>(cz) < static_cast<unsigned>(dz);
+      return cx + cy * dx + cz * dxy;
+    };
+    bool in_prev;
+    int pos_prev = cell_of(0, in_prev);
+    uint32_t val = in_prev ? src[pos_prev] : 0u;
+    for (int k0 = 0; k0 < F; k0 += U) {
+      // positions after frames k0..k0+U-1, then all their loads, then the merges
+      bool in_c[U];
+      int pos[U];
+      uint32_t o[U], kk[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) pos[u] = cell_of(k0 + u + 1, in_c[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool in_r = u == 0 ? in_prev : in_c[u - 1];
+        const int r = u == 0 ? pos_prev : pos[u - 1];
+        const bool ld = k0 + u < F && in_c[u] && in_r;
+        const long long off = static_cast<long long>(k0 + u) * p.n + r;
+        o[u] = ld ? __ldcs(occ0 + off) : 0u;
+        kk[u] = ld ? __ldcs(key0 + off) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = k0 + u;
+        if (k >= F) break;
+        const bool in_r = u == 0 ? in_prev : in_c[u - 1];
+        if (in_c[u]) val = in_r ? merge_cell(val, decode_cell(o[u], kk[u], ep[k])) : 0u;  // shifted in: Unknown
+        const unsigned long long both = !in_c[u] ? 0ull : (val == 2u ? 1ull : (val == 1u ? (1ull << 32) : 0ull));
+        const unsigned long long w = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(both)) |
+                                     (static_cast<unsigned long long>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(both >> 32))) << 32);
+        if (lane == 0 && w) atomicAdd(&cnt[k], w);
+      }
+      // position after the group's last frame (F may end inside the group)
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (k0 + u < F) {
+          in_prev = in_c[u];
+          pos_prev = pos[u];
+        }
+      }
+    }
+    if (in_prev) dst[pos_prev] = static_cast<uint8_t>(val);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < F; k += blockDim.x) {
+    Counters& c = p.counters[static_cast<long long>(s) * F + k];
+    const unsigned long long v = cnt[k];
+    if (v & 0xffffffffull) atomicAdd(&c.occupied, v & 0xffffffffull);
+    if (v >> 32) atomicAdd(&c.freed, v >> 32);
+  }
+}
+
 }  // namespace vxm

@@ -226,7 +226,9 @@ void vxm_set_error(const char* msg) { g_err = msg ? msg : ""; }
 // ---------------------------------------------------------------------------
 struct vxm_ctx {
   vxm_config cfg{};
-  int S = 1;
+  int S = 1;       // independent sensor streams
+  int F = 1;       // consecutive frames of each stream per call
+  int nslots = 1;  // S * F measurement grids (slot = s * F + k)
   int device = 0;
   uint32_t flags = 0;
   int nsm = 148;
@@ -267,8 +269,9 @@ struct vxm_ctx {
   std::vector<uint32_t> epoch;
   std::vector<uint32_t> cur;
   std::vector<double> origin;  // 3 per stream
-  std::vector<int32_t> last_off;
-  std::vector<int32_t> last_shifted;
+  std::vector<int32_t> last_off;      // per slot
+  std::vector<int32_t> last_shifted;  // per slot
+  std::vector<double> origin_after;   // per slot: local origin after that frame
 
   cudaGraphExec_t graph_depth = nullptr;
   cudaGraphExec_t graph_cloud = nullptr;
@@ -290,7 +293,7 @@ namespace {
 // capturing: inside stream capture the stage events must be recorded as
 // external event-record nodes (a plain record only adds a dependency edge).
 void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
-  const int S = c->S;
+  const int S = c->nslots;  // K1-K3 run on every frame slot
   vxm::KParams kp = c->kp;
   auto mark = [&](cudaEvent_t e) {
     VXM_CK(capturing ? cudaEventRecordWithFlags(e, c->stream, cudaEventRecordExternal)
@@ -336,7 +339,7 @@ void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
     VXM_CK(cudaGetLastError());
   }
   mark(c->ev[3]);
-  {
+  if (c->F == 1) {
     const long long rows = static_cast<long long>(kp.dy) * kp.dz;
     // one row per warp unless the batch fills the GPU several times over
     const long long warps = rows * S;
@@ -346,9 +349,18 @@ void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
     dim3 grid(static_cast<unsigned>((rows + rows_per_block - 1) / rows_per_block), S);
     vxm::merge_shift_count_kernel<<<grid, kMergeThreads, 0, c->stream>>>(kp, rpw);
     VXM_CK(cudaGetLastError());
+  } else {
+    // chains of F frames per stream; the chain box varies per call, so the
+    // launch covers it with a fixed grid-stride shape
+    const long long chains = c->n * 2;
+    const long long blocks = std::min<long long>((chains + kMergeThreads - 1) / kMergeThreads,
+                                                 std::max<long long>(1, c->nsm * 8LL / c->S));
+    dim3 grid(static_cast<unsigned>(std::max<long long>(1, blocks)), c->S);
+    vxm::merge_sequence_kernel<<<grid, kMergeThreads, 0, c->stream>>>(kp, c->F);
+    VXM_CK(cudaGetLastError());
   }
   mark(c->ev[4]);
-  VXM_CK(cudaMemcpyAsync(c->counters_host, c->counters, sizeof(vxm::Counters) * S,
+  VXM_CK(cudaMemcpyAsync(c->counters_host, c->counters, sizeof(vxm::Counters) * c->nslots,
                          cudaMemcpyDeviceToHost, c->stream));
 }
 
@@ -400,42 +412,56 @@ void apply_stage_events(vxm_ctx* c, cudaGraphExec_t exec, int gi) {
 void next_slot(vxm_ctx* c) {
   c->ring_slot = (c->ring_slot + 1) % vxm_ctx::kRing;
   VXM_CK(cudaEventSynchronize(c->ring_ev[c->ring_slot]));
-  c->frames_host = c->frames_ring + static_cast<size_t>(c->ring_slot) * c->S;
+  c->frames_host = c->frames_ring + static_cast<size_t>(c->ring_slot) * c->nslots;
 }
 
 void prepare_frames(vxm_ctx* c, const vxm_pose* poses, const float* depth_dev_base,
                     size_t frame_elems) {
-  for (int s = 0; s < c->S; ++s) {
-    if (!pose_valid(poses[s], 1e-6)) throw InvalidArg{"MeasurementFrame: invalid transform"};
+  for (int i = 0; i < c->nslots; ++i) {
+    if (!pose_valid(poses[i], 1e-6)) throw InvalidArg{"MeasurementFrame: invalid transform"};
   }
   for (int s = 0; s < c->S; ++s) {
-    vxm::FrameParams& f = c->frames_host[s];
     double* org = &c->origin[3 * s];
-    // the measurement grid takes the local grid's pre-shift origin (pipeline.cpp:84-85)
-    camera_to_grid(poses[s], org, f.rot, f.trans);
-    if (depth_dev_base) f.depth = depth_dev_base + frame_elems * s;
-    f.cur = c->cur[s];
-    f.occ_s = c->occ + c->n * s;
-    f.key_s = c->key + c->n * s;
-    int32_t off[3];
-    const bool moved = shift_decision(c->cfg.grid, org, poses[s].translation, off);
+    int32_t P[3] = {0, 0, 0}, lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    for (int k = 0; k < c->F; ++k) {
+      const int slot = s * c->F + k;
+      vxm::FrameParams& f = c->frames_host[slot];
+      // the measurement grid takes the local grid's pre-shift origin (pipeline.cpp:84-85)
+      camera_to_grid(poses[slot], org, f.rot, f.trans);
+      if (depth_dev_base) f.depth = depth_dev_base + frame_elems * slot;
+      f.cur = c->cur[s];
+      f.occ_s = c->occ + c->n * slot;
+      f.key_s = c->key + c->n * slot;
+      int32_t off[3];
+      const bool moved = shift_decision(c->cfg.grid, org, poses[slot].translation, off);
+      for (int a = 0; a < 3; ++a) {
+        f.off[a] = off[a];
+        c->last_off[3 * slot + a] = off[a];
+        c->origin_after[3 * slot + a] = org[a];
+        P[a] += off[a];
+        lo[a] = std::min(lo[a], P[a]);
+        hi[a] = std::max(hi[a], P[a]);
+      }
+      c->last_shifted[slot] = moved ? 1 : 0;
+      // epoch-tagged cells need no per-frame reset; the 8-bit epoch wraps
+      // every 255 frames, when this slot's arrays are cleared once
+      if (c->epoch[slot] >= vxm::kMaxEpoch) {
+        VXM_CK(cudaMemsetAsync(c->occ + c->n * slot, 0, c->n, c->stream));
+        if (c->ctr) VXM_CK(cudaMemsetAsync(c->ctr + c->n * slot, 0, c->n, c->stream));
+        VXM_CK(cudaMemsetAsync(c->key + c->n * slot, 0, sizeof(uint32_t) * c->n, c->stream));
+        c->epoch[slot] = 0;
+      }
+      c->epoch[slot] += 1;
+      f.epoch = c->epoch[slot];
+    }
+    // chain box of the stream (merge_sequence_kernel): g in [min P, max P + dims)
+    vxm::FrameParams& f0 = c->frames_host[s * c->F];
     for (int a = 0; a < 3; ++a) {
-      f.off[a] = off[a];
-      c->last_off[3 * s + a] = off[a];
+      f0.box_lo[a] = lo[a];
+      f0.box_ext[a] = hi[a] - lo[a] + c->cfg.grid.dims[a];
     }
-    c->last_shifted[s] = moved ? 1 : 0;
-    // epoch-tagged cells need no per-frame reset; the 8-bit epoch wraps
-    // every 255 frames, when this stream's arrays are cleared once
-    if (c->epoch[s] >= vxm::kMaxEpoch) {
-      VXM_CK(cudaMemsetAsync(c->occ + c->n * s, 0, c->n, c->stream));
-      if (c->ctr) VXM_CK(cudaMemsetAsync(c->ctr + c->n * s, 0, c->n, c->stream));
-      VXM_CK(cudaMemsetAsync(c->key + c->n * s, 0, sizeof(uint32_t) * c->n, c->stream));
-      c->epoch[s] = 0;
-    }
-    c->epoch[s] += 1;
-    f.epoch = c->epoch[s];
   }
-  VXM_CK(cudaMemcpyAsync(c->frames_dev, c->frames_host, sizeof(vxm::FrameParams) * c->S,
+  VXM_CK(cudaMemcpyAsync(c->frames_dev, c->frames_host, sizeof(vxm::FrameParams) * c->nslots,
                          cudaMemcpyHostToDevice, c->stream));
   VXM_CK(cudaEventRecord(c->ring_ev[c->ring_slot], c->stream));
 }
@@ -481,7 +507,7 @@ void collect_stats(vxm_ctx* c, vxm_stats* out) {
     c->pending = false;
   }
   if (!out) return;
-  for (int s = 0; s < c->S; ++s) {
+  for (int s = 0; s < c->nslots; ++s) {
     const vxm::Counters& k = c->counters_host[s];
     vxm_stats& o = out[s];
     std::memset(&o, 0, sizeof(o));
@@ -496,7 +522,7 @@ void collect_stats(vxm_ctx* c, vxm_stats* out) {
     o.shifted = c->last_shifted[s];
     for (int a = 0; a < 3; ++a) {
       o.shift_offset[a] = c->last_off[3 * s + a];
-      o.origin[a] = c->origin[3 * s + a];
+      o.origin[a] = c->origin_after[3 * s + a];
     }
     o.populate_us = c->stage_us[0];
     o.trace_us = c->stage_us[1];
@@ -615,11 +641,18 @@ int vxm_bundle_dimensions(const vxm_camera* cam, double depth, double vs, int32_
 
 int vxm_create(const vxm_config* cfg, int32_t n_streams, int32_t device, uint32_t flags,
                vxm_ctx** out) {
-  *out = nullptr;
+  return vxm_create_multi(cfg, n_streams, 1, device, flags, out);
+}
+
+int vxm_create_multi(const vxm_config* cfg, int32_t n_streams, int32_t frames_per_call,
+                     int32_t device, uint32_t flags, vxm_ctx** out) {
+  if (out) *out = nullptr;
   vxm_ctx* c = nullptr;
   const int rc = guarded([&] {
-    if (!cfg) throw InvalidArg{"null config"};
+    if (!cfg || !out) throw InvalidArg{"null argument"};
     if (n_streams < 1) throw InvalidArg{"n_streams must be >= 1"};
+    if (frames_per_call < 1 || frames_per_call > vxm::kMaxFramesPerCall)
+      throw InvalidArg{"frames_per_call must lie in [1, " + std::to_string(vxm::kMaxFramesPerCall) + "]"};
     validate_config(*cfg);
     check_device(device);
     VXM_CK(cudaSetDevice(device));
@@ -627,6 +660,8 @@ int vxm_create(const vxm_config* cfg, int32_t n_streams, int32_t device, uint32_
     c->device = device;
     c->cfg = *cfg;
     c->S = n_streams;
+    c->F = frames_per_call;
+    c->nslots = n_streams * frames_per_call;
     c->flags = flags;
     c->nsm = sm_count(device);
     const vxm_grid_spec& g = cfg->grid;
@@ -638,7 +673,8 @@ int vxm_create(const vxm_config* cfg, int32_t n_streams, int32_t device, uint32_
 
     VXM_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     for (auto& e : c->ev) VXM_CK(cudaEventCreate(&e));
-    const size_t S = static_cast<size_t>(n_streams);
+    const size_t S = static_cast<size_t>(c->nslots);  // measurement-grid slots
+    const size_t NS = static_cast<size_t>(n_streams);  // local grids
     const size_t npix = static_cast<size_t>(cfg->camera.width) * cfg->camera.height;
     VXM_CK(cudaMalloc(&c->occ, c->n * S));
     VXM_CK(cudaMemsetAsync(c->occ, 0, c->n * S, c->stream));
@@ -649,8 +685,8 @@ int vxm_create(const vxm_config* cfg, int32_t n_streams, int32_t device, uint32_
       VXM_CK(cudaMemsetAsync(c->ctr, 0, c->n * S, c->stream));
     }
     for (int b = 0; b < 2; ++b) {
-      VXM_CK(cudaMalloc(&c->loc[b], c->n * S));
-      VXM_CK(cudaMemsetAsync(c->loc[b], 0, c->n * S, c->stream));
+      VXM_CK(cudaMalloc(&c->loc[b], c->n * NS));
+      VXM_CK(cudaMemsetAsync(c->loc[b], 0, c->n * NS, c->stream));
     }
     VXM_CK(cudaMalloc(&c->counters, sizeof(vxm::Counters) * S));
     VXM_CK(cudaMalloc(&c->frames_dev, sizeof(vxm::FrameParams) * S));
@@ -662,12 +698,15 @@ int vxm_create(const vxm_config* cfg, int32_t n_streams, int32_t device, uint32_
     VXM_CK(cudaMallocHost(&c->counters_host, sizeof(vxm::Counters) * S));
     std::memset(c->counters_host, 0, sizeof(vxm::Counters) * S);
     c->epoch.assign(S, 0);
-    c->cur.assign(S, 0);
-    c->origin.resize(3 * S);
+    c->cur.assign(NS, 0);
+    c->origin.resize(3 * NS);
     c->last_off.assign(3 * S, 0);
     c->last_shifted.assign(S, 0);
-    for (size_t s = 0; s < S; ++s)
+    c->origin_after.resize(3 * S);
+    for (size_t s = 0; s < NS; ++s)
       for (int a = 0; a < 3; ++a) c->origin[3 * s + a] = g.origin[a];
+    for (size_t s = 0; s < S; ++s)
+      for (int a = 0; a < 3; ++a) c->origin_after[3 * s + a] = g.origin[a];
 
     vxm::KParams& kp = c->kp;
     kp.dx = g.dims[0];
@@ -738,6 +777,8 @@ int vxm_destroy(vxm_ctx* ctx) {
 
 int vxm_num_streams(const vxm_ctx* ctx) { return ctx ? ctx->S : 0; }
 
+int vxm_frames_per_call(const vxm_ctx* ctx) { return ctx ? ctx->F : 0; }
+
 void* vxm_cuda_stream(vxm_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
 
 int vxm_last_frame_ms(vxm_ctx* ctx, float* ms) {
@@ -756,7 +797,7 @@ int vxm_integrate_depth(vxm_ctx* ctx, const float* depth, const vxm_pose* t_wc, 
     prepare_frames(ctx, t_wc, ctx->depth_dev, frame);
     // pinned host buffers go straight to the copy engine; pageable ones are
     // staged by the driver
-    VXM_CK(cudaMemcpyAsync(ctx->depth_dev, depth, sizeof(float) * frame * ctx->S,
+    VXM_CK(cudaMemcpyAsync(ctx->depth_dev, depth, sizeof(float) * frame * ctx->nslots,
                            cudaMemcpyHostToDevice, ctx->stream));
     run_frame(ctx, false);
     collect_stats(ctx, stats);
@@ -782,7 +823,7 @@ int vxm_integrate_depth_async(vxm_ctx* ctx, const float* depth, const vxm_pose* 
     if (!ctx || !depth || !t_wc) throw InvalidArg{"null argument"};
     VXM_CK(cudaSetDevice(ctx->device));
     const size_t frame = static_cast<size_t>(ctx->kp.W) * ctx->kp.H;
-    const size_t bytes = sizeof(float) * frame * ctx->S;
+    const size_t bytes = sizeof(float) * frame * ctx->nslots;
     if (!ctx->copy_stream) {
       VXM_CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
       for (int b = 0; b < 2; ++b) {
@@ -824,7 +865,7 @@ int vxm_integrate_cloud(vxm_ctx* ctx, const double* xs, const double* ys, const 
                         size_t n, const vxm_pose* t_wc, vxm_stats* stats) {
   return guarded([&] {
     if (!ctx || !t_wc) throw InvalidArg{"null argument"};
-    if (ctx->S != 1) throw InvalidArg{"vxm_integrate_cloud needs a single-stream context"};
+    if (ctx->nslots != 1) throw InvalidArg{"vxm_integrate_cloud needs a single-stream, single-frame context"};
     if (n > 0 && (!xs || !ys || !zs)) throw InvalidArg{"null cloud arrays"};
     VXM_CK(cudaSetDevice(ctx->device));
     if (n > ctx->cloud_cap) {

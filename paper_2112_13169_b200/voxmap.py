@@ -143,9 +143,11 @@ def stats_dict(s: N.StatsC) -> dict:
 class MappingPipeline:
     """MappingPipeline (pipeline.hpp:50-74) for `n_streams` independent sensor
     streams sharing one configuration; every integrate call advances all of
-    them by one frame on one GPU."""
+    them by `frames_per_call` consecutive frames on one GPU (frames, poses and
+    stats stream-major: frame k of stream s at s*frames_per_call + k)."""
 
-    def __init__(self, cfg: PipelineConfig, initial_position=None, n_streams=1, device=0, flags=0):
+    def __init__(self, cfg: PipelineConfig, initial_position=None, n_streams=1, device=0, flags=0,
+                 frames_per_call=1):
         if initial_position is not None:
             g = cfg.grid.c
             cfg = PipelineConfig(GridSpec.create_centered(g.size[0], g.size[1], g.size[2], g.vox_size,
@@ -153,11 +155,14 @@ class MappingPipeline:
                                  cfg.camera, cfg.vox_inf, cfg.depth, cfg.tracer_mode)
         self.cfg = cfg
         self.n_streams = n_streams
+        self.frames_per_call = frames_per_call
+        self.n_slots = n_streams * frames_per_call
         self._lib = N.load()
         self._ctx = C.c_void_p()
-        N.check(self._lib.vxm_create(C.byref(cfg.to_c()), n_streams, device, flags, C.byref(self._ctx)))
-        self._stats = (N.StatsC * n_streams)()
-        self._poses = (N.PoseC * n_streams)()
+        N.check(self._lib.vxm_create_multi(C.byref(cfg.to_c()), n_streams, frames_per_call, device, flags,
+                                           C.byref(self._ctx)))
+        self._stats = (N.StatsC * self.n_slots)()
+        self._poses = (N.PoseC * self.n_slots)()
 
     def close(self):
         if self._ctx:
@@ -171,8 +176,8 @@ class MappingPipeline:
             pass
 
     def _set_poses(self, poses):
-        if len(poses) != self.n_streams:
-            raise ValueError("need one pose per stream")
+        if len(poses) != self.n_slots:
+            raise ValueError("need one pose per stream and frame")
         for i, p in enumerate(poses):
             self._poses[i] = pose_c(p)
 
@@ -180,15 +185,15 @@ class MappingPipeline:
         """depth: float32 array (S, H, W) or (H, W) in host memory."""
         depth = np.ascontiguousarray(depth, dtype=np.float32)
         cam = self.cfg.camera
-        if depth.size != self.n_streams * cam.width * cam.height:
+        if depth.size != self.n_slots * cam.width * cam.height:
             raise ValueError("depth buffer size does not match camera model")
-        if self.n_streams == 1 and not isinstance(poses, list):
+        if self.n_slots == 1 and not isinstance(poses, list):
             poses = [poses]
         self._set_poses(poses)
         N.check(self._lib.vxm_integrate_depth(self._ctx, C.c_void_p(depth.ctypes.data), self._poses,
                                               self._stats))
         out = [stats_dict(s) for s in self._stats]
-        return out[0] if self.n_streams == 1 else out
+        return out[0] if self.n_slots == 1 else out
 
     def integrate_depth_ptr(self, depth_ptr: int, poses):
         """Host-buffer entry point for a raw (e.g. pinned) pointer."""

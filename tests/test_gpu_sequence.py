@@ -1,0 +1,140 @@
+"""Multi-frame pipelining (SURVEY.md §8f "next" #1): F consecutive frames of
+each stream per call (vxm_create_multi). Every frame's stats and the local
+grid after each call must equal F successive single-frame integrations —
+against the reference's Sequential build (oracle/_ref) and against the
+single-frame GPU path — bit for bit, including shifts along every axis,
+back-and-forth motion and jumps larger than the grid."""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from paper_2112_13169_b200 import voxmap as vm
+from tests import scenes
+from tests.oracle_api import have_ref, oracle_pipeline
+
+pytestmark = pytest.mark.gpu
+
+if not have_ref():
+    pytest.skip("oracle/_ref not built", allow_module_level=True)
+
+DEG = math.pi / 180.0
+KEYS = ("points_total", "points_outside", "rays_traced", "voxels_freed", "voxels_marked_unknown_traced",
+        "voxels_skipped_out_of_bounds", "occupied_count", "freed_count", "shifted", "shift_offset", "origin")
+
+
+def _check(sg, sr, where):
+    for key in KEYS:
+        assert sg[key] == sr[key], (where, key, sg[key], sr[key])
+
+
+def test_sequence_matches_reference_along_a_corridor(gpu_lib):
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 64, 48, 6.5)
+    grid = vm.GridSpec.create_centered(6.0, 6.0, 3.0, 0.1, (0.0, -8.0, 0.0))
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=1, depth=6.5)
+    boxes = scenes.corridor_boxes(-12.0, 25.0)
+    F = 8
+    seq = vm.MappingPipeline(cfg, frames_per_call=F)
+    orc = oracle_pipeline(cfg)
+    k = 0
+    for call in range(5):
+        poses = [vm.look_along_x((0.0, -8.0 + 0.1001 * (k + j), 0.0)) for j in range(F)]
+        depth = np.stack([scenes.render(cam, p, boxes) for p in poses])
+        stats = seq.integrate_depth(depth, poses)
+        for j in range(F):
+            _check(stats[j], orc.integrate_depth(depth[j], poses[j]), (call, j))
+        k += F
+        cells, origin = seq.local_grid()
+        rc, ro = orc.local_grid()
+        assert np.array_equal(cells, rc), call
+        assert np.array_equal(origin, ro)
+
+
+def _wander(rng, n, start):
+    """Poses that shift along x, y and z, turn back, stand still and jump
+    further than the grid is wide."""
+    p = np.array(start, dtype=float)
+    out = []
+    for i in range(n):
+        if i % 11 == 7:
+            p = p + np.array([0.0, 9.0 if (i // 11) % 2 == 0 else -9.0, 0.0])  # jump past the grid
+        elif i % 5 == 3:
+            pass  # stand still
+        else:
+            p = p + rng.uniform(-0.17, 0.17, 3) * np.array([1.0, 1.0, 0.6])
+        yaw = rng.uniform(-0.3, 0.3)
+        R = vm.look_along_x((0, 0, 0))[0] @ np.array([[math.cos(yaw), 0, math.sin(yaw)], [0, 1, 0],
+                                                      [-math.sin(yaw), 0, math.cos(yaw)]])
+        out.append((R, p.copy()))
+    return out
+
+
+@pytest.mark.parametrize("S,F", [(1, 3), (2, 7), (3, 16)])
+def test_sequence_equals_single_frame_path_while_wandering(gpu_lib, S, F):
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 96, 72, 6.5)
+    grid = vm.GridSpec.create_centered(5.0, 4.0, 3.0, 0.1, (0.0, 0.0, 0.0))
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=2, depth=6.0)
+    rng = np.random.default_rng(100 * S + F)
+    calls = 3
+    trajs = [_wander(rng, calls * F, (0.05 * s, 0.0, 0.0)) for s in range(S)]
+    boxes = [scenes.box_field_boxes(3 + s) for s in range(S)]
+    seq = vm.MappingPipeline(cfg, n_streams=S, frames_per_call=F)
+    singles = [vm.MappingPipeline(cfg) for _ in range(S)]
+    for call in range(calls):
+        poses = [trajs[s][call * F + j] for s in range(S) for j in range(F)]
+        depth = np.stack([scenes.render(cam, poses[s * F + j], boxes[s]) for s in range(S) for j in range(F)])
+        stats = seq.integrate_depth(depth, poses)
+        for s in range(S):
+            for j in range(F):
+                i = s * F + j
+                _check(stats[i], singles[s].integrate_depth(depth[i], poses[i]), (call, s, j))
+            assert np.array_equal(seq.local_grid(s)[0], singles[s].local_grid()[0]), (call, s)
+            assert np.array_equal(seq.local_grid(s)[1], singles[s].local_grid()[1])
+    # and the single-frame path against the reference build on the last stream
+    orc = oracle_pipeline(cfg)
+    for i in range(calls * F):
+        pose = trajs[S - 1][i]
+        orc.integrate_depth(scenes.render(cam, pose, boxes[S - 1]), pose)
+    assert np.array_equal(seq.local_grid(S - 1)[0], orc.local_grid()[0])
+
+
+def test_sequence_device_frames_and_restored_grid(gpu_lib):
+    """Device-resident frames (the bench path) and a local grid restored from
+    a checkpoint before the first call."""
+    import torch
+
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 80, 60, 6.5)
+    grid = vm.GridSpec.create_centered(6.0, 6.0, 3.0, 0.15, (0.0, 0.0, 0.0))
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=0, depth=6.5)
+    F = 5
+    rng = np.random.default_rng(5)
+    start = rng.integers(0, 4, grid.cell_count()).astype(np.uint8)
+    seq = vm.MappingPipeline(cfg, frames_per_call=F)
+    one = vm.MappingPipeline(cfg)
+    org = grid.origin + np.array([0.3, -0.15, 0.0])
+    seq.set_local_grid(start, org)
+    one.set_local_grid(start, org)
+    poses = [vm.look_along_x((0.0, 0.13 * j - 0.3, 0.02 * j)) for j in range(F)]
+    depth = np.stack([scenes.render(cam, p, scenes.box_field_boxes(2)) for p in poses])
+    dev = torch.from_numpy(depth).cuda()
+    seq.integrate_depth_device(dev.data_ptr(), poses)
+    stats = seq.wait_stats()
+    for j in range(F):
+        _check(stats[j], one.integrate_depth(depth[j], poses[j]), j)
+    assert np.array_equal(seq.local_grid()[0], one.local_grid()[0])
+
+
+def test_sequence_argument_checks(gpu_lib):
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 32, 24, 6.5)
+    grid = vm.GridSpec.create_centered(3.0, 3.0, 3.0, 0.15, (0.0, 0.0, 0.0))
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=0, depth=6.5)
+    for bad in (0, -1, 65):
+        with pytest.raises(ValueError, match="frames_per_call"):
+            vm.MappingPipeline(cfg, frames_per_call=bad)
+    seq = vm.MappingPipeline(cfg, frames_per_call=2)
+    with pytest.raises(ValueError):
+        seq.integrate_depth(np.ones((24, 32), np.float32), [vm.look_along_x((0, 0, 0))])
+    with pytest.raises(ValueError, match="single-frame"):
+        seq.integrate(np.ones(3), np.ones(3), np.ones(3), vm.look_along_x((0, 0, 0)))

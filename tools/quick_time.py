@@ -9,16 +9,20 @@ from tests import scenes
 DEG = math.pi / 180
 CFGS = {"cfg1": (0, 6.5), "cfg2": (2, 5.0)}
 for item in os.environ.get("QT_CONFIGS", "cfg1:1,cfg2:1,cfg2:64,cfg1:64").split(","):
-    name, S = item.split(":"); S = int(S)
+    parts = item.split(":"); name, S = parts[0], int(parts[1]); F = int(parts[2]) if len(parts) > 2 else 1
     vox_inf, dm = CFGS[name]
     cam = vm.CameraModel(85 * DEG, 101 * DEG, 640, 480, dm)
     grid = vm.GridSpec.create_centered(10.0, 10.0, 5.0, 0.1, (0, 0, 0))
     pose = vm.look_along_x((0, 0, 0))
     d = scenes.render(cam, pose, scenes.box_field_boxes(1))
-    dev = torch.from_numpy(np.stack([d] * S)).cuda()
-    poses = [pose] * S
+    if F > 1:  # a moving robot: one voxel per frame along y (cfg4-like)
+        poses = [vm.look_along_x((0, 0.1001 * j, 0)) for _ in range(S) for j in range(F)]
+    else:
+        poses = [pose] * S
+    dev = torch.from_numpy(np.stack([d] * (S * F))).cuda()
     for flags in (0, 1):
-        p = vm.MappingPipeline(vm.PipelineConfig(grid, cam, vox_inf=vox_inf, depth=dm), n_streams=S, flags=flags)
+        p = vm.MappingPipeline(vm.PipelineConfig(grid, cam, vox_inf=vox_inf, depth=dm), n_streams=S, flags=flags,
+                               frames_per_call=F)
         for _ in range(5):
             p.integrate_depth_device(dev.data_ptr(), poses); p.wait_stats()
         ts, st3 = [], []
@@ -27,7 +31,7 @@ for item in os.environ.get("QT_CONFIGS", "cfg1:1,cfg2:1,cfg2:64,cfg1:64").split(
             st3.append((st[0]["populate_us"], st[0]["trace_us"], st[0]["merge_us"]))
         ts = np.array(ts)
         if flags == 0:
-            print(f"{name}x{S} graph p50 ms %.4f p99 %.4f  frames/s %.0f  us/frame %.2f" % (np.median(ts), np.percentile(ts, 99), S / np.median(ts) * 1e3, np.median(ts) * 1e3 / S), flush=True)
+            print(f"{name}x{S}x{F} graph p50 ms %.4f p99 %.4f  frames/s %.0f  us/frame %.2f" % (np.median(ts), np.percentile(ts, 99), S * F / np.median(ts) * 1e3, np.median(ts) * 1e3 / (S * F)), flush=True)
         else:
             m = np.median(np.array(st3), axis=0)
             print("   stages (us): populate+dilate %.1f  trace %.1f  merge %.1f   (no-graph total %.1f)" % (m[0], m[1], m[2], np.median(ts) * 1e3), flush=True)
