@@ -97,6 +97,11 @@ def kernel_section(tag, k):
         for r in sorted(data, key=lambda r: -int(r[i_s] or 0))[:10]:
             out.append(f"{int(r[i_s] or 0) / tot:6.1%}  {r[1].strip()[:90]}")
         out.append("```")
+        st = [i for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
+        sums = {hdr[i][6:]: sum(int(r[i] or 0) for r in data) for i in st}
+        s_all = sum(sums.values()) or 1
+        out += ["", "Warp stall reasons (share of samples): " + ", ".join(
+            f"{k} {v / s_all:.1%}" for k, v in sorted(sums.items(), key=lambda kv: -kv[1]) if v > 0.01 * s_all)]
     return "\n".join(out), vals
 
 
@@ -108,13 +113,13 @@ def main():
           f"`{tag}_gpu.txt`). Launch list = `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
           "dram__bytes_write.sum --clock-control none` of `bench.py --steps 2 --warmup 3` (cold-cache and "
           "serialised: compare shares, not absolutes). Per-kernel sections = `ncu --set full` of one launch in a "
-          "batched cfg2 step (64 streams).", ""]
+          "batched cfg2 step (64 streams); merge_sequence from one 64-frame call of a single moving stream.", ""]
     gpu = RAW / f"{tag}_gpu.txt"
     if gpu.exists():
         md += ["```", gpu.read_text().strip(), "```", ""]
     md += ["## Launch list of the bench command", "", launch_table(tag), ""]
     traffic = None
-    for k in ("trace_bundle", "populate_depth", "dilate", "merge_shift"):
+    for k in ("trace_bundle", "populate_depth", "dilate_rows", "dilate_tiles", "merge_shift", "merge_sequence"):
         sec, vals = kernel_section(tag, k)
         md += [sec, ""]
         if k == "trace_bundle" and vals:
