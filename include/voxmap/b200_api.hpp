@@ -355,16 +355,27 @@ class MappingPipeline {
   // Extension: the fused depth path (depth_to_cloud folded into the first
   // kernel); equal to integrate({depth_to_cloud(depth, camera), t_wc}).
   PipelineStats integrate_depth(const DepthImage& depth, const RigidTransform& t_wc);
+  // Extension: multi-frame pipelining. Equal to calling integrate_depth on
+  // each (depths[i], poses[i]) in order, bit for bit, but the populate and
+  // ray-cast stages of up to kMaxFramesPerCall frames run concurrently and
+  // one chain kernel folds their merges and shifts.
+  static constexpr int kMaxFramesPerCall = 64;
+  std::vector<PipelineStats> integrate_depth_sequence(const std::vector<DepthImage>& depths,
+                                                      const std::vector<RigidTransform>& poses);
 
   const VoxelGrid& local_grid() const;
   const PipelineConfig& config() const { return cfg_; }
 
  private:
   PipelineConfig cfg_;
-  vxm_ctx* ctx_ = nullptr;
+  int device_ = 0;
+  vxm_ctx* ctx_ = nullptr;      // single-frame context
+  vxm_ctx* seq_ctx_ = nullptr;  // multi-frame context, created on first use
+  bool seq_active_ = false;     // which context holds the current local grid
   mutable VoxelGrid local_;
   mutable bool local_stale_ = false;
   PipelineStats finish(const vxm_stats& s);
+  void activate(bool sequence);
 };
 
 // ------------------------------------------------------------ kernel table

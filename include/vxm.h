@@ -164,6 +164,11 @@ int vxm_frames_per_call(const vxm_ctx* ctx);
 int vxm_integrate_depth(vxm_ctx* ctx, const float* depth, const vxm_pose* t_wc,
                         vxm_stats* stats);
 
+/* Single-stream contexts: n_frames (1..frames_per_call) consecutive HOST depth
+ * frames with their poses, synchronous; n_frames stats. Equals n_frames
+ * successive vxm_integrate_depth calls on a single-frame context. */
+int vxm_integrate_depth_frames(vxm_ctx* ctx, const float* depth, const vxm_pose* t_wc,
+                               int32_t n_frames, vxm_stats* stats);
 /* Same, with the depth frames already in device memory (n_streams*W*H
  * floats). Asynchronous on the context's stream: returns after enqueueing;
  * read the stats with vxm_wait_stats(). */

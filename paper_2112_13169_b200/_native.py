@@ -76,6 +76,7 @@ SIGNATURES = {
     "vxm_num_streams": (C.c_int, [C.c_void_p]),
     "vxm_create_multi": (C.c_int, [P(ConfigC), C.c_int32, C.c_int32, C.c_int32, C.c_uint32, P(C.c_void_p)]),
     "vxm_frames_per_call": (C.c_int, [C.c_void_p]),
+    "vxm_integrate_depth_frames": (C.c_int, [C.c_void_p, C.c_void_p, P(PoseC), C.c_int32, P(StatsC)]),
     "vxm_integrate_depth": (C.c_int, [C.c_void_p, C.c_void_p, P(PoseC), P(StatsC)]),
     "vxm_integrate_depth_device": (C.c_int, [C.c_void_p, C.c_void_p, P(PoseC)]),
     "vxm_wait_stats": (C.c_int, [C.c_void_p, P(StatsC)]),

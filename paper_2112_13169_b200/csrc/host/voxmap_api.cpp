@@ -330,7 +330,7 @@ PipelineConfig recentered(PipelineConfig cfg, const Eigen::Vector3d& position) {
 }  // namespace
 
 MappingPipeline::MappingPipeline(PipelineConfig cfg, int device)
-    : cfg_(validated(std::move(cfg))), local_(cfg_.grid) {
+    : cfg_(validated(std::move(cfg))), device_(device), local_(cfg_.grid) {
   vxm_config c{};
   c.grid = cfg_.grid.to_c();
   c.camera = cfg_.camera.to_c();
@@ -345,21 +345,46 @@ MappingPipeline::MappingPipeline(PipelineConfig cfg, const Eigen::Vector3d& init
 
 MappingPipeline::~MappingPipeline() {
   if (ctx_) vxm_destroy(ctx_);
+  if (seq_ctx_) vxm_destroy(seq_ctx_);
 }
 
 MappingPipeline::MappingPipeline(MappingPipeline&& o) noexcept
-    : cfg_(std::move(o.cfg_)), ctx_(std::exchange(o.ctx_, nullptr)), local_(std::move(o.local_)),
+    : cfg_(std::move(o.cfg_)), device_(o.device_), ctx_(std::exchange(o.ctx_, nullptr)),
+      seq_ctx_(std::exchange(o.seq_ctx_, nullptr)), seq_active_(o.seq_active_), local_(std::move(o.local_)),
       local_stale_(o.local_stale_) {}
 
 MappingPipeline& MappingPipeline::operator=(MappingPipeline&& o) noexcept {
   if (this != &o) {
     if (ctx_) vxm_destroy(ctx_);
+    if (seq_ctx_) vxm_destroy(seq_ctx_);
     cfg_ = std::move(o.cfg_);
+    device_ = o.device_;
     ctx_ = std::exchange(o.ctx_, nullptr);
+    seq_ctx_ = std::exchange(o.seq_ctx_, nullptr);
+    seq_active_ = o.seq_active_;
     local_ = std::move(o.local_);
     local_stale_ = o.local_stale_;
   }
   return *this;
+}
+
+// Moves the local grid (cells + origin) to the context that runs next.
+void MappingPipeline::activate(bool sequence) {
+  if (sequence == seq_active_) return;
+  if (sequence && !seq_ctx_) {
+    vxm_config c{};
+    c.grid = cfg_.grid.to_c();
+    c.camera = cfg_.camera.to_c();
+    c.vox_inf = cfg_.integrator.vox_inf;
+    c.tracer_mode = cfg_.tracer_mode == TracerMode::Bundled ? VXM_TRACER_BUNDLED : VXM_TRACER_PER_PIXEL;
+    c.depth = cfg_.depth;
+    check(vxm_create_multi(&c, 1, kMaxFramesPerCall, device_, 0, &seq_ctx_));
+  }
+  std::vector<std::uint8_t> cells(local_.size());
+  double origin[3];
+  check(vxm_download_local(sequence ? ctx_ : seq_ctx_, 0, cells.data(), origin));
+  check(vxm_upload_local(sequence ? seq_ctx_ : ctx_, 0, cells.data(), origin));
+  seq_active_ = sequence;
 }
 
 PipelineStats MappingPipeline::finish(const vxm_stats& s) {
@@ -385,6 +410,7 @@ PipelineStats MappingPipeline::integrate(const MeasurementFrame& frame) {
   if (!frame.t_wc.is_valid(1e-6)) throw std::invalid_argument("MeasurementFrame: invalid transform");
   const vxm_pose p = frame.t_wc.to_c();
   vxm_stats s{};
+  activate(false);
   check(vxm_integrate_cloud(ctx_, frame.cloud.xs().data(), frame.cloud.ys().data(),
                             frame.cloud.zs().data(), frame.cloud.size(), &p, &s));
   return finish(s);
@@ -397,14 +423,47 @@ PipelineStats MappingPipeline::integrate_depth(const DepthImage& depth, const Ri
   if (!t_wc.is_valid(1e-6)) throw std::invalid_argument("MeasurementFrame: invalid transform");
   const vxm_pose p = t_wc.to_c();
   vxm_stats s{};
+  activate(false);
   check(vxm_integrate_depth(ctx_, depth.depths.data(), &p, &s));
   return finish(s);
+}
+
+std::vector<PipelineStats> MappingPipeline::integrate_depth_sequence(const std::vector<DepthImage>& depths,
+                                                                     const std::vector<RigidTransform>& poses) {
+  if (depths.size() != poses.size()) throw std::invalid_argument("integrate_depth_sequence: one pose per frame");
+  const std::size_t npix = static_cast<std::size_t>(cfg_.camera.width) * cfg_.camera.height;
+  for (std::size_t i = 0; i < depths.size(); ++i) {
+    const DepthImage& d = depths[i];
+    if (d.width != cfg_.camera.width || d.height != cfg_.camera.height || d.depths.size() != npix)
+      throw std::invalid_argument("depth_to_cloud: image size does not match camera model");
+    if (!poses[i].is_valid(1e-6)) throw std::invalid_argument("MeasurementFrame: invalid transform");
+  }
+  std::vector<PipelineStats> out;
+  out.reserve(depths.size());
+  if (depths.empty()) return out;
+  activate(true);
+  std::vector<float> buf;
+  std::vector<vxm_pose> p;
+  std::vector<vxm_stats> st;
+  for (std::size_t i0 = 0; i0 < depths.size(); i0 += kMaxFramesPerCall) {
+    const std::size_t n = std::min<std::size_t>(kMaxFramesPerCall, depths.size() - i0);
+    buf.resize(n * npix);
+    p.resize(n);
+    st.assign(n, vxm_stats{});
+    for (std::size_t j = 0; j < n; ++j) {
+      std::copy(depths[i0 + j].depths.begin(), depths[i0 + j].depths.end(), buf.begin() + j * npix);
+      p[j] = poses[i0 + j].to_c();
+    }
+    check(vxm_integrate_depth_frames(seq_ctx_, buf.data(), p.data(), static_cast<int32_t>(n), st.data()));
+    for (std::size_t j = 0; j < n; ++j) out.push_back(finish(st[j]));
+  }
+  return out;
 }
 
 const VoxelGrid& MappingPipeline::local_grid() const {
   if (local_stale_) {
     double origin[3];
-    check(vxm_download_local(ctx_, 0, local_.raw(), origin));
+    check(vxm_download_local(seq_active_ ? seq_ctx_ : ctx_, 0, local_.raw(), origin));
     local_.set_origin(Eigen::Vector3d(origin[0], origin[1], origin[2]));
     local_stale_ = false;
   }

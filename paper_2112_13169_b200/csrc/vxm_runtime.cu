@@ -466,9 +466,9 @@ void prepare_frames(vxm_ctx* c, const vxm_pose* poses, const float* depth_dev_ba
   VXM_CK(cudaEventRecord(c->ring_ev[c->ring_slot], c->stream));
 }
 
-void run_frame(vxm_ctx* c, bool cloud) {
+void run_frame(vxm_ctx* c, bool cloud, bool direct = false) {
   const bool timed = (c->flags & VXM_FLAG_STAGE_TIMING) != 0;
-  if (timed || (c->flags & VXM_FLAG_NO_GRAPH)) {
+  if (timed || direct || (c->flags & VXM_FLAG_NO_GRAPH)) {
     VXM_CK(cudaEventRecord(c->ev[0], c->stream));
     launch_frame(c, cloud, false);
   } else {
@@ -801,6 +801,33 @@ int vxm_integrate_depth(vxm_ctx* ctx, const float* depth, const vxm_pose* t_wc, 
                            cudaMemcpyHostToDevice, ctx->stream));
     run_frame(ctx, false);
     collect_stats(ctx, stats);
+  });
+}
+
+int vxm_integrate_depth_frames(vxm_ctx* ctx, const float* depth, const vxm_pose* t_wc, int32_t n_frames,
+                               vxm_stats* stats) {
+  return guarded([&] {
+    if (!ctx || !depth || !t_wc) throw InvalidArg{"null argument"};
+    if (ctx->S != 1) throw InvalidArg{"vxm_integrate_depth_frames needs a single-stream context"};
+    if (n_frames < 1 || n_frames > ctx->F) throw InvalidArg{"n_frames must lie in [1, frames_per_call]"};
+    VXM_CK(cudaSetDevice(ctx->device));
+    const size_t frame = static_cast<size_t>(ctx->kp.W) * ctx->kp.H;
+    const int F = ctx->F;
+    // a shorter call runs the first n_frames slots with direct launches (the
+    // captured graph has the full shape); slots keep their own epochs
+    ctx->F = ctx->nslots = n_frames;
+    try {
+      next_slot(ctx);
+      prepare_frames(ctx, t_wc, ctx->depth_dev, frame);
+      VXM_CK(cudaMemcpyAsync(ctx->depth_dev, depth, sizeof(float) * frame * n_frames,
+                             cudaMemcpyHostToDevice, ctx->stream));
+      run_frame(ctx, false, n_frames != F);
+      collect_stats(ctx, stats);
+    } catch (...) {
+      ctx->F = ctx->nslots = F;
+      throw;
+    }
+    ctx->F = ctx->nslots = F;
   });
 }
 

@@ -195,6 +195,19 @@ class MappingPipeline:
         out = [stats_dict(s) for s in self._stats]
         return out[0] if self.n_slots == 1 else out
 
+    def integrate_depth_frames(self, depth, poses):
+        """Single-stream contexts: 1..frames_per_call consecutive host frames
+        (n, H, W) with n poses; returns n stats dicts (synchronous)."""
+        depth = np.ascontiguousarray(depth, dtype=np.float32)
+        cam = self.cfg.camera
+        n = len(poses)
+        if depth.size != n * cam.width * cam.height:
+            raise ValueError("depth buffer size does not match camera model")
+        pa = (N.PoseC * max(1, n))(*(pose_c(p) for p in poses))
+        st = (N.StatsC * max(1, n))()
+        N.check(self._lib.vxm_integrate_depth_frames(self._ctx, C.c_void_p(depth.ctypes.data), pa, n, st))
+        return [stats_dict(st[i]) for i in range(n)]
+
     def integrate_depth_ptr(self, depth_ptr: int, poses):
         """Host-buffer entry point for a raw (e.g. pinned) pointer."""
         self._set_poses(poses)

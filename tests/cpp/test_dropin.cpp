@@ -193,6 +193,39 @@ static void pipeline_cases() {
     CHECK(sa.trace.voxels_freed == sb.trace.voxels_freed);
     CHECK(a.local_grid() == b.local_grid());
   }
+  {
+    // extension: integrate_depth_sequence == integrate_depth frame by frame,
+    // across the 64-frame call boundary, interleaved with single frames
+    PipelineConfig cfg = small_config();
+    cfg.integrator.vox_inf = 2;
+    MappingPipeline seq(cfg), one(cfg);
+    std::vector<DepthImage> imgs;
+    std::vector<RigidTransform> poses;
+    for (int k = 0; k < 70; ++k) {
+      DepthImage img(320, 240);
+      for (int v = 0; v < 240; ++v)
+        for (int u = 0; u < 320; ++u)
+          img.at(u, v) = ((u + 3 * k) / 40 + v / 30) % 4 == 0 ? 0.0f : 1.2f + 0.003f * u + 0.01f * (k % 5);
+      imgs.push_back(img);
+      poses.push_back(look_along_x({0.04 * (k % 9), 0.11 * k - 3.0, 0.02 * (k % 3)}));
+    }
+    const std::vector<PipelineStats> ss = seq.integrate_depth_sequence(imgs, poses);
+    bool same = ss.size() == imgs.size();
+    for (std::size_t k = 0; k < imgs.size() && same; ++k) {
+      const PipelineStats so = one.integrate_depth(imgs[k], poses[k]);
+      same = so.occupied_count == ss[k].occupied_count && so.freed_count == ss[k].freed_count &&
+             so.trace.voxels_freed == ss[k].trace.voxels_freed && so.shifted == ss[k].shifted &&
+             so.shift_offset == ss[k].shift_offset && so.populate.points_total == ss[k].populate.points_total;
+    }
+    CHECK(same);
+    CHECK(seq.local_grid() == one.local_grid());
+    CHECK(seq.local_grid().spec().origin == one.local_grid().spec().origin);
+    const PipelineStats a1 = seq.integrate_depth(imgs[3], poses[60]);
+    const PipelineStats b1 = one.integrate_depth(imgs[3], poses[60]);
+    CHECK(a1.freed_count == b1.freed_count);
+    CHECK(seq.local_grid() == one.local_grid());
+    CHECK_THROWS_AS(seq.integrate_depth_sequence(imgs, {}), std::invalid_argument);
+  }
 }
 
 static void grid_cases() {

@@ -138,3 +138,27 @@ def test_sequence_argument_checks(gpu_lib):
         seq.integrate_depth(np.ones((24, 32), np.float32), [vm.look_along_x((0, 0, 0))])
     with pytest.raises(ValueError, match="single-frame"):
         seq.integrate(np.ones(3), np.ones(3), np.ones(3), vm.look_along_x((0, 0, 0)))
+
+
+def test_sequence_partial_calls_host_frames(gpu_lib):
+    """vxm_integrate_depth_frames: 1..F host frames per call on a
+    single-stream multi-frame context (the C++ integrate_depth_sequence path)."""
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 80, 60, 6.5)
+    grid = vm.GridSpec.create_centered(6.0, 5.0, 3.0, 0.1, (0.0, 0.0, 0.0))
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=1, depth=6.5)
+    seq = vm.MappingPipeline(cfg, frames_per_call=8)
+    one = vm.MappingPipeline(cfg)
+    rng = np.random.default_rng(11)
+    traj = _wander(rng, 3 + 8 + 1 + 5 + 8, (0.0, 0.0, 0.0))
+    i = 0
+    for n in (3, 8, 1, 5, 8):
+        poses = traj[i:i + n]
+        depth = np.stack([scenes.render(cam, p, scenes.box_field_boxes(4)) for p in poses])
+        stats = seq.integrate_depth_frames(depth, poses)
+        assert len(stats) == n
+        for j in range(n):
+            _check(stats[j], one.integrate_depth(depth[j], poses[j]), (n, j))
+        assert np.array_equal(seq.local_grid()[0], one.local_grid()[0]), n
+        i += n
+    with pytest.raises(ValueError, match="n_frames"):
+        seq.integrate_depth_frames(np.zeros((9, 60, 80), np.float32), traj[:9])
