@@ -152,6 +152,18 @@ __device__ __noinline__ int voxel_coord_exact(double acc, double vs) {
 // fraction tests read the high words, so the fast path costs four fp64
 // operations and a few integer compares. Otherwise (near an integer, zero,
 // large, NaN) the exact division runs.
+// The fast path alone: ok = false when the exact division must decide.
+__device__ __forceinline__ int voxel_coord_fast(double acc, double inv_vs, bool& ok) {
+  constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+  const double q = dmul(acc, inv_vs);
+  const double t = __dadd_rd(q, kMagic);
+  const double frac = dsub(q, dsub(t, kMagic));
+  const uint32_t qhi = static_cast<uint32_t>(__double2hiint(q)) & 0x7fffffffu;
+  const uint32_t fhi = static_cast<uint32_t>(__double2hiint(frac));
+  ok = qhi < 0x41C00000u && fhi > 0x3EF00000u && fhi < 0x3FEFFFE0u;
+  return __double2loint(t);
+}
+
 __device__ __forceinline__ int voxel_coord(double acc, double vs, double inv_vs) {
   constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
   const double q = dmul(acc, inv_vs);

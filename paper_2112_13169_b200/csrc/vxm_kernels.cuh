@@ -440,21 +440,18 @@ inline cudaError_t dilate_set_smem(int bytes) {
 // The walk runs in chunks of kChunk DDA steps: (A) the chunk's cell indices
 // are computed (they do not depend on grid contents), (B) their occupancy
 // bytes are loaded together through the read-only path, (C) the chunk is
-// resolved in order with predicated, branch-free PTX. A chunk that provably
-// cannot reach the stop distance or the grid boundary for any ray of the
-// warp (a conservative bound from the tmax/tdelta values, checked per chunk)
-// runs only the axis choice and the advance; the last chunks of a ray run
-// the exact per-step stop and in-grid tests. ncu (profiles/) showed the
-// kernel issue- and ALU-pipe bound, so both paths are written to minimise
-// instructions per visit. The Sequential last-writer rule is a fire-and-forget
-// RED.max on the cell key; before issuing it a lane drops its write when
-// lane+1 or lane+8 (both higher ray indices) writes the same cell in the
-// same step, which removes most same-address traffic near the camera.
+// resolved in order with predicated, branch-free PTX. Inside the grid each
+// step only compares the chosen axis' tmax with a per-axis threshold
+// min(stop, E_a), E_a being the exact tmax at which the walk would leave the
+// grid along a (summed once per ray with the walk's own additions), so there
+// are no per-step bounds tests or step counters. ncu (profiles/) showed the
+// kernel issue- and ALU-pipe bound, so the step and the resolve are written to
+// minimise instructions per visit. The Sequential last-writer rule is a
+// fire-and-forget RED.max on the cell key; before issuing it a lane drops its
+// write when lane+1 or lane+8 (both higher ray indices) writes the same cell
+// in the same step, which removes most same-address traffic near the camera.
 // Counters go to 32 per-stream slots (one RED per warp each), summed by K4.
 // ---------------------------------------------------------------------------
-#ifndef VXM_FAST_MUL
-#define VXM_FAST_MUL 1
-#endif
 constexpr int kChunk = 8;  // 4 and 16 measured equal; without the dedup 2-3x slower
 constexpr int kTraceSlots = 32;
 
@@ -594,113 +591,75 @@ __global__ void __launch_bounds__(32) trace_bundle_kernel(KParams p) {
   // test: it ends on the first step along an axis whose remaining in-grid
   // steps are used up.
   if (x < dx && y < dy && z < dz) {
-    const double d0 = st.tdelta[0], d1 = st.tdelta[1], d2 = st.tdelta[2];
-    // r_a = A_a + B_a * coordinate: in-grid steps left along axis a
-    // (coordinate to the far face for step +1, to 0 for step -1, a large
-    // constant for an axis the ray never steps along)
-    const int A0 = st.step[0] > 0 ? static_cast<int>(dx) - 1 : (st.step[0] < 0 ? 0 : (1 << 30));
-    const int A1 = st.step[1] > 0 ? static_cast<int>(dy) - 1 : (st.step[1] < 0 ? 0 : (1 << 30));
-    const int A2 = st.step[2] > 0 ? static_cast<int>(dz) - 1 : (st.step[2] < 0 ? 0 : (1 << 30));
-    const int B0 = -st.step[0], B1 = -st.step[1], B2 = -st.step[2];
-    // conservative reach of a chunk: tmax grows by at most kChunk * tdelta
-    // (plus rounding) along any axis, so if min_a(tmax_a + kChunk*tdelta_a)
-    // stays below the stop distance no step of the chunk can hit it
-    const double span0 = dmul(d0, static_cast<double>(kChunk) * (1.0 + 0x1p-40));
-    const double span1 = dmul(d1, static_cast<double>(kChunk) * (1.0 + 0x1p-40));
-    const double span2 = dmul(d2, static_cast<double>(kChunk) * (1.0 + 0x1p-40));
+    // The walk ends at the first step whose chosen axis a has tmax_a >= M_a,
+    // M_a = min(stop, E_a), where E_a is the exact tmax_a value of the step
+    // that would leave the grid along a (its rem_a-th step: the same
+    // repeated additions as the walk, done once here). So every step checks
+    // one threshold and nothing else; no per-step bounds or counters.
+    const int rem[3] = {st.step[0] > 0 ? static_cast<int>(dx - 1 - x) : static_cast<int>(x),
+                        st.step[1] > 0 ? static_cast<int>(dy - 1 - y) : static_cast<int>(y),
+                        st.step[2] > 0 ? static_cast<int>(dz - 1 - z) : static_cast<int>(z)};
+    double M[3];
+    const double tt[3] = {t0, t1, t2};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      M[a] = stop;
+      // exit beyond the stop distance (with a 2^-30 margin on the estimate):
+      // the stop decides; otherwise sum exactly
+      if (st.step[a] != 0 &&
+          !(dadd(tt[a], dmul(static_cast<double>(rem[a]), st.tdelta[a])) > dmul(stop, 1.0 + 0x1p-30))) {
+        double e = tt[a];
+        for (int k = 0; k < rem[a]; ++k) e = dadd(e, st.tdelta[a]);
+        M[a] = fmin(stop, e);
+      }
+    }
+    const double M0 = M[0], M1 = M[1], M2 = M[2];
+    // tdelta of an axis the ray never steps along is +inf; that axis is never
+    // chosen, and the selected-addend form below needs a finite value for it
+    const double e0 = st.step[0] ? st.tdelta[0] : 0.0, e1 = st.step[1] ? st.tdelta[1] : 0.0,
+                 e2 = st.step[2] ? st.tdelta[2] : 0.0;
+    uint32_t al = active ? 1u : 0u;
     bool alive = active;
     uint32_t uidx = static_cast<uint32_t>(idx);
-    // tdelta of an axis the ray never steps along is +inf; that axis is never
-    // chosen, and the multiply-add form below needs a finite addend for it
-    const double e0 = st.step[0] ? d0 : 0.0, e1 = st.step[1] ? d1 : 0.0, e2 = st.step[2] ? d2 : 0.0;
-    // Where the walk can end: at the stop distance, or at the step that
-    // leaves the grid along axis a, which happens at tmax_a after rem_a steps
-    // along a, i.e. at ~ tmax_a + rem_a * tdelta_a (repeated rounding moves
-    // that by far less than the 2^-30 relative margin used below).
-    double end = stop;
-    {
-      const int rr[3] = {A0 + B0 * static_cast<int>(x), A1 + B1 * static_cast<int>(y), A2 + B2 * static_cast<int>(z)};
-      const double tt[3] = {t0, t1, t2};
-#pragma unroll
-      for (int a = 0; a < 3; ++a)
-        if (st.step[a]) end = fmin(end, dadd(tt[a], dmul(static_cast<double>(rr[a]), st.tdelta[a])));
-      end = dmul(end, 1.0 - 0x1p-30);
-    }
     while (__any_sync(0xffffffffu, alive)) {
       uint32_t cell[kChunk];
-      const double reach = fmin(fmin(dadd(t0, span0), dadd(t1, span1)), dadd(t2, span2));
-      const bool fast = !alive || reach < end;
-      if (__all_sync(0xffffffffu, fast)) {
-        // No ray of the warp can stop or leave the grid within the chunk:
-        // only the axis choice (ties x, then y, then z) and the advance.
 #pragma unroll
-        for (int j = 0; j < kChunk; ++j) {
-          cell[j] = alive ? uidx : 0xffffffffu;
-          const bool px = t0 <= t1 && t0 <= t2;
-          const bool py = !px && t1 <= t2;
-          const bool pz = !px && !py;
-#if VXM_FAST_MUL
-          // t + tdelta*1 == RN(t + tdelta); t + tdelta*0 == t (t >= 0)
-          t0 = dadd(t0, dmul(e0, px ? 1.0 : 0.0));
-          t1 = dadd(t1, dmul(e1, py ? 1.0 : 0.0));
-          t2 = dadd(t2, dmul(e2, pz ? 1.0 : 0.0));
-#else
-          t0 = px ? dadd(t0, d0) : t0;
-          t1 = py ? dadd(t1, d1) : t1;
-          t2 = pz ? dadd(t2, d2) : t2;
-#endif
-          uidx += px ? lin0 : (py ? lin1 : lin2);
-        }
-      } else {
-        uint32_t al = alive ? 1u : 0u;
-        // in-grid steps left per axis, from the cell coordinates
-        const uint32_t cz = uidx / static_cast<uint32_t>(dxy);
-        const uint32_t rxy = uidx - cz * static_cast<uint32_t>(dxy);
-        const uint32_t cy = rxy / dx;
-        int r0 = A0 + B0 * static_cast<int>(rxy - cy * dx);
-        int r1 = A1 + B1 * static_cast<int>(cy);
-        int r2 = A2 + B2 * static_cast<int>(cz);
-#pragma unroll
-        for (int j = 0; j < kChunk; ++j) {
-          cell[j] = al ? uidx : 0xffffffffu;
-          // walk_ray's step (raytracer.hpp:103-116): the axis with the
-          // smallest tmax, ties x then y then z; stop when that tmax >=
-          // max_dist - 1e-10, or when the step would leave the grid (r < 0).
-          asm("{\n\t"
-              ".reg .pred q, px, py, pz, npx, s0, s1, s2, ok, rg;\n\t"
-              ".reg .b32 m;\n\t"
-              "setp.le.f64 q, %0, %1;\n\t"
-              "setp.le.and.f64 px, %0, %2, q;\n\t"
-              "setp.le.f64 q, %1, %2;\n\t"
-              "not.pred npx, px;\n\t"
-              "and.pred py, q, npx;\n\t"
-              "or.pred pz, px, py;\n\t"
-              "not.pred pz, pz;\n\t"
-              "setp.lt.and.f64 s0, %0, %11, px;\n\t"
-              "setp.lt.and.f64 s1, %1, %11, py;\n\t"
-              "setp.lt.and.f64 s2, %2, %11, pz;\n\t"
-              "or.pred ok, s0, s1;\n\t"
-              "or.pred ok, ok, s2;\n\t"
-              "@px add.rn.f64 %0, %0, %8;\n\t"
-              "@py add.rn.f64 %1, %1, %9;\n\t"
-              "@pz add.rn.f64 %2, %2, %10;\n\t"
-              "@px add.s32 %3, %3, -1;\n\t"
-              "@py add.s32 %4, %4, -1;\n\t"
-              "@pz add.s32 %5, %5, -1;\n\t"
-              "@px add.s32 %6, %6, %12;\n\t"
-              "@py add.s32 %6, %6, %13;\n\t"
-              "@pz add.s32 %6, %6, %14;\n\t"
-              "or.b32 m, %3, %4;\n\t"
-              "or.b32 m, m, %5;\n\t"
-              "setp.ge.s32 rg, m, 0;\n\t"
-              "and.pred ok, ok, rg;\n\t"
-              "selp.u32 %7, %7, 0, ok;\n\t"
-              "}"
-              : "+d"(t0), "+d"(t1), "+d"(t2), "+r"(r0), "+r"(r1), "+r"(r2), "+r"(uidx), "+r"(al)
-              : "d"(d0), "d"(d1), "d"(d2), "d"(stop), "r"(lin0), "r"(lin1), "r"(lin2));
-        }
-        alive = al != 0u;
+      for (int j = 0; j < kChunk; ++j) {
+        cell[j] = al ? uidx : 0xffffffffu;
+        // walk_ray's step (raytracer.hpp:103-116): the axis with the smallest
+        // tmax, ties x then y then z; the walk goes on while that tmax is
+        // below its threshold. t + 0 == t for the axes not taken (t >= 0).
+        asm("{\n\t"
+            ".reg .pred q, px, py, pz, npx, s0, s1, s2, ok;\n\t"
+            ".reg .f64 a0, a1, a2;\n\t"
+            ".reg .b32 l;\n\t"
+            "setp.le.f64 q, %0, %1;\n\t"
+            "setp.le.and.f64 px, %0, %2, q;\n\t"
+            "setp.le.f64 q, %1, %2;\n\t"
+            "not.pred npx, px;\n\t"
+            "and.pred py, q, npx;\n\t"
+            "or.pred pz, px, py;\n\t"
+            "not.pred pz, pz;\n\t"
+            "setp.lt.and.f64 s0, %0, %8, px;\n\t"
+            "setp.lt.and.f64 s1, %1, %9, py;\n\t"
+            "setp.lt.and.f64 s2, %2, %10, pz;\n\t"
+            "or.pred ok, s0, s1;\n\t"
+            "or.pred ok, ok, s2;\n\t"
+            "selp.u32 %4, %4, 0, ok;\n\t"
+            "selp.f64 a0, %5, 0d0000000000000000, px;\n\t"
+            "selp.f64 a1, %6, 0d0000000000000000, py;\n\t"
+            "selp.f64 a2, %7, 0d0000000000000000, pz;\n\t"
+            "add.rn.f64 %0, %0, a0;\n\t"
+            "add.rn.f64 %1, %1, a1;\n\t"
+            "add.rn.f64 %2, %2, a2;\n\t"
+            "selp.b32 l, %12, %13, py;\n\t"
+            "selp.b32 l, %11, l, px;\n\t"
+            "add.s32 %3, %3, l;\n\t"
+            "}"
+            : "+d"(t0), "+d"(t1), "+d"(t2), "+r"(uidx), "+r"(al)
+            : "d"(e0), "d"(e1), "d"(e2), "d"(M0), "d"(M1), "d"(M2), "r"(lin0), "r"(lin1), "r"(lin2));
       }
+      alive = al != 0u;
       resolve(cell);
     }
     freed += lw - lt;
