@@ -23,11 +23,14 @@ __global__ void encode_ms_kernel(const uint8_t* ms, uint8_t* occ, uint32_t* key,
   }
 }
 
+// keep_occupied: cells that were Occupied in ms before stay Occupied (the
+// vectorised dilation may zero occ bytes next to the cells it marks).
 __global__ void decode_ms_kernel(const uint8_t* occ, const uint32_t* key, uint8_t* ms,
-                                 long long n, uint32_t epoch) {
+                                 long long n, uint32_t epoch, int keep_occupied = 0) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    ms[i] = static_cast<uint8_t>(decode_cell(occ[i], key[i], epoch));
+    const uint32_t v = decode_cell(occ[i], key[i], epoch);
+    ms[i] = static_cast<uint8_t>(keep_occupied && ms[i] == 2 ? 2u : v);
   }
 }
 

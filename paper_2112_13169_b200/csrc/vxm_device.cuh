@@ -115,6 +115,7 @@ struct KParams {
   // buffers (stream s at offset s*n)
   uint8_t* occ;
   uint8_t* ctr;        // centre bytes when vox_inf > 0
+  uint8_t* rowflag;    // [dy*dz] per slot: == epoch when the x-row holds a centre (vox_inf > 0)
   uint32_t* dbits;     // x-dilated centre bit rows [dy*dz][row words] (vox_inf > 0)
   uint32_t* key;
   uint8_t* loc0;

@@ -22,7 +22,8 @@ namespace vxm {
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ unsigned populate_point(const KParams& p, const double* R,
                                                    const double* t, uint8_t* target,
-                                                   uint8_t mark, double x, double y, double z) {
+                                                   uint8_t* rowflag, uint8_t mark, double x,
+                                                   double y, double z) {
   int c[3];
   transform_voxelize(R, t, x, y, z, p.vs, p.inv_vs, c);
   if (static_cast<unsigned>(c[0]) >= static_cast<unsigned>(p.dx) ||
@@ -33,6 +34,8 @@ __device__ __forceinline__ unsigned populate_point(const KParams& p, const doubl
   const uint32_t idx = static_cast<uint32_t>(c[0]) + static_cast<uint32_t>(c[1]) * p.dx +
                        static_cast<uint32_t>(c[2]) * static_cast<uint32_t>(p.dx * p.dy);
   target[idx] = mark;  // idempotent: every writer stores the same byte
+  // the dilation only visits x-rows that hold a centre this frame
+  if (rowflag) rowflag[static_cast<uint32_t>(c[1]) + static_cast<uint32_t>(c[2]) * p.dy] = mark;
   return 0u;
 }
 
@@ -54,6 +57,7 @@ __global__ void __launch_bounds__(256) populate_depth_kernel(KParams p, int iter
   const FrameParams* fp = p.frames + s;
   const uint8_t mark = static_cast<uint8_t>(fp->epoch);
   uint8_t* target = (p.vox_inf > 0 ? p.ctr : p.occ) + static_cast<long long>(s) * p.n;
+  uint8_t* rowflag = p.vox_inf > 0 ? p.rowflag + static_cast<long long>(s) * p.dy * p.dz : nullptr;
   double R[9], t[3];
 #pragma unroll
   for (int i = 0; i < 9; ++i) R[i] = fp->rot[i];
@@ -82,7 +86,7 @@ __global__ void __launch_bounds__(256) populate_depth_kernel(KParams p, int iter
       const double D = static_cast<double>(d[k]);
       if (D > p.max_depth) continue;
       ++total;
-      outside += populate_point(p, R, t, target, mark, dmul(__ldg(p.qx + u), D),
+      outside += populate_point(p, R, t, target, rowflag, mark, dmul(__ldg(p.qx + u), D),
                                 dmul(__ldg(p.qy + v), D), D);
     }
     first = nfirst;
@@ -107,6 +111,7 @@ __global__ void __launch_bounds__(256) populate_depth_tma_kernel(KParams p, int 
   const FrameParams* fp = p.frames + s;
   const uint8_t mark = static_cast<uint8_t>(fp->epoch);
   uint8_t* target = (p.vox_inf > 0 ? p.ctr : p.occ) + static_cast<long long>(s) * p.n;
+  uint8_t* rowflag = p.vox_inf > 0 ? p.rowflag + static_cast<long long>(s) * p.dy * p.dz : nullptr;
   const float* depth = fp->depth;
   const int nq = (p.W * p.H) >> 2;
   const int T = blockDim.x;
@@ -156,7 +161,7 @@ __global__ void __launch_bounds__(256) populate_depth_tma_kernel(KParams p, int 
       const double D = static_cast<double>(d[k]);
       if (D > p.max_depth) continue;
       ++total;
-      outside += populate_point(p, R, t, target, mark, dmul(__ldg(p.qx + u), D),
+      outside += populate_point(p, R, t, target, rowflag, mark, dmul(__ldg(p.qx + u), D),
                                 dmul(__ldg(p.qy + v), D), D);
     }
   }
@@ -173,6 +178,7 @@ __global__ void __launch_bounds__(256) populate_cloud_kernel(KParams p) {
   const FrameParams* fp = p.frames + s;
   const uint8_t mark = static_cast<uint8_t>(fp->epoch);
   uint8_t* target = (p.vox_inf > 0 ? p.ctr : p.occ) + static_cast<long long>(s) * p.n;
+  uint8_t* rowflag = p.vox_inf > 0 ? p.rowflag + static_cast<long long>(s) * p.dy * p.dz : nullptr;
   double R[9], t[3];
 #pragma unroll
   for (int i = 0; i < 9; ++i) R[i] = fp->rot[i];
@@ -186,7 +192,7 @@ __global__ void __launch_bounds__(256) populate_cloud_kernel(KParams p) {
     const double x = xs[i], y = ys[i], z = zs[i];
     if (!(isfinite(x) && isfinite(y) && isfinite(z))) continue;
     ++total;
-    outside += populate_point(p, R, t, target, mark, x, y, z);
+    outside += populate_point(p, R, t, target, rowflag, mark, x, y, z);
   }
   unsigned vals[2] = {total, outside};
   unsigned long long* dst[2] = {&p.counters[s].points_total, &p.counters[s].points_outside};
@@ -228,7 +234,9 @@ __global__ void __launch_bounds__(256) dilate_rows_kernel(KParams p, int r) {
   const int WP = dilate_row_words(p.dx);
   const uint8_t* ctr = p.ctr + static_cast<long long>(s) * p.n;
   uint32_t* plane = p.dbits + static_cast<long long>(s) * rows * WP;
+  const uint8_t* rf = p.rowflag + static_cast<long long>(s) * rows;
   for (int row = row0; row < row0 + kDilRowsPerWarp && row < rows; ++row) {
+    if (rf[row] != e) continue;  // no centre in this row (K2b never reads its bits)
     const uint8_t* src = ctr + static_cast<uint32_t>(row) * p.dx;
     uint32_t mine = 0;  // lane w keeps word w
     for (int w0 = 0; w0 < W; w0 += 4) {
@@ -281,6 +289,9 @@ __global__ void __launch_bounds__(256) dilate_rows_vec_kernel(KParams p, int r) 
   const int rows = p.dy * p.dz;
   const int row0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * G;
   if (row0 >= rows) return;
+  // rows without a centre this frame are skipped (K2b never reads their bits)
+  const uint8_t* rf = p.rowflag + static_cast<long long>(s) * rows;
+  if (!__any_sync(0xffffffffu, lane < G && row0 + lane < rows && rf[row0 + lane] == e)) return;
   const int span = min(G, rows - row0) * p.dx;  // bytes of this group
   const uint8_t* src = p.ctr + static_cast<long long>(s) * p.n + static_cast<long long>(row0) * p.dx;
   uint32_t m = 0;  // bit i: byte 16*lane + i holds a centre
@@ -324,7 +335,8 @@ __global__ void __launch_bounds__(256) dilate_rows_vec_kernel(KParams p, int r) 
 // Shared memory of K2b: the (8+2r)^2 halo bit rows and the y-dilated rows.
 __host__ __device__ constexpr size_t dilate_smem_bytes(int r, int dx) {
   return sizeof(uint32_t) * static_cast<size_t>(dilate_row_words(dx)) *
-         (static_cast<size_t>(kDilT + 2 * r) * (kDilT + 2 * r) + static_cast<size_t>(kDilT) * (kDilT + 2 * r));
+             (static_cast<size_t>(kDilT + 2 * r) * (kDilT + 2 * r) + static_cast<size_t>(kDilT) * (kDilT + 2 * r)) +
+         ((static_cast<size_t>(kDilT + 2 * r) * (kDilT + 2 * r) + 3) & ~static_cast<size_t>(3));  // row flags
 }
 
 // K2b: a block owns an 8x8 (y,z) tile of x-dilated bit rows, loads them with
@@ -349,17 +361,25 @@ __global__ void __launch_bounds__(256) dilate_tiles_kernel(KParams p, int r_rt) 
   uint32_t* by = bx + (H * H << lg);    // [H z][kDilT y][WP], y-dilated
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
 
-  uint32_t any = 0;
+  uint8_t* fl = reinterpret_cast<uint8_t*>(by + ((H * kDilT) << lg));  // [H z][H y] row holds a centre
+  const uint8_t* rf = p.rowflag + static_cast<long long>(s) * p.dy * p.dz;
+  bool anyf = false;
+  for (int i = threadIdx.x; i < H * H; i += blockDim.x) {
+    const int hz = i / H, hy = i - hz * H;
+    const int y = y0 - r + hy, z = z0 - r + hz;
+    const bool f = y >= 0 && y < p.dy && z >= 0 && z < p.dz && rf[z * p.dy + y] == e;
+    fl[i] = f ? 1 : 0;
+    anyf = anyf || f;
+  }
+  // surfaces are sparse in 3-D: a tile with no centre within r writes nothing
+  if (!__syncthreads_or(anyf)) return;
   for (int i = threadIdx.x; i < (H * H) << lg; i += blockDim.x) {
     const int w = i & (WP - 1), row = i >> lg;
     const int hz = row / H, hy = row - hz * H;
     const int y = y0 - r + hy, z = z0 - r + hz;
-    const uint32_t v = (y >= 0 && y < p.dy && z >= 0 && z < p.dz) ? __ldg(plane + ((z * p.dy + y) << lg) + w) : 0u;
-    bx[i] = v;
-    any |= v;
+    bx[i] = fl[row] ? __ldg(plane + ((z * p.dy + y) << lg) + w) : 0u;
   }
-  // surfaces are sparse in 3-D: a tile with no centre within r writes nothing
-  if (!__syncthreads_or(any != 0u)) return;
+  __syncthreads();
   for (int i = threadIdx.x; i < (H * kDilT) << lg; i += blockDim.x) {
     const int w = i & (WP - 1), yz = i >> lg;
     const int y = yz & (kDilT - 1), hz = yz / kDilT;
@@ -378,6 +398,27 @@ __global__ void __launch_bounds__(256) dilate_tiles_kernel(KParams p, int r_rt) 
     const int gy = y0 + y, gz = z0 + z;
     if (gy >= p.dy || gz >= p.dz) continue;
     uint8_t* dst = occ + static_cast<uint32_t>(gy) * p.dx + static_cast<uint32_t>(gz) * dxy;
+    if ((p.dx & 3) == 0) {
+      // 4 cells per lane, one 32-bit store per word holding a dilated cell:
+      // the tile owns its rows and the only other bytes this frame could
+      // have set are its own, so the rest of the word may become 0 (never an
+      // epoch); the stage API restores pre-existing Occupied cells itself
+      for (int x0 = lane * 4; x0 < p.dx; x0 += 128) {
+        const uint32_t* col = by + ((z * kDilT + y) << lg) + (x0 >> 5);
+        uint32_t d = 0;
+#pragma unroll
+        for (int k = 0; k <= 2 * (kR > 0 ? kR : 16); ++k) {
+          if (kR == 0 && k > 2 * r) break;
+          d |= col[(k * kDilT) << lg];
+        }
+        const uint32_t nib = (d >> (x0 & 31)) & 0xFu;
+        if (nib) {
+          const uint32_t m = ((nib * 0x00204081u) & 0x01010101u) * 0xFFu;  // 0xFF per set bit
+          *reinterpret_cast<uint32_t*>(dst + x0) = e * 0x01010101u & m;
+        }
+      }
+      continue;
+    }
     for (int w = 0; w < W; ++w) {
       const uint32_t* col = by + ((z * kDilT + y) << lg) + w;
       uint32_t d = 0;

@@ -235,11 +235,13 @@ struct vxm_ctx {
   cudaStream_t stream = nullptr;
   vxm::KParams kp{};
   long long n = 0;
+  long long rows = 0;  // x-rows per grid (dy * dz)
   int32_t bundle[3] = {0, 0, 0};
 
   // device buffers
   uint8_t* occ = nullptr;
   uint8_t* ctr = nullptr;
+  uint8_t* rowflag = nullptr;  // per slot: dy*dz x-row flags (vox_inf > 0)
   uint32_t* key = nullptr;
   uint8_t* loc[2] = {nullptr, nullptr};
   double* qtab = nullptr;  // W column + H row back-projection factors
@@ -448,6 +450,7 @@ void prepare_frames(vxm_ctx* c, const vxm_pose* poses, const float* depth_dev_ba
       if (c->epoch[slot] >= vxm::kMaxEpoch) {
         VXM_CK(cudaMemsetAsync(c->occ + c->n * slot, 0, c->n, c->stream));
         if (c->ctr) VXM_CK(cudaMemsetAsync(c->ctr + c->n * slot, 0, c->n, c->stream));
+        if (c->rowflag) VXM_CK(cudaMemsetAsync(c->rowflag + c->rows * slot, 0, c->rows, c->stream));
         VXM_CK(cudaMemsetAsync(c->key + c->n * slot, 0, sizeof(uint32_t) * c->n, c->stream));
         c->epoch[slot] = 0;
       }
@@ -554,6 +557,7 @@ void destroy_ctx(vxm_ctx* c) {
     if (e) cudaEventDestroy(e);
   cudaFree(c->occ);
   cudaFree(c->ctr);
+  cudaFree(c->rowflag);
   cudaFree(c->key);
   cudaFree(c->qtab);
   cudaFree(c->dbits);
@@ -666,6 +670,7 @@ int vxm_create_multi(const vxm_config* cfg, int32_t n_streams, int32_t frames_pe
     c->nsm = sm_count(device);
     const vxm_grid_spec& g = cfg->grid;
     c->n = static_cast<long long>(g.dims[0]) * g.dims[1] * g.dims[2];
+    c->rows = static_cast<long long>(g.dims[1]) * g.dims[2];
     bundle_dims(cfg->camera, cfg->depth, g.vox_size, c->bundle);
     const long long rays = static_cast<long long>(c->bundle[1]) * c->bundle[2];
     if (rays > static_cast<long long>(vxm::kMaxRays))
@@ -683,6 +688,8 @@ int vxm_create_multi(const vxm_config* cfg, int32_t n_streams, int32_t frames_pe
     if (cfg->vox_inf > 0) {
       VXM_CK(cudaMalloc(&c->ctr, c->n * S));
       VXM_CK(cudaMemsetAsync(c->ctr, 0, c->n * S, c->stream));
+      VXM_CK(cudaMalloc(&c->rowflag, c->rows * S));
+      VXM_CK(cudaMemsetAsync(c->rowflag, 0, c->rows * S, c->stream));
     }
     for (int b = 0; b < 2; ++b) {
       VXM_CK(cudaMalloc(&c->loc[b], c->n * NS));
@@ -744,6 +751,7 @@ int vxm_create_multi(const vxm_config* cfg, int32_t n_streams, int32_t frames_pe
     kp.tiles_y = (kp.vh + 3) / 4;
     kp.occ = c->occ;
     kp.ctr = c->ctr;
+    kp.rowflag = c->rowflag;
     kp.key = c->key;
     kp.loc0 = c->loc[0];
     kp.loc1 = c->loc[1];

@@ -116,6 +116,7 @@ int vxm_populate_occupied(const vxm_grid_spec* grid, uint8_t* ms, const double* 
     vxm::KParams kp = grid_params(*grid);
     const long long N = kp.n;
     DevBuf<uint8_t> d_ms(N), d_occ(N), d_ctr(vox_inf > 0 ? N : 0);
+    DevBuf<uint8_t> d_rowflag(vox_inf > 0 ? static_cast<long long>(kp.dy) * kp.dz : 0);
     DevBuf<uint32_t> d_key(N);
     DevBuf<double> d_pts(3 * n + 1);
     DevBuf<vxm::Counters> d_cnt(1);
@@ -136,10 +137,12 @@ int vxm_populate_occupied(const vxm_grid_spec* grid, uint8_t* ms, const double* 
     VXM_SCK(cudaMemcpy(d_ms.p, ms, N, cudaMemcpyHostToDevice));
     VXM_SCK(cudaMemset(d_cnt.p, 0, sizeof(vxm::Counters)));
     if (d_ctr.p) VXM_SCK(cudaMemset(d_ctr.p, 0, N));
+    if (d_rowflag.p) VXM_SCK(cudaMemset(d_rowflag.p, 0, static_cast<size_t>(kp.dy) * kp.dz));
     vxm::encode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_ms.p, d_occ.p, d_key.p, N, kEpoch);
     kp.occ = d_occ.p;
     kp.key = d_key.p;
     kp.ctr = d_ctr.p;
+    kp.rowflag = d_rowflag.p;
     kp.vox_inf = vox_inf;
     kp.counters = d_cnt.p;
     kp.frames = d_frame.p;
@@ -156,7 +159,7 @@ int vxm_populate_occupied(const vxm_grid_spec* grid, uint8_t* ms, const double* 
       vxm::launch_dilate(kp, r, 1, smem, 0);
       VXM_SCK(cudaGetLastError());
     }
-    vxm::decode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_occ.p, d_key.p, d_ms.p, N, kEpoch);
+    vxm::decode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_occ.p, d_key.p, d_ms.p, N, kEpoch, 1);
     VXM_SCK(cudaGetLastError());
     vxm::Counters cnt{};
     VXM_SCK(cudaMemcpy(&cnt, d_cnt.p, sizeof(cnt), cudaMemcpyDeviceToHost));
