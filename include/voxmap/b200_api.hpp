@@ -22,11 +22,13 @@
 #include <cstddef>
 #include <cstdint>
 #include <cstdlib>
+#include <iosfwd>
 #include <limits>
 #include <memory>
 #include <optional>
 #include <span>
 #include <stdexcept>
+#include <string>
 #include <vector>
 
 #include "vxm.h"
@@ -116,6 +118,13 @@ class VoxelGrid {
 };
 
 VoxelGrid shift_grid_by(const VoxelGrid& grid, const Eigen::Vector3i& offset_voxels);
+
+// grid_io (proj/include/voxmap/grid_io.hpp:10-17): VOXGRID1 dumps, host only;
+// std::runtime_error on I/O or format errors.
+void write_grid(const VoxelGrid& grid, std::ostream& out);
+void write_grid(const VoxelGrid& grid, const std::string& path);
+VoxelGrid read_grid(std::istream& in);
+VoxelGrid read_grid(const std::string& path);
 VoxelGrid shift_grid(const VoxelGrid& grid, const Eigen::Vector3d& new_center);
 Eigen::Vector3i shift_offset_for_center(const GridSpec& spec, const Eigen::Vector3d& new_center);
 
@@ -365,6 +374,10 @@ class MappingPipeline {
 
   const VoxelGrid& local_grid() const;
   const PipelineConfig& config() const { return cfg_; }
+  // Extension (checkpoint/resume): continue from a saved
+  // local grid, e.g. read_grid(path) of an earlier write_grid(local_grid()).
+  // Its dims and vox_size must match the configuration's grid.
+  void restore_local_grid(const VoxelGrid& grid);
 
  private:
   PipelineConfig cfg_;

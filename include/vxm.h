@@ -35,7 +35,8 @@ enum vxm_status {
   VXM_ECUDA = 2,    /* CUDA runtime / launch failure */
   VXM_ENOMEM = 3,   /* device or pinned host allocation failed */
   VXM_ENODEV = 4,   /* no sm_100 device visible */
-  VXM_ESTATE = 5    /* call not valid in the context's current state */
+  VXM_ESTATE = 5,   /* call not valid in the context's current state */
+  VXM_EIO = 6       /* file I/O or format error (reference: std::runtime_error) */
 };
 
 /* Voxel states, one byte per cell (proj/include/voxmap/voxel_state.hpp:9-17). */
@@ -192,6 +193,18 @@ int vxm_download_local(vxm_ctx* ctx, int32_t s, uint8_t* cells, double origin[3]
 /* Restores stream `s`'s local grid (checkpoint/resume, grid_io.cpp:14-63). */
 int vxm_upload_local(vxm_ctx* ctx, int32_t s, const uint8_t* cells, const double origin[3]);
 
+/* VOXGRID1 grid dumps, the reference's snapshot format
+ * (proj/include/voxmap/grid_io.hpp:10-17, proj/src/grid_io.cpp:14-69): text
+ * header (magic, dims, vox_size, origin with 17 significant digits) then one
+ * state byte per cell. vxm_grid_read fills *spec (size = dims * vox_size) and,
+ * when cells != NULL, copies the cells (capacity >= cell count). Host only,
+ * no GPU needed. VXM_EIO for I/O or format errors. */
+int vxm_grid_write(const char* path, const vxm_grid_spec* spec, const uint8_t* cells);
+int vxm_grid_read(const char* path, vxm_grid_spec* spec, uint8_t* cells, size_t capacity);
+/* Checkpoint / resume of stream s's local grid (cells + origin) through a
+ * VOXGRID1 file; the file's dims and vox_size must match the context. */
+int vxm_snapshot_save(vxm_ctx* ctx, int32_t s, const char* path);
+int vxm_snapshot_load(vxm_ctx* ctx, int32_t s, const char* path);
 /* The context's CUDA stream (cudaStream_t) and the device time of the last
  * integrate call's kernels in milliseconds (CUDA events on that stream). */
 void* vxm_cuda_stream(vxm_ctx* ctx);

@@ -40,6 +40,8 @@ SIGS = {
     "ref_trace_bundle": (C.c_int, [P(N.GridSpecC), _u8p, _i32p, P(N.PoseC), C.c_int, P(N.TraceStatsC)]),
     "ref_trace_per_pixel": (C.c_int, [P(N.GridSpecC), _u8p, _f64p, _f64p, _f64p, C.c_size_t, P(N.PoseC), P(N.TraceStatsC)]),
     "ref_shift": (C.c_int, [P(N.GridSpecC), _u8p, _u8p, _i32p]),
+    "ref_write_grid": (C.c_int, [P(N.GridSpecC), _u8p, C.c_char_p]),
+    "ref_read_grid": (C.c_int, [C.c_char_p, P(N.GridSpecC), C.c_void_p, C.c_size_t]),
     "ref_pipeline_create": (C.c_void_p, [P(N.ConfigC), C.c_int]),
     "ref_pipeline_destroy": (None, [C.c_void_p]),
     "ref_pipeline_integrate_cloud": (C.c_int, [C.c_void_p, _f64p, _f64p, _f64p, C.c_size_t, P(N.PoseC), P(N.StatsC)]),
@@ -165,6 +167,20 @@ def shift(grid_c, cells, off):
     o = np.asarray(off, dtype=np.int32)
     _check(lib().ref_shift(C.byref(grid_c), _u8(cells), _u8(out), _i32(o)))
     return out
+
+
+def write_grid(grid_c, cells, path):
+    cells = np.ascontiguousarray(cells, dtype=np.uint8)
+    _check(lib().ref_write_grid(C.byref(grid_c), _u8(cells), str(path).encode()))
+
+
+def read_grid(path):
+    """-> (GridSpecC, cells) through the reference's read_grid"""
+    g = N.GridSpecC()
+    _check(lib().ref_read_grid(str(path).encode(), C.byref(g), None, 0))
+    cells = np.empty(g.dims[0] * g.dims[1] * g.dims[2], dtype=np.uint8)
+    _check(lib().ref_read_grid(str(path).encode(), C.byref(g), cells.ctypes.data, cells.size))
+    return g, cells
 
 
 class Pipeline:

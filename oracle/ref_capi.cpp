@@ -14,6 +14,7 @@
 
 #include "../include/vxm.h"
 #include "voxmap/grid.hpp"
+#include "voxmap/grid_io.hpp"
 #include "voxmap/integrator.hpp"
 #include "voxmap/kernels/kernels.hpp"
 #include "voxmap/pipeline.hpp"
@@ -253,6 +254,32 @@ int ref_trace_per_pixel(const vxm_grid_spec* g, uint8_t* ms, const double* xs,
     st->voxels_freed = s.voxels_freed;
     st->voxels_marked_unknown_traced = s.voxels_marked_unknown_traced;
     st->voxels_skipped_out_of_bounds = s.voxels_skipped_out_of_bounds;
+  });
+}
+
+// grid_io (proj/src/grid_io.cpp): the reference's own VOXGRID1 writer/reader
+int ref_write_grid(const vxm_grid_spec* g, const uint8_t* cells, const char* path) {
+  return guarded([&] {
+    VoxelGrid grid(to_spec(*g));
+    std::memcpy(grid.raw(), cells, grid.size());
+    write_grid(grid, std::string(path));
+  });
+}
+
+int ref_read_grid(const char* path, vxm_grid_spec* g, uint8_t* cells, size_t capacity) {
+  return guarded([&] {
+    const VoxelGrid grid = read_grid(std::string(path));
+    const GridSpec& s = grid.spec();
+    g->size[0] = s.grid_size_x;
+    g->size[1] = s.grid_size_y;
+    g->size[2] = s.grid_size_z;
+    g->vox_size = s.vox_size;
+    g->dims[0] = s.dims_x;
+    g->dims[1] = s.dims_y;
+    g->dims[2] = s.dims_z;
+    g->pad_ = 0;
+    for (int a = 0; a < 3; ++a) g->origin[a] = s.origin[a];
+    if (cells && capacity >= grid.size()) std::memcpy(cells, grid.raw(), grid.size());
   });
 }
 

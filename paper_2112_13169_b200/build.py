@@ -27,7 +27,7 @@ NVFLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler",
 
 CU_SOURCES = ["vxm_unity.cu"]
 CU_INCLUDED = ["vxm_runtime.cu", "vxm_stages.cu"]
-CU_HEADERS = ["vxm_device.cuh", "vxm_kernels.cuh", "vxm_aux_kernels.cuh"]
+CU_HEADERS = ["vxm_device.cuh", "vxm_kernels.cuh", "vxm_aux_kernels.cuh", "host/voxgrid_format.hpp"]
 
 
 def _run(cmd, cwd=None):
@@ -70,8 +70,9 @@ def build_dropin(force=False):
     plus the C++ test driver tests/cpp/build/test_dropin."""
     lib = LIBDIR / "libvoxmap_b200.so"
     src = CSRC / "host" / "voxmap_api.cpp"
+    fmt = CSRC / "host" / "voxgrid_format.hpp"
     hdrs = list((ROOT / "include" / "voxmap").rglob("*.hpp")) + [ROOT / "include" / "vxm.h"]
-    if force or _stale(lib, [src, LIBDIR / "libvxm.so", *hdrs]):
+    if force or _stale(lib, [src, fmt, LIBDIR / "libvxm.so", *hdrs]):
         _run([*HOST_CXX, "-shared", str(src), f"-L{LIBDIR}", "-lvxm", "-Wl,-rpath,$ORIGIN", "-o", str(lib)])
     test_src = ROOT / "tests" / "cpp" / "test_dropin.cpp"
     test_bin = ROOT / "tests" / "cpp" / "build" / "test_dropin"

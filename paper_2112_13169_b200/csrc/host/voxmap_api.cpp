@@ -7,11 +7,16 @@
 
 #include <cmath>
 #include <cstring>
+#include <fstream>
+#include <istream>
+#include <iterator>
 #include <numbers>
+#include <ostream>
 #include <stdexcept>
 #include <string>
 #include <utility>
 
+#include "voxgrid_format.hpp"
 #include "voxmap/b200_api.hpp"
 
 namespace voxmap {
@@ -468,6 +473,61 @@ const VoxelGrid& MappingPipeline::local_grid() const {
     local_stale_ = false;
   }
   return local_;
+}
+
+// ---------------------------------------------------------------- grid io
+
+void write_grid(const VoxelGrid& grid, std::ostream& out) {
+  const GridSpec& g = grid.spec();
+  const int dims[3] = {g.dims_x, g.dims_y, g.dims_z};
+  const double origin[3] = {g.origin.x(), g.origin.y(), g.origin.z()};
+  const std::string h = vxm_io::voxgrid_header(dims, g.vox_size, origin);
+  out.write(h.data(), static_cast<std::streamsize>(h.size()));
+  out.write(reinterpret_cast<const char*>(grid.raw()), static_cast<std::streamsize>(grid.size()));
+  if (!out) throw std::runtime_error("write_grid: stream write failed");
+}
+
+void write_grid(const VoxelGrid& grid, const std::string& path) {
+  std::ofstream out(path, std::ios::binary);
+  if (!out) throw std::runtime_error("write_grid: cannot open " + path);
+  write_grid(grid, out);
+}
+
+VoxelGrid read_grid(std::istream& in) {
+  const std::string buf((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  vxm_io::VoxgridHeader h;
+  std::string err = vxm_io::parse_voxgrid_header(buf.data(), buf.size(), h);
+  if (err.empty()) err = vxm_io::check_voxgrid_cells(buf.data(), buf.size(), h);
+  if (!err.empty()) throw std::runtime_error(err);
+  GridSpec spec;
+  spec.dims_x = h.dims[0];
+  spec.dims_y = h.dims[1];
+  spec.dims_z = h.dims[2];
+  spec.vox_size = h.vox_size;
+  spec.grid_size_x = h.dims[0] * h.vox_size;
+  spec.grid_size_y = h.dims[1] * h.vox_size;
+  spec.grid_size_z = h.dims[2] * h.vox_size;
+  spec.origin = Eigen::Vector3d(h.origin[0], h.origin[1], h.origin[2]);
+  VoxelGrid grid(spec);
+  std::memcpy(grid.raw(), buf.data() + h.data_offset, grid.size());
+  return grid;
+}
+
+VoxelGrid read_grid(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw std::runtime_error("read_grid: cannot open " + path);
+  return read_grid(in);
+}
+
+void MappingPipeline::restore_local_grid(const VoxelGrid& grid) {
+  const GridSpec& a = grid.spec();
+  const GridSpec& b = cfg_.grid;
+  if (a.dims_x != b.dims_x || a.dims_y != b.dims_y || a.dims_z != b.dims_z || a.vox_size != b.vox_size)
+    throw std::invalid_argument("restore_local_grid: grid layout differs from the pipeline's");
+  const double origin[3] = {a.origin.x(), a.origin.y(), a.origin.z()};
+  check(vxm_upload_local(seq_active_ ? seq_ctx_ : ctx_, 0, grid.raw(), origin));
+  local_ = grid;
+  local_stale_ = false;
 }
 
 // ----------------------------------------------------------- kernel table

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "../../include/vxm.h"
+#include "host/voxgrid_format.hpp"
 #include "vxm_aux_kernels.cuh"
 #include "vxm_kernels.cuh"
 
@@ -51,6 +52,10 @@ struct InvalidArg {
   std::string what;
 };
 
+struct IoError {
+  std::string what;
+};
+
 template <typename F>
 int guarded(F&& f) {
   try {
@@ -60,6 +65,8 @@ int guarded(F&& f) {
     return e.code;
   } catch (const InvalidArg& e) {
     return fail(VXM_EINVAL, e.what);
+  } catch (const IoError& e) {
+    return fail(VXM_EIO, e.what);
   } catch (const std::bad_alloc&) {
     return fail(VXM_ENOMEM, "host allocation failed");
   }
@@ -949,6 +956,94 @@ int vxm_upload_local(vxm_ctx* ctx, int32_t s, const uint8_t* cells, const double
       VXM_CK(cudaMemcpy(ctx->loc[ctx->cur[s]] + ctx->n * s, cells, ctx->n, cudaMemcpyHostToDevice));
     if (origin)
       for (int a = 0; a < 3; ++a) ctx->origin[3 * s + a] = origin[a];
+  });
+}
+
+// ---------------------------------------------------------------------------
+// VOXGRID1 snapshots (proj/include/voxmap/grid_io.hpp:10-17, grid_io.cpp:14-69)
+// ---------------------------------------------------------------------------
+namespace {
+void write_voxgrid(const char* path, const int dims[3], double vs, const double origin[3], const uint8_t* cells) {
+  FILE* f = std::fopen(path, "wb");
+  if (!f) throw IoError{std::string("write_grid: cannot open ") + path};
+  const std::string h = vxm_io::voxgrid_header(dims, vs, origin);
+  const size_t n = static_cast<size_t>(dims[0]) * dims[1] * dims[2];
+  const bool ok = std::fwrite(h.data(), 1, h.size(), f) == h.size() && std::fwrite(cells, 1, n, f) == n;
+  if (std::fclose(f) != 0 || !ok) throw IoError{"write_grid: stream write failed"};
+}
+
+std::vector<char> slurp(const char* path) {
+  FILE* f = std::fopen(path, "rb");
+  if (!f) throw IoError{std::string("read_grid: cannot open ") + path};
+  std::vector<char> buf;
+  char tmp[1 << 16];
+  size_t got;
+  while ((got = std::fread(tmp, 1, sizeof(tmp), f)) > 0) buf.insert(buf.end(), tmp, tmp + got);
+  std::fclose(f);
+  return buf;
+}
+
+vxm_io::VoxgridHeader read_voxgrid(const std::vector<char>& buf) {
+  vxm_io::VoxgridHeader h;
+  std::string err = vxm_io::parse_voxgrid_header(buf.data(), buf.size(), h);
+  if (err.empty()) err = vxm_io::check_voxgrid_cells(buf.data(), buf.size(), h);
+  if (!err.empty()) throw IoError{err};
+  return h;
+}
+}  // namespace
+
+int vxm_grid_write(const char* path, const vxm_grid_spec* spec, const uint8_t* cells) {
+  return guarded([&] {
+    if (!path || !spec || !cells) throw InvalidArg{"null argument"};
+    write_voxgrid(path, spec->dims, spec->vox_size, spec->origin, cells);
+  });
+}
+
+int vxm_grid_read(const char* path, vxm_grid_spec* spec, uint8_t* cells, size_t capacity) {
+  return guarded([&] {
+    if (!path || !spec) throw InvalidArg{"null argument"};
+    const std::vector<char> buf = slurp(path);
+    const vxm_io::VoxgridHeader h = read_voxgrid(buf);
+    std::memset(spec, 0, sizeof(*spec));
+    for (int a = 0; a < 3; ++a) {
+      spec->dims[a] = h.dims[a];
+      spec->size[a] = h.dims[a] * h.vox_size;  // grid_io.cpp: grid_size = dims * vox_size
+      spec->origin[a] = h.origin[a];
+    }
+    spec->vox_size = h.vox_size;
+    if (cells) {
+      if (capacity < h.cells()) throw InvalidArg{"read_grid: cell buffer too small"};
+      std::memcpy(cells, buf.data() + h.data_offset, h.cells());
+    }
+  });
+}
+
+int vxm_snapshot_save(vxm_ctx* ctx, int32_t s, const char* path) {
+  return guarded([&] {
+    if (!ctx || s < 0 || s >= ctx->S) throw InvalidArg{"stream index out of range"};
+    if (!path) throw InvalidArg{"null path"};
+    VXM_CK(cudaSetDevice(ctx->device));
+    collect_stats(ctx, nullptr);
+    std::vector<uint8_t> cells(static_cast<size_t>(ctx->n));
+    VXM_CK(cudaMemcpy(cells.data(), ctx->loc[ctx->cur[s]] + ctx->n * s, ctx->n, cudaMemcpyDeviceToHost));
+    write_voxgrid(path, ctx->cfg.grid.dims, ctx->cfg.grid.vox_size, &ctx->origin[3 * s], cells.data());
+  });
+}
+
+int vxm_snapshot_load(vxm_ctx* ctx, int32_t s, const char* path) {
+  return guarded([&] {
+    if (!ctx || s < 0 || s >= ctx->S) throw InvalidArg{"stream index out of range"};
+    if (!path) throw InvalidArg{"null path"};
+    const std::vector<char> buf = slurp(path);
+    const vxm_io::VoxgridHeader h = read_voxgrid(buf);
+    const vxm_grid_spec& g = ctx->cfg.grid;
+    if (h.dims[0] != g.dims[0] || h.dims[1] != g.dims[1] || h.dims[2] != g.dims[2] || h.vox_size != g.vox_size)
+      throw InvalidArg{"snapshot grid does not match the pipeline's GridSpec"};
+    VXM_CK(cudaSetDevice(ctx->device));
+    collect_stats(ctx, nullptr);
+    VXM_CK(cudaMemcpy(ctx->loc[ctx->cur[s]] + ctx->n * s, buf.data() + h.data_offset, ctx->n,
+                      cudaMemcpyHostToDevice));
+    for (int a = 0; a < 3; ++a) ctx->origin[3 * s + a] = h.origin[a];
   });
 }
 

@@ -250,6 +250,14 @@ class MappingPipeline:
         origin = np.ascontiguousarray(origin, dtype=np.float64)
         N.check(self._lib.vxm_upload_local(self._ctx, s, _u8(cells), _f64(origin)))
 
+    def save_snapshot(self, path, s=0):
+        """Checkpoint stream s's local grid as a VOXGRID1 file (grid_io.cpp:14-29)."""
+        N.check(self._lib.vxm_snapshot_save(self._ctx, s, str(path).encode()))
+
+    def load_snapshot(self, path, s=0):
+        """Resume stream s from a VOXGRID1 file of the same grid layout."""
+        N.check(self._lib.vxm_snapshot_load(self._ctx, s, str(path).encode()))
+
     def set_origin(self, origin, s=0):
         """Places stream s's (empty) local grid, e.g. centred on that stream's
         first camera position (pipeline.hpp:63)."""
@@ -270,6 +278,25 @@ class MappingPipeline:
     @property
     def cuda_stream(self) -> int:
         return self._lib.vxm_cuda_stream(self._ctx) or 0
+
+
+# --- VOXGRID1 dumps (proj/include/voxmap/grid_io.hpp:10-17), host only ----------
+
+def write_grid(grid: "GridSpec", cells, path):
+    cells = np.ascontiguousarray(cells, dtype=np.uint8)
+    if cells.size != grid.cell_count():
+        raise ValueError("write_grid: cell count does not match the grid")
+    N.check(N.load().vxm_grid_write(str(path).encode(), C.byref(grid.c), _u8(cells)))
+
+
+def read_grid(path):
+    """-> (GridSpec, cells uint8[N])"""
+    spec = N.GridSpecC()
+    lib = N.load()
+    N.check(lib.vxm_grid_read(str(path).encode(), C.byref(spec), None, 0))
+    cells = np.empty(spec.dims[0] * spec.dims[1] * spec.dims[2], dtype=np.uint8)
+    N.check(lib.vxm_grid_read(str(path).encode(), C.byref(spec), _u8(cells), cells.size))
+    return GridSpec(spec), cells
 
 
 # --- free functions (stage entry points on host grids) --------------------------

@@ -228,6 +228,31 @@ static void pipeline_cases() {
   }
 }
 
+static void gridio_cases() {
+  // VOXGRID1 round trip (grid_io.hpp) and checkpoint/resume of a pipeline
+  PipelineConfig cfg = small_config();
+  MappingPipeline a(cfg);
+  DepthImage img(320, 240);
+  for (int v = 0; v < 240; ++v)
+    for (int u = 0; u < 320; ++u) img.at(u, v) = (u / 40 + v / 30) % 3 == 0 ? 0.0f : 1.5f + 0.004f * u;
+  a.integrate_depth(img, look_along_x({0.0, 0.2, 0.0}));
+  a.integrate_depth(img, look_along_x({0.1, 0.4, 0.0}));
+  const std::string path = "/tmp/vxm_dropin_snapshot.vox";
+  write_grid(a.local_grid(), path);
+  const VoxelGrid back = read_grid(path);
+  CHECK(back == a.local_grid());
+  CHECK(back.spec().origin == a.local_grid().spec().origin);
+  MappingPipeline b(cfg);
+  b.restore_local_grid(back);
+  const PipelineStats sa = a.integrate_depth(img, look_along_x({0.2, 0.55, 0.0}));
+  const PipelineStats sb = b.integrate_depth(img, look_along_x({0.2, 0.55, 0.0}));
+  CHECK(sa.freed_count == sb.freed_count && sa.occupied_count == sb.occupied_count);
+  CHECK(a.local_grid() == b.local_grid());
+  CHECK_THROWS_AS(read_grid(std::string("/tmp/definitely_missing_grid.vox")), std::runtime_error);
+  VoxelGrid other(GridSpec::create(1.0, 1.0, 1.0, 0.1));
+  CHECK_THROWS_AS(b.restore_local_grid(other), std::invalid_argument);
+}
+
 static void grid_cases() {
   const GridSpec spec = GridSpec::create_centered(15.0, 15.0, 3.0, 0.15, Eigen::Vector3d::Zero());
   CHECK(spec.dims_x == 100 && spec.dims_y == 100 && spec.dims_z == 20);
@@ -250,6 +275,7 @@ int main() {
     raytracer_cases();
     pipeline_cases();
     grid_cases();
+    gridio_cases();
   } catch (const std::exception& e) {
     std::fprintf(stderr, "FAIL: uncaught %s\n", e.what());
     ++g_fail;

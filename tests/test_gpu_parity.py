@@ -142,7 +142,9 @@ def test_populate_dilation_row_layouts(gpu_lib, dims, vox_inf):
     for n in (1, 50, 3000):
         xs, ys, zs = (rng.uniform(-0.3, d * vox + 0.3, n) for d in dims)
         pose = vm.identity_pose()
-        ms_ref = np.zeros(grid.cell_count(), dtype=np.uint8)
+        # pre-existing states (populate never clears, test_integrator.cpp:127-137)
+        ms_ref = rng.integers(0, 4, grid.cell_count()).astype(np.uint8) if n == 50 else \
+            np.zeros(grid.cell_count(), dtype=np.uint8)
         ms_gpu = ms_ref.copy()
         st_ref = ref.populate(grid.c, ms_ref, xs, ys, zs, pose, vox_inf)
         st_gpu = vm.populate_occupied(grid, ms_gpu, xs, ys, zs, pose, vox_inf)
@@ -384,3 +386,35 @@ def test_async_double_buffered_host_path(gpu_lib):
             sr = refs[s].integrate_depth(frames[k][s], poses[k][s])
         assert last[s]["freed_count"] == sr["freed_count"]
         assert np.array_equal(pipe.local_grid(s)[0], refs[s].local_grid()[0]), s
+
+
+def test_snapshot_save_resume_matches_uninterrupted(gpu_lib, tmp_path):
+    """Checkpoint/resume through VOXGRID1 files: a pipeline
+    resumed from a snapshot continues exactly like the uninterrupted one, and
+    the snapshot file equals the reference's write_grid of the same grid."""
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 96, 72, 6.5)
+    grid = vm.GridSpec.create_centered(6.0, 6.0, 3.0, 0.1, (0.0, 0.0, 0.0))
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=1, depth=6.5)
+    boxes = scenes.box_field_boxes(2)
+    poses = [vm.look_along_x((0.05 * k, 0.12 * k - 0.4, 0.0)) for k in range(10)]
+    frames = [scenes.render(cam, p, boxes) for p in poses]
+    full = vm.MappingPipeline(cfg, n_streams=2)
+    for k in range(5):
+        full.integrate_depth(np.stack([frames[k]] * 2), [poses[k]] * 2)
+    snap = tmp_path / "s1.vox"
+    full.save_snapshot(snap, s=1)
+    cells, origin = full.local_grid(1)
+    g = vm.GridSpec.create(6.0, 6.0, 3.0, 0.1, origin)
+    ref.write_grid(g.c, cells, tmp_path / "ref.vox")
+    assert snap.read_bytes() == (tmp_path / "ref.vox").read_bytes()
+    resumed = vm.MappingPipeline(cfg)
+    resumed.load_snapshot(snap)
+    for k in range(5, 10):
+        sf = full.integrate_depth(np.stack([frames[k]] * 2), [poses[k]] * 2)[1]
+        sr = resumed.integrate_depth(frames[k], poses[k])
+        assert sf["freed_count"] == sr["freed_count"] and sf["origin"] == sr["origin"], k
+    assert np.array_equal(full.local_grid(1)[0], resumed.local_grid()[0])
+    bad = vm.MappingPipeline(vm.PipelineConfig(vm.GridSpec.create_centered(6.0, 6.0, 3.0, 0.15, (0, 0, 0)),
+                                               cam, vox_inf=1, depth=6.5))
+    with pytest.raises(ValueError, match="does not match"):
+        bad.load_snapshot(snap)
