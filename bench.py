@@ -243,7 +243,10 @@ def our_arm(args, world, rank, local):
     cam = vm.CameraModel(85 * DEG, 101 * DEG, c["width"], c["height"], c["depth"])
     boxes = scenes.box_field_boxes(1)
     poses = [vm.look_along_x((0.0, Y0 + 0.1001 * j, 0.0)) for j in range(POOL)]
-    pool = np.stack([scenes.render(cam, poses[j], boxes) for j in range(POOL)])  # (P, H, W)
+    # the frame pool is rendered on the GPU (vxm_render_depth, bit-identical to
+    # the reference's sim::render_depth); frame 0 is checked against the host
+    pool = vm.render_depth(cam, poses, boxes)  # (P, H, W)
+    assert np.array_equal(pool[0], scenes.render(cam, poses[0], boxes))
     npix = c["width"] * c["height"]
 
     # this rank's streams (global ids); slot q holds, for every stream g,

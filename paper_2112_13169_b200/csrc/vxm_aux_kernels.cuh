@@ -176,4 +176,66 @@ __global__ void __launch_bounds__(256) cloud_write_rows_kernel(const float* dept
 // Stand-alone trace: fold K3's slots (K4 does this in the per-frame graph).
 __global__ void fold_trace_slots_kernel(Counters* c) { fold_trace_slots(*c); }
 
+// ---------------------------------------------------------------------------
+// sim::render_depth (proj/src/sim/render.cpp:26-58) with ray_box_hit
+// (render.cpp:8-24): one thread per pixel, a block row of frames per
+// blockIdx.y. dir = R * ((u+0.5-cx)/fx, (v+0.5-cy)/fy, 1) with left-to-right
+// row sums (the Eigen subset's order), slab test per box with IEEE
+// divisions and std::max/std::min comparison semantics, nearest s > 0,
+// depth = (float)s when s <= max_depth, else the invalid sentinel 0.
+// boxes: nb x (minx miny minz maxx maxy maxz); poses: 12 doubles per frame
+// (R row-major, t).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) render_depth_kernel(const double* qtab, int W, int H, double max_depth,
+                                                           const double* poses, const double* boxes, int nb,
+                                                           float* out) {
+  extern __shared__ double sbox[];
+  const bool in_smem = nb <= 1024;
+  if (in_smem)
+    for (int i = threadIdx.x; i < 6 * nb; i += blockDim.x) sbox[i] = boxes[i];
+  __syncthreads();
+  const double* bx = in_smem ? sbox : boxes;
+  const int f = blockIdx.y;
+  const long long npix = static_cast<long long>(W) * H;
+  const long long pix = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (pix >= npix) return;
+  const int v = static_cast<int>(pix / W), u = static_cast<int>(pix - static_cast<long long>(v) * W);
+  const double* P = poses + 12 * f;
+  const double dc[3] = {qtab[u], qtab[W + v], 1.0};
+  double dir[3], o[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    dir[a] = dadd(dadd(dmul(P[3 * a], dc[0]), dmul(P[3 * a + 1], dc[1])), dmul(P[3 * a + 2], dc[2]));
+    o[a] = P[9 + a];
+  }
+  double best = __longlong_as_double(0x7ff0000000000000ll);
+  for (int b = 0; b < nb; ++b) {
+    const double* lo = bx + 6 * b;
+    const double* hi = lo + 3;
+    double t_near = -__longlong_as_double(0x7ff0000000000000ll);
+    double t_far = __longlong_as_double(0x7ff0000000000000ll);
+    bool miss = false;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (dir[a] == 0.0) {
+        miss = miss || o[a] < lo[a] || o[a] > hi[a];
+        continue;
+      }
+      double ta = ddiv(dsub(lo[a], o[a]), dir[a]);
+      double tb = ddiv(dsub(hi[a], o[a]), dir[a]);
+      if (ta > tb) {
+        const double w = ta;
+        ta = tb;
+        tb = w;
+      }
+      t_near = t_near < ta ? ta : t_near;  // std::max(t_near, ta)
+      t_far = tb < t_far ? tb : t_far;     // std::min(t_far, tb)
+    }
+    if (miss || t_near > t_far || t_far <= 0.0) continue;
+    const double s = t_near > 0.0 ? t_near : t_far;
+    if (s > 0.0 && s < best) best = s;
+  }
+  out[static_cast<long long>(f) * npix + pix] = best <= max_depth ? __double2float_rn(best) : 0.0f;
+}
+
 }  // namespace vxm

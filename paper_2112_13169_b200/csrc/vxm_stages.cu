@@ -312,6 +312,61 @@ int vxm_depth_to_cloud(const vxm_camera* cam, const float* depth, double* xs, do
   });
 }
 
+// sim::render_depth for n_frames poses. out: HOST or DEVICE
+// memory of n_frames * width * height floats.
+int vxm_render_depth(const vxm_camera* cam, const vxm_pose* t_wc, int32_t n_frames, const double* boxes,
+                     int32_t n_boxes, float* out) {
+  return stage_guard([&] {
+    if (!cam || !t_wc || !out || (n_boxes > 0 && !boxes)) throw StageError{VXM_EINVAL, "null argument"};
+    if (n_frames < 1 || n_boxes < 0) throw StageError{VXM_EINVAL, "n_frames must be >= 1, n_boxes >= 0"};
+    // CameraModel::validate (geometry.cpp:28-41) and Aabb::validate (scene.cpp:12-17)
+    const double pi = 3.14159265358979323846;
+    if (cam->width <= 0 || cam->height <= 0)
+      throw StageError{VXM_EINVAL, "CameraModel: width and height must be positive"};
+    if (!(cam->fov_x > 0.0) || !(cam->fov_x < pi) || !(cam->fov_y > 0.0) || !(cam->fov_y < pi))
+      throw StageError{VXM_EINVAL, "CameraModel: FOV must lie in (0, pi)"};
+    if (!(cam->max_depth > 0.0) || !std::isfinite(cam->max_depth))
+      throw StageError{VXM_EINVAL, "CameraModel: max_depth must be positive and finite"};
+    for (int b = 0; b < n_boxes; ++b)
+      for (int a = 0; a < 3; ++a) {
+        const double lo = boxes[6 * b + a], hi = boxes[6 * b + 3 + a];
+        if (!std::isfinite(lo) || !std::isfinite(hi) || !(lo < hi))
+          throw StageError{VXM_EINVAL, "Aabb: min must be strictly below max on every axis"};
+      }
+    const int W = cam->width, H = cam->height;
+    const size_t npix = static_cast<size_t>(W) * H;
+    // ((u + 0.5) - cx) / fx per column, likewise per row (render.cpp:30-41)
+    const double fx = (W / 2.0) / std::tan(cam->fov_x / 2.0);
+    const double fy = (H / 2.0) / std::tan(cam->fov_y / 2.0);
+    std::vector<double> q(static_cast<size_t>(W) + H);
+    for (int u = 0; u < W; ++u) q[u] = ((u + 0.5) - W / 2.0) / fx;
+    for (int v = 0; v < H; ++v) q[W + v] = ((v + 0.5) - H / 2.0) / fy;
+    std::vector<double> P(12 * static_cast<size_t>(n_frames));
+    for (int f = 0; f < n_frames; ++f) {
+      for (int i = 0; i < 9; ++i) P[12 * f + i] = t_wc[f].rotation[i];
+      for (int i = 0; i < 3; ++i) P[12 * f + 9 + i] = t_wc[f].translation[i];
+    }
+    DevBuf<double> d_q(q.size()), d_p(P.size()), d_b(6 * static_cast<size_t>(n_boxes) + 1);
+    VXM_SCK(cudaMemcpy(d_q.p, q.data(), sizeof(double) * q.size(), cudaMemcpyHostToDevice));
+    VXM_SCK(cudaMemcpy(d_p.p, P.data(), sizeof(double) * P.size(), cudaMemcpyHostToDevice));
+    if (n_boxes) VXM_SCK(cudaMemcpy(d_b.p, boxes, sizeof(double) * 6 * n_boxes, cudaMemcpyHostToDevice));
+    cudaPointerAttributes attr{};
+    const bool dev_out = cudaPointerGetAttributes(&attr, out) == cudaSuccess && attr.type == cudaMemoryTypeDevice;
+    cudaGetLastError();
+    DevBuf<float> d_out(dev_out ? 0 : npix * n_frames);
+    float* dst = dev_out ? out : d_out.p;
+    const size_t smem = n_boxes <= 1024 ? sizeof(double) * 6 * n_boxes : 0;
+    vxm::render_depth_kernel<<<dim3(static_cast<unsigned>((npix + 255) / 256), n_frames), 256, smem>>>(
+        d_q.p, W, H, cam->max_depth, d_p.p, d_b.p, n_boxes, dst);
+    VXM_SCK(cudaGetLastError());
+    if (dev_out) {
+      VXM_SCK(cudaDeviceSynchronize());
+    } else {
+      VXM_SCK(cudaMemcpy(out, d_out.p, sizeof(float) * npix * n_frames, cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
 // KernelTable adapter. The reference signatures are void with no error
 // channel, so a failure here is fatal and loud.
 static void adapter_fail(const char* what) {

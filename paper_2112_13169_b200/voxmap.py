@@ -280,6 +280,25 @@ class MappingPipeline:
         return self._lib.vxm_cuda_stream(self._ctx) or 0
 
 
+# --- synthetic frames on the GPU (sim::render_depth, render.cpp:26-58) -----------
+
+def render_depth(cam: "CameraModel", poses, boxes, out_ptr=None):
+    """Depth frames of an AABB scene for a list of (R, t) camera->world poses.
+    boxes: (n, 6) min/max corners. Returns (n_frames, H, W) float32 on the
+    host, or renders into a device buffer at out_ptr (n_frames*H*W floats)."""
+    boxes = np.ascontiguousarray(boxes, dtype=np.float64).reshape(-1, 6)
+    n = len(poses)
+    pa = (N.PoseC * n)(*(pose_c(p) for p in poses))
+    if out_ptr is None:
+        out = np.empty((n, cam.height, cam.width), dtype=np.float32)
+        ptr = out.ctypes.data
+    else:
+        out, ptr = None, out_ptr
+    N.check(N.load().vxm_render_depth(C.byref(cam.to_c()), pa, n, boxes.ctypes.data if len(boxes) else None,
+                                      len(boxes), C.c_void_p(ptr)))
+    return out
+
+
 # --- VOXGRID1 dumps (proj/include/voxmap/grid_io.hpp:10-17), host only ----------
 
 def write_grid(grid: "GridSpec", cells, path):
