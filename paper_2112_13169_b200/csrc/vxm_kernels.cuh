@@ -100,10 +100,14 @@ __global__ void __launch_bounds__(256) populate_depth_kernel(KParams p, int iter
 // engine: one elected thread issues `iters` bulk copies (one per 256-quad
 // tile, 4 KB each) on per-tile mbarriers at block start, so every block keeps
 // its whole span in flight (HBM latency no longer bounds the launch); the
-// threads then consume tile after tile as the copies land. Requires W*H % 4
-// == 0 and a 16-byte aligned frame (checked; otherwise the plain loads).
+// threads then consume tile after tile as the copies land. kCompact: each
+// warp first lists its valid pixels and transforms them densely (frames with
+// many invalid / out-of-range pixels); the host picks the variant from the
+// valid fraction it last observed. Requires W*H % 4 == 0 and a 16-byte
+// aligned frame (checked; otherwise the plain loads).
 constexpr int kPopMaxIters = 8;
 
+template <bool kCompact>
 __global__ void __launch_bounds__(256) populate_depth_tma_kernel(KParams p, int iters) {
   extern __shared__ float4 sq[];  // iters * blockDim.x quads
   __shared__ uint64_t bar[kPopMaxIters];
@@ -136,6 +140,58 @@ __global__ void __launch_bounds__(256) populate_depth_tma_kernel(KParams p, int 
   __syncthreads();  // barriers initialised before anyone waits on them
 
   unsigned total = 0, outside = 0;
+  if constexpr (kCompact) {
+  // Each warp lists the valid pixels of its own quads (ballot positions, no
+  // block barrier) and then transforms them 32 at a time, so no lane idles on
+  // an invalid pixel (sparse frames: a cfg2 frame is ~70% beyond max_depth).
+  uint16_t* wl = reinterpret_cast<uint16_t*>(sq + iters * T) + (threadIdx.x >> 5) * (iters * 128);
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  int nlist = 0;
+  for (int it = 0; it < iters; ++it) {
+    if (q0 + it * T >= nq) break;
+    const int q = q0 + it * T + threadIdx.x;
+    float4 cur = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (aligned) {
+      mbar_wait(&bar[it], 0);
+      if (q < nq) cur = sq[it * T + threadIdx.x];
+    } else if (q < nq) {
+      cur = load_quad(depth, q * 4, nq * 4);
+      sq[it * T + threadIdx.x] = cur;
+    }
+    const float d[4] = {cur.x, cur.y, cur.z, cur.w};
+    bool ok[4];
+    unsigned b[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      // DepthImage::valid_depth (geometry.hpp:124): finite and > 0; then the
+      // max-depth cut on the promoted double (geometry.cpp:53-54).
+      ok[k] = q < nq && isfinite(d[k]) && d[k] > 0.0f && !(static_cast<double>(d[k]) > p.max_depth);
+      b[k] = __ballot_sync(0xffffffffu, ok[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (ok[k]) wl[nlist + __popc(b[k] & lt)] = static_cast<uint16_t>((it * T + threadIdx.x) * 4 + k);
+      nlist += __popc(b[k]);
+    }
+  }
+  __syncwarp();
+  const float* spx = reinterpret_cast<const float*>(sq);
+  const int pix0 = q0 * 4;
+  const float invW = 1.0f / static_cast<float>(p.W);
+  total += lane == 0 ? static_cast<unsigned>(nlist) : 0u;
+  for (int i = lane; i < nlist; i += 32) {
+    const int off = wl[i];
+    const int pix = pix0 + off;
+    int v = static_cast<int>((static_cast<float>(pix) + 0.5f) * invW);  // pix / W, corrected below
+    v -= v * p.W > pix ? 1 : 0;
+    v += (v + 1) * p.W <= pix ? 1 : 0;
+    const int u = pix - v * p.W;
+    const double D = static_cast<double>(spx[off]);
+    outside += populate_point(p, R, t, target, rowflag, mark, dmul(__ldg(p.qx + u), D),
+                              dmul(__ldg(p.qy + v), D), D);
+  }
+  } else {
   for (int it = 0; it < iters; ++it) {
     const int q = q0 + it * T + threadIdx.x;
     if (q0 + it * T >= nq) break;
@@ -164,6 +220,7 @@ __global__ void __launch_bounds__(256) populate_depth_tma_kernel(KParams p, int 
       outside += populate_point(p, R, t, target, rowflag, mark, dmul(__ldg(p.qx + u), D),
                                 dmul(__ldg(p.qy + v), D), D);
     }
+  }
   }
   unsigned vals[2] = {total, outside};
   unsigned long long* dst[2] = {&p.counters[s].points_total, &p.counters[s].points_outside};

@@ -282,12 +282,14 @@ struct vxm_ctx {
   std::vector<int32_t> last_shifted;  // per slot
   std::vector<double> origin_after;   // per slot: local origin after that frame
 
-  cudaGraphExec_t graph_depth = nullptr;
-  cudaGraphExec_t graph_cloud = nullptr;
-  cudaGraph_t graph_tmpl[2] = {nullptr, nullptr};          // kept for node updates
-  cudaGraphNode_t stage_nodes[2][4] = {};                  // event-record nodes per graph
+  // captured frame graphs: 0 depth, 1 cloud, 2 depth with the compacting K1
+  static constexpr int kGraphs = 3;
+  cudaGraphExec_t graph_exec[kGraphs] = {};
+  cudaGraph_t graph_tmpl[kGraphs] = {};                    // kept for node updates
+  cudaGraphNode_t stage_nodes[kGraphs][4] = {};            // event-record nodes per graph
+  bool pop_compact = false;  // K1 variant: valid fraction of the last observed frames < 1/2
   void* user_stage_ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  bool stage_dirty[2] = {true, true};                      // node events need re-pointing
+  bool stage_dirty[kGraphs] = {true, true, true};          // node events need re-pointing
   // ev[0] / ev[5] bracket the frame outside the graph; ev[1..4] are the
   // stage boundaries recorded inside it (before populate, before trace,
   // after trace, after merge)
@@ -319,8 +321,12 @@ void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
     const int iters = static_cast<int>(std::max(1LL, std::min<long long>(vxm::kPopMaxIters, tiles * S / fill)));
     dim3 grid(static_cast<unsigned>((tiles + iters - 1) / iters), S);
     if (npix % 4 == 0) {
-      const size_t smem = sizeof(float4) * kPopulateThreads * static_cast<size_t>(iters);
-      vxm::populate_depth_tma_kernel<<<grid, kPopulateThreads, smem, c->stream>>>(kp, iters);
+      // staged quads + per-warp lists of valid pixels (u16, 4 per quad)
+      const size_t smem = (sizeof(float4) + 4 * sizeof(uint16_t)) * kPopulateThreads * static_cast<size_t>(iters);
+      if (c->pop_compact)
+        vxm::populate_depth_tma_kernel<true><<<grid, kPopulateThreads, smem, c->stream>>>(kp, iters);
+      else
+        vxm::populate_depth_tma_kernel<false><<<grid, kPopulateThreads, smem, c->stream>>>(kp, iters);
     } else {
       vxm::populate_depth_kernel<<<grid, kPopulateThreads, 0, c->stream>>>(kp, iters);
     }
@@ -373,7 +379,7 @@ void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
                          cudaMemcpyDeviceToHost, c->stream));
 }
 
-cudaGraphExec_t capture(vxm_ctx* c, bool cloud) {
+cudaGraphExec_t capture(vxm_ctx* c, bool cloud, int gi) {
   cudaGraph_t g = nullptr;
   VXM_CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   try {
@@ -384,7 +390,6 @@ cudaGraphExec_t capture(vxm_ctx* c, bool cloud) {
     throw;
   }
   VXM_CK(cudaStreamEndCapture(c->stream, &g));
-  const int gi = cloud ? 1 : 0;
   c->graph_tmpl[gi] = g;
   // locate the stage event-record nodes so callers can redirect them
   size_t nn = 0;
@@ -482,10 +487,10 @@ void run_frame(vxm_ctx* c, bool cloud, bool direct = false) {
     VXM_CK(cudaEventRecord(c->ev[0], c->stream));
     launch_frame(c, cloud, false);
   } else {
-    const int gi = cloud ? 1 : 0;
-    cudaGraphExec_t& g = cloud ? c->graph_cloud : c->graph_depth;
+    const int gi = cloud ? 1 : (c->pop_compact ? 2 : 0);
+    cudaGraphExec_t& g = c->graph_exec[gi];
     if (!g) {
-      g = capture(c, cloud);
+      g = capture(c, cloud, gi);
       c->stage_dirty[gi] = true;
     }
     if (c->stage_dirty[gi]) {
@@ -515,6 +520,14 @@ void collect_stats(vxm_ctx* c, vxm_stats* out) {
       for (int i = 0; i < 3; ++i) c->stage_us[i] = t[i] * 1000.0;
     }
     c->pending = false;
+  }
+  // K1 variant for the next frames: compact the valid pixels when fewer than
+  // half of the last frames' pixels were valid (depth path only)
+  {
+    unsigned long long pts = 0;
+    for (int s = 0; s < c->nslots; ++s) pts += c->counters_host[s].points_total;
+    const double npix = static_cast<double>(c->kp.W) * c->kp.H * c->nslots;
+    c->pop_compact = static_cast<double>(pts) < 0.5 * npix;
   }
   if (!out) return;
   for (int s = 0; s < c->nslots; ++s) {
@@ -554,8 +567,8 @@ void destroy_ctx(vxm_ctx* c) {
   if (!c) return;
   if (c->device >= 0) cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  if (c->graph_depth) cudaGraphExecDestroy(c->graph_depth);
-  if (c->graph_cloud) cudaGraphExecDestroy(c->graph_cloud);
+  for (auto& g : c->graph_exec)
+    if (g) cudaGraphExecDestroy(g);
   for (auto& g : c->graph_tmpl)
     if (g) cudaGraphDestroy(g);
   for (auto& e : c->ev)
@@ -756,6 +769,11 @@ int vxm_create_multi(const vxm_config* cfg, int32_t n_streams, int32_t frames_pe
     kp.vh = c->bundle[2];
     kp.tiles_x = (kp.vw + 7) / 8;
     kp.tiles_y = (kp.vh + 3) / 4;
+    for (const void* fn : {reinterpret_cast<const void*>(vxm::populate_depth_tma_kernel<true>),
+                           reinterpret_cast<const void*>(vxm::populate_depth_tma_kernel<false>)})
+      VXM_CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>((sizeof(float4) + 4 * sizeof(uint16_t)) * kPopulateThreads *
+                                                   vxm::kPopMaxIters)));
     kp.occ = c->occ;
     kp.ctr = c->ctr;
     kp.rowflag = c->rowflag;
@@ -892,7 +910,7 @@ int vxm_set_stage_events(vxm_ctx* ctx, void* const events[4]) {
   return guarded([&] {
     if (!ctx) throw InvalidArg{"null context"};
     for (int i = 0; i < 4; ++i) ctx->user_stage_ev[i] = events ? events[i] : nullptr;
-    ctx->stage_dirty[0] = ctx->stage_dirty[1] = true;
+    for (bool& d : ctx->stage_dirty) d = true;
   });
 }
 
