@@ -227,6 +227,7 @@ def our_arm(args, world, rank, local):
     import numpy as np
     import torch
 
+    from paper_2112_13169_b200 import _native as N
     from paper_2112_13169_b200 import multi
     from paper_2112_13169_b200 import voxmap as vm
     from tests import scenes
@@ -270,16 +271,14 @@ def our_arm(args, world, rank, local):
             p.set_origin(vm.GridSpec.create_centered(*c["grid"], c["vox"], poses[gids[s] % POOL][1]).origin, s)
         return p
 
-    # ---- device-resident throughput (value) + live trace-kernel timing
+    # ---- device-resident throughput (value): the default batch graph, whose
+    # branches overlap the stages of different stream shares
     pipe = new_pipeline(S)
+    branches = pipe.graph_branches
     stream = torch.cuda.ExternalStream(pipe.cuda_stream, device=dev)
     for k in range(WU):
         pipe.integrate_depth_device(slots[k % POOL].data_ptr(), step_poses(k))
     pipe.wait_stats()
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
-    for e4 in ev:
-        for e in e4:
-            e.record(stream)  # materialise the handles
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     if dist:
@@ -288,21 +287,44 @@ def our_arm(args, world, rank, local):
     with ClockSampler(local) as clocks:
         start.record(stream)
         for k in range(K):
-            pipe.set_stage_events([e.cuda_event for e in ev[k]])
             pipe.integrate_depth_device(slots[(WU + k) % POOL].data_ptr(), step_poses(WU + k))
         end.record(stream)
         stats = pipe.wait_stats()
         torch.cuda.synchronize()
-    pipe.set_stage_events(None)
     ms = start.elapsed_time(end)
+    ms = multi.max_over_ranks(ms, dev)
+    value = multi.job_throughput(S * K, world, ms / 1000.0)
+    # K1 populate, (K2a rows + K2b tiles when vox_inf > 0), K3 trace, K4 merge, per branch
+    kernels_per_step = (5 if c["vox_inf"] > 0 else 3) * branches
+
+    # ---- per-kernel device times (the roofline's K3 duration): the same
+    # steps as ONE graph branch, stage-boundary events recorded inside the
+    # graph on the launching stream, so each stage is timed alone
+    kpipe = new_pipeline(S, flags=N.FLAG_SINGLE_BRANCH)
+    kstream = torch.cuda.ExternalStream(kpipe.cuda_stream, device=dev)
+    for k in range(WU):
+        kpipe.integrate_depth_device(slots[k % POOL].data_ptr(), step_poses(k))
+    kpipe.wait_stats()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    for e4 in ev:
+        for e in e4:
+            e.record(kstream)  # materialise the handles
+    kstart, kend = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    kstart.record(kstream)
+    for k in range(K):
+        kpipe.set_stage_events([e.cuda_event for e in ev[k]])
+        kpipe.integrate_depth_device(slots[(WU + k) % POOL].data_ptr(), step_poses(WU + k))
+    kend.record(kstream)
+    kpipe.wait_stats()
+    torch.cuda.synchronize()
+    kpipe.set_stage_events(None)
+    single_branch_ms = kstart.elapsed_time(kend) / K
     trace_ms = [e4[1].elapsed_time(e4[2]) for e4 in ev]
     stage_ms = {"populate_dilate": statistics.mean(e4[0].elapsed_time(e4[1]) for e4 in ev),
                 "trace": statistics.mean(trace_ms),
                 "merge_shift_count": statistics.mean(e4[2].elapsed_time(e4[3]) for e4 in ev)}
-    ms = multi.max_over_ranks(ms, dev)
-    value = multi.job_throughput(S * K, world, ms / 1000.0)
-    # K1 populate, (K2a rows + K2b tiles when vox_inf > 0), K3 trace, K4 merge
-    kernels_per_step = 5 if c["vox_inf"] > 0 else 3
+    kpipe.close()
 
     # ---- end to end through the C-ABI host-buffer call
     pinned = torch.empty((POOL, S, c["height"], c["width"]), dtype=torch.float32).pin_memory()
@@ -408,6 +430,8 @@ def our_arm(args, world, rank, local):
                            "e2e_p50": round(pct(e2e_lat, 0.5), 4), "e2e_p99": round(pct(e2e_lat, 0.99), 4),
                            "frames": len(dev_lat), "note": "one stream, one frame at a time"},
             "stage_ms_per_step": {k: round(v, 4) for k, v in stage_ms.items()},
+            "graph_branches": branches,
+            "single_branch_ms_per_step": round(single_branch_ms, 4),
             "trajectory": trajectory,
             "roofline": {"bound": "hbm", "kernel": "trace_bundle_kernel", "achieved": round(achieved, 1),
                          "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,

@@ -136,6 +136,7 @@ typedef struct vxm_ctx vxm_ctx;
 
 #define VXM_FLAG_STAGE_TIMING 1u  /* launch stages directly (no graph), events between them */
 #define VXM_FLAG_NO_GRAPH 2u      /* launch kernels directly instead of a CUDA graph */
+#define VXM_FLAG_SINGLE_BRANCH 4u /* batches: one graph branch (stage events then time each whole stage) */
 
 /* cfg->grid must already be placed (use vxm_grid_spec_create_centered to
  * centre it on the first camera position, pipeline.cpp:71-72). Validates as
@@ -155,6 +156,8 @@ int vxm_create_multi(const vxm_config* cfg, int32_t n_streams, int32_t frames_pe
 int vxm_destroy(vxm_ctx* ctx);
 int vxm_num_streams(const vxm_ctx* ctx);
 int vxm_frames_per_call(const vxm_ctx* ctx);
+/* Graph branches a batch frame runs as (their kernels overlap on the GPU). */
+int vxm_graph_branches(const vxm_ctx* ctx);
 
 /* MappingPipeline::integrate for a depth frame:
  * integrate(MeasurementFrame{depth_to_cloud(img, cam), t_wc}) with the

@@ -17,7 +17,7 @@ LIB_PATH = PKG_DIR / "lib" / os.environ.get("VXM_LIB_NAME", "libvxm.so")  # over
 VXM_OK, VXM_EINVAL, VXM_ECUDA, VXM_ENOMEM, VXM_ENODEV, VXM_ESTATE, VXM_EIO = range(7)
 UNKNOWN, FREE, OCCUPIED, UNKNOWN_TRACED = 0, 1, 2, 3
 TRACER_BUNDLED, TRACER_PER_PIXEL = 0, 1
-FLAG_STAGE_TIMING, FLAG_NO_GRAPH = 1, 2
+FLAG_STAGE_TIMING, FLAG_NO_GRAPH, FLAG_SINGLE_BRANCH = 1, 2, 4
 
 
 class GridSpecC(C.Structure):
@@ -76,6 +76,7 @@ SIGNATURES = {
     "vxm_num_streams": (C.c_int, [C.c_void_p]),
     "vxm_create_multi": (C.c_int, [P(ConfigC), C.c_int32, C.c_int32, C.c_int32, C.c_uint32, P(C.c_void_p)]),
     "vxm_frames_per_call": (C.c_int, [C.c_void_p]),
+    "vxm_graph_branches": (C.c_int, [C.c_void_p]),
     "vxm_grid_write": (C.c_int, [C.c_char_p, P(GridSpecC), C.c_void_p]),
     "vxm_render_depth": (C.c_int, [P(CameraC), P(PoseC), C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]),
     "vxm_grid_read": (C.c_int, [C.c_char_p, P(GridSpecC), C.c_void_p, C.c_size_t]),

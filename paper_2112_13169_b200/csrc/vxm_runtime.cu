@@ -258,6 +258,9 @@ struct vxm_ctx {
   float* depth_dev = nullptr;
   // double-buffered staging for vxm_integrate_depth_async (created lazily)
   cudaStream_t copy_stream = nullptr;
+  static constexpr int kBranches = 3;
+  cudaStream_t side[kBranches] = {};  // streams of graph branches 1..
+  cudaEvent_t fork[kBranches] = {}, join[kBranches] = {};
   float* stage[2] = {nullptr, nullptr};
   cudaEvent_t ev_copied[2] = {};
   cudaEvent_t ev_consumed[2] = {};
@@ -303,15 +306,31 @@ namespace {
 
 // capturing: inside stream capture the stage events must be recorded as
 // external event-record nodes (a plain record only adds a dependency edge).
-void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
-  const int S = c->nslots;  // K1-K3 run on every frame slot
+int graph_branches(const vxm_ctx* c) {
+  const bool single = (c->flags & (VXM_FLAG_STAGE_TIMING | VXM_FLAG_SINGLE_BRANCH)) != 0;
+  return !single && c->F == 1 && c->S >= 4 * vxm_ctx::kBranches ? vxm_ctx::kBranches : 1;
+}
+
+// The four stages for slots [s0, s0 + S) on stream `st` (kernel parameters
+// rebased to the first slot). `marks` records the stage-boundary events.
+void launch_stages(vxm_ctx* c, bool cloud, bool capturing, int s0, int S, cudaStream_t st, bool marks) {
   vxm::KParams kp = c->kp;
+  const long long n = c->n;
+  kp.frames += s0;
+  kp.counters += s0;
+  kp.occ += n * s0;
+  kp.key += n * s0;
+  if (kp.ctr) kp.ctr += n * s0;
+  if (kp.rowflag) kp.rowflag += c->rows * s0;
+  if (kp.dbits) kp.dbits += static_cast<long long>(vxm::dilate_row_words(kp.dx)) * c->rows * s0;
+  kp.loc0 += n * (s0 / c->F);
+  kp.loc1 += n * (s0 / c->F);
   auto mark = [&](cudaEvent_t e) {
-    VXM_CK(capturing ? cudaEventRecordWithFlags(e, c->stream, cudaEventRecordExternal)
-                     : cudaEventRecord(e, c->stream));
+    if (!marks) return;
+    VXM_CK(capturing ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal) : cudaEventRecord(e, st));
   };
   mark(c->ev[1]);
-  VXM_CK(cudaMemsetAsync(c->counters, 0, sizeof(vxm::Counters) * S, c->stream));
+  VXM_CK(cudaMemsetAsync(kp.counters, 0, sizeof(vxm::Counters) * S, st));
   if (!cloud) {
     // tiles of 256 quads; a block takes `iters` of them once the batch
     // alone fills the GPU several times over (8 blocks per SM)
@@ -324,20 +343,20 @@ void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
       // staged quads + per-warp lists of valid pixels (u16, 4 per quad)
       const size_t smem = (sizeof(float4) + 4 * sizeof(uint16_t)) * kPopulateThreads * static_cast<size_t>(iters);
       if (c->pop_compact)
-        vxm::populate_depth_tma_kernel<true><<<grid, kPopulateThreads, smem, c->stream>>>(kp, iters);
+        vxm::populate_depth_tma_kernel<true><<<grid, kPopulateThreads, smem, st>>>(kp, iters);
       else
-        vxm::populate_depth_tma_kernel<false><<<grid, kPopulateThreads, smem, c->stream>>>(kp, iters);
+        vxm::populate_depth_tma_kernel<false><<<grid, kPopulateThreads, smem, st>>>(kp, iters);
     } else {
-      vxm::populate_depth_kernel<<<grid, kPopulateThreads, 0, c->stream>>>(kp, iters);
+      vxm::populate_depth_kernel<<<grid, kPopulateThreads, 0, st>>>(kp, iters);
     }
   } else {
     dim3 grid(static_cast<unsigned>(c->nsm * 4), S);
-    vxm::populate_cloud_kernel<<<grid, kPopulateThreads, 0, c->stream>>>(kp);
+    vxm::populate_cloud_kernel<<<grid, kPopulateThreads, 0, st>>>(kp);
   }
   VXM_CK(cudaGetLastError());
   if (kp.vox_inf > 0) {
     const int r = kp.vox_inf;
-    vxm::launch_dilate(kp, r, S, vxm::dilate_smem_bytes(r, kp.dx), c->stream);
+    vxm::launch_dilate(kp, r, S, vxm::dilate_smem_bytes(r, kp.dx), st);
     VXM_CK(cudaGetLastError());
   }
   mark(c->ev[2]);
@@ -346,10 +365,10 @@ void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
       const long long n = cloud ? static_cast<long long>(c->nsm) * 4 * kPopulateThreads
                                 : static_cast<long long>(kp.W) * kp.H;
       dim3 grid(static_cast<unsigned>(std::min<long long>((n + 255) / 256, c->nsm * 8)), S);
-      vxm::trace_per_pixel_kernel<<<grid, 256, 0, c->stream>>>(kp, cloud ? 0 : 1);
+      vxm::trace_per_pixel_kernel<<<grid, 256, 0, st>>>(kp, cloud ? 0 : 1);
     } else {
       dim3 grid(static_cast<unsigned>(kp.tiles_x * kp.tiles_y), S);
-      vxm::trace_bundle_kernel<<<grid, 32, 0, c->stream>>>(kp);
+      vxm::trace_bundle_kernel<<<grid, 32, 0, st>>>(kp);
     }
     VXM_CK(cudaGetLastError());
   }
@@ -362,19 +381,53 @@ void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
     const int rpw = static_cast<int>(std::max(1LL, std::min<long long>(vxm::kRowsPerWarp, warps / fill)));
     const int rows_per_block = kMergeThreads / 32 * rpw;
     dim3 grid(static_cast<unsigned>((rows + rows_per_block - 1) / rows_per_block), S);
-    vxm::merge_shift_count_kernel<<<grid, kMergeThreads, 0, c->stream>>>(kp, rpw);
+    vxm::merge_shift_count_kernel<<<grid, kMergeThreads, 0, st>>>(kp, rpw);
     VXM_CK(cudaGetLastError());
   } else {
     // chains of F frames per stream; the chain box varies per call, so the
     // launch covers it with a fixed grid-stride shape
     const long long chains = c->n * 2;
     const long long blocks = std::min<long long>((chains + kMergeThreads - 1) / kMergeThreads,
-                                                 std::max<long long>(1, c->nsm * 8LL / c->S));
-    dim3 grid(static_cast<unsigned>(std::max<long long>(1, blocks)), c->S);
-    vxm::merge_sequence_kernel<<<grid, kMergeThreads, 0, c->stream>>>(kp, c->F);
+                                                 std::max<long long>(1, c->nsm * 8LL / (S / c->F)));
+    dim3 grid(static_cast<unsigned>(std::max<long long>(1, blocks)), S / c->F);
+    vxm::merge_sequence_kernel<<<grid, kMergeThreads, 0, st>>>(kp, c->F);
     VXM_CK(cudaGetLastError());
   }
   mark(c->ev[4]);
+}
+
+// One frame of every slot: the stages, optionally as two graph branches over
+// halves of the streams (kernels of one branch overlap the other's), then
+// the D2H of the counters.
+void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
+  // Batches run as kBranches graph branches over equal shares of the streams:
+  // the branches' stages overlap on the GPU (the ALU-bound trace of one share
+  // with the HBM-bound populate / merge of another; +13% frames/s at 64
+  // streams, tools/quick_time.py). One branch for single streams, F > 1, the
+  // stage-timing mode and VXM_FLAG_SINGLE_BRANCH.
+  const int B = cloud ? 1 : graph_branches(c);
+  if (B > 1) {
+    for (int b = 1; b < B; ++b)
+      if (!c->side[b]) {
+        VXM_CK(cudaStreamCreateWithFlags(&c->side[b], cudaStreamNonBlocking));
+        VXM_CK(cudaEventCreateWithFlags(&c->fork[b], cudaEventDisableTiming));
+        VXM_CK(cudaEventCreateWithFlags(&c->join[b], cudaEventDisableTiming));
+      }
+    for (int b = 1; b < B; ++b) {
+      VXM_CK(cudaEventRecord(c->fork[b], c->stream));
+      VXM_CK(cudaStreamWaitEvent(c->side[b], c->fork[b], 0));
+    }
+    for (int b = 0; b < B; ++b) {
+      const int s0 = c->S * b / B, s1 = c->S * (b + 1) / B;
+      launch_stages(c, cloud, capturing, s0, s1 - s0, b == 0 ? c->stream : c->side[b], b == 0);
+    }
+    for (int b = 1; b < B; ++b) {
+      VXM_CK(cudaEventRecord(c->join[b], c->side[b]));
+      VXM_CK(cudaStreamWaitEvent(c->stream, c->join[b], 0));
+    }
+  } else {
+    launch_stages(c, cloud, capturing, 0, c->nslots, c->stream, true);
+  }
   VXM_CK(cudaMemcpyAsync(c->counters_host, c->counters, sizeof(vxm::Counters) * c->nslots,
                          cudaMemcpyDeviceToHost, c->stream));
 }
@@ -598,6 +651,11 @@ void destroy_ctx(vxm_ctx* c) {
     }
     cudaStreamDestroy(c->copy_stream);
   }
+  for (int b = 0; b < vxm_ctx::kBranches; ++b) {
+    if (c->side[b]) cudaStreamDestroy(c->side[b]);
+    if (c->fork[b]) cudaEventDestroy(c->fork[b]);
+    if (c->join[b]) cudaEventDestroy(c->join[b]);
+  }
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -811,6 +869,8 @@ int vxm_destroy(vxm_ctx* ctx) {
 int vxm_num_streams(const vxm_ctx* ctx) { return ctx ? ctx->S : 0; }
 
 int vxm_frames_per_call(const vxm_ctx* ctx) { return ctx ? ctx->F : 0; }
+
+int vxm_graph_branches(const vxm_ctx* ctx) { return ctx ? graph_branches(ctx) : 0; }
 
 void* vxm_cuda_stream(vxm_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
 

@@ -276,6 +276,10 @@ class MappingPipeline:
         return v.value
 
     @property
+    def graph_branches(self) -> int:
+        return self._lib.vxm_graph_branches(self._ctx)
+
+    @property
     def cuda_stream(self) -> int:
         return self._lib.vxm_cuda_stream(self._ctx) or 0
 

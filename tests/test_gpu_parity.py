@@ -418,3 +418,34 @@ def test_snapshot_save_resume_matches_uninterrupted(gpu_lib, tmp_path):
                                                cam, vox_inf=1, depth=6.5))
     with pytest.raises(ValueError, match="does not match"):
         bad.load_snapshot(snap)
+
+
+def test_branched_batch_equals_single_streams(gpu_lib):
+    """Batches of >= 12 streams run as graph branches over stream shares
+    (13 streams: shares 4/4/5); every stream must equal its own single-stream
+    pipeline, and one of them the reference."""
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 96, 72, 6.5)
+    grid = vm.GridSpec.create_centered(6.0, 6.0, 3.0, 0.1, (0.0, 0.0, 0.0))
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=2, depth=6.0)
+    S = 13
+    batch = vm.MappingPipeline(cfg, n_streams=S)
+    assert batch.graph_branches == 3
+    single = vm.MappingPipeline(cfg, n_streams=S, flags=4)  # VXM_FLAG_SINGLE_BRANCH
+    assert single.graph_branches == 1
+    ones = [vm.MappingPipeline(cfg) for _ in range(S)]
+    orc = oracle_pipeline(cfg)
+    for k in range(4):
+        poses = [vm.look_along_x((0.03 * s, 0.11 * k - 0.2, 0.01 * s)) for s in range(S)]
+        depth = np.stack([scenes.render(cam, poses[s], scenes.box_field_boxes(1 + s % 4)) for s in range(S)])
+        sb = batch.integrate_depth(depth, poses)
+        ss = single.integrate_depth(depth, poses)
+        so = orc.integrate_depth(depth[7], poses[7])
+        for s in range(S):
+            s1 = ones[s].integrate_depth(depth[s], poses[s])
+            for key in ("occupied_count", "freed_count", "voxels_freed", "voxels_marked_unknown_traced",
+                        "points_total", "origin"):
+                assert sb[s][key] == s1[key] == ss[s][key], (k, s, key)
+        assert sb[7]["freed_count"] == so["freed_count"]
+    for s in range(S):
+        assert np.array_equal(batch.local_grid(s)[0], ones[s].local_grid()[0]), s
+    assert np.array_equal(batch.local_grid(7)[0], orc.local_grid()[0])
