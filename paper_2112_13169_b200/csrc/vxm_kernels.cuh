@@ -647,6 +647,9 @@ __global__ void __launch_bounds__(32) trace_bundle_kernel(KParams p) {
   // predicates, and a predicated fire-and-forget RED.max on the key.
   unsigned lw = 0, lt = 0;
   const unsigned long long key_base = reinterpret_cast<unsigned long long>(key);
+  // A write is dropped when lane+1 or lane+8 (higher ray indices) makes the
+  // same cell in the same step (measured: dropping the dedup after the first
+  // chunks slows the kernel, the extra L2 atomics cost more than the check).
   auto resolve = [&](const uint32_t (&cell)[kChunk]) {
     uint32_t o[kChunk];
 #pragma unroll
@@ -1105,15 +1108,19 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
   const FrameParams* f0 = p.frames + static_cast<long long>(s) * F;
   const int lane = threadIdx.x & 31;
   for (int k = threadIdx.x; k < kMaxFramesPerCall; k += blockDim.x) cnt[k] = 0ull;
+  __shared__ int vec_ok;
   if (threadIdx.x == 0) {
     int P[3] = {0, 0, 0};
+    bool aligned = (p.dx & 3) == 0;
     for (int k = 0; k <= F; ++k) {
       for (int a = 0; a < 3; ++a) Pc[k][a] = P[a];
+      aligned = aligned && (P[0] & 3) == 0;
       if (k < F) {
         for (int a = 0; a < 3; ++a) P[a] += f0[k].off[a];
         ep[k] = f0[k].epoch;
       }
     }
+    vec_ok = aligned ? 1 : 0;
   }
   if (blockIdx.x == 0) {
     // fold the trace counters of every frame slot of this stream (one warp each)
@@ -1131,6 +1138,67 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
   const uint8_t* occ0 = p.occ + static_cast<long long>(s) * F * p.n;
   const uint32_t* key0 = p.key + static_cast<long long>(s) * F * p.n;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  if (vec_ok) {
+    // Every frame's x shift is a multiple of 4 (and dims_x too): a thread
+    // folds 4 neighbouring chains at once, moving the 4 cells as one word
+    // (occupancy u32, keys uint4) and merging / counting them with the
+    // byte-SIMD helpers of K4.
+    const int ex4 = ex >> 2;
+    const long long ngroup = static_cast<long long>(ex4) * ey * ez;
+    for (long long base = static_cast<long long>(blockIdx.x) * blockDim.x; base < ngroup; base += stride) {
+      const long long i = base + threadIdx.x;
+      const bool active = i < ngroup;
+      const int iz = static_cast<int>(i / (static_cast<long long>(ex4) * ey));
+      const int rem = static_cast<int>(i - static_cast<long long>(iz) * ex4 * ey);
+      const int iy = rem / ex4;
+      const int gx = bx + 4 * (rem - iy * ex4), gy = by + iy, gz = bz + iz;
+      auto group_of = [&](int k, bool& in) {  // first cell of the group at c_{k-1}
+        const int cx = gx - Pc[k][0], cy = gy - Pc[k][1], cz = gz - Pc[k][2];
+        in = active && static_cast<unsigned>(cx) < static_cast<unsigned>(dx) &&
+             static_cast<unsigned>(cy) < static_cast<unsigned>(dy) && static_cast<unsigned>(cz) < static_cast<unsigned>(dz);
+        return cx + cy * dx + cz * dxy;
+      };
+      bool in_prev;
+      int pos_prev = group_of(0, in_prev);
+      uint32_t val = in_prev ? *reinterpret_cast<const uint32_t*>(src + pos_prev) : 0u;
+      for (int k0 = 0; k0 < F; k0 += U) {
+        bool in_c[U];
+        int pos[U];
+        uint32_t o[U];
+        uint4 kk[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) pos[u] = group_of(k0 + u + 1, in_c[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const bool in_r = u == 0 ? in_prev : in_c[u - 1];
+          const int r = u == 0 ? pos_prev : pos[u - 1];
+          const bool ld = k0 + u < F && in_c[u] && in_r;
+          const long long off = static_cast<long long>(k0 + u) * p.n + r;
+          o[u] = ld ? __ldcs(reinterpret_cast<const uint32_t*>(occ0 + off)) : 0u;
+          kk[u] = ld ? __ldcs(reinterpret_cast<const uint4*>(key0 + off)) : make_uint4(0u, 0u, 0u, 0u);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int k = k0 + u;
+          if (k >= F) break;
+          const bool in_r = u == 0 ? in_prev : in_c[u - 1];
+          if (in_c[u]) val = in_r ? merge4(val, o[u], kk[u], ep[k]) : 0u;  // shifted in: Unknown
+          const unsigned oc = in_c[u] ? count_occupied4(val) : 0u, fr = in_c[u] ? count_free4(val) : 0u;
+          const unsigned long long w = __reduce_add_sync(0xffffffffu, oc) |
+                                       (static_cast<unsigned long long>(__reduce_add_sync(0xffffffffu, fr)) << 32);
+          if (lane == 0 && w) atomicAdd(&cnt[k], w);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (k0 + u < F) {
+            in_prev = in_c[u];
+            pos_prev = pos[u];
+          }
+        }
+      }
+      if (in_prev) *reinterpret_cast<uint32_t*>(dst + pos_prev) = val;
+    }
+  } else
   for (long long base = static_cast<long long>(blockIdx.x) * blockDim.x; base < nchain; base += stride) {
     const long long i = base + threadIdx.x;
     const bool active = i < nchain;
