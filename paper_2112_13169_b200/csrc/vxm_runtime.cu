@@ -308,12 +308,15 @@ namespace {
 // external event-record nodes (a plain record only adds a dependency edge).
 int graph_branches(const vxm_ctx* c) {
   const bool single = (c->flags & (VXM_FLAG_STAGE_TIMING | VXM_FLAG_SINGLE_BRANCH)) != 0;
-  return !single && c->F == 1 && c->S >= 4 * vxm_ctx::kBranches ? vxm_ctx::kBranches : 1;
+  return !single && c->nslots >= 4 * vxm_ctx::kBranches ? vxm_ctx::kBranches : 1;
 }
 
 // The four stages for slots [s0, s0 + S) on stream `st` (kernel parameters
 // rebased to the first slot). `marks` records the stage-boundary events.
-void launch_stages(vxm_ctx* c, bool cloud, bool capturing, int s0, int S, cudaStream_t st, bool marks) {
+void launch_merge(vxm_ctx* c, const vxm::KParams& kp, int S, cudaStream_t st);
+
+void launch_stages(vxm_ctx* c, bool cloud, bool capturing, int s0, int S, cudaStream_t st, bool marks,
+                   bool merge = true) {
   vxm::KParams kp = c->kp;
   const long long n = c->n;
   kp.frames += s0;
@@ -373,6 +376,13 @@ void launch_stages(vxm_ctx* c, bool cloud, bool capturing, int s0, int S, cudaSt
     VXM_CK(cudaGetLastError());
   }
   mark(c->ev[3]);
+  if (merge) launch_merge(c, kp, S, st);
+  mark(c->ev[4]);
+}
+
+// K4 for S slots of rebased parameters: merge + shift + counts (F == 1), or
+// the chain kernel over S / F streams (F > 1).
+void launch_merge(vxm_ctx* c, const vxm::KParams& kp, int S, cudaStream_t st) {
   if (c->F == 1) {
     const long long rows = static_cast<long long>(kp.dy) * kp.dz;
     // one row per warp unless the batch fills the GPU several times over
@@ -393,7 +403,6 @@ void launch_stages(vxm_ctx* c, bool cloud, bool capturing, int s0, int S, cudaSt
     vxm::merge_sequence_kernel<<<grid, kMergeThreads, 0, st>>>(kp, c->F);
     VXM_CK(cudaGetLastError());
   }
-  mark(c->ev[4]);
 }
 
 // One frame of every slot: the stages, optionally as two graph branches over
@@ -417,14 +426,19 @@ void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
       VXM_CK(cudaEventRecord(c->fork[b], c->stream));
       VXM_CK(cudaStreamWaitEvent(c->side[b], c->fork[b], 0));
     }
+    // F == 1: each branch runs all stages for its streams; F > 1: the
+    // branches run K1-K3 for shares of the frame slots and the chain merge
+    // follows for every stream once they joined
+    const int units = c->F == 1 ? c->S : c->nslots;
     for (int b = 0; b < B; ++b) {
-      const int s0 = c->S * b / B, s1 = c->S * (b + 1) / B;
-      launch_stages(c, cloud, capturing, s0, s1 - s0, b == 0 ? c->stream : c->side[b], b == 0);
+      const int s0 = units * b / B, s1 = units * (b + 1) / B;
+      launch_stages(c, cloud, capturing, s0, s1 - s0, b == 0 ? c->stream : c->side[b], b == 0, c->F == 1);
     }
     for (int b = 1; b < B; ++b) {
       VXM_CK(cudaEventRecord(c->join[b], c->side[b]));
       VXM_CK(cudaStreamWaitEvent(c->stream, c->join[b], 0));
     }
+    if (c->F > 1) launch_merge(c, c->kp, c->nslots, c->stream);
   } else {
     launch_stages(c, cloud, capturing, 0, c->nslots, c->stream, true);
   }
