@@ -13,7 +13,7 @@ for name, vox_inf, dm, S, F in (("cfg1", 0, 6.5, 1, 1), ("cfg2", 2, 5.0, 1, 1), 
         continue
     cam = vm.CameraModel(85 * DEG, 101 * DEG, 640, 480, dm)
     grid = vm.GridSpec.create_centered(10.0, 10.0, 5.0, 0.1, (0, 0, 0))
-    p = vm.MappingPipeline(vm.PipelineConfig(grid, cam, vox_inf=vox_inf, depth=dm), n_streams=S, flags=2,
+    p = vm.MappingPipeline(vm.PipelineConfig(grid, cam, vox_inf=vox_inf, depth=dm), n_streams=S, flags=6,
                            frames_per_call=F)
     pose = vm.look_along_x((0, 0, 0))
     d = scenes.render(cam, pose, scenes.box_field_boxes(1))
