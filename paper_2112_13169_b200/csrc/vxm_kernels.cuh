@@ -8,6 +8,8 @@
 //   K4 merge_shift_count                merge into the local grid, shift, count
 #pragma once
 
+#include <type_traits>
+
 #include "vxm_device.cuh"
 
 namespace vxm {
@@ -550,7 +552,10 @@ inline cudaError_t dilate_set_smem(int bytes) {
 // in the same step, which removes most same-address traffic near the camera.
 // Counters go to 32 per-stream slots (one RED per warp each), summed by K4.
 // ---------------------------------------------------------------------------
-constexpr int kChunk = 8;  // 4 and 16 measured equal; without the dedup 2-3x slower
+#ifndef VXM_TSEL_MUL
+#define VXM_TSEL_MUL 0
+#endif
+
 constexpr int kTraceSlots = 32;
 
 struct RayState {
@@ -603,7 +608,13 @@ __device__ __forceinline__ void ray_setup(const double* R, const double* start, 
   }
 }
 
-__global__ void __launch_bounds__(32) trace_bundle_kernel(KParams p) {
+// Two shapes (measured, tools/ab_time.sh): batches of frames run kChunk = 4
+// steps per chunk in 2-warp blocks held to 40 registers (48 warps per SM, a
+// few spilled values; 4-7% faster than one warp per block at 64 registers),
+// a lone frame (358 warps, GPU far from full) runs 8-step chunks at 64
+// registers, where per-warp latency decides.
+template <int kChunk, int kTraceWarps, int kMinBlocks>
+__global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_kernel(KParams p) {
   const int s = blockIdx.y;
   const FrameParams* fp = p.frames + s;
   const uint32_t epoch = fp->epoch;
@@ -615,8 +626,8 @@ __global__ void __launch_bounds__(32) trace_bundle_kernel(KParams p) {
 #pragma unroll
   for (int i = 0; i < 3; ++i) start[i] = fp->trans[i];
 
-  const int lane = threadIdx.x;
-  const int tile = blockIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int tile = blockIdx.x * kTraceWarps + (threadIdx.x >> 5);
   const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
   const int xi_idx = tx * 8 + (lane & 7);
   const int yi_idx = ty * 4 + (lane >> 3);
@@ -650,14 +661,46 @@ __global__ void __launch_bounds__(32) trace_bundle_kernel(KParams p) {
   // A write is dropped when lane+1 or lane+8 (higher ray indices) makes the
   // same cell in the same step (measured: dropping the dedup after the first
   // chunks slows the kernel, the extra L2 atomics cost more than the check).
-  auto resolve = [&](const uint32_t (&cell)[kChunk]) {
+  // kTail: invalid cells only follow the end of the ray (the in-grid walk);
+  // otherwise they can precede its entry into the grid (camera outside).
+  auto resolve_t = [&](const uint32_t (&cell)[kChunk], auto tail_tag) {
+    constexpr bool kTail = decltype(tail_tag)::value;
     uint32_t o[kChunk];
 #pragma unroll
     for (int j = 0; j < kChunk; ++j) {
-      o[j] = cell[j] != 0xffffffffu ? __ldg(occ + cell[j]) : 0u;
+      // a lane whose ray has ended reads as "occupied": no write, no count
+      // (its traced bit no longer matters)
+      o[j] = cell[j] != 0xffffffffu ? __ldg(occ + cell[j]) : (kTail ? epoch : 0u);
     }
 #pragma unroll
     for (int j = 0; j < kChunk; ++j) {
+      if constexpr (kTail)
+      asm volatile("{\n\t"
+                   ".reg .pred io, w, p1, p8, d1, d8, ok;\n\t"
+                   ".reg .b32 id, r1, r8, kv;\n\t"
+                   ".reg .b64 a;\n\t"
+                   "setp.eq.u32 io, %4, %5;\n\t"
+                   "setp.ne.u32 w, %4, %5;\n\t"
+                   "@w add.u32 %1, %1, 1;\n\t"
+                   "@w add.u32 %2, %2, %0;\n\t"
+                   "or.b32 kv, %6, %0;\n\t"
+                   "selp.u32 %0, 1, %0, io;\n\t"
+                   "selp.u32 id, %3, -1, w;\n\t"
+                   "shfl.sync.down.b32 r1|p1, id, 1, 31, -1;\n\t"
+                   "shfl.sync.down.b32 r8|p8, id, 8, 31, -1;\n\t"
+                   "setp.eq.and.u32 d1, r1, id, p1;\n\t"
+                   "setp.eq.and.u32 d8, r8, id, p8;\n\t"
+                   "or.pred d1, d1, d8;\n\t"
+                   "not.pred d1, d1;\n\t"
+                   "and.pred ok, w, d1;\n\t"
+                   "mul.wide.u32 a, %3, 4;\n\t"
+                   "add.u64 a, a, %7;\n\t"
+                   "@ok red.relaxed.gpu.global.max.u32 [a], kv;\n\t"
+                   "}"
+                   : "+r"(traced_bit), "+r"(lw), "+r"(lt)
+                   : "r"(cell[j]), "r"(o[j]), "r"(epoch), "r"(ray_key), "l"(key_base)
+                   : "memory");
+      else
       asm volatile("{\n\t"
                    ".reg .pred v, io, w, p1, p8, d1, d8, ok;\n\t"
                    ".reg .b32 id, r1, r8, kv;\n\t"
@@ -686,6 +729,8 @@ __global__ void __launch_bounds__(32) trace_bundle_kernel(KParams p) {
                    : "memory");
     }
   };
+  auto resolve = [&](const uint32_t (&cell)[kChunk]) { resolve_t(cell, std::false_type{}); };
+  auto resolve_tail = [&](const uint32_t (&cell)[kChunk]) { resolve_t(cell, std::true_type{}); };
 
   // The camera (every ray's start) is shared by the whole frame, so this
   // branch is uniform. Inside the grid the walk needs no per-cell bounds
@@ -732,8 +777,9 @@ __global__ void __launch_bounds__(32) trace_bundle_kernel(KParams p) {
         // below its threshold. t + 0 == t for the axes not taken (t >= 0).
         asm("{\n\t"
             ".reg .pred q, px, py, pz, npx, s0, s1, s2, ok;\n\t"
-            ".reg .f64 a0, a1, a2;\n\t"
-            ".reg .b32 l;\n\t"
+            ".reg .f64 a0, a1, a2, f0, f1, f2;\n\t"
+            ".reg .b32 l, h0, h1, h2, zl;\n\t"
+            "mov.b32 zl, 0;\n\t"
             "setp.le.f64 q, %0, %1;\n\t"
             "setp.le.and.f64 px, %0, %2, q;\n\t"
             "setp.le.f64 q, %1, %2;\n\t"
@@ -747,9 +793,23 @@ __global__ void __launch_bounds__(32) trace_bundle_kernel(KParams p) {
             "or.pred ok, s0, s1;\n\t"
             "or.pred ok, ok, s2;\n\t"
             "selp.u32 %4, %4, 0, ok;\n\t"
+#if VXM_TSEL_MUL
+            // tdelta * (1.0 or 0.0): one 32-bit select per axis (the low
+            // words of both factors are 0) and a multiply on the fp64 pipe
+            "selp.b32 h0, 1072693248, 0, px;\n\t"
+            "selp.b32 h1, 1072693248, 0, py;\n\t"
+            "selp.b32 h2, 1072693248, 0, pz;\n\t"
+            "mov.b64 f0, {zl, h0};\n\t"
+            "mov.b64 f1, {zl, h1};\n\t"
+            "mov.b64 f2, {zl, h2};\n\t"
+            "mul.rn.f64 a0, %5, f0;\n\t"
+            "mul.rn.f64 a1, %6, f1;\n\t"
+            "mul.rn.f64 a2, %7, f2;\n\t"
+#else
             "selp.f64 a0, %5, 0d0000000000000000, px;\n\t"
             "selp.f64 a1, %6, 0d0000000000000000, py;\n\t"
             "selp.f64 a2, %7, 0d0000000000000000, pz;\n\t"
+#endif
             "add.rn.f64 %0, %0, a0;\n\t"
             "add.rn.f64 %1, %1, a1;\n\t"
             "add.rn.f64 %2, %2, a2;\n\t"
@@ -761,7 +821,7 @@ __global__ void __launch_bounds__(32) trace_bundle_kernel(KParams p) {
             : "d"(e0), "d"(e1), "d"(e2), "d"(M0), "d"(M1), "d"(M2), "r"(lin0), "r"(lin1), "r"(lin2));
       }
       alive = al != 0u;
-      resolve(cell);
+      resolve_tail(cell);
     }
     freed += lw - lt;
     traced += lt;
@@ -812,6 +872,16 @@ __global__ void __launch_bounds__(32) trace_bundle_kernel(KParams p) {
     if (f_n) atomicAdd(slot + 1, f_n);
     if (t_n) atomicAdd(slot + 2, t_n);
     if (k_n) atomicAdd(slot + 3, k_n);
+  }
+}
+
+// Launches K3 over `slots` frame slots in the shape that suits the batch.
+inline void launch_trace(const KParams& kp, int slots, cudaStream_t st) {
+  const int tiles = kp.tiles_x * kp.tiles_y;
+  if (slots >= 8) {
+    trace_bundle_kernel<4, 2, 24><<<dim3((tiles + 1) / 2, slots), 64, 0, st>>>(kp);
+  } else {
+    trace_bundle_kernel<8, 1, 1><<<dim3(tiles, slots), 32, 0, st>>>(kp);
   }
 }
 

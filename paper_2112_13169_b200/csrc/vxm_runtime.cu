@@ -370,8 +370,7 @@ void launch_stages(vxm_ctx* c, bool cloud, bool capturing, int s0, int S, cudaSt
       dim3 grid(static_cast<unsigned>(std::min<long long>((n + 255) / 256, c->nsm * 8)), S);
       vxm::trace_per_pixel_kernel<<<grid, 256, 0, st>>>(kp, cloud ? 0 : 1);
     } else {
-      dim3 grid(static_cast<unsigned>(kp.tiles_x * kp.tiles_y), S);
-      vxm::trace_bundle_kernel<<<grid, 32, 0, st>>>(kp);
+      vxm::launch_trace(kp, S, st);
     }
     VXM_CK(cudaGetLastError());
   }
