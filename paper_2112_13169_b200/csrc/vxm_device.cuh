@@ -10,6 +10,8 @@
 
 #include <cstdint>
 
+#include <cuda_runtime.h>
+
 namespace vxm {
 
 // ---------------------------------------------------------------------------
@@ -253,6 +255,30 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
                "@!p bra WAIT_%=;\n\t}"
                ::"r"(smem_u32(bar)), "r"(phase)
                : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch: a kernel launched with launch_pdl may start
+// while the previous kernel on its stream drains; it runs its independent
+// prologue, then pdl_wait() blocks until that kernel has completed and its
+// writes are visible (a no-op for an ordinary launch).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr{};
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
 }  // namespace vxm

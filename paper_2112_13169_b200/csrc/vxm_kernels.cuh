@@ -284,6 +284,7 @@ __host__ __device__ constexpr int dilate_row_words(int dx) {
 constexpr int kDilRowsPerWarp = 4;
 
 __global__ void __launch_bounds__(256) dilate_rows_kernel(KParams p, int r) {
+  pdl_wait();  // K1's centre bytes and row flags
   const int s = blockIdx.y;
   const uint32_t e = p.frames[s].epoch;
   const int lane = threadIdx.x & 31;
@@ -338,6 +339,7 @@ __host__ __device__ constexpr int dilate_rows_group(int dx) {
 }
 
 __global__ void __launch_bounds__(256) dilate_rows_vec_kernel(KParams p, int r) {
+  pdl_wait();  // K1's centre bytes and row flags
   const int s = blockIdx.y;
   const uint32_t e = p.frames[s].epoch;
   const int lane = threadIdx.x & 31;
@@ -404,6 +406,7 @@ __host__ __device__ constexpr size_t dilate_smem_bytes(int r, int dx) {
 // kR > 0: radius fixed at compile time; kR == 0: radius at run time.
 template <int kR>
 __global__ void __launch_bounds__(256) dilate_tiles_kernel(KParams p, int r_rt) {
+  pdl_wait();  // K2a's bit rows
   extern __shared__ uint32_t bits[];
   const int r = kR > 0 ? kR : r_rt;
   const int s = blockIdx.z;
@@ -500,18 +503,18 @@ inline void launch_dilate(const KParams& kp, int r, int streams, size_t smem, cu
   const int G = dilate_rows_group(kp.dx);
   if (kp.n % 16 == 0 && G * kp.dx <= 512 && G * dilate_row_words(kp.dx) <= 32) {
     const int per_block = 8 * G;
-    dilate_rows_vec_kernel<<<dim3((rows + per_block - 1) / per_block, streams), 256, 0, st>>>(kp, r);
+    launch_pdl(dilate_rows_vec_kernel, dim3((rows + per_block - 1) / per_block, streams), dim3(256), 0, st, kp, r);
   } else {
     const int per_block = 8 * kDilRowsPerWarp;
-    dilate_rows_kernel<<<dim3((rows + per_block - 1) / per_block, streams), 256, 0, st>>>(kp, r);
+    launch_pdl(dilate_rows_kernel, dim3((rows + per_block - 1) / per_block, streams), dim3(256), 0, st, kp, r);
   }
   const dim3 grid((kp.dy + kDilT - 1) / kDilT, (kp.dz + kDilT - 1) / kDilT, streams);
   switch (r) {
-    case 1: dilate_tiles_kernel<1><<<grid, 256, smem, st>>>(kp, r); break;
-    case 2: dilate_tiles_kernel<2><<<grid, 256, smem, st>>>(kp, r); break;
-    case 3: dilate_tiles_kernel<3><<<grid, 256, smem, st>>>(kp, r); break;
-    case 4: dilate_tiles_kernel<4><<<grid, 256, smem, st>>>(kp, r); break;
-    default: dilate_tiles_kernel<0><<<grid, 256, smem, st>>>(kp, r); break;
+    case 1: launch_pdl(dilate_tiles_kernel<1>, grid, dim3(256), smem, st, kp, r); break;
+    case 2: launch_pdl(dilate_tiles_kernel<2>, grid, dim3(256), smem, st, kp, r); break;
+    case 3: launch_pdl(dilate_tiles_kernel<3>, grid, dim3(256), smem, st, kp, r); break;
+    case 4: launch_pdl(dilate_tiles_kernel<4>, grid, dim3(256), smem, st, kp, r); break;
+    default: launch_pdl(dilate_tiles_kernel<0>, grid, dim3(256), smem, st, kp, r); break;
   }
 }
 
@@ -637,6 +640,9 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
 
   RayState st;
   ray_setup(R, start, p.vs, p.ray_vs, xi_idx - (p.vw - 1) / 2, yi_idx - (p.vh - 1) / 2, p.vd, st);
+  // the ray setup above overlaps the tail of the populate/dilation kernels;
+  // occupancy is read only from here on
+  pdl_wait();
 
   const unsigned dx = p.dx, dy = p.dy, dz = p.dz;
   const int dxy = p.dx * p.dy;
@@ -879,9 +885,9 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
 inline void launch_trace(const KParams& kp, int slots, cudaStream_t st) {
   const int tiles = kp.tiles_x * kp.tiles_y;
   if (slots >= 8) {
-    trace_bundle_kernel<4, 2, 24><<<dim3((tiles + 1) / 2, slots), 64, 0, st>>>(kp);
+    launch_pdl(trace_bundle_kernel<4, 2, 24>, dim3((tiles + 1) / 2, slots), dim3(64), 0, st, kp);
   } else {
-    trace_bundle_kernel<8, 1, 1><<<dim3(tiles, slots), 32, 0, st>>>(kp);
+    launch_pdl(trace_bundle_kernel<8, 1, 1>, dim3(tiles, slots), dim3(32), 0, st, kp);
   }
 }
 
@@ -976,6 +982,7 @@ __device__ __forceinline__ void pp_trace_point(const KParams& p, const double* R
 
 // from_depth: pixels of fp->depth (back-projected as K1), else fp->xs/ys/zs.
 __global__ void __launch_bounds__(256) trace_per_pixel_kernel(KParams p, int from_depth) {
+  pdl_wait();
   const int s = blockIdx.y;
   const FrameParams* fp = p.frames + s;
   const uint32_t epoch = fp->epoch;
@@ -1053,6 +1060,7 @@ __device__ __forceinline__ unsigned count_occupied4(uint32_t x) { return __popc(
 __device__ __forceinline__ unsigned count_free4(uint32_t x) { return __popc(x & ~(x >> 1) & 0x01010101u); }
 
 __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int rows_per_warp) {
+  pdl_wait();  // K3's keys and counters
   const int s = blockIdx.y;
   const FrameParams* fp = p.frames + s;
   const uint32_t epoch = fp->epoch;
@@ -1170,6 +1178,7 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int r
 constexpr int kMaxFramesPerCall = 64;
 
 __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
+  pdl_wait();  // K3's keys and counters
   constexpr int U = 4;  // frames whose loads are issued together
   __shared__ unsigned long long cnt[kMaxFramesPerCall];     // occupied | freed << 32
   __shared__ int Pc[kMaxFramesPerCall + U][3];              // P_{k-1} at index k

@@ -368,7 +368,7 @@ void launch_stages(vxm_ctx* c, bool cloud, bool capturing, int s0, int S, cudaSt
       const long long n = cloud ? static_cast<long long>(c->nsm) * 4 * kPopulateThreads
                                 : static_cast<long long>(kp.W) * kp.H;
       dim3 grid(static_cast<unsigned>(std::min<long long>((n + 255) / 256, c->nsm * 8)), S);
-      vxm::trace_per_pixel_kernel<<<grid, 256, 0, st>>>(kp, cloud ? 0 : 1);
+      VXM_CK(vxm::launch_pdl(vxm::trace_per_pixel_kernel, grid, dim3(256), 0, st, kp, cloud ? 0 : 1));
     } else {
       vxm::launch_trace(kp, S, st);
     }
@@ -390,7 +390,7 @@ void launch_merge(vxm_ctx* c, const vxm::KParams& kp, int S, cudaStream_t st) {
     const int rpw = static_cast<int>(std::max(1LL, std::min<long long>(vxm::kRowsPerWarp, warps / fill)));
     const int rows_per_block = kMergeThreads / 32 * rpw;
     dim3 grid(static_cast<unsigned>((rows + rows_per_block - 1) / rows_per_block), S);
-    vxm::merge_shift_count_kernel<<<grid, kMergeThreads, 0, st>>>(kp, rpw);
+    VXM_CK(vxm::launch_pdl(vxm::merge_shift_count_kernel, grid, dim3(kMergeThreads), 0, st, kp, rpw));
     VXM_CK(cudaGetLastError());
   } else {
     // chains of F frames per stream; the chain box varies per call, so the
@@ -399,7 +399,7 @@ void launch_merge(vxm_ctx* c, const vxm::KParams& kp, int S, cudaStream_t st) {
     const long long blocks = std::min<long long>((chains + kMergeThreads - 1) / kMergeThreads,
                                                  std::max<long long>(1, c->nsm * 8LL / (S / c->F)));
     dim3 grid(static_cast<unsigned>(std::max<long long>(1, blocks)), S / c->F);
-    vxm::merge_sequence_kernel<<<grid, kMergeThreads, 0, st>>>(kp, c->F);
+    VXM_CK(vxm::launch_pdl(vxm::merge_sequence_kernel, grid, dim3(kMergeThreads), 0, st, kp, c->F));
     VXM_CK(cudaGetLastError());
   }
 }
