@@ -246,7 +246,7 @@ def our_arm(args, world, rank, local):
     poses = [vm.look_along_x((0.0, Y0 + 0.1001 * j, 0.0)) for j in range(POOL)]
     # the frame pool is rendered on the GPU (vxm_render_depth, bit-identical to
     # the reference's sim::render_depth); frame 0 is checked against the host
-    pool = vm.render_depth(cam, poses, boxes)  # (P, H, W)
+    pool = vm.render_depth(cam, poses, boxes, device=local)  # (P, H, W)
     assert np.array_equal(pool[0], scenes.render(cam, poses[0], boxes))
     npix = c["width"] * c["height"]
 

@@ -267,10 +267,10 @@ int vxm_depth_to_cloud(const vxm_camera* cam, const float* depth, double* xs, do
  * proj/src/sim/render.cpp:8-58): synthetic depth frames of an AABB scene
  * (boxes: n_boxes x {min_x, min_y, min_z, max_x, max_y, max_z}) from n_frames
  * camera->world poses, bit-identical to the reference renderer. out: HOST or
- * DEVICE memory, n_frames * width * height floats (0 = no return within
- * max_depth). Input generation for large batches. */
+ * DEVICE memory (on `device`), n_frames * width * height floats (0 = no
+ * return within max_depth). Input generation for large batches. */
 int vxm_render_depth(const vxm_camera* cam, const vxm_pose* t_wc, int32_t n_frames,
-                     const double* boxes, int32_t n_boxes, float* out);
+                     const double* boxes, int32_t n_boxes, float* out, int32_t device);
 /* ------------------------------------------------------------------------ */
 /* KernelTable adapter (proj/include/voxmap/kernels/kernels.hpp:8-33): the
  * exact MergeFn / TransformVoxelizeFn signatures, HOST pointers, void, no

@@ -78,7 +78,7 @@ SIGNATURES = {
     "vxm_frames_per_call": (C.c_int, [C.c_void_p]),
     "vxm_graph_branches": (C.c_int, [C.c_void_p]),
     "vxm_grid_write": (C.c_int, [C.c_char_p, P(GridSpecC), C.c_void_p]),
-    "vxm_render_depth": (C.c_int, [P(CameraC), P(PoseC), C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]),
+    "vxm_render_depth": (C.c_int, [P(CameraC), P(PoseC), C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32]),
     "vxm_grid_read": (C.c_int, [C.c_char_p, P(GridSpecC), C.c_void_p, C.c_size_t]),
     "vxm_snapshot_save": (C.c_int, [C.c_void_p, C.c_int32, C.c_char_p]),
     "vxm_snapshot_load": (C.c_int, [C.c_void_p, C.c_int32, C.c_char_p]),

@@ -315,8 +315,12 @@ int vxm_depth_to_cloud(const vxm_camera* cam, const float* depth, double* xs, do
 // sim::render_depth for n_frames poses. out: HOST or DEVICE
 // memory of n_frames * width * height floats.
 int vxm_render_depth(const vxm_camera* cam, const vxm_pose* t_wc, int32_t n_frames, const double* boxes,
-                     int32_t n_boxes, float* out) {
+                     int32_t n_boxes, float* out, int32_t device) {
   return stage_guard([&] {
+    int count = 0;
+    VXM_SCK(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) throw StageError{VXM_EINVAL, "device index out of range"};
+    VXM_SCK(cudaSetDevice(device));
     if (!cam || !t_wc || !out || (n_boxes > 0 && !boxes)) throw StageError{VXM_EINVAL, "null argument"};
     if (n_frames < 1 || n_boxes < 0) throw StageError{VXM_EINVAL, "n_frames must be >= 1, n_boxes >= 0"};
     // CameraModel::validate (geometry.cpp:28-41) and Aabb::validate (scene.cpp:12-17)

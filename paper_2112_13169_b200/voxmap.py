@@ -286,7 +286,7 @@ class MappingPipeline:
 
 # --- synthetic frames on the GPU (sim::render_depth, render.cpp:26-58) -----------
 
-def render_depth(cam: "CameraModel", poses, boxes, out_ptr=None):
+def render_depth(cam: "CameraModel", poses, boxes, out_ptr=None, device=0):
     """Depth frames of an AABB scene for a list of (R, t) camera->world poses.
     boxes: (n, 6) min/max corners. Returns (n_frames, H, W) float32 on the
     host, or renders into a device buffer at out_ptr (n_frames*H*W floats)."""
@@ -299,7 +299,7 @@ def render_depth(cam: "CameraModel", poses, boxes, out_ptr=None):
     else:
         out, ptr = None, out_ptr
     N.check(N.load().vxm_render_depth(C.byref(cam.to_c()), pa, n, boxes.ctypes.data if len(boxes) else None,
-                                      len(boxes), C.c_void_p(ptr)))
+                                      len(boxes), C.c_void_p(ptr), device))
     return out
 
 
