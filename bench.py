@@ -212,7 +212,8 @@ def hbm_peak():
 
 
 def profiled_traffic():
-    """dram bytes per trace launch from the committed ncu --set full capture."""
+    """dram bytes per trace launch (and the pipe utilisation) from the
+    committed ncu --set full capture."""
     f = ROOT / "profiles" / "trace_traffic.json"
     if f.exists():
         try:
@@ -418,7 +419,7 @@ def our_arm(args, world, rank, local):
     trace_avg_s = statistics.mean(trace_ms) / 1000.0
     achieved = bytes_per_frame * S / trace_avg_s / 1e9
     peak, peak_kind = hbm_peak()
-    traffic, _ = profiled_traffic()
+    traffic, prof = profiled_traffic()
 
     line = {"metric": "frames_per_s", "value": round(value, 1), "unit": "frames/s", "n_gpus": world,
             "steps": K, "warmup": WU, "ms_per_step": round(ms / K, 4), "higher_is_better": True,
@@ -436,7 +437,12 @@ def our_arm(args, world, rank, local):
             "roofline": {"bound": "hbm", "kernel": "trace_bundle_kernel", "achieved": round(achieved, 1),
                          "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                          "peak_source": peak_kind,
-                         "bytes_per_launch": bytes_per_frame * S},
+                         "bytes_per_launch": bytes_per_frame * S,
+                         # K3 is not HBM-bound: ncu shows its ALU pipe as the binding unit
+                         "binding_pipe": None if not prof else {
+                             "pipe": "alu", "pct_of_peak": prof.get("alu_pipe_pct_of_peak"),
+                             "issue_active_pct": prof.get("issue_active_pct"),
+                             "source": f"profiles/{prof.get('tag')}_kernels.md (ncu --set full)"}},
             "gpu_launches": kernels_per_step * K,
             "hbm_gbs_pipeline": round(bytes_per_frame * value / world / 1e9, 1),
             "checks": {"occupied_count_s0": stats[0]["occupied_count"], "freed_count_s0": stats[0]["freed_count"]}}

@@ -25,6 +25,8 @@ KEEP = ["Duration", "Elapsed Cycles", "SM Active Cycles", "DRAM Throughput", "Me
         "Executed Instructions", "Issued Warp Per Scheduler", "Grid Size", "Block Size",
         "Avg. Active Threads Per Warp"]
 RAW_METRICS = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
+               "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+               "smsp__issue_active.avg.pct_of_peak_sustained_active",
                "lts__t_bytes.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_elapsed",
                "l1tex__t_requests_pipe_lsu_mem_global_op_red.sum"]
 
@@ -118,19 +120,22 @@ def main():
     if gpu.exists():
         md += ["```", gpu.read_text().strip(), "```", ""]
     md += ["## Launch list of the bench command", "", launch_table(tag), ""]
-    traffic = None
+    traffic = alu = issue = None
     for k in ("trace_bundle", "populate_depth", "dilate_rows", "dilate_tiles", "merge_shift", "merge_sequence"):
         sec, vals = kernel_section(tag, k)
         md += [sec, ""]
         if k == "trace_bundle" and vals:
             try:
                 traffic = float(vals.get("dram__bytes_read.sum", 0)) + float(vals.get("dram__bytes_write.sum", 0))
+                alu = vals.get("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active")
+                issue = vals.get("smsp__issue_active.avg.pct_of_peak_sustained_active")
             except ValueError:
                 traffic = None
     (OUT / f"{tag}_kernels.md").write_text("\n".join(md))
     if traffic is not None:
         (OUT / "trace_traffic.json").write_text(json.dumps(
             {"tag": tag, "kernel": "trace_bundle_kernel", "dram_bytes_per_launch": traffic,
+             "alu_pipe_pct_of_peak": alu, "issue_active_pct": issue,
              "launch": "cfg2, 64 streams (one batched step)", "source": f"gpurun_out/{tag}_trace_bundle.ncu-rep"},
             indent=1))
     print((OUT / f"{tag}_kernels.md").read_text()[:3000])
