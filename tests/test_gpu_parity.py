@@ -449,3 +449,46 @@ def test_branched_batch_equals_single_streams(gpu_lib):
     for s in range(S):
         assert np.array_equal(batch.local_grid(s)[0], ones[s].local_grid()[0]), s
     assert np.array_equal(batch.local_grid(7)[0], orc.local_grid()[0])
+
+
+@pytest.mark.parametrize("shape", [(63, 47), (61, 40), (66, 49)])
+def test_pipeline_odd_frame_shapes_and_special_depths(gpu_lib, shape):
+    """W*H not a multiple of 4 (K1 without the TMA staging), rows that end
+    inside a 4-pixel quad, and depth values the validity test must reject:
+    NaN, +-inf, negative, -0, subnormal, exactly max_depth and just above."""
+    W, H = shape
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, W, H, 5.0)
+    grid = vm.GridSpec.create_centered(6.0, 5.0, 3.0, 0.1, (0.0, 0.0, 0.0))
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=1, depth=5.0)
+    rng = np.random.default_rng(W * H)
+    frames = []
+    for k in range(3):
+        pose = vm.look_along_x((0.0, 0.13 * k, 0.02 * k))
+        d = scenes.render(cam, pose, scenes.box_field_boxes(2 + k)).copy()
+        special = np.array([np.nan, np.inf, -np.inf, -1.0, -0.0, 1e-40, 5.0, np.nextafter(np.float32(5.0), 10),
+                            0.0, 4.9999995], dtype=np.float32)
+        idx = rng.choice(d.size, 200, replace=False)
+        d.flat[idx] = special[rng.integers(0, special.size, idx.size)]
+        frames.append((d, pose))
+    frames.append((scenes.stress_depth(cam, seed=3, invalid=0.3), vm.look_along_x((0.0, 0.4, 0.0))))
+    _run_pair(cfg, frames)
+
+
+def test_per_pixel_tracer_branched_batch(gpu_lib):
+    """TracerMode::PerPixelBaseline in a batch big enough for graph branches."""
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 80, 60, 6.5)
+    grid = vm.GridSpec.create_centered(6.0, 6.0, 3.0, 0.1, (0.0, 0.0, 0.0))
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=1, depth=6.5, tracer_mode=1)
+    S = 12
+    batch = vm.MappingPipeline(cfg, n_streams=S)
+    assert batch.graph_branches == 3
+    orc = [oracle_pipeline(cfg) for _ in (0, 11)]
+    for k in range(3):
+        poses = [vm.look_along_x((0.02 * s, 0.1 * k, 0.0)) for s in range(S)]
+        depth = np.stack([scenes.render(cam, poses[s], scenes.box_field_boxes(1 + s % 3)) for s in range(S)])
+        st = batch.integrate_depth(depth, poses)
+        for o, s in zip(orc, (0, 11)):
+            sr = o.integrate_depth(depth[s], poses[s])
+            assert st[s]["voxels_freed"] == sr["voxels_freed"] and st[s]["freed_count"] == sr["freed_count"]
+    for o, s in zip(orc, (0, 11)):
+        assert np.array_equal(batch.local_grid(s)[0], o.local_grid()[0])
