@@ -7,12 +7,16 @@ import numpy as np, torch
 from paper_2112_13169_b200 import voxmap as vm
 from tests import scenes
 DEG = math.pi / 180
-CFGS = {"cfg1": (0, 6.5), "cfg2": (2, 5.0)}
+CFGS = {"cfg1": (0, 6.5), "cfg2": (2, 5.0), "cfg3": (0, 6.5)}
 for item in os.environ.get("QT_CONFIGS", "cfg1:1,cfg2:1,cfg2:64,cfg1:64").split(","):
     parts = item.split(":"); name, S = parts[0], int(parts[1]); F = int(parts[2]) if len(parts) > 2 else 1
     vox_inf, dm = CFGS[name]
-    cam = vm.CameraModel(85 * DEG, 101 * DEG, 640, 480, dm)
-    grid = vm.GridSpec.create_centered(10.0, 10.0, 5.0, 0.1, (0, 0, 0))
+    if name == "cfg3":  # 1280x720, 0.05 m voxels, 200x200x100
+        cam = vm.CameraModel(85 * DEG, 101 * DEG, 1280, 720, dm)
+        grid = vm.GridSpec.create_centered(10.0, 10.0, 5.0, 0.05, (0, 0, 0))
+    else:
+        cam = vm.CameraModel(85 * DEG, 101 * DEG, 640, 480, dm)
+        grid = vm.GridSpec.create_centered(10.0, 10.0, 5.0, 0.1, (0, 0, 0))
     pose = vm.look_along_x((0, 0, 0))
     d = scenes.render(cam, pose, scenes.box_field_boxes(1))
     if F > 1:  # a moving robot: one voxel per frame along y (cfg4-like)
