@@ -194,6 +194,17 @@ __device__ __forceinline__ void transform_voxelize(const double* R, const double
   }
 }
 
+// Warp-wide sums of NC counters; one atomic per counter per warp (no block
+// barrier, so a warp with little work exits at once).
+template <int NC>
+__device__ __forceinline__ void warp_accumulate(unsigned (&v)[NC], unsigned long long* dst[NC]) {
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    const unsigned s = __reduce_add_sync(0xffffffffu, v[i]);
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd(dst[i], static_cast<unsigned long long>(s));
+  }
+}
+
 // Block-wide sums of NC counters; one atomic per counter per block.
 template <int NC>
 __device__ __forceinline__ void block_accumulate(unsigned (&v)[NC], unsigned long long* dst[NC]) {

@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(256) populate_depth_tma_kernel(KParams p, int 
   }
   unsigned vals[2] = {total, outside};
   unsigned long long* dst[2] = {&p.counters[s].points_total, &p.counters[s].points_outside};
-  block_accumulate<2>(vals, dst);
+  warp_accumulate<2>(vals, dst);
 }
 
 // K1 for an explicit camera-frame cloud (MeasurementFrame::cloud). Points
