@@ -137,6 +137,7 @@ typedef struct vxm_ctx vxm_ctx;
 #define VXM_FLAG_STAGE_TIMING 1u  /* launch stages directly (no graph), events between them */
 #define VXM_FLAG_NO_GRAPH 2u      /* launch kernels directly instead of a CUDA graph */
 #define VXM_FLAG_SINGLE_BRANCH 4u /* batches: one graph branch (stage events then time each whole stage) */
+#define VXM_FLAG_NO_TMA_MERGE 8u  /* K4 with direct loads instead of TMA-staged rows (A/B and fallback) */
 
 /* cfg->grid must already be placed (use vxm_grid_spec_create_centered to
  * centre it on the first camera position, pipeline.cpp:71-72). Validates as

@@ -1159,6 +1159,176 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int r
 }
 
 
+// K4, TMA-staged: a group is merge_tma_rows(dx, dy) consecutive x-rows of
+// one z-slab (about kMergeStageCells cells, so one stage is ~19 KB whatever
+// the row length); each block pipelines several groups through two stages.
+// The source rows these come from after the shift (rows y + off_y of slab
+// z + off_z) are contiguous in memory, so one elected thread stages them with
+// three bulk copies (local bytes, occupancy bytes, keys; each window widened
+// to 16-byte boundaries) on one mbarrier, and the warps merge, shift and
+// count out of shared memory: 4 cells per lane as one word when dims_x and
+// the x shift are multiples of 4, else cell by cell. Needs 16 bytes of slack
+// after each array (allocated by the runtime).
+constexpr int kMergeStageCells = 3200;
+constexpr int kMergeTmaMaxDx = 1024;  // larger rows take the direct-load K4
+
+__host__ __device__ constexpr int merge_tma_rows(int dx, int dy) {
+  return kMergeStageCells / dx < 1 ? 1 : (kMergeStageCells / dx < dy ? kMergeStageCells / dx : dy);
+}
+// one stage: local and occupancy bytes and keys of `cells` cells, each window
+// widened to 16-byte boundaries
+__host__ __device__ constexpr size_t merge_tma_smem_bytes(int cells) {
+  return 2 * (static_cast<size_t>(cells) + 32) + 4 * static_cast<size_t>(cells) + 32;
+}
+
+__device__ __forceinline__ const unsigned char* align16_down(const void* p) {
+  return reinterpret_cast<const unsigned char*>(reinterpret_cast<uintptr_t>(p) & ~static_cast<uintptr_t>(15));
+}
+__device__ __forceinline__ const unsigned char* align16_up(const void* p) {
+  return reinterpret_cast<const unsigned char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~static_cast<uintptr_t>(15));
+}
+
+__global__ void __launch_bounds__(256) merge_shift_count_tma_kernel(KParams p) {
+  extern __shared__ __align__(16) unsigned char msm[];
+  __shared__ uint64_t bar[2];
+  const int s = blockIdx.y;
+  const FrameParams* fp = p.frames + s;
+  const int dx = p.dx, dy = p.dy, dz = p.dz;
+  const long long dxy = static_cast<long long>(dx) * dy;
+  const int ox = fp->off[0], oy = fp->off[1], oz = fp->off[2];
+  const uint32_t epoch = fp->epoch;
+  const uint32_t cur = fp->cur;
+  const long long base = static_cast<long long>(s) * p.n;
+  const uint8_t* src = (cur ? p.loc1 : p.loc0) + base;
+  uint8_t* dst = (cur ? p.loc0 : p.loc1) + base;
+  const uint8_t* occ = p.occ + base;
+  const uint32_t* key = p.key + base;
+  const int rows = merge_tma_rows(dx, dy);
+  const int ngy = (dy + rows - 1) / rows;
+  const int ngroups = ngy * dz;
+  const size_t stage_bytes = merge_tma_smem_bytes(rows * dx);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool vec = ((dx | ox) & 3) == 0;
+
+  // geometry of group g: rows [y0, y0 + ny) of slab z, sourced from rows
+  // [sy_lo, sy_hi) of slab z + off_z (cells [c0, c1) of the slot)
+  struct Group {
+    int y0, ny, z, sy_lo, sy_hi;
+    bool any;
+    long long c0, c1;
+  };
+  auto group = [&](int g) {
+    Group G;
+    G.z = g / ngy;
+    G.y0 = (g - G.z * ngy) * rows;
+    G.ny = min(rows, dy - G.y0);
+    const int sz = G.z + oz;
+    G.sy_lo = max(0, G.y0 + oy);
+    G.sy_hi = min(dy, G.y0 + oy + G.ny);
+    G.any = sz >= 0 && sz < dz && G.sy_lo < G.sy_hi;
+    G.c0 = static_cast<long long>(G.sy_lo) * dx + sz * dxy;
+    G.c1 = static_cast<long long>(G.sy_hi) * dx + sz * dxy;
+    return G;
+  };
+  // one elected thread stages group g into stage buffer b (possibly nothing)
+  auto issue = [&](int g, int b) {
+    const Group G = group(g);
+    unsigned char* sl = msm + b * stage_bytes;
+    uint32_t lb = 0, ob = 0, kb = 0;
+    const unsigned char *lw0 = nullptr, *ow0 = nullptr, *kw0 = nullptr;
+    if (G.any) {
+      lw0 = align16_down(src + G.c0);
+      ow0 = align16_down(occ + G.c0);
+      kw0 = align16_down(key + G.c0);
+      lb = static_cast<uint32_t>(align16_up(src + G.c1) - lw0);
+      ob = static_cast<uint32_t>(align16_up(occ + G.c1) - ow0);
+      kb = static_cast<uint32_t>(align16_up(key + G.c1) - kw0);
+    }
+    mbar_expect_tx(&bar[b], lb + ob + kb);
+    if (G.any) {
+      unsigned char* so = sl + ((lb + 15u) & ~15u);
+      unsigned char* sk = so + ((ob + 15u) & ~15u);
+      bulk_g2s(sl, lw0, lb, &bar[b]);
+      bulk_g2s(so, ow0, ob, &bar[b]);
+      bulk_g2s(sk, kw0, kb, &bar[b]);
+    }
+  };
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_wait();  // K3's keys and counters
+  if (blockIdx.x == 0 && threadIdx.x < 32) fold_trace_slots(p.counters[s]);
+  unsigned occ_n = 0, free_n = 0;
+  int g = blockIdx.x;
+  if (g < ngroups && threadIdx.x == 0) issue(g, 0);
+  for (int it = 0; g < ngroups; ++it, g += gridDim.x) {
+    const int b = it & 1;
+    // refill the other stage (consumed in the previous iteration, after its
+    // closing barrier) while this one lands
+    if (g + gridDim.x < ngroups && threadIdx.x == 0) issue(g + gridDim.x, b ^ 1);
+    mbar_wait(&bar[b], (it >> 1) & 1);
+    const Group G = group(g);
+    const unsigned char* sl = msm + b * stage_bytes;
+    int ll = 0, ol = 0, kl = 0;
+    const unsigned char *so = sl, *sk = sl;
+    if (G.any) {
+      const unsigned char* lw0 = align16_down(src + G.c0);
+      const unsigned char* ow0 = align16_down(occ + G.c0);
+      const unsigned char* kw0 = align16_down(key + G.c0);
+      const uint32_t lb = static_cast<uint32_t>(align16_up(src + G.c1) - lw0);
+      const uint32_t ob = static_cast<uint32_t>(align16_up(occ + G.c1) - ow0);
+      so = sl + ((lb + 15u) & ~15u);
+      sk = so + ((ob + 15u) & ~15u);
+      ll = static_cast<int>((src + G.c0) - lw0);
+      ol = static_cast<int>((occ + G.c0) - ow0);
+      kl = static_cast<int>(reinterpret_cast<const unsigned char*>(key + G.c0) - kw0);
+    }
+    for (int r = warp; r < G.ny; r += blockDim.x >> 5) {
+      const int y = G.y0 + r, sy = y + oy;
+      const bool row_ok = G.any && sy >= G.sy_lo && sy < G.sy_hi;
+      uint8_t* drow = dst + static_cast<long long>(y) * dx + G.z * dxy;
+      const long long rrow = static_cast<long long>(sy - G.sy_lo) * dx;  // relative to c0
+      for (int x0 = lane * 4; x0 < dx; x0 += 128) {
+        uint32_t out = 0;
+        if (vec) {
+          const int sx = x0 + ox;
+          if (row_ok && sx >= 0 && sx < dx) {
+            const long long rel = rrow + sx;
+            out = merge4(*reinterpret_cast<const uint32_t*>(sl + ll + rel),
+                         *reinterpret_cast<const uint32_t*>(so + ol + rel),
+                         *reinterpret_cast<const uint4*>(sk + kl + 4 * rel), epoch);
+          }
+          *reinterpret_cast<uint32_t*>(drow + x0) = out;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int x = x0 + k, sx = x + ox;
+            if (x >= dx) break;
+            uint32_t v = 0;
+            if (row_ok && sx >= 0 && sx < dx) {
+              const long long rel = rrow + sx;
+              v = merge_cell(sl[ll + rel],
+                             decode_cell(so[ol + rel], *reinterpret_cast<const uint32_t*>(sk + kl + 4 * rel), epoch));
+            }
+            out |= v << (8 * k);
+            drow[x] = static_cast<uint8_t>(v);
+          }
+        }
+        occ_n += count_occupied4(out);
+        free_n += count_free4(out);
+      }
+    }
+    __syncthreads();  // stage b is refilled two groups from now
+  }
+  unsigned vals[2] = {occ_n, free_n};
+  unsigned long long* dsts[2] = {&p.counters[s].occupied, &p.counters[s].freed};
+  warp_accumulate<2>(vals, dsts);
+}
+
 // ---------------------------------------------------------------------------
 // K4 for F > 1 consecutive frames of each stream in one call (SURVEY §8f
 // "next" #1: populate and trace of all F frames run as F independent slots,

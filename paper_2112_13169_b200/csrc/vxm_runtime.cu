@@ -382,7 +382,21 @@ void launch_stages(vxm_ctx* c, bool cloud, bool capturing, int s0, int S, cudaSt
 // K4 for S slots of rebased parameters: merge + shift + counts (F == 1), or
 // the chain kernel over S / F streams (F > 1).
 void launch_merge(vxm_ctx* c, const vxm::KParams& kp, int S, cudaStream_t st) {
-  if (c->F == 1) {
+  // Short rows whose cells move as words (dx % 4 == 0, dx <= 128: every
+  // benchmark grid) take the direct-load K4 with four rows of loads in flight
+  // per lane; it measured faster there than the TMA-staged K4 (57 vs 70 us for
+  // 64 cfg2 slots). Longer or odd rows take the TMA-staged K4 (57 vs 72 us for
+  // 8 cfg3 slots of 200-cell rows).
+  const bool direct_vec = kp.dx % 4 == 0 && kp.dx <= 128;
+  if (c->F == 1 && !direct_vec && kp.dx <= vxm::kMergeTmaMaxDx && !(c->flags & VXM_FLAG_NO_TMA_MERGE)) {
+    // groups of merge_tma_rows rows; each block pipelines several (two stages)
+    const int rows = vxm::merge_tma_rows(kp.dx, kp.dy);
+    const long long groups = static_cast<long long>((kp.dy + rows - 1) / rows) * kp.dz;
+    const long long per_slot = std::max(1LL, std::min(groups, c->nsm * 8LL / S));
+    const dim3 grid(static_cast<unsigned>(per_slot), S);
+    VXM_CK(vxm::launch_pdl(vxm::merge_shift_count_tma_kernel, grid, dim3(kMergeThreads),
+                           2 * vxm::merge_tma_smem_bytes(rows * kp.dx), st, kp));
+  } else if (c->F == 1) {
     const long long rows = static_cast<long long>(kp.dy) * kp.dz;
     // one row per warp unless the batch fills the GPU several times over
     const long long warps = rows * S;
@@ -772,9 +786,11 @@ int vxm_create_multi(const vxm_config* cfg, int32_t n_streams, int32_t frames_pe
     const size_t S = static_cast<size_t>(c->nslots);  // measurement-grid slots
     const size_t NS = static_cast<size_t>(n_streams);  // local grids
     const size_t npix = static_cast<size_t>(cfg->camera.width) * cfg->camera.height;
-    VXM_CK(cudaMalloc(&c->occ, c->n * S));
+    // 64 bytes of slack after each array: the TMA-staged K4 reads windows
+    // widened to 16-byte boundaries
+    VXM_CK(cudaMalloc(&c->occ, c->n * S + 64));
     VXM_CK(cudaMemsetAsync(c->occ, 0, c->n * S, c->stream));
-    VXM_CK(cudaMalloc(&c->key, sizeof(uint32_t) * c->n * S));
+    VXM_CK(cudaMalloc(&c->key, sizeof(uint32_t) * c->n * S + 64));
     VXM_CK(cudaMemsetAsync(c->key, 0, sizeof(uint32_t) * c->n * S, c->stream));
     if (cfg->vox_inf > 0) {
       VXM_CK(cudaMalloc(&c->ctr, c->n * S));
@@ -783,7 +799,7 @@ int vxm_create_multi(const vxm_config* cfg, int32_t n_streams, int32_t frames_pe
       VXM_CK(cudaMemsetAsync(c->rowflag, 0, c->rows * S, c->stream));
     }
     for (int b = 0; b < 2; ++b) {
-      VXM_CK(cudaMalloc(&c->loc[b], c->n * NS));
+      VXM_CK(cudaMalloc(&c->loc[b], c->n * NS + 64));
       VXM_CK(cudaMemsetAsync(c->loc[b], 0, c->n * NS, c->stream));
     }
     VXM_CK(cudaMalloc(&c->counters, sizeof(vxm::Counters) * S));
@@ -840,6 +856,9 @@ int vxm_create_multi(const vxm_config* cfg, int32_t n_streams, int32_t frames_pe
     kp.vh = c->bundle[2];
     kp.tiles_x = (kp.vw + 7) / 8;
     kp.tiles_y = (kp.vh + 3) / 4;
+    VXM_CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(vxm::merge_shift_count_tma_kernel),
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(2 * vxm::merge_tma_smem_bytes(vxm::kMergeStageCells))));
     for (const void* fn : {reinterpret_cast<const void*>(vxm::populate_depth_tma_kernel<true>),
                            reinterpret_cast<const void*>(vxm::populate_depth_tma_kernel<false>)})
       VXM_CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -363,6 +363,31 @@ def test_pipeline_long_trajectory_wraps_epochs(gpu_lib):
     assert shifts > 250
 
 
+@pytest.mark.parametrize("flags", [0, 8], ids=["default", "no_tma_merge"])
+@pytest.mark.parametrize("extent,vox", [((5.0, 3.0, 2.0), 0.1), ((10.0, 3.0, 2.0), 0.05), ((3.3, 2.0, 1.5), 0.1)],
+                         ids=["dx50", "dx200", "dx33"])
+def test_k4_variants_diagonal_motion(gpu_lib, flags, extent, vox):
+    """Both K4 variants (TMA-staged rows for long / odd rows, direct loads
+    for short word-aligned rows; flag 8 forces the direct one) against the
+    reference while the robot drifts along x, y and z, so the grid shifts by
+    one voxel in every axis and in x by amounts that are not multiples of 4."""
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 64, 48, 6.5)
+    grid = vm.GridSpec.create_centered(*extent, vox, (0.0, 0.0, 0.0))
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=1, depth=6.5)
+    boxes = scenes.box_field_boxes(3)
+    gpu = vm.MappingPipeline(cfg, flags=flags)
+    orc = oracle_pipeline(cfg)
+    for k in range(24):
+        step = 1.37 * vox * k
+        pose = vm.look_along_x((step, 0.6 * step, -0.4 * step))
+        depth = scenes.render(cam, pose, boxes)
+        sg = gpu.integrate_depth(depth, pose)
+        sr = orc.integrate_depth(depth, pose)
+        for key in ("occupied_count", "freed_count", "shifted", "shift_offset", "origin"):
+            assert sg[key] == sr[key], (k, key, sg[key], sr[key])
+        assert np.array_equal(gpu.local_grid()[0], orc.local_grid()[0]), k
+
+
 def test_async_double_buffered_host_path(gpu_lib):
     """vxm_integrate_depth_async: queued host frames (pinned) give the same
     grids as the synchronous path and the reference."""

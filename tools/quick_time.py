@@ -24,7 +24,8 @@ for item in os.environ.get("QT_CONFIGS", "cfg1:1,cfg2:1,cfg2:64,cfg1:64").split(
     else:
         poses = [pose] * S
     dev = torch.from_numpy(np.stack([d] * (S * F))).cuda()
-    for flags in (0, 1):
+    xflags = int(os.environ.get("QT_FLAGS", "0"))  # extra context flags (A/B)
+    for flags in (xflags, 1 | xflags):
         p = vm.MappingPipeline(vm.PipelineConfig(grid, cam, vox_inf=vox_inf, depth=dm), n_streams=S, flags=flags,
                                frames_per_call=F)
         for _ in range(5):
@@ -34,7 +35,7 @@ for item in os.environ.get("QT_CONFIGS", "cfg1:1,cfg2:1,cfg2:64,cfg1:64").split(
             p.integrate_depth_device(dev.data_ptr(), poses); st = p.wait_stats(); ts.append(p.last_frame_ms())
             st3.append((st[0]["populate_us"], st[0]["trace_us"], st[0]["merge_us"]))
         ts = np.array(ts)
-        if flags == 0:
+        if not (flags & 1):
             print(f"{name}x{S}x{F} graph p50 ms %.4f p99 %.4f  frames/s %.0f  us/frame %.2f" % (np.median(ts), np.percentile(ts, 99), S * F / np.median(ts) * 1e3, np.median(ts) * 1e3 / (S * F)), flush=True)
         else:
             m = np.median(np.array(st3), axis=0)
