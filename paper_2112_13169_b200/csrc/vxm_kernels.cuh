@@ -1059,6 +1059,30 @@ __device__ __forceinline__ uint32_t merge4(uint32_t l4, uint32_t o4, uint4 k4, u
 __device__ __forceinline__ unsigned count_occupied4(uint32_t x) { return __popc((x >> 1) & ~x & 0x01010101u); }
 __device__ __forceinline__ unsigned count_free4(uint32_t x) { return __popc(x & ~(x >> 1) & 0x01010101u); }
 
+// floor(a / d) for a < 2^24 with a fp32 reciprocal and one correction (the
+// estimate is off by at most one there)
+__device__ __forceinline__ uint32_t div_small(uint32_t a, uint32_t d, float inv_d) {
+  uint32_t q = __float2uint_rz(__uint2float_rn(a) * inv_d);
+  const int r = static_cast<int>(a) - static_cast<int>(q * d);
+  q = r < 0 ? q - 1 : q;
+  return r >= static_cast<int>(d) ? q + 1 : q;
+}
+
+// number of bytes equal to 2 / to 1 over four words of states (byte sums of
+// the per-byte flags, each at most 4, gathered by one multiply)
+__device__ __forceinline__ unsigned count_occupied16(const uint32_t (&x)[4]) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) m += (x[i] >> 1) & ~x[i] & 0x01010101u;
+  return (m * 0x01010101u) >> 24;
+}
+__device__ __forceinline__ unsigned count_free16(const uint32_t (&x)[4]) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) m += x[i] & ~(x[i] >> 1) & 0x01010101u;
+  return (m * 0x01010101u) >> 24;
+}
+
 __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int rows_per_warp) {
   pdl_wait();  // K3's keys and counters
   const int s = blockIdx.y;
@@ -1080,6 +1104,64 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int r
 
   unsigned occ_n = 0, free_n = 0;
   const bool vec = (p.dx & 3) == 0 && (ox & 3) == 0;
+  if (ox == 0 && (p.dx & 3) == 0 && p.dx >= 16 && (p.n & 15) == 0 && p.n < (1 << 24)) {
+    // No x shift: destination cell c reads c + delta (delta = off_y*dx +
+    // off_z*dx*dy), and the valid destination cells of a slab are one run of
+    // whole rows. A thread takes 16 consecutive cells: 16 local and occupancy
+    // bytes and 16 keys, no per-row arithmetic. A chunk spans at most two
+    // rows (dx >= 16), so it is valid throughout when its first and last
+    // cells are; chunks at a run boundary test their words one by one (a
+    // word never straddles a row since dx % 4 == 0).
+    const uint32_t dx = p.dx;
+    const int delta = oy * p.dx + oz * static_cast<int>(dxy);
+    const int ylo = max(0, -oy), yhi = min(p.dy, p.dy - oy), zlo = max(0, -oz), zhi = min(p.dz, p.dz - oz);
+    const float inv_dx = 1.0f / static_cast<float>(dx), inv_dxy = 1.0f / static_cast<float>(dxy);
+    auto valid = [&](uint32_t c) {
+      const uint32_t z = div_small(c, dxy, inv_dxy);
+      const uint32_t y = div_small(c - z * dxy, dx, inv_dx);
+      return static_cast<int>(y) >= ylo && static_cast<int>(y) < yhi && static_cast<int>(z) >= zlo &&
+             static_cast<int>(z) < zhi;
+    };
+    const bool aligned = (delta & 15) == 0;
+    const uint32_t nch = static_cast<uint32_t>(p.n >> 4);
+    for (uint32_t ch = blockIdx.x * blockDim.x + threadIdx.x; ch < nch; ch += gridDim.x * blockDim.x) {
+      const uint32_t c = ch << 4;
+      const int sc = static_cast<int>(c) + delta;
+      uint32_t out[4] = {0u, 0u, 0u, 0u};
+      if (valid(c) && valid(c + 15)) {
+        uint32_t l[4], o[4];
+        if (aligned) {
+          const uint4 L = __ldcs(reinterpret_cast<const uint4*>(src + sc));
+          const uint4 O = __ldcs(reinterpret_cast<const uint4*>(occ + sc));
+          l[0] = L.x; l[1] = L.y; l[2] = L.z; l[3] = L.w;
+          o[0] = O.x; o[1] = O.y; o[2] = O.z; o[3] = O.w;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            l[i] = __ldcs(reinterpret_cast<const unsigned int*>(src + sc + 4 * i));
+            o[i] = __ldcs(reinterpret_cast<const unsigned int*>(occ + sc + 4 * i));
+          }
+        }
+        uint4 k[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) k[i] = __ldcs(reinterpret_cast<const uint4*>(key + sc + 4 * i));
+#pragma unroll
+        for (int i = 0; i < 4; ++i) out[i] = merge4(l[i], o[i], k[i], epoch);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (valid(c + 4 * i)) {
+            const int si = sc + 4 * i;
+            out[i] = merge4(*reinterpret_cast<const uint32_t*>(src + si), *reinterpret_cast<const uint32_t*>(occ + si),
+                            *reinterpret_cast<const uint4*>(key + si), epoch);
+          }
+        }
+      }
+      *reinterpret_cast<uint4*>(dst + c) = make_uint4(out[0], out[1], out[2], out[3]);
+      occ_n += count_occupied16(out);
+      free_n += count_free16(out);
+    }
+  } else
   if (vec && p.dx <= 128 && rows_per_warp == kRowsPerWarp) {
     // A row is at most one 4-cell group per lane: issue the loads of all the
     // warp's rows before resolving any, so each lane keeps kRowsPerWarp x 24 B

@@ -364,13 +364,20 @@ def test_pipeline_long_trajectory_wraps_epochs(gpu_lib):
 
 
 @pytest.mark.parametrize("flags", [0, 8], ids=["default", "no_tma_merge"])
-@pytest.mark.parametrize("extent,vox", [((5.0, 3.0, 2.0), 0.1), ((10.0, 3.0, 2.0), 0.05), ((3.3, 2.0, 1.5), 0.1)],
-                         ids=["dx50", "dx200", "dx33"])
-def test_k4_variants_diagonal_motion(gpu_lib, flags, extent, vox):
-    """Both K4 variants (TMA-staged rows for long / odd rows, direct loads
-    for short word-aligned rows; flag 8 forces the direct one) against the
-    reference while the robot drifts along x, y and z, so the grid shifts by
-    one voxel in every axis and in x by amounts that are not multiples of 4."""
+@pytest.mark.parametrize("extent,vox,motion", [((5.0, 3.0, 2.0), 0.1, (1.0, 0.6, -0.4)),
+                                               ((10.0, 3.0, 2.0), 0.05, (1.0, 0.6, -0.4)),
+                                               ((3.3, 2.0, 1.5), 0.1, (1.0, 0.6, -0.4)),
+                                               ((6.4, 3.2, 1.6), 0.1, (1.0, 0.6, -0.4)),
+                                               ((6.4, 3.2, 1.6), 0.1, (0.0, 1.0, -0.7)),
+                                               ((6.4, 3.2, 1.6), 0.1, (0.0, -0.3, 1.0)),
+                                               ((10.0, 3.0, 2.0), 0.05, (0.0, 1.0, 0.5))],
+                         ids=["dx50", "dx200", "dx33", "dx64", "dx64-yz", "dx64-zy", "dx200-yz"])
+def test_k4_variants_diagonal_motion(gpu_lib, flags, extent, vox, motion):
+    """The K4 variants (TMA-staged rows for long / odd rows; direct loads for
+    short word-aligned rows, with 16-cell flat chunks when the frame has no x
+    shift; flag 8 forces the direct kernel) against the reference while the
+    robot drifts, so the grid shifts by one or two voxels per frame, in x by
+    amounts that are not multiples of 4, or only in y and z."""
     cam = vm.CameraModel(85 * DEG, 101 * DEG, 64, 48, 6.5)
     grid = vm.GridSpec.create_centered(*extent, vox, (0.0, 0.0, 0.0))
     cfg = vm.PipelineConfig(grid, cam, vox_inf=1, depth=6.5)
@@ -379,7 +386,7 @@ def test_k4_variants_diagonal_motion(gpu_lib, flags, extent, vox):
     orc = oracle_pipeline(cfg)
     for k in range(24):
         step = 1.37 * vox * k
-        pose = vm.look_along_x((step, 0.6 * step, -0.4 * step))
+        pose = vm.look_along_x(tuple(m * step for m in motion))
         depth = scenes.render(cam, pose, boxes)
         sg = gpu.integrate_depth(depth, pose)
         sr = orc.integrate_depth(depth, pose)

@@ -27,6 +27,17 @@ ms = np.zeros(grid.cell_count(), np.uint8)
 vm.populate_occupied(grid, ms, np.random.uniform(0, 4, 200), np.random.uniform(0, 4, 200),
                      np.random.uniform(0, 2, 200), vm.identity_pose(), 2)
 vm.trace_bundle(grid, ms, vm.bundle_dimensions(cam, 2.0, 0.1), vm.look_along_x((2.0, 2.0, 1.0)))
+# K4 variants under motion: flat chunks (y/z shifts), word rows (x shifts),
+# TMA-staged rows (200-cell rows)
+movers = []
+for ext, vox, mot in (((6.4, 3.2, 1.6), 0.1, (0.0, 1.0, -0.7)), ((6.4, 3.2, 1.6), 0.1, (1.0, 0.6, -0.4)),
+                      ((10.0, 3.0, 2.0), 0.05, (1.0, 0.6, -0.4)), ((10.0, 3.0, 2.0), 0.05, (0.0, 1.0, 0.5))):
+    g = vm.GridSpec.create_centered(*ext, vox, (0.0, 0.0, 0.0))
+    m = vm.MappingPipeline(vm.PipelineConfig(g, cam, vox_inf=1, depth=5.0), flags=vm.N.FLAG_NO_GRAPH)
+    for k in range(6):
+        pose = vm.look_along_x(tuple(c * 1.37 * vox * k for c in mot))
+        m.integrate_depth(vm.render_depth(cam, [pose], boxes)[0], pose)
+    movers.append(m)
 print("sanitize case done", sb[0]["freed_count"])
-for p in (batch, one, seq):
+for p in [batch, one, seq] + movers:
     p.close()
