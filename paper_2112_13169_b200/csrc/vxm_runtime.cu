@@ -254,7 +254,14 @@ struct vxm_ctx {
   double* qtab = nullptr;  // W column + H row back-projection factors
   uint32_t* dbits = nullptr;  // x-dilated centre bit rows (vox_inf > 0)
   vxm::Counters* counters = nullptr;
-  vxm::FrameParams* frames_dev = nullptr;
+  // FrameParams on the device, two buffers: the upload for the next call
+  // (on param_stream) overlaps the graph of this one, and each buffer has
+  // its own instance of every frame graph
+  static constexpr int kPP = 2;
+  vxm::FrameParams* frames_pp[kPP] = {nullptr, nullptr};
+  int pp = 0;  // buffer of the current call
+  cudaStream_t param_stream = nullptr;
+  cudaEvent_t pp_ready[kPP] = {}, pp_free[kPP] = {};
   float* depth_dev = nullptr;
   // double-buffered staging for vxm_integrate_depth_async (created lazily)
   cudaStream_t copy_stream = nullptr;
@@ -287,12 +294,12 @@ struct vxm_ctx {
 
   // captured frame graphs: 0 depth, 1 cloud, 2 depth with the compacting K1
   static constexpr int kGraphs = 3;
-  cudaGraphExec_t graph_exec[kGraphs] = {};
-  cudaGraph_t graph_tmpl[kGraphs] = {};                    // kept for node updates
-  cudaGraphNode_t stage_nodes[kGraphs][4] = {};            // event-record nodes per graph
+  cudaGraphExec_t graph_exec[kGraphs][kPP] = {};
+  cudaGraph_t graph_tmpl[kGraphs][kPP] = {};               // kept for node updates
+  cudaGraphNode_t stage_nodes[kGraphs][kPP][4] = {};       // event-record nodes per graph
   bool pop_compact = false;  // K1 variant: valid fraction of the last observed frames < 1/2
   void* user_stage_ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  bool stage_dirty[kGraphs] = {true, true, true};          // node events need re-pointing
+  bool stage_dirty[kGraphs][kPP] = {{true, true}, {true, true}, {true, true}};  // node events need re-pointing
   // ev[0] / ev[5] bracket the frame outside the graph; ev[1..4] are the
   // stage boundaries recorded inside it (before populate, before trace,
   // after trace, after merge)
@@ -459,10 +466,12 @@ void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
                          cudaMemcpyDeviceToHost, c->stream));
 }
 
-cudaGraphExec_t capture(vxm_ctx* c, bool cloud, int gi) {
+cudaGraphExec_t capture(vxm_ctx* c, bool cloud, int gi, int pp) {
   cudaGraph_t g = nullptr;
   VXM_CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   try {
+    // the frame time starts when the graph does
+    VXM_CK(cudaEventRecordWithFlags(c->ev[0], c->stream, cudaEventRecordExternal));
     launch_frame(c, cloud, true);
   } catch (...) {
     cudaStreamEndCapture(c->stream, &g);
@@ -470,7 +479,7 @@ cudaGraphExec_t capture(vxm_ctx* c, bool cloud, int gi) {
     throw;
   }
   VXM_CK(cudaStreamEndCapture(c->stream, &g));
-  c->graph_tmpl[gi] = g;
+  c->graph_tmpl[gi][pp] = g;
   // locate the stage event-record nodes so callers can redirect them
   size_t nn = 0;
   VXM_CK(cudaGraphGetNodes(g, nullptr, &nn));
@@ -483,7 +492,7 @@ cudaGraphExec_t capture(vxm_ctx* c, bool cloud, int gi) {
     cudaEvent_t e = nullptr;
     VXM_CK(cudaGraphEventRecordNodeGetEvent(node, &e));
     for (int i = 0; i < 4; ++i)
-      if (e == c->ev[1 + i]) c->stage_nodes[gi][i] = node;
+      if (e == c->ev[1 + i]) c->stage_nodes[gi][pp][i] = node;
   }
   cudaGraphExec_t exec = nullptr;
   VXM_CK(cudaGraphInstantiate(&exec, g, 0));
@@ -492,11 +501,11 @@ cudaGraphExec_t capture(vxm_ctx* c, bool cloud, int gi) {
 
 // Points the graph's stage event-record nodes at the caller's events (or
 // back at the context's own).
-void apply_stage_events(vxm_ctx* c, cudaGraphExec_t exec, int gi) {
+void apply_stage_events(vxm_ctx* c, cudaGraphExec_t exec, int gi, int pp) {
   for (int i = 0; i < 4; ++i) {
-    if (!c->stage_nodes[gi][i]) continue;
+    if (!c->stage_nodes[gi][pp][i]) continue;
     cudaEvent_t e = c->user_stage_ev[i] ? static_cast<cudaEvent_t>(c->user_stage_ev[i]) : c->ev[1 + i];
-    VXM_CK(cudaGraphExecEventRecordNodeSetEvent(exec, c->stage_nodes[gi][i], e));
+    VXM_CK(cudaGraphExecEventRecordNodeSetEvent(exec, c->stage_nodes[gi][pp][i], e));
   }
 }
 
@@ -556,9 +565,17 @@ void prepare_frames(vxm_ctx* c, const vxm_pose* poses, const float* depth_dev_ba
       f0.box_ext[a] = hi[a] - lo[a] + c->cfg.grid.dims[a];
     }
   }
-  VXM_CK(cudaMemcpyAsync(c->frames_dev, c->frames_host, sizeof(vxm::FrameParams) * c->nslots,
-                         cudaMemcpyHostToDevice, c->stream));
-  VXM_CK(cudaEventRecord(c->ring_ev[c->ring_slot], c->stream));
+  // upload into the buffer the call before last used, on the param stream,
+  // so the copy runs while the previous graph is still executing
+  c->pp ^= 1;
+  const int pp = c->pp;
+  VXM_CK(cudaStreamWaitEvent(c->param_stream, c->pp_free[pp], 0));
+  VXM_CK(cudaMemcpyAsync(c->frames_pp[pp], c->frames_host, sizeof(vxm::FrameParams) * c->nslots,
+                         cudaMemcpyHostToDevice, c->param_stream));
+  VXM_CK(cudaEventRecord(c->ring_ev[c->ring_slot], c->param_stream));
+  VXM_CK(cudaEventRecord(c->pp_ready[pp], c->param_stream));
+  VXM_CK(cudaStreamWaitEvent(c->stream, c->pp_ready[pp], 0));
+  c->kp.frames = c->frames_pp[pp];
 }
 
 void run_frame(vxm_ctx* c, bool cloud, bool direct = false) {
@@ -568,20 +585,20 @@ void run_frame(vxm_ctx* c, bool cloud, bool direct = false) {
     launch_frame(c, cloud, false);
   } else {
     const int gi = cloud ? 1 : (c->pop_compact ? 2 : 0);
-    cudaGraphExec_t& g = c->graph_exec[gi];
+    const int pp = c->pp;
+    cudaGraphExec_t& g = c->graph_exec[gi][pp];
     if (!g) {
-      g = capture(c, cloud, gi);
-      c->stage_dirty[gi] = true;
+      g = capture(c, cloud, gi, pp);
+      c->stage_dirty[gi][pp] = true;
     }
-    if (c->stage_dirty[gi]) {
-      apply_stage_events(c, g, gi);
-      c->stage_dirty[gi] = false;
+    if (c->stage_dirty[gi][pp]) {
+      apply_stage_events(c, g, gi, pp);
+      c->stage_dirty[gi][pp] = false;
     }
-    // recorded after the host-side work so the frame time is device time only
-    VXM_CK(cudaEventRecord(c->ev[0], c->stream));
-    VXM_CK(cudaGraphLaunch(g, c->stream));
+    VXM_CK(cudaGraphLaunch(g, c->stream));  // records ev[0] as its first node
   }
   VXM_CK(cudaEventRecord(c->ev[5], c->stream));
+  VXM_CK(cudaEventRecord(c->pp_free[c->pp], c->stream));  // its FrameParams may be overwritten
   for (int s = 0; s < c->S; ++s) c->cur[s] ^= 1u;  // K4 wrote the other buffer
   c->pending = true;
 }
@@ -647,10 +664,19 @@ void destroy_ctx(vxm_ctx* c) {
   if (!c) return;
   if (c->device >= 0) cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  for (auto& g : c->graph_exec)
-    if (g) cudaGraphExecDestroy(g);
-  for (auto& g : c->graph_tmpl)
-    if (g) cudaGraphDestroy(g);
+  for (auto& gg : c->graph_exec)
+    for (auto& g : gg)
+      if (g) cudaGraphExecDestroy(g);
+  for (auto& gg : c->graph_tmpl)
+    for (auto& g : gg)
+      if (g) cudaGraphDestroy(g);
+  if (c->param_stream) cudaStreamSynchronize(c->param_stream);
+  for (int b = 0; b < vxm_ctx::kPP; ++b) {
+    if (c->pp_ready[b]) cudaEventDestroy(c->pp_ready[b]);
+    if (c->pp_free[b]) cudaEventDestroy(c->pp_free[b]);
+    cudaFree(c->frames_pp[b]);
+  }
+  if (c->param_stream) cudaStreamDestroy(c->param_stream);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : c->ring_ev)
@@ -664,7 +690,6 @@ void destroy_ctx(vxm_ctx* c) {
   cudaFree(c->loc[0]);
   cudaFree(c->loc[1]);
   cudaFree(c->counters);
-  cudaFree(c->frames_dev);
   cudaFree(c->depth_dev);
   cudaFree(c->cloud_dev);
   cudaFreeHost(c->frames_ring);
@@ -803,7 +828,12 @@ int vxm_create_multi(const vxm_config* cfg, int32_t n_streams, int32_t frames_pe
       VXM_CK(cudaMemsetAsync(c->loc[b], 0, c->n * NS, c->stream));
     }
     VXM_CK(cudaMalloc(&c->counters, sizeof(vxm::Counters) * S));
-    VXM_CK(cudaMalloc(&c->frames_dev, sizeof(vxm::FrameParams) * S));
+    for (int b = 0; b < vxm_ctx::kPP; ++b) {
+      VXM_CK(cudaMalloc(&c->frames_pp[b], sizeof(vxm::FrameParams) * S));
+      VXM_CK(cudaEventCreateWithFlags(&c->pp_ready[b], cudaEventDisableTiming));
+      VXM_CK(cudaEventCreateWithFlags(&c->pp_free[b], cudaEventDisableTiming));
+    }
+    VXM_CK(cudaStreamCreateWithFlags(&c->param_stream, cudaStreamNonBlocking));
     VXM_CK(cudaMalloc(&c->depth_dev, sizeof(float) * npix * S));
     VXM_CK(cudaMallocHost(&c->frames_ring, sizeof(vxm::FrameParams) * S * vxm_ctx::kRing));
     std::memset(c->frames_ring, 0, sizeof(vxm::FrameParams) * S * vxm_ctx::kRing);
@@ -871,7 +901,7 @@ int vxm_create_multi(const vxm_config* cfg, int32_t n_streams, int32_t frames_pe
     kp.loc0 = c->loc[0];
     kp.loc1 = c->loc[1];
     kp.counters = c->counters;
-    kp.frames = c->frames_dev;
+    kp.frames = c->frames_pp[0];
     if (cfg->vox_inf > 0) {
       const size_t smem = vxm::dilate_smem_bytes(cfg->vox_inf, kp.dx);
       if (cfg->vox_inf > vxm::kMaxVoxInf || smem > 200 * 1024 || kp.dx > 1024)
@@ -1002,7 +1032,8 @@ int vxm_set_stage_events(vxm_ctx* ctx, void* const events[4]) {
   return guarded([&] {
     if (!ctx) throw InvalidArg{"null context"};
     for (int i = 0; i < 4; ++i) ctx->user_stage_ev[i] = events ? events[i] : nullptr;
-    for (bool& d : ctx->stage_dirty) d = true;
+    for (auto& dd : ctx->stage_dirty)
+      for (bool& d : dd) d = true;
   });
 }
 

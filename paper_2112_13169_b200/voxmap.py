@@ -45,6 +45,17 @@ def pose_c(pose) -> N.PoseC:
     return p
 
 
+def pose_array(poses) -> np.ndarray:
+    """Poses as one (n, 12) float64 array in vxm_pose layout (rotation
+    row-major, then translation): the form the batched calls take without
+    per-pose marshalling."""
+    out = np.empty((len(poses), 12), dtype=np.float64)
+    for i, (R, t) in enumerate(poses):
+        out[i, :9] = np.asarray(R, dtype=np.float64).reshape(9)
+        out[i, 9:] = np.asarray(t, dtype=np.float64).reshape(3)
+    return out
+
+
 def look_along_x(position):
     """sim::look_along_x (proj/src/sim/trajectory.cpp:7-13): optical axis +x,
     image right -y, image down -z."""
@@ -176,6 +187,12 @@ class MappingPipeline:
             pass
 
     def _set_poses(self, poses):
+        """poses: a list of (R, t), or an (n, 12) float64 array (pose_array)."""
+        if isinstance(poses, np.ndarray):
+            if poses.shape != (self.n_slots, 12) or poses.dtype != np.float64:
+                raise ValueError("pose array must be float64 of shape (n_slots, 12)")
+            C.memmove(self._poses, np.ascontiguousarray(poses).ctypes.data, poses.nbytes)
+            return
         if len(poses) != self.n_slots:
             raise ValueError("need one pose per stream and frame")
         for i, p in enumerate(poses):
