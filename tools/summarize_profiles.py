@@ -115,13 +115,15 @@ def main():
           f"`{tag}_gpu.txt`). Launch list = `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
           "dram__bytes_write.sum --clock-control none` of `bench.py --steps 2 --warmup 3` (cold-cache and "
           "serialised: compare shares, not absolutes). Per-kernel sections = `ncu --set full` of one launch in a "
-          "batched cfg2 step (64 streams); merge_sequence from one 64-frame call of a single moving stream.", ""]
+          "batched cfg2 step (64 streams); merge_sequence from one 64-frame call of a single moving stream; "
+          "merge_tma (the TMA-staged K4 of rows longer than 128 cells) from a batched cfg3 step (8 streams).", ""]
     gpu = RAW / f"{tag}_gpu.txt"
     if gpu.exists():
         md += ["```", gpu.read_text().strip(), "```", ""]
     md += ["## Launch list of the bench command", "", launch_table(tag), ""]
     traffic = alu = issue = None
-    for k in ("trace_bundle", "populate_depth", "dilate_rows", "dilate_tiles", "merge_shift", "merge_sequence"):
+    for k in ("trace_bundle", "populate_depth", "dilate_rows", "dilate_tiles", "merge_shift", "merge_sequence",
+              "merge_tma"):
         sec, vals = kernel_section(tag, k)
         md += [sec, ""]
         if k == "trace_bundle" and vals:
