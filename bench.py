@@ -305,7 +305,7 @@ def our_arm(args, world, rank, local):
     # ---- per-kernel device times (the roofline's K3 duration): the same
     # steps as ONE graph branch, stage-boundary events recorded inside the
     # graph on the launching stream, so each stage is timed alone
-    kpipe = new_pipeline(S, flags=N.FLAG_SINGLE_BRANCH)
+    kpipe = new_pipeline(S, flags=N.FLAG_SINGLE_BRANCH | N.FLAG_STAGE_EVENTS)
     kstream = torch.cuda.ExternalStream(kpipe.cuda_stream, device=dev)
     for k in range(WU):
         kpipe.integrate_depth_device(slots[k % POOL].data_ptr(), step_poses(k))

@@ -88,9 +88,10 @@ typedef struct vxm_pose {
 
 /* PipelineStats + TraceStats + PopulateStats (pipeline.hpp:30-41,
  * raytracer.hpp:44-57, integrator.hpp:18-21). The *_us fields are device
- * times of the stages from CUDA events recorded inside the frame
- * (populate_us includes the dilation; shift_us is 0 because the shift is
- * fused into the merge kernel). */
+ * times of the stages from CUDA events recorded at the stage boundaries
+ * when the context records them (VXM_FLAG_STAGE_EVENTS, VXM_FLAG_STAGE_TIMING
+ * or VXM_FLAG_NO_GRAPH), else 0; populate_us includes the dilation; shift_us
+ * is 0 because the shift is fused into the merge kernel. */
 typedef struct vxm_stats {
   uint64_t points_total;
   uint64_t points_outside;
@@ -138,6 +139,8 @@ typedef struct vxm_ctx vxm_ctx;
 #define VXM_FLAG_NO_GRAPH 2u      /* launch kernels directly instead of a CUDA graph */
 #define VXM_FLAG_SINGLE_BRANCH 4u /* batches: one graph branch (stage events then time each whole stage) */
 #define VXM_FLAG_NO_TMA_MERGE 8u  /* K4 with direct loads instead of TMA-staged rows (A/B and fallback) */
+#define VXM_FLAG_STAGE_EVENTS 16u /* record the stage-boundary events inside the frame graph (fills
+                                     vxm_stats::*_us; each event node costs a few us per frame) */
 
 /* cfg->grid must already be placed (use vxm_grid_spec_create_centered to
  * centre it on the first camera position, pipeline.cpp:71-72). Validates as
@@ -214,11 +217,11 @@ int vxm_snapshot_load(vxm_ctx* ctx, int32_t s, const char* path);
 void* vxm_cuda_stream(vxm_ctx* ctx);
 int vxm_last_frame_ms(vxm_ctx* ctx, float* ms);
 
-/* Redirects the four stage-boundary events recorded inside every following
- * frame (cudaEvent_t: before populate, before trace, after trace, after
- * merge) to the caller's events, so per-kernel device times can be read for
- * many queued frames without synchronizing; NULL restores the context's own
- * (whose stage times fill vxm_stats::*_us). */
+/* Records the four stage-boundary events inside every following frame into
+ * the caller's events (cudaEvent_t: before populate, before trace, after
+ * trace, after merge), so per-kernel device times can be read for many
+ * queued frames without synchronizing; NULL stops (the context's own events
+ * fill vxm_stats::*_us when VXM_FLAG_STAGE_EVENTS is set). */
 int vxm_set_stage_events(vxm_ctx* ctx, void* const events[4]);
 
 /* ------------------------------------------------------------------------ */

@@ -300,6 +300,9 @@ struct vxm_ctx {
   bool pop_compact = false;  // K1 variant: valid fraction of the last observed frames < 1/2
   void* user_stage_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   bool stage_dirty[kGraphs][kPP] = {{true, true}, {true, true}, {true, true}};  // node events need re-pointing
+  bool graph_marks[kGraphs][kPP] = {};  // the instance holds the stage event-record nodes
+  bool capture_marks = false;           // capture in progress records them
+  bool last_marks = false;              // the last frame recorded them
   // ev[0] / ev[5] bracket the frame outside the graph; ev[1..4] are the
   // stage boundaries recorded inside it (before populate, before trace,
   // after trace, after merge)
@@ -429,6 +432,11 @@ void launch_merge(vxm_ctx* c, const vxm::KParams& kp, int S, cudaStream_t st) {
 // halves of the streams (kernels of one branch overlap the other's), then
 // the D2H of the counters.
 void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
+  // stage-boundary events: always for direct launches (cheap stream
+  // records); in a graph only when asked for, since every event-record node
+  // splits the graph's execution (measured: 17 us per single-stream frame
+  // for five nodes, 0.065 -> 0.048 ms)
+  const bool marks = !capturing || c->capture_marks;
   // Batches run as kBranches graph branches over equal shares of the streams:
   // the branches' stages overlap on the GPU (the ALU-bound trace of one share
   // with the HBM-bound populate / merge of another; +13% frames/s at 64
@@ -452,7 +460,8 @@ void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
     const int units = c->F == 1 ? c->S : c->nslots;
     for (int b = 0; b < B; ++b) {
       const int s0 = units * b / B, s1 = units * (b + 1) / B;
-      launch_stages(c, cloud, capturing, s0, s1 - s0, b == 0 ? c->stream : c->side[b], b == 0, c->F == 1);
+      launch_stages(c, cloud, capturing, s0, s1 - s0, b == 0 ? c->stream : c->side[b], b == 0 && marks,
+                    c->F == 1);
     }
     for (int b = 1; b < B; ++b) {
       VXM_CK(cudaEventRecord(c->join[b], c->side[b]));
@@ -460,18 +469,18 @@ void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
     }
     if (c->F > 1) launch_merge(c, c->kp, c->nslots, c->stream);
   } else {
-    launch_stages(c, cloud, capturing, 0, c->nslots, c->stream, true);
+    launch_stages(c, cloud, capturing, 0, c->nslots, c->stream, marks);
   }
   VXM_CK(cudaMemcpyAsync(c->counters_host, c->counters, sizeof(vxm::Counters) * c->nslots,
                          cudaMemcpyDeviceToHost, c->stream));
 }
 
-cudaGraphExec_t capture(vxm_ctx* c, bool cloud, int gi, int pp) {
+cudaGraphExec_t capture(vxm_ctx* c, bool cloud, int gi, int pp, bool marks) {
+  c->capture_marks = marks;
+  c->graph_marks[gi][pp] = marks;
   cudaGraph_t g = nullptr;
   VXM_CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   try {
-    // the frame time starts when the graph does
-    VXM_CK(cudaEventRecordWithFlags(c->ev[0], c->stream, cudaEventRecordExternal));
     launch_frame(c, cloud, true);
   } catch (...) {
     cudaStreamEndCapture(c->stream, &g);
@@ -578,24 +587,42 @@ void prepare_frames(vxm_ctx* c, const vxm_pose* poses, const float* depth_dev_ba
   c->kp.frames = c->frames_pp[pp];
 }
 
+bool stage_events_wanted(const vxm_ctx* c) {
+  if (c->flags & VXM_FLAG_STAGE_EVENTS) return true;
+  for (void* e : c->user_stage_ev)
+    if (e) return true;
+  return false;
+}
+
 void run_frame(vxm_ctx* c, bool cloud, bool direct = false) {
   const bool timed = (c->flags & VXM_FLAG_STAGE_TIMING) != 0;
   if (timed || direct || (c->flags & VXM_FLAG_NO_GRAPH)) {
     VXM_CK(cudaEventRecord(c->ev[0], c->stream));
     launch_frame(c, cloud, false);
+    c->last_marks = true;
   } else {
     const int gi = cloud ? 1 : (c->pop_compact ? 2 : 0);
     const int pp = c->pp;
     cudaGraphExec_t& g = c->graph_exec[gi][pp];
+    const bool marks = stage_events_wanted(c);
+    if (g && c->graph_marks[gi][pp] != marks) {  // recapture with / without the event nodes
+      VXM_CK(cudaGraphExecDestroy(g));
+      VXM_CK(cudaGraphDestroy(c->graph_tmpl[gi][pp]));
+      g = nullptr;
+      c->graph_tmpl[gi][pp] = nullptr;
+      for (auto& n : c->stage_nodes[gi][pp]) n = nullptr;
+    }
     if (!g) {
-      g = capture(c, cloud, gi, pp);
+      g = capture(c, cloud, gi, pp, marks);
       c->stage_dirty[gi][pp] = true;
     }
     if (c->stage_dirty[gi][pp]) {
       apply_stage_events(c, g, gi, pp);
       c->stage_dirty[gi][pp] = false;
     }
-    VXM_CK(cudaGraphLaunch(g, c->stream));  // records ev[0] as its first node
+    VXM_CK(cudaEventRecord(c->ev[0], c->stream));
+    VXM_CK(cudaGraphLaunch(g, c->stream));
+    c->last_marks = marks;
   }
   VXM_CK(cudaEventRecord(c->ev[5], c->stream));
   VXM_CK(cudaEventRecord(c->pp_free[c->pp], c->stream));  // its FrameParams may be overwritten
@@ -609,7 +636,8 @@ void collect_stats(vxm_ctx* c, vxm_stats* out) {
     VXM_CK(cudaEventElapsedTime(&c->last_ms, c->ev[0], c->ev[5]));
     const bool own = !c->user_stage_ev[0] && !c->user_stage_ev[1] && !c->user_stage_ev[2] &&
                      !c->user_stage_ev[3];
-    if (own) {
+    for (double& t : c->stage_us) t = 0.0;
+    if (own && c->last_marks) {
       float t[3] = {0, 0, 0};
       VXM_CK(cudaEventElapsedTime(&t[0], c->ev[1], c->ev[2]));
       VXM_CK(cudaEventElapsedTime(&t[1], c->ev[2], c->ev[3]));
