@@ -355,7 +355,7 @@ def our_arm(args, world, rank, local):
     e2e_s = multi.max_over_ranks(e2e_s, dev)
     e2e_value = multi.job_throughput(S * K, world, e2e_s)
     h2d = S * npix * 4 + S * 160  # depth frames + per-stream FrameParams
-    d2h = S * 1088                # per-stream counters
+    d2h = S * 96                  # per-stream counters + stage stamps (vxm::kCountersHostBytes)
     e2e_pipe.close()
 
     # ---- single-stream latency

@@ -8,6 +8,7 @@
 // with -fmad=false as a second guard.
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 
 #include <cuda_runtime.h>
@@ -68,8 +69,21 @@ struct Counters {
   unsigned long long voxels_skipped;
   unsigned long long occupied;
   unsigned long long freed;
-  unsigned long long trace_slots[32][4];  // K3 partials, folded by K4
+  // %globaltimer stamps (ns) of the stage starts for this slot: populate
+  // (K1 block 0), trace and merge (block 0, once the previous stage has
+  // completed), and the merge's end (max over its blocks); the host turns
+  // them into vxm_stats::*_us without event nodes in the frame graph
+  unsigned long long t_pop, t_trace, t_merge, t_end;
+  unsigned long long trace_slots[32][4];  // K3 partials, folded by K4 (device only)
 };
+// the part of Counters the host reads back
+constexpr size_t kCountersHostBytes = offsetof(Counters, trace_slots);
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Per-stream, per-frame parameters: uploaded each frame as one small H2D
 // copy so that the captured CUDA graph never changes.

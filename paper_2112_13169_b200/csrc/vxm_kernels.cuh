@@ -56,6 +56,7 @@ __device__ __forceinline__ float4 load_quad(const float* depth, int first, int n
 
 __global__ void __launch_bounds__(256) populate_depth_kernel(KParams p, int iters) {
   const int s = blockIdx.y;
+  if (blockIdx.x == 0 && threadIdx.x == 0) p.counters[s].t_pop = global_ns();
   const FrameParams* fp = p.frames + s;
   const uint8_t mark = static_cast<uint8_t>(fp->epoch);
   uint8_t* target = (p.vox_inf > 0 ? p.ctr : p.occ) + static_cast<long long>(s) * p.n;
@@ -114,6 +115,7 @@ __global__ void __launch_bounds__(256) populate_depth_tma_kernel(KParams p, int 
   extern __shared__ float4 sq[];  // iters * blockDim.x quads
   __shared__ uint64_t bar[kPopMaxIters];
   const int s = blockIdx.y;
+  if (blockIdx.x == 0 && threadIdx.x == 0) p.counters[s].t_pop = global_ns();
   const FrameParams* fp = p.frames + s;
   const uint8_t mark = static_cast<uint8_t>(fp->epoch);
   uint8_t* target = (p.vox_inf > 0 ? p.ctr : p.occ) + static_cast<long long>(s) * p.n;
@@ -234,6 +236,7 @@ __global__ void __launch_bounds__(256) populate_depth_tma_kernel(KParams p, int 
 // (proj/include/voxmap/geometry.hpp:84-89).
 __global__ void __launch_bounds__(256) populate_cloud_kernel(KParams p) {
   const int s = blockIdx.y;
+  if (blockIdx.x == 0 && threadIdx.x == 0) p.counters[s].t_pop = global_ns();
   const FrameParams* fp = p.frames + s;
   const uint8_t mark = static_cast<uint8_t>(fp->epoch);
   uint8_t* target = (p.vox_inf > 0 ? p.ctr : p.occ) + static_cast<long long>(s) * p.n;
@@ -643,6 +646,7 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   // the ray setup above overlaps the tail of the populate/dilation kernels;
   // occupancy is read only from here on
   pdl_wait();
+  if (blockIdx.x == 0 && threadIdx.x == 0) p.counters[s].t_trace = global_ns();
 
   const unsigned dx = p.dx, dy = p.dy, dz = p.dz;
   const int dxy = p.dx * p.dy;
@@ -984,6 +988,7 @@ __device__ __forceinline__ void pp_trace_point(const KParams& p, const double* R
 __global__ void __launch_bounds__(256) trace_per_pixel_kernel(KParams p, int from_depth) {
   pdl_wait();
   const int s = blockIdx.y;
+  if (blockIdx.x == 0 && threadIdx.x == 0) p.counters[s].t_trace = global_ns();
   const FrameParams* fp = p.frames + s;
   const uint32_t epoch = fp->epoch;
   uint32_t* key = p.key + static_cast<long long>(s) * p.n;
@@ -1086,6 +1091,7 @@ __device__ __forceinline__ unsigned count_free16(const uint32_t (&x)[4]) {
 __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int rows_per_warp) {
   pdl_wait();  // K3's keys and counters
   const int s = blockIdx.y;
+  if (blockIdx.x == 0 && threadIdx.x == 0) p.counters[s].t_merge = global_ns();
   const FrameParams* fp = p.frames + s;
   const uint32_t epoch = fp->epoch;
   const uint32_t cur = fp->cur;
@@ -1237,7 +1243,8 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int r
   }
   unsigned vals[2] = {occ_n, free_n};
   unsigned long long* dsts[2] = {&p.counters[s].occupied, &p.counters[s].freed};
-  block_accumulate<2>(vals, dsts);
+  block_accumulate<2>(vals, dsts);  // ends after every warp's work (a block barrier)
+  if (threadIdx.x == 0) atomicMax(&p.counters[s].t_end, global_ns());
 }
 
 
@@ -1343,6 +1350,7 @@ __global__ void __launch_bounds__(256) merge_shift_count_tma_kernel(KParams p) {
   }
   __syncthreads();
   pdl_wait();  // K3's keys and counters
+  if (blockIdx.x == 0 && threadIdx.x == 0) p.counters[s].t_merge = global_ns();
   if (blockIdx.x == 0 && threadIdx.x < 32) fold_trace_slots(p.counters[s]);
   unsigned occ_n = 0, free_n = 0;
   int g = blockIdx.x;
@@ -1406,6 +1414,8 @@ __global__ void __launch_bounds__(256) merge_shift_count_tma_kernel(KParams p) {
     }
     __syncthreads();  // stage b is refilled two groups from now
   }
+  // every warp has passed the last group's barrier
+  if (threadIdx.x == 0) atomicMax(&p.counters[s].t_end, global_ns());
   unsigned vals[2] = {occ_n, free_n};
   unsigned long long* dsts[2] = {&p.counters[s].occupied, &p.counters[s].freed};
   warp_accumulate<2>(vals, dsts);
@@ -1438,6 +1448,10 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
   const int s = blockIdx.y;  // stream
   const FrameParams* f0 = p.frames + static_cast<long long>(s) * F;
   const int lane = threadIdx.x & 31;
+  if (blockIdx.x == 0) {
+    const unsigned long long t = global_ns();
+    for (int k = threadIdx.x; k < F; k += blockDim.x) p.counters[static_cast<long long>(s) * F + k].t_merge = t;
+  }
   for (int k = threadIdx.x; k < kMaxFramesPerCall; k += blockDim.x) cnt[k] = 0ull;
   __shared__ int vec_ok;
   if (threadIdx.x == 0) {
@@ -1585,11 +1599,13 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
     if (in_prev) dst[pos_prev] = static_cast<uint8_t>(val);
   }
   __syncthreads();
+  const unsigned long long t_end = global_ns();
   for (int k = threadIdx.x; k < F; k += blockDim.x) {
     Counters& c = p.counters[static_cast<long long>(s) * F + k];
     const unsigned long long v = cnt[k];
     if (v & 0xffffffffull) atomicAdd(&c.occupied, v & 0xffffffffull);
     if (v >> 32) atomicAdd(&c.freed, v >> 32);
+    atomicMax(&c.t_end, t_end);
   }
 }
 

@@ -309,7 +309,6 @@ struct vxm_ctx {
   cudaEvent_t ev[6] = {};
   bool pending = false;
   float last_ms = 0.f;
-  double stage_us[4] = {0, 0, 0, 0};
 };
 
 namespace {
@@ -340,7 +339,13 @@ void launch_stages(vxm_ctx* c, bool cloud, bool capturing, int s0, int S, cudaSt
   kp.loc1 += n * (s0 / c->F);
   auto mark = [&](cudaEvent_t e) {
     if (!marks) return;
-    VXM_CK(capturing ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal) : cudaEventRecord(e, st));
+    if (capturing) {  // graph nodes, re-pointed at the caller's events by apply_stage_events
+      VXM_CK(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
+      return;
+    }
+    for (int i = 0; i < 4; ++i)  // direct launches record the caller's events when attached
+      if (e == c->ev[1 + i] && c->user_stage_ev[i]) e = static_cast<cudaEvent_t>(c->user_stage_ev[i]);
+    VXM_CK(cudaEventRecord(e, st));
   };
   mark(c->ev[1]);
   VXM_CK(cudaMemsetAsync(kp.counters, 0, sizeof(vxm::Counters) * S, st));
@@ -471,8 +476,9 @@ void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
   } else {
     launch_stages(c, cloud, capturing, 0, c->nslots, c->stream, marks);
   }
-  VXM_CK(cudaMemcpyAsync(c->counters_host, c->counters, sizeof(vxm::Counters) * c->nslots,
-                         cudaMemcpyDeviceToHost, c->stream));
+  // the counters and stage stamps of every slot (not K3's per-warp partials)
+  VXM_CK(cudaMemcpy2DAsync(c->counters_host, sizeof(vxm::Counters), c->counters, sizeof(vxm::Counters),
+                           vxm::kCountersHostBytes, c->nslots, cudaMemcpyDeviceToHost, c->stream));
 }
 
 cudaGraphExec_t capture(vxm_ctx* c, bool cloud, int gi, int pp, bool marks) {
@@ -634,16 +640,6 @@ void collect_stats(vxm_ctx* c, vxm_stats* out) {
   VXM_CK(cudaStreamSynchronize(c->stream));
   if (c->pending) {
     VXM_CK(cudaEventElapsedTime(&c->last_ms, c->ev[0], c->ev[5]));
-    const bool own = !c->user_stage_ev[0] && !c->user_stage_ev[1] && !c->user_stage_ev[2] &&
-                     !c->user_stage_ev[3];
-    for (double& t : c->stage_us) t = 0.0;
-    if (own && c->last_marks) {
-      float t[3] = {0, 0, 0};
-      VXM_CK(cudaEventElapsedTime(&t[0], c->ev[1], c->ev[2]));
-      VXM_CK(cudaEventElapsedTime(&t[1], c->ev[2], c->ev[3]));
-      VXM_CK(cudaEventElapsedTime(&t[2], c->ev[3], c->ev[4]));
-      for (int i = 0; i < 3; ++i) c->stage_us[i] = t[i] * 1000.0;
-    }
     c->pending = false;
   }
   // K1 variant for the next frames: compact the valid pixels when fewer than
@@ -672,9 +668,14 @@ void collect_stats(vxm_ctx* c, vxm_stats* out) {
       o.shift_offset[a] = c->last_off[3 * s + a];
       o.origin[a] = c->origin_after[3 * s + a];
     }
-    o.populate_us = c->stage_us[0];
-    o.trace_us = c->stage_us[1];
-    o.merge_us = c->stage_us[2];
+    // stage device times from the kernels' %globaltimer stamps (populate
+    // includes the dilation; a stage whose stamps are missing reads 0)
+    auto span_us = [](unsigned long long a, unsigned long long b) {
+      return a && b && b > a ? static_cast<double>(b - a) * 1e-3 : 0.0;
+    };
+    o.populate_us = span_us(k.t_pop, k.t_trace);
+    o.trace_us = span_us(k.t_trace, k.t_merge);
+    o.merge_us = span_us(k.t_merge, k.t_end);
     o.shift_us = 0.0;  // fused into the merge kernel
   }
 }

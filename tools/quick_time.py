@@ -31,9 +31,15 @@ for item in os.environ.get("QT_CONFIGS", "cfg1:1,cfg2:1,cfg2:64,cfg1:64").split(
         for _ in range(5):
             p.integrate_depth_device(dev.data_ptr(), poses); p.wait_stats()
         ts, st3 = [], []
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        if flags & 1:  # whole-stage device times: the four stage-boundary events
+            for e in evs:
+                e.record(torch.cuda.ExternalStream(p.cuda_stream))
+            p.set_stage_events([e.cuda_event for e in evs])
         for k in range(100):
             p.integrate_depth_device(dev.data_ptr(), poses); st = p.wait_stats(); ts.append(p.last_frame_ms())
-            st3.append((st[0]["populate_us"], st[0]["trace_us"], st[0]["merge_us"]))
+            if flags & 1:
+                st3.append(tuple(evs[i].elapsed_time(evs[i + 1]) * 1e3 for i in range(3)))
         ts = np.array(ts)
         if not (flags & 1):
             print(f"{name}x{S}x{F} graph p50 ms %.4f p99 %.4f  frames/s %.0f  us/frame %.2f" % (np.median(ts), np.percentile(ts, 99), S * F / np.median(ts) * 1e3, np.median(ts) * 1e3 / (S * F)), flush=True)
