@@ -299,8 +299,8 @@ def our_arm(args, world, rank, local):
     ms = start.elapsed_time(end)
     ms = multi.max_over_ranks(ms, dev)
     value = multi.job_throughput(S * K, world, ms / 1000.0)
-    # K1 populate, (K2a rows + K2b tiles when vox_inf > 0), K3 trace, K4 merge, per branch
-    kernels_per_step = (5 if c["vox_inf"] > 0 else 3) * branches
+    # K1 populate, (K2a rows + K2b tiles when vox_inf > 0), K3 trace, K4 merge, K5 publish, per branch
+    kernels_per_step = (6 if c["vox_inf"] > 0 else 4) * branches
 
     # ---- per-kernel device times (the roofline's K3 duration): the same
     # steps as ONE graph branch, stage-boundary events recorded inside the

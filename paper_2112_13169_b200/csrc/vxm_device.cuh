@@ -76,8 +76,14 @@ struct Counters {
   unsigned long long t_pop, t_trace, t_merge, t_end;
   unsigned long long trace_slots[32][4];  // K3 partials, folded by K4 (device only)
 };
-// the part of Counters the host reads back
-constexpr size_t kCountersHostBytes = offsetof(Counters, trace_slots);
+// The part of Counters the host reads back: K5 copies it into host-mapped
+// memory and clears the slot's Counters for the next frame.
+struct CountersHead {
+  unsigned long long points_total, points_outside, rays_traced, voxels_freed, voxels_traced, voxels_skipped,
+      occupied, freed, t_pop, t_trace, t_merge, t_end;
+};
+static_assert(sizeof(CountersHead) == offsetof(Counters, trace_slots), "CountersHead mirrors Counters");
+constexpr size_t kCountersHostBytes = sizeof(CountersHead);
 
 __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;
@@ -137,6 +143,7 @@ struct KParams {
   uint8_t* loc0;
   uint8_t* loc1;
   Counters* counters;
+  CountersHead* counters_out;  // host-mapped read-back (K5)
   const FrameParams* frames;
 };
 

@@ -1043,6 +1043,24 @@ __global__ void __launch_bounds__(256) trace_per_pixel_kernel(KParams p, int fro
 // ---------------------------------------------------------------------------
 constexpr int kRowsPerWarp = 4;
 
+// K5: after K4, one block per slot copies the slot's counters to the
+// host-mapped read-back buffer and zeroes them, K3's per-warp partials
+// included, for the next frame (so the frame graph has neither a memset nor
+// a D2H copy node; a last-block check-in inside K4 cost its ~10k blocks more
+// than this launch).
+__global__ void __launch_bounds__(128) publish_counters_kernel(KParams p) {
+  pdl_wait();  // K4 complete
+  const int s = blockIdx.x;
+  constexpr int kHead = sizeof(CountersHead) / sizeof(unsigned long long);
+  constexpr int kParts = sizeof(Counters::trace_slots) / sizeof(unsigned long long);
+  unsigned long long* c = reinterpret_cast<unsigned long long*>(p.counters + s);
+  if (threadIdx.x < kHead) {
+    reinterpret_cast<unsigned long long*>(p.counters_out + s)[threadIdx.x] = c[threadIdx.x];
+    c[threadIdx.x] = 0ull;
+  }
+  for (int i = threadIdx.x; i < kParts; i += blockDim.x) (&p.counters[s].trace_slots[0][0])[i] = 0ull;
+}
+
 // merge of 4 packed cells: local l4, occupancy o4 (epoch bytes), 4 keys.
 // States are 0..3 per byte, so "== 0" and "== 3" are two-bit tests.
 __device__ __forceinline__ uint32_t merge4(uint32_t l4, uint32_t o4, uint4 k4, uint32_t epoch) {

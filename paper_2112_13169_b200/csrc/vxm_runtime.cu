@@ -6,8 +6,9 @@
 //   host:  validate t_wc, T_vc = compose(T(-origin), t_wc), shift decision,
 //          epoch bump -> FrameParams[S] in pinned memory
 //   H2D:   FrameParams (and the depth frames for the host-buffer entry point)
-//   graph: memset counters | K1 populate | K2 dilate (vox_inf > 0) |
-//          K3 trace_bundle | K4 merge+shift+count | D2H counters
+//   graph: K1 populate | K2 dilate (vox_inf > 0) | K3 trace_bundle |
+//          K4 merge+shift+count | K5 publish (counters to host-mapped
+//          memory, cleared for the next frame)
 // The measurement grid is never reset: epoch-tagged words (vxm_device.cuh).
 
 #include <cuda_runtime.h>
@@ -282,7 +283,7 @@ struct vxm_ctx {
   cudaEvent_t ring_ev[kRing] = {};
   int ring_slot = 0;
   vxm::FrameParams* frames_host = nullptr;  // current ring slot
-  vxm::Counters* counters_host = nullptr;
+  vxm::CountersHead* counters_host = nullptr;  // host-mapped, written by K4
 
   // host state per stream
   std::vector<uint32_t> epoch;
@@ -324,12 +325,18 @@ int graph_branches(const vxm_ctx* c) {
 // rebased to the first slot). `marks` records the stage-boundary events.
 void launch_merge(vxm_ctx* c, const vxm::KParams& kp, int S, cudaStream_t st);
 
+// K5 over S slots: counters -> host-mapped read-back, cleared for the next frame
+void launch_publish(const vxm::KParams& kp, int S, cudaStream_t st) {
+  VXM_CK(vxm::launch_pdl(vxm::publish_counters_kernel, dim3(S), dim3(128), 0, st, kp));
+}
+
 void launch_stages(vxm_ctx* c, bool cloud, bool capturing, int s0, int S, cudaStream_t st, bool marks,
                    bool merge = true) {
   vxm::KParams kp = c->kp;
   const long long n = c->n;
   kp.frames += s0;
   kp.counters += s0;
+  kp.counters_out += s0;
   kp.occ += n * s0;
   kp.key += n * s0;
   if (kp.ctr) kp.ctr += n * s0;
@@ -348,7 +355,6 @@ void launch_stages(vxm_ctx* c, bool cloud, bool capturing, int s0, int S, cudaSt
     VXM_CK(cudaEventRecord(e, st));
   };
   mark(c->ev[1]);
-  VXM_CK(cudaMemsetAsync(kp.counters, 0, sizeof(vxm::Counters) * S, st));
   if (!cloud) {
     // tiles of 256 quads; a block takes `iters` of them once the batch
     // alone fills the GPU several times over (8 blocks per SM)
@@ -390,7 +396,10 @@ void launch_stages(vxm_ctx* c, bool cloud, bool capturing, int s0, int S, cudaSt
     VXM_CK(cudaGetLastError());
   }
   mark(c->ev[3]);
-  if (merge) launch_merge(c, kp, S, st);
+  if (merge) {
+    launch_merge(c, kp, S, st);
+    launch_publish(kp, S, st);
+  }
   mark(c->ev[4]);
 }
 
@@ -433,9 +442,9 @@ void launch_merge(vxm_ctx* c, const vxm::KParams& kp, int S, cudaStream_t st) {
   }
 }
 
-// One frame of every slot: the stages, optionally as two graph branches over
-// halves of the streams (kernels of one branch overlap the other's), then
-// the D2H of the counters.
+// One frame of every slot: the stages, optionally as graph branches over
+// shares of the streams (kernels of one branch overlap the others'); K4
+// then K5 publishes the counters to the host-mapped read-back buffer.
 void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
   // stage-boundary events: always for direct launches (cheap stream
   // records); in a graph only when asked for, since every event-record node
@@ -472,13 +481,13 @@ void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
       VXM_CK(cudaEventRecord(c->join[b], c->side[b]));
       VXM_CK(cudaStreamWaitEvent(c->stream, c->join[b], 0));
     }
-    if (c->F > 1) launch_merge(c, c->kp, c->nslots, c->stream);
+    if (c->F > 1) {
+      launch_merge(c, c->kp, c->nslots, c->stream);
+      launch_publish(c->kp, c->nslots, c->stream);
+    }
   } else {
     launch_stages(c, cloud, capturing, 0, c->nslots, c->stream, marks);
   }
-  // the counters and stage stamps of every slot (not K3's per-warp partials)
-  VXM_CK(cudaMemcpy2DAsync(c->counters_host, sizeof(vxm::Counters), c->counters, sizeof(vxm::Counters),
-                           vxm::kCountersHostBytes, c->nslots, cudaMemcpyDeviceToHost, c->stream));
 }
 
 cudaGraphExec_t capture(vxm_ctx* c, bool cloud, int gi, int pp, bool marks) {
@@ -652,7 +661,7 @@ void collect_stats(vxm_ctx* c, vxm_stats* out) {
   }
   if (!out) return;
   for (int s = 0; s < c->nslots; ++s) {
-    const vxm::Counters& k = c->counters_host[s];
+    const vxm::CountersHead& k = c->counters_host[s];
     vxm_stats& o = out[s];
     std::memset(&o, 0, sizeof(o));
     o.points_total = k.points_total;
@@ -857,6 +866,7 @@ int vxm_create_multi(const vxm_config* cfg, int32_t n_streams, int32_t frames_pe
       VXM_CK(cudaMemsetAsync(c->loc[b], 0, c->n * NS, c->stream));
     }
     VXM_CK(cudaMalloc(&c->counters, sizeof(vxm::Counters) * S));
+    VXM_CK(cudaMemsetAsync(c->counters, 0, sizeof(vxm::Counters) * S, c->stream));  // then cleared by K4
     for (int b = 0; b < vxm_ctx::kPP; ++b) {
       VXM_CK(cudaMalloc(&c->frames_pp[b], sizeof(vxm::FrameParams) * S));
       VXM_CK(cudaEventCreateWithFlags(&c->pp_ready[b], cudaEventDisableTiming));
@@ -868,8 +878,9 @@ int vxm_create_multi(const vxm_config* cfg, int32_t n_streams, int32_t frames_pe
     std::memset(c->frames_ring, 0, sizeof(vxm::FrameParams) * S * vxm_ctx::kRing);
     for (auto& e : c->ring_ev) VXM_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     c->frames_host = c->frames_ring;
-    VXM_CK(cudaMallocHost(&c->counters_host, sizeof(vxm::Counters) * S));
-    std::memset(c->counters_host, 0, sizeof(vxm::Counters) * S);
+    VXM_CK(cudaHostAlloc(&c->counters_host, sizeof(vxm::CountersHead) * S, cudaHostAllocMapped));
+    std::memset(c->counters_host, 0, sizeof(vxm::CountersHead) * S);
+
     c->epoch.assign(S, 0);
     c->cur.assign(NS, 0);
     c->origin.resize(3 * NS);
@@ -930,6 +941,8 @@ int vxm_create_multi(const vxm_config* cfg, int32_t n_streams, int32_t frames_pe
     kp.loc0 = c->loc[0];
     kp.loc1 = c->loc[1];
     kp.counters = c->counters;
+    VXM_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&kp.counters_out), c->counters_host, 0));
+
     kp.frames = c->frames_pp[0];
     if (cfg->vox_inf > 0) {
       const size_t smem = vxm::dilate_smem_bytes(cfg->vox_inf, kp.dx);
