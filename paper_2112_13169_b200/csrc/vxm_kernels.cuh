@@ -671,6 +671,8 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   // A write is dropped when lane+1 or lane+8 (higher ray indices) makes the
   // same cell in the same step (measured: dropping the dedup after the first
   // chunks slows the kernel, the extra L2 atomics cost more than the check).
+  // The lanes compare cells only: two lanes on the same cell read the same
+  // occupancy byte, so either both write or neither does.
   // kTail: invalid cells only follow the end of the ray (the in-grid walk);
   // otherwise they can precede its entry into the grid (camera outside).
   auto resolve_t = [&](const uint32_t (&cell)[kChunk], auto tail_tag) {
@@ -687,19 +689,17 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
       if constexpr (kTail)
       asm volatile("{\n\t"
                    ".reg .pred io, w, p1, p8, d1, d8, ok;\n\t"
-                   ".reg .b32 id, r1, r8, kv;\n\t"
+                   ".reg .b32 r1, r8, kv;\n\t"
                    ".reg .b64 a;\n\t"
-                   "setp.eq.u32 io, %4, %5;\n\t"
-                   "setp.ne.u32 w, %4, %5;\n\t"
+                   "setp.eq.u32 io|w, %4, %5;\n\t"
                    "@w add.u32 %1, %1, 1;\n\t"
                    "@w add.u32 %2, %2, %0;\n\t"
                    "or.b32 kv, %6, %0;\n\t"
                    "selp.u32 %0, 1, %0, io;\n\t"
-                   "selp.u32 id, %3, -1, w;\n\t"
-                   "shfl.sync.down.b32 r1|p1, id, 1, 31, -1;\n\t"
-                   "shfl.sync.down.b32 r8|p8, id, 8, 31, -1;\n\t"
-                   "setp.eq.and.u32 d1, r1, id, p1;\n\t"
-                   "setp.eq.and.u32 d8, r8, id, p8;\n\t"
+                   "shfl.sync.down.b32 r1|p1, %3, 1, 31, -1;\n\t"
+                   "shfl.sync.down.b32 r8|p8, %3, 8, 31, -1;\n\t"
+                   "setp.eq.and.u32 d1, r1, %3, p1;\n\t"
+                   "setp.eq.and.u32 d8, r8, %3, p8;\n\t"
                    "or.pred d1, d1, d8;\n\t"
                    "not.pred d1, d1;\n\t"
                    "and.pred ok, w, d1;\n\t"
@@ -713,7 +713,7 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
       else
       asm volatile("{\n\t"
                    ".reg .pred v, io, w, p1, p8, d1, d8, ok;\n\t"
-                   ".reg .b32 id, r1, r8, kv;\n\t"
+                   ".reg .b32 r1, r8, kv;\n\t"
                    ".reg .b64 a;\n\t"
                    "setp.ne.u32 v, %3, -1;\n\t"
                    "setp.eq.and.u32 io, %4, %5, v;\n\t"
@@ -722,11 +722,10 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
                    "@w add.u32 %2, %2, %0;\n\t"
                    "or.b32 kv, %6, %0;\n\t"
                    "selp.u32 %0, 1, %0, io;\n\t"
-                   "selp.u32 id, %3, -1, w;\n\t"
-                   "shfl.sync.down.b32 r1|p1, id, 1, 31, -1;\n\t"
-                   "shfl.sync.down.b32 r8|p8, id, 8, 31, -1;\n\t"
-                   "setp.eq.and.u32 d1, r1, id, p1;\n\t"
-                   "setp.eq.and.u32 d8, r8, id, p8;\n\t"
+                   "shfl.sync.down.b32 r1|p1, %3, 1, 31, -1;\n\t"
+                   "shfl.sync.down.b32 r8|p8, %3, 8, 31, -1;\n\t"
+                   "setp.eq.and.u32 d1, r1, %3, p1;\n\t"
+                   "setp.eq.and.u32 d8, r8, %3, p8;\n\t"
                    "or.pred d1, d1, d8;\n\t"
                    "not.pred d1, d1;\n\t"
                    "and.pred ok, w, d1;\n\t"
