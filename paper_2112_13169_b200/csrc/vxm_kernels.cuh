@@ -554,12 +554,18 @@ inline cudaError_t dilate_set_smem(int bytes) {
 // kernel issue- and ALU-pipe bound, so the step and the resolve are written to
 // minimise instructions per visit. The Sequential last-writer rule is a
 // fire-and-forget RED.max on the cell key; before issuing it a lane drops its
-// write when lane+1 or lane+8 (both higher ray indices) writes the same cell
-// in the same step, which removes most same-address traffic near the camera.
+// write when a higher lane (a higher ray index) writes the same cell in the
+// same step, which removes most same-address traffic near the camera: over
+// the whole warp with one match.any in the batch kernel, against lane+1 and
+// lane+8 with two shuffles in the lone-frame kernel (shorter latency).
 // Counters go to 32 per-stream slots (one RED per warp each), summed by K4.
 // ---------------------------------------------------------------------------
 #ifndef VXM_TSEL_MUL
 #define VXM_TSEL_MUL 0
+#endif
+
+#ifndef VXM_DEDUP_MATCH
+#define VXM_DEDUP_MATCH 1
 #endif
 
 constexpr int kTraceSlots = 32;
@@ -619,7 +625,7 @@ __device__ __forceinline__ void ray_setup(const double* R, const double* start, 
 // few spilled values; 4-7% faster than one warp per block at 64 registers),
 // a lone frame (358 warps, GPU far from full) runs 8-step chunks at 64
 // registers, where per-warp latency decides.
-template <int kChunk, int kTraceWarps, int kMinBlocks>
+template <int kChunk, int kTraceWarps, int kMinBlocks, bool kMatch>
 __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_kernel(KParams p) {
   const int s = blockIdx.y;
   const FrameParams* fp = p.frames + s;
@@ -668,8 +674,10 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   // predicates, and a predicated fire-and-forget RED.max on the key.
   unsigned lw = 0, lt = 0;
   const unsigned long long key_base = reinterpret_cast<unsigned long long>(key);
-  // A write is dropped when lane+1 or lane+8 (higher ray indices) makes the
-  // same cell in the same step (measured: dropping the dedup after the first
+  uint32_t gt_mask;  // lanes above this one (higher ray indices)
+  asm("mov.u32 %0, %%lanemask_gt;" : "=r"(gt_mask));
+  // A write is dropped when a higher lane (higher ray index) makes the same
+  // cell in the same step (measured: dropping the dedup after the first
   // chunks slows the kernel, the extra L2 atomics cost more than the check).
   // The lanes compare cells only: two lanes on the same cell read the same
   // occupancy byte, so either both write or neither does.
@@ -686,56 +694,65 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
     }
 #pragma unroll
     for (int j = 0; j < kChunk; ++j) {
-      if constexpr (kTail)
-      asm volatile("{\n\t"
-                   ".reg .pred io, w, p1, p8, d1, d8, ok;\n\t"
-                   ".reg .b32 r1, r8, kv;\n\t"
-                   ".reg .b64 a;\n\t"
-                   "setp.eq.u32 io|w, %4, %5;\n\t"
-                   "@w add.u32 %1, %1, 1;\n\t"
-                   "@w add.u32 %2, %2, %0;\n\t"
-                   "or.b32 kv, %6, %0;\n\t"
-                   "selp.u32 %0, 1, %0, io;\n\t"
-                   "shfl.sync.down.b32 r1|p1, %3, 1, 31, -1;\n\t"
-                   "shfl.sync.down.b32 r8|p8, %3, 8, 31, -1;\n\t"
-                   "setp.eq.and.u32 d1, r1, %3, p1;\n\t"
-                   "setp.eq.and.u32 d8, r8, %3, p8;\n\t"
-                   "or.pred d1, d1, d8;\n\t"
-                   "not.pred d1, d1;\n\t"
-                   "and.pred ok, w, d1;\n\t"
-                   "mul.wide.u32 a, %3, 4;\n\t"
-                   "add.u64 a, a, %7;\n\t"
-                   "@ok red.relaxed.gpu.global.max.u32 [a], kv;\n\t"
-                   "}"
-                   : "+r"(traced_bit), "+r"(lw), "+r"(lt)
-                   : "r"(cell[j]), "r"(o[j]), "r"(epoch), "r"(ray_key), "l"(key_base)
-                   : "memory");
+// the per-cell resolve: predicates io (occupied) / w (write), the counters,
+// the traced-bit state, the dedup into ok, the predicated RED.max
+#define VXM_RESOLVE_COUNT                 \
+  "@w add.u32 %1, %1, 1;\n\t"            \
+  "@w add.u32 %2, %2, %0;\n\t"           \
+  "or.b32 kv, %6, %0;\n\t"               \
+  "selp.u32 %0, 1, %0, io;\n\t"
+// dedup with lane+1 and lane+8 (two shuffles; the lone-frame kernel, whose
+// serial chain favours short latency)
+#define VXM_DEDUP_SHFL                              \
+  "shfl.sync.down.b32 r1|p1, %3, 1, 31, -1;\n\t"  \
+  "shfl.sync.down.b32 r8|p8, %3, 8, 31, -1;\n\t"  \
+  "setp.eq.and.u32 d1, r1, %3, p1;\n\t"           \
+  "setp.eq.and.u32 d8, r8, %3, p8;\n\t"           \
+  "or.pred d1, d1, d8;\n\t"                       \
+  "not.pred d1, d1;\n\t"                          \
+  "and.pred ok, w, d1;\n\t"
+// dedup over the whole warp: only the highest lane of each distinct cell
+// writes (one match; batches, where instruction count decides)
+#define VXM_DEDUP_MATCH                    \
+  "match.any.sync.b32 r1, %3, -1;\n\t"   \
+  "and.b32 r1, r1, %8;\n\t"              \
+  "setp.eq.and.u32 ok, r1, 0, w;\n\t"
+#define VXM_RESOLVE_RED                    \
+  "mul.wide.u32 a, %3, 4;\n\t"           \
+  "add.u64 a, a, %7;\n\t"                \
+  "@ok red.relaxed.gpu.global.max.u32 [a], kv;\n\t"
+#define VXM_RESOLVE_DECL                                \
+  ".reg .pred v, io, w, p1, p8, d1, d8, ok;\n\t"      \
+  ".reg .b32 r1, r8, kv;\n\t"                         \
+  ".reg .b64 a;\n\t"
+// kTail: the cell is valid or the ray has ended (o == epoch: no write)
+#define VXM_RESOLVE_HEAD_TAIL "setp.eq.u32 io|w, %4, %5;\n\t"
+// otherwise invalid cells (0xffffffff) may also precede the grid entry
+#define VXM_RESOLVE_HEAD_ANY                \
+  "setp.ne.u32 v, %3, -1;\n\t"            \
+  "setp.eq.and.u32 io, %4, %5, v;\n\t"    \
+  "setp.ne.and.u32 w, %4, %5, v;\n\t"
+#define VXM_RESOLVE_ASM(HEAD, DEDUP)                                                            \
+  asm volatile("{\n\t" VXM_RESOLVE_DECL HEAD VXM_RESOLVE_COUNT DEDUP VXM_RESOLVE_RED "}"      \
+               : "+r"(traced_bit), "+r"(lw), "+r"(lt)                                           \
+               : "r"(cell[j]), "r"(o[j]), "r"(epoch), "r"(ray_key), "l"(key_base), "r"(gt_mask) \
+               : "memory")
+      if constexpr (kTail && kMatch)
+        VXM_RESOLVE_ASM(VXM_RESOLVE_HEAD_TAIL, VXM_DEDUP_MATCH);
+      else if constexpr (kTail)
+        VXM_RESOLVE_ASM(VXM_RESOLVE_HEAD_TAIL, VXM_DEDUP_SHFL);
+      else if constexpr (kMatch)
+        VXM_RESOLVE_ASM(VXM_RESOLVE_HEAD_ANY, VXM_DEDUP_MATCH);
       else
-      asm volatile("{\n\t"
-                   ".reg .pred v, io, w, p1, p8, d1, d8, ok;\n\t"
-                   ".reg .b32 r1, r8, kv;\n\t"
-                   ".reg .b64 a;\n\t"
-                   "setp.ne.u32 v, %3, -1;\n\t"
-                   "setp.eq.and.u32 io, %4, %5, v;\n\t"
-                   "setp.ne.and.u32 w, %4, %5, v;\n\t"
-                   "@w add.u32 %1, %1, 1;\n\t"
-                   "@w add.u32 %2, %2, %0;\n\t"
-                   "or.b32 kv, %6, %0;\n\t"
-                   "selp.u32 %0, 1, %0, io;\n\t"
-                   "shfl.sync.down.b32 r1|p1, %3, 1, 31, -1;\n\t"
-                   "shfl.sync.down.b32 r8|p8, %3, 8, 31, -1;\n\t"
-                   "setp.eq.and.u32 d1, r1, %3, p1;\n\t"
-                   "setp.eq.and.u32 d8, r8, %3, p8;\n\t"
-                   "or.pred d1, d1, d8;\n\t"
-                   "not.pred d1, d1;\n\t"
-                   "and.pred ok, w, d1;\n\t"
-                   "mul.wide.u32 a, %3, 4;\n\t"
-                   "add.u64 a, a, %7;\n\t"
-                   "@ok red.relaxed.gpu.global.max.u32 [a], kv;\n\t"
-                   "}"
-                   : "+r"(traced_bit), "+r"(lw), "+r"(lt)
-                   : "r"(cell[j]), "r"(o[j]), "r"(epoch), "r"(ray_key), "l"(key_base)
-                   : "memory");
+        VXM_RESOLVE_ASM(VXM_RESOLVE_HEAD_ANY, VXM_DEDUP_SHFL);
+#undef VXM_RESOLVE_ASM
+#undef VXM_RESOLVE_HEAD_ANY
+#undef VXM_RESOLVE_HEAD_TAIL
+#undef VXM_RESOLVE_DECL
+#undef VXM_RESOLVE_RED
+#undef VXM_DEDUP_MATCH
+#undef VXM_DEDUP_SHFL
+#undef VXM_RESOLVE_COUNT
     }
   };
   auto resolve = [&](const uint32_t (&cell)[kChunk]) { resolve_t(cell, std::false_type{}); };
@@ -888,9 +905,9 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
 inline void launch_trace(const KParams& kp, int slots, cudaStream_t st) {
   const int tiles = kp.tiles_x * kp.tiles_y;
   if (slots >= 8) {
-    launch_pdl(trace_bundle_kernel<4, 2, 24>, dim3((tiles + 1) / 2, slots), dim3(64), 0, st, kp);
+    launch_pdl(trace_bundle_kernel<4, 2, 24, true>, dim3((tiles + 1) / 2, slots), dim3(64), 0, st, kp);
   } else {
-    launch_pdl(trace_bundle_kernel<8, 1, 1>, dim3(tiles, slots), dim3(32), 0, st, kp);
+    launch_pdl(trace_bundle_kernel<8, 1, 1, false>, dim3(tiles, slots), dim3(32), 0, st, kp);
   }
 }
 
