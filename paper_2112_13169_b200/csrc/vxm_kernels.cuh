@@ -560,9 +560,6 @@ inline cudaError_t dilate_set_smem(int bytes) {
 // lane+8 with two shuffles in the lone-frame kernel (shorter latency).
 // Counters go to 32 per-stream slots (one RED per warp each), summed by K4.
 // ---------------------------------------------------------------------------
-#ifndef VXM_TSEL_MUL
-#define VXM_TSEL_MUL 0
-#endif
 
 #ifndef VXM_DEDUP_MATCH
 #define VXM_DEDUP_MATCH 1
@@ -803,9 +800,8 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
         // below its threshold. t + 0 == t for the axes not taken (t >= 0).
         asm("{\n\t"
             ".reg .pred q, px, py, pz, npx, s0, s1, s2, ok;\n\t"
-            ".reg .f64 a0, a1, a2, f0, f1, f2;\n\t"
-            ".reg .b32 l, h0, h1, h2, zl;\n\t"
-            "mov.b32 zl, 0;\n\t"
+            ".reg .f64 a0, a1, a2;\n\t"
+            ".reg .b32 l;\n\t"
             "setp.le.f64 q, %0, %1;\n\t"
             "setp.le.and.f64 px, %0, %2, q;\n\t"
             "setp.le.f64 q, %1, %2;\n\t"
@@ -819,23 +815,9 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
             "or.pred ok, s0, s1;\n\t"
             "or.pred ok, ok, s2;\n\t"
             "selp.u32 %4, %4, 0, ok;\n\t"
-#if VXM_TSEL_MUL
-            // tdelta * (1.0 or 0.0): one 32-bit select per axis (the low
-            // words of both factors are 0) and a multiply on the fp64 pipe
-            "selp.b32 h0, 1072693248, 0, px;\n\t"
-            "selp.b32 h1, 1072693248, 0, py;\n\t"
-            "selp.b32 h2, 1072693248, 0, pz;\n\t"
-            "mov.b64 f0, {zl, h0};\n\t"
-            "mov.b64 f1, {zl, h1};\n\t"
-            "mov.b64 f2, {zl, h2};\n\t"
-            "mul.rn.f64 a0, %5, f0;\n\t"
-            "mul.rn.f64 a1, %6, f1;\n\t"
-            "mul.rn.f64 a2, %7, f2;\n\t"
-#else
             "selp.f64 a0, %5, 0d0000000000000000, px;\n\t"
             "selp.f64 a1, %6, 0d0000000000000000, py;\n\t"
             "selp.f64 a2, %7, 0d0000000000000000, pz;\n\t"
-#endif
             "add.rn.f64 %0, %0, a0;\n\t"
             "add.rn.f64 %1, %1, a1;\n\t"
             "add.rn.f64 %2, %2, a2;\n\t"
