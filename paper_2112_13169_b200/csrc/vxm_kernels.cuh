@@ -622,7 +622,7 @@ __device__ __forceinline__ void ray_setup(const double* R, const double* start, 
 // few spilled values; 4-7% faster than one warp per block at 64 registers),
 // a lone frame (358 warps, GPU far from full) runs 8-step chunks at 64
 // registers, where per-warp latency decides.
-template <int kChunk, int kTraceWarps, int kMinBlocks, bool kMatch>
+template <int kChunk, int kTraceWarps, int kMinBlocks, bool kMatch, bool kFast>
 __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_kernel(KParams p) {
   const int s = blockIdx.y;
   const FrameParams* fp = p.frames + s;
@@ -790,7 +790,51 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
     uint32_t al = active ? 1u : 0u;
     bool alive = active;
     uint32_t uidx = static_cast<uint32_t>(idx);
+    // Fast chunks (kFast): the walk can only end at a step whose chosen tmax (the
+    // current minimum) reaches min(M_a); the minimum grows by at most
+    // max(tdelta) per step, so while min(t) < lim = min(M) - (kChunk-1) *
+    // max(tdelta) (less a 2^-40 relative margin for the rounded adds) no
+    // step of the next chunk can end the walk and the threshold tests are
+    // skipped. The warp takes the fast form when all its live lanes qualify.
+    // Measured: 2-5% faster for a lone frame (8-step chunks, 72 registers);
+    // 2% slower in the 40-register batch kernel, which does not use it.
+    const double dmax = fmax(fmax(e0, e1), e2);
+    const double Mmin = fmin(fmin(M0, M1), M2);
+    const double lim = dsub(Mmin, dadd(dmul(static_cast<double>(kChunk - 1), dmax),
+                                       dmul(0x1p-40, dadd(fabs(Mmin), dmul(static_cast<double>(kChunk), dmax)))));
     while (__any_sync(0xffffffffu, alive)) {
+      if (kFast && __all_sync(0xffffffffu, !al || t0 < lim || t1 < lim || t2 < lim)) {
+        uint32_t cell[kChunk];
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) {
+          cell[j] = al ? uidx : 0xffffffffu;
+          asm("{\n\t"
+              ".reg .pred q, px, py, pz, npx;\n\t"
+              ".reg .f64 a0, a1, a2;\n\t"
+              ".reg .b32 l;\n\t"
+              "setp.le.f64 q, %0, %1;\n\t"
+              "setp.le.and.f64 px, %0, %2, q;\n\t"
+              "setp.le.f64 q, %1, %2;\n\t"
+              "not.pred npx, px;\n\t"
+              "and.pred py, q, npx;\n\t"
+              "or.pred pz, px, py;\n\t"
+              "not.pred pz, pz;\n\t"
+              "selp.f64 a0, %4, 0d0000000000000000, px;\n\t"
+              "selp.f64 a1, %5, 0d0000000000000000, py;\n\t"
+              "selp.f64 a2, %6, 0d0000000000000000, pz;\n\t"
+              "add.rn.f64 %0, %0, a0;\n\t"
+              "add.rn.f64 %1, %1, a1;\n\t"
+              "add.rn.f64 %2, %2, a2;\n\t"
+              "selp.b32 l, %8, %9, py;\n\t"
+              "selp.b32 l, %7, l, px;\n\t"
+              "add.s32 %3, %3, l;\n\t"
+              "}"
+              : "+d"(t0), "+d"(t1), "+d"(t2), "+r"(uidx)
+              : "d"(e0), "d"(e1), "d"(e2), "r"(lin0), "r"(lin1), "r"(lin2));
+        }
+        resolve_tail(cell);
+        continue;
+      }
       uint32_t cell[kChunk];
 #pragma unroll
       for (int j = 0; j < kChunk; ++j) {
@@ -887,9 +931,9 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
 inline void launch_trace(const KParams& kp, int slots, cudaStream_t st) {
   const int tiles = kp.tiles_x * kp.tiles_y;
   if (slots >= 8) {
-    launch_pdl(trace_bundle_kernel<4, 2, 24, true>, dim3((tiles + 1) / 2, slots), dim3(64), 0, st, kp);
+    launch_pdl(trace_bundle_kernel<4, 2, 24, true, false>, dim3((tiles + 1) / 2, slots), dim3(64), 0, st, kp);
   } else {
-    launch_pdl(trace_bundle_kernel<8, 1, 1, false>, dim3(tiles, slots), dim3(32), 0, st, kp);
+    launch_pdl(trace_bundle_kernel<8, 1, 1, false, true>, dim3(tiles, slots), dim3(32), 0, st, kp);
   }
 }
 
