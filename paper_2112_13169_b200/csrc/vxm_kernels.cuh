@@ -1499,10 +1499,32 @@ __global__ void __launch_bounds__(256) merge_shift_count_tma_kernel(KParams p) {
 // ---------------------------------------------------------------------------
 constexpr int kMaxFramesPerCall = 64;
 
+// Warp sums of per-frame Occupied / Free counts packed as bytes (frame k0+u:
+// byte pair u&1 of word u>>1; every warp sum is <= 128), added by lane 0 into
+// the block's per-frame counters (32-bit shared atomics: [k] occupied,
+// [kMaxFramesPerCall + k] freed).
+template <int U>
+__device__ __forceinline__ void add_frame_counts(const uint32_t (&packed)[U / 2], unsigned* cnt, int k0, int F,
+                                                 int lane) {
+#pragma unroll
+  for (int h = 0; h < U / 2; ++h) {
+    const uint32_t sum = __reduce_add_sync(0xffffffffu, packed[h]);
+    if (lane == 0 && sum) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int k = k0 + 2 * h + q;
+        const uint32_t half = (sum >> (16 * q)) & 0xffffu;
+        if (k < F && (half & 0xffu)) atomicAdd(&cnt[k], half & 0xffu);
+        if (k < F && (half >> 8)) atomicAdd(&cnt[kMaxFramesPerCall + k], half >> 8);
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
   pdl_wait();  // K3's keys and counters
   constexpr int U = 4;  // frames whose loads are issued together
-  __shared__ unsigned long long cnt[kMaxFramesPerCall];     // occupied | freed << 32
+  __shared__ unsigned cnt[2 * kMaxFramesPerCall];           // occupied, then freed, per frame
   __shared__ int Pc[kMaxFramesPerCall + U][3];              // P_{k-1} at index k
   __shared__ uint32_t ep[kMaxFramesPerCall];
   const int s = blockIdx.y;  // stream
@@ -1512,7 +1534,7 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
     const unsigned long long t = global_ns();
     for (int k = threadIdx.x; k < F; k += blockDim.x) p.counters[static_cast<long long>(s) * F + k].t_merge = t;
   }
-  for (int k = threadIdx.x; k < kMaxFramesPerCall; k += blockDim.x) cnt[k] = 0ull;
+  for (int k = threadIdx.x; k < 2 * kMaxFramesPerCall; k += blockDim.x) cnt[k] = 0u;
   __shared__ int vec_ok;
   if (threadIdx.x == 0) {
     int P[3] = {0, 0, 0};
@@ -1582,6 +1604,9 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
           o[u] = ld ? __ldcs(reinterpret_cast<const uint32_t*>(occ0 + off)) : 0u;
           kk[u] = ld ? __ldcs(reinterpret_cast<const uint4*>(key0 + off)) : make_uint4(0u, 0u, 0u, 0u);
         }
+        // per frame: Occupied / Free counts of this thread's 4 cells (each
+        // <= 4, so a warp sum fits a byte); two frames share one reduction
+        uint32_t packed[U / 2] = {};
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int k = k0 + u;
@@ -1589,10 +1614,9 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
           const bool in_r = u == 0 ? in_prev : in_c[u - 1];
           if (in_c[u]) val = in_r ? merge4(val, o[u], kk[u], ep[k]) : 0u;  // shifted in: Unknown
           const unsigned oc = in_c[u] ? count_occupied4(val) : 0u, fr = in_c[u] ? count_free4(val) : 0u;
-          const unsigned long long w = __reduce_add_sync(0xffffffffu, oc) |
-                                       (static_cast<unsigned long long>(__reduce_add_sync(0xffffffffu, fr)) << 32);
-          if (lane == 0 && w) atomicAdd(&cnt[k], w);
+          packed[u >> 1] |= (oc | (fr << 8)) << (16 * (u & 1));
         }
+        add_frame_counts<U>(packed, cnt, k0, F, lane);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           if (k0 + u < F) {
@@ -1636,17 +1660,17 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
         o[u] = ld ? __ldcs(occ0 + off) : 0u;
         kk[u] = ld ? __ldcs(key0 + off) : 0u;
       }
+      uint32_t packed[U / 2] = {};
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int k = k0 + u;
         if (k >= F) break;
         const bool in_r = u == 0 ? in_prev : in_c[u - 1];
         if (in_c[u]) val = in_r ? merge_cell(val, decode_cell(o[u], kk[u], ep[k])) : 0u;  // shifted in: Unknown
-        const unsigned long long both = !in_c[u] ? 0ull : (val == 2u ? 1ull : (val == 1u ? (1ull << 32) : 0ull));
-        const unsigned long long w = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(both)) |
-                                     (static_cast<unsigned long long>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(both >> 32))) << 32);
-        if (lane == 0 && w) atomicAdd(&cnt[k], w);
+        const unsigned oc = in_c[u] && val == 2u ? 1u : 0u, fr = in_c[u] && val == 1u ? 1u : 0u;
+        packed[u >> 1] |= (oc | (fr << 8)) << (16 * (u & 1));
       }
+      add_frame_counts<U>(packed, cnt, k0, F, lane);
       // position after the group's last frame (F may end inside the group)
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -1662,9 +1686,8 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
   const unsigned long long t_end = global_ns();
   for (int k = threadIdx.x; k < F; k += blockDim.x) {
     Counters& c = p.counters[static_cast<long long>(s) * F + k];
-    const unsigned long long v = cnt[k];
-    if (v & 0xffffffffull) atomicAdd(&c.occupied, v & 0xffffffffull);
-    if (v >> 32) atomicAdd(&c.freed, v >> 32);
+    if (cnt[k]) atomicAdd(&c.occupied, static_cast<unsigned long long>(cnt[k]));
+    if (cnt[kMaxFramesPerCall + k]) atomicAdd(&c.freed, static_cast<unsigned long long>(cnt[kMaxFramesPerCall + k]));
     atomicMax(&c.t_end, t_end);
   }
 }
