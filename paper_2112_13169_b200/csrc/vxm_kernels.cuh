@@ -561,10 +561,6 @@ inline cudaError_t dilate_set_smem(int bytes) {
 // Counters go to 32 per-stream slots (one RED per warp each), summed by K4.
 // ---------------------------------------------------------------------------
 
-#ifndef VXM_DEDUP_MATCH
-#define VXM_DEDUP_MATCH 1
-#endif
-
 constexpr int kTraceSlots = 32;
 
 struct RayState {
@@ -689,38 +685,50 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
       // (its traced bit no longer matters)
       o[j] = cell[j] != 0xffffffffu ? __ldg(occ + cell[j]) : (kTail ? epoch : 0u);
     }
+    // the dedup first, for all cells of the chunk (it does not depend on the
+    // loads, so its shuffle / match latency overlaps theirs): dup[j] != 0
+    // when a higher lane makes the same cell in step j
+    uint32_t dup[kChunk];
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j) {
+      if constexpr (kMatch) {
+        // the whole warp: only the highest lane of each distinct cell writes
+        // (one match; batches, where instruction count decides)
+        asm("match.any.sync.b32 %0, %1, -1;" : "=r"(dup[j]) : "r"(cell[j]));
+        dup[j] &= gt_mask;
+      } else {
+        // lane+1 and lane+8 (two shuffles; the lone-frame kernel, whose serial
+        // chain favours short latency)
+        asm("{\n\t"
+            ".reg .pred p1, p8, d1, d8;\n\t"
+            ".reg .b32 r1, r8;\n\t"
+            "shfl.sync.down.b32 r1|p1, %1, 1, 31, -1;\n\t"
+            "shfl.sync.down.b32 r8|p8, %1, 8, 31, -1;\n\t"
+            "setp.eq.and.u32 d1, r1, %1, p1;\n\t"
+            "setp.eq.and.u32 d8, r8, %1, p8;\n\t"
+            "or.pred d1, d1, d8;\n\t"
+            "selp.u32 %0, 1, 0, d1;\n\t"
+            "}"
+            : "=r"(dup[j])
+            : "r"(cell[j]));
+      }
+    }
 #pragma unroll
     for (int j = 0; j < kChunk; ++j) {
 // the per-cell resolve: predicates io (occupied) / w (write), the counters,
-// the traced-bit state, the dedup into ok, the predicated RED.max
-#define VXM_RESOLVE_COUNT                 \
+// the traced-bit state, ok = w and no higher-lane duplicate, the RED.max
+#define VXM_RESOLVE_BODY                   \
   "@w add.u32 %1, %1, 1;\n\t"            \
   "@w add.u32 %2, %2, %0;\n\t"           \
   "or.b32 kv, %6, %0;\n\t"               \
-  "selp.u32 %0, 1, %0, io;\n\t"
-// dedup with lane+1 and lane+8 (two shuffles; the lone-frame kernel, whose
-// serial chain favours short latency)
-#define VXM_DEDUP_SHFL                              \
-  "shfl.sync.down.b32 r1|p1, %3, 1, 31, -1;\n\t"  \
-  "shfl.sync.down.b32 r8|p8, %3, 8, 31, -1;\n\t"  \
-  "setp.eq.and.u32 d1, r1, %3, p1;\n\t"           \
-  "setp.eq.and.u32 d8, r8, %3, p8;\n\t"           \
-  "or.pred d1, d1, d8;\n\t"                       \
-  "not.pred d1, d1;\n\t"                          \
-  "and.pred ok, w, d1;\n\t"
-// dedup over the whole warp: only the highest lane of each distinct cell
-// writes (one match; batches, where instruction count decides)
-#define VXM_DEDUP_MATCH                    \
-  "match.any.sync.b32 r1, %3, -1;\n\t"   \
-  "and.b32 r1, r1, %8;\n\t"              \
-  "setp.eq.and.u32 ok, r1, 0, w;\n\t"
-#define VXM_RESOLVE_RED                    \
+  "selp.u32 %0, 1, %0, io;\n\t"          \
+  "setp.eq.and.u32 ok, %8, 0, w;\n\t"    \
   "mul.wide.u32 a, %3, 4;\n\t"           \
   "add.u64 a, a, %7;\n\t"                \
   "@ok red.relaxed.gpu.global.max.u32 [a], kv;\n\t"
-#define VXM_RESOLVE_DECL                                \
-  ".reg .pred v, io, w, p1, p8, d1, d8, ok;\n\t"      \
-  ".reg .b32 r1, r8, kv;\n\t"                         \
+#define VXM_RESOLVE_DECL                   \
+  ".reg .pred v, io, w, ok;\n\t"         \
+  ".reg .b32 kv;\n\t"                    \
   ".reg .b64 a;\n\t"
 // kTail: the cell is valid or the ray has ended (o == epoch: no write)
 #define VXM_RESOLVE_HEAD_TAIL "setp.eq.u32 io|w, %4, %5;\n\t"
@@ -729,27 +737,20 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   "setp.ne.u32 v, %3, -1;\n\t"            \
   "setp.eq.and.u32 io, %4, %5, v;\n\t"    \
   "setp.ne.and.u32 w, %4, %5, v;\n\t"
-#define VXM_RESOLVE_ASM(HEAD, DEDUP)                                                            \
-  asm volatile("{\n\t" VXM_RESOLVE_DECL HEAD VXM_RESOLVE_COUNT DEDUP VXM_RESOLVE_RED "}"      \
-               : "+r"(traced_bit), "+r"(lw), "+r"(lt)                                           \
-               : "r"(cell[j]), "r"(o[j]), "r"(epoch), "r"(ray_key), "l"(key_base), "r"(gt_mask) \
+#define VXM_RESOLVE_ASM(HEAD)                                                                 \
+  asm volatile("{\n\t" VXM_RESOLVE_DECL HEAD VXM_RESOLVE_BODY "}"                            \
+               : "+r"(traced_bit), "+r"(lw), "+r"(lt)                                         \
+               : "r"(cell[j]), "r"(o[j]), "r"(epoch), "r"(ray_key), "l"(key_base), "r"(dup[j]) \
                : "memory")
-      if constexpr (kTail && kMatch)
-        VXM_RESOLVE_ASM(VXM_RESOLVE_HEAD_TAIL, VXM_DEDUP_MATCH);
-      else if constexpr (kTail)
-        VXM_RESOLVE_ASM(VXM_RESOLVE_HEAD_TAIL, VXM_DEDUP_SHFL);
-      else if constexpr (kMatch)
-        VXM_RESOLVE_ASM(VXM_RESOLVE_HEAD_ANY, VXM_DEDUP_MATCH);
+      if constexpr (kTail)
+        VXM_RESOLVE_ASM(VXM_RESOLVE_HEAD_TAIL);
       else
-        VXM_RESOLVE_ASM(VXM_RESOLVE_HEAD_ANY, VXM_DEDUP_SHFL);
+        VXM_RESOLVE_ASM(VXM_RESOLVE_HEAD_ANY);
 #undef VXM_RESOLVE_ASM
 #undef VXM_RESOLVE_HEAD_ANY
 #undef VXM_RESOLVE_HEAD_TAIL
 #undef VXM_RESOLVE_DECL
-#undef VXM_RESOLVE_RED
-#undef VXM_DEDUP_MATCH
-#undef VXM_DEDUP_SHFL
-#undef VXM_RESOLVE_COUNT
+#undef VXM_RESOLVE_BODY
     }
   };
   auto resolve = [&](const uint32_t (&cell)[kChunk]) { resolve_t(cell, std::false_type{}); };
@@ -928,9 +929,11 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
 }
 
 // Launches K3 over `slots` frame slots in the shape that suits the batch.
-inline void launch_trace(const KParams& kp, int slots, cudaStream_t st) {
+// `batch` is the number of slots of the whole call (graph branches launch
+// shares of it concurrently, so the GPU is as full as the total says).
+inline void launch_trace(const KParams& kp, int slots, int batch, cudaStream_t st) {
   const int tiles = kp.tiles_x * kp.tiles_y;
-  if (slots >= 8) {
+  if (batch >= 8) {
     launch_pdl(trace_bundle_kernel<4, 2, 24, true, false>, dim3((tiles + 1) / 2, slots), dim3(64), 0, st, kp);
   } else {
     launch_pdl(trace_bundle_kernel<8, 1, 1, false, true>, dim3(tiles, slots), dim3(32), 0, st, kp);

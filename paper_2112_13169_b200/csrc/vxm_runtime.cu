@@ -391,7 +391,7 @@ void launch_stages(vxm_ctx* c, bool cloud, bool capturing, int s0, int S, cudaSt
       dim3 grid(static_cast<unsigned>(std::min<long long>((n + 255) / 256, c->nsm * 8)), S);
       VXM_CK(vxm::launch_pdl(vxm::trace_per_pixel_kernel, grid, dim3(256), 0, st, kp, cloud ? 0 : 1));
     } else {
-      vxm::launch_trace(kp, S, st);
+      vxm::launch_trace(kp, S, c->nslots, st);
     }
     VXM_CK(cudaGetLastError());
   }

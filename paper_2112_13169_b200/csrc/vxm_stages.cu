@@ -227,7 +227,7 @@ int vxm_trace_bundle(const vxm_grid_spec* grid, uint8_t* ms, const int32_t bundl
     kp.key = d_key.p;
     kp.counters = d_cnt.p;
     kp.frames = d_frame.p;
-    vxm::launch_trace(kp, 1, 0);
+    vxm::launch_trace(kp, 1, 1, 0);
     VXM_SCK(cudaGetLastError());
     vxm::fold_trace_slots_kernel<<<1, 32>>>(d_cnt.p);
     vxm::decode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_occ.p, d_key.p, d_ms.p, N, kEpoch);
