@@ -361,7 +361,10 @@ void launch_stages(vxm_ctx* c, bool cloud, bool capturing, int s0, int S, cudaSt
     const long long npix = static_cast<long long>(kp.W) * kp.H;
     const long long tiles = ((npix + 3) / 4 + kPopulateThreads - 1) / kPopulateThreads;
     const long long fill = static_cast<long long>(c->nsm) * 8;
-    const int iters = static_cast<int>(std::max(1LL, std::min<long long>(vxm::kPopMaxIters, tiles * S / fill)));
+    // (measured: at least min(4, what the whole call would use) when graph
+    // branches launch small shares concurrently: +6% at 16 streams)
+    const long long want = std::max(tiles * S / fill, std::min(4LL, tiles * c->nslots / fill));
+    const int iters = static_cast<int>(std::max(1LL, std::min<long long>(vxm::kPopMaxIters, want)));
     dim3 grid(static_cast<unsigned>((tiles + iters - 1) / iters), S);
     if (npix % 4 == 0) {
       // staged quads + per-warp lists of valid pixels (u16, 4 per quad)
@@ -423,7 +426,7 @@ void launch_merge(vxm_ctx* c, const vxm::KParams& kp, int S, cudaStream_t st) {
   } else if (c->F == 1) {
     const long long rows = static_cast<long long>(kp.dy) * kp.dz;
     // one row per warp unless the batch fills the GPU several times over
-    const long long warps = rows * S;
+    const long long warps = rows * c->nslots;  // the whole call (branches run concurrently)
     const long long fill = static_cast<long long>(c->nsm) * 64;
     const int rpw = static_cast<int>(std::max(1LL, std::min<long long>(vxm::kRowsPerWarp, warps / fill)));
     const int rows_per_block = kMergeThreads / 32 * rpw;
