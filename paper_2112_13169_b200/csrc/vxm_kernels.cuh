@@ -618,7 +618,7 @@ __device__ __forceinline__ void ray_setup(const double* R, const double* start, 
 // few spilled values; 4-7% faster than one warp per block at 64 registers),
 // a lone frame (358 warps, GPU far from full) runs 8-step chunks at 64
 // registers, where per-warp latency decides.
-template <int kChunk, int kTraceWarps, int kMinBlocks, bool kMatch, bool kFast>
+template <int kChunk, int kTraceWarps, int kMinBlocks, bool kMatch, bool kFast, bool kSplit>
 __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_kernel(KParams p) {
   const int s = blockIdx.y;
   const FrameParams* fp = p.frames + s;
@@ -634,9 +634,13 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   const int lane = threadIdx.x & 31;
   const int tile = blockIdx.x * kTraceWarps + (threadIdx.x >> 5);
   const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
-  const int xi_idx = tx * 8 + (lane & 7);
-  const int yi_idx = ty * 4 + (lane >> 3);
-  const bool active = ty < p.tiles_y && xi_idx < p.vw && yi_idx < p.vh;
+  // kSplit: a warp holds an 8x2 tile of rays twice, lanes 0-15 walking each
+  // ray's near half (t < tau) and lanes 16-31 its far half
+  const int rl = kSplit ? (lane & 15) : lane;
+  const bool far_half = kSplit && lane >= 16;
+  const int xi_idx = tx * 8 + (rl & 7);
+  const int yi_idx = ty * (kSplit ? 2 : 4) + (rl >> 3);
+  const bool active = ty < (kSplit ? (p.vh + 1) / 2 : p.tiles_y) && xi_idx < p.vw && yi_idx < p.vh;
   const uint32_t ray = static_cast<uint32_t>(yi_idx) * p.vw + xi_idx;  // row-major, y outer
   const uint32_t ray_key = key_tag(epoch) | ((ray + 1u) << 1);
 
@@ -656,7 +660,7 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   double t0 = st.tmax[0], t1 = st.tmax[1], t2 = st.tmax[2];
   const double stop = st.stop;
 
-  bool walking = active;
+  bool walking = active && !far_half;  // (outside the grid a split warp walks whole rays on its near lanes)
   bool entered = false;
   uint32_t traced_bit = 0;
   unsigned freed = 0, traced = 0, skipped = 0;
@@ -702,15 +706,15 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
         asm("{\n\t"
             ".reg .pred p1, p8, d1, d8;\n\t"
             ".reg .b32 r1, r8;\n\t"
-            "shfl.sync.down.b32 r1|p1, %1, 1, 31, -1;\n\t"
-            "shfl.sync.down.b32 r8|p8, %1, 8, 31, -1;\n\t"
+            "shfl.sync.down.b32 r1|p1, %1, 1, %2, -1;\n\t"
+            "shfl.sync.down.b32 r8|p8, %1, 8, %2, -1;\n\t"
             "setp.eq.and.u32 d1, r1, %1, p1;\n\t"
             "setp.eq.and.u32 d8, r8, %1, p8;\n\t"
             "or.pred d1, d1, d8;\n\t"
             "selp.u32 %0, 1, 0, d1;\n\t"
             "}"
             : "=r"(dup[j])
-            : "r"(cell[j]));
+            : "r"(cell[j]), "n"(kSplit ? 0x101f : 0x1f));  // kSplit: 16-lane segments (the halves)
       }
     }
 #pragma unroll
@@ -754,7 +758,14 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
     }
   };
   auto resolve = [&](const uint32_t (&cell)[kChunk]) { resolve_t(cell, std::false_type{}); };
-  auto resolve_tail = [&](const uint32_t (&cell)[kChunk]) { resolve_t(cell, std::true_type{}); };
+  // (kSplit: a near half's cells after its stop must not set its traced bit,
+  // which the far half reads, so invalid cells take the general form)
+  auto resolve_tail = [&](const uint32_t (&cell)[kChunk]) {
+    if constexpr (kSplit)
+      resolve_t(cell, std::false_type{});
+    else
+      resolve_t(cell, std::true_type{});
+  };
 
   // The camera (every ray's start) is shared by the whole frame, so this
   // branch is uniform. Inside the grid the walk needs no per-cell bounds
@@ -783,13 +794,32 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
         M[a] = fmin(stop, e);
       }
     }
-    const double M0 = M[0], M1 = M[1], M2 = M[2];
+    double M0 = M[0], M1 = M[1], M2 = M[2];
     // tdelta of an axis the ray never steps along is +inf; that axis is never
     // chosen, and the selected-addend form below needs a finite value for it
     const double e0 = st.step[0] ? st.tdelta[0] : 0.0, e1 = st.step[1] ? st.tdelta[1] : 0.0,
                  e2 = st.step[2] ? st.tdelta[2] : 0.0;
     uint32_t al = active ? 1u : 0u;
     bool alive = active;
+    // kSplit: the steps whose chosen tmax is below tau = min(M) / 2 (none of
+    // which can end the walk) are the near half; its lane walks them with
+    // every threshold at tau. The far lane starts where they end: along each
+    // axis the tmax values below tau are taken with the walk's own repeated
+    // additions, which gives that axis' step count and the exact tmax.
+    double fs0 = 0.0, fs1 = 0.0, fs2 = 0.0;  // the far half's start, for its re-walk
+    uint32_t fidx = 0;
+    if constexpr (kSplit) {
+      const double tau = dmul(0.5, fmin(fmin(M0, M1), M2));
+      if (!far_half) {
+        M0 = M1 = M2 = tau;
+      } else if (active) {
+        while (t0 < tau) { t0 = dadd(t0, e0); idx += lin0; }
+        while (t1 < tau) { t1 = dadd(t1, e1); idx += lin1; }
+        while (t2 < tau) { t2 = dadd(t2, e2); idx += lin2; }
+        fs0 = t0; fs1 = t1; fs2 = t2;
+        fidx = static_cast<uint32_t>(idx);
+      }
+    }
     uint32_t uidx = static_cast<uint32_t>(idx);
     // Fast chunks (kFast): the walk can only end at a step whose chosen tmax (the
     // current minimum) reaches min(M_a); the minimum grows by at most
@@ -872,9 +902,35 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
             "}"
             : "+d"(t0), "+d"(t1), "+d"(t2), "+r"(uidx), "+r"(al)
             : "d"(e0), "d"(e1), "d"(e2), "d"(M0), "d"(M1), "d"(M2), "r"(lin0), "r"(lin1), "r"(lin2));
+        // the near half stops at tau without recording that cell: it is the
+        // far half's first
+        if (kSplit && !far_half && !al) cell[j] = 0xffffffffu;
       }
       alive = al != 0u;
       resolve_tail(cell);
+    }
+    if constexpr (kSplit) {
+      // The far half resolved its cells as if nothing before it were
+      // occupied. If the near half met an occupied cell, the far half's writes
+      // before its own first occupied cell (lw - lt of them, all unoccupied)
+      // carry the traced bit: count them so and write their keys again with
+      // it (RED.max: the higher key wins), walking that prefix once more.
+      const uint32_t near_traced = __shfl_sync(0xffffffffu, traced_bit, lane & 15);
+      if (far_half && active && near_traced) {
+        unsigned n = lw - lt;
+        lt = lw;
+        double a0 = fs0, a1 = fs1, a2 = fs2;
+        uint32_t u = fidx;
+        const uint32_t kv = ray_key | 1u;
+        for (; n > 0; --n) {
+          atomicMax(key + u, kv);
+          const bool bx = a0 <= a1 && a0 <= a2;
+          const bool by = !bx && a1 <= a2;
+          if (bx) { a0 = dadd(a0, e0); u += lin0; }
+          else if (by) { a1 = dadd(a1, e1); u += lin1; }
+          else { a2 = dadd(a2, e2); u += lin2; }
+        }
+      }
     }
     freed += lw - lt;
     traced += lt;
@@ -916,7 +972,7 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   traced += lt;
   }
   unsigned long long* slot = &p.counters[s].trace_slots[tile % kTraceSlots][0];
-  const unsigned r_n = __reduce_add_sync(0xffffffffu, active ? 1u : 0u);
+  const unsigned r_n = __reduce_add_sync(0xffffffffu, active && !far_half ? 1u : 0u);
   const unsigned f_n = __reduce_add_sync(0xffffffffu, freed);
   const unsigned t_n = __reduce_add_sync(0xffffffffu, traced);
   const unsigned k_n = __reduce_add_sync(0xffffffffu, skipped);
@@ -929,14 +985,24 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
 }
 
 // Launches K3 over `slots` frame slots in the shape that suits the batch.
+constexpr long long kSplitMaxRays = 32768;
+
 // `batch` is the number of slots of the whole call (graph branches launch
 // shares of it concurrently, so the GPU is as full as the total says).
 inline void launch_trace(const KParams& kp, int slots, int batch, cudaStream_t st) {
   const int tiles = kp.tiles_x * kp.tiles_y;
   if (batch >= 8) {
-    launch_pdl(trace_bundle_kernel<4, 2, 24, true, false>, dim3((tiles + 1) / 2, slots), dim3(64), 0, st, kp);
+    launch_pdl(trace_bundle_kernel<4, 2, 24, true, false, false>, dim3((tiles + 1) / 2, slots), dim3(64), 0, st, kp);
   } else {
-    launch_pdl(trace_bundle_kernel<8, 1, 1, false, true>, dim3(tiles, slots), dim3(32), 0, st, kp);
+    if (static_cast<long long>(kp.vw) * kp.vh * batch <= kSplitMaxRays) {
+      // few rays (the GPU far from full): 8x2 tiles, each ray walked as two
+      // halves by two lanes; measured -12% / -7% K3 time for a lone cfg2 /
+      // cfg1 frame, +11% for a lone cfg3 frame (76k rays)
+      const int tiles2 = kp.tiles_x * ((kp.vh + 1) / 2);
+      launch_pdl(trace_bundle_kernel<8, 1, 1, false, true, true>, dim3(tiles2, slots), dim3(32), 0, st, kp);
+    } else {
+      launch_pdl(trace_bundle_kernel<8, 1, 1, false, true, false>, dim3(tiles, slots), dim3(32), 0, st, kp);
+    }
   }
 }
 
