@@ -71,8 +71,10 @@ def _wander(rng, n, start):
     return out
 
 
-@pytest.mark.parametrize("S,F", [(1, 3), (2, 7), (3, 16)])
+@pytest.mark.parametrize("S,F", [(1, 3), (2, 7), (3, 16), (1, 33), (1, 64)])
 def test_sequence_equals_single_frame_path_while_wandering(gpu_lib, S, F):
+    """(1, 33) and (1, 64): a single stream with F >= 32 merges its frame
+    ranges as chained per-branch merges (uneven ranges for 33)."""
     cam = vm.CameraModel(85 * DEG, 101 * DEG, 96, 72, 6.5)
     grid = vm.GridSpec.create_centered(5.0, 4.0, 3.0, 0.1, (0.0, 0.0, 0.0))
     cfg = vm.PipelineConfig(grid, cam, vox_inf=2, depth=6.0)
