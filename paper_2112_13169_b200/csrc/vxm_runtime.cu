@@ -490,15 +490,20 @@ void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
       VXM_CK(cudaEventRecord(c->fork[b], c->stream));
       VXM_CK(cudaStreamWaitEvent(c->side[b], c->fork[b], 0));
     }
-    // F == 1: each branch runs all stages for its streams; F > 1: the
-    // branches run K1-K3 for shares of the frame slots and the chain merge
-    // follows for every stream once they joined
-    const int units = c->F == 1 ? c->S : c->nslots;
-    const bool chained = merge_ranges(c) > 1;
+    // At least as many streams as branches: each branch runs all stages for
+    // whole streams (all F frames of each, chain merge included). Fewer
+    // streams (F > 1): the branches run K1-K3 for shares of the frame slots,
+    // then either each merges its frame range as a chain after the previous
+    // range (one stream, merge_ranges) or the chain merge of every stream
+    // follows once they joined.
+    const bool by_stream = c->S >= B;
+    const int units = by_stream ? c->S : c->nslots;
+    const int per_unit = by_stream ? c->F : 1;  // slots per unit
+    const bool chained = !by_stream && merge_ranges(c) > 1;
     for (int b = 0; b < B; ++b) {
-      const int s0 = units * b / B, s1 = units * (b + 1) / B;
+      const int s0 = units * b / B * per_unit, s1 = units * (b + 1) / B * per_unit;
       cudaStream_t bs = b == 0 ? c->stream : c->side[b];
-      launch_stages(c, cloud, capturing, s0, s1 - s0, bs, b == 0 && marks, c->F == 1);
+      launch_stages(c, cloud, capturing, s0, s1 - s0, bs, b == 0 && marks, by_stream);
       if (chained) {
         // this range's chain merge, after the previous range's
         if (b > 0) VXM_CK(cudaStreamWaitEvent(bs, c->chain[b - 1], 0));
@@ -517,7 +522,7 @@ void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
       VXM_CK(cudaEventRecord(c->join[b], c->side[b]));
       VXM_CK(cudaStreamWaitEvent(c->stream, c->join[b], 0));
     }
-    if (c->F > 1 && !chained) {
+    if (!by_stream && !chained) {
       launch_merge(c, c->kp, c->nslots, c->stream);
       launch_publish(c->kp, c->nslots, c->stream);
     }
