@@ -396,10 +396,12 @@ __global__ void __launch_bounds__(256) dilate_rows_vec_kernel(KParams p, int r) 
   }
 }
 
-// Shared memory of K2b: the (8+2r)^2 halo bit rows and the y-dilated rows.
-__host__ __device__ constexpr size_t dilate_smem_bytes(int r, int dx) {
+// Shared memory of K2b: the (8+2r)^2 halo bit rows and the y-dilated rows
+// (fused: also the packed, not yet x-dilated, halo rows).
+__host__ __device__ constexpr size_t dilate_smem_bytes(int r, int dx, bool fused = false) {
   return sizeof(uint32_t) * static_cast<size_t>(dilate_row_words(dx)) *
-             (static_cast<size_t>(kDilT + 2 * r) * (kDilT + 2 * r) + static_cast<size_t>(kDilT) * (kDilT + 2 * r)) +
+             (static_cast<size_t>(kDilT + 2 * r) * (kDilT + 2 * r) * (fused ? 2 : 1) +
+              static_cast<size_t>(kDilT) * (kDilT + 2 * r)) +
          ((static_cast<size_t>(kDilT + 2 * r) * (kDilT + 2 * r) + 3) & ~static_cast<size_t>(3));  // row flags
 }
 
@@ -407,9 +409,11 @@ __host__ __device__ constexpr size_t dilate_smem_bytes(int r, int dx) {
 // an r-row halo into shared memory, ORs along y then z, and writes one
 // Occupied byte per set bit (a warp covers 32 consecutive cells).
 // kR > 0: radius fixed at compile time; kR == 0: radius at run time.
-template <int kR>
+// kFused: no K2a; the block packs and x-dilates its halo rows itself from the
+// centre bytes (dims_x % 4 == 0: 4-byte loads), one launch fewer.
+template <int kR, bool kFused>
 __global__ void __launch_bounds__(256) dilate_tiles_kernel(KParams p, int r_rt) {
-  pdl_wait();  // K2a's bit rows
+  pdl_wait();  // K1's centre bytes (fused) or K2a's bit rows
   extern __shared__ uint32_t bits[];
   const int r = kR > 0 ? kR : r_rt;
   const int s = blockIdx.z;
@@ -438,11 +442,57 @@ __global__ void __launch_bounds__(256) dilate_tiles_kernel(KParams p, int r_rt) 
   }
   // surfaces are sparse in 3-D: a tile with no centre within r writes nothing
   if (!__syncthreads_or(anyf)) return;
-  for (int i = threadIdx.x; i < (H * H) << lg; i += blockDim.x) {
-    const int w = i & (WP - 1), row = i >> lg;
-    const int hz = row / H, hy = row - hz * H;
-    const int y = y0 - r + hy, z = z0 - r + hz;
-    bx[i] = fl[row] ? __ldg(plane + ((z * p.dy + y) << lg) + w) : 0u;
+  if constexpr (kFused) {
+    // pack: word w of a flagged halo row = its 32 centre bytes == epoch
+    uint32_t* raw = reinterpret_cast<uint32_t*>(fl + ((H * H + 3) & ~3)) ;
+    const uint8_t* ctr = p.ctr + static_cast<long long>(s) * p.n;
+    const uint32_t ee = e * 0x01010101u;
+    for (int i = threadIdx.x; i < (H * H) << lg; i += blockDim.x) {
+      const int w = i & (WP - 1), row = i >> lg;
+      uint32_t m = 0;
+      if (fl[row] && w < W) {
+        const int hz = row / H, hy = row - hz * H;
+        const int y = y0 - r + hy, z = z0 - r + hz;
+        const uint32_t* src =
+            reinterpret_cast<const uint32_t*>(ctr + static_cast<uint32_t>(y) * p.dx + static_cast<uint32_t>(z) * dxy) +
+            8 * w;
+        const int nq = min(8, (p.dx - 32 * w) >> 2);  // 4-byte words of this 32-cell word inside the row
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (q < nq) {
+            const uint32_t hit = zero_bytes(__ldg(src + q) ^ ee) & 0x80808080u;  // 0x80 per centre byte
+            m |= ((hit * 0x00204081u) >> 28) << (4 * q);
+          }
+        }
+      }
+      raw[i] = m;
+    }
+    __syncthreads();
+    // x-dilation with the neighbouring words of the row
+    for (int i = threadIdx.x; i < (H * H) << lg; i += blockDim.x) {
+      const int w = i & (WP - 1);
+      const uint32_t m = raw[i];
+      const uint32_t pv = w > 0 ? raw[i - 1] : 0u;
+      const uint32_t nx = w + 1 < W ? raw[i + 1] : 0u;
+      uint32_t d = m;
+      if (m | pv | nx) {
+#pragma unroll
+        for (int q = 1; q <= (kR > 0 ? kR : 16); ++q) {
+          if (kR == 0 && q > r) break;
+          d |= (m << q) | (pv >> (32 - q)) | (m >> q) | (nx << (32 - q));
+        }
+        const int valid = min(32, p.dx - 32 * w);
+        if (valid < 32) d &= valid > 0 ? (1u << valid) - 1u : 0u;
+      }
+      bx[i] = w < W ? d : 0u;
+    }
+  } else {
+    for (int i = threadIdx.x; i < (H * H) << lg; i += blockDim.x) {
+      const int w = i & (WP - 1), row = i >> lg;
+      const int hz = row / H, hy = row - hz * H;
+      const int y = y0 - r + hy, z = z0 - r + hz;
+      bx[i] = fl[row] ? __ldg(plane + ((z * p.dy + y) << lg) + w) : 0u;
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < (H * kDilT) << lg; i += blockDim.x) {
@@ -499,36 +549,61 @@ __global__ void __launch_bounds__(256) dilate_tiles_kernel(KParams p, int r_rt) 
 }
 
 // Launches K2a and the radius-specialised K2b (1..4) or the generic one.
-inline void launch_dilate(const KParams& kp, int r, int streams, size_t smem, cudaStream_t st) {
+// The fused K2 (no K2a) when the centre rows load as 4-byte words and its
+// shared memory fits.
+inline bool dilate_fused(int r, int dx) {
+#ifdef VXM_NO_FUSED_DILATE
+  return false;
+#endif
+  return dx % 4 == 0 && dilate_smem_bytes(r, dx, true) <= 200 * 1024;
+}
+
+template <int kR>
+inline void launch_dilate_tiles(const KParams& kp, int r, bool fused, dim3 grid, cudaStream_t st) {
+  if (fused)
+    launch_pdl(dilate_tiles_kernel<kR, true>, grid, dim3(256), dilate_smem_bytes(r, kp.dx, true), st, kp, r);
+  else
+    launch_pdl(dilate_tiles_kernel<kR, false>, grid, dim3(256), dilate_smem_bytes(r, kp.dx), st, kp, r);
+}
+
+inline void launch_dilate(const KParams& kp, int r, int streams, size_t /*smem*/, cudaStream_t st) {
   const int rows = kp.dy * kp.dz;
-  // a single stream gets one row per warp-step of parallelism anyway; batches
-  // amortise the per-warp setup over kDilRowsPerWarp rows
-  const int G = dilate_rows_group(kp.dx);
-  if (kp.n % 16 == 0 && G * kp.dx <= 512 && G * dilate_row_words(kp.dx) <= 32) {
-    const int per_block = 8 * G;
-    launch_pdl(dilate_rows_vec_kernel, dim3((rows + per_block - 1) / per_block, streams), dim3(256), 0, st, kp, r);
-  } else {
-    const int per_block = 8 * kDilRowsPerWarp;
-    launch_pdl(dilate_rows_kernel, dim3((rows + per_block - 1) / per_block, streams), dim3(256), 0, st, kp, r);
+  const bool fused = dilate_fused(r, kp.dx);
+  if (!fused) {
+    // a single stream gets one row per warp-step of parallelism anyway; batches
+    // amortise the per-warp setup over kDilRowsPerWarp rows
+    const int G = dilate_rows_group(kp.dx);
+    if (kp.n % 16 == 0 && G * kp.dx <= 512 && G * dilate_row_words(kp.dx) <= 32) {
+      const int per_block = 8 * G;
+      launch_pdl(dilate_rows_vec_kernel, dim3((rows + per_block - 1) / per_block, streams), dim3(256), 0, st, kp, r);
+    } else {
+      const int per_block = 8 * kDilRowsPerWarp;
+      launch_pdl(dilate_rows_kernel, dim3((rows + per_block - 1) / per_block, streams), dim3(256), 0, st, kp, r);
+    }
   }
   const dim3 grid((kp.dy + kDilT - 1) / kDilT, (kp.dz + kDilT - 1) / kDilT, streams);
   switch (r) {
-    case 1: launch_pdl(dilate_tiles_kernel<1>, grid, dim3(256), smem, st, kp, r); break;
-    case 2: launch_pdl(dilate_tiles_kernel<2>, grid, dim3(256), smem, st, kp, r); break;
-    case 3: launch_pdl(dilate_tiles_kernel<3>, grid, dim3(256), smem, st, kp, r); break;
-    case 4: launch_pdl(dilate_tiles_kernel<4>, grid, dim3(256), smem, st, kp, r); break;
-    default: launch_pdl(dilate_tiles_kernel<0>, grid, dim3(256), smem, st, kp, r); break;
+    case 1: launch_dilate_tiles<1>(kp, r, fused, grid, st); break;
+    case 2: launch_dilate_tiles<2>(kp, r, fused, grid, st); break;
+    case 3: launch_dilate_tiles<3>(kp, r, fused, grid, st); break;
+    case 4: launch_dilate_tiles<4>(kp, r, fused, grid, st); break;
+    default: launch_dilate_tiles<0>(kp, r, fused, grid, st); break;
   }
 }
 
 // Opt-in to large dynamic shared memory for every K2b instance.
 inline cudaError_t dilate_set_smem(int bytes) {
   cudaError_t e = cudaSuccess;
-  const void* fns[5] = {reinterpret_cast<const void*>(dilate_tiles_kernel<0>),
-                        reinterpret_cast<const void*>(dilate_tiles_kernel<1>),
-                        reinterpret_cast<const void*>(dilate_tiles_kernel<2>),
-                        reinterpret_cast<const void*>(dilate_tiles_kernel<3>),
-                        reinterpret_cast<const void*>(dilate_tiles_kernel<4>)};
+  const void* fns[10] = {reinterpret_cast<const void*>(dilate_tiles_kernel<0, false>),
+                         reinterpret_cast<const void*>(dilate_tiles_kernel<1, false>),
+                         reinterpret_cast<const void*>(dilate_tiles_kernel<2, false>),
+                         reinterpret_cast<const void*>(dilate_tiles_kernel<3, false>),
+                         reinterpret_cast<const void*>(dilate_tiles_kernel<4, false>),
+                         reinterpret_cast<const void*>(dilate_tiles_kernel<0, true>),
+                         reinterpret_cast<const void*>(dilate_tiles_kernel<1, true>),
+                         reinterpret_cast<const void*>(dilate_tiles_kernel<2, true>),
+                         reinterpret_cast<const void*>(dilate_tiles_kernel<3, true>),
+                         reinterpret_cast<const void*>(dilate_tiles_kernel<4, true>)};
   for (const void* f : fns) {
     const cudaError_t x = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (x != cudaSuccess) e = x;

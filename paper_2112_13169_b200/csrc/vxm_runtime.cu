@@ -1009,7 +1009,8 @@ int vxm_create_multi(const vxm_config* cfg, int32_t n_streams, int32_t frames_pe
       const size_t words = static_cast<size_t>(vxm::dilate_row_words(kp.dx)) * kp.dy * kp.dz * S;
       VXM_CK(cudaMalloc(&c->dbits, sizeof(uint32_t) * words));
       kp.dbits = c->dbits;
-      VXM_CK(vxm::dilate_set_smem(static_cast<int>(smem)));
+      VXM_CK(vxm::dilate_set_smem(static_cast<int>(
+          vxm::dilate_smem_bytes(cfg->vox_inf, kp.dx, vxm::dilate_fused(cfg->vox_inf, kp.dx)))));
     }
     VXM_CK(cudaStreamSynchronize(c->stream));
   });

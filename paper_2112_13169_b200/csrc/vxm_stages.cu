@@ -154,7 +154,7 @@ int vxm_populate_occupied(const vxm_grid_spec* grid, uint8_t* ms, const double* 
       const size_t smem = vxm::dilate_smem_bytes(r, kp.dx);
       if (r > vxm::kMaxVoxInf || smem > 200 * 1024 || kp.dx > 1024)
         throw StageError{VXM_EINVAL, "vox_inf / dims_x exceed the dilation limits (16 / 1024)"};
-      VXM_SCK(vxm::dilate_set_smem(static_cast<int>(smem)));
+      VXM_SCK(vxm::dilate_set_smem(static_cast<int>(vxm::dilate_smem_bytes(r, kp.dx, vxm::dilate_fused(r, kp.dx)))));
       kp.dbits = d_bits.p;
       vxm::launch_dilate(kp, r, 1, smem, 0);
       VXM_SCK(cudaGetLastError());
