@@ -280,6 +280,7 @@ def our_arm(args, world, rank, local):
     # branches overlap the stages of different stream shares
     pipe = new_pipeline(S)
     branches = pipe.graph_branches
+    pipe_dims = tuple(vm.GridSpec.create_centered(*c["grid"], c["vox"], poses[0][1]).dims)
     stream = torch.cuda.ExternalStream(pipe.cuda_stream, device=dev)
     for k in range(WU):
         pipe.integrate_depth_device(slots[k % POOL].data_ptr(), step_poses(k))
@@ -299,8 +300,10 @@ def our_arm(args, world, rank, local):
     ms = start.elapsed_time(end)
     ms = multi.max_over_ranks(ms, dev)
     value = multi.job_throughput(S * K, world, ms / 1000.0)
-    # K1 populate, (K2a rows + K2b tiles when vox_inf > 0), K3 trace, K4 merge, K5 publish, per branch
-    kernels_per_step = (6 if c["vox_inf"] > 0 else 4) * branches
+    # K1 populate, K2 dilation when vox_inf > 0 (one fused tile kernel when dims_x % 4 == 0, else K2a rows +
+    # K2b tiles), K3 trace, K4 merge, K5 publish, per branch
+    k2 = 0 if c["vox_inf"] == 0 else (1 if pipe_dims[0] % 4 == 0 else 2)
+    kernels_per_step = (4 + k2) * branches
 
     # ---- per-kernel device times (the roofline's K3 duration): the same
     # steps as ONE graph branch, stage-boundary events recorded inside the
