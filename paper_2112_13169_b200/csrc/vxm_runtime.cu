@@ -261,6 +261,7 @@ struct vxm_ctx {
   static constexpr int kPP = 2;
   vxm::FrameParams* frames_pp[kPP] = {nullptr, nullptr};
   int pp = 0;  // buffer of the current call
+  bool sync_call = false;  // the current call waits for its stats (vxm_integrate_depth / _cloud)
   cudaStream_t param_stream = nullptr;
   cudaEvent_t pp_ready[kPP] = {}, pp_free[kPP] = {};
   float* depth_dev = nullptr;
@@ -647,12 +648,20 @@ void prepare_frames(vxm_ctx* c, const vxm_pose* poses, const float* depth_dev_ba
   // so the copy runs while the previous graph is still executing
   c->pp ^= 1;
   const int pp = c->pp;
-  VXM_CK(cudaStreamWaitEvent(c->param_stream, c->pp_free[pp], 0));
-  VXM_CK(cudaMemcpyAsync(c->frames_pp[pp], c->frames_host, sizeof(vxm::FrameParams) * c->nslots,
-                         cudaMemcpyHostToDevice, c->param_stream));
-  VXM_CK(cudaEventRecord(c->ring_ev[c->ring_slot], c->param_stream));
-  VXM_CK(cudaEventRecord(c->pp_ready[pp], c->param_stream));
-  VXM_CK(cudaStreamWaitEvent(c->stream, c->pp_ready[pp], 0));
+  if (c->sync_call) {
+    // a synchronous call (the stream is idle): the copy goes on the stream
+    // itself, without the cross-stream events
+    VXM_CK(cudaMemcpyAsync(c->frames_pp[pp], c->frames_host, sizeof(vxm::FrameParams) * c->nslots,
+                           cudaMemcpyHostToDevice, c->stream));
+    VXM_CK(cudaEventRecord(c->ring_ev[c->ring_slot], c->stream));
+  } else {
+    VXM_CK(cudaStreamWaitEvent(c->param_stream, c->pp_free[pp], 0));
+    VXM_CK(cudaMemcpyAsync(c->frames_pp[pp], c->frames_host, sizeof(vxm::FrameParams) * c->nslots,
+                           cudaMemcpyHostToDevice, c->param_stream));
+    VXM_CK(cudaEventRecord(c->ring_ev[c->ring_slot], c->param_stream));
+    VXM_CK(cudaEventRecord(c->pp_ready[pp], c->param_stream));
+    VXM_CK(cudaStreamWaitEvent(c->stream, c->pp_ready[pp], 0));
+  }
   c->kp.frames = c->frames_pp[pp];
 }
 
@@ -1048,11 +1057,18 @@ int vxm_integrate_depth(vxm_ctx* ctx, const float* depth, const vxm_pose* t_wc, 
     VXM_CK(cudaSetDevice(ctx->device));
     const size_t frame = static_cast<size_t>(ctx->kp.W) * ctx->kp.H;
     next_slot(ctx);
-    prepare_frames(ctx, t_wc, ctx->depth_dev, frame);
     // pinned host buffers go straight to the copy engine; pageable ones are
     // staged by the driver
     VXM_CK(cudaMemcpyAsync(ctx->depth_dev, depth, sizeof(float) * frame * ctx->nslots,
                            cudaMemcpyHostToDevice, ctx->stream));
+    ctx->sync_call = true;
+    try {
+      prepare_frames(ctx, t_wc, ctx->depth_dev, frame);
+    } catch (...) {
+      ctx->sync_call = false;
+      throw;
+    }
+    ctx->sync_call = false;
     run_frame(ctx, false);
     collect_stats(ctx, stats);
   });
