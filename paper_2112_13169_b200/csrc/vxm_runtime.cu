@@ -267,7 +267,10 @@ struct vxm_ctx {
   float* depth_dev = nullptr;
   // double-buffered staging for vxm_integrate_depth_async (created lazily)
   cudaStream_t copy_stream = nullptr;
-  static constexpr int kBranches = 3;
+#ifndef VXM_BRANCHES
+#define VXM_BRANCHES 3
+#endif
+  static constexpr int kBranches = VXM_BRANCHES;
   cudaStream_t side[kBranches] = {};  // streams of graph branches 1..
   cudaEvent_t fork[kBranches] = {}, join[kBranches] = {};
   cudaEvent_t chain[kBranches] = {};  // a chained range's merge is done (merge_ranges)
