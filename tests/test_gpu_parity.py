@@ -524,3 +524,55 @@ def test_per_pixel_tracer_branched_batch(gpu_lib):
             assert st[s]["voxels_freed"] == sr["voxels_freed"] and st[s]["freed_count"] == sr["freed_count"]
     for o, s in zip(orc, (0, 11)):
         assert np.array_equal(batch.local_grid(s)[0], o.local_grid()[0])
+
+
+def test_stage_times_from_kernel_stamps(gpu_lib):
+    """vxm_stats::*_us come from the kernels' %globaltimer stamps (no event
+    nodes in the frame graph): positive for every stage, shift_us 0, and the
+    graph-timed frame brackets their sum."""
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 160, 120, 5.0)
+    grid = vm.GridSpec.create_centered(6.0, 6.0, 3.0, 0.1, (0.0, 0.0, 0.0))
+    pipe = vm.MappingPipeline(vm.PipelineConfig(grid, cam, vox_inf=2, depth=5.0))
+    pose = vm.look_along_x((0.0, 0.0, 0.0))
+    depth = scenes.render(cam, pose, scenes.box_field_boxes(1))
+    for _ in range(3):
+        st = pipe.integrate_depth(depth, pose)
+    assert st["populate_us"] > 0.0 and st["trace_us"] > 0.0 and st["merge_us"] > 0.0
+    assert st["shift_us"] == 0.0
+    assert st["populate_us"] + st["trace_us"] + st["merge_us"] <= pipe.last_frame_ms() * 1000.0 + 1.0
+
+
+def test_stage_events_attached_to_graph(gpu_lib):
+    """Caller events recorded at the stage boundaries inside the frame graph
+    (VXM_FLAG_STAGE_EVENTS; the bench's kernel-timing pass) time the stages
+    in order, and the results equal a pipeline without them."""
+    import torch
+
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 160, 120, 5.0)
+    grid = vm.GridSpec.create_centered(6.0, 6.0, 3.0, 0.1, (0.0, 0.0, 0.0))
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=2, depth=5.0)
+    S = 12
+    poses = [vm.look_along_x((0.0, 0.05 * s, 0.0)) for s in range(S)]
+    depth = vm.render_depth(cam, poses, scenes.box_field_boxes(2))
+    dev = torch.from_numpy(depth).cuda()
+    timed = vm.MappingPipeline(cfg, n_streams=S, flags=vm.N.FLAG_STAGE_EVENTS | vm.N.FLAG_SINGLE_BRANCH)
+    plain = vm.MappingPipeline(cfg, n_streams=S)
+    stream = torch.cuda.ExternalStream(timed.cuda_stream)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    for e in evs:
+        e.record(stream)
+    timed.set_stage_events([e.cuda_event for e in evs])
+    pa = vm.pose_array(poses)
+    for _ in range(2):
+        timed.integrate_depth_device(dev.data_ptr(), pa)
+        st_t = timed.wait_stats()
+        plain.integrate_depth_device(dev.data_ptr(), pa)
+        st_p = plain.wait_stats()
+    torch.cuda.synchronize()
+    spans = [evs[i].elapsed_time(evs[i + 1]) for i in range(3)]
+    assert all(t > 0.0 for t in spans), spans
+    timed.set_stage_events(None)
+    for s in range(S):
+        for key in ("occupied_count", "freed_count", "voxels_freed", "rays_traced"):
+            assert st_t[s][key] == st_p[s][key]
+        assert np.array_equal(timed.local_grid(s)[0], plain.local_grid(s)[0])
