@@ -18,6 +18,7 @@ VXM_OK, VXM_EINVAL, VXM_ECUDA, VXM_ENOMEM, VXM_ENODEV, VXM_ESTATE, VXM_EIO = ran
 UNKNOWN, FREE, OCCUPIED, UNKNOWN_TRACED = 0, 1, 2, 3
 TRACER_BUNDLED, TRACER_PER_PIXEL = 0, 1
 FLAG_STAGE_TIMING, FLAG_NO_GRAPH, FLAG_SINGLE_BRANCH, FLAG_NO_TMA_MERGE, FLAG_STAGE_EVENTS = 1, 2, 4, 8, 16
+FLAG_NO_DESYNC = 32
 
 
 class GridSpecC(C.Structure):

@@ -576,3 +576,46 @@ def test_stage_events_attached_to_graph(gpu_lib):
         for key in ("occupied_count", "freed_count", "voxels_freed", "rays_traced"):
             assert st_t[s][key] == st_p[s][key]
         assert np.array_equal(timed.local_grid(s)[0], plain.local_grid(s)[0])
+
+
+@pytest.mark.parametrize("path", ["device", "async", "host"])
+def test_desynchronised_batch_across_epoch_wrap(gpu_lib, path):
+    """A batch of 12 streams runs as three per-branch graphs on their own
+    streams (each waiting only for its call's inputs); 300 back-to-back calls
+    cross the 8-bit epoch wrap, whose array clears go on the owning branch's
+    stream. Every stream ends equal to an independent single-stream pipeline
+    (and to the per-call joined-branch form, VXM_FLAG_NO_DESYNC)."""
+    import torch
+
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 48, 36, 6.5)
+    grid = vm.GridSpec.create_centered(4.0, 4.0, 2.0, 0.1, (0.0, 0.0, 0.0))
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=1, depth=6.0)
+    S, calls = 12, 300
+    boxes = scenes.box_field_boxes(4)
+    poses = [[vm.look_along_x((0.03 * (k % 40), 0.02 * s + 0.01 * (k % 17), 0.0)) for s in range(S)]
+             for k in range(12)]
+    frames = [vm.render_depth(cam, poses[k], boxes) for k in range(12)]
+    pa = [vm.pose_array(poses[k]) for k in range(12)]
+    batch = vm.MappingPipeline(cfg, n_streams=S)
+    joined = vm.MappingPipeline(cfg, n_streams=S, flags=vm.N.FLAG_NO_DESYNC)
+    singles = [vm.MappingPipeline(cfg) for _ in (0, S - 1)]
+    dev = [torch.from_numpy(f).cuda() for f in frames]
+    pinned = [torch.from_numpy(f).pin_memory() for f in frames]
+    for k in range(calls):
+        q = k % 12
+        if path == "device":
+            batch.integrate_depth_device(dev[q].data_ptr(), pa[q])
+        elif path == "async":
+            batch.integrate_depth_async(pinned[q].data_ptr(), pa[q])
+        else:
+            batch.integrate_depth_ptr(pinned[q].data_ptr(), pa[q])
+        joined.integrate_depth_device(dev[q].data_ptr(), pa[q])
+        for i, s in enumerate((0, S - 1)):
+            singles[i].integrate_depth(frames[q][s], poses[q][s])
+    st = batch.wait_stats()
+    sj = joined.wait_stats()
+    for s in range(S):
+        assert st[s]["freed_count"] == sj[s]["freed_count"]
+        assert np.array_equal(batch.local_grid(s)[0], joined.local_grid(s)[0]), s
+    for i, s in enumerate((0, S - 1)):
+        assert np.array_equal(batch.local_grid(s)[0], singles[i].local_grid()[0]), s

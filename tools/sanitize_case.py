@@ -38,6 +38,11 @@ for ext, vox, mot in (((6.4, 3.2, 1.6), 0.1, (0.0, 1.0, -0.7)), ((6.4, 3.2, 1.6)
         pose = vm.look_along_x(tuple(c * 1.37 * vox * k for c in mot))
         m.integrate_depth(vm.render_depth(cam, [pose], boxes)[0], pose)
     movers.append(m)
+# desynchronised batch graphs (per-branch streams), back to back
+dbatch = vm.MappingPipeline(cfg, n_streams=S)
+for k in range(4):
+    dbatch.integrate_depth(depth, poses)
+movers.append(dbatch)
 print("sanitize case done", sb[0]["freed_count"])
 for p in [batch, one, seq] + movers:
     p.close()
