@@ -279,6 +279,8 @@ struct vxm_ctx {
   cudaStream_t dside[kBranches] = {};
   cudaEvent_t ddone[kBranches] = {};
   cudaEvent_t input_ready = nullptr;  // set by a call whose inputs arrive on another stream
+  cudaEvent_t tail_ev = nullptr;      // end of the last call that ran on the context stream itself
+  bool tail_pending = false;          // ... which desynchronised branches must still wait for
   std::vector<int> wrapped;           // slots whose arrays are cleared before this call (epoch wrap)
   float* stage[2] = {nullptr, nullptr};
   cudaEvent_t ev_copied[2] = {};
@@ -714,6 +716,7 @@ void run_frame(vxm_ctx* c, bool cloud, bool direct = false) {
   const bool timed = (c->flags & VXM_FLAG_STAGE_TIMING) != 0;
   const int B = graph_branches(c);
   const bool graphs = !(timed || direct || (c->flags & VXM_FLAG_NO_GRAPH));
+  bool desync_call = false;
   if (graphs && !cloud && c->F == 1 && B > 1 && !stage_events_wanted(c) && !(c->flags & VXM_FLAG_NO_DESYNC)) {
     // Desynchronised batch: branch b's graph (its streams' stages) runs on
     // its own stream and waits only for this call's FrameParams and inputs,
@@ -723,6 +726,7 @@ void run_frame(vxm_ctx* c, bool cloud, bool direct = false) {
     // 64 streams 0.238 -> 0.220 ms per call back to back).
     const int gi = c->pop_compact ? 2 : 0;
     const int pp = c->pp;
+    desync_call = true;
     VXM_CK(cudaEventRecord(c->ev[0], c->stream));
     for (int b = 0; b < B; ++b) {
       if (!c->dside[b]) {
@@ -731,12 +735,53 @@ void run_frame(vxm_ctx* c, bool cloud, bool direct = false) {
       }
       const int s0 = c->S * b / B, s1 = c->S * (b + 1) / B;
       cudaStream_t bs = c->dside[b];
+      if (c->tail_pending) VXM_CK(cudaStreamWaitEvent(bs, c->tail_ev, 0));
       VXM_CK(cudaStreamWaitEvent(bs, c->pp_ready[pp], 0));
       if (c->input_ready) VXM_CK(cudaStreamWaitEvent(bs, c->input_ready, 0));
       clear_wrapped(c, s0, s1 - s0, bs);
       cudaGraphExec_t& g = c->bgraph[gi][pp][b];
       if (!g) g = capture_branch(c, s0, s1 - s0, bs);
       VXM_CK(cudaGraphLaunch(g, bs));
+      VXM_CK(cudaEventRecord(c->ddone[b], bs));
+      VXM_CK(cudaStreamWaitEvent(c->stream, c->ddone[b], 0));
+    }
+    c->last_marks = false;
+  } else if (graphs && !cloud && merge_ranges(c) > 1 && !stage_events_wanted(c) &&
+             !(c->flags & VXM_FLAG_NO_DESYNC)) {
+    // One stream, F >= 32 frames per call, desynchronised the same way: branch
+    // b populates and traces its frame range on its own stream as soon as
+    // this call's inputs are there, then merges the range as a chain after
+    // the previous range's merge (range 0 after the previous call's last
+    // range), so the next call's populate and trace overlap this call's chain
+    // merges. Direct launches (ten per call).
+    const int pp = c->pp;
+    desync_call = true;
+    VXM_CK(cudaEventRecord(c->ev[0], c->stream));
+    for (int b = 0; b < B; ++b) {
+      if (!c->dside[b]) {
+        VXM_CK(cudaStreamCreateWithFlags(&c->dside[b], cudaStreamNonBlocking));
+        VXM_CK(cudaEventCreateWithFlags(&c->ddone[b], cudaEventDisableTiming));
+      }
+      if (!c->chain[b]) VXM_CK(cudaEventCreateWithFlags(&c->chain[b], cudaEventDisableTiming));
+    }
+    for (int b = 0; b < B; ++b) {
+      const int s0 = c->nslots * b / B, s1 = c->nslots * (b + 1) / B;
+      cudaStream_t bs = c->dside[b];
+      if (c->tail_pending) VXM_CK(cudaStreamWaitEvent(bs, c->tail_ev, 0));
+      VXM_CK(cudaStreamWaitEvent(bs, c->pp_ready[pp], 0));
+      if (c->input_ready) VXM_CK(cudaStreamWaitEvent(bs, c->input_ready, 0));
+      clear_wrapped(c, s0, s1 - s0, bs);
+      launch_stages(c, false, false, s0, s1 - s0, bs, false, false);
+      VXM_CK(cudaStreamWaitEvent(bs, c->chain[b == 0 ? B - 1 : b - 1], 0));
+      vxm::KParams kp = c->kp;
+      kp.frames += s0;
+      kp.counters += s0;
+      kp.counters_out += s0;
+      kp.occ += c->n * s0;
+      kp.key += c->n * s0;
+      launch_merge_chain(c, kp, s1 - s0, 1, bs);
+      launch_publish(kp, s1 - s0, bs);
+      VXM_CK(cudaEventRecord(c->chain[b], bs));
       VXM_CK(cudaEventRecord(c->ddone[b], bs));
       VXM_CK(cudaStreamWaitEvent(c->stream, c->ddone[b], 0));
     }
@@ -773,6 +818,14 @@ void run_frame(vxm_ctx* c, bool cloud, bool direct = false) {
   }
   VXM_CK(cudaEventRecord(c->ev[5], c->stream));
   VXM_CK(cudaEventRecord(c->pp_free[c->pp], c->stream));  // its FrameParams may be overwritten
+  if (desync_call) {
+    c->tail_pending = false;
+  } else {
+    // a later desynchronised call's branches start only after this call
+    if (!c->tail_ev) VXM_CK(cudaEventCreateWithFlags(&c->tail_ev, cudaEventDisableTiming));
+    VXM_CK(cudaEventRecord(c->tail_ev, c->stream));
+    c->tail_pending = true;
+  }
   const uint32_t flips = static_cast<uint32_t>(merge_ranges(c) & 1);  // K4 wrote the other buffer
   for (int s = 0; s < c->S; ++s) c->cur[s] ^= flips;
   c->pending = true;
@@ -846,6 +899,7 @@ void destroy_ctx(vxm_ctx* c) {
     for (auto& g : gg)
       if (g) cudaGraphDestroy(g);
   if (c->param_stream) cudaStreamSynchronize(c->param_stream);
+  if (c->tail_ev) cudaEventDestroy(c->tail_ev);
   for (int b = 0; b < vxm_ctx::kPP; ++b) {
     if (c->pp_ready[b]) cudaEventDestroy(c->pp_ready[b]);
     if (c->pp_free[b]) cudaEventDestroy(c->pp_free[b]);

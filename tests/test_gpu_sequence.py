@@ -164,3 +164,37 @@ def test_sequence_partial_calls_host_frames(gpu_lib):
         i += n
     with pytest.raises(ValueError, match="n_frames"):
         seq.integrate_depth_frames(np.zeros((9, 60, 80), np.float32), traj[:9])
+
+
+def test_chained_desync_calls_mixed_with_partial_calls(gpu_lib):
+    """F = 40 on one stream: full calls run desynchronised branch streams with
+    chained range merges (the next call's populate/trace may start before
+    this call's merges end); partial calls in between run on the context
+    stream. Every frame's stats and the grid equal the single-frame path."""
+    import torch
+
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 64, 48, 6.5)
+    grid = vm.GridSpec.create_centered(5.0, 4.0, 3.0, 0.1, (0.0, 0.0, 0.0))
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=2, depth=6.0)
+    F = 40
+    seq = vm.MappingPipeline(cfg, frames_per_call=F)
+    one = vm.MappingPipeline(cfg)
+    rng = np.random.default_rng(40)
+    plan = [F, F, 7, F, 1, F, F]
+    traj = _wander(rng, sum(plan), (0.0, 0.0, 0.0))
+    boxes = scenes.box_field_boxes(5)
+    i = 0
+    for n in plan:
+        poses = traj[i:i + n]
+        depth = np.stack([scenes.render(cam, p, boxes) for p in poses])
+        if n == F:
+            # device frames, asynchronous: queue it, check after the next call
+            dev = torch.from_numpy(depth).cuda()
+            seq.integrate_depth_device(dev.data_ptr(), vm.pose_array(poses))
+            stats = seq.wait_stats()
+        else:
+            stats = seq.integrate_depth_frames(depth, poses)
+        for j in range(n):
+            _check(stats[j], one.integrate_depth(depth[j], poses[j]), (i, n, j))
+        assert np.array_equal(seq.local_grid()[0], one.local_grid()[0]), i
+        i += n
