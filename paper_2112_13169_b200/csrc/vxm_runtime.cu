@@ -717,7 +717,8 @@ void run_frame(vxm_ctx* c, bool cloud, bool direct = false) {
   const int B = graph_branches(c);
   const bool graphs = !(timed || direct || (c->flags & VXM_FLAG_NO_GRAPH));
   bool desync_call = false;
-  if (graphs && !cloud && c->F == 1 && B > 1 && !stage_events_wanted(c) && !(c->flags & VXM_FLAG_NO_DESYNC)) {
+  if (graphs && !cloud && (c->F == 1 || c->S >= B) && B > 1 && !stage_events_wanted(c) &&
+      !(c->flags & VXM_FLAG_NO_DESYNC)) {
     // Desynchronised batch: branch b's graph (its streams' stages) runs on
     // its own stream and waits only for this call's FrameParams and inputs,
     // not for the other branches of the previous call, so the branches drift
@@ -733,7 +734,7 @@ void run_frame(vxm_ctx* c, bool cloud, bool direct = false) {
         VXM_CK(cudaStreamCreateWithFlags(&c->dside[b], cudaStreamNonBlocking));
         VXM_CK(cudaEventCreateWithFlags(&c->ddone[b], cudaEventDisableTiming));
       }
-      const int s0 = c->S * b / B, s1 = c->S * (b + 1) / B;
+      const int s0 = c->S * b / B * c->F, s1 = c->S * (b + 1) / B * c->F;  // whole streams
       cudaStream_t bs = c->dside[b];
       if (c->tail_pending) VXM_CK(cudaStreamWaitEvent(bs, c->tail_ev, 0));
       VXM_CK(cudaStreamWaitEvent(bs, c->pp_ready[pp], 0));
