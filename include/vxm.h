@@ -179,9 +179,15 @@ int vxm_integrate_depth(vxm_ctx* ctx, const float* depth, const vxm_pose* t_wc,
 int vxm_integrate_depth_frames(vxm_ctx* ctx, const float* depth, const vxm_pose* t_wc,
                                int32_t n_frames, vxm_stats* stats);
 /* Same, with the depth frames already in device memory (n_streams*W*H
- * floats). Asynchronous on the context's stream: returns after enqueueing;
- * read the stats with vxm_wait_stats(). */
+ * floats). Asynchronous: returns after enqueueing; read the stats with
+ * vxm_wait_stats(). Batches run on internal streams that the context stream
+ * joins, so work the caller enqueues on vxm_cuda_stream() afterwards is
+ * ordered after the call; the frames themselves must be complete when the
+ * call is made, or signalled by an event passed to vxm_set_input_event. */
 int vxm_integrate_depth_device(vxm_ctx* ctx, const float* depth_dev, const vxm_pose* t_wc);
+/* The next integrate call's kernels wait for this cudaEvent_t (recorded by
+ * the caller after producing the device frames on any stream). One call. */
+int vxm_set_input_event(vxm_ctx* ctx, void* cuda_event);
 int vxm_wait_stats(vxm_ctx* ctx, vxm_stats* stats);
 
 /* Host frames (pinned for full overlap), asynchronous: the H2D copy runs on a

@@ -93,6 +93,7 @@ SIGNATURES = {
     "vxm_upload_local": (C.c_int, [C.c_void_p, C.c_int32, _u8p, _f64p]),
     "vxm_cuda_stream": (C.c_void_p, [C.c_void_p]),
     "vxm_last_frame_ms": (C.c_int, [C.c_void_p, P(C.c_float)]),
+    "vxm_set_input_event": (C.c_int, [C.c_void_p, C.c_void_p]),
     "vxm_set_stage_events": (C.c_int, [C.c_void_p, P(C.c_void_p)]),
     "vxm_populate_occupied": (C.c_int, [P(GridSpecC), _u8p, _f64p, _f64p, _f64p, C.c_size_t, P(PoseC), C.c_int32, P(PopulateStatsC)]),
     "vxm_trace_bundle": (C.c_int, [P(GridSpecC), _u8p, _i32p, P(PoseC), C.c_double, P(TraceStatsC)]),

@@ -279,6 +279,7 @@ struct vxm_ctx {
   cudaStream_t dside[kBranches] = {};
   cudaEvent_t ddone[kBranches] = {};
   cudaEvent_t input_ready = nullptr;  // set by a call whose inputs arrive on another stream
+  cudaEvent_t user_input = nullptr;   // vxm_set_input_event: the next call's kernels wait for it
   cudaEvent_t tail_ev = nullptr;      // end of the last call that ran on the context stream itself
   bool tail_pending = false;          // ... which desynchronised branches must still wait for
   std::vector<int> wrapped;           // slots whose arrays are cleared before this call (epoch wrap)
@@ -717,6 +718,8 @@ void run_frame(vxm_ctx* c, bool cloud, bool direct = false) {
   const int B = graph_branches(c);
   const bool graphs = !(timed || direct || (c->flags & VXM_FLAG_NO_GRAPH));
   bool desync_call = false;
+  cudaEvent_t user_input = c->user_input;  // (one call)
+  c->user_input = nullptr;
   if (graphs && !cloud && (c->F == 1 || c->S >= B) && B > 1 && !stage_events_wanted(c) &&
       !(c->flags & VXM_FLAG_NO_DESYNC)) {
     // Desynchronised batch: branch b's graph (its streams' stages) runs on
@@ -739,6 +742,7 @@ void run_frame(vxm_ctx* c, bool cloud, bool direct = false) {
       if (c->tail_pending) VXM_CK(cudaStreamWaitEvent(bs, c->tail_ev, 0));
       VXM_CK(cudaStreamWaitEvent(bs, c->pp_ready[pp], 0));
       if (c->input_ready) VXM_CK(cudaStreamWaitEvent(bs, c->input_ready, 0));
+      if (user_input) VXM_CK(cudaStreamWaitEvent(bs, user_input, 0));
       clear_wrapped(c, s0, s1 - s0, bs);
       cudaGraphExec_t& g = c->bgraph[gi][pp][b];
       if (!g) g = capture_branch(c, s0, s1 - s0, bs);
@@ -771,6 +775,7 @@ void run_frame(vxm_ctx* c, bool cloud, bool direct = false) {
       if (c->tail_pending) VXM_CK(cudaStreamWaitEvent(bs, c->tail_ev, 0));
       VXM_CK(cudaStreamWaitEvent(bs, c->pp_ready[pp], 0));
       if (c->input_ready) VXM_CK(cudaStreamWaitEvent(bs, c->input_ready, 0));
+      if (user_input) VXM_CK(cudaStreamWaitEvent(bs, user_input, 0));
       clear_wrapped(c, s0, s1 - s0, bs);
       launch_stages(c, false, false, s0, s1 - s0, bs, false, false);
       VXM_CK(cudaStreamWaitEvent(bs, c->chain[b == 0 ? B - 1 : b - 1], 0));
@@ -788,6 +793,7 @@ void run_frame(vxm_ctx* c, bool cloud, bool direct = false) {
     }
     c->last_marks = false;
   } else if (!graphs) {
+    if (user_input) VXM_CK(cudaStreamWaitEvent(c->stream, user_input, 0));
     clear_wrapped(c, 0, c->nslots, c->stream);
     VXM_CK(cudaEventRecord(c->ev[0], c->stream));
     launch_frame(c, cloud, false);
@@ -812,6 +818,7 @@ void run_frame(vxm_ctx* c, bool cloud, bool direct = false) {
       apply_stage_events(c, g, gi, pp);
       c->stage_dirty[gi][pp] = false;
     }
+    if (user_input) VXM_CK(cudaStreamWaitEvent(c->stream, user_input, 0));
     clear_wrapped(c, 0, c->nslots, c->stream);
     VXM_CK(cudaEventRecord(c->ev[0], c->stream));
     VXM_CK(cudaGraphLaunch(g, c->stream));
@@ -1275,6 +1282,13 @@ int vxm_integrate_depth_async(vxm_ctx* ctx, const float* depth, const vxm_pose* 
     run_frame(ctx, false);
     ctx->input_ready = nullptr;
     VXM_CK(cudaEventRecord(ctx->ev_consumed[b], ctx->stream));
+  });
+}
+
+int vxm_set_input_event(vxm_ctx* ctx, void* cuda_event) {
+  return guarded([&] {
+    if (!ctx) throw InvalidArg{"null context"};
+    ctx->user_input = static_cast<cudaEvent_t>(cuda_event);
   });
 }
 

@@ -287,6 +287,12 @@ class MappingPipeline:
         arr = (C.c_void_p * 4)(*(events or [None] * 4))
         N.check(self._lib.vxm_set_stage_events(self._ctx, arr if events else None))
 
+    def set_input_event(self, event):
+        """The next integrate call's kernels wait for this cudaEvent_t (an
+        int handle, e.g. torch.cuda.Event.cuda_event) recorded after the
+        device frames were produced on another stream."""
+        N.check(self._lib.vxm_set_input_event(self._ctx, C.c_void_p(event)))
+
     def last_frame_ms(self):
         v = C.c_float()
         N.check(self._lib.vxm_last_frame_ms(self._ctx, C.byref(v)))

@@ -619,3 +619,38 @@ def test_desynchronised_batch_across_epoch_wrap(gpu_lib, path):
         assert np.array_equal(batch.local_grid(s)[0], joined.local_grid(s)[0]), s
     for i, s in enumerate((0, S - 1)):
         assert np.array_equal(batch.local_grid(s)[0], singles[i].local_grid()[0]), s
+
+
+def test_device_frames_produced_on_another_stream(gpu_lib):
+    """Frames written by the caller on its own stream right before the call:
+    vxm_set_input_event makes the (desynchronised) batch wait for them."""
+    import torch
+
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 160, 120, 5.0)
+    grid = vm.GridSpec.create_centered(6.0, 6.0, 3.0, 0.1, (0.0, 0.0, 0.0))
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=2, depth=5.0)
+    S = 12
+    poses = [vm.look_along_x((0.0, 0.05 * s, 0.0)) for s in range(S)]
+    frames = vm.render_depth(cam, poses, scenes.box_field_boxes(3))
+    host = torch.from_numpy(frames).pin_memory()
+    dev = torch.empty_like(host, device="cuda")
+    producer = torch.cuda.Stream()
+    pipe = vm.MappingPipeline(cfg, n_streams=S)
+    ref = vm.MappingPipeline(cfg, n_streams=S)
+    pa = vm.pose_array(poses)
+    for k in range(3):
+        with torch.cuda.stream(producer):
+            dev.zero_()
+            torch.cuda._sleep(2_000_000)  # a slow producer
+            dev.copy_(host, non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(producer)
+        pipe.set_input_event(ready.cuda_event)
+        pipe.integrate_depth_device(dev.data_ptr(), pa)
+        st = pipe.wait_stats()
+        sr = ref.integrate_depth(frames, poses)
+        for s in range(S):
+            assert st[s]["points_total"] == sr[s]["points_total"]
+            assert st[s]["freed_count"] == sr[s]["freed_count"]
+    for s in range(S):
+        assert np.array_equal(pipe.local_grid(s)[0], ref.local_grid(s)[0])
