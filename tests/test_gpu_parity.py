@@ -578,8 +578,8 @@ def test_stage_events_attached_to_graph(gpu_lib):
         assert np.array_equal(timed.local_grid(s)[0], plain.local_grid(s)[0])
 
 
-@pytest.mark.parametrize("path", ["device", "async", "host"])
-def test_desynchronised_batch_across_epoch_wrap(gpu_lib, path):
+@pytest.mark.parametrize("path,S", [("device", 12), ("async", 12), ("host", 12), ("device", 13)])
+def test_desynchronised_batch_across_epoch_wrap(gpu_lib, path, S):
     """A batch of 12 streams runs as three per-branch graphs on their own
     streams (each waiting only for its call's inputs); 300 back-to-back calls
     cross the 8-bit epoch wrap, whose array clears go on the owning branch's
@@ -590,7 +590,7 @@ def test_desynchronised_batch_across_epoch_wrap(gpu_lib, path):
     cam = vm.CameraModel(85 * DEG, 101 * DEG, 48, 36, 6.5)
     grid = vm.GridSpec.create_centered(4.0, 4.0, 2.0, 0.1, (0.0, 0.0, 0.0))
     cfg = vm.PipelineConfig(grid, cam, vox_inf=1, depth=6.0)
-    S, calls = 12, 300
+    calls = 300
     boxes = scenes.box_field_boxes(4)
     poses = [[vm.look_along_x((0.03 * (k % 40), 0.02 * s + 0.01 * (k % 17), 0.0)) for s in range(S)]
              for k in range(12)]

@@ -71,7 +71,7 @@ def _wander(rng, n, start):
     return out
 
 
-@pytest.mark.parametrize("S,F", [(1, 3), (2, 7), (3, 16), (1, 33), (1, 64)])
+@pytest.mark.parametrize("S,F", [(1, 3), (2, 7), (3, 16), (5, 4), (1, 33), (1, 64)])
 def test_sequence_equals_single_frame_path_while_wandering(gpu_lib, S, F):
     """(1, 33) and (1, 64): a single stream with F >= 32 merges its frame
     ranges as chained per-branch merges (uneven ranges for 33)."""
