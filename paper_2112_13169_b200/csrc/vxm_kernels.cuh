@@ -1061,13 +1061,16 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
 
 // Launches K3 over `slots` frame slots in the shape that suits the batch.
 constexpr long long kSplitMaxRays = 32768;
+#ifndef VXM_TB_MINB
+#define VXM_TB_MINB 24  // batch K3: 2-warp blocks at 40 registers (A/B define)
+#endif
 
 // `batch` is the number of slots of the whole call (graph branches launch
 // shares of it concurrently, so the GPU is as full as the total says).
 inline void launch_trace(const KParams& kp, int slots, int batch, cudaStream_t st) {
   const int tiles = kp.tiles_x * kp.tiles_y;
   if (batch >= 8) {
-    launch_pdl(trace_bundle_kernel<4, 2, 24, true, false, false>, dim3((tiles + 1) / 2, slots), dim3(64), 0, st, kp);
+    launch_pdl(trace_bundle_kernel<4, 2, VXM_TB_MINB, true, false, false>, dim3((tiles + 1) / 2, slots), dim3(64), 0, st, kp);
   } else {
     if (static_cast<long long>(kp.vw) * kp.vh * batch <= kSplitMaxRays) {
       // few rays (the GPU far from full): 8x2 tiles, each ray walked as two
