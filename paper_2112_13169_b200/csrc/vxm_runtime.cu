@@ -258,7 +258,10 @@ struct vxm_ctx {
   // FrameParams on the device, two buffers: the upload for the next call
   // (on param_stream) overlaps the graph of this one, and each buffer has
   // its own instance of every frame graph
-  static constexpr int kPP = 2;
+#ifndef VXM_PP
+#define VXM_PP 2
+#endif
+  static constexpr int kPP = VXM_PP;
   vxm::FrameParams* frames_pp[kPP] = {nullptr, nullptr};
   int pp = 0;  // buffer of the current call
   bool sync_call = false;  // the current call waits for its stats (vxm_integrate_depth / _cloud)
@@ -315,7 +318,7 @@ struct vxm_ctx {
   cudaGraphNode_t stage_nodes[kGraphs][kPP][4] = {};       // event-record nodes per graph
   bool pop_compact = false;  // K1 variant: valid fraction of the last observed frames < 1/2
   void* user_stage_ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  bool stage_dirty[kGraphs][kPP] = {{true, true}, {true, true}, {true, true}};  // node events need re-pointing
+  bool stage_clean[kGraphs][kPP] = {};  // node events point where they should
   bool graph_marks[kGraphs][kPP] = {};  // the instance holds the stage event-record nodes
   bool capture_marks = false;           // capture in progress records them
   bool last_marks = false;              // the last frame recorded them
@@ -657,7 +660,7 @@ void prepare_frames(vxm_ctx* c, const vxm_pose* poses, const float* depth_dev_ba
   }
   // upload into the buffer the call before last used, on the param stream,
   // so the copy runs while the previous graph is still executing
-  c->pp ^= 1;
+  c->pp = (c->pp + 1) % vxm_ctx::kPP;
   const int pp = c->pp;
   if (c->sync_call) {
     // a synchronous call (the stream is idle): the copy goes on the stream
@@ -812,11 +815,11 @@ void run_frame(vxm_ctx* c, bool cloud, bool direct = false) {
     }
     if (!g) {
       g = capture(c, cloud, gi, pp, marks);
-      c->stage_dirty[gi][pp] = true;
+      c->stage_clean[gi][pp] = false;
     }
-    if (c->stage_dirty[gi][pp]) {
+    if (!c->stage_clean[gi][pp]) {
       apply_stage_events(c, g, gi, pp);
-      c->stage_dirty[gi][pp] = false;
+      c->stage_clean[gi][pp] = true;
     }
     if (user_input) VXM_CK(cudaStreamWaitEvent(c->stream, user_input, 0));
     clear_wrapped(c, 0, c->nslots, c->stream);
@@ -1296,8 +1299,8 @@ int vxm_set_stage_events(vxm_ctx* ctx, void* const events[4]) {
   return guarded([&] {
     if (!ctx) throw InvalidArg{"null context"};
     for (int i = 0; i < 4; ++i) ctx->user_stage_ev[i] = events ? events[i] : nullptr;
-    for (auto& dd : ctx->stage_dirty)
-      for (bool& d : dd) d = true;
+    for (auto& dd : ctx->stage_clean)
+      for (bool& d : dd) d = false;
   });
 }
 
