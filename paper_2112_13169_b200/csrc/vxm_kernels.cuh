@@ -875,7 +875,6 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
     const double e0 = st.step[0] ? st.tdelta[0] : 0.0, e1 = st.step[1] ? st.tdelta[1] : 0.0,
                  e2 = st.step[2] ? st.tdelta[2] : 0.0;
     uint32_t al = active ? 1u : 0u;
-    bool alive = active;
     // kSplit: the steps whose chosen tmax is below tau = min(M) / 2 (none of
     // which can end the walk) are the near half; its lane walks them with
     // every threshold at tau. The far lane starts where they end: along each
@@ -908,7 +907,7 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
     const double Mmin = fmin(fmin(M0, M1), M2);
     const double lim = dsub(Mmin, dadd(dmul(static_cast<double>(kChunk - 1), dmax),
                                        dmul(0x1p-40, dadd(fabs(Mmin), dmul(static_cast<double>(kChunk), dmax)))));
-    while (__any_sync(0xffffffffu, alive)) {
+    while (__any_sync(0xffffffffu, al != 0u)) {
       if (kFast && __all_sync(0xffffffffu, !al || t0 < lim || t1 < lim || t2 < lim)) {
         uint32_t cell[kChunk];
 #pragma unroll
@@ -981,7 +980,6 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
         // far half's first
         if (kSplit && !far_half && !al) cell[j] = 0xffffffffu;
       }
-      alive = al != 0u;
       resolve_tail(cell);
     }
     if constexpr (kSplit) {
