@@ -9,7 +9,11 @@
 //   graph: K1 populate | K2 dilate (vox_inf > 0) | K3 trace_bundle |
 //          K4 merge+shift+count | K5 publish (counters to host-mapped
 //          memory, cleared for the next frame)
-// The measurement grid is never reset: epoch-tagged words (vxm_device.cuh).
+// Batches of >= 12 slots run as three branches over shares of the streams;
+// for single-frame batches each branch is its own graph on its own stream,
+// waiting only for its call's inputs, and the context stream joins them
+// (run_frame). The measurement grid is never reset: epoch-tagged words
+// (vxm_device.cuh).
 
 #include <cuda_runtime.h>
 
