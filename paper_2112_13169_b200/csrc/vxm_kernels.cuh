@@ -1472,7 +1472,9 @@ __host__ __device__ constexpr int merge_tma_rows(int dx, int dy) {
 // one stage: local and occupancy bytes and keys of `cells` cells, each window
 // widened to 16-byte boundaries
 __host__ __device__ constexpr size_t merge_tma_smem_bytes(int cells) {
-  return 2 * (static_cast<size_t>(cells) + 32) + 4 * static_cast<size_t>(cells) + 32;
+  // rounded to 16 bytes: the second stage starts right after the first and
+  // bulk copies need 16-byte aligned destinations
+  return (2 * (static_cast<size_t>(cells) + 32) + 4 * static_cast<size_t>(cells) + 32 + 15) & ~static_cast<size_t>(15);
 }
 
 __device__ __forceinline__ const unsigned char* align16_down(const void* p) {

@@ -654,3 +654,28 @@ def test_device_frames_produced_on_another_stream(gpu_lib):
             assert st[s]["freed_count"] == sr[s]["freed_count"]
     for s in range(S):
         assert np.array_equal(pipe.local_grid(s)[0], ref.local_grid(s)[0])
+
+
+@pytest.mark.parametrize("dims_cells", [(159, 21, 9), (133, 17, 7), (201, 13, 5)])
+def test_tma_merge_odd_rows_two_stages(gpu_lib, dims_cells):
+    """TMA-staged K4 with row groups whose stage size is not a multiple of
+    16 bytes (found by tools/fuzz_parity.py: 159-cell rows): the second stage
+    buffer stays 16-byte aligned. A moving robot, batch of 13 streams."""
+    vox = 0.1
+    grid = vm.GridSpec.create_centered(*(d * vox for d in dims_cells), vox, (0.0, 0.0, 0.0))
+    assert tuple(grid.dims) == dims_cells
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 40, 32, 6.0)
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=2, depth=6.0)
+    S = 13
+    gpu = vm.MappingPipeline(cfg, n_streams=S)
+    refs = [oracle_pipeline(cfg) for _ in (0, S - 1)]
+    boxes = scenes.box_field_boxes(6)
+    for k in range(6):
+        poses = [vm.look_along_x((0.13 * k + 0.02 * s, -0.07 * k, 0.05 * k)) for s in range(S)]
+        depth = vm.render_depth(cam, poses, boxes)
+        st = gpu.integrate_depth(depth, poses)
+        for i, s in enumerate((0, S - 1)):
+            sr = refs[i].integrate_depth(depth[s], poses[s])
+            assert st[s]["freed_count"] == sr["freed_count"] and st[s]["occupied_count"] == sr["occupied_count"]
+    for i, s in enumerate((0, S - 1)):
+        assert np.array_equal(gpu.local_grid(s)[0], refs[i].local_grid()[0])

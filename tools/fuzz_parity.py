@@ -1,0 +1,79 @@
+"""Randomised parity sweep (test infrastructure; run under gpurun): random grid
+shapes and voxel sizes (odd and even dims_x, rows above and below 128 cells),
+camera sizes, vox_inf 0-5, depth limits, general rotations and robot motion
+(shifts along every axis, jumps), single streams and batches (desynchronised
+branches), compared frame by frame (stats) and grid by grid with the
+reference's Sequential pipeline. Prints one summary line per case and a total;
+exits non-zero on the first mismatch. Usage: python tools/fuzz_parity.py [seconds]"""
+import math, sys, time
+sys.path.insert(0, '.')
+import numpy as np
+from paper_2112_13169_b200 import voxmap as vm
+from tests import scenes
+from tests.oracle_api import oracle_pipeline
+
+KEYS = ("points_total", "points_outside", "rays_traced", "voxels_freed", "voxels_marked_unknown_traced",
+        "voxels_skipped_out_of_bounds", "occupied_count", "freed_count", "shifted", "shift_offset", "origin")
+
+
+def rotation(rng, tilt):
+    yaw, pitch, roll = rng.uniform(-math.pi, math.pi), rng.uniform(-tilt, tilt), rng.uniform(-tilt, tilt)
+    cz, sz, cy, sy, cx, sx = math.cos(yaw), math.sin(yaw), math.cos(pitch), math.sin(pitch), math.cos(roll), math.sin(roll)
+    Rz = np.array([[cz, -sz, 0], [sz, cz, 0], [0, 0, 1]])
+    Ry = np.array([[cy, 0, sy], [0, 1, 0], [-sy, 0, cy]])
+    Rx = np.array([[1, 0, 0], [0, cx, -sx], [0, sx, cx]])
+    return vm.look_along_x((0, 0, 0))[0] @ (Rz @ Ry @ Rx)
+
+
+def main():
+    budget = float(sys.argv[1]) if len(sys.argv) > 1 else 240.0
+    seed = int(sys.argv[2]) if len(sys.argv) > 2 else int(time.time()) % 100000
+    print("seed", seed, flush=True)
+    rng = np.random.default_rng(seed)
+    t_end = time.time() + budget
+    cases = frames = 0
+    while time.time() < t_end:
+        vox = float(rng.choice([0.05, 0.08, 0.1, 0.13, 0.15]))
+        ext = rng.uniform([1.5, 1.5, 0.8], [9.0, 6.0, 3.0])
+        grid = vm.GridSpec.create_centered(*ext, vox, (0.0, 0.0, 0.0))
+        w, h = int(rng.integers(24, 120)), int(rng.integers(18, 90))
+        depth_m = float(rng.uniform(2.0, 7.0))
+        cam = vm.CameraModel(math.radians(rng.uniform(60, 100)), math.radians(rng.uniform(70, 110)), w, h, depth_m)
+        vox_inf = int(rng.integers(0, 6))
+        cfg = vm.PipelineConfig(grid, cam, vox_inf=vox_inf, depth=depth_m)
+        S = int(rng.choice([1, 1, 2, 12, 13]))
+        n = int(rng.integers(3, 12))
+        boxes = scenes.box_field_boxes(int(rng.integers(1, 9)))
+        step = rng.uniform(-1.5, 1.5, 3) * vox
+        tilt = float(rng.uniform(0.0, 0.6))
+        poses = [[(rotation(rng, tilt), np.array([0.1 * s, 0.0, 0.0]) + k * step
+                   + (np.array([0.0, 3.0, 0.0]) if k == n // 2 and rng.random() < 0.3 else 0.0))
+                  for s in range(S)] for k in range(n)]
+        desc = dict(vox=vox, dims=tuple(grid.dims), cam=(w, h), vox_inf=vox_inf, S=S, n=n, depth=round(depth_m, 3))
+        print(f"case {cases}: {desc}", flush=True)
+        gpu = vm.MappingPipeline(cfg, n_streams=S)
+        refs = [oracle_pipeline(cfg) for _ in range(S)]
+        for k in range(n):
+            depth = np.stack([scenes.render(cam, poses[k][s], boxes) for s in range(S)])
+            st = gpu.integrate_depth(depth if S > 1 else depth[0], poses[k] if S > 1 else poses[k][0])
+            st = st if S > 1 else [st]
+            for s in range(S):
+                sr = refs[s].integrate_depth(depth[s], poses[k][s])
+                for key in KEYS:
+                    if st[s][key] != sr[key]:
+                        print(f"MISMATCH case {cases} frame {k} stream {s} {key}: {st[s][key]} vs {sr[key]}",
+                              dict(vox=vox, dims=tuple(grid.dims), cam=(w, h), vox_inf=vox_inf, S=S), flush=True)
+                        sys.exit(1)
+            frames += S
+        for s in range(S):
+            if not np.array_equal(gpu.local_grid(s)[0], refs[s].local_grid()[0]):
+                print(f"GRID MISMATCH case {cases} stream {s}", flush=True)
+                sys.exit(1)
+        gpu.close()
+        print(f"case {cases} ok", flush=True)
+        cases += 1
+    print(f"fuzz parity: {cases} cases, {frames} frames, all bit-exact", flush=True)
+
+
+if __name__ == "__main__":
+    main()
