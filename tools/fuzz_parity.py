@@ -51,9 +51,32 @@ def main():
                   for s in range(S)] for k in range(n)]
         desc = dict(vox=vox, dims=tuple(grid.dims), cam=(w, h), vox_inf=vox_inf, S=S, n=n, depth=round(depth_m, 3))
         print(f"case {cases}: {desc}", flush=True)
-        gpu = vm.MappingPipeline(cfg, n_streams=S)
         refs = [oracle_pipeline(cfg) for _ in range(S)]
-        for k in range(n):
+        F = int(rng.choice([1, 1, 1, 2, 5, 33])) if S <= 3 else 1
+        if F > 1:
+            # multi-frame calls: frames_per_call consecutive frames of each stream
+            gpu = vm.MappingPipeline(cfg, n_streams=S, frames_per_call=F)
+            print(f"  frames_per_call {F}", flush=True)
+            calls = max(1, n // 2)
+            traj = [[(rotation(rng, tilt), np.array([0.1 * s, 0.0, 0.0]) + j * step) for j in range(calls * F)]
+                    for s in range(S)]
+            for c in range(calls):
+                ps = [traj[s][c * F + j] for s in range(S) for j in range(F)]
+                depth = np.stack([scenes.render(cam, p, boxes) for p in ps])
+                st = gpu.integrate_depth(depth, ps)
+                for s in range(S):
+                    for j in range(F):
+                        i = s * F + j
+                        sr = refs[s].integrate_depth(depth[i], ps[i])
+                        for key in KEYS:
+                            if st[i][key] != sr[key]:
+                                print(f"MISMATCH case {cases} call {c} stream {s} frame {j} {key}: "
+                                      f"{st[i][key]} vs {sr[key]}", flush=True)
+                                sys.exit(1)
+                frames += S * F
+        else:
+          gpu = vm.MappingPipeline(cfg, n_streams=S)
+          for k in range(n):
             depth = np.stack([scenes.render(cam, poses[k][s], boxes) for s in range(S)])
             st = gpu.integrate_depth(depth if S > 1 else depth[0], poses[k] if S > 1 else poses[k][0])
             st = st if S > 1 else [st]
