@@ -40,7 +40,8 @@ def main():
         depth_m = float(rng.uniform(2.0, 7.0))
         cam = vm.CameraModel(math.radians(rng.uniform(60, 100)), math.radians(rng.uniform(70, 110)), w, h, depth_m)
         vox_inf = int(rng.integers(0, 6))
-        cfg = vm.PipelineConfig(grid, cam, vox_inf=vox_inf, depth=depth_m)
+        tracer = vm.N.TRACER_PER_PIXEL if rng.random() < 0.15 else vm.N.TRACER_BUNDLED
+        cfg = vm.PipelineConfig(grid, cam, vox_inf=vox_inf, depth=depth_m, tracer_mode=tracer)
         S = int(rng.choice([1, 1, 2, 12, 13]))
         n = int(rng.integers(3, 12))
         boxes = scenes.box_field_boxes(int(rng.integers(1, 9)))
@@ -49,7 +50,8 @@ def main():
         poses = [[(rotation(rng, tilt), np.array([0.1 * s, 0.0, 0.0]) + k * step
                    + (np.array([0.0, 3.0, 0.0]) if k == n // 2 and rng.random() < 0.3 else 0.0))
                   for s in range(S)] for k in range(n)]
-        desc = dict(vox=vox, dims=tuple(grid.dims), cam=(w, h), vox_inf=vox_inf, S=S, n=n, depth=round(depth_m, 3))
+        desc = dict(vox=vox, dims=tuple(grid.dims), cam=(w, h), vox_inf=vox_inf, S=S, n=n, depth=round(depth_m, 3),
+                    per_pixel=tracer == vm.N.TRACER_PER_PIXEL)
         print(f"case {cases}: {desc}", flush=True)
         refs = [oracle_pipeline(cfg) for _ in range(S)]
         F = int(rng.choice([1, 1, 1, 2, 5, 33])) if S <= 3 else 1
