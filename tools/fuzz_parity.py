@@ -78,10 +78,23 @@ def main():
                 frames += S * F
         else:
           gpu = vm.MappingPipeline(cfg, n_streams=S)
+          path = str(rng.choice(["host", "device", "async"]))
+          print(f"  path {path}", flush=True)
+          keep = []
           for k in range(n):
             depth = np.stack([scenes.render(cam, poses[k][s], boxes) for s in range(S)])
-            st = gpu.integrate_depth(depth if S > 1 else depth[0], poses[k] if S > 1 else poses[k][0])
-            st = st if S > 1 else [st]
+            if path == "host":
+                st = gpu.integrate_depth(depth if S > 1 else depth[0], poses[k] if S > 1 else poses[k][0])
+                st = st if S > 1 else [st]
+            else:
+                import torch
+                buf = torch.from_numpy(depth).cuda() if path == "device" else torch.from_numpy(depth).pin_memory()
+                keep.append(buf)  # (async: the staging copy reads it later)
+                if path == "device":
+                    gpu.integrate_depth_device(buf.data_ptr(), vm.pose_array(poses[k]))
+                else:
+                    gpu.integrate_depth_async(buf.data_ptr(), vm.pose_array(poses[k]))
+                st = gpu.wait_stats()
             for s in range(S):
                 sr = refs[s].integrate_depth(depth[s], poses[k][s])
                 for key in KEYS:
