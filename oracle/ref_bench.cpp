@@ -15,6 +15,20 @@
 //
 // Prints one JSON object: frames/s over the timed steps, per-frame latency
 // percentiles (linear interpolation as proj/src/sim/bench.cpp:19-25).
+//
+// Parity dumps (bench.py and tests/test_gpu_bench_parity.py compare the GPU
+// against them): --dump-stats FILE writes, for every step (warm-up steps
+// included) and stream, the nine PipelineStats counters as int64
+// (points_total, points_outside, rays_traced, voxels_freed,
+// voxels_marked_unknown_traced, voxels_skipped_out_of_bounds,
+// occupied_count, freed_count, shifted); --dump-grids FILE writes every
+// stream's final local grid (cells) followed by all origins (3 doubles each).
+//
+// Latency mode (--latency-frames N > 0): one stream, N frames of the pool
+// rule (stream 0), depth_to_cloud + integrate timed per frame after 5
+// warm-up frames as sim::measure does (proj/src/sim/bench.cpp:44-55), with
+// --parallel 0 (Sequential, one core) or 1 (DataParallel, OpenMP over
+// --threads threads, AVX2 kernels via dispatch()).
 
 #include <algorithm>
 #include <atomic>
@@ -24,6 +38,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <numbers>
+#include <omp.h>
 #include <string>
 #include <thread>
 #include <vector>
@@ -70,7 +85,16 @@ int main(int argc, char** argv) {
   const unsigned seed = static_cast<unsigned>(arg_d(argc, argv, "--seed", 1));
   int T = static_cast<int>(arg_d(argc, argv, "--threads", 0));
   if (T <= 0) T = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+  const int T_all = T;
   T = std::min(T, S);
+  const int lat_frames = static_cast<int>(arg_d(argc, argv, "--latency-frames", 0));
+  const bool parallel = arg_d(argc, argv, "--parallel", 0) != 0;
+  const char* dump_stats = nullptr;
+  const char* dump_grids = nullptr;
+  for (int i = 1; i + 1 < argc; ++i) {
+    if (std::strcmp(argv[i], "--dump-stats") == 0) dump_stats = argv[i + 1];
+    if (std::strcmp(argv[i], "--dump-grids") == 0) dump_grids = argv[i + 1];
+  }
 
   CameraModel cam;
   cam.fov_x = 85.0 * std::numbers::pi / 180.0;
@@ -99,6 +123,36 @@ int main(int argc, char** argv) {
   pc.depth = depth;
   pc.tracer_mode = TracerMode::Bundled;
   pc.parallelism = ExecutionMode::Sequential;
+
+  if (lat_frames > 0) {
+    const ExecutionMode mode = parallel ? ExecutionMode::DataParallel : ExecutionMode::Sequential;
+    omp_set_num_threads(parallel ? T_all : 1);
+    PipelineConfig c = pc;
+    c.parallelism = mode;
+    c.grid = GridSpec::create_centered(gx, gy, gz, vs, poses[0].translation);
+    MappingPipeline pipe(c);
+    std::vector<double> us;
+    us.reserve(static_cast<size_t>(lat_frames));
+    constexpr int kWarm = 5;  // sim::measure's warm-up
+    for (int k = 0; k < kWarm + lat_frames; ++k) {
+      const int j = k % P;
+      const auto f0 = Clock::now();
+      MeasurementFrame f;
+      f.cloud = depth_to_cloud(frames[j], cam, mode);
+      f.t_wc = poses[j];
+      pipe.integrate(f);
+      const double t = std::chrono::duration<double, std::micro>(Clock::now() - f0).count();
+      if (k >= kWarm) us.push_back(t);
+    }
+    double sum = 0.0;
+    for (double v : us) sum += v;
+    std::printf(
+        "{\"mode\": \"%s\", \"frames\": %d, \"threads\": %d, \"p50_ms\": %.4f, \"p99_ms\": %.4f, "
+        "\"mean_ms\": %.4f}\n",
+        parallel ? "DataParallel" : "Sequential", lat_frames, parallel ? T_all : 1, percentile(us, 0.5) / 1000.0,
+        percentile(us, 0.99) / 1000.0, sum / us.size() / 1000.0);
+    return 0;
+  }
   std::vector<MappingPipeline> pipes;
   pipes.reserve(S);
   for (int s = 0; s < S; ++s) {
@@ -109,6 +163,7 @@ int main(int argc, char** argv) {
 
   std::vector<std::vector<double>> lat(T);
   std::atomic<unsigned long long> checksum{0};
+  std::vector<long long> stats_dump(dump_stats ? static_cast<size_t>(WU + K) * S * 9 : 0);
   auto run_steps = [&](int k0, int nsteps, bool record) {
     std::vector<std::thread> th;
     for (int t = 0; t < T; ++t)
@@ -125,6 +180,18 @@ int main(int argc, char** argv) {
             const double us = std::chrono::duration<double, std::micro>(Clock::now() - f0).count();
             if (record) lat[t].push_back(us);
             cs += st.occupied_count * 1000003ull + st.freed_count;
+            if (dump_stats) {
+              long long* d = &stats_dump[(static_cast<size_t>(k) * S + s) * 9];
+              d[0] = static_cast<long long>(st.populate.points_total);
+              d[1] = static_cast<long long>(st.populate.points_outside);
+              d[2] = static_cast<long long>(st.trace.rays_traced);
+              d[3] = static_cast<long long>(st.trace.voxels_freed);
+              d[4] = static_cast<long long>(st.trace.voxels_marked_unknown_traced);
+              d[5] = static_cast<long long>(st.trace.voxels_skipped_out_of_bounds);
+              d[6] = static_cast<long long>(st.occupied_count);
+              d[7] = static_cast<long long>(st.freed_count);
+              d[8] = st.shifted ? 1 : 0;
+            }
           }
         }
         checksum += cs;
@@ -137,6 +204,25 @@ int main(int argc, char** argv) {
   const double secs = std::chrono::duration<double>(Clock::now() - t0).count();
   std::vector<double> all;
   for (auto& v : lat) all.insert(all.end(), v.begin(), v.end());
+  if (dump_stats) {
+    FILE* f = std::fopen(dump_stats, "wb");
+    if (!f || std::fwrite(stats_dump.data(), sizeof(long long), stats_dump.size(), f) != stats_dump.size()) return 2;
+    std::fclose(f);
+  }
+  if (dump_grids) {
+    FILE* f = std::fopen(dump_grids, "wb");
+    if (!f) return 2;
+    for (int s = 0; s < S; ++s) {
+      const VoxelGrid& g = pipes[s].local_grid();
+      if (std::fwrite(g.raw(), 1, g.size(), f) != g.size()) return 2;
+    }
+    for (int s = 0; s < S; ++s) {
+      const Eigen::Vector3d o = pipes[s].local_grid().spec().origin;
+      const double od[3] = {o.x(), o.y(), o.z()};
+      if (std::fwrite(od, sizeof(double), 3, f) != 3) return 2;
+    }
+    std::fclose(f);
+  }
   std::printf(
       "{\"frames\": %d, \"seconds\": %.6f, \"frames_per_s\": %.3f, \"p50_ms\": %.4f, \"p99_ms\": %.4f, "
       "\"threads\": %d, \"streams\": %d, \"steps\": %d, \"checksum\": %llu}\n",

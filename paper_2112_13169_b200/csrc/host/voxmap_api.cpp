@@ -494,10 +494,22 @@ void write_grid(const VoxelGrid& grid, const std::string& path) {
 }
 
 VoxelGrid read_grid(std::istream& in) {
-  const std::string buf((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  // Consumes exactly the header (eight formatted fields and the one
+  // character after them) and the cell bytes, leaving the stream positioned
+  // after the grid as grid_io.cpp:31-63 does, so several grids (or a grid and
+  // other data) can follow each other on one stream.
   vxm_io::VoxgridHeader h;
-  std::string err = vxm_io::parse_voxgrid_header(buf.data(), buf.size(), h);
-  if (err.empty()) err = vxm_io::check_voxgrid_cells(buf.data(), buf.size(), h);
+  std::string magic;
+  in >> magic >> h.dims[0] >> h.dims[1] >> h.dims[2] >> h.vox_size >> h.origin[0] >> h.origin[1] >> h.origin[2];
+  if (!in || magic != "VOXGRID1") throw std::runtime_error("read_grid: bad header");
+  if (h.dims[0] <= 0 || h.dims[1] <= 0 || h.dims[2] <= 0 || !(h.vox_size > 0.0))
+    throw std::runtime_error("read_grid: invalid dimensions");
+  in.ignore(1);  // the newline ending the header
+  std::string buf(h.cells(), '\0');
+  in.read(buf.data(), static_cast<std::streamsize>(buf.size()));
+  if (in.gcount() != static_cast<std::streamsize>(buf.size())) throw std::runtime_error("read_grid: truncated cell data");
+  h.data_offset = 0;
+  const std::string err = vxm_io::check_voxgrid_cells(buf.data(), buf.size(), h);
   if (!err.empty()) throw std::runtime_error(err);
   GridSpec spec;
   spec.dims_x = h.dims[0];
@@ -537,6 +549,9 @@ const KernelTable& cuda_table() {
   static const KernelTable t{vxm_kernel_merge, vxm_kernel_transform_voxelize, "cuda-sm100a"};
   return t;
 }
+// Deliberately the CUDA table: this library has no CPU compute path (a
+// caller that asks for the scalar table gets the sm_100a kernels, which
+// produce the same bytes; see b200_api.hpp and INTEGRATION.md).
 const KernelTable& scalar_table() { return cuda_table(); }
 const KernelTable& dispatch() { return cuda_table(); }
 }  // namespace kernels

@@ -225,6 +225,15 @@ class MappingPipeline:
         N.check(self._lib.vxm_integrate_depth_frames(self._ctx, C.c_void_p(depth.ctypes.data), pa, n, st))
         return [stats_dict(st[i]) for i in range(n)]
 
+    def integrate_depth_frames_ptr(self, depth_ptr: int, poses):
+        """integrate_depth_frames from a raw host pointer (e.g. pinned memory,
+        which the copy engine reads asynchronously)."""
+        n = len(poses)
+        pa = (N.PoseC * max(1, n))(*(pose_c(p) for p in poses))
+        st = (N.StatsC * max(1, n))()
+        N.check(self._lib.vxm_integrate_depth_frames(self._ctx, C.c_void_p(depth_ptr), pa, n, st))
+        return [stats_dict(st[i]) for i in range(n)]
+
     def integrate_depth_ptr(self, depth_ptr: int, poses):
         """Host-buffer entry point for a raw (e.g. pinned) pointer."""
         self._set_poses(poses)

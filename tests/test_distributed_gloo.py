@@ -52,3 +52,36 @@ def test_two_rank_sharding_and_max_timing():
     assert (a0, b0, a1, b1) == (0, 63, 64, 127)  # disjoint contiguous stream blocks
     assert s0 == s1 == 2.0                        # both see the slowest rank's time
     assert f0 == f1 == pytest.approx(64 * 10 * 2 / 2.0)
+
+
+def _bench(*extra):
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    env = {k: v for k, v in __import__("os").environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, str(root / "bench.py"), "--plumbing-only", "--steps", "3", *extra],
+                         capture_output=True, text=True, timeout=240, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+@pytest.mark.parametrize("scaling,per_rank", [("weak", 64), ("strong", 32)])
+def test_bench_relaunches_ranks_for_gpus_flag(scaling, per_rank):
+    """`python bench.py --gpus 2` without a torchrun environment spawns two
+    ranks itself (gloo here: no GPUs), each owning its own stream block, and
+    rank 0 reports n_gpus 2 with the max over ranks of the timed region (rank 1
+    sleeps 10 ms in it)."""
+    line = _bench("--gpus", "2", "--scaling", scaling)
+    assert line["n_gpus"] == 2 and line["backend"] == "gloo"
+    assert line["streams_per_rank"] == per_rank
+    assert line["owned"] == [[0, per_rank - 1], [per_rank, 2 * per_rank - 1]]
+    assert line["max_seconds"] >= 0.01
+    assert line["config"]["streams_total"] == 2 * per_rank
+
+
+def test_bench_single_rank_default():
+    line = _bench()
+    assert line["n_gpus"] == 1 and line["backend"] is None and line["owned"] == [[0, 63]]

@@ -198,3 +198,30 @@ def test_chained_desync_calls_mixed_with_partial_calls(gpu_lib):
             _check(stats[j], one.integrate_depth(depth[j], poses[j]), (i, n, j))
         assert np.array_equal(seq.local_grid()[0], one.local_grid()[0]), i
         i += n
+
+
+@pytest.mark.parametrize("F", [40, 64])
+def test_full_frames_call_from_pinned_buffer(gpu_lib, F):
+    """vxm_integrate_depth_frames with n_frames == F >= 32 from a pinned host
+    buffer: the call runs the desynchronised chained-range branches, which
+    must not start populating before the H2D copy of the frames has landed
+    (the copy is read asynchronously from pinned memory). Checked against the
+    reference build frame by frame, twice in a row."""
+    import torch
+
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 320, 240, 6.5)
+    grid = vm.GridSpec.create_centered(6.0, 6.0, 3.0, 0.1, (0.0, 0.0, 0.0))
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=1, depth=6.5)
+    seq = vm.MappingPipeline(cfg, frames_per_call=F)
+    orc = oracle_pipeline(cfg)
+    rng = np.random.default_rng(F)
+    traj = _wander(rng, 2 * F, (0.0, 0.0, 0.0))
+    boxes = scenes.box_field_boxes(2)
+    for call in range(2):
+        poses = traj[call * F:(call + 1) * F]
+        depth = vm.render_depth(cam, poses, boxes)
+        pinned = torch.from_numpy(depth).pin_memory()
+        stats = seq.integrate_depth_frames_ptr(pinned.data_ptr(), poses)
+        for j in range(F):
+            _check(stats[j], orc.integrate_depth(depth[j], poses[j]), (call, j))
+        assert np.array_equal(seq.local_grid()[0], orc.local_grid()[0]), call
