@@ -101,11 +101,24 @@ def build_oracle(force=False):
     return built
 
 
+def build_ref_suites(force=False):
+    """The reference's own unit-test programs (proj/tests/test_*.cpp,
+    unmodified) against the drop-in headers and libvoxmap_b200.so
+    (tests/cpp/Makefile.refsuites). Needs /root/reference: built here, the
+    binaries travel to the GPU box. Test infrastructure."""
+    if not Path("/root/reference/proj/tests").exists():
+        return []
+    _run(["make", "-s", "-f", "tests/cpp/Makefile.refsuites", f"-j{os.cpu_count() or 4}"]
+         + (["-B"] if force else []), cwd=ROOT)
+    return sorted((ROOT / "tests" / "cpp" / "build" / "ref_suites").glob("test_*[!.o]"))
+
+
 def build_all(force=False):
     lib = build_libvxm(force)
     dropin = build_dropin(force)
     oracle = build_oracle(force)
-    return [lib, dropin, *oracle]
+    suites = build_ref_suites(force)
+    return [lib, dropin, *oracle, *suites]
 
 
 if __name__ == "__main__":

@@ -18,6 +18,7 @@
 
 #include "voxgrid_format.hpp"
 #include "voxmap/b200_api.hpp"
+#include "voxmap/sim/trajectory.hpp"
 
 namespace voxmap {
 
@@ -555,5 +556,29 @@ const KernelTable& cuda_table() {
 const KernelTable& scalar_table() { return cuda_table(); }
 const KernelTable& dispatch() { return cuda_table(); }
 }  // namespace kernels
+
+// ----------------------------------------------------------- pose helpers
+
+namespace sim {
+RigidTransform look_along_x(const Eigen::Vector3d& position) {
+  Eigen::Matrix3d r;
+  r(0, 0) = 0.0;  r(0, 1) = 0.0;  r(0, 2) = 1.0;
+  r(1, 0) = -1.0; r(1, 1) = 0.0;  r(1, 2) = 0.0;
+  r(2, 0) = 0.0;  r(2, 1) = -1.0; r(2, 2) = 0.0;
+  return RigidTransform::from_rotation(r, position);
+}
+
+std::vector<RigidTransform> sweep_trajectory(const Eigen::Vector3d& start, const Eigen::Vector3d& end, int frames) {
+  if (frames < 1) throw std::invalid_argument("sweep_trajectory: frames must be >= 1");
+  std::vector<RigidTransform> poses;
+  poses.reserve(static_cast<std::size_t>(frames));
+  const Eigen::Vector3d span = end - start;
+  for (int i = 0; i < frames; ++i) {
+    const double s = frames == 1 ? 0.0 : static_cast<double>(i) / (frames - 1);
+    poses.push_back(look_along_x(start + s * span));
+  }
+  return poses;
+}
+}  // namespace sim
 
 }  // namespace voxmap
