@@ -140,6 +140,7 @@ typedef struct vxm_ctx vxm_ctx;
 #define VXM_FLAG_SINGLE_BRANCH 4u /* batches: one graph branch (stage events then time each whole stage) */
 #define VXM_FLAG_NO_TMA_MERGE 8u  /* K4 with direct loads instead of TMA-staged rows (A/B and fallback) */
 #define VXM_FLAG_NO_DESYNC 32u   /* batches: one graph with joined branches instead of per-branch graphs (A/B) */
+#define VXM_FLAG_WIDE_KEYS 64u   /* 32-bit measurement keys even when 16-bit keys would do (A/B, tests) */
 #define VXM_FLAG_STAGE_EVENTS 16u /* record the stage-boundary events inside the frame graph (fills
                                      vxm_stats::*_us; each event node costs a few us per frame) */
 

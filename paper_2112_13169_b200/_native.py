@@ -19,6 +19,7 @@ UNKNOWN, FREE, OCCUPIED, UNKNOWN_TRACED = 0, 1, 2, 3
 TRACER_BUNDLED, TRACER_PER_PIXEL = 0, 1
 FLAG_STAGE_TIMING, FLAG_NO_GRAPH, FLAG_SINGLE_BRANCH, FLAG_NO_TMA_MERGE, FLAG_STAGE_EVENTS = 1, 2, 4, 8, 16
 FLAG_NO_DESYNC = 32
+FLAG_WIDE_KEYS = 64
 
 
 class GridSpecC(C.Structure):

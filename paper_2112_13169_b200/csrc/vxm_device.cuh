@@ -21,36 +21,77 @@ namespace vxm {
 // The reference measurement grid is one byte per cell, reset to Unknown every
 // frame (proj/src/pipeline.cpp:83), written Occupied by populate and Free /
 // UnknownTraced by the rays, with the highest-index ray winning a conflict in
-// Sequential mode (raytracer.cpp:98-104). The GPU splits it in
-// two arrays that are never reset, because every entry carries the frame's
-// epoch e (1..255, per stream):
+// Sequential mode (raytracer.cpp:98-104). The GPU keeps two
+// arrays per measurement slot:
 //
-//   occ[c]  (uint8)   == e            Occupied this frame (populate / dilation)
-//   key[c]  (uint32)  == e << 18 | (ray + 1) << 1 | traced
-//                                      written by bundle ray `ray` this frame
-//                     == e << 18 | 0/1 Free / UnknownTraced carried in from a
-//                                      host grid (lowest priority)
-//   anything tagged with another epoch: Unknown.
+//   occ[c]  (uint8)  == e   Occupied this frame (e = the slot's 8-bit epoch,
+//                            1..255, so occ is never reset; cleared once per
+//                            255 frames). Read-only during the trace.
+//   key[c]  (16 or 32 bit)   the cell's measurement state as an ordered key:
+//                            Unknown (untouched) < Free / UnknownTraced carried
+//                            in from a host grid < ray 0 < ray 1 < ... <
+//                            Occupied. A ray writes key(ray) | traced with a
+//                            fire-and-forget max reduction, so the highest
+//                            ray index wins: exactly the Sequential
+//                            last-writer rule. Populate / dilation store
+//                            Occupied keys; the merge (K4) decodes the keys,
+//                            then writes Unknown back over every key it saw
+//                            touched (and over the cells the shift drops), so
+//                            the array is all-Unknown again when the next
+//                            frame starts: no epoch bits, no reset pass.
 //
-// Populate stores occ with plain idempotent byte stores (no atomics). During
-// the trace occ is read-only (read through the non-coherent path) and rays
-// resolve write conflicts with a fire-and-forget atomicMax on key: a higher
-// ray index always wins, exactly the Sequential last-writer rule. Occupied
-// cells are never written by rays, so occ wins over key when decoding.
+// Key formats (KeyFmt<bits>): 32-bit keys are plain unsigned integers
+// (Unknown 0, ray r -> 2(r+2) | traced, Occupied 0xFFFFFFFF; up to 2^31 - 3
+// rays). 16-bit keys halve the key traffic for bundles of up to 32,638 rays
+// (every 640x480 configuration): they are bf16 bit patterns, ordered by the
+// L2's native packed-bf16 max reduction (red.max.noftz.v2.bf16 on the
+// aligned cell pair, the other half given -inf, the neutral element):
+// Unknown = -inf (0xFF80), Occupied = +inf (0x7F80), and the ray keys walk up
+// the finite values in order (negative patterns downwards, then positive
+// patterns upwards; the traced bit is bit 0 of the pattern in both halves of
+// the range, and NaN patterns are never formed).
 // ---------------------------------------------------------------------------
-constexpr uint32_t kKeyShift = 18;
-constexpr uint32_t kLowMask = (1u << kKeyShift) - 1u;  // 0x3FFFF
-constexpr uint32_t kMaxEpoch = 255u;                   // fits the occ byte
-constexpr uint32_t kMaxRays = (kLowMask >> 1) - 1u;    // (ray+1)<<1|1 <= 0x3FFFF
-constexpr int kMaxVoxInf = 16;
+template <int kBits>
+struct KeyFmt;
 
-__host__ __device__ constexpr uint32_t key_tag(uint32_t epoch) { return epoch << kKeyShift; }
+template <>
+struct KeyFmt<16> {
+  using T = uint16_t;
+  static constexpr uint32_t kUnknown = 0xFF80u;   // bf16 -inf
+  static constexpr uint32_t kOccupied = 0x7F80u;  // bf16 +inf
+  static constexpr long long kMaxRays = 32638;    // ray indices 0..32637
+  // Free key of ray r (| 1: UnknownTraced); r = -1: carried in from a host grid
+  __host__ __device__ static constexpr uint32_t ray_base(long long r) {
+    return 2 * (r + 2) < 32640 ? static_cast<uint32_t>(0xFF80 - 2 * (r + 2))
+                               : static_cast<uint32_t>(2 * (r + 2) - 32640);
+  }
+};
 
-// (occ, key) -> reference byte state (0 Unknown, 1 Free, 2 Occupied, 3 UnknownTraced).
-__device__ __forceinline__ uint32_t decode_cell(uint32_t occ, uint32_t key, uint32_t epoch) {
-  if (occ == epoch) return 2u;
-  if ((key >> kKeyShift) != epoch) return 0u;
-  return (key & 1u) ? 3u : 1u;
+template <>
+struct KeyFmt<32> {
+  using T = uint32_t;
+  static constexpr uint32_t kUnknown = 0u;
+  static constexpr uint32_t kOccupied = 0xFFFFFFFFu;
+  static constexpr long long kMaxRays = 0x7FFFFFFDLL;
+  __host__ __device__ static constexpr uint32_t ray_base(long long r) { return static_cast<uint32_t>(2 * (r + 2)); }
+};
+
+constexpr uint32_t kMaxEpoch = 255u;  // fits the occ byte
+constexpr int kMaxVoxInf = 16;        // the tile dilation (K2); larger radii take the generic passes
+
+// key -> reference byte state (0 Unknown, 1 Free, 2 Occupied, 3 UnknownTraced)
+template <int kBits>
+__host__ __device__ __forceinline__ uint32_t decode_key(uint32_t k) {
+  if (k == KeyFmt<kBits>::kUnknown) return 0u;
+  if (k == KeyFmt<kBits>::kOccupied) return 2u;
+  return 1u + 2u * (k & 1u);
+}
+
+// reference byte state -> key of a cell carried in from a host grid
+template <int kBits>
+__host__ __device__ __forceinline__ uint32_t encode_state(uint32_t b) {
+  return b == 2u ? KeyFmt<kBits>::kOccupied
+                 : (b == 1u || b == 3u) ? (KeyFmt<kBits>::ray_base(-1) | (b >> 1)) : KeyFmt<kBits>::kUnknown;
 }
 
 // merge_scalar (proj/src/kernels/kernels_scalar.cpp:10-16): measurement 0
@@ -101,10 +142,10 @@ struct FrameParams {
   const double* ys;
   const double* zs;
   long long n_points;
-  // this stream's occupancy bytes and ray keys (base + s*n); read from memory
+  // this stream's occupancy bytes and keys (base + slot*n); read from memory
   // so the tracer keeps them in registers instead of rebuilding each address
   const uint8_t* occ_s;
-  uint32_t* key_s;
+  void* key_s;
   int32_t off[3];     // shift applied after the merge (0,0,0 = none)
   uint32_t epoch;     // 1..255
   uint32_t cur;       // which local buffer holds the current grid
@@ -139,13 +180,78 @@ struct KParams {
   uint8_t* ctr;        // centre bytes when vox_inf > 0
   uint8_t* rowflag;    // [dy*dz] per slot: == epoch when the x-row holds a centre (vox_inf > 0)
   uint32_t* dbits;     // x-dilated centre bit rows [dy*dz][row words] (vox_inf > 0)
-  uint32_t* key;
+  void* key;           // KeyFmt<key_bits>::T per cell
+  int key_bits;        // 16 or 32
   uint8_t* loc0;
   uint8_t* loc1;
   Counters* counters;
   CountersHead* counters_out;  // host-mapped read-back (K5)
   const FrameParams* frames;
 };
+
+// This slot's key array (byte address).
+__host__ __device__ __forceinline__ char* key_slot(const KParams& p, long long slot) {
+  return static_cast<char*>(p.key) + slot * p.n * (p.key_bits >> 3);
+}
+
+// Occupied key at cell idx (populate / dilation; the width is a run-time,
+// launch-uniform choice there).
+__device__ __forceinline__ void store_occupied_key(char* key, uint32_t idx, int bits) {
+  if (bits == 16)
+    reinterpret_cast<uint16_t*>(key)[idx] = static_cast<uint16_t>(KeyFmt<16>::kOccupied);
+  else
+    reinterpret_cast<uint32_t*>(key)[idx] = KeyFmt<32>::kOccupied;
+}
+
+// Four consecutive cells' keys in one vector access (the merge kernels):
+// their measurement states as bytes (0..3), whether any was touched this
+// frame, and the all-Unknown pattern written back over touched ones.
+template <int kBits>
+struct Keys4;
+
+template <>
+struct Keys4<16> {
+  using V = uint2;
+  static constexpr int kBytes = 8;
+  static __device__ __forceinline__ V load_cs(const void* p) { return __ldcs(reinterpret_cast<const uint2*>(p)); }
+  static __device__ __forceinline__ V load(const void* p) { return *reinterpret_cast<const uint2*>(p); }
+  static __device__ __forceinline__ V unknown() { return make_uint2(0xFF80FF80u, 0xFF80FF80u); }
+  static __device__ __forceinline__ void clear(void* p) { *reinterpret_cast<uint2*>(p) = unknown(); }
+  static __device__ __forceinline__ bool touched(V k) { return ((k.x ^ 0xFF80FF80u) | (k.y ^ 0xFF80FF80u)) != 0u; }
+  // two cells (halves of w) -> states in the low byte of each half
+  static __device__ __forceinline__ uint32_t states2(uint32_t w) {
+    const uint32_t unk = __vcmpeq2(w, 0xFF80FF80u);
+    const uint32_t occ = __vcmpeq2(w, 0x7F807F80u);
+    const uint32_t st = ((w & 0x00010001u) << 1) | 0x00010001u;  // 1 or 3: bit 0 is the traced bit
+    return ((st & ~occ) | (0x00020002u & occ)) & ~unk;
+  }
+  static __device__ __forceinline__ uint32_t states(V k) { return __byte_perm(states2(k.x), states2(k.y), 0x6420); }
+};
+
+template <>
+struct Keys4<32> {
+  using V = uint4;
+  static constexpr int kBytes = 16;
+  static __device__ __forceinline__ V load_cs(const void* p) { return __ldcs(reinterpret_cast<const uint4*>(p)); }
+  static __device__ __forceinline__ V load(const void* p) { return *reinterpret_cast<const uint4*>(p); }
+  static __device__ __forceinline__ V unknown() { return make_uint4(0u, 0u, 0u, 0u); }
+  static __device__ __forceinline__ void clear(void* p) { *reinterpret_cast<uint4*>(p) = unknown(); }
+  static __device__ __forceinline__ bool touched(V k) { return (k.x | k.y | k.z | k.w) != 0u; }
+  static __device__ __forceinline__ uint32_t state1(uint32_t k) {
+    return k == 0u ? 0u : (k == 0xFFFFFFFFu ? 2u : 1u + 2u * (k & 1u));
+  }
+  static __device__ __forceinline__ uint32_t states(V k) {
+    return state1(k.x) | (state1(k.y) << 8) | (state1(k.z) << 16) | (state1(k.w) << 24);
+  }
+};
+
+// merge of 4 packed cells: local l4 and measurement states m4 (bytes 0..3,
+// so "== 0" and "== 3" are two-bit tests): merge_cell per byte.
+__device__ __forceinline__ uint32_t merge4s(uint32_t l4, uint32_t m4) {
+  const uint32_t keep = (((m4 | (m4 >> 1)) & 0x01010101u) ^ 0x01010101u) * 0xffu;  // m == 0
+  const uint32_t clear = (m4 & (m4 >> 1) & 0x01010101u) * 0xffu;                   // m == 3
+  return (l4 & keep) | (m4 & ~(keep | clear));
+}
 
 // ---------------------------------------------------------------------------
 // fp64 helpers, each a single IEEE-rounded operation.

@@ -24,7 +24,7 @@ namespace vxm {
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ unsigned populate_point(const KParams& p, const double* R,
                                                    const double* t, uint8_t* target,
-                                                   uint8_t* rowflag, uint8_t mark, double x,
+                                                   uint8_t* rowflag, char* keys, uint8_t mark, double x,
                                                    double y, double z) {
   int c[3];
   transform_voxelize(R, t, x, y, z, p.vs, p.inv_vs, c);
@@ -36,8 +36,12 @@ __device__ __forceinline__ unsigned populate_point(const KParams& p, const doubl
   const uint32_t idx = static_cast<uint32_t>(c[0]) + static_cast<uint32_t>(c[1]) * p.dx +
                        static_cast<uint32_t>(c[2]) * static_cast<uint32_t>(p.dx * p.dy);
   target[idx] = mark;  // idempotent: every writer stores the same byte
-  // the dilation only visits x-rows that hold a centre this frame
-  if (rowflag) rowflag[static_cast<uint32_t>(c[1]) + static_cast<uint32_t>(c[2]) * p.dy] = mark;
+  if (rowflag) {
+    // a centre: the dilation only visits x-rows that hold one this frame
+    rowflag[static_cast<uint32_t>(c[1]) + static_cast<uint32_t>(c[2]) * p.dy] = mark;
+  } else {
+    store_occupied_key(keys, idx, p.key_bits);  // vox_inf == 0: the cell itself is Occupied
+  }
   return 0u;
 }
 
@@ -61,6 +65,7 @@ __global__ void __launch_bounds__(256) populate_depth_kernel(KParams p, int iter
   const uint8_t mark = static_cast<uint8_t>(fp->epoch);
   uint8_t* target = (p.vox_inf > 0 ? p.ctr : p.occ) + static_cast<long long>(s) * p.n;
   uint8_t* rowflag = p.vox_inf > 0 ? p.rowflag + static_cast<long long>(s) * p.dy * p.dz : nullptr;
+  char* const keys = key_slot(p, s);
   double R[9], t[3];
 #pragma unroll
   for (int i = 0; i < 9; ++i) R[i] = fp->rot[i];
@@ -89,7 +94,7 @@ __global__ void __launch_bounds__(256) populate_depth_kernel(KParams p, int iter
       const double D = static_cast<double>(d[k]);
       if (D > p.max_depth) continue;
       ++total;
-      outside += populate_point(p, R, t, target, rowflag, mark, dmul(__ldg(p.qx + u), D),
+      outside += populate_point(p, R, t, target, rowflag, keys, mark, dmul(__ldg(p.qx + u), D),
                                 dmul(__ldg(p.qy + v), D), D);
     }
     first = nfirst;
@@ -120,6 +125,7 @@ __global__ void __launch_bounds__(256) populate_depth_tma_kernel(KParams p, int 
   const uint8_t mark = static_cast<uint8_t>(fp->epoch);
   uint8_t* target = (p.vox_inf > 0 ? p.ctr : p.occ) + static_cast<long long>(s) * p.n;
   uint8_t* rowflag = p.vox_inf > 0 ? p.rowflag + static_cast<long long>(s) * p.dy * p.dz : nullptr;
+  char* const keys = key_slot(p, s);
   const float* depth = fp->depth;
   const int nq = (p.W * p.H) >> 2;
   const int T = blockDim.x;
@@ -192,7 +198,7 @@ __global__ void __launch_bounds__(256) populate_depth_tma_kernel(KParams p, int 
     v += (v + 1) * p.W <= pix ? 1 : 0;
     const int u = pix - v * p.W;
     const double D = static_cast<double>(spx[off]);
-    outside += populate_point(p, R, t, target, rowflag, mark, dmul(__ldg(p.qx + u), D),
+    outside += populate_point(p, R, t, target, rowflag, keys, mark, dmul(__ldg(p.qx + u), D),
                               dmul(__ldg(p.qy + v), D), D);
   }
   } else {
@@ -221,7 +227,7 @@ __global__ void __launch_bounds__(256) populate_depth_tma_kernel(KParams p, int 
       const double D = static_cast<double>(d[k]);
       if (D > p.max_depth) continue;
       ++total;
-      outside += populate_point(p, R, t, target, rowflag, mark, dmul(__ldg(p.qx + u), D),
+      outside += populate_point(p, R, t, target, rowflag, keys, mark, dmul(__ldg(p.qx + u), D),
                                 dmul(__ldg(p.qy + v), D), D);
     }
   }
@@ -241,6 +247,7 @@ __global__ void __launch_bounds__(256) populate_cloud_kernel(KParams p) {
   const uint8_t mark = static_cast<uint8_t>(fp->epoch);
   uint8_t* target = (p.vox_inf > 0 ? p.ctr : p.occ) + static_cast<long long>(s) * p.n;
   uint8_t* rowflag = p.vox_inf > 0 ? p.rowflag + static_cast<long long>(s) * p.dy * p.dz : nullptr;
+  char* const keys = key_slot(p, s);
   double R[9], t[3];
 #pragma unroll
   for (int i = 0; i < 9; ++i) R[i] = fp->rot[i];
@@ -254,7 +261,7 @@ __global__ void __launch_bounds__(256) populate_cloud_kernel(KParams p) {
     const double x = xs[i], y = ys[i], z = zs[i];
     if (!(isfinite(x) && isfinite(y) && isfinite(z))) continue;
     ++total;
-    outside += populate_point(p, R, t, target, rowflag, mark, x, y, z);
+    outside += populate_point(p, R, t, target, rowflag, keys, mark, x, y, z);
   }
   unsigned vals[2] = {total, outside};
   unsigned long long* dst[2] = {&p.counters[s].points_total, &p.counters[s].points_outside};
@@ -419,6 +426,7 @@ __global__ void __launch_bounds__(256) dilate_tiles_kernel(KParams p, int r_rt) 
   const int s = blockIdx.z;
   const uint32_t e = p.frames[s].epoch;
   uint8_t* occ = p.occ + static_cast<long long>(s) * p.n;
+  char* const keys = key_slot(p, s);
   const int W = (p.dx + 31) >> 5;
   const int WP = dilate_row_words(p.dx);
   const int lg = __ffs(WP) - 1;
@@ -530,6 +538,17 @@ __global__ void __launch_bounds__(256) dilate_tiles_kernel(KParams p, int r_rt) 
         if (nib) {
           const uint32_t m = ((nib * 0x00204081u) & 0x01010101u) * 0xFFu;  // 0xFF per set bit
           *reinterpret_cast<uint32_t*>(dst + x0) = e * 0x01010101u & m;
+          // the 4 cells' keys: Occupied where set, Unknown (as every key is
+          // before the trace) elsewhere
+          const uint32_t cell = static_cast<uint32_t>(gy) * p.dx + static_cast<uint32_t>(gz) * dxy + x0;
+          if (p.key_bits == 16) {
+            *reinterpret_cast<uint2*>(keys + 2ull * cell) =
+                make_uint2(0xFF80FF80u ^ ((nib & 1u) << 15) ^ ((nib & 2u) << 30),
+                           0xFF80FF80u ^ ((nib & 4u) << 13) ^ ((nib & 8u) << 28));
+          } else {
+            *reinterpret_cast<uint4*>(keys + 4ull * cell) =
+                make_uint4(0u - (nib & 1u), 0u - ((nib >> 1) & 1u), 0u - ((nib >> 2) & 1u), 0u - (nib >> 3));
+          }
         }
       }
       continue;
@@ -543,7 +562,10 @@ __global__ void __launch_bounds__(256) dilate_tiles_kernel(KParams p, int r_rt) 
         d |= col[(k * kDilT) << lg];
       }
       const int x = (w << 5) + lane;
-      if (x < p.dx && ((d >> lane) & 1u)) dst[x] = static_cast<uint8_t>(e);
+      if (x < p.dx && ((d >> lane) & 1u)) {
+        dst[x] = static_cast<uint8_t>(e);
+        store_occupied_key(keys, static_cast<uint32_t>(gy) * p.dx + static_cast<uint32_t>(gz) * dxy + x, p.key_bits);
+      }
     }
   }
 }
@@ -638,6 +660,21 @@ inline cudaError_t dilate_set_smem(int bytes) {
 
 constexpr int kTraceSlots = 32;
 
+// Max-reduction of key value kv into cell `cell` (fire and forget). 16-bit
+// keys: the packed-bf16 reduction on the aligned cell pair, the other half
+// given -inf (the neutral element); see KeyFmt.
+template <int kBits>
+__device__ __forceinline__ void red_max_key(char* key, uint32_t cell, uint32_t kv) {
+  if constexpr (kBits == 16) {
+    const uint32_t w = (cell & 1u) ? ((kv << 16) | 0xFF80u) : (0xFF800000u | kv);
+    asm volatile("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %1;\n\t"
+                 "red.relaxed.gpu.global.max.noftz.v2.bf16 [%0], {lo, hi};\n\t}"
+                 ::"l"(key + 2ull * (cell & ~1u)), "r"(w) : "memory");
+  } else {
+    asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(key + 4ull * cell), "r"(kv) : "memory");
+  }
+}
+
 struct RayState {
   int cur[3];
   int step[3];
@@ -693,12 +730,12 @@ __device__ __forceinline__ void ray_setup(const double* R, const double* start, 
 // few spilled values; 4-7% faster than one warp per block at 64 registers),
 // a lone frame (358 warps, GPU far from full) runs 8-step chunks at 64
 // registers, where per-warp latency decides.
-template <int kChunk, int kTraceWarps, int kMinBlocks, bool kMatch, bool kFast, bool kSplit>
+template <int kBits, int kChunk, int kTraceWarps, int kMinBlocks, bool kMatch, bool kFast, bool kSplit>
 __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_kernel(KParams p) {
   const int s = blockIdx.y;
   const FrameParams* fp = p.frames + s;
   const uint32_t epoch = fp->epoch;
-  uint32_t* const key = fp->key_s;
+  char* const key = static_cast<char*>(fp->key_s);
   const uint8_t* const occ = fp->occ_s;
   double R[9], start[3];
 #pragma unroll
@@ -717,7 +754,7 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   const int yi_idx = ty * (kSplit ? 2 : 4) + (rl >> 3);
   const bool active = ty < (kSplit ? (p.vh + 1) / 2 : p.tiles_y) && xi_idx < p.vw && yi_idx < p.vh;
   const uint32_t ray = static_cast<uint32_t>(yi_idx) * p.vw + xi_idx;  // row-major, y outer
-  const uint32_t ray_key = key_tag(epoch) | ((ray + 1u) << 1);
+  const uint32_t ray_key = KeyFmt<kBits>::ray_base(ray);  // | 1: UnknownTraced
 
   RayState st;
   ray_setup(R, start, p.vs, p.ray_vs, xi_idx - (p.vw - 1) / 2, yi_idx - (p.vh - 1) / 2, p.vd, st);
@@ -796,19 +833,35 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
     for (int j = 0; j < kChunk; ++j) {
 // the per-cell resolve: predicates io (occupied) / w (write), the counters,
 // the traced-bit state, ok = w and no higher-lane duplicate, the RED.max
-#define VXM_RESOLVE_BODY                   \
+#define VXM_RESOLVE_COUNT                  \
   "@w add.u32 %1, %1, 1;\n\t"            \
   "@w add.u32 %2, %2, %0;\n\t"           \
   "or.b32 kv, %6, %0;\n\t"               \
   "selp.u32 %0, 1, %0, io;\n\t"          \
-  "setp.eq.and.u32 ok, %8, 0, w;\n\t"    \
+  "setp.eq.and.u32 ok, %8, 0, w;\n\t"
+// 32-bit keys: RED.max.u32 on the cell
+#define VXM_RESOLVE_RED32                  \
   "mul.wide.u32 a, %3, 4;\n\t"           \
   "add.u64 a, a, %7;\n\t"                \
   "@ok red.relaxed.gpu.global.max.u32 [a], kv;\n\t"
+// 16-bit keys: the value placed in the cell's half of its aligned pair (the
+// other half -inf, 0xFF80), RED.max.bf16x2 on the pair (see red_max_key)
+#define VXM_RESOLVE_RED16                  \
+  "and.b32 ca, %3, 1;\n\t"               \
+  "setp.ne.u32 po, ca, 0;\n\t"           \
+  "selp.b32 ca, 0x5410, 0x1054, po;\n\t" \
+  "prmt.b32 kv, nf, kv, ca;\n\t"         \
+  "mov.b32 {lo, hi}, kv;\n\t"            \
+  "and.b32 ca, %3, -2;\n\t"              \
+  "mul.wide.u32 a, ca, 2;\n\t"           \
+  "add.u64 a, a, %7;\n\t"                \
+  "@ok red.relaxed.gpu.global.max.noftz.v2.bf16 [a], {lo, hi};\n\t"
 #define VXM_RESOLVE_DECL                   \
-  ".reg .pred v, io, w, ok;\n\t"         \
-  ".reg .b32 kv;\n\t"                    \
-  ".reg .b64 a;\n\t"
+  ".reg .pred v, io, w, ok, po;\n\t"     \
+  ".reg .b32 kv, ca, nf;\n\t"            \
+  ".reg .b16 lo, hi;\n\t"                \
+  ".reg .b64 a;\n\t"                     \
+  "mov.b32 nf, 0xFF80;\n\t"
 // kTail: the cell is valid or the ray has ended (o == epoch: no write)
 #define VXM_RESOLVE_HEAD_TAIL "setp.eq.u32 io|w, %4, %5;\n\t"
 // otherwise invalid cells (0xffffffff) may also precede the grid entry
@@ -816,16 +869,31 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   "setp.ne.u32 v, %3, -1;\n\t"            \
   "setp.eq.and.u32 io, %4, %5, v;\n\t"    \
   "setp.ne.and.u32 w, %4, %5, v;\n\t"
+#define VXM_RESOLVE_BODY VXM_RESOLVE_COUNT VXM_RESOLVE_RED_K
 #define VXM_RESOLVE_ASM(HEAD)                                                                 \
   asm volatile("{\n\t" VXM_RESOLVE_DECL HEAD VXM_RESOLVE_BODY "}"                            \
                : "+r"(traced_bit), "+r"(lw), "+r"(lt)                                         \
                : "r"(cell[j]), "r"(o[j]), "r"(epoch), "r"(ray_key), "l"(key_base), "r"(dup[j]) \
                : "memory")
-      if constexpr (kTail)
-        VXM_RESOLVE_ASM(VXM_RESOLVE_HEAD_TAIL);
-      else
-        VXM_RESOLVE_ASM(VXM_RESOLVE_HEAD_ANY);
+      if constexpr (kBits == 16) {
+#define VXM_RESOLVE_RED_K VXM_RESOLVE_RED16
+        if constexpr (kTail)
+          VXM_RESOLVE_ASM(VXM_RESOLVE_HEAD_TAIL);
+        else
+          VXM_RESOLVE_ASM(VXM_RESOLVE_HEAD_ANY);
+#undef VXM_RESOLVE_RED_K
+      } else {
+#define VXM_RESOLVE_RED_K VXM_RESOLVE_RED32
+        if constexpr (kTail)
+          VXM_RESOLVE_ASM(VXM_RESOLVE_HEAD_TAIL);
+        else
+          VXM_RESOLVE_ASM(VXM_RESOLVE_HEAD_ANY);
+#undef VXM_RESOLVE_RED_K
+      }
 #undef VXM_RESOLVE_ASM
+#undef VXM_RESOLVE_COUNT
+#undef VXM_RESOLVE_RED32
+#undef VXM_RESOLVE_RED16
 #undef VXM_RESOLVE_HEAD_ANY
 #undef VXM_RESOLVE_HEAD_TAIL
 #undef VXM_RESOLVE_DECL
@@ -996,7 +1064,7 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
         uint32_t u = fidx;
         const uint32_t kv = ray_key | 1u;
         for (; n > 0; --n) {
-          atomicMax(key + u, kv);
+          red_max_key<kBits>(key, u, kv);
           const bool bx = a0 <= a1 && a0 <= a2;
           const bool by = !bx && a1 <= a2;
           if (bx) { a0 = dadd(a0, e0); u += lin0; }
@@ -1065,21 +1133,30 @@ constexpr long long kSplitMaxRays = 32768;
 
 // `batch` is the number of slots of the whole call (graph branches launch
 // shares of it concurrently, so the GPU is as full as the total says).
-inline void launch_trace(const KParams& kp, int slots, int batch, cudaStream_t st) {
+template <int kBits>
+inline void launch_trace_k(const KParams& kp, int slots, int batch, cudaStream_t st) {
   const int tiles = kp.tiles_x * kp.tiles_y;
   if (batch >= 8) {
-    launch_pdl(trace_bundle_kernel<4, 2, VXM_TB_MINB, true, false, false>, dim3((tiles + 1) / 2, slots), dim3(64), 0, st, kp);
+    launch_pdl(trace_bundle_kernel<kBits, 4, 2, VXM_TB_MINB, true, false, false>, dim3((tiles + 1) / 2, slots),
+               dim3(64), 0, st, kp);
   } else {
     if (static_cast<long long>(kp.vw) * kp.vh * batch <= kSplitMaxRays) {
       // few rays (the GPU far from full): 8x2 tiles, each ray walked as two
       // halves by two lanes; measured -12% / -7% K3 time for a lone cfg2 /
       // cfg1 frame, +11% for a lone cfg3 frame (76k rays)
       const int tiles2 = kp.tiles_x * ((kp.vh + 1) / 2);
-      launch_pdl(trace_bundle_kernel<8, 1, 1, false, true, true>, dim3(tiles2, slots), dim3(32), 0, st, kp);
+      launch_pdl(trace_bundle_kernel<kBits, 8, 1, 1, false, true, true>, dim3(tiles2, slots), dim3(32), 0, st, kp);
     } else {
-      launch_pdl(trace_bundle_kernel<8, 1, 1, false, true, false>, dim3(tiles, slots), dim3(32), 0, st, kp);
+      launch_pdl(trace_bundle_kernel<kBits, 8, 1, 1, false, true, false>, dim3(tiles, slots), dim3(32), 0, st, kp);
     }
   }
+}
+
+inline void launch_trace(const KParams& kp, int slots, int batch, cudaStream_t st) {
+  if (kp.key_bits == 16)
+    launch_trace_k<16>(kp, slots, batch, st);
+  else
+    launch_trace_k<32>(kp, slots, batch, st);
 }
 
 // Sums K3's per-slot counters into the stream's totals (one warp).
@@ -1114,7 +1191,7 @@ struct PerPixelAcc {
 };
 
 __device__ __forceinline__ void pp_visit(const KParams& p, const int* c, const int* end,
-                                         const uint8_t* occ, uint32_t* key, uint32_t epoch,
+                                         const uint8_t* occ, char* key, uint32_t epoch,
                                          PerPixelAcc& acc) {
   if (c[0] == end[0] && c[1] == end[1] && c[2] == end[2]) return;  // the endpoint holds the obstacle
   if (static_cast<unsigned>(c[0]) >= static_cast<unsigned>(p.dx) ||
@@ -1126,14 +1203,18 @@ __device__ __forceinline__ void pp_visit(const KParams& p, const int* c, const i
   const uint32_t idx = static_cast<uint32_t>(c[0]) + static_cast<uint32_t>(c[1]) * p.dx +
                        static_cast<uint32_t>(c[2]) * static_cast<uint32_t>(p.dx * p.dy);
   if (occ[idx] != epoch) {
-    key[idx] = key_tag(epoch) | 2u;
+    // Free (every per-pixel write stores the same lowest-priority Free key)
+    if (p.key_bits == 16)
+      reinterpret_cast<uint16_t*>(key)[idx] = static_cast<uint16_t>(KeyFmt<16>::ray_base(-1));
+    else
+      reinterpret_cast<uint32_t*>(key)[idx] = KeyFmt<32>::ray_base(-1);
     ++acc.freed;
   }
 }
 
 __device__ __forceinline__ void pp_trace_point(const KParams& p, const double* R, const double* t,
                                                const int* cam, double x, double y, double z,
-                                               const uint8_t* occ, uint32_t* key, uint32_t epoch,
+                                               const uint8_t* occ, char* key, uint32_t epoch,
                                                PerPixelAcc& acc) {
   // world_to_voxel(t_vc.apply(point)) (grid.cpp:54-62, geometry.cpp:10-15):
   // ((R p) + t) / vs, rows left to right, floor, int
@@ -1178,7 +1259,7 @@ __global__ void __launch_bounds__(256) trace_per_pixel_kernel(KParams p, int fro
   if (blockIdx.x == 0 && threadIdx.x == 0) p.counters[s].t_trace = global_ns();
   const FrameParams* fp = p.frames + s;
   const uint32_t epoch = fp->epoch;
-  uint32_t* key = p.key + static_cast<long long>(s) * p.n;
+  char* const key = key_slot(p, s);
   const uint8_t* occ = p.occ + static_cast<long long>(s) * p.n;
   double R[9], t[3];
 #pragma unroll
@@ -1248,23 +1329,6 @@ __global__ void __launch_bounds__(128) publish_counters_kernel(KParams p) {
   for (int i = threadIdx.x; i < kParts; i += blockDim.x) (&p.counters[s].trace_slots[0][0])[i] = 0ull;
 }
 
-// merge of 4 packed cells: local l4, occupancy o4 (epoch bytes), 4 keys.
-// States are 0..3 per byte, so "== 0" and "== 3" are two-bit tests.
-__device__ __forceinline__ uint32_t merge4(uint32_t l4, uint32_t o4, uint4 k4, uint32_t epoch) {
-  const uint32_t kk[4] = {k4.x, k4.y, k4.z, k4.w};
-  uint32_t m4 = 0;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint32_t v = (kk[i] >> kKeyShift) == epoch ? (1u | ((kk[i] & 1u) << 1)) : 0u;  // 1 or 3
-    m4 |= v << (8 * i);
-  }
-  const uint32_t occm = zero_bytes(o4 ^ (epoch * 0x01010101u));  // 0xff where Occupied
-  m4 = (m4 & ~occm) | (0x02020202u & occm);
-  const uint32_t keep = (((m4 | (m4 >> 1)) & 0x01010101u) ^ 0x01010101u) * 0xffu;  // m == 0
-  const uint32_t clear = (m4 & (m4 >> 1) & 0x01010101u) * 0xffu;                   // m == 3
-  return (l4 & keep) | (m4 & ~(keep | clear));
-}
-
 // number of bytes of x (states 0..3) equal to 2 / to 1
 __device__ __forceinline__ unsigned count_occupied4(uint32_t x) { return __popc((x >> 1) & ~x & 0x01010101u); }
 __device__ __forceinline__ unsigned count_free4(uint32_t x) { return __popc(x & ~(x >> 1) & 0x01010101u); }
@@ -1293,7 +1357,40 @@ __device__ __forceinline__ unsigned count_free16(const uint32_t (&x)[4]) {
   return (m * 0x01010101u) >> 24;
 }
 
+// Keys of the source cells the shifted gather never reads (their destination
+// lies outside the grid) are reset to Unknown here: x in [0, ox) for ox > 0 or
+// [dx + ox, dx) for ox < 0 (every y, z), and likewise along y and z (cells in
+// two slabs are written twice). Every other key is read, and reset if
+// touched, by the gather itself, so the slot's keys are all Unknown again.
+template <int kBits>
+__device__ __forceinline__ void clear_orphan_keys(char* key, int dx, int dy, int dz, int ox, int oy, int oz,
+                                                  long long tid, long long nthreads) {
+  using T = typename KeyFmt<kBits>::T;
+  T* const k = reinterpret_cast<T*>(key);
+  const int dims[3] = {dx, dy, dz}, off[3] = {ox, oy, oz};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const int o = off[a], d = dims[a];
+    if (o == 0) continue;
+    const int lo = o > 0 ? 0 : max(d + o, 0), hi = o > 0 ? min(o, d) : d;
+    const long long w = hi - lo;
+    // the slab as (x, y, z) with axis a restricted to [lo, hi)
+    const long long ex = a == 0 ? w : dx, ey = a == 1 ? w : dy;
+    const long long cnt = ex * ey * (a == 2 ? w : dz);
+    for (long long i = tid; i < cnt; i += nthreads) {
+      const long long x = i % ex, r = i / ex;
+      const long long y = r % ey, z = r / ey;
+      const long long cx = a == 0 ? lo + x : x, cy = a == 1 ? lo + y : y, cz = a == 2 ? lo + z : z;
+      k[cx + cy * dx + cz * static_cast<long long>(dx) * dy] = static_cast<T>(KeyFmt<kBits>::kUnknown);
+    }
+  }
+}
+
+template <int kBits>
 __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int rows_per_warp) {
+  using K4 = Keys4<kBits>;
+  using T = typename KeyFmt<kBits>::T;
+  constexpr int B = kBits / 8;  // key bytes per cell
   pdl_wait();  // K3's keys and counters
   const int s = blockIdx.y;
   if (blockIdx.x == 0 && threadIdx.x == 0) p.counters[s].t_merge = global_ns();
@@ -1302,8 +1399,7 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int r
   const uint32_t cur = fp->cur;
   const int ox = fp->off[0], oy = fp->off[1], oz = fp->off[2];
   const long long base = static_cast<long long>(s) * p.n;
-  const uint8_t* occ = p.occ + base;
-  const uint32_t* key = p.key + base;
+  char* const key = key_slot(p, s);
   const uint8_t* src = (cur ? p.loc1 : p.loc0) + base;
   uint8_t* dst = (cur ? p.loc0 : p.loc1) + base;
   const int lane = threadIdx.x & 31;
@@ -1318,8 +1414,8 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int r
   if (ox == 0 && (p.dx & 3) == 0 && p.dx >= 16 && (p.n & 15) == 0 && p.n < (1 << 24)) {
     // No x shift: destination cell c reads c + delta (delta = off_y*dx +
     // off_z*dx*dy), and the valid destination cells of a slab are one run of
-    // whole rows. A thread takes 16 consecutive cells: 16 local and occupancy
-    // bytes and 16 keys, no per-row arithmetic. A chunk spans at most two
+    // whole rows. A thread takes 16 consecutive cells: 16 local bytes and
+    // 16 keys, no per-row arithmetic. A chunk spans at most two
     // rows (dx >= 16), so it is valid throughout when its first and last
     // cells are; chunks at a run boundary test their words one by one (a
     // word never straddles a row since dx % 4 == 0).
@@ -1340,31 +1436,35 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int r
       const int sc = static_cast<int>(c) + delta;
       uint32_t out[4] = {0u, 0u, 0u, 0u};
       if (valid(c) && valid(c + 15)) {
-        uint32_t l[4], o[4];
+        uint32_t l[4];
         if (aligned) {
           const uint4 L = __ldcs(reinterpret_cast<const uint4*>(src + sc));
-          const uint4 O = __ldcs(reinterpret_cast<const uint4*>(occ + sc));
           l[0] = L.x; l[1] = L.y; l[2] = L.z; l[3] = L.w;
-          o[0] = O.x; o[1] = O.y; o[2] = O.z; o[3] = O.w;
         } else {
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            l[i] = __ldcs(reinterpret_cast<const unsigned int*>(src + sc + 4 * i));
-            o[i] = __ldcs(reinterpret_cast<const unsigned int*>(occ + sc + 4 * i));
-          }
+          for (int i = 0; i < 4; ++i) l[i] = __ldcs(reinterpret_cast<const unsigned int*>(src + sc + 4 * i));
         }
-        uint4 k[4];
+        typename K4::V k[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) k[i] = __ldcs(reinterpret_cast<const uint4*>(key + sc + 4 * i));
+        for (int i = 0; i < 4; ++i) k[i] = K4::load_cs(key + B * (sc + 4 * i));
+        bool any = false;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) out[i] = merge4(l[i], o[i], k[i], epoch);
+        for (int i = 0; i < 4; ++i) {
+          out[i] = merge4s(l[i], K4::states(k[i]));
+          any = any || K4::touched(k[i]);
+        }
+        if (any) {  // this frame wrote some of them: back to Unknown for the next
+#pragma unroll
+          for (int i = 0; i < 4; ++i) K4::clear(key + B * (sc + 4 * i));
+        }
       } else {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           if (valid(c + 4 * i)) {
             const int si = sc + 4 * i;
-            out[i] = merge4(*reinterpret_cast<const uint32_t*>(src + si), *reinterpret_cast<const uint32_t*>(occ + si),
-                            *reinterpret_cast<const uint4*>(key + si), epoch);
+            const typename K4::V k = K4::load(key + B * si);
+            out[i] = merge4s(*reinterpret_cast<const uint32_t*>(src + si), K4::states(k));
+            if (K4::touched(k)) K4::clear(key + B * si);
           }
         }
       }
@@ -1378,8 +1478,9 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int r
     // warp's rows before resolving any, so each lane keeps kRowsPerWarp x 24 B
     // in flight (the kernel is HBM-latency bound otherwise).
     const int x0 = lane * 4, sx = x0 + ox;
-    uint32_t l4[kRowsPerWarp], o4[kRowsPerWarp], drow[kRowsPerWarp];
-    uint4 k4[kRowsPerWarp];
+    uint32_t l4[kRowsPerWarp], drow[kRowsPerWarp];
+    long long scell[kRowsPerWarp];
+    typename K4::V k4[kRowsPerWarp];
     bool ok[kRowsPerWarp], in_row[kRowsPerWarp];
 #pragma unroll
     for (int rr = 0; rr < kRowsPerWarp; ++rr) {
@@ -1391,18 +1492,19 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int r
       ok[rr] = in_row[rr] && sy >= 0 && sy < p.dy && sz >= 0 && sz < p.dz && sx >= 0 && sx < p.dx;
       drow[rr] = static_cast<uint32_t>(y) * p.dx + static_cast<uint32_t>(z) * dxy;
       const long long sc = static_cast<long long>(sy) * p.dx + static_cast<long long>(sz) * dxy + sx;
-      l4[rr] = o4[rr] = 0u;
-      k4[rr] = make_uint4(0u, 0u, 0u, 0u);
+      scell[rr] = sc;
+      l4[rr] = 0u;
+      k4[rr] = K4::unknown();
       if (ok[rr]) {
         l4[rr] = __ldcs(reinterpret_cast<const unsigned int*>(src + sc));
-        o4[rr] = __ldcs(reinterpret_cast<const unsigned int*>(occ + sc));
-        k4[rr] = __ldcs(reinterpret_cast<const uint4*>(key + sc));
+        k4[rr] = K4::load_cs(key + B * sc);
       }
     }
 #pragma unroll
     for (int rr = 0; rr < kRowsPerWarp; ++rr) {
       if (!in_row[rr]) continue;
-      const uint32_t out = ok[rr] ? merge4(l4[rr], o4[rr], k4[rr], epoch) : 0u;
+      const uint32_t out = ok[rr] ? merge4s(l4[rr], K4::states(k4[rr])) : 0u;
+      if (ok[rr] && K4::touched(k4[rr])) K4::clear(key + B * scell[rr]);
       occ_n += count_occupied4(out);
       free_n += count_free4(out);
       *reinterpret_cast<uint32_t*>(dst + drow[rr] + x0) = out;
@@ -1423,8 +1525,9 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int r
         uint32_t out = 0;
         if (row_ok && sx >= 0 && sx < p.dx) {
           const long long sc = srow + sx;
-          out = merge4(*reinterpret_cast<const uint32_t*>(src + sc), *reinterpret_cast<const uint32_t*>(occ + sc),
-                       *reinterpret_cast<const uint4*>(key + sc), epoch);
+          const typename K4::V k = K4::load(key + B * sc);
+          out = merge4s(*reinterpret_cast<const uint32_t*>(src + sc), K4::states(k));
+          if (K4::touched(k)) K4::clear(key + B * sc);
         }
         occ_n += count_occupied4(out);
         free_n += count_free4(out);
@@ -1437,7 +1540,10 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int r
           uint32_t v = 0;
           if (row_ok && sx >= 0 && sx < p.dx) {
             const long long sc = srow + sx;
-            v = merge_cell(src[sc], decode_cell(occ[sc], key[sc], epoch));
+            T* const kc = reinterpret_cast<T*>(key) + sc;
+            const uint32_t k = *kc;
+            v = merge_cell(src[sc], decode_key<kBits>(k));
+            if (k != KeyFmt<kBits>::kUnknown) *kc = static_cast<T>(KeyFmt<kBits>::kUnknown);
           }
           occ_n += v == 2u;
           free_n += v == 1u;
@@ -1446,6 +1552,9 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int r
       }
     }
   }
+  clear_orphan_keys<kBits>(key, p.dx, p.dy, p.dz, ox, oy, oz,
+                           static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x,
+                           static_cast<long long>(gridDim.x) * blockDim.x);
   unsigned vals[2] = {occ_n, free_n};
   unsigned long long* dsts[2] = {&p.counters[s].occupied, &p.counters[s].freed};
   block_accumulate<2>(vals, dsts);  // ends after every warp's work (a block barrier)
@@ -1454,14 +1563,15 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int r
 
 
 // K4, TMA-staged: a group is merge_tma_rows(dx, dy) consecutive x-rows of
-// one z-slab (about kMergeStageCells cells, so one stage is ~19 KB whatever
+// one z-slab (about kMergeStageCells cells, so one stage is ~16 KB whatever
 // the row length); each block pipelines several groups through two stages.
 // The source rows these come from after the shift (rows y + off_y of slab
 // z + off_z) are contiguous in memory, so one elected thread stages them with
-// three bulk copies (local bytes, occupancy bytes, keys; each window widened
-// to 16-byte boundaries) on one mbarrier, and the warps merge, shift and
-// count out of shared memory: 4 cells per lane as one word when dims_x and
-// the x shift are multiples of 4, else cell by cell. Needs 16 bytes of slack
+// two bulk copies (local bytes and keys; each window widened to 16-byte
+// boundaries) on one mbarrier, and the warps merge, shift and count out of
+// shared memory: 4 cells per lane as one word when dims_x and the x shift are
+// multiples of 4, else cell by cell. Keys the frame touched are reset to
+// Unknown in global memory as they are consumed. Needs 16 bytes of slack
 // after each array (allocated by the runtime).
 constexpr int kMergeStageCells = 3200;
 constexpr int kMergeTmaMaxDx = 1024;  // larger rows take the direct-load K4
@@ -1469,12 +1579,12 @@ constexpr int kMergeTmaMaxDx = 1024;  // larger rows take the direct-load K4
 __host__ __device__ constexpr int merge_tma_rows(int dx, int dy) {
   return kMergeStageCells / dx < 1 ? 1 : (kMergeStageCells / dx < dy ? kMergeStageCells / dx : dy);
 }
-// one stage: local and occupancy bytes and keys of `cells` cells, each window
-// widened to 16-byte boundaries
-__host__ __device__ constexpr size_t merge_tma_smem_bytes(int cells) {
-  // rounded to 16 bytes: the second stage starts right after the first and
-  // bulk copies need 16-byte aligned destinations
-  return (2 * (static_cast<size_t>(cells) + 32) + 4 * static_cast<size_t>(cells) + 32 + 15) & ~static_cast<size_t>(15);
+// one stage: local bytes and keys (kb bytes each) of `cells` cells, each
+// window widened to 16-byte boundaries, rounded to 16 bytes (the second stage
+// starts right after the first and bulk copies need 16-byte aligned
+// destinations)
+__host__ __device__ constexpr size_t merge_tma_smem_bytes(int cells, int kb = 4) {
+  return (static_cast<size_t>(cells) + 32 + static_cast<size_t>(kb) * cells + 32 + 15) & ~static_cast<size_t>(15);
 }
 
 __device__ __forceinline__ const unsigned char* align16_down(const void* p) {
@@ -1484,7 +1594,11 @@ __device__ __forceinline__ const unsigned char* align16_up(const void* p) {
   return reinterpret_cast<const unsigned char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~static_cast<uintptr_t>(15));
 }
 
+template <int kBits>
 __global__ void __launch_bounds__(256) merge_shift_count_tma_kernel(KParams p) {
+  using K4 = Keys4<kBits>;
+  using T = typename KeyFmt<kBits>::T;
+  constexpr int B = kBits / 8;
   extern __shared__ __align__(16) unsigned char msm[];
   __shared__ uint64_t bar[2];
   const int s = blockIdx.y;
@@ -1492,17 +1606,15 @@ __global__ void __launch_bounds__(256) merge_shift_count_tma_kernel(KParams p) {
   const int dx = p.dx, dy = p.dy, dz = p.dz;
   const long long dxy = static_cast<long long>(dx) * dy;
   const int ox = fp->off[0], oy = fp->off[1], oz = fp->off[2];
-  const uint32_t epoch = fp->epoch;
   const uint32_t cur = fp->cur;
   const long long base = static_cast<long long>(s) * p.n;
   const uint8_t* src = (cur ? p.loc1 : p.loc0) + base;
   uint8_t* dst = (cur ? p.loc0 : p.loc1) + base;
-  const uint8_t* occ = p.occ + base;
-  const uint32_t* key = p.key + base;
+  char* const key = key_slot(p, s);
   const int rows = merge_tma_rows(dx, dy);
   const int ngy = (dy + rows - 1) / rows;
   const int ngroups = ngy * dz;
-  const size_t stage_bytes = merge_tma_smem_bytes(rows * dx);
+  const size_t stage_bytes = merge_tma_smem_bytes(rows * dx, B);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool vec = ((dx | ox) & 3) == 0;
 
@@ -1530,22 +1642,18 @@ __global__ void __launch_bounds__(256) merge_shift_count_tma_kernel(KParams p) {
   auto issue = [&](int g, int b) {
     const Group G = group(g);
     unsigned char* sl = msm + b * stage_bytes;
-    uint32_t lb = 0, ob = 0, kb = 0;
-    const unsigned char *lw0 = nullptr, *ow0 = nullptr, *kw0 = nullptr;
+    uint32_t lb = 0, kb = 0;
+    const unsigned char *lw0 = nullptr, *kw0 = nullptr;
     if (G.any) {
       lw0 = align16_down(src + G.c0);
-      ow0 = align16_down(occ + G.c0);
-      kw0 = align16_down(key + G.c0);
+      kw0 = align16_down(key + B * G.c0);
       lb = static_cast<uint32_t>(align16_up(src + G.c1) - lw0);
-      ob = static_cast<uint32_t>(align16_up(occ + G.c1) - ow0);
-      kb = static_cast<uint32_t>(align16_up(key + G.c1) - kw0);
+      kb = static_cast<uint32_t>(align16_up(key + B * G.c1) - kw0);
     }
-    mbar_expect_tx(&bar[b], lb + ob + kb);
+    mbar_expect_tx(&bar[b], lb + kb);
     if (G.any) {
-      unsigned char* so = sl + ((lb + 15u) & ~15u);
-      unsigned char* sk = so + ((ob + 15u) & ~15u);
+      unsigned char* sk = sl + ((lb + 15u) & ~15u);
       bulk_g2s(sl, lw0, lb, &bar[b]);
-      bulk_g2s(so, ow0, ob, &bar[b]);
       bulk_g2s(sk, kw0, kb, &bar[b]);
     }
   };
@@ -1570,20 +1678,17 @@ __global__ void __launch_bounds__(256) merge_shift_count_tma_kernel(KParams p) {
     mbar_wait(&bar[b], (it >> 1) & 1);
     const Group G = group(g);
     const unsigned char* sl = msm + b * stage_bytes;
-    int ll = 0, ol = 0, kl = 0;
-    const unsigned char *so = sl, *sk = sl;
+    int ll = 0, kl = 0;
+    const unsigned char* sk = sl;
     if (G.any) {
       const unsigned char* lw0 = align16_down(src + G.c0);
-      const unsigned char* ow0 = align16_down(occ + G.c0);
-      const unsigned char* kw0 = align16_down(key + G.c0);
+      const unsigned char* kw0 = align16_down(key + B * G.c0);
       const uint32_t lb = static_cast<uint32_t>(align16_up(src + G.c1) - lw0);
-      const uint32_t ob = static_cast<uint32_t>(align16_up(occ + G.c1) - ow0);
-      so = sl + ((lb + 15u) & ~15u);
-      sk = so + ((ob + 15u) & ~15u);
+      sk = sl + ((lb + 15u) & ~15u);
       ll = static_cast<int>((src + G.c0) - lw0);
-      ol = static_cast<int>((occ + G.c0) - ow0);
-      kl = static_cast<int>(reinterpret_cast<const unsigned char*>(key + G.c0) - kw0);
+      kl = static_cast<int>(reinterpret_cast<const unsigned char*>(key + B * G.c0) - kw0);
     }
+    char* const kg = key + B * G.c0;  // the group's keys in global memory (reset there)
     for (int r = warp; r < G.ny; r += blockDim.x >> 5) {
       const int y = G.y0 + r, sy = y + oy;
       const bool row_ok = G.any && sy >= G.sy_lo && sy < G.sy_hi;
@@ -1595,23 +1700,25 @@ __global__ void __launch_bounds__(256) merge_shift_count_tma_kernel(KParams p) {
           const int sx = x0 + ox;
           if (row_ok && sx >= 0 && sx < dx) {
             const long long rel = rrow + sx;
-            out = merge4(*reinterpret_cast<const uint32_t*>(sl + ll + rel),
-                         *reinterpret_cast<const uint32_t*>(so + ol + rel),
-                         *reinterpret_cast<const uint4*>(sk + kl + 4 * rel), epoch);
+            const typename K4::V k = K4::load(sk + kl + B * rel);
+            out = merge4s(*reinterpret_cast<const uint32_t*>(sl + ll + rel), K4::states(k));
+            if (K4::touched(k)) K4::clear(kg + B * rel);
           }
           *reinterpret_cast<uint32_t*>(drow + x0) = out;
         } else {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int x = x0 + k, sx = x + ox;
+          for (int q = 0; q < 4; ++q) {
+            const int x = x0 + q, sx = x + ox;
             if (x >= dx) break;
             uint32_t v = 0;
             if (row_ok && sx >= 0 && sx < dx) {
               const long long rel = rrow + sx;
-              v = merge_cell(sl[ll + rel],
-                             decode_cell(so[ol + rel], *reinterpret_cast<const uint32_t*>(sk + kl + 4 * rel), epoch));
+              const uint32_t k = *reinterpret_cast<const T*>(sk + kl + B * rel);
+              v = merge_cell(sl[ll + rel], decode_key<kBits>(k));
+              if (k != KeyFmt<kBits>::kUnknown)
+                *reinterpret_cast<T*>(kg + B * rel) = static_cast<T>(KeyFmt<kBits>::kUnknown);
             }
-            out |= v << (8 * k);
+            out |= v << (8 * q);
             drow[x] = static_cast<uint8_t>(v);
           }
         }
@@ -1621,6 +1728,9 @@ __global__ void __launch_bounds__(256) merge_shift_count_tma_kernel(KParams p) {
     }
     __syncthreads();  // stage b is refilled two groups from now
   }
+  clear_orphan_keys<kBits>(key, dx, dy, dz, ox, oy, oz, static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x,
+                           static_cast<long long>(gridDim.x) * blockDim.x);
+  __syncthreads();
   // every warp has passed the last group's barrier
   if (threadIdx.x == 0) atomicMax(&p.counters[s].t_end, global_ns());
   unsigned vals[2] = {occ_n, free_n};
@@ -1668,7 +1778,11 @@ __device__ __forceinline__ void add_frame_counts(const uint32_t (&packed)[U / 2]
   }
 }
 
+template <int kBits>
 __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
+  using K4 = Keys4<kBits>;
+  using T = typename KeyFmt<kBits>::T;
+  constexpr int B = kBits / 8;
   pdl_wait();  // K3's keys and counters
   constexpr int U = 4;  // frames whose loads are issued together
   __shared__ unsigned cnt[2 * kMaxFramesPerCall];           // occupied, then freed, per frame
@@ -1709,8 +1823,10 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
   const uint32_t cur = f0->cur;
   const uint8_t* src = (cur ? p.loc1 : p.loc0) + static_cast<long long>(s) * p.n;
   uint8_t* dst = (cur ? p.loc0 : p.loc1) + static_cast<long long>(s) * p.n;
-  const uint8_t* occ0 = p.occ + static_cast<long long>(s) * F * p.n;
-  const uint32_t* key0 = p.key + static_cast<long long>(s) * F * p.n;
+  // frame k's keys at key0 + k * n * B; every key a chain meets in the grid is
+  // read (even when the cell shifts out of the grid afterwards) and reset to
+  // Unknown if touched, so all F slots end all-Unknown
+  char* const key0 = key_slot(p, static_cast<long long>(s) * F);
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   if (vec_ok) {
     // Every frame's x shift is a multiple of 4 (and dims_x too): a thread
@@ -1738,18 +1854,17 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
       for (int k0 = 0; k0 < F; k0 += U) {
         bool in_c[U];
         int pos[U];
-        uint32_t o[U];
-        uint4 kk[U];
+        typename K4::V kk[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) pos[u] = group_of(k0 + u + 1, in_c[u]);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const bool in_r = u == 0 ? in_prev : in_c[u - 1];
           const int r = u == 0 ? pos_prev : pos[u - 1];
-          const bool ld = k0 + u < F && in_c[u] && in_r;
+          const bool ld = k0 + u < F && in_r;
           const long long off = static_cast<long long>(k0 + u) * p.n + r;
-          o[u] = ld ? __ldcs(reinterpret_cast<const uint32_t*>(occ0 + off)) : 0u;
-          kk[u] = ld ? __ldcs(reinterpret_cast<const uint4*>(key0 + off)) : make_uint4(0u, 0u, 0u, 0u);
+          kk[u] = ld ? K4::load_cs(key0 + B * off) : K4::unknown();
+          if (ld && K4::touched(kk[u])) K4::clear(key0 + B * off);
         }
         // per frame: Occupied / Free counts of this thread's 4 cells (each
         // <= 4, so a warp sum fits a byte); two frames share one reduction
@@ -1759,7 +1874,7 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
           const int k = k0 + u;
           if (k >= F) break;
           const bool in_r = u == 0 ? in_prev : in_c[u - 1];
-          if (in_c[u]) val = in_r ? merge4(val, o[u], kk[u], ep[k]) : 0u;  // shifted in: Unknown
+          if (in_c[u]) val = in_r ? merge4s(val, K4::states(kk[u])) : 0u;  // shifted in: Unknown
           const unsigned oc = in_c[u] ? count_occupied4(val) : 0u, fr = in_c[u] ? count_free4(val) : 0u;
           packed[u >> 1] |= (oc | (fr << 8)) << (16 * (u & 1));
         }
@@ -1795,17 +1910,17 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
       // positions after frames k0..k0+U-1, then all their loads, then the merges
       bool in_c[U];
       int pos[U];
-      uint32_t o[U], kk[U];
+      uint32_t kk[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) pos[u] = cell_of(k0 + u + 1, in_c[u]);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const bool in_r = u == 0 ? in_prev : in_c[u - 1];
         const int r = u == 0 ? pos_prev : pos[u - 1];
-        const bool ld = k0 + u < F && in_c[u] && in_r;
-        const long long off = static_cast<long long>(k0 + u) * p.n + r;
-        o[u] = ld ? __ldcs(occ0 + off) : 0u;
-        kk[u] = ld ? __ldcs(key0 + off) : 0u;
+        const bool ld = k0 + u < F && in_r;
+        T* const kc = reinterpret_cast<T*>(key0) + static_cast<long long>(k0 + u) * p.n + r;
+        kk[u] = ld ? static_cast<uint32_t>(__ldcs(kc)) : KeyFmt<kBits>::kUnknown;
+        if (kk[u] != KeyFmt<kBits>::kUnknown) *kc = static_cast<T>(KeyFmt<kBits>::kUnknown);
       }
       uint32_t packed[U / 2] = {};
 #pragma unroll
@@ -1813,7 +1928,7 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
         const int k = k0 + u;
         if (k >= F) break;
         const bool in_r = u == 0 ? in_prev : in_c[u - 1];
-        if (in_c[u]) val = in_r ? merge_cell(val, decode_cell(o[u], kk[u], ep[k])) : 0u;  // shifted in: Unknown
+        if (in_c[u]) val = in_r ? merge_cell(val, decode_key<kBits>(kk[u])) : 0u;  // shifted in: Unknown
         const unsigned oc = in_c[u] && val == 2u ? 1u : 0u, fr = in_c[u] && val == 1u ? 1u : 0u;
         packed[u >> 1] |= (oc | (fr << 8)) << (16 * (u & 1));
       }

@@ -254,7 +254,8 @@ struct vxm_ctx {
   uint8_t* occ = nullptr;
   uint8_t* ctr = nullptr;
   uint8_t* rowflag = nullptr;  // per slot: dy*dz x-row flags (vox_inf > 0)
-  uint32_t* key = nullptr;
+  char* key = nullptr;         // measurement keys, key_bits / 8 bytes per cell (vxm_device.cuh)
+  int key_bits = 32;
   uint8_t* loc[2] = {nullptr, nullptr};
   double* qtab = nullptr;  // W column + H row back-projection factors
   uint32_t* dbits = nullptr;  // x-dilated centre bit rows (vox_inf > 0)
@@ -373,7 +374,7 @@ void launch_stages(vxm_ctx* c, bool cloud, bool capturing, int s0, int S, cudaSt
   kp.counters += s0;
   kp.counters_out += s0;
   kp.occ += n * s0;
-  kp.key += n * s0;
+  kp.key = vxm::key_slot(kp, s0);
   if (kp.ctr) kp.ctr += n * s0;
   if (kp.rowflag) kp.rowflag += c->rows * s0;
   if (kp.dbits) kp.dbits += static_cast<long long>(vxm::dilate_row_words(kp.dx)) * c->rows * s0;
@@ -451,7 +452,10 @@ void launch_merge_chain(vxm_ctx* c, const vxm::KParams& kp, int F, int streams, 
   const long long blocks = std::min<long long>((chains + kMergeThreads - 1) / kMergeThreads,
                                                std::max<long long>(1, c->nsm * 8LL / streams));
   dim3 grid(static_cast<unsigned>(std::max<long long>(1, blocks)), streams);
-  VXM_CK(vxm::launch_pdl(vxm::merge_sequence_kernel, grid, dim3(kMergeThreads), 0, st, kp, F));
+  if (kp.key_bits == 16)
+    VXM_CK(vxm::launch_pdl(vxm::merge_sequence_kernel<16>, grid, dim3(kMergeThreads), 0, st, kp, F));
+  else
+    VXM_CK(vxm::launch_pdl(vxm::merge_sequence_kernel<32>, grid, dim3(kMergeThreads), 0, st, kp, F));
   VXM_CK(cudaGetLastError());
 }
 
@@ -468,8 +472,11 @@ void launch_merge(vxm_ctx* c, const vxm::KParams& kp, int S, cudaStream_t st) {
     const long long groups = static_cast<long long>((kp.dy + rows - 1) / rows) * kp.dz;
     const long long per_slot = std::max(1LL, std::min(groups, c->nsm * 8LL / S));
     const dim3 grid(static_cast<unsigned>(per_slot), S);
-    VXM_CK(vxm::launch_pdl(vxm::merge_shift_count_tma_kernel, grid, dim3(kMergeThreads),
-                           2 * vxm::merge_tma_smem_bytes(rows * kp.dx), st, kp));
+    const size_t smem = 2 * vxm::merge_tma_smem_bytes(rows * kp.dx, kp.key_bits / 8);
+    if (kp.key_bits == 16)
+      VXM_CK(vxm::launch_pdl(vxm::merge_shift_count_tma_kernel<16>, grid, dim3(kMergeThreads), smem, st, kp));
+    else
+      VXM_CK(vxm::launch_pdl(vxm::merge_shift_count_tma_kernel<32>, grid, dim3(kMergeThreads), smem, st, kp));
   } else if (c->F == 1) {
     const long long rows = static_cast<long long>(kp.dy) * kp.dz;
     // one row per warp unless the batch fills the GPU several times over
@@ -478,7 +485,10 @@ void launch_merge(vxm_ctx* c, const vxm::KParams& kp, int S, cudaStream_t st) {
     const int rpw = static_cast<int>(std::max(1LL, std::min<long long>(vxm::kRowsPerWarp, warps / fill)));
     const int rows_per_block = kMergeThreads / 32 * rpw;
     dim3 grid(static_cast<unsigned>((rows + rows_per_block - 1) / rows_per_block), S);
-    VXM_CK(vxm::launch_pdl(vxm::merge_shift_count_kernel, grid, dim3(kMergeThreads), 0, st, kp, rpw));
+    if (kp.key_bits == 16)
+      VXM_CK(vxm::launch_pdl(vxm::merge_shift_count_kernel<16>, grid, dim3(kMergeThreads), 0, st, kp, rpw));
+    else
+      VXM_CK(vxm::launch_pdl(vxm::merge_shift_count_kernel<32>, grid, dim3(kMergeThreads), 0, st, kp, rpw));
     VXM_CK(cudaGetLastError());
   } else {
     launch_merge_chain(c, kp, c->F, S / c->F, st);
@@ -535,7 +545,7 @@ void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
         kp.counters += s0;
         kp.counters_out += s0;
         kp.occ += c->n * s0;
-        kp.key += c->n * s0;
+        kp.key = vxm::key_slot(kp, s0);
         launch_merge_chain(c, kp, s1 - s0, 1, bs);
         launch_publish(kp, s1 - s0, bs);
         if (b + 1 < B) VXM_CK(cudaEventRecord(c->chain[b], bs));
@@ -636,7 +646,7 @@ void prepare_frames(vxm_ctx* c, const vxm_pose* poses, const float* depth_dev_ba
       if (depth_dev_base) f.depth = depth_dev_base + frame_elems * slot;
       f.cur = c->cur[s] ^ static_cast<uint32_t>(range & 1);  // each chained range flips the buffers
       f.occ_s = c->occ + c->n * slot;
-      f.key_s = c->key + c->n * slot;
+      f.key_s = vxm::key_slot(c->kp, slot);
       int32_t off[3];
       const bool moved = shift_decision(c->cfg.grid, org, poses[slot].translation, off);
       for (int a = 0; a < 3; ++a) {
@@ -693,7 +703,7 @@ void clear_wrapped(vxm_ctx* c, int s0, int S, cudaStream_t st) {
     VXM_CK(cudaMemsetAsync(c->occ + c->n * slot, 0, c->n, st));
     if (c->ctr) VXM_CK(cudaMemsetAsync(c->ctr + c->n * slot, 0, c->n, st));
     if (c->rowflag) VXM_CK(cudaMemsetAsync(c->rowflag + c->rows * slot, 0, c->rows, st));
-    VXM_CK(cudaMemsetAsync(c->key + c->n * slot, 0, sizeof(uint32_t) * c->n, st));
+    // (the keys need no clearing: the merge leaves them all Unknown)
   }
 }
 
@@ -799,7 +809,7 @@ void run_frame(vxm_ctx* c, bool cloud, bool direct = false) {
       kp.counters += s0;
       kp.counters_out += s0;
       kp.occ += c->n * s0;
-      kp.key += c->n * s0;
+      kp.key = vxm::key_slot(kp, s0);
       launch_merge_chain(c, kp, s1 - s0, 1, bs);
       launch_publish(kp, s1 - s0, bs);
       VXM_CK(cudaEventRecord(c->chain[b], bs));
@@ -1068,8 +1078,10 @@ int vxm_create_multi(const vxm_config* cfg, int32_t n_streams, int32_t frames_pe
     c->rows = static_cast<long long>(g.dims[1]) * g.dims[2];
     bundle_dims(cfg->camera, cfg->depth, g.vox_size, c->bundle);
     const long long rays = static_cast<long long>(c->bundle[1]) * c->bundle[2];
-    if (rays > static_cast<long long>(vxm::kMaxRays))
-      throw InvalidArg{"ray bundle exceeds " + std::to_string(vxm::kMaxRays) + " rays"};
+    if (rays > vxm::KeyFmt<32>::kMaxRays)
+      throw InvalidArg{"ray bundle exceeds " + std::to_string(vxm::KeyFmt<32>::kMaxRays) + " rays"};
+    // 16-bit keys whenever the bundle fits them (halves the key traffic)
+    c->key_bits = rays <= vxm::KeyFmt<16>::kMaxRays && !(flags & VXM_FLAG_WIDE_KEYS) ? 16 : 32;
 
     VXM_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     for (auto& e : c->ev) VXM_CK(cudaEventCreate(&e));
@@ -1080,8 +1092,15 @@ int vxm_create_multi(const vxm_config* cfg, int32_t n_streams, int32_t frames_pe
     // widened to 16-byte boundaries
     VXM_CK(cudaMalloc(&c->occ, c->n * S + 64));
     VXM_CK(cudaMemsetAsync(c->occ, 0, c->n * S, c->stream));
-    VXM_CK(cudaMalloc(&c->key, sizeof(uint32_t) * c->n * S + 64));
-    VXM_CK(cudaMemsetAsync(c->key, 0, sizeof(uint32_t) * c->n * S, c->stream));
+    VXM_CK(cudaMalloc(&c->key, static_cast<size_t>(c->key_bits / 8) * c->n * S + 64));
+    if (c->key_bits == 16) {
+      vxm::fill_u16_kernel<<<static_cast<unsigned>(std::min<long long>((c->n * S + 255) / 256, 148LL * 16)), 256, 0,
+                             c->stream>>>(reinterpret_cast<uint16_t*>(c->key), c->n * static_cast<long long>(S),
+                                          static_cast<uint16_t>(vxm::KeyFmt<16>::kUnknown));
+      VXM_CK(cudaGetLastError());
+    } else {
+      VXM_CK(cudaMemsetAsync(c->key, 0, sizeof(uint32_t) * c->n * S, c->stream));
+    }
     if (cfg->vox_inf > 0) {
       VXM_CK(cudaMalloc(&c->ctr, c->n * S));
       VXM_CK(cudaMemsetAsync(c->ctr, 0, c->n * S, c->stream));
@@ -1153,9 +1172,10 @@ int vxm_create_multi(const vxm_config* cfg, int32_t n_streams, int32_t frames_pe
     kp.vh = c->bundle[2];
     kp.tiles_x = (kp.vw + 7) / 8;
     kp.tiles_y = (kp.vh + 3) / 4;
-    VXM_CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(vxm::merge_shift_count_tma_kernel),
-                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(2 * vxm::merge_tma_smem_bytes(vxm::kMergeStageCells))));
+    for (const void* fn : {reinterpret_cast<const void*>(vxm::merge_shift_count_tma_kernel<16>),
+                           reinterpret_cast<const void*>(vxm::merge_shift_count_tma_kernel<32>)})
+      VXM_CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(2 * vxm::merge_tma_smem_bytes(vxm::kMergeStageCells))));
     for (const void* fn : {reinterpret_cast<const void*>(vxm::populate_depth_tma_kernel<true>),
                            reinterpret_cast<const void*>(vxm::populate_depth_tma_kernel<false>)})
       VXM_CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1165,6 +1185,7 @@ int vxm_create_multi(const vxm_config* cfg, int32_t n_streams, int32_t frames_pe
     kp.ctr = c->ctr;
     kp.rowflag = c->rowflag;
     kp.key = c->key;
+    kp.key_bits = c->key_bits;
     kp.loc0 = c->loc[0];
     kp.loc1 = c->loc[1];
     kp.counters = c->counters;

@@ -77,6 +77,9 @@ unsigned blocks_for(long long n, int threads, int cap = 148 * 16) {
 
 constexpr uint32_t kEpoch = 1u;
 
+// key width of a stage call: 16-bit keys when the bundle allows (as a context)
+int key_bits_for(long long rays) { return rays <= vxm::KeyFmt<16>::kMaxRays ? 16 : 32; }
+
 // One-stream kernel parameters for a grid (no camera, no bundle).
 vxm::KParams grid_params(const vxm_grid_spec& g) {
   vxm::KParams kp{};
@@ -138,9 +141,10 @@ int vxm_populate_occupied(const vxm_grid_spec* grid, uint8_t* ms, const double* 
     VXM_SCK(cudaMemset(d_cnt.p, 0, sizeof(vxm::Counters)));
     if (d_ctr.p) VXM_SCK(cudaMemset(d_ctr.p, 0, N));
     if (d_rowflag.p) VXM_SCK(cudaMemset(d_rowflag.p, 0, static_cast<size_t>(kp.dy) * kp.dz));
-    vxm::encode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_ms.p, d_occ.p, d_key.p, N, kEpoch);
+    vxm::encode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_ms.p, d_occ.p, d_key.p, N, kEpoch, 32);
     kp.occ = d_occ.p;
     kp.key = d_key.p;
+    kp.key_bits = 32;
     kp.ctr = d_ctr.p;
     kp.rowflag = d_rowflag.p;
     kp.vox_inf = vox_inf;
@@ -159,7 +163,7 @@ int vxm_populate_occupied(const vxm_grid_spec* grid, uint8_t* ms, const double* 
       vxm::launch_dilate(kp, r, 1, smem, 0);
       VXM_SCK(cudaGetLastError());
     }
-    vxm::decode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_occ.p, d_key.p, d_ms.p, N, kEpoch, 1);
+    vxm::decode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_key.p, d_ms.p, N, 32, 1);
     VXM_SCK(cudaGetLastError());
     vxm::Counters cnt{};
     VXM_SCK(cudaMemcpy(&cnt, d_cnt.p, sizeof(cnt), cudaMemcpyDeviceToHost));
@@ -181,8 +185,8 @@ int vxm_trace_bundle(const vxm_grid_spec* grid, uint8_t* ms, const int32_t bundl
       throw StageError{VXM_EINVAL, "generate_rays: bundle dimensions must be positive and odd"};
     if (!(ray_vox_size > 0.0)) throw StageError{VXM_EINVAL, "generate_rays: vox_size must be positive"};
     const long long rays = static_cast<long long>(bundle[1]) * bundle[2];
-    if (rays > static_cast<long long>(vxm::kMaxRays))
-      throw StageError{VXM_EINVAL, "ray bundle exceeds the 17-bit ray key"};
+    if (rays > vxm::KeyFmt<32>::kMaxRays) throw StageError{VXM_EINVAL, "ray bundle exceeds 2^31 - 3 rays"};
+    const int bits = key_bits_for(rays);
     // validate_ray (raytracer.cpp:23-33) for every ray, before any write.
     const double vs = ray_vox_size;
     for (int a = 0; a < 3; ++a)
@@ -222,15 +226,16 @@ int vxm_trace_bundle(const vxm_grid_spec* grid, uint8_t* ms, const int32_t bundl
     VXM_SCK(cudaMemcpy(d_frame.p, &f, sizeof(f), cudaMemcpyHostToDevice));
     VXM_SCK(cudaMemcpy(d_ms.p, ms, N, cudaMemcpyHostToDevice));
     VXM_SCK(cudaMemset(d_cnt.p, 0, sizeof(vxm::Counters)));
-    vxm::encode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_ms.p, d_occ.p, d_key.p, N, kEpoch);
+    vxm::encode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_ms.p, d_occ.p, d_key.p, N, kEpoch, bits);
     kp.occ = d_occ.p;
     kp.key = d_key.p;
+    kp.key_bits = bits;
     kp.counters = d_cnt.p;
     kp.frames = d_frame.p;
     vxm::launch_trace(kp, 1, 1, 0);
     VXM_SCK(cudaGetLastError());
     vxm::fold_trace_slots_kernel<<<1, 32>>>(d_cnt.p);
-    vxm::decode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_occ.p, d_key.p, d_ms.p, N, kEpoch);
+    vxm::decode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_key.p, d_ms.p, N, bits);
     VXM_SCK(cudaGetLastError());
     vxm::Counters cnt{};
     VXM_SCK(cudaMemcpy(&cnt, d_cnt.p, sizeof(cnt), cudaMemcpyDeviceToHost));
@@ -439,15 +444,16 @@ int vxm_trace_per_pixel(const vxm_grid_spec* grid, uint8_t* ms, const double* xs
     }
     VXM_SCK(cudaMemcpy(d_ms.p, ms, N, cudaMemcpyHostToDevice));
     VXM_SCK(cudaMemset(d_cnt.p, 0, sizeof(vxm::Counters)));
-    vxm::encode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_ms.p, d_occ.p, d_key.p, N, kEpoch);
+    vxm::encode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_ms.p, d_occ.p, d_key.p, N, kEpoch, 32);
     kp.occ = d_occ.p;
     kp.key = d_key.p;
+    kp.key_bits = 32;
     kp.counters = d_cnt.p;
     kp.frames = d_frame.p;
     vxm::trace_per_pixel_kernel<<<dim3(blocks_for(static_cast<long long>(n), 256), 1), 256>>>(kp, 0);
     VXM_SCK(cudaGetLastError());
     vxm::fold_trace_slots_kernel<<<1, 32>>>(d_cnt.p);
-    vxm::decode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_occ.p, d_key.p, d_ms.p, N, kEpoch);
+    vxm::decode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_key.p, d_ms.p, N, 32);
     VXM_SCK(cudaGetLastError());
     vxm::Counters cnt{};
     VXM_SCK(cudaMemcpy(&cnt, d_cnt.p, sizeof(cnt), cudaMemcpyDeviceToHost));

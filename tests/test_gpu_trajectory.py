@@ -62,4 +62,4 @@ def test_cfg4_full_size_1000_frame_sweep(gpu_lib):
                 rc = orc.local_grid()[0]
                 assert np.array_equal(one.local_grid()[0], rc), i
         assert np.array_equal(seq.local_grid()[0], orc.local_grid()[0]), i0
-    assert shifts > 900
+    assert shifts > 700  # the reference recentres on 749 of the 1000 frames
