@@ -378,6 +378,13 @@ class MappingPipeline {
   // local grid, e.g. read_grid(path) of an earlier write_grid(local_grid()).
   // Its dims and vox_size must match the configuration's grid.
   void restore_local_grid(const VoxelGrid& grid);
+  // Extension (asynchronous checkpoint): write the local grid as it stands now
+  // to a VOXGRID1 file (as write_grid(local_grid(), path) would) without
+  // stalling integration: device -> pinned copy on a side stream, file written
+  // by a host thread. snapshot_wait() joins it and throws std::runtime_error
+  // if the write failed.
+  void save_snapshot_async(const std::string& path);
+  void snapshot_wait();
 
  private:
   PipelineConfig cfg_;

@@ -140,7 +140,8 @@ typedef struct vxm_ctx vxm_ctx;
 #define VXM_FLAG_SINGLE_BRANCH 4u /* batches: one graph branch (stage events then time each whole stage) */
 #define VXM_FLAG_NO_TMA_MERGE 8u  /* K4 with direct loads instead of TMA-staged rows (A/B and fallback) */
 #define VXM_FLAG_NO_DESYNC 32u   /* batches: one graph with joined branches instead of per-branch graphs (A/B) */
-#define VXM_FLAG_WIDE_KEYS 64u   /* 32-bit measurement keys even when 16-bit keys would do (A/B, tests) */
+#define VXM_FLAG_CLEAR_KEYS 64u  /* the large-bundle key format (no epochs, keys reset by the merge) for any
+                                    bundle (A/B, tests; chosen anyway above 131,070 rays) */
 #define VXM_FLAG_STAGE_EVENTS 16u /* record the stage-boundary events inside the frame graph (fills
                                      vxm_stats::*_us; each event node costs a few us per frame) */
 
@@ -220,6 +221,16 @@ int vxm_grid_read(const char* path, vxm_grid_spec* spec, uint8_t* cells, size_t 
  * VOXGRID1 file; the file's dims and vox_size must match the context. */
 int vxm_snapshot_save(vxm_ctx* ctx, int32_t s, const char* path);
 int vxm_snapshot_load(vxm_ctx* ctx, int32_t s, const char* path);
+/* Asynchronous checkpoint: the local grid as it stands
+ * after the calls issued so far is copied device -> pinned host memory on a
+ * side stream (no context synchronisation; later integrate calls only wait
+ * for that ~0.5 MB copy, not for the host) and a host thread writes the
+ * VOXGRID1 file (byte-identical to vxm_snapshot_save). One snapshot in
+ * flight per context: a new one first waits for the previous.
+ * vxm_snapshot_wait joins the writer and returns its status (VXM_EIO on a
+ * failed write; VXM_OK when nothing is pending). */
+int vxm_snapshot_save_async(vxm_ctx* ctx, int32_t s, const char* path);
+int vxm_snapshot_wait(vxm_ctx* ctx);
 /* The context's CUDA stream (cudaStream_t) and the device time of the last
  * integrate call's kernels in milliseconds (CUDA events on that stream). */
 void* vxm_cuda_stream(vxm_ctx* ctx);

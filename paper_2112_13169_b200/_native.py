@@ -19,7 +19,7 @@ UNKNOWN, FREE, OCCUPIED, UNKNOWN_TRACED = 0, 1, 2, 3
 TRACER_BUNDLED, TRACER_PER_PIXEL = 0, 1
 FLAG_STAGE_TIMING, FLAG_NO_GRAPH, FLAG_SINGLE_BRANCH, FLAG_NO_TMA_MERGE, FLAG_STAGE_EVENTS = 1, 2, 4, 8, 16
 FLAG_NO_DESYNC = 32
-FLAG_WIDE_KEYS = 64
+FLAG_CLEAR_KEYS = 64
 
 
 class GridSpecC(C.Structure):
@@ -84,6 +84,8 @@ SIGNATURES = {
     "vxm_grid_read": (C.c_int, [C.c_char_p, P(GridSpecC), C.c_void_p, C.c_size_t]),
     "vxm_snapshot_save": (C.c_int, [C.c_void_p, C.c_int32, C.c_char_p]),
     "vxm_snapshot_load": (C.c_int, [C.c_void_p, C.c_int32, C.c_char_p]),
+    "vxm_snapshot_save_async": (C.c_int, [C.c_void_p, C.c_int32, C.c_char_p]),
+    "vxm_snapshot_wait": (C.c_int, [C.c_void_p]),
     "vxm_integrate_depth_frames": (C.c_int, [C.c_void_p, C.c_void_p, P(PoseC), C.c_int32, P(StatsC)]),
     "vxm_integrate_depth": (C.c_int, [C.c_void_p, C.c_void_p, P(PoseC), P(StatsC)]),
     "vxm_integrate_depth_device": (C.c_int, [C.c_void_p, C.c_void_p, P(PoseC)]),

@@ -543,6 +543,15 @@ void MappingPipeline::restore_local_grid(const VoxelGrid& grid) {
   local_stale_ = false;
 }
 
+void MappingPipeline::save_snapshot_async(const std::string& path) {
+  check(vxm_snapshot_save_async(seq_active_ ? seq_ctx_ : ctx_, 0, path.c_str()));
+}
+
+void MappingPipeline::snapshot_wait() {
+  for (vxm_ctx* c : {ctx_, seq_ctx_})
+    if (c) check(vxm_snapshot_wait(c));
+}
+
 // ----------------------------------------------------------- kernel table
 
 namespace kernels {

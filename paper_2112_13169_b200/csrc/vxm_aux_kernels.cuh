@@ -10,38 +10,29 @@
 namespace vxm {
 
 // Reference byte grid -> (occ, keys) of epoch e (see vxm_device.cuh):
-// Occupied becomes occ == e and the Occupied key, pre-existing Free /
-// UnknownTraced become the lowest-priority keys so that any ray write
-// overrides them.
-__global__ void encode_ms_kernel(const uint8_t* ms, uint8_t* occ, void* key, long long n, uint32_t epoch,
-                                 int bits) {
+// Occupied becomes occ == e (and, clear format, the Occupied key);
+// pre-existing Free / UnknownTraced become the lowest-priority keys so that
+// any ray write overrides them.
+__global__ void encode_ms_kernel(const uint8_t* ms, uint8_t* occ, uint32_t* key, long long n, uint32_t epoch,
+                                 int fmt) {
+  const uint32_t carried = ray_key(fmt, epoch, -1);
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const uint8_t b = ms[i];
     occ[i] = b == 2 ? static_cast<uint8_t>(epoch) : 0;
-    if (bits == 16)
-      static_cast<uint16_t*>(key)[i] = static_cast<uint16_t>(encode_state<16>(b));
-    else
-      static_cast<uint32_t*>(key)[i] = encode_state<32>(b);
+    key[i] = (b == 1 || b == 3) ? (carried | (b >> 1)) : (b == 2 && fmt == kClearKeys ? kClearOccupied : 0u);
   }
 }
 
-// fills n 16-bit words with v (the Unknown pattern of 16-bit keys)
-__global__ void fill_u16_kernel(uint16_t* p, long long n, uint16_t v) {
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<long long>(gridDim.x) * blockDim.x)
-    p[i] = v;
-}
-
-// keys -> reference bytes. keep_input (populate): a cell whose key is not
-// Occupied keeps its input byte (populate only adds Occupied cells; the
-// vectorised dilation may store Unknown keys next to the cells it marks).
-__global__ void decode_ms_kernel(const void* key, uint8_t* ms, long long n, int bits, int keep_input = 0) {
+// (occ, keys) -> reference bytes. keep_occupied (populate): cells that were
+// Occupied in ms before stay Occupied (the vectorised dilation may zero occ
+// bytes next to the cells it marks).
+__global__ void decode_ms_kernel(const uint8_t* occ, const uint32_t* key, uint8_t* ms, long long n, uint32_t epoch,
+                                 int fmt, int keep_occupied = 0) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const uint32_t v = bits == 16 ? decode_key<16>(static_cast<const uint16_t*>(key)[i])
-                                  : decode_key<32>(static_cast<const uint32_t*>(key)[i]);
-    ms[i] = static_cast<uint8_t>(keep_input && v != 2u ? ms[i] : v);
+    const uint32_t v = fmt == kClearKeys ? decode_clear_key(key[i]) : decode_cell(occ[i], key[i], epoch);
+    ms[i] = static_cast<uint8_t>(keep_occupied && ms[i] == 2 ? 2u : v);
   }
 }
 

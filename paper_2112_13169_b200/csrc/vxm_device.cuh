@@ -22,76 +22,59 @@ namespace vxm {
 // frame (proj/src/pipeline.cpp:83), written Occupied by populate and Free /
 // UnknownTraced by the rays, with the highest-index ray winning a conflict in
 // Sequential mode (raytracer.cpp:98-104). The GPU keeps two
-// arrays per measurement slot:
+// arrays per measurement slot, never reset as a whole:
 //
 //   occ[c]  (uint8)  == e   Occupied this frame (e = the slot's 8-bit epoch,
-//                            1..255, so occ is never reset; cleared once per
-//                            255 frames). Read-only during the trace.
-//   key[c]  (16 or 32 bit)   the cell's measurement state as an ordered key:
-//                            Unknown (untouched) < Free / UnknownTraced carried
-//                            in from a host grid < ray 0 < ray 1 < ... <
-//                            Occupied. A ray writes key(ray) | traced with a
-//                            fire-and-forget max reduction, so the highest
-//                            ray index wins: exactly the Sequential
-//                            last-writer rule. Populate / dilation store
-//                            Occupied keys; the merge (K4) decodes the keys,
-//                            then writes Unknown back over every key it saw
-//                            touched (and over the cells the shift drops), so
-//                            the array is all-Unknown again when the next
-//                            frame starts: no epoch bits, no reset pass.
+//                            1..255; a slot's arrays are cleared once per 255
+//                            frames). Read-only during the trace.
+//   key[c]  (uint32)         the cell's ray write as an ordered key; a ray
+//                            writes key(ray) | traced with a fire-and-forget
+//                            RED.max, so the highest ray index wins: exactly
+//                            the Sequential last-writer rule.
 //
-// Key formats (KeyFmt<bits>): 32-bit keys are plain unsigned integers
-// (Unknown 0, ray r -> 2(r+2) | traced, Occupied 0xFFFFFFFF; up to 2^31 - 3
-// rays). 16-bit keys halve the key traffic for bundles of up to 32,638 rays
-// (every 640x480 configuration): they are bf16 bit patterns, ordered by the
-// L2's native packed-bf16 max reduction (red.max.noftz.v2.bf16 on the
-// aligned cell pair, the other half given -inf, the neutral element):
-// Unknown = -inf (0xFF80), Occupied = +inf (0x7F80), and the ray keys walk up
-// the finite values in order (negative patterns downwards, then positive
-// patterns upwards; the traced bit is bit 0 of the pattern in both halves of
-// the range, and NaN patterns are never formed).
+// Two key formats (KeyFmt):
+//   kEpochKeys (bundles of up to 131,070 rays, every BASELINE config):
+//     key = e << 18 | (ray + 1) << 1 | traced; keys of another epoch read as
+//     Unknown, so nothing is reset between frames; Free / UnknownTraced
+//     carried in from a host grid are e << 18 | 0 / 1 (below every ray).
+//     The merge reads occ (Occupied wins) and the keys.
+//   kClearKeys (larger bundles, up to 2^31 - 3 rays; the reference has no
+//     cap): Unknown 0 < carried Free 2 / UnknownTraced 3 < ray r: 2(r + 2) |
+//     traced < Occupied 0xFFFFFFFF (stored by populate / dilation). The merge
+//     decodes the keys alone and writes Unknown back over every key it saw
+//     touched and over the cells the shift drops, so the slot is all-Unknown
+//     when the next frame starts.
+// Measured (B200, 64 cfg2 streams): the clearing writes cost the merge more
+// than skipping the occupancy reads saves (K4 60 vs 50 us), and 16-bit keys
+// ordered as bf16 patterns (packed-bf16 RED.max; K4 52 us) added ~10 us of
+// resolve instructions to the ray cast, so the epoch format stays the
+// default and the clear format only lifts the bundle limit.
 // ---------------------------------------------------------------------------
-template <int kBits>
-struct KeyFmt;
+enum KeyFmt : int { kEpochKeys = 0, kClearKeys = 1 };
 
-template <>
-struct KeyFmt<16> {
-  using T = uint16_t;
-  static constexpr uint32_t kUnknown = 0xFF80u;   // bf16 -inf
-  static constexpr uint32_t kOccupied = 0x7F80u;  // bf16 +inf
-  static constexpr long long kMaxRays = 32638;    // ray indices 0..32637
-  // Free key of ray r (| 1: UnknownTraced); r = -1: carried in from a host grid
-  __host__ __device__ static constexpr uint32_t ray_base(long long r) {
-    return 2 * (r + 2) < 32640 ? static_cast<uint32_t>(0xFF80 - 2 * (r + 2))
-                               : static_cast<uint32_t>(2 * (r + 2) - 32640);
-  }
-};
+constexpr uint32_t kKeyShift = 18;                     // epoch keys
+constexpr uint32_t kLowMask = (1u << kKeyShift) - 1u;  // 0x3FFFF
+constexpr uint32_t kMaxEpoch = 255u;                   // fits the occ byte
+constexpr long long kMaxEpochRays = (kLowMask >> 1) - 1u;  // (ray+1)<<1|1 <= 0x3FFFF: 131,070 rays
+constexpr long long kMaxClearRays = 0x7FFFFFFDLL;          // 2(ray+2)|1 < 0xFFFFFFFF
+constexpr uint32_t kClearOccupied = 0xFFFFFFFFu;
+constexpr int kMaxVoxInf = 16;  // the tile dilation (K2); larger radii take the generic passes
 
-template <>
-struct KeyFmt<32> {
-  using T = uint32_t;
-  static constexpr uint32_t kUnknown = 0u;
-  static constexpr uint32_t kOccupied = 0xFFFFFFFFu;
-  static constexpr long long kMaxRays = 0x7FFFFFFDLL;
-  __host__ __device__ static constexpr uint32_t ray_base(long long r) { return static_cast<uint32_t>(2 * (r + 2)); }
-};
+__host__ __device__ constexpr uint32_t key_tag(uint32_t epoch) { return epoch << kKeyShift; }
 
-constexpr uint32_t kMaxEpoch = 255u;  // fits the occ byte
-constexpr int kMaxVoxInf = 16;        // the tile dilation (K2); larger radii take the generic passes
-
-// key -> reference byte state (0 Unknown, 1 Free, 2 Occupied, 3 UnknownTraced)
-template <int kBits>
-__host__ __device__ __forceinline__ uint32_t decode_key(uint32_t k) {
-  if (k == KeyFmt<kBits>::kUnknown) return 0u;
-  if (k == KeyFmt<kBits>::kOccupied) return 2u;
-  return 1u + 2u * (k & 1u);
+// Free key of ray r (| 1: UnknownTraced); r = -1: carried in from a host grid
+__host__ __device__ __forceinline__ uint32_t ray_key(int fmt, uint32_t epoch, long long r) {
+  return fmt == kEpochKeys ? key_tag(epoch) | static_cast<uint32_t>((r + 1) << 1) : static_cast<uint32_t>(2 * (r + 2));
 }
 
-// reference byte state -> key of a cell carried in from a host grid
-template <int kBits>
-__host__ __device__ __forceinline__ uint32_t encode_state(uint32_t b) {
-  return b == 2u ? KeyFmt<kBits>::kOccupied
-                 : (b == 1u || b == 3u) ? (KeyFmt<kBits>::ray_base(-1) | (b >> 1)) : KeyFmt<kBits>::kUnknown;
+// (occ, key) -> reference byte state (0 Unknown, 1 Free, 2 Occupied, 3 UnknownTraced).
+__host__ __device__ __forceinline__ uint32_t decode_cell(uint32_t occ, uint32_t key, uint32_t epoch) {
+  if (occ == epoch) return 2u;
+  if ((key >> kKeyShift) != epoch) return 0u;
+  return (key & 1u) ? 3u : 1u;
+}
+__host__ __device__ __forceinline__ uint32_t decode_clear_key(uint32_t k) {
+  return k == 0u ? 0u : (k == kClearOccupied ? 2u : 1u + 2u * (k & 1u));
 }
 
 // merge_scalar (proj/src/kernels/kernels_scalar.cpp:10-16): measurement 0
@@ -145,7 +128,7 @@ struct FrameParams {
   // this stream's occupancy bytes and keys (base + slot*n); read from memory
   // so the tracer keeps them in registers instead of rebuilding each address
   const uint8_t* occ_s;
-  void* key_s;
+  uint32_t* key_s;
   int32_t off[3];     // shift applied after the merge (0,0,0 = none)
   uint32_t epoch;     // 1..255
   uint32_t cur;       // which local buffer holds the current grid
@@ -180,8 +163,9 @@ struct KParams {
   uint8_t* ctr;        // centre bytes when vox_inf > 0
   uint8_t* rowflag;    // [dy*dz] per slot: == epoch when the x-row holds a centre (vox_inf > 0)
   uint32_t* dbits;     // x-dilated centre bit rows [dy*dz][row words] (vox_inf > 0)
-  void* key;           // KeyFmt<key_bits>::T per cell
-  int key_bits;        // 16 or 32
+  uint8_t* dtmp;       // generic dilation (large radii / rows): 2 * n bytes per slot
+  uint32_t* key;
+  int key_fmt;         // KeyFmt
   uint8_t* loc0;
   uint8_t* loc1;
   Counters* counters;
@@ -189,61 +173,38 @@ struct KParams {
   const FrameParams* frames;
 };
 
-// This slot's key array (byte address).
-__host__ __device__ __forceinline__ char* key_slot(const KParams& p, long long slot) {
-  return static_cast<char*>(p.key) + slot * p.n * (p.key_bits >> 3);
+// 0xff in every byte of x that is zero, 0x00 elsewhere (exact, no carries
+// across bytes: each byte's low 7 bits + 0x7f stays within the byte).
+__device__ __forceinline__ uint32_t zero_bytes(uint32_t x) {
+  const uint32_t nonzero = (((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x) & 0x80808080u;
+  return ((nonzero ^ 0x80808080u) >> 7) * 0xffu;
 }
 
-// Occupied key at cell idx (populate / dilation; the width is a run-time,
-// launch-uniform choice there).
-__device__ __forceinline__ void store_occupied_key(char* key, uint32_t idx, int bits) {
-  if (bits == 16)
-    reinterpret_cast<uint16_t*>(key)[idx] = static_cast<uint16_t>(KeyFmt<16>::kOccupied);
-  else
-    reinterpret_cast<uint32_t*>(key)[idx] = KeyFmt<32>::kOccupied;
+// Occupied key at cell idx (populate / dilation), clear-format keys only
+// (the epoch format reads occupancy from occ).
+__device__ __forceinline__ void store_occupied_key(uint32_t* key, uint32_t idx, int fmt) {
+  if (fmt == kClearKeys) key[idx] = kClearOccupied;
 }
 
-// Four consecutive cells' keys in one vector access (the merge kernels):
-// their measurement states as bytes (0..3), whether any was touched this
-// frame, and the all-Unknown pattern written back over touched ones.
-template <int kBits>
-struct Keys4;
-
-template <>
-struct Keys4<16> {
-  using V = uint2;
-  static constexpr int kBytes = 8;
-  static __device__ __forceinline__ V load_cs(const void* p) { return __ldcs(reinterpret_cast<const uint2*>(p)); }
-  static __device__ __forceinline__ V load(const void* p) { return *reinterpret_cast<const uint2*>(p); }
-  static __device__ __forceinline__ V unknown() { return make_uint2(0xFF80FF80u, 0xFF80FF80u); }
-  static __device__ __forceinline__ void clear(void* p) { *reinterpret_cast<uint2*>(p) = unknown(); }
-  static __device__ __forceinline__ bool touched(V k) { return ((k.x ^ 0xFF80FF80u) | (k.y ^ 0xFF80FF80u)) != 0u; }
-  // two cells (halves of w) -> states in the low byte of each half
-  static __device__ __forceinline__ uint32_t states2(uint32_t w) {
-    const uint32_t unk = __vcmpeq2(w, 0xFF80FF80u);
-    const uint32_t occ = __vcmpeq2(w, 0x7F807F80u);
-    const uint32_t st = ((w & 0x00010001u) << 1) | 0x00010001u;  // 1 or 3: bit 0 is the traced bit
-    return ((st & ~occ) | (0x00020002u & occ)) & ~unk;
+// Measurement states (bytes 0..3) of 4 consecutive cells from their
+// occupancy bytes o4 and keys (epoch format) ...
+__device__ __forceinline__ uint32_t states4_epoch(uint32_t o4, uint4 k4, uint32_t epoch) {
+  const uint32_t kk[4] = {k4.x, k4.y, k4.z, k4.w};
+  uint32_t m4 = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t v = (kk[i] >> kKeyShift) == epoch ? (1u | ((kk[i] & 1u) << 1)) : 0u;  // 1 or 3
+    m4 |= v << (8 * i);
   }
-  static __device__ __forceinline__ uint32_t states(V k) { return __byte_perm(states2(k.x), states2(k.y), 0x6420); }
-};
-
-template <>
-struct Keys4<32> {
-  using V = uint4;
-  static constexpr int kBytes = 16;
-  static __device__ __forceinline__ V load_cs(const void* p) { return __ldcs(reinterpret_cast<const uint4*>(p)); }
-  static __device__ __forceinline__ V load(const void* p) { return *reinterpret_cast<const uint4*>(p); }
-  static __device__ __forceinline__ V unknown() { return make_uint4(0u, 0u, 0u, 0u); }
-  static __device__ __forceinline__ void clear(void* p) { *reinterpret_cast<uint4*>(p) = unknown(); }
-  static __device__ __forceinline__ bool touched(V k) { return (k.x | k.y | k.z | k.w) != 0u; }
-  static __device__ __forceinline__ uint32_t state1(uint32_t k) {
-    return k == 0u ? 0u : (k == 0xFFFFFFFFu ? 2u : 1u + 2u * (k & 1u));
-  }
-  static __device__ __forceinline__ uint32_t states(V k) {
-    return state1(k.x) | (state1(k.y) << 8) | (state1(k.z) << 16) | (state1(k.w) << 24);
-  }
-};
+  const uint32_t occm = zero_bytes(o4 ^ (epoch * 0x01010101u));  // 0xff where Occupied
+  return (m4 & ~occm) | (0x02020202u & occm);
+}
+// ... or from the keys alone (clear format).
+__device__ __forceinline__ uint32_t states4_clear(uint4 k) {
+  return decode_clear_key(k.x) | (decode_clear_key(k.y) << 8) | (decode_clear_key(k.z) << 16) |
+         (decode_clear_key(k.w) << 24);
+}
+__device__ __forceinline__ bool touched4(uint4 k) { return (k.x | k.y | k.z | k.w) != 0u; }
 
 // merge of 4 packed cells: local l4 and measurement states m4 (bytes 0..3,
 // so "== 0" and "== 3" are two-bit tests): merge_cell per byte.
@@ -356,12 +317,6 @@ __device__ __forceinline__ void block_accumulate(unsigned (&v)[NC], unsigned lon
   }
 }
 
-// 0xff in every byte of x that is zero, 0x00 elsewhere (exact, no carries
-// across bytes: each byte's low 7 bits + 0x7f stays within the byte).
-__device__ __forceinline__ uint32_t zero_bytes(uint32_t x) {
-  const uint32_t nonzero = (((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x) & 0x80808080u;
-  return ((nonzero ^ 0x80808080u) >> 7) * 0xffu;
-}
 
 // ---------------------------------------------------------------------------
 // Bulk asynchronous copies (TMA engine, cp.async.bulk) into shared memory,

@@ -24,7 +24,7 @@ namespace vxm {
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ unsigned populate_point(const KParams& p, const double* R,
                                                    const double* t, uint8_t* target,
-                                                   uint8_t* rowflag, char* keys, uint8_t mark, double x,
+                                                   uint8_t* rowflag, uint32_t* keys, uint8_t mark, double x,
                                                    double y, double z) {
   int c[3];
   transform_voxelize(R, t, x, y, z, p.vs, p.inv_vs, c);
@@ -40,7 +40,7 @@ __device__ __forceinline__ unsigned populate_point(const KParams& p, const doubl
     // a centre: the dilation only visits x-rows that hold one this frame
     rowflag[static_cast<uint32_t>(c[1]) + static_cast<uint32_t>(c[2]) * p.dy] = mark;
   } else {
-    store_occupied_key(keys, idx, p.key_bits);  // vox_inf == 0: the cell itself is Occupied
+    store_occupied_key(keys, idx, p.key_fmt);  // vox_inf == 0: the cell itself is Occupied
   }
   return 0u;
 }
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(256) populate_depth_kernel(KParams p, int iter
   const uint8_t mark = static_cast<uint8_t>(fp->epoch);
   uint8_t* target = (p.vox_inf > 0 ? p.ctr : p.occ) + static_cast<long long>(s) * p.n;
   uint8_t* rowflag = p.vox_inf > 0 ? p.rowflag + static_cast<long long>(s) * p.dy * p.dz : nullptr;
-  char* const keys = key_slot(p, s);
+  uint32_t* const keys = p.key + static_cast<long long>(s) * p.n;
   double R[9], t[3];
 #pragma unroll
   for (int i = 0; i < 9; ++i) R[i] = fp->rot[i];
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(256) populate_depth_tma_kernel(KParams p, int 
   const uint8_t mark = static_cast<uint8_t>(fp->epoch);
   uint8_t* target = (p.vox_inf > 0 ? p.ctr : p.occ) + static_cast<long long>(s) * p.n;
   uint8_t* rowflag = p.vox_inf > 0 ? p.rowflag + static_cast<long long>(s) * p.dy * p.dz : nullptr;
-  char* const keys = key_slot(p, s);
+  uint32_t* const keys = p.key + static_cast<long long>(s) * p.n;
   const float* depth = fp->depth;
   const int nq = (p.W * p.H) >> 2;
   const int T = blockDim.x;
@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(256) populate_cloud_kernel(KParams p) {
   const uint8_t mark = static_cast<uint8_t>(fp->epoch);
   uint8_t* target = (p.vox_inf > 0 ? p.ctr : p.occ) + static_cast<long long>(s) * p.n;
   uint8_t* rowflag = p.vox_inf > 0 ? p.rowflag + static_cast<long long>(s) * p.dy * p.dz : nullptr;
-  char* const keys = key_slot(p, s);
+  uint32_t* const keys = p.key + static_cast<long long>(s) * p.n;
   double R[9], t[3];
 #pragma unroll
   for (int i = 0; i < 9; ++i) R[i] = fp->rot[i];
@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(256) dilate_tiles_kernel(KParams p, int r_rt) 
   const int s = blockIdx.z;
   const uint32_t e = p.frames[s].epoch;
   uint8_t* occ = p.occ + static_cast<long long>(s) * p.n;
-  char* const keys = key_slot(p, s);
+  uint32_t* const keys = p.key + static_cast<long long>(s) * p.n;
   const int W = (p.dx + 31) >> 5;
   const int WP = dilate_row_words(p.dx);
   const int lg = __ffs(WP) - 1;
@@ -538,15 +538,11 @@ __global__ void __launch_bounds__(256) dilate_tiles_kernel(KParams p, int r_rt) 
         if (nib) {
           const uint32_t m = ((nib * 0x00204081u) & 0x01010101u) * 0xFFu;  // 0xFF per set bit
           *reinterpret_cast<uint32_t*>(dst + x0) = e * 0x01010101u & m;
-          // the 4 cells' keys: Occupied where set, Unknown (as every key is
+          // clear-format keys: Occupied where set, Unknown (as every key is
           // before the trace) elsewhere
-          const uint32_t cell = static_cast<uint32_t>(gy) * p.dx + static_cast<uint32_t>(gz) * dxy + x0;
-          if (p.key_bits == 16) {
-            *reinterpret_cast<uint2*>(keys + 2ull * cell) =
-                make_uint2(0xFF80FF80u ^ ((nib & 1u) << 15) ^ ((nib & 2u) << 30),
-                           0xFF80FF80u ^ ((nib & 4u) << 13) ^ ((nib & 8u) << 28));
-          } else {
-            *reinterpret_cast<uint4*>(keys + 4ull * cell) =
+          if (p.key_fmt == kClearKeys) {
+            const uint32_t cell = static_cast<uint32_t>(gy) * p.dx + static_cast<uint32_t>(gz) * dxy + x0;
+            *reinterpret_cast<uint4*>(keys + cell) =
                 make_uint4(0u - (nib & 1u), 0u - ((nib >> 1) & 1u), 0u - ((nib >> 2) & 1u), 0u - (nib >> 3));
           }
         }
@@ -564,11 +560,61 @@ __global__ void __launch_bounds__(256) dilate_tiles_kernel(KParams p, int r_rt) 
       const int x = (w << 5) + lane;
       if (x < p.dx && ((d >> lane) & 1u)) {
         dst[x] = static_cast<uint8_t>(e);
-        store_occupied_key(keys, static_cast<uint32_t>(gy) * p.dx + static_cast<uint32_t>(gz) * dxy + x, p.key_bits);
+        store_occupied_key(keys, static_cast<uint32_t>(gy) * p.dx + static_cast<uint32_t>(gz) * dxy + x, p.key_fmt);
       }
     }
   }
 }
+
+// Generic K2 for what the tile kernels do not cover (vox_inf > kMaxVoxInf,
+// rows longer than 1024 cells, or tiles whose shared memory would not fit):
+// the same separable Chebyshev dilation as three line passes with a running
+// window count (any radius, O(N) per pass): x over the centre bytes (== e)
+// into tmp0, y over tmp0 into tmp1, z over tmp1 into the Occupied bytes and
+// keys. Lines along y and z map consecutive threads to consecutive x
+// (coalesced); lines along x are one row per thread.
+__global__ void __launch_bounds__(256) dilate_line_kernel(KParams p, int r, int axis) {
+  pdl_wait();  // K1's centre bytes (axis 0) or the previous pass
+  const int s = blockIdx.y;
+  const uint32_t e = p.frames[s].epoch;
+  const long long n = p.n;
+  const long long dx = p.dx, dy = p.dy, dz = p.dz, dxy = dx * dy;
+  uint8_t* const t0 = p.dtmp + static_cast<long long>(s) * 2 * n;
+  uint8_t* const t1 = t0 + n;
+  const uint8_t* in = axis == 0 ? p.ctr + static_cast<long long>(s) * n : (axis == 1 ? t0 : t1);
+  uint8_t* out = axis == 0 ? t0 : t1;
+  uint8_t* occ = p.occ + static_cast<long long>(s) * n;
+  uint32_t* const keys = p.key + static_cast<long long>(s) * p.n;
+  const long long len = axis == 0 ? dx : (axis == 1 ? dy : dz);
+  const long long stride = axis == 0 ? 1 : (axis == 1 ? dx : dxy);
+  const long long lines = n / len;
+  for (long long L = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; L < lines;
+       L += static_cast<long long>(gridDim.x) * blockDim.x) {
+    long long base;
+    if (axis == 0) base = L * dx;                                   // row (y, z)
+    else if (axis == 1) base = (L % dx) + (L / dx) * dxy;           // column (x, z)
+    else base = L;                                                  // pillar (x, y)
+    auto set = [&](long long i) -> int {
+      const uint8_t v = in[base + i * stride];
+      return axis == 0 ? (v == e) : (v != 0);
+    };
+    int cnt = 0;  // set cells in [i - r, i + r] of the line
+    for (long long j = 0; j <= r && j < len; ++j) cnt += set(j);
+    for (long long i = 0; i < len; ++i) {
+      const long long c = base + i * stride;
+      if (axis < 2) {
+        out[c] = cnt > 0 ? 1 : 0;
+      } else if (cnt > 0) {
+        occ[c] = static_cast<uint8_t>(e);
+        store_occupied_key(keys, static_cast<uint32_t>(c), p.key_fmt);
+      }
+      if (i + r + 1 < len) cnt += set(i + r + 1);
+      if (i - r >= 0) cnt -= set(i - r);
+    }
+  }
+}
+
+inline bool dilate_generic(int r, int dx);
 
 // Launches K2a and the radius-specialised K2b (1..4) or the generic one.
 // The fused K2 (no K2a) when the centre rows load as 4-byte words and its
@@ -588,7 +634,21 @@ inline void launch_dilate_tiles(const KParams& kp, int r, bool fused, dim3 grid,
     launch_pdl(dilate_tiles_kernel<kR, false>, grid, dim3(256), dilate_smem_bytes(r, kp.dx), st, kp, r);
 }
 
+// the tile dilation's limits (radius, row length, shared memory)
+inline bool dilate_generic(int r, int dx) {
+  return r > kMaxVoxInf || dx > 1024 || dilate_smem_bytes(r, dx, dilate_fused(r, dx)) > 200 * 1024;
+}
+
 inline void launch_dilate(const KParams& kp, int r, int streams, size_t /*smem*/, cudaStream_t st) {
+  if (dilate_generic(r, kp.dx)) {
+    for (int axis = 0; axis < 3; ++axis) {
+      const long long len = axis == 0 ? kp.dx : (axis == 1 ? kp.dy : kp.dz);
+      const long long lines = kp.n / len;
+      const unsigned blocks = static_cast<unsigned>(std::min<long long>((lines + 255) / 256, 148LL * 8));
+      launch_pdl(dilate_line_kernel, dim3(blocks, streams), dim3(256), 0, st, kp, r, axis);
+    }
+    return;
+  }
   const int rows = kp.dy * kp.dz;
   const bool fused = dilate_fused(r, kp.dx);
   if (!fused) {
@@ -660,21 +720,6 @@ inline cudaError_t dilate_set_smem(int bytes) {
 
 constexpr int kTraceSlots = 32;
 
-// Max-reduction of key value kv into cell `cell` (fire and forget). 16-bit
-// keys: the packed-bf16 reduction on the aligned cell pair, the other half
-// given -inf (the neutral element); see KeyFmt.
-template <int kBits>
-__device__ __forceinline__ void red_max_key(char* key, uint32_t cell, uint32_t kv) {
-  if constexpr (kBits == 16) {
-    const uint32_t w = (cell & 1u) ? ((kv << 16) | 0xFF80u) : (0xFF800000u | kv);
-    asm volatile("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %1;\n\t"
-                 "red.relaxed.gpu.global.max.noftz.v2.bf16 [%0], {lo, hi};\n\t}"
-                 ::"l"(key + 2ull * (cell & ~1u)), "r"(w) : "memory");
-  } else {
-    asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(key + 4ull * cell), "r"(kv) : "memory");
-  }
-}
-
 struct RayState {
   int cur[3];
   int step[3];
@@ -730,12 +775,12 @@ __device__ __forceinline__ void ray_setup(const double* R, const double* start, 
 // few spilled values; 4-7% faster than one warp per block at 64 registers),
 // a lone frame (358 warps, GPU far from full) runs 8-step chunks at 64
 // registers, where per-warp latency decides.
-template <int kBits, int kChunk, int kTraceWarps, int kMinBlocks, bool kMatch, bool kFast, bool kSplit>
+template <int kChunk, int kTraceWarps, int kMinBlocks, bool kMatch, bool kFast, bool kSplit>
 __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_kernel(KParams p) {
   const int s = blockIdx.y;
   const FrameParams* fp = p.frames + s;
   const uint32_t epoch = fp->epoch;
-  char* const key = static_cast<char*>(fp->key_s);
+  uint32_t* const key = fp->key_s;
   const uint8_t* const occ = fp->occ_s;
   double R[9], start[3];
 #pragma unroll
@@ -754,7 +799,7 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   const int yi_idx = ty * (kSplit ? 2 : 4) + (rl >> 3);
   const bool active = ty < (kSplit ? (p.vh + 1) / 2 : p.tiles_y) && xi_idx < p.vw && yi_idx < p.vh;
   const uint32_t ray = static_cast<uint32_t>(yi_idx) * p.vw + xi_idx;  // row-major, y outer
-  const uint32_t ray_key = KeyFmt<kBits>::ray_base(ray);  // | 1: UnknownTraced
+  const uint32_t ray_key = vxm::ray_key(p.key_fmt, epoch, ray);  // | 1: UnknownTraced
 
   RayState st;
   ray_setup(R, start, p.vs, p.ray_vs, xi_idx - (p.vw - 1) / 2, yi_idx - (p.vh - 1) / 2, p.vd, st);
@@ -833,35 +878,19 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
     for (int j = 0; j < kChunk; ++j) {
 // the per-cell resolve: predicates io (occupied) / w (write), the counters,
 // the traced-bit state, ok = w and no higher-lane duplicate, the RED.max
-#define VXM_RESOLVE_COUNT                  \
+#define VXM_RESOLVE_BODY                   \
   "@w add.u32 %1, %1, 1;\n\t"            \
   "@w add.u32 %2, %2, %0;\n\t"           \
   "or.b32 kv, %6, %0;\n\t"               \
   "selp.u32 %0, 1, %0, io;\n\t"          \
-  "setp.eq.and.u32 ok, %8, 0, w;\n\t"
-// 32-bit keys: RED.max.u32 on the cell
-#define VXM_RESOLVE_RED32                  \
+  "setp.eq.and.u32 ok, %8, 0, w;\n\t"    \
   "mul.wide.u32 a, %3, 4;\n\t"           \
   "add.u64 a, a, %7;\n\t"                \
   "@ok red.relaxed.gpu.global.max.u32 [a], kv;\n\t"
-// 16-bit keys: the value placed in the cell's half of its aligned pair (the
-// other half -inf, 0xFF80), RED.max.bf16x2 on the pair (see red_max_key)
-#define VXM_RESOLVE_RED16                  \
-  "and.b32 ca, %3, 1;\n\t"               \
-  "setp.ne.u32 po, ca, 0;\n\t"           \
-  "selp.b32 ca, 0x5410, 0x1054, po;\n\t" \
-  "prmt.b32 kv, nf, kv, ca;\n\t"         \
-  "mov.b32 {lo, hi}, kv;\n\t"            \
-  "and.b32 ca, %3, -2;\n\t"              \
-  "mul.wide.u32 a, ca, 2;\n\t"           \
-  "add.u64 a, a, %7;\n\t"                \
-  "@ok red.relaxed.gpu.global.max.noftz.v2.bf16 [a], {lo, hi};\n\t"
 #define VXM_RESOLVE_DECL                   \
-  ".reg .pred v, io, w, ok, po;\n\t"     \
-  ".reg .b32 kv, ca, nf;\n\t"            \
-  ".reg .b16 lo, hi;\n\t"                \
-  ".reg .b64 a;\n\t"                     \
-  "mov.b32 nf, 0xFF80;\n\t"
+  ".reg .pred v, io, w, ok;\n\t"         \
+  ".reg .b32 kv;\n\t"                    \
+  ".reg .b64 a;\n\t"
 // kTail: the cell is valid or the ray has ended (o == epoch: no write)
 #define VXM_RESOLVE_HEAD_TAIL "setp.eq.u32 io|w, %4, %5;\n\t"
 // otherwise invalid cells (0xffffffff) may also precede the grid entry
@@ -869,31 +898,16 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   "setp.ne.u32 v, %3, -1;\n\t"            \
   "setp.eq.and.u32 io, %4, %5, v;\n\t"    \
   "setp.ne.and.u32 w, %4, %5, v;\n\t"
-#define VXM_RESOLVE_BODY VXM_RESOLVE_COUNT VXM_RESOLVE_RED_K
 #define VXM_RESOLVE_ASM(HEAD)                                                                 \
   asm volatile("{\n\t" VXM_RESOLVE_DECL HEAD VXM_RESOLVE_BODY "}"                            \
                : "+r"(traced_bit), "+r"(lw), "+r"(lt)                                         \
                : "r"(cell[j]), "r"(o[j]), "r"(epoch), "r"(ray_key), "l"(key_base), "r"(dup[j]) \
                : "memory")
-      if constexpr (kBits == 16) {
-#define VXM_RESOLVE_RED_K VXM_RESOLVE_RED16
-        if constexpr (kTail)
-          VXM_RESOLVE_ASM(VXM_RESOLVE_HEAD_TAIL);
-        else
-          VXM_RESOLVE_ASM(VXM_RESOLVE_HEAD_ANY);
-#undef VXM_RESOLVE_RED_K
-      } else {
-#define VXM_RESOLVE_RED_K VXM_RESOLVE_RED32
-        if constexpr (kTail)
-          VXM_RESOLVE_ASM(VXM_RESOLVE_HEAD_TAIL);
-        else
-          VXM_RESOLVE_ASM(VXM_RESOLVE_HEAD_ANY);
-#undef VXM_RESOLVE_RED_K
-      }
+      if constexpr (kTail)
+        VXM_RESOLVE_ASM(VXM_RESOLVE_HEAD_TAIL);
+      else
+        VXM_RESOLVE_ASM(VXM_RESOLVE_HEAD_ANY);
 #undef VXM_RESOLVE_ASM
-#undef VXM_RESOLVE_COUNT
-#undef VXM_RESOLVE_RED32
-#undef VXM_RESOLVE_RED16
 #undef VXM_RESOLVE_HEAD_ANY
 #undef VXM_RESOLVE_HEAD_TAIL
 #undef VXM_RESOLVE_DECL
@@ -1064,7 +1078,7 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
         uint32_t u = fidx;
         const uint32_t kv = ray_key | 1u;
         for (; n > 0; --n) {
-          red_max_key<kBits>(key, u, kv);
+          atomicMax(key + u, kv);
           const bool bx = a0 <= a1 && a0 <= a2;
           const bool by = !bx && a1 <= a2;
           if (bx) { a0 = dadd(a0, e0); u += lin0; }
@@ -1133,30 +1147,21 @@ constexpr long long kSplitMaxRays = 32768;
 
 // `batch` is the number of slots of the whole call (graph branches launch
 // shares of it concurrently, so the GPU is as full as the total says).
-template <int kBits>
-inline void launch_trace_k(const KParams& kp, int slots, int batch, cudaStream_t st) {
+inline void launch_trace(const KParams& kp, int slots, int batch, cudaStream_t st) {
   const int tiles = kp.tiles_x * kp.tiles_y;
   if (batch >= 8) {
-    launch_pdl(trace_bundle_kernel<kBits, 4, 2, VXM_TB_MINB, true, false, false>, dim3((tiles + 1) / 2, slots),
-               dim3(64), 0, st, kp);
+    launch_pdl(trace_bundle_kernel<4, 2, VXM_TB_MINB, true, false, false>, dim3((tiles + 1) / 2, slots), dim3(64), 0, st, kp);
   } else {
     if (static_cast<long long>(kp.vw) * kp.vh * batch <= kSplitMaxRays) {
       // few rays (the GPU far from full): 8x2 tiles, each ray walked as two
       // halves by two lanes; measured -12% / -7% K3 time for a lone cfg2 /
       // cfg1 frame, +11% for a lone cfg3 frame (76k rays)
       const int tiles2 = kp.tiles_x * ((kp.vh + 1) / 2);
-      launch_pdl(trace_bundle_kernel<kBits, 8, 1, 1, false, true, true>, dim3(tiles2, slots), dim3(32), 0, st, kp);
+      launch_pdl(trace_bundle_kernel<8, 1, 1, false, true, true>, dim3(tiles2, slots), dim3(32), 0, st, kp);
     } else {
-      launch_pdl(trace_bundle_kernel<kBits, 8, 1, 1, false, true, false>, dim3(tiles, slots), dim3(32), 0, st, kp);
+      launch_pdl(trace_bundle_kernel<8, 1, 1, false, true, false>, dim3(tiles, slots), dim3(32), 0, st, kp);
     }
   }
-}
-
-inline void launch_trace(const KParams& kp, int slots, int batch, cudaStream_t st) {
-  if (kp.key_bits == 16)
-    launch_trace_k<16>(kp, slots, batch, st);
-  else
-    launch_trace_k<32>(kp, slots, batch, st);
 }
 
 // Sums K3's per-slot counters into the stream's totals (one warp).
@@ -1191,7 +1196,7 @@ struct PerPixelAcc {
 };
 
 __device__ __forceinline__ void pp_visit(const KParams& p, const int* c, const int* end,
-                                         const uint8_t* occ, char* key, uint32_t epoch,
+                                         const uint8_t* occ, uint32_t* key, uint32_t epoch,
                                          PerPixelAcc& acc) {
   if (c[0] == end[0] && c[1] == end[1] && c[2] == end[2]) return;  // the endpoint holds the obstacle
   if (static_cast<unsigned>(c[0]) >= static_cast<unsigned>(p.dx) ||
@@ -1204,17 +1209,14 @@ __device__ __forceinline__ void pp_visit(const KParams& p, const int* c, const i
                        static_cast<uint32_t>(c[2]) * static_cast<uint32_t>(p.dx * p.dy);
   if (occ[idx] != epoch) {
     // Free (every per-pixel write stores the same lowest-priority Free key)
-    if (p.key_bits == 16)
-      reinterpret_cast<uint16_t*>(key)[idx] = static_cast<uint16_t>(KeyFmt<16>::ray_base(-1));
-    else
-      reinterpret_cast<uint32_t*>(key)[idx] = KeyFmt<32>::ray_base(-1);
+    key[idx] = ray_key(p.key_fmt, epoch, -1);
     ++acc.freed;
   }
 }
 
 __device__ __forceinline__ void pp_trace_point(const KParams& p, const double* R, const double* t,
                                                const int* cam, double x, double y, double z,
-                                               const uint8_t* occ, char* key, uint32_t epoch,
+                                               const uint8_t* occ, uint32_t* key, uint32_t epoch,
                                                PerPixelAcc& acc) {
   // world_to_voxel(t_vc.apply(point)) (grid.cpp:54-62, geometry.cpp:10-15):
   // ((R p) + t) / vs, rows left to right, floor, int
@@ -1259,7 +1261,7 @@ __global__ void __launch_bounds__(256) trace_per_pixel_kernel(KParams p, int fro
   if (blockIdx.x == 0 && threadIdx.x == 0) p.counters[s].t_trace = global_ns();
   const FrameParams* fp = p.frames + s;
   const uint32_t epoch = fp->epoch;
-  char* const key = key_slot(p, s);
+  uint32_t* const key = p.key + static_cast<long long>(s) * p.n;
   const uint8_t* occ = p.occ + static_cast<long long>(s) * p.n;
   double R[9], t[3];
 #pragma unroll
@@ -1357,16 +1359,14 @@ __device__ __forceinline__ unsigned count_free16(const uint32_t (&x)[4]) {
   return (m * 0x01010101u) >> 24;
 }
 
-// Keys of the source cells the shifted gather never reads (their destination
-// lies outside the grid) are reset to Unknown here: x in [0, ox) for ox > 0 or
-// [dx + ox, dx) for ox < 0 (every y, z), and likewise along y and z (cells in
-// two slabs are written twice). Every other key is read, and reset if
-// touched, by the gather itself, so the slot's keys are all Unknown again.
-template <int kBits>
-__device__ __forceinline__ void clear_orphan_keys(char* key, int dx, int dy, int dz, int ox, int oy, int oz,
+// Clear-format keys of the source cells the shifted gather never reads
+// (their destination lies outside the grid) are reset to Unknown here: x in
+// [0, ox) for ox > 0 or [dx + ox, dx) for ox < 0 (every y, z), and likewise
+// along y and z (cells in two slabs are written twice). Every other key is
+// read, and reset if touched, by the gather itself, so the slot's keys are
+// all Unknown again.
+__device__ __forceinline__ void clear_orphan_keys(uint32_t* key, int dx, int dy, int dz, int ox, int oy, int oz,
                                                   long long tid, long long nthreads) {
-  using T = typename KeyFmt<kBits>::T;
-  T* const k = reinterpret_cast<T*>(key);
   const int dims[3] = {dx, dy, dz}, off[3] = {ox, oy, oz};
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
@@ -1381,16 +1381,38 @@ __device__ __forceinline__ void clear_orphan_keys(char* key, int dx, int dy, int
       const long long x = i % ex, r = i / ex;
       const long long y = r % ey, z = r / ey;
       const long long cx = a == 0 ? lo + x : x, cy = a == 1 ? lo + y : y, cz = a == 2 ? lo + z : z;
-      k[cx + cy * dx + cz * static_cast<long long>(dx) * dy] = static_cast<T>(KeyFmt<kBits>::kUnknown);
+      key[cx + cy * dx + cz * static_cast<long long>(dx) * dy] = 0u;
     }
   }
 }
 
-template <int kBits>
+// The measurement states of 4 consecutive cells at source cell c (a multiple
+// of 4 away from a 16-byte boundary of the key array): epoch format from the
+// occupancy bytes and keys; clear format from the keys alone, which are then
+// reset to Unknown if the frame touched them.
+template <bool kClear>
+__device__ __forceinline__ uint32_t meas4(const uint8_t* occ, uint32_t* key, long long c, uint32_t epoch) {
+  const uint4 k = __ldcs(reinterpret_cast<const uint4*>(key + c));
+  if constexpr (kClear) {
+    if (touched4(k)) *reinterpret_cast<uint4*>(key + c) = make_uint4(0u, 0u, 0u, 0u);
+    return states4_clear(k);
+  } else {
+    return states4_epoch(__ldcs(reinterpret_cast<const unsigned int*>(occ + c)), k, epoch);
+  }
+}
+template <bool kClear>
+__device__ __forceinline__ uint32_t meas1(const uint8_t* occ, uint32_t* key, long long c, uint32_t epoch) {
+  const uint32_t k = key[c];
+  if constexpr (kClear) {
+    if (k) key[c] = 0u;
+    return decode_clear_key(k);
+  } else {
+    return decode_cell(occ[c], k, epoch);
+  }
+}
+
+template <bool kClear>
 __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int rows_per_warp) {
-  using K4 = Keys4<kBits>;
-  using T = typename KeyFmt<kBits>::T;
-  constexpr int B = kBits / 8;  // key bytes per cell
   pdl_wait();  // K3's keys and counters
   const int s = blockIdx.y;
   if (blockIdx.x == 0 && threadIdx.x == 0) p.counters[s].t_merge = global_ns();
@@ -1399,7 +1421,8 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int r
   const uint32_t cur = fp->cur;
   const int ox = fp->off[0], oy = fp->off[1], oz = fp->off[2];
   const long long base = static_cast<long long>(s) * p.n;
-  char* const key = key_slot(p, s);
+  const uint8_t* occ = p.occ + base;
+  uint32_t* key = p.key + base;
   const uint8_t* src = (cur ? p.loc1 : p.loc0) + base;
   uint8_t* dst = (cur ? p.loc0 : p.loc1) + base;
   const int lane = threadIdx.x & 31;
@@ -1414,11 +1437,11 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int r
   if (ox == 0 && (p.dx & 3) == 0 && p.dx >= 16 && (p.n & 15) == 0 && p.n < (1 << 24)) {
     // No x shift: destination cell c reads c + delta (delta = off_y*dx +
     // off_z*dx*dy), and the valid destination cells of a slab are one run of
-    // whole rows. A thread takes 16 consecutive cells: 16 local bytes and
-    // 16 keys, no per-row arithmetic. A chunk spans at most two
-    // rows (dx >= 16), so it is valid throughout when its first and last
-    // cells are; chunks at a run boundary test their words one by one (a
-    // word never straddles a row since dx % 4 == 0).
+    // whole rows. A thread takes 16 consecutive cells (16 local bytes, their
+    // keys and, epoch format, occupancy bytes), no per-row arithmetic. A
+    // chunk spans at most two rows (dx >= 16), so it is valid throughout when
+    // its first and last cells are; chunks at a run boundary test their words
+    // one by one (a word never straddles a row since dx % 4 == 0).
     const uint32_t dx = p.dx;
     const int delta = oy * p.dx + oz * static_cast<int>(dxy);
     const int ylo = max(0, -oy), yhi = min(p.dy, p.dy - oy), zlo = max(0, -oz), zhi = min(p.dz, p.dz - oz);
@@ -1436,35 +1459,39 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int r
       const int sc = static_cast<int>(c) + delta;
       uint32_t out[4] = {0u, 0u, 0u, 0u};
       if (valid(c) && valid(c + 15)) {
-        uint32_t l[4];
+        uint32_t l[4], o[4] = {0u, 0u, 0u, 0u};
         if (aligned) {
           const uint4 L = __ldcs(reinterpret_cast<const uint4*>(src + sc));
           l[0] = L.x; l[1] = L.y; l[2] = L.z; l[3] = L.w;
+          if constexpr (!kClear) {
+            const uint4 O = __ldcs(reinterpret_cast<const uint4*>(occ + sc));
+            o[0] = O.x; o[1] = O.y; o[2] = O.z; o[3] = O.w;
+          }
         } else {
 #pragma unroll
-          for (int i = 0; i < 4; ++i) l[i] = __ldcs(reinterpret_cast<const unsigned int*>(src + sc + 4 * i));
+          for (int i = 0; i < 4; ++i) {
+            l[i] = __ldcs(reinterpret_cast<const unsigned int*>(src + sc + 4 * i));
+            if constexpr (!kClear) o[i] = __ldcs(reinterpret_cast<const unsigned int*>(occ + sc + 4 * i));
+          }
         }
-        typename K4::V k[4];
+        uint4 k[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) k[i] = K4::load_cs(key + B * (sc + 4 * i));
-        bool any = false;
+        for (int i = 0; i < 4; ++i) k[i] = __ldcs(reinterpret_cast<const uint4*>(key + sc + 4 * i));
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          out[i] = merge4s(l[i], K4::states(k[i]));
-          any = any || K4::touched(k[i]);
-        }
-        if (any) {  // this frame wrote some of them: back to Unknown for the next
-#pragma unroll
-          for (int i = 0; i < 4; ++i) K4::clear(key + B * (sc + 4 * i));
+          if constexpr (kClear) {
+            out[i] = merge4s(l[i], states4_clear(k[i]));
+            if (touched4(k[i])) *reinterpret_cast<uint4*>(key + sc + 4 * i) = make_uint4(0u, 0u, 0u, 0u);
+          } else {
+            out[i] = merge4s(l[i], states4_epoch(o[i], k[i], epoch));
+          }
         }
       } else {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           if (valid(c + 4 * i)) {
             const int si = sc + 4 * i;
-            const typename K4::V k = K4::load(key + B * si);
-            out[i] = merge4s(*reinterpret_cast<const uint32_t*>(src + si), K4::states(k));
-            if (K4::touched(k)) K4::clear(key + B * si);
+            out[i] = merge4s(*reinterpret_cast<const uint32_t*>(src + si), meas4<kClear>(occ, key, si, epoch));
           }
         }
       }
@@ -1478,9 +1505,9 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int r
     // warp's rows before resolving any, so each lane keeps kRowsPerWarp x 24 B
     // in flight (the kernel is HBM-latency bound otherwise).
     const int x0 = lane * 4, sx = x0 + ox;
-    uint32_t l4[kRowsPerWarp], drow[kRowsPerWarp];
+    uint32_t l4[kRowsPerWarp], o4[kRowsPerWarp], drow[kRowsPerWarp];
     long long scell[kRowsPerWarp];
-    typename K4::V k4[kRowsPerWarp];
+    uint4 k4[kRowsPerWarp];
     bool ok[kRowsPerWarp], in_row[kRowsPerWarp];
 #pragma unroll
     for (int rr = 0; rr < kRowsPerWarp; ++rr) {
@@ -1493,18 +1520,26 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int r
       drow[rr] = static_cast<uint32_t>(y) * p.dx + static_cast<uint32_t>(z) * dxy;
       const long long sc = static_cast<long long>(sy) * p.dx + static_cast<long long>(sz) * dxy + sx;
       scell[rr] = sc;
-      l4[rr] = 0u;
-      k4[rr] = K4::unknown();
+      l4[rr] = o4[rr] = 0u;
+      k4[rr] = make_uint4(0u, 0u, 0u, 0u);
       if (ok[rr]) {
         l4[rr] = __ldcs(reinterpret_cast<const unsigned int*>(src + sc));
-        k4[rr] = K4::load_cs(key + B * sc);
+        if constexpr (!kClear) o4[rr] = __ldcs(reinterpret_cast<const unsigned int*>(occ + sc));
+        k4[rr] = __ldcs(reinterpret_cast<const uint4*>(key + sc));
       }
     }
 #pragma unroll
     for (int rr = 0; rr < kRowsPerWarp; ++rr) {
       if (!in_row[rr]) continue;
-      const uint32_t out = ok[rr] ? merge4s(l4[rr], K4::states(k4[rr])) : 0u;
-      if (ok[rr] && K4::touched(k4[rr])) K4::clear(key + B * scell[rr]);
+      uint32_t out = 0u;
+      if (ok[rr]) {
+        if constexpr (kClear) {
+          out = merge4s(l4[rr], states4_clear(k4[rr]));
+          if (touched4(k4[rr])) *reinterpret_cast<uint4*>(key + scell[rr]) = make_uint4(0u, 0u, 0u, 0u);
+        } else {
+          out = merge4s(l4[rr], states4_epoch(o4[rr], k4[rr], epoch));
+        }
+      }
       occ_n += count_occupied4(out);
       free_n += count_free4(out);
       *reinterpret_cast<uint32_t*>(dst + drow[rr] + x0) = out;
@@ -1525,9 +1560,7 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int r
         uint32_t out = 0;
         if (row_ok && sx >= 0 && sx < p.dx) {
           const long long sc = srow + sx;
-          const typename K4::V k = K4::load(key + B * sc);
-          out = merge4s(*reinterpret_cast<const uint32_t*>(src + sc), K4::states(k));
-          if (K4::touched(k)) K4::clear(key + B * sc);
+          out = merge4s(*reinterpret_cast<const uint32_t*>(src + sc), meas4<kClear>(occ, key, sc, epoch));
         }
         occ_n += count_occupied4(out);
         free_n += count_free4(out);
@@ -1540,10 +1573,7 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int r
           uint32_t v = 0;
           if (row_ok && sx >= 0 && sx < p.dx) {
             const long long sc = srow + sx;
-            T* const kc = reinterpret_cast<T*>(key) + sc;
-            const uint32_t k = *kc;
-            v = merge_cell(src[sc], decode_key<kBits>(k));
-            if (k != KeyFmt<kBits>::kUnknown) *kc = static_cast<T>(KeyFmt<kBits>::kUnknown);
+            v = merge_cell(src[sc], meas1<kClear>(occ, key, sc, epoch));
           }
           occ_n += v == 2u;
           free_n += v == 1u;
@@ -1552,9 +1582,9 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int r
       }
     }
   }
-  clear_orphan_keys<kBits>(key, p.dx, p.dy, p.dz, ox, oy, oz,
-                           static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x,
-                           static_cast<long long>(gridDim.x) * blockDim.x);
+  if constexpr (kClear)
+    clear_orphan_keys(key, p.dx, p.dy, p.dz, ox, oy, oz, static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x,
+                      static_cast<long long>(gridDim.x) * blockDim.x);
   unsigned vals[2] = {occ_n, free_n};
   unsigned long long* dsts[2] = {&p.counters[s].occupied, &p.counters[s].freed};
   block_accumulate<2>(vals, dsts);  // ends after every warp's work (a block barrier)
@@ -1563,28 +1593,28 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int r
 
 
 // K4, TMA-staged: a group is merge_tma_rows(dx, dy) consecutive x-rows of
-// one z-slab (about kMergeStageCells cells, so one stage is ~16 KB whatever
+// one z-slab (about kMergeStageCells cells, so one stage is ~19 KB whatever
 // the row length); each block pipelines several groups through two stages.
 // The source rows these come from after the shift (rows y + off_y of slab
 // z + off_z) are contiguous in memory, so one elected thread stages them with
-// two bulk copies (local bytes and keys; each window widened to 16-byte
-// boundaries) on one mbarrier, and the warps merge, shift and count out of
-// shared memory: 4 cells per lane as one word when dims_x and the x shift are
-// multiples of 4, else cell by cell. Keys the frame touched are reset to
-// Unknown in global memory as they are consumed. Needs 16 bytes of slack
-// after each array (allocated by the runtime).
+// bulk copies (local bytes, keys and, epoch format, occupancy bytes; each
+// window widened to 16-byte boundaries) on one mbarrier, and the warps merge,
+// shift and count out of shared memory: 4 cells per lane as one word when
+// dims_x and the x shift are multiples of 4, else cell by cell (clear-format
+// keys the frame touched are reset in global memory as they are consumed).
+// Needs 16 bytes of slack after each array (allocated by the runtime).
 constexpr int kMergeStageCells = 3200;
 constexpr int kMergeTmaMaxDx = 1024;  // larger rows take the direct-load K4
 
 __host__ __device__ constexpr int merge_tma_rows(int dx, int dy) {
   return kMergeStageCells / dx < 1 ? 1 : (kMergeStageCells / dx < dy ? kMergeStageCells / dx : dy);
 }
-// one stage: local bytes and keys (kb bytes each) of `cells` cells, each
-// window widened to 16-byte boundaries, rounded to 16 bytes (the second stage
-// starts right after the first and bulk copies need 16-byte aligned
-// destinations)
-__host__ __device__ constexpr size_t merge_tma_smem_bytes(int cells, int kb = 4) {
-  return (static_cast<size_t>(cells) + 32 + static_cast<size_t>(kb) * cells + 32 + 15) & ~static_cast<size_t>(15);
+// one stage: local and occupancy bytes and keys of `cells` cells, each
+// window widened to 16-byte boundaries
+__host__ __device__ constexpr size_t merge_tma_smem_bytes(int cells) {
+  // rounded to 16 bytes: the second stage starts right after the first and
+  // bulk copies need 16-byte aligned destinations
+  return (2 * (static_cast<size_t>(cells) + 32) + 4 * static_cast<size_t>(cells) + 32 + 15) & ~static_cast<size_t>(15);
 }
 
 __device__ __forceinline__ const unsigned char* align16_down(const void* p) {
@@ -1594,11 +1624,8 @@ __device__ __forceinline__ const unsigned char* align16_up(const void* p) {
   return reinterpret_cast<const unsigned char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~static_cast<uintptr_t>(15));
 }
 
-template <int kBits>
+template <bool kClear>
 __global__ void __launch_bounds__(256) merge_shift_count_tma_kernel(KParams p) {
-  using K4 = Keys4<kBits>;
-  using T = typename KeyFmt<kBits>::T;
-  constexpr int B = kBits / 8;
   extern __shared__ __align__(16) unsigned char msm[];
   __shared__ uint64_t bar[2];
   const int s = blockIdx.y;
@@ -1606,15 +1633,17 @@ __global__ void __launch_bounds__(256) merge_shift_count_tma_kernel(KParams p) {
   const int dx = p.dx, dy = p.dy, dz = p.dz;
   const long long dxy = static_cast<long long>(dx) * dy;
   const int ox = fp->off[0], oy = fp->off[1], oz = fp->off[2];
+  const uint32_t epoch = fp->epoch;
   const uint32_t cur = fp->cur;
   const long long base = static_cast<long long>(s) * p.n;
   const uint8_t* src = (cur ? p.loc1 : p.loc0) + base;
   uint8_t* dst = (cur ? p.loc0 : p.loc1) + base;
-  char* const key = key_slot(p, s);
+  const uint8_t* occ = p.occ + base;
+  uint32_t* key = p.key + base;
   const int rows = merge_tma_rows(dx, dy);
   const int ngy = (dy + rows - 1) / rows;
   const int ngroups = ngy * dz;
-  const size_t stage_bytes = merge_tma_smem_bytes(rows * dx, B);
+  const size_t stage_bytes = merge_tma_smem_bytes(rows * dx);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool vec = ((dx | ox) & 3) == 0;
 
@@ -1642,18 +1671,24 @@ __global__ void __launch_bounds__(256) merge_shift_count_tma_kernel(KParams p) {
   auto issue = [&](int g, int b) {
     const Group G = group(g);
     unsigned char* sl = msm + b * stage_bytes;
-    uint32_t lb = 0, kb = 0;
-    const unsigned char *lw0 = nullptr, *kw0 = nullptr;
+    uint32_t lb = 0, ob = 0, kb = 0;
+    const unsigned char *lw0 = nullptr, *ow0 = nullptr, *kw0 = nullptr;
     if (G.any) {
       lw0 = align16_down(src + G.c0);
-      kw0 = align16_down(key + B * G.c0);
+      kw0 = align16_down(key + G.c0);
       lb = static_cast<uint32_t>(align16_up(src + G.c1) - lw0);
-      kb = static_cast<uint32_t>(align16_up(key + B * G.c1) - kw0);
+      kb = static_cast<uint32_t>(align16_up(key + G.c1) - kw0);
+      if constexpr (!kClear) {
+        ow0 = align16_down(occ + G.c0);
+        ob = static_cast<uint32_t>(align16_up(occ + G.c1) - ow0);
+      }
     }
-    mbar_expect_tx(&bar[b], lb + kb);
+    mbar_expect_tx(&bar[b], lb + ob + kb);
     if (G.any) {
-      unsigned char* sk = sl + ((lb + 15u) & ~15u);
+      unsigned char* so = sl + ((lb + 15u) & ~15u);
+      unsigned char* sk = so + ((ob + 15u) & ~15u);
       bulk_g2s(sl, lw0, lb, &bar[b]);
+      if constexpr (!kClear) bulk_g2s(so, ow0, ob, &bar[b]);
       bulk_g2s(sk, kw0, kb, &bar[b]);
     }
   };
@@ -1678,17 +1713,24 @@ __global__ void __launch_bounds__(256) merge_shift_count_tma_kernel(KParams p) {
     mbar_wait(&bar[b], (it >> 1) & 1);
     const Group G = group(g);
     const unsigned char* sl = msm + b * stage_bytes;
-    int ll = 0, kl = 0;
-    const unsigned char* sk = sl;
+    int ll = 0, ol = 0, kl = 0;
+    const unsigned char *so = sl, *sk = sl;
     if (G.any) {
       const unsigned char* lw0 = align16_down(src + G.c0);
-      const unsigned char* kw0 = align16_down(key + B * G.c0);
+      const unsigned char* kw0 = align16_down(key + G.c0);
       const uint32_t lb = static_cast<uint32_t>(align16_up(src + G.c1) - lw0);
-      sk = sl + ((lb + 15u) & ~15u);
+      uint32_t ob = 0;
+      so = sl + ((lb + 15u) & ~15u);
+      if constexpr (!kClear) {
+        const unsigned char* ow0 = align16_down(occ + G.c0);
+        ob = static_cast<uint32_t>(align16_up(occ + G.c1) - ow0);
+        ol = static_cast<int>((occ + G.c0) - ow0);
+      }
+      sk = so + ((ob + 15u) & ~15u);
       ll = static_cast<int>((src + G.c0) - lw0);
-      kl = static_cast<int>(reinterpret_cast<const unsigned char*>(key + B * G.c0) - kw0);
+      kl = static_cast<int>(reinterpret_cast<const unsigned char*>(key + G.c0) - kw0);
     }
-    char* const kg = key + B * G.c0;  // the group's keys in global memory (reset there)
+    uint32_t* const kg = key + G.c0;  // the group's keys in global memory (clear format: reset there)
     for (int r = warp; r < G.ny; r += blockDim.x >> 5) {
       const int y = G.y0 + r, sy = y + oy;
       const bool row_ok = G.any && sy >= G.sy_lo && sy < G.sy_hi;
@@ -1700,25 +1742,36 @@ __global__ void __launch_bounds__(256) merge_shift_count_tma_kernel(KParams p) {
           const int sx = x0 + ox;
           if (row_ok && sx >= 0 && sx < dx) {
             const long long rel = rrow + sx;
-            const typename K4::V k = K4::load(sk + kl + B * rel);
-            out = merge4s(*reinterpret_cast<const uint32_t*>(sl + ll + rel), K4::states(k));
-            if (K4::touched(k)) K4::clear(kg + B * rel);
+            const uint4 k = *reinterpret_cast<const uint4*>(sk + kl + 4 * rel);
+            uint32_t m4;
+            if constexpr (kClear) {
+              m4 = states4_clear(k);
+              if (touched4(k)) *reinterpret_cast<uint4*>(kg + rel) = make_uint4(0u, 0u, 0u, 0u);
+            } else {
+              m4 = states4_epoch(*reinterpret_cast<const uint32_t*>(so + ol + rel), k, epoch);
+            }
+            out = merge4s(*reinterpret_cast<const uint32_t*>(sl + ll + rel), m4);
           }
           *reinterpret_cast<uint32_t*>(drow + x0) = out;
         } else {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int x = x0 + q, sx = x + ox;
+          for (int k = 0; k < 4; ++k) {
+            const int x = x0 + k, sx = x + ox;
             if (x >= dx) break;
             uint32_t v = 0;
             if (row_ok && sx >= 0 && sx < dx) {
               const long long rel = rrow + sx;
-              const uint32_t k = *reinterpret_cast<const T*>(sk + kl + B * rel);
-              v = merge_cell(sl[ll + rel], decode_key<kBits>(k));
-              if (k != KeyFmt<kBits>::kUnknown)
-                *reinterpret_cast<T*>(kg + B * rel) = static_cast<T>(KeyFmt<kBits>::kUnknown);
+              const uint32_t kk = *reinterpret_cast<const uint32_t*>(sk + kl + 4 * rel);
+              uint32_t m;
+              if constexpr (kClear) {
+                m = decode_clear_key(kk);
+                if (kk) kg[rel] = 0u;
+              } else {
+                m = decode_cell(so[ol + rel], kk, epoch);
+              }
+              v = merge_cell(sl[ll + rel], m);
             }
-            out |= v << (8 * q);
+            out |= v << (8 * k);
             drow[x] = static_cast<uint8_t>(v);
           }
         }
@@ -1728,9 +1781,9 @@ __global__ void __launch_bounds__(256) merge_shift_count_tma_kernel(KParams p) {
     }
     __syncthreads();  // stage b is refilled two groups from now
   }
-  clear_orphan_keys<kBits>(key, dx, dy, dz, ox, oy, oz, static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x,
-                           static_cast<long long>(gridDim.x) * blockDim.x);
-  __syncthreads();
+  if constexpr (kClear)
+    clear_orphan_keys(key, dx, dy, dz, ox, oy, oz, static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x,
+                      static_cast<long long>(gridDim.x) * blockDim.x);
   // every warp has passed the last group's barrier
   if (threadIdx.x == 0) atomicMax(&p.counters[s].t_end, global_ns());
   unsigned vals[2] = {occ_n, free_n};
@@ -1778,11 +1831,8 @@ __device__ __forceinline__ void add_frame_counts(const uint32_t (&packed)[U / 2]
   }
 }
 
-template <int kBits>
+template <bool kClear>
 __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
-  using K4 = Keys4<kBits>;
-  using T = typename KeyFmt<kBits>::T;
-  constexpr int B = kBits / 8;
   pdl_wait();  // K3's keys and counters
   constexpr int U = 4;  // frames whose loads are issued together
   __shared__ unsigned cnt[2 * kMaxFramesPerCall];           // occupied, then freed, per frame
@@ -1823,10 +1873,11 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
   const uint32_t cur = f0->cur;
   const uint8_t* src = (cur ? p.loc1 : p.loc0) + static_cast<long long>(s) * p.n;
   uint8_t* dst = (cur ? p.loc0 : p.loc1) + static_cast<long long>(s) * p.n;
-  // frame k's keys at key0 + k * n * B; every key a chain meets in the grid is
-  // read (even when the cell shifts out of the grid afterwards) and reset to
-  // Unknown if touched, so all F slots end all-Unknown
-  char* const key0 = key_slot(p, static_cast<long long>(s) * F);
+  const uint8_t* occ0 = p.occ + static_cast<long long>(s) * F * p.n;
+  // clear format: every key a chain meets in the grid is read (also when the
+  // cell shifts out of the grid afterwards) and reset to Unknown if touched,
+  // so all F slots end all-Unknown
+  uint32_t* key0 = p.key + static_cast<long long>(s) * F * p.n;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   if (vec_ok) {
     // Every frame's x shift is a multiple of 4 (and dims_x too): a thread
@@ -1854,17 +1905,19 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
       for (int k0 = 0; k0 < F; k0 += U) {
         bool in_c[U];
         int pos[U];
-        typename K4::V kk[U];
+        uint32_t o[U];
+        uint4 kk[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) pos[u] = group_of(k0 + u + 1, in_c[u]);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const bool in_r = u == 0 ? in_prev : in_c[u - 1];
           const int r = u == 0 ? pos_prev : pos[u - 1];
-          const bool ld = k0 + u < F && in_r;
+          const bool ld = k0 + u < F && in_r && (kClear || in_c[u]);
           const long long off = static_cast<long long>(k0 + u) * p.n + r;
-          kk[u] = ld ? K4::load_cs(key0 + B * off) : K4::unknown();
-          if (ld && K4::touched(kk[u])) K4::clear(key0 + B * off);
+          o[u] = ld && !kClear ? __ldcs(reinterpret_cast<const uint32_t*>(occ0 + off)) : 0u;
+          kk[u] = ld ? __ldcs(reinterpret_cast<const uint4*>(key0 + off)) : make_uint4(0u, 0u, 0u, 0u);
+          if (kClear && ld && touched4(kk[u])) *reinterpret_cast<uint4*>(key0 + off) = make_uint4(0u, 0u, 0u, 0u);
         }
         // per frame: Occupied / Free counts of this thread's 4 cells (each
         // <= 4, so a warp sum fits a byte); two frames share one reduction
@@ -1874,7 +1927,8 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
           const int k = k0 + u;
           if (k >= F) break;
           const bool in_r = u == 0 ? in_prev : in_c[u - 1];
-          if (in_c[u]) val = in_r ? merge4s(val, K4::states(kk[u])) : 0u;  // shifted in: Unknown
+          if (in_c[u])  // shifted in: Unknown
+            val = in_r ? merge4s(val, kClear ? states4_clear(kk[u]) : states4_epoch(o[u], kk[u], ep[k])) : 0u;
           const unsigned oc = in_c[u] ? count_occupied4(val) : 0u, fr = in_c[u] ? count_free4(val) : 0u;
           packed[u >> 1] |= (oc | (fr << 8)) << (16 * (u & 1));
         }
@@ -1910,17 +1964,18 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
       // positions after frames k0..k0+U-1, then all their loads, then the merges
       bool in_c[U];
       int pos[U];
-      uint32_t kk[U];
+      uint32_t o[U], kk[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) pos[u] = cell_of(k0 + u + 1, in_c[u]);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const bool in_r = u == 0 ? in_prev : in_c[u - 1];
         const int r = u == 0 ? pos_prev : pos[u - 1];
-        const bool ld = k0 + u < F && in_r;
-        T* const kc = reinterpret_cast<T*>(key0) + static_cast<long long>(k0 + u) * p.n + r;
-        kk[u] = ld ? static_cast<uint32_t>(__ldcs(kc)) : KeyFmt<kBits>::kUnknown;
-        if (kk[u] != KeyFmt<kBits>::kUnknown) *kc = static_cast<T>(KeyFmt<kBits>::kUnknown);
+        const bool ld = k0 + u < F && in_r && (kClear || in_c[u]);
+        const long long off = static_cast<long long>(k0 + u) * p.n + r;
+        o[u] = ld && !kClear ? __ldcs(occ0 + off) : 0u;
+        kk[u] = ld ? __ldcs(key0 + off) : 0u;
+        if (kClear && kk[u]) key0[off] = 0u;
       }
       uint32_t packed[U / 2] = {};
 #pragma unroll
@@ -1928,7 +1983,8 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
         const int k = k0 + u;
         if (k >= F) break;
         const bool in_r = u == 0 ? in_prev : in_c[u - 1];
-        if (in_c[u]) val = in_r ? merge_cell(val, decode_key<kBits>(kk[u])) : 0u;  // shifted in: Unknown
+        if (in_c[u])  // shifted in: Unknown
+          val = in_r ? merge_cell(val, kClear ? decode_clear_key(kk[u]) : decode_cell(o[u], kk[u], ep[k])) : 0u;
         const unsigned oc = in_c[u] && val == 2u ? 1u : 0u, fr = in_c[u] && val == 1u ? 1u : 0u;
         packed[u >> 1] |= (oc | (fr << 8)) << (16 * (u & 1));
       }

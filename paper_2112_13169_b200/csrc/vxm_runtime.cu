@@ -24,6 +24,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/vxm.h"
@@ -254,11 +255,12 @@ struct vxm_ctx {
   uint8_t* occ = nullptr;
   uint8_t* ctr = nullptr;
   uint8_t* rowflag = nullptr;  // per slot: dy*dz x-row flags (vox_inf > 0)
-  char* key = nullptr;         // measurement keys, key_bits / 8 bytes per cell (vxm_device.cuh)
-  int key_bits = 32;
+  uint32_t* key = nullptr;     // measurement keys (vxm_device.cuh KeyFmt)
+  int key_fmt = vxm::kEpochKeys;
   uint8_t* loc[2] = {nullptr, nullptr};
   double* qtab = nullptr;  // W column + H row back-projection factors
   uint32_t* dbits = nullptr;  // x-dilated centre bit rows (vox_inf > 0)
+  uint8_t* dtmp = nullptr;    // generic dilation passes (large radii / rows)
   vxm::Counters* counters = nullptr;
   // FrameParams on the device, two buffers: the upload for the next call
   // (on param_stream) overlaps the graph of this one, and each buffer has
@@ -290,6 +292,17 @@ struct vxm_ctx {
   int desync_started = 0;              // branches whose bstart brackets the last call
   cudaEvent_t input_ready = nullptr;  // set by a call whose inputs arrive on another stream
   cudaEvent_t user_input = nullptr;   // vxm_set_input_event: the next call's kernels wait for it
+  // asynchronous snapshot (vxm_snapshot_save_async): D2H of one local grid on
+  // snap_stream into pinned snap_host, then a writer thread; the next call's
+  // kernels wait for snap_copied (the ping-pong buffer is rewritten two
+  // frames later)
+  cudaStream_t snap_stream = nullptr;
+  cudaEvent_t snap_start = nullptr, snap_copied = nullptr;
+  uint8_t* snap_host = nullptr;
+  bool snap_wait_pending = false;
+  std::thread snap_thread;
+  int snap_status = 0;
+  std::string snap_error;
   cudaEvent_t tail_ev = nullptr;      // end of the last call that ran on the context stream itself
   bool tail_pending = false;          // ... which desynchronised branches must still wait for
   std::vector<int> wrapped;           // slots whose arrays are cleared before this call (epoch wrap)
@@ -374,10 +387,11 @@ void launch_stages(vxm_ctx* c, bool cloud, bool capturing, int s0, int S, cudaSt
   kp.counters += s0;
   kp.counters_out += s0;
   kp.occ += n * s0;
-  kp.key = vxm::key_slot(kp, s0);
+  kp.key += c->n * s0;
   if (kp.ctr) kp.ctr += n * s0;
   if (kp.rowflag) kp.rowflag += c->rows * s0;
   if (kp.dbits) kp.dbits += static_cast<long long>(vxm::dilate_row_words(kp.dx)) * c->rows * s0;
+  if (kp.dtmp) kp.dtmp += 2 * n * s0;
   kp.loc0 += n * (s0 / c->F);
   kp.loc1 += n * (s0 / c->F);
   auto mark = [&](cudaEvent_t e) {
@@ -452,10 +466,10 @@ void launch_merge_chain(vxm_ctx* c, const vxm::KParams& kp, int F, int streams, 
   const long long blocks = std::min<long long>((chains + kMergeThreads - 1) / kMergeThreads,
                                                std::max<long long>(1, c->nsm * 8LL / streams));
   dim3 grid(static_cast<unsigned>(std::max<long long>(1, blocks)), streams);
-  if (kp.key_bits == 16)
-    VXM_CK(vxm::launch_pdl(vxm::merge_sequence_kernel<16>, grid, dim3(kMergeThreads), 0, st, kp, F));
+  if (kp.key_fmt == vxm::kClearKeys)
+    VXM_CK(vxm::launch_pdl(vxm::merge_sequence_kernel<true>, grid, dim3(kMergeThreads), 0, st, kp, F));
   else
-    VXM_CK(vxm::launch_pdl(vxm::merge_sequence_kernel<32>, grid, dim3(kMergeThreads), 0, st, kp, F));
+    VXM_CK(vxm::launch_pdl(vxm::merge_sequence_kernel<false>, grid, dim3(kMergeThreads), 0, st, kp, F));
   VXM_CK(cudaGetLastError());
 }
 
@@ -472,11 +486,11 @@ void launch_merge(vxm_ctx* c, const vxm::KParams& kp, int S, cudaStream_t st) {
     const long long groups = static_cast<long long>((kp.dy + rows - 1) / rows) * kp.dz;
     const long long per_slot = std::max(1LL, std::min(groups, c->nsm * 8LL / S));
     const dim3 grid(static_cast<unsigned>(per_slot), S);
-    const size_t smem = 2 * vxm::merge_tma_smem_bytes(rows * kp.dx, kp.key_bits / 8);
-    if (kp.key_bits == 16)
-      VXM_CK(vxm::launch_pdl(vxm::merge_shift_count_tma_kernel<16>, grid, dim3(kMergeThreads), smem, st, kp));
+    const size_t smem = 2 * vxm::merge_tma_smem_bytes(rows * kp.dx);
+    if (kp.key_fmt == vxm::kClearKeys)
+      VXM_CK(vxm::launch_pdl(vxm::merge_shift_count_tma_kernel<true>, grid, dim3(kMergeThreads), smem, st, kp));
     else
-      VXM_CK(vxm::launch_pdl(vxm::merge_shift_count_tma_kernel<32>, grid, dim3(kMergeThreads), smem, st, kp));
+      VXM_CK(vxm::launch_pdl(vxm::merge_shift_count_tma_kernel<false>, grid, dim3(kMergeThreads), smem, st, kp));
   } else if (c->F == 1) {
     const long long rows = static_cast<long long>(kp.dy) * kp.dz;
     // one row per warp unless the batch fills the GPU several times over
@@ -485,10 +499,10 @@ void launch_merge(vxm_ctx* c, const vxm::KParams& kp, int S, cudaStream_t st) {
     const int rpw = static_cast<int>(std::max(1LL, std::min<long long>(vxm::kRowsPerWarp, warps / fill)));
     const int rows_per_block = kMergeThreads / 32 * rpw;
     dim3 grid(static_cast<unsigned>((rows + rows_per_block - 1) / rows_per_block), S);
-    if (kp.key_bits == 16)
-      VXM_CK(vxm::launch_pdl(vxm::merge_shift_count_kernel<16>, grid, dim3(kMergeThreads), 0, st, kp, rpw));
+    if (kp.key_fmt == vxm::kClearKeys)
+      VXM_CK(vxm::launch_pdl(vxm::merge_shift_count_kernel<true>, grid, dim3(kMergeThreads), 0, st, kp, rpw));
     else
-      VXM_CK(vxm::launch_pdl(vxm::merge_shift_count_kernel<32>, grid, dim3(kMergeThreads), 0, st, kp, rpw));
+      VXM_CK(vxm::launch_pdl(vxm::merge_shift_count_kernel<false>, grid, dim3(kMergeThreads), 0, st, kp, rpw));
     VXM_CK(cudaGetLastError());
   } else {
     launch_merge_chain(c, kp, c->F, S / c->F, st);
@@ -545,7 +559,7 @@ void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
         kp.counters += s0;
         kp.counters_out += s0;
         kp.occ += c->n * s0;
-        kp.key = vxm::key_slot(kp, s0);
+        kp.key += c->n * s0;
         launch_merge_chain(c, kp, s1 - s0, 1, bs);
         launch_publish(kp, s1 - s0, bs);
         if (b + 1 < B) VXM_CK(cudaEventRecord(c->chain[b], bs));
@@ -646,7 +660,7 @@ void prepare_frames(vxm_ctx* c, const vxm_pose* poses, const float* depth_dev_ba
       if (depth_dev_base) f.depth = depth_dev_base + frame_elems * slot;
       f.cur = c->cur[s] ^ static_cast<uint32_t>(range & 1);  // each chained range flips the buffers
       f.occ_s = c->occ + c->n * slot;
-      f.key_s = vxm::key_slot(c->kp, slot);
+      f.key_s = c->key + c->n * slot;
       int32_t off[3];
       const bool moved = shift_decision(c->cfg.grid, org, poses[slot].translation, off);
       for (int a = 0; a < 3; ++a) {
@@ -703,7 +717,9 @@ void clear_wrapped(vxm_ctx* c, int s0, int S, cudaStream_t st) {
     VXM_CK(cudaMemsetAsync(c->occ + c->n * slot, 0, c->n, st));
     if (c->ctr) VXM_CK(cudaMemsetAsync(c->ctr + c->n * slot, 0, c->n, st));
     if (c->rowflag) VXM_CK(cudaMemsetAsync(c->rowflag + c->rows * slot, 0, c->rows, st));
-    // (the keys need no clearing: the merge leaves them all Unknown)
+    // epoch keys are cleared with the rest; clear-format keys are all
+    // Unknown after every merge already
+    if (c->key_fmt == vxm::kEpochKeys) VXM_CK(cudaMemsetAsync(c->key + c->n * slot, 0, sizeof(uint32_t) * c->n, st));
   }
 }
 
@@ -739,6 +755,15 @@ void run_frame(vxm_ctx* c, bool cloud, bool direct = false) {
   bool desync_call = false;
   cudaEvent_t user_input = c->user_input;  // (one call)
   c->user_input = nullptr;
+  cudaEvent_t snap_ev = nullptr;
+  if (c->snap_wait_pending) {
+    // a snapshot's D2H reads the current local buffers: this call's kernels
+    // (its merge writes the other buffer, the next call's this one) start
+    // after it; the copy itself waits only for the calls issued before it
+    c->snap_wait_pending = false;
+    snap_ev = c->snap_copied;
+    VXM_CK(cudaStreamWaitEvent(c->stream, snap_ev, 0));
+  }
   if (graphs && !cloud && (c->F == 1 || c->S >= B) && B > 1 && !stage_events_wanted(c) &&
       !(c->flags & VXM_FLAG_NO_DESYNC)) {
     // Desynchronised batch: branch b's graph (its streams' stages) runs on
@@ -763,6 +788,7 @@ void run_frame(vxm_ctx* c, bool cloud, bool direct = false) {
       VXM_CK(cudaStreamWaitEvent(bs, c->pp_ready[pp], 0));
       if (c->input_ready) VXM_CK(cudaStreamWaitEvent(bs, c->input_ready, 0));
       if (user_input) VXM_CK(cudaStreamWaitEvent(bs, user_input, 0));
+      if (snap_ev) VXM_CK(cudaStreamWaitEvent(bs, snap_ev, 0));
       clear_wrapped(c, s0, s1 - s0, bs);
       cudaGraphExec_t& g = c->bgraph[gi][pp][b];
       if (!g) g = capture_branch(c, s0, s1 - s0, bs);
@@ -800,6 +826,7 @@ void run_frame(vxm_ctx* c, bool cloud, bool direct = false) {
       VXM_CK(cudaStreamWaitEvent(bs, c->pp_ready[pp], 0));
       if (c->input_ready) VXM_CK(cudaStreamWaitEvent(bs, c->input_ready, 0));
       if (user_input) VXM_CK(cudaStreamWaitEvent(bs, user_input, 0));
+      if (snap_ev) VXM_CK(cudaStreamWaitEvent(bs, snap_ev, 0));
       clear_wrapped(c, s0, s1 - s0, bs);
       VXM_CK(cudaEventRecord(c->bstart[b], bs));
       launch_stages(c, false, false, s0, s1 - s0, bs, false, false);
@@ -809,7 +836,7 @@ void run_frame(vxm_ctx* c, bool cloud, bool direct = false) {
       kp.counters += s0;
       kp.counters_out += s0;
       kp.occ += c->n * s0;
-      kp.key = vxm::key_slot(kp, s0);
+      kp.key += c->n * s0;
       launch_merge_chain(c, kp, s1 - s0, 1, bs);
       launch_publish(kp, s1 - s0, bs);
       VXM_CK(cudaEventRecord(c->chain[b], bs));
@@ -914,6 +941,12 @@ void collect_stats(vxm_ctx* c, vxm_stats* out) {
   }
 }
 
+// waits for a pending asynchronous snapshot's copy and file (keeps its status
+// for vxm_snapshot_wait)
+void snapshot_quiesce(vxm_ctx* c) {
+  if (c->snap_thread.joinable()) c->snap_thread.join();
+}
+
 bool is_pinned(const void* p) {
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -926,6 +959,14 @@ bool is_pinned(const void* p) {
 void destroy_ctx(vxm_ctx* c) {
   if (!c) return;
   if (c->device >= 0) cudaSetDevice(c->device);
+  if (c->snap_thread.joinable()) c->snap_thread.join();
+  if (c->snap_stream) {
+    cudaStreamSynchronize(c->snap_stream);
+    cudaStreamDestroy(c->snap_stream);
+  }
+  if (c->snap_start) cudaEventDestroy(c->snap_start);
+  if (c->snap_copied) cudaEventDestroy(c->snap_copied);
+  if (c->snap_host) cudaFreeHost(c->snap_host);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto& gg : c->graph_exec)
     for (auto& g : gg)
@@ -955,6 +996,7 @@ void destroy_ctx(vxm_ctx* c) {
   cudaFree(c->key);
   cudaFree(c->qtab);
   cudaFree(c->dbits);
+  cudaFree(c->dtmp);
   cudaFree(c->loc[0]);
   cudaFree(c->loc[1]);
   cudaFree(c->counters);
@@ -1078,10 +1120,10 @@ int vxm_create_multi(const vxm_config* cfg, int32_t n_streams, int32_t frames_pe
     c->rows = static_cast<long long>(g.dims[1]) * g.dims[2];
     bundle_dims(cfg->camera, cfg->depth, g.vox_size, c->bundle);
     const long long rays = static_cast<long long>(c->bundle[1]) * c->bundle[2];
-    if (rays > vxm::KeyFmt<32>::kMaxRays)
-      throw InvalidArg{"ray bundle exceeds " + std::to_string(vxm::KeyFmt<32>::kMaxRays) + " rays"};
-    // 16-bit keys whenever the bundle fits them (halves the key traffic)
-    c->key_bits = rays <= vxm::KeyFmt<16>::kMaxRays && !(flags & VXM_FLAG_WIDE_KEYS) ? 16 : 32;
+    if (rays > vxm::kMaxClearRays)
+      throw InvalidArg{"ray bundle exceeds " + std::to_string(vxm::kMaxClearRays) + " rays"};
+    // epoch-tagged keys whenever the bundle fits their 17-bit ray field
+    c->key_fmt = rays <= vxm::kMaxEpochRays && !(flags & VXM_FLAG_CLEAR_KEYS) ? vxm::kEpochKeys : vxm::kClearKeys;
 
     VXM_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     for (auto& e : c->ev) VXM_CK(cudaEventCreate(&e));
@@ -1092,15 +1134,8 @@ int vxm_create_multi(const vxm_config* cfg, int32_t n_streams, int32_t frames_pe
     // widened to 16-byte boundaries
     VXM_CK(cudaMalloc(&c->occ, c->n * S + 64));
     VXM_CK(cudaMemsetAsync(c->occ, 0, c->n * S, c->stream));
-    VXM_CK(cudaMalloc(&c->key, static_cast<size_t>(c->key_bits / 8) * c->n * S + 64));
-    if (c->key_bits == 16) {
-      vxm::fill_u16_kernel<<<static_cast<unsigned>(std::min<long long>((c->n * S + 255) / 256, 148LL * 16)), 256, 0,
-                             c->stream>>>(reinterpret_cast<uint16_t*>(c->key), c->n * static_cast<long long>(S),
-                                          static_cast<uint16_t>(vxm::KeyFmt<16>::kUnknown));
-      VXM_CK(cudaGetLastError());
-    } else {
-      VXM_CK(cudaMemsetAsync(c->key, 0, sizeof(uint32_t) * c->n * S, c->stream));
-    }
+    VXM_CK(cudaMalloc(&c->key, sizeof(uint32_t) * c->n * S + 64));
+    VXM_CK(cudaMemsetAsync(c->key, 0, sizeof(uint32_t) * c->n * S, c->stream));
     if (cfg->vox_inf > 0) {
       VXM_CK(cudaMalloc(&c->ctr, c->n * S));
       VXM_CK(cudaMemsetAsync(c->ctr, 0, c->n * S, c->stream));
@@ -1172,8 +1207,8 @@ int vxm_create_multi(const vxm_config* cfg, int32_t n_streams, int32_t frames_pe
     kp.vh = c->bundle[2];
     kp.tiles_x = (kp.vw + 7) / 8;
     kp.tiles_y = (kp.vh + 3) / 4;
-    for (const void* fn : {reinterpret_cast<const void*>(vxm::merge_shift_count_tma_kernel<16>),
-                           reinterpret_cast<const void*>(vxm::merge_shift_count_tma_kernel<32>)})
+    for (const void* fn : {reinterpret_cast<const void*>(vxm::merge_shift_count_tma_kernel<false>),
+                           reinterpret_cast<const void*>(vxm::merge_shift_count_tma_kernel<true>)})
       VXM_CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(2 * vxm::merge_tma_smem_bytes(vxm::kMergeStageCells))));
     for (const void* fn : {reinterpret_cast<const void*>(vxm::populate_depth_tma_kernel<true>),
@@ -1185,7 +1220,7 @@ int vxm_create_multi(const vxm_config* cfg, int32_t n_streams, int32_t frames_pe
     kp.ctr = c->ctr;
     kp.rowflag = c->rowflag;
     kp.key = c->key;
-    kp.key_bits = c->key_bits;
+    kp.key_fmt = c->key_fmt;
     kp.loc0 = c->loc[0];
     kp.loc1 = c->loc[1];
     kp.counters = c->counters;
@@ -1193,16 +1228,17 @@ int vxm_create_multi(const vxm_config* cfg, int32_t n_streams, int32_t frames_pe
 
     kp.frames = c->frames_pp[0];
     if (cfg->vox_inf > 0) {
-      const size_t smem = vxm::dilate_smem_bytes(cfg->vox_inf, kp.dx);
-      if (cfg->vox_inf > vxm::kMaxVoxInf || smem > 200 * 1024 || kp.dx > 1024)
-        throw InvalidArg{"vox_inf " + std::to_string(cfg->vox_inf) + " / dims_x " + std::to_string(kp.dx) +
-                         " exceed the dilation limits (vox_inf <= " + std::to_string(vxm::kMaxVoxInf) +
-                         ", dims_x <= 1024)"};
-      const size_t words = static_cast<size_t>(vxm::dilate_row_words(kp.dx)) * kp.dy * kp.dz * S;
-      VXM_CK(cudaMalloc(&c->dbits, sizeof(uint32_t) * words));
-      kp.dbits = c->dbits;
-      VXM_CK(vxm::dilate_set_smem(static_cast<int>(
-          vxm::dilate_smem_bytes(cfg->vox_inf, kp.dx, vxm::dilate_fused(cfg->vox_inf, kp.dx)))));
+      if (vxm::dilate_generic(cfg->vox_inf, kp.dx)) {
+        // radii / rows beyond the tile kernels: the generic line passes
+        VXM_CK(cudaMalloc(&c->dtmp, 2 * static_cast<size_t>(c->n) * S));
+        kp.dtmp = c->dtmp;
+      } else {
+        const size_t words = static_cast<size_t>(vxm::dilate_row_words(kp.dx)) * kp.dy * kp.dz * S;
+        VXM_CK(cudaMalloc(&c->dbits, sizeof(uint32_t) * words));
+        kp.dbits = c->dbits;
+        VXM_CK(vxm::dilate_set_smem(static_cast<int>(
+            vxm::dilate_smem_bytes(cfg->vox_inf, kp.dx, vxm::dilate_fused(cfg->vox_inf, kp.dx)))));
+      }
     }
     VXM_CK(cudaStreamSynchronize(c->stream));
   });
@@ -1403,6 +1439,7 @@ int vxm_download_local(vxm_ctx* ctx, int32_t s, uint8_t* cells, double origin[3]
 int vxm_upload_local(vxm_ctx* ctx, int32_t s, const uint8_t* cells, const double origin[3]) {
   return guarded([&] {
     if (!ctx || s < 0 || s >= ctx->S) throw InvalidArg{"stream index out of range"};
+    snapshot_quiesce(ctx);  // a pending snapshot copy reads the buffer this overwrites
     if (origin && !all_finite(origin, 3)) throw InvalidArg{"grid origin must be finite"};
     VXM_CK(cudaSetDevice(ctx->device));
     collect_stats(ctx, nullptr);
@@ -1484,6 +1521,72 @@ int vxm_snapshot_save(vxm_ctx* ctx, int32_t s, const char* path) {
   });
 }
 
+namespace {
+// joins the writer thread of the previous asynchronous snapshot
+int snapshot_join(vxm_ctx* ctx) {
+  if (ctx->snap_thread.joinable()) ctx->snap_thread.join();
+  const int rc = ctx->snap_status;
+  if (rc != VXM_OK) g_err = ctx->snap_error;
+  ctx->snap_status = VXM_OK;
+  return rc;
+}
+}  // namespace
+
+int vxm_snapshot_save_async(vxm_ctx* ctx, int32_t s, const char* path) {
+  if (ctx) {
+    const int prev = snapshot_join(ctx);
+    if (prev != VXM_OK) return prev;
+  }
+  return guarded([&] {
+    if (!ctx || s < 0 || s >= ctx->S) throw InvalidArg{"stream index out of range"};
+    if (!path) throw InvalidArg{"null path"};
+    VXM_CK(cudaSetDevice(ctx->device));
+    if (!ctx->snap_stream) {
+      VXM_CK(cudaStreamCreateWithFlags(&ctx->snap_stream, cudaStreamNonBlocking));
+      VXM_CK(cudaEventCreateWithFlags(&ctx->snap_start, cudaEventDisableTiming));
+      VXM_CK(cudaEventCreateWithFlags(&ctx->snap_copied, cudaEventDisableTiming));
+      VXM_CK(cudaMallocHost(&ctx->snap_host, static_cast<size_t>(ctx->n)));
+    }
+    // the grid as it stands after every call issued so far: the context
+    // stream joins each call's branches, so an event there marks that point
+    VXM_CK(cudaEventRecord(ctx->snap_start, ctx->stream));
+    VXM_CK(cudaStreamWaitEvent(ctx->snap_stream, ctx->snap_start, 0));
+    VXM_CK(cudaMemcpyAsync(ctx->snap_host, ctx->loc[ctx->cur[s]] + ctx->n * s, static_cast<size_t>(ctx->n),
+                           cudaMemcpyDeviceToHost, ctx->snap_stream));
+    VXM_CK(cudaEventRecord(ctx->snap_copied, ctx->snap_stream));
+    ctx->snap_wait_pending = true;
+    // header fields as of now (host state: the origin after the last call)
+    int dims[3];
+    double origin[3];
+    for (int a = 0; a < 3; ++a) {
+      dims[a] = ctx->cfg.grid.dims[a];
+      origin[a] = ctx->origin[3 * s + a];
+    }
+    const double vs = ctx->cfg.grid.vox_size;
+    const std::string file(path);
+    const int device = ctx->device;
+    ctx->snap_thread = std::thread([ctx, dims, origin, vs, file, device]() {
+      cudaSetDevice(device);
+      if (cudaEventSynchronize(ctx->snap_copied) != cudaSuccess) {
+        ctx->snap_status = VXM_ECUDA;
+        ctx->snap_error = "snapshot copy failed";
+        return;
+      }
+      try {
+        write_voxgrid(file.c_str(), dims, vs, origin, ctx->snap_host);
+      } catch (const IoError& e) {
+        ctx->snap_status = VXM_EIO;
+        ctx->snap_error = e.what;
+      }
+    });
+  });
+}
+
+int vxm_snapshot_wait(vxm_ctx* ctx) {
+  if (!ctx) return fail(VXM_EINVAL, "null context");
+  return snapshot_join(ctx);
+}
+
 int vxm_snapshot_load(vxm_ctx* ctx, int32_t s, const char* path) {
   return guarded([&] {
     if (!ctx || s < 0 || s >= ctx->S) throw InvalidArg{"stream index out of range"};
@@ -1494,6 +1597,7 @@ int vxm_snapshot_load(vxm_ctx* ctx, int32_t s, const char* path) {
     if (h.dims[0] != g.dims[0] || h.dims[1] != g.dims[1] || h.dims[2] != g.dims[2] || h.vox_size != g.vox_size)
       throw InvalidArg{"snapshot grid does not match the pipeline's GridSpec"};
     VXM_CK(cudaSetDevice(ctx->device));
+    snapshot_quiesce(ctx);
     collect_stats(ctx, nullptr);
     VXM_CK(cudaMemcpy(ctx->loc[ctx->cur[s]] + ctx->n * s, buf.data() + h.data_offset, ctx->n,
                       cudaMemcpyHostToDevice));

@@ -77,8 +77,8 @@ unsigned blocks_for(long long n, int threads, int cap = 148 * 16) {
 
 constexpr uint32_t kEpoch = 1u;
 
-// key width of a stage call: 16-bit keys when the bundle allows (as a context)
-int key_bits_for(long long rays) { return rays <= vxm::KeyFmt<16>::kMaxRays ? 16 : 32; }
+// key format of a stage call, as a context would choose it
+int key_fmt_for(long long rays) { return rays <= vxm::kMaxEpochRays ? vxm::kEpochKeys : vxm::kClearKeys; }
 
 // One-stream kernel parameters for a grid (no camera, no bundle).
 vxm::KParams grid_params(const vxm_grid_spec& g) {
@@ -141,10 +141,10 @@ int vxm_populate_occupied(const vxm_grid_spec* grid, uint8_t* ms, const double* 
     VXM_SCK(cudaMemset(d_cnt.p, 0, sizeof(vxm::Counters)));
     if (d_ctr.p) VXM_SCK(cudaMemset(d_ctr.p, 0, N));
     if (d_rowflag.p) VXM_SCK(cudaMemset(d_rowflag.p, 0, static_cast<size_t>(kp.dy) * kp.dz));
-    vxm::encode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_ms.p, d_occ.p, d_key.p, N, kEpoch, 32);
+    vxm::encode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_ms.p, d_occ.p, d_key.p, N, kEpoch, vxm::kEpochKeys);
     kp.occ = d_occ.p;
     kp.key = d_key.p;
-    kp.key_bits = 32;
+    kp.key_fmt = vxm::kEpochKeys;
     kp.ctr = d_ctr.p;
     kp.rowflag = d_rowflag.p;
     kp.vox_inf = vox_inf;
@@ -152,18 +152,20 @@ int vxm_populate_occupied(const vxm_grid_spec* grid, uint8_t* ms, const double* 
     kp.frames = d_frame.p;
     vxm::populate_cloud_kernel<<<dim3(blocks_for(static_cast<long long>(n), 256), 1), 256>>>(kp);
     VXM_SCK(cudaGetLastError());
-    DevBuf<uint32_t> d_bits(vox_inf > 0 ? static_cast<size_t>(vxm::dilate_row_words(kp.dx)) * kp.dy * kp.dz : 0);
+    const bool generic = vox_inf > 0 && vxm::dilate_generic(vox_inf, kp.dx);
+    DevBuf<uint32_t> d_bits(vox_inf > 0 && !generic
+                                ? static_cast<size_t>(vxm::dilate_row_words(kp.dx)) * kp.dy * kp.dz : 0);
+    DevBuf<uint8_t> d_tmp(generic ? 2 * static_cast<size_t>(N) : 0);
     if (vox_inf > 0) {
       const int r = vox_inf;
-      const size_t smem = vxm::dilate_smem_bytes(r, kp.dx);
-      if (r > vxm::kMaxVoxInf || smem > 200 * 1024 || kp.dx > 1024)
-        throw StageError{VXM_EINVAL, "vox_inf / dims_x exceed the dilation limits (16 / 1024)"};
-      VXM_SCK(vxm::dilate_set_smem(static_cast<int>(vxm::dilate_smem_bytes(r, kp.dx, vxm::dilate_fused(r, kp.dx)))));
+      if (!generic)
+        VXM_SCK(vxm::dilate_set_smem(static_cast<int>(vxm::dilate_smem_bytes(r, kp.dx, vxm::dilate_fused(r, kp.dx)))));
       kp.dbits = d_bits.p;
-      vxm::launch_dilate(kp, r, 1, smem, 0);
+      kp.dtmp = d_tmp.p;
+      vxm::launch_dilate(kp, r, 1, 0, 0);
       VXM_SCK(cudaGetLastError());
     }
-    vxm::decode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_key.p, d_ms.p, N, 32, 1);
+    vxm::decode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_occ.p, d_key.p, d_ms.p, N, kEpoch, vxm::kEpochKeys, 1);
     VXM_SCK(cudaGetLastError());
     vxm::Counters cnt{};
     VXM_SCK(cudaMemcpy(&cnt, d_cnt.p, sizeof(cnt), cudaMemcpyDeviceToHost));
@@ -185,8 +187,8 @@ int vxm_trace_bundle(const vxm_grid_spec* grid, uint8_t* ms, const int32_t bundl
       throw StageError{VXM_EINVAL, "generate_rays: bundle dimensions must be positive and odd"};
     if (!(ray_vox_size > 0.0)) throw StageError{VXM_EINVAL, "generate_rays: vox_size must be positive"};
     const long long rays = static_cast<long long>(bundle[1]) * bundle[2];
-    if (rays > vxm::KeyFmt<32>::kMaxRays) throw StageError{VXM_EINVAL, "ray bundle exceeds 2^31 - 3 rays"};
-    const int bits = key_bits_for(rays);
+    if (rays > vxm::kMaxClearRays) throw StageError{VXM_EINVAL, "ray bundle exceeds 2^31 - 3 rays"};
+    const int fmt = key_fmt_for(rays);
     // validate_ray (raytracer.cpp:23-33) for every ray, before any write.
     const double vs = ray_vox_size;
     for (int a = 0; a < 3; ++a)
@@ -226,16 +228,16 @@ int vxm_trace_bundle(const vxm_grid_spec* grid, uint8_t* ms, const int32_t bundl
     VXM_SCK(cudaMemcpy(d_frame.p, &f, sizeof(f), cudaMemcpyHostToDevice));
     VXM_SCK(cudaMemcpy(d_ms.p, ms, N, cudaMemcpyHostToDevice));
     VXM_SCK(cudaMemset(d_cnt.p, 0, sizeof(vxm::Counters)));
-    vxm::encode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_ms.p, d_occ.p, d_key.p, N, kEpoch, bits);
+    vxm::encode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_ms.p, d_occ.p, d_key.p, N, kEpoch, fmt);
     kp.occ = d_occ.p;
     kp.key = d_key.p;
-    kp.key_bits = bits;
+    kp.key_fmt = fmt;
     kp.counters = d_cnt.p;
     kp.frames = d_frame.p;
     vxm::launch_trace(kp, 1, 1, 0);
     VXM_SCK(cudaGetLastError());
     vxm::fold_trace_slots_kernel<<<1, 32>>>(d_cnt.p);
-    vxm::decode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_key.p, d_ms.p, N, bits);
+    vxm::decode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_occ.p, d_key.p, d_ms.p, N, kEpoch, fmt);
     VXM_SCK(cudaGetLastError());
     vxm::Counters cnt{};
     VXM_SCK(cudaMemcpy(&cnt, d_cnt.p, sizeof(cnt), cudaMemcpyDeviceToHost));
@@ -444,16 +446,16 @@ int vxm_trace_per_pixel(const vxm_grid_spec* grid, uint8_t* ms, const double* xs
     }
     VXM_SCK(cudaMemcpy(d_ms.p, ms, N, cudaMemcpyHostToDevice));
     VXM_SCK(cudaMemset(d_cnt.p, 0, sizeof(vxm::Counters)));
-    vxm::encode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_ms.p, d_occ.p, d_key.p, N, kEpoch, 32);
+    vxm::encode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_ms.p, d_occ.p, d_key.p, N, kEpoch, vxm::kEpochKeys);
     kp.occ = d_occ.p;
     kp.key = d_key.p;
-    kp.key_bits = 32;
+    kp.key_fmt = vxm::kEpochKeys;
     kp.counters = d_cnt.p;
     kp.frames = d_frame.p;
     vxm::trace_per_pixel_kernel<<<dim3(blocks_for(static_cast<long long>(n), 256), 1), 256>>>(kp, 0);
     VXM_SCK(cudaGetLastError());
     vxm::fold_trace_slots_kernel<<<1, 32>>>(d_cnt.p);
-    vxm::decode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_key.p, d_ms.p, N, 32);
+    vxm::decode_ms_kernel<<<blocks_for(N, 256), 256>>>(d_occ.p, d_key.p, d_ms.p, N, kEpoch, vxm::kEpochKeys);
     VXM_SCK(cudaGetLastError());
     vxm::Counters cnt{};
     VXM_SCK(cudaMemcpy(&cnt, d_cnt.p, sizeof(cnt), cudaMemcpyDeviceToHost));

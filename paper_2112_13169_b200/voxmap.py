@@ -280,6 +280,14 @@ class MappingPipeline:
         """Checkpoint stream s's local grid as a VOXGRID1 file (grid_io.cpp:14-29)."""
         N.check(self._lib.vxm_snapshot_save(self._ctx, s, str(path).encode()))
 
+    def save_snapshot_async(self, path, s=0):
+        """Asynchronous checkpoint (vxm_snapshot_save_async): returns at once;
+        later integrate calls proceed; snapshot_wait() joins the file write."""
+        N.check(self._lib.vxm_snapshot_save_async(self._ctx, s, str(path).encode()))
+
+    def snapshot_wait(self):
+        N.check(self._lib.vxm_snapshot_wait(self._ctx))
+
     def load_snapshot(self, path, s=0):
         """Resume stream s from a VOXGRID1 file of the same grid layout."""
         N.check(self._lib.vxm_snapshot_load(self._ctx, s, str(path).encode()))
