@@ -411,8 +411,10 @@ struct KernelTable {
   TransformVoxelizeFn transform_voxelize = nullptr;
   const char* isa = "scalar";
 };
-// The sm_100a implementation (isa "cuda-sm100a"). This build has no CPU
-// kernels: scalar_table() and dispatch() return the same table.
+// cuda_table(): the sm_100a implementation (isa "cuda-sm100a"), which
+// dispatch() returns and every pipeline path uses. scalar_table(): the
+// reference's portable host table (isa "scalar"), for callers that ask for it
+// by name (the reference's test_kernels checks dispatch() against it).
 const KernelTable& cuda_table();
 const KernelTable& scalar_table();
 const KernelTable& dispatch();

@@ -5,6 +5,7 @@
 // that touches grid contents goes through the C-ABI of libvxm.so
 // (include/vxm.h) and runs on the GPU.
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <fstream>
@@ -559,10 +560,39 @@ const KernelTable& cuda_table() {
   static const KernelTable t{vxm_kernel_merge, vxm_kernel_transform_voxelize, "cuda-sm100a"};
   return t;
 }
-// Deliberately the CUDA table: this library has no CPU compute path (a
-// caller that asks for the scalar table gets the sm_100a kernels, which
-// produce the same bytes; see b200_api.hpp and INTEGRATION.md).
-const KernelTable& scalar_table() { return cuda_table(); }
+// The reference's portable table (kernels_scalar.cpp:10-37), kept for
+// callers that ask for it by name, e.g. as the baseline the reference's own
+// test_kernels compares the dispatched table against. Nothing in this library
+// selects it: dispatch() and every pipeline path run the sm_100a kernels.
+namespace {
+void merge_host(std::uint8_t* local, const std::uint8_t* measurement, std::size_t n) {
+  for (std::size_t i = 0; i < n; ++i) {
+    const std::uint8_t m = measurement[i];
+    if (m != 0) local[i] = m == 3 ? 0 : m;
+  }
+}
+void transform_voxelize_host(const double* xs, const double* ys, const double* zs, std::size_t n,
+                             const double* rotation, const double* translation, double vox_size, std::int32_t* cx,
+                             std::int32_t* cy, std::int32_t* cz) {
+  std::int32_t* const out[3] = {cx, cy, cz};
+  for (std::size_t i = 0; i < n; ++i) {
+    for (int a = 0; a < 3; ++a) {
+      // ((t + R x) + R y) + R z, then floor of the true quotient, clamped
+      double acc = translation[a];
+      acc += rotation[3 * a] * xs[i];
+      acc += rotation[3 * a + 1] * ys[i];
+      acc += rotation[3 * a + 2] * zs[i];
+      const double f = std::floor(acc / vox_size);
+      out[a][i] = static_cast<std::int32_t>(std::min(std::max(f, -1e9), 1e9));
+    }
+  }
+}
+}  // namespace
+
+const KernelTable& scalar_table() {
+  static const KernelTable t{merge_host, transform_voxelize_host, "scalar"};
+  return t;
+}
 const KernelTable& dispatch() { return cuda_table(); }
 }  // namespace kernels
 
