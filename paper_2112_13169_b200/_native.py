@@ -121,7 +121,10 @@ def load() -> C.CDLL:
                 f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
             )
         lib = C.CDLL(os.fspath(LIB_PATH))
+        lenient = os.environ.get("VXM_LIB_NAME") is not None  # A/B builds of older revisions
         for name, (res, args) in SIGNATURES.items():
+            if lenient and not hasattr(lib, name):
+                continue
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

@@ -24,15 +24,15 @@ __global__ void encode_ms_kernel(const uint8_t* ms, uint8_t* occ, uint32_t* key,
   }
 }
 
-// (occ, keys) -> reference bytes. keep_occupied (populate): cells that were
-// Occupied in ms before stay Occupied (the vectorised dilation may zero occ
-// bytes next to the cells it marks).
+// (occ, keys) -> reference bytes. keep_input (populate, which only adds
+// Occupied cells): every cell not Occupied now keeps its input byte (the
+// vectorised dilation may store Unknown next to the cells it marks).
 __global__ void decode_ms_kernel(const uint8_t* occ, const uint32_t* key, uint8_t* ms, long long n, uint32_t epoch,
-                                 int fmt, int keep_occupied = 0) {
+                                 int fmt, int keep_input = 0) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const uint32_t v = fmt == kClearKeys ? decode_clear_key(key[i]) : decode_cell(occ[i], key[i], epoch);
-    ms[i] = static_cast<uint8_t>(keep_occupied && ms[i] == 2 ? 2u : v);
+    ms[i] = static_cast<uint8_t>(keep_input && v != 2u ? ms[i] : v);
   }
 }
 

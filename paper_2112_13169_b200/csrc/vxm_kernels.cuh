@@ -22,6 +22,7 @@ namespace vxm {
 // same IEEE operations, and floor(acc / vs) avoids the fp64 division when
 // provably exact (voxel_coord).
 // ---------------------------------------------------------------------------
+template <bool kClear>
 __device__ __forceinline__ unsigned populate_point(const KParams& p, const double* R,
                                                    const double* t, uint8_t* target,
                                                    uint8_t* rowflag, uint32_t* keys, uint8_t mark, double x,
@@ -39,8 +40,8 @@ __device__ __forceinline__ unsigned populate_point(const KParams& p, const doubl
   if (rowflag) {
     // a centre: the dilation only visits x-rows that hold one this frame
     rowflag[static_cast<uint32_t>(c[1]) + static_cast<uint32_t>(c[2]) * p.dy] = mark;
-  } else {
-    store_occupied_key(keys, idx, p.key_fmt);  // vox_inf == 0: the cell itself is Occupied
+  } else if constexpr (kClear) {
+    keys[idx] = kClearOccupied;  // vox_inf == 0: the cell itself is Occupied (clear-format keys)
   }
   return 0u;
 }
@@ -58,6 +59,7 @@ __device__ __forceinline__ float4 load_quad(const float* depth, int first, int n
   return make_float4(d[0], d[1], d[2], d[3]);
 }
 
+template <bool kClear>
 __global__ void __launch_bounds__(256) populate_depth_kernel(KParams p, int iters) {
   const int s = blockIdx.y;
   if (blockIdx.x == 0 && threadIdx.x == 0) p.counters[s].t_pop = global_ns();
@@ -94,7 +96,7 @@ __global__ void __launch_bounds__(256) populate_depth_kernel(KParams p, int iter
       const double D = static_cast<double>(d[k]);
       if (D > p.max_depth) continue;
       ++total;
-      outside += populate_point(p, R, t, target, rowflag, keys, mark, dmul(__ldg(p.qx + u), D),
+      outside += populate_point<kClear>(p, R, t, target, rowflag, keys, mark, dmul(__ldg(p.qx + u), D),
                                 dmul(__ldg(p.qy + v), D), D);
     }
     first = nfirst;
@@ -115,7 +117,7 @@ __global__ void __launch_bounds__(256) populate_depth_kernel(KParams p, int iter
 // aligned frame (checked; otherwise the plain loads).
 constexpr int kPopMaxIters = 8;
 
-template <bool kCompact>
+template <bool kCompact, bool kClear>
 __global__ void __launch_bounds__(256) populate_depth_tma_kernel(KParams p, int iters) {
   extern __shared__ float4 sq[];  // iters * blockDim.x quads
   __shared__ uint64_t bar[kPopMaxIters];
@@ -198,7 +200,7 @@ __global__ void __launch_bounds__(256) populate_depth_tma_kernel(KParams p, int 
     v += (v + 1) * p.W <= pix ? 1 : 0;
     const int u = pix - v * p.W;
     const double D = static_cast<double>(spx[off]);
-    outside += populate_point(p, R, t, target, rowflag, keys, mark, dmul(__ldg(p.qx + u), D),
+    outside += populate_point<kClear>(p, R, t, target, rowflag, keys, mark, dmul(__ldg(p.qx + u), D),
                               dmul(__ldg(p.qy + v), D), D);
   }
   } else {
@@ -227,7 +229,7 @@ __global__ void __launch_bounds__(256) populate_depth_tma_kernel(KParams p, int 
       const double D = static_cast<double>(d[k]);
       if (D > p.max_depth) continue;
       ++total;
-      outside += populate_point(p, R, t, target, rowflag, keys, mark, dmul(__ldg(p.qx + u), D),
+      outside += populate_point<kClear>(p, R, t, target, rowflag, keys, mark, dmul(__ldg(p.qx + u), D),
                                 dmul(__ldg(p.qy + v), D), D);
     }
   }
@@ -240,6 +242,7 @@ __global__ void __launch_bounds__(256) populate_depth_tma_kernel(KParams p, int 
 // K1 for an explicit camera-frame cloud (MeasurementFrame::cloud). Points
 // that PointCloud::add would have dropped (non-finite) are skipped uncounted
 // (proj/include/voxmap/geometry.hpp:84-89).
+template <bool kClear>
 __global__ void __launch_bounds__(256) populate_cloud_kernel(KParams p) {
   const int s = blockIdx.y;
   if (blockIdx.x == 0 && threadIdx.x == 0) p.counters[s].t_pop = global_ns();
@@ -261,7 +264,7 @@ __global__ void __launch_bounds__(256) populate_cloud_kernel(KParams p) {
     const double x = xs[i], y = ys[i], z = zs[i];
     if (!(isfinite(x) && isfinite(y) && isfinite(z))) continue;
     ++total;
-    outside += populate_point(p, R, t, target, rowflag, keys, mark, x, y, z);
+    outside += populate_point<kClear>(p, R, t, target, rowflag, keys, mark, x, y, z);
   }
   unsigned vals[2] = {total, outside};
   unsigned long long* dst[2] = {&p.counters[s].points_total, &p.counters[s].points_outside};
@@ -418,7 +421,7 @@ __host__ __device__ constexpr size_t dilate_smem_bytes(int r, int dx, bool fused
 // kR > 0: radius fixed at compile time; kR == 0: radius at run time.
 // kFused: no K2a; the block packs and x-dilates its halo rows itself from the
 // centre bytes (dims_x % 4 == 0: 4-byte loads), one launch fewer.
-template <int kR, bool kFused>
+template <int kR, bool kFused, bool kClear>
 __global__ void __launch_bounds__(256) dilate_tiles_kernel(KParams p, int r_rt) {
   pdl_wait();  // K1's centre bytes (fused) or K2a's bit rows
   extern __shared__ uint32_t bits[];
@@ -540,7 +543,7 @@ __global__ void __launch_bounds__(256) dilate_tiles_kernel(KParams p, int r_rt) 
           *reinterpret_cast<uint32_t*>(dst + x0) = e * 0x01010101u & m;
           // clear-format keys: Occupied where set, Unknown (as every key is
           // before the trace) elsewhere
-          if (p.key_fmt == kClearKeys) {
+          if constexpr (kClear) {
             const uint32_t cell = static_cast<uint32_t>(gy) * p.dx + static_cast<uint32_t>(gz) * dxy + x0;
             *reinterpret_cast<uint4*>(keys + cell) =
                 make_uint4(0u - (nib & 1u), 0u - ((nib >> 1) & 1u), 0u - ((nib >> 2) & 1u), 0u - (nib >> 3));
@@ -560,7 +563,7 @@ __global__ void __launch_bounds__(256) dilate_tiles_kernel(KParams p, int r_rt) 
       const int x = (w << 5) + lane;
       if (x < p.dx && ((d >> lane) & 1u)) {
         dst[x] = static_cast<uint8_t>(e);
-        store_occupied_key(keys, static_cast<uint32_t>(gy) * p.dx + static_cast<uint32_t>(gz) * dxy + x, p.key_fmt);
+        if constexpr (kClear) keys[static_cast<uint32_t>(gy) * p.dx + static_cast<uint32_t>(gz) * dxy + x] = kClearOccupied;
       }
     }
   }
@@ -620,18 +623,22 @@ inline bool dilate_generic(int r, int dx);
 // The fused K2 (no K2a) when the centre rows load as 4-byte words and its
 // shared memory fits.
 inline bool dilate_fused(int r, int dx) {
-#ifdef VXM_NO_FUSED_DILATE
-  return false;
-#endif
   return dx % 4 == 0 && dilate_smem_bytes(r, dx, true) <= 200 * 1024;
 }
 
+template <int kR, bool kClear>
+inline void launch_dilate_tiles_k(const KParams& kp, int r, bool fused, dim3 grid, cudaStream_t st) {
+  if (fused)
+    launch_pdl(dilate_tiles_kernel<kR, true, kClear>, grid, dim3(256), dilate_smem_bytes(r, kp.dx, true), st, kp, r);
+  else
+    launch_pdl(dilate_tiles_kernel<kR, false, kClear>, grid, dim3(256), dilate_smem_bytes(r, kp.dx), st, kp, r);
+}
 template <int kR>
 inline void launch_dilate_tiles(const KParams& kp, int r, bool fused, dim3 grid, cudaStream_t st) {
-  if (fused)
-    launch_pdl(dilate_tiles_kernel<kR, true>, grid, dim3(256), dilate_smem_bytes(r, kp.dx, true), st, kp, r);
+  if (kp.key_fmt == kClearKeys)
+    launch_dilate_tiles_k<kR, true>(kp, r, fused, grid, st);
   else
-    launch_pdl(dilate_tiles_kernel<kR, false>, grid, dim3(256), dilate_smem_bytes(r, kp.dx), st, kp, r);
+    launch_dilate_tiles_k<kR, false>(kp, r, fused, grid, st);
 }
 
 // the tile dilation's limits (radius, row length, shared memory)
@@ -674,23 +681,26 @@ inline void launch_dilate(const KParams& kp, int r, int streams, size_t /*smem*/
 }
 
 // Opt-in to large dynamic shared memory for every K2b instance.
-inline cudaError_t dilate_set_smem(int bytes) {
+template <bool kFused, bool kClear>
+inline cudaError_t dilate_set_smem_k(int bytes) {
   cudaError_t e = cudaSuccess;
-  const void* fns[10] = {reinterpret_cast<const void*>(dilate_tiles_kernel<0, false>),
-                         reinterpret_cast<const void*>(dilate_tiles_kernel<1, false>),
-                         reinterpret_cast<const void*>(dilate_tiles_kernel<2, false>),
-                         reinterpret_cast<const void*>(dilate_tiles_kernel<3, false>),
-                         reinterpret_cast<const void*>(dilate_tiles_kernel<4, false>),
-                         reinterpret_cast<const void*>(dilate_tiles_kernel<0, true>),
-                         reinterpret_cast<const void*>(dilate_tiles_kernel<1, true>),
-                         reinterpret_cast<const void*>(dilate_tiles_kernel<2, true>),
-                         reinterpret_cast<const void*>(dilate_tiles_kernel<3, true>),
-                         reinterpret_cast<const void*>(dilate_tiles_kernel<4, true>)};
+  const void* fns[5] = {reinterpret_cast<const void*>(dilate_tiles_kernel<0, kFused, kClear>),
+                        reinterpret_cast<const void*>(dilate_tiles_kernel<1, kFused, kClear>),
+                        reinterpret_cast<const void*>(dilate_tiles_kernel<2, kFused, kClear>),
+                        reinterpret_cast<const void*>(dilate_tiles_kernel<3, kFused, kClear>),
+                        reinterpret_cast<const void*>(dilate_tiles_kernel<4, kFused, kClear>)};
   for (const void* f : fns) {
     const cudaError_t x = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (x != cudaSuccess) e = x;
   }
   return e;
+}
+inline cudaError_t dilate_set_smem(int bytes) {
+  cudaError_t e[4] = {dilate_set_smem_k<false, false>(bytes), dilate_set_smem_k<true, false>(bytes),
+                      dilate_set_smem_k<false, true>(bytes), dilate_set_smem_k<true, true>(bytes)};
+  for (cudaError_t x : e)
+    if (x != cudaSuccess) return x;
+  return cudaSuccess;
 }
 
 // ---------------------------------------------------------------------------
@@ -800,6 +810,7 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   const bool active = ty < (kSplit ? (p.vh + 1) / 2 : p.tiles_y) && xi_idx < p.vw && yi_idx < p.vh;
   const uint32_t ray = static_cast<uint32_t>(yi_idx) * p.vw + xi_idx;  // row-major, y outer
   const uint32_t ray_key = vxm::ray_key(p.key_fmt, epoch, ray);  // | 1: UnknownTraced
+
 
   RayState st;
   ray_setup(R, start, p.vs, p.ray_vs, xi_idx - (p.vw - 1) / 2, yi_idx - (p.vh - 1) / 2, p.vd, st);
@@ -1359,6 +1370,185 @@ __device__ __forceinline__ unsigned count_free16(const uint32_t (&x)[4]) {
   return (m * 0x01010101u) >> 24;
 }
 
+// merge of 4 packed cells: local l4, occupancy o4 (epoch bytes), 4 epoch keys.
+// States are 0..3 per byte, so "== 0" and "== 3" are two-bit tests.
+__device__ __forceinline__ uint32_t merge4(uint32_t l4, uint32_t o4, uint4 k4, uint32_t epoch) {
+  const uint32_t kk[4] = {k4.x, k4.y, k4.z, k4.w};
+  uint32_t m4 = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t v = (kk[i] >> kKeyShift) == epoch ? (1u | ((kk[i] & 1u) << 1)) : 0u;  // 1 or 3
+    m4 |= v << (8 * i);
+  }
+  const uint32_t occm = zero_bytes(o4 ^ (epoch * 0x01010101u));  // 0xff where Occupied
+  m4 = (m4 & ~occm) | (0x02020202u & occm);
+  const uint32_t keep = (((m4 | (m4 >> 1)) & 0x01010101u) ^ 0x01010101u) * 0xffu;  // m == 0
+  const uint32_t clear = (m4 & (m4 >> 1) & 0x01010101u) * 0xffu;                   // m == 3
+  return (l4 & keep) | (m4 & ~(keep | clear));
+}
+
+// K4, epoch-format keys (every bundle of up to 131,070 rays): merge4 decodes
+// occupancy bytes and keys; nothing is reset (keys of an older epoch read as
+// Unknown). The clear-format variant follows.
+__global__ void __launch_bounds__(256) merge_epoch_kernel(KParams p, int rows_per_warp) {
+  pdl_wait();  // K3's keys and counters
+  const int s = blockIdx.y;
+  if (blockIdx.x == 0 && threadIdx.x == 0) p.counters[s].t_merge = global_ns();
+  const FrameParams* fp = p.frames + s;
+  const uint32_t epoch = fp->epoch;
+  const uint32_t cur = fp->cur;
+  const int ox = fp->off[0], oy = fp->off[1], oz = fp->off[2];
+  const long long base = static_cast<long long>(s) * p.n;
+  const uint8_t* occ = p.occ + base;
+  const uint32_t* key = p.key + base;
+  const uint8_t* src = (cur ? p.loc1 : p.loc0) + base;
+  uint8_t* dst = (cur ? p.loc0 : p.loc1) + base;
+  const int lane = threadIdx.x & 31;
+  const int warp_id = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int rows = p.dy * p.dz;
+  const uint32_t dxy = static_cast<uint32_t>(p.dx) * p.dy;
+
+  if (blockIdx.x == 0 && threadIdx.x < 32) fold_trace_slots(p.counters[s]);
+
+  unsigned occ_n = 0, free_n = 0;
+  const bool vec = (p.dx & 3) == 0 && (ox & 3) == 0;
+  if (ox == 0 && (p.dx & 3) == 0 && p.dx >= 16 && (p.n & 15) == 0 && p.n < (1 << 24)) {
+    // No x shift: destination cell c reads c + delta (delta = off_y*dx +
+    // off_z*dx*dy), and the valid destination cells of a slab are one run of
+    // whole rows. A thread takes 16 consecutive cells: 16 local and occupancy
+    // bytes and 16 keys, no per-row arithmetic. A chunk spans at most two
+    // rows (dx >= 16), so it is valid throughout when its first and last
+    // cells are; chunks at a run boundary test their words one by one (a
+    // word never straddles a row since dx % 4 == 0).
+    const uint32_t dx = p.dx;
+    const int delta = oy * p.dx + oz * static_cast<int>(dxy);
+    const int ylo = max(0, -oy), yhi = min(p.dy, p.dy - oy), zlo = max(0, -oz), zhi = min(p.dz, p.dz - oz);
+    const float inv_dx = 1.0f / static_cast<float>(dx), inv_dxy = 1.0f / static_cast<float>(dxy);
+    auto valid = [&](uint32_t c) {
+      const uint32_t z = div_small(c, dxy, inv_dxy);
+      const uint32_t y = div_small(c - z * dxy, dx, inv_dx);
+      return static_cast<int>(y) >= ylo && static_cast<int>(y) < yhi && static_cast<int>(z) >= zlo &&
+             static_cast<int>(z) < zhi;
+    };
+    const bool aligned = (delta & 15) == 0;
+    const uint32_t nch = static_cast<uint32_t>(p.n >> 4);
+    for (uint32_t ch = blockIdx.x * blockDim.x + threadIdx.x; ch < nch; ch += gridDim.x * blockDim.x) {
+      const uint32_t c = ch << 4;
+      const int sc = static_cast<int>(c) + delta;
+      uint32_t out[4] = {0u, 0u, 0u, 0u};
+      if (valid(c) && valid(c + 15)) {
+        uint32_t l[4], o[4];
+        if (aligned) {
+          const uint4 L = __ldcs(reinterpret_cast<const uint4*>(src + sc));
+          const uint4 O = __ldcs(reinterpret_cast<const uint4*>(occ + sc));
+          l[0] = L.x; l[1] = L.y; l[2] = L.z; l[3] = L.w;
+          o[0] = O.x; o[1] = O.y; o[2] = O.z; o[3] = O.w;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            l[i] = __ldcs(reinterpret_cast<const unsigned int*>(src + sc + 4 * i));
+            o[i] = __ldcs(reinterpret_cast<const unsigned int*>(occ + sc + 4 * i));
+          }
+        }
+        uint4 k[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) k[i] = __ldcs(reinterpret_cast<const uint4*>(key + sc + 4 * i));
+#pragma unroll
+        for (int i = 0; i < 4; ++i) out[i] = merge4(l[i], o[i], k[i], epoch);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (valid(c + 4 * i)) {
+            const int si = sc + 4 * i;
+            out[i] = merge4(*reinterpret_cast<const uint32_t*>(src + si), *reinterpret_cast<const uint32_t*>(occ + si),
+                            *reinterpret_cast<const uint4*>(key + si), epoch);
+          }
+        }
+      }
+      *reinterpret_cast<uint4*>(dst + c) = make_uint4(out[0], out[1], out[2], out[3]);
+      occ_n += count_occupied16(out);
+      free_n += count_free16(out);
+    }
+  } else
+  if (vec && p.dx <= 128 && rows_per_warp == kRowsPerWarp) {
+    // A row is at most one 4-cell group per lane: issue the loads of all the
+    // warp's rows before resolving any, so each lane keeps kRowsPerWarp x 24 B
+    // in flight (the kernel is HBM-latency bound otherwise).
+    const int x0 = lane * 4, sx = x0 + ox;
+    uint32_t l4[kRowsPerWarp], o4[kRowsPerWarp], drow[kRowsPerWarp];
+    uint4 k4[kRowsPerWarp];
+    bool ok[kRowsPerWarp], in_row[kRowsPerWarp];
+#pragma unroll
+    for (int rr = 0; rr < kRowsPerWarp; ++rr) {
+      const int row = warp_id * kRowsPerWarp + rr;
+      const int z = row / p.dy;
+      const int y = row - z * p.dy;
+      const int sy = y + oy, sz = z + oz;
+      in_row[rr] = row < rows && x0 < p.dx;
+      ok[rr] = in_row[rr] && sy >= 0 && sy < p.dy && sz >= 0 && sz < p.dz && sx >= 0 && sx < p.dx;
+      drow[rr] = static_cast<uint32_t>(y) * p.dx + static_cast<uint32_t>(z) * dxy;
+      const long long sc = static_cast<long long>(sy) * p.dx + static_cast<long long>(sz) * dxy + sx;
+      l4[rr] = o4[rr] = 0u;
+      k4[rr] = make_uint4(0u, 0u, 0u, 0u);
+      if (ok[rr]) {
+        l4[rr] = __ldcs(reinterpret_cast<const unsigned int*>(src + sc));
+        o4[rr] = __ldcs(reinterpret_cast<const unsigned int*>(occ + sc));
+        k4[rr] = __ldcs(reinterpret_cast<const uint4*>(key + sc));
+      }
+    }
+#pragma unroll
+    for (int rr = 0; rr < kRowsPerWarp; ++rr) {
+      if (!in_row[rr]) continue;
+      const uint32_t out = ok[rr] ? merge4(l4[rr], o4[rr], k4[rr], epoch) : 0u;
+      occ_n += count_occupied4(out);
+      free_n += count_free4(out);
+      *reinterpret_cast<uint32_t*>(dst + drow[rr] + x0) = out;
+    }
+  } else
+  for (int rr = 0; rr < rows_per_warp; ++rr) {
+    const int row = warp_id * rows_per_warp + rr;
+    if (row >= rows) break;
+    const int z = row / p.dy;
+    const int y = row - z * p.dy;
+    const int sy = y + oy, sz = z + oz;
+    const bool row_ok = sy >= 0 && sy < p.dy && sz >= 0 && sz < p.dz;
+    const uint32_t drow = static_cast<uint32_t>(y) * p.dx + static_cast<uint32_t>(z) * dxy;
+    const long long srow = static_cast<long long>(sy) * p.dx + static_cast<long long>(sz) * dxy;
+    if (vec) {
+      for (int x0 = lane * 4; x0 < p.dx; x0 += 128) {
+        const int sx = x0 + ox;
+        uint32_t out = 0;
+        if (row_ok && sx >= 0 && sx < p.dx) {
+          const long long sc = srow + sx;
+          out = merge4(*reinterpret_cast<const uint32_t*>(src + sc), *reinterpret_cast<const uint32_t*>(occ + sc),
+                       *reinterpret_cast<const uint4*>(key + sc), epoch);
+        }
+        occ_n += count_occupied4(out);
+        free_n += count_free4(out);
+        *reinterpret_cast<uint32_t*>(dst + drow + x0) = out;
+      }
+    } else {
+      for (int x0 = lane * 4; x0 < p.dx; x0 += 128) {
+        for (int i = 0; i < 4 && x0 + i < p.dx; ++i) {
+          const int sx = x0 + i + ox;
+          uint32_t v = 0;
+          if (row_ok && sx >= 0 && sx < p.dx) {
+            const long long sc = srow + sx;
+            v = merge_cell(src[sc], decode_cell(occ[sc], key[sc], epoch));
+          }
+          occ_n += v == 2u;
+          free_n += v == 1u;
+          dst[drow + x0 + i] = static_cast<uint8_t>(v);
+        }
+      }
+    }
+  }
+  unsigned vals[2] = {occ_n, free_n};
+  unsigned long long* dsts[2] = {&p.counters[s].occupied, &p.counters[s].freed};
+  block_accumulate<2>(vals, dsts);  // ends after every warp's work (a block barrier)
+  if (threadIdx.x == 0) atomicMax(&p.counters[s].t_end, global_ns());
+}
+
 // Clear-format keys of the source cells the shifted gather never reads
 // (their destination lies outside the grid) are reset to Unknown here: x in
 // [0, ox) for ox > 0 or [dx + ox, dx) for ox < 0 (every y, z), and likewise
@@ -1624,6 +1814,150 @@ __device__ __forceinline__ const unsigned char* align16_up(const void* p) {
   return reinterpret_cast<const unsigned char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~static_cast<uintptr_t>(15));
 }
 
+__global__ void __launch_bounds__(256) merge_epoch_tma_kernel(KParams p) {
+  extern __shared__ __align__(16) unsigned char msm[];
+  __shared__ uint64_t bar[2];
+  const int s = blockIdx.y;
+  const FrameParams* fp = p.frames + s;
+  const int dx = p.dx, dy = p.dy, dz = p.dz;
+  const long long dxy = static_cast<long long>(dx) * dy;
+  const int ox = fp->off[0], oy = fp->off[1], oz = fp->off[2];
+  const uint32_t epoch = fp->epoch;
+  const uint32_t cur = fp->cur;
+  const long long base = static_cast<long long>(s) * p.n;
+  const uint8_t* src = (cur ? p.loc1 : p.loc0) + base;
+  uint8_t* dst = (cur ? p.loc0 : p.loc1) + base;
+  const uint8_t* occ = p.occ + base;
+  const uint32_t* key = p.key + base;
+  const int rows = merge_tma_rows(dx, dy);
+  const int ngy = (dy + rows - 1) / rows;
+  const int ngroups = ngy * dz;
+  const size_t stage_bytes = merge_tma_smem_bytes(rows * dx);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool vec = ((dx | ox) & 3) == 0;
+
+  // geometry of group g: rows [y0, y0 + ny) of slab z, sourced from rows
+  // [sy_lo, sy_hi) of slab z + off_z (cells [c0, c1) of the slot)
+  struct Group {
+    int y0, ny, z, sy_lo, sy_hi;
+    bool any;
+    long long c0, c1;
+  };
+  auto group = [&](int g) {
+    Group G;
+    G.z = g / ngy;
+    G.y0 = (g - G.z * ngy) * rows;
+    G.ny = min(rows, dy - G.y0);
+    const int sz = G.z + oz;
+    G.sy_lo = max(0, G.y0 + oy);
+    G.sy_hi = min(dy, G.y0 + oy + G.ny);
+    G.any = sz >= 0 && sz < dz && G.sy_lo < G.sy_hi;
+    G.c0 = static_cast<long long>(G.sy_lo) * dx + sz * dxy;
+    G.c1 = static_cast<long long>(G.sy_hi) * dx + sz * dxy;
+    return G;
+  };
+  // one elected thread stages group g into stage buffer b (possibly nothing)
+  auto issue = [&](int g, int b) {
+    const Group G = group(g);
+    unsigned char* sl = msm + b * stage_bytes;
+    uint32_t lb = 0, ob = 0, kb = 0;
+    const unsigned char *lw0 = nullptr, *ow0 = nullptr, *kw0 = nullptr;
+    if (G.any) {
+      lw0 = align16_down(src + G.c0);
+      ow0 = align16_down(occ + G.c0);
+      kw0 = align16_down(key + G.c0);
+      lb = static_cast<uint32_t>(align16_up(src + G.c1) - lw0);
+      ob = static_cast<uint32_t>(align16_up(occ + G.c1) - ow0);
+      kb = static_cast<uint32_t>(align16_up(key + G.c1) - kw0);
+    }
+    mbar_expect_tx(&bar[b], lb + ob + kb);
+    if (G.any) {
+      unsigned char* so = sl + ((lb + 15u) & ~15u);
+      unsigned char* sk = so + ((ob + 15u) & ~15u);
+      bulk_g2s(sl, lw0, lb, &bar[b]);
+      bulk_g2s(so, ow0, ob, &bar[b]);
+      bulk_g2s(sk, kw0, kb, &bar[b]);
+    }
+  };
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_wait();  // K3's keys and counters
+  if (blockIdx.x == 0 && threadIdx.x == 0) p.counters[s].t_merge = global_ns();
+  if (blockIdx.x == 0 && threadIdx.x < 32) fold_trace_slots(p.counters[s]);
+  unsigned occ_n = 0, free_n = 0;
+  int g = blockIdx.x;
+  if (g < ngroups && threadIdx.x == 0) issue(g, 0);
+  for (int it = 0; g < ngroups; ++it, g += gridDim.x) {
+    const int b = it & 1;
+    // refill the other stage (consumed in the previous iteration, after its
+    // closing barrier) while this one lands
+    if (g + gridDim.x < ngroups && threadIdx.x == 0) issue(g + gridDim.x, b ^ 1);
+    mbar_wait(&bar[b], (it >> 1) & 1);
+    const Group G = group(g);
+    const unsigned char* sl = msm + b * stage_bytes;
+    int ll = 0, ol = 0, kl = 0;
+    const unsigned char *so = sl, *sk = sl;
+    if (G.any) {
+      const unsigned char* lw0 = align16_down(src + G.c0);
+      const unsigned char* ow0 = align16_down(occ + G.c0);
+      const unsigned char* kw0 = align16_down(key + G.c0);
+      const uint32_t lb = static_cast<uint32_t>(align16_up(src + G.c1) - lw0);
+      const uint32_t ob = static_cast<uint32_t>(align16_up(occ + G.c1) - ow0);
+      so = sl + ((lb + 15u) & ~15u);
+      sk = so + ((ob + 15u) & ~15u);
+      ll = static_cast<int>((src + G.c0) - lw0);
+      ol = static_cast<int>((occ + G.c0) - ow0);
+      kl = static_cast<int>(reinterpret_cast<const unsigned char*>(key + G.c0) - kw0);
+    }
+    for (int r = warp; r < G.ny; r += blockDim.x >> 5) {
+      const int y = G.y0 + r, sy = y + oy;
+      const bool row_ok = G.any && sy >= G.sy_lo && sy < G.sy_hi;
+      uint8_t* drow = dst + static_cast<long long>(y) * dx + G.z * dxy;
+      const long long rrow = static_cast<long long>(sy - G.sy_lo) * dx;  // relative to c0
+      for (int x0 = lane * 4; x0 < dx; x0 += 128) {
+        uint32_t out = 0;
+        if (vec) {
+          const int sx = x0 + ox;
+          if (row_ok && sx >= 0 && sx < dx) {
+            const long long rel = rrow + sx;
+            out = merge4(*reinterpret_cast<const uint32_t*>(sl + ll + rel),
+                         *reinterpret_cast<const uint32_t*>(so + ol + rel),
+                         *reinterpret_cast<const uint4*>(sk + kl + 4 * rel), epoch);
+          }
+          *reinterpret_cast<uint32_t*>(drow + x0) = out;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int x = x0 + k, sx = x + ox;
+            if (x >= dx) break;
+            uint32_t v = 0;
+            if (row_ok && sx >= 0 && sx < dx) {
+              const long long rel = rrow + sx;
+              v = merge_cell(sl[ll + rel],
+                             decode_cell(so[ol + rel], *reinterpret_cast<const uint32_t*>(sk + kl + 4 * rel), epoch));
+            }
+            out |= v << (8 * k);
+            drow[x] = static_cast<uint8_t>(v);
+          }
+        }
+        occ_n += count_occupied4(out);
+        free_n += count_free4(out);
+      }
+    }
+    __syncthreads();  // stage b is refilled two groups from now
+  }
+  // every warp has passed the last group's barrier
+  if (threadIdx.x == 0) atomicMax(&p.counters[s].t_end, global_ns());
+  unsigned vals[2] = {occ_n, free_n};
+  unsigned long long* dsts[2] = {&p.counters[s].occupied, &p.counters[s].freed};
+  warp_accumulate<2>(vals, dsts);
+}
+
 template <bool kClear>
 __global__ void __launch_bounds__(256) merge_shift_count_tma_kernel(KParams p) {
   extern __shared__ __align__(16) unsigned char msm[];
@@ -1828,6 +2162,177 @@ __device__ __forceinline__ void add_frame_counts(const uint32_t (&packed)[U / 2]
         if (k < F && (half >> 8)) atomicAdd(&cnt[kMaxFramesPerCall + k], half >> 8);
       }
     }
+  }
+}
+
+__global__ void __launch_bounds__(256) merge_sequence_epoch_kernel(KParams p, int F) {
+  pdl_wait();  // K3's keys and counters
+  constexpr int U = 4;  // frames whose loads are issued together
+  __shared__ unsigned cnt[2 * kMaxFramesPerCall];           // occupied, then freed, per frame
+  __shared__ int Pc[kMaxFramesPerCall + U][3];              // P_{k-1} at index k
+  __shared__ uint32_t ep[kMaxFramesPerCall];
+  const int s = blockIdx.y;  // stream
+  const FrameParams* f0 = p.frames + static_cast<long long>(s) * F;
+  const int lane = threadIdx.x & 31;
+  if (blockIdx.x == 0) {
+    const unsigned long long t = global_ns();
+    for (int k = threadIdx.x; k < F; k += blockDim.x) p.counters[static_cast<long long>(s) * F + k].t_merge = t;
+  }
+  for (int k = threadIdx.x; k < 2 * kMaxFramesPerCall; k += blockDim.x) cnt[k] = 0u;
+  __shared__ int vec_ok;
+  if (threadIdx.x == 0) {
+    int P[3] = {0, 0, 0};
+    bool aligned = (p.dx & 3) == 0;
+    for (int k = 0; k <= F; ++k) {
+      for (int a = 0; a < 3; ++a) Pc[k][a] = P[a];
+      aligned = aligned && (P[0] & 3) == 0;
+      if (k < F) {
+        for (int a = 0; a < 3; ++a) P[a] += f0[k].off[a];
+        ep[k] = f0[k].epoch;
+      }
+    }
+    vec_ok = aligned ? 1 : 0;
+  }
+  if (blockIdx.x == 0) {
+    // fold the trace counters of every frame slot of this stream (one warp each)
+    for (int k = threadIdx.x >> 5; k < F; k += blockDim.x >> 5) fold_trace_slots(p.counters[static_cast<long long>(s) * F + k]);
+  }
+  __syncthreads();
+  const int dx = p.dx, dy = p.dy, dz = p.dz;
+  const int dxy = dx * dy;
+  const int bx = f0->box_lo[0], by = f0->box_lo[1], bz = f0->box_lo[2];
+  const int ex = f0->box_ext[0], ey = f0->box_ext[1], ez = f0->box_ext[2];
+  const long long nchain = static_cast<long long>(ex) * ey * ez;
+  const uint32_t cur = f0->cur;
+  const uint8_t* src = (cur ? p.loc1 : p.loc0) + static_cast<long long>(s) * p.n;
+  uint8_t* dst = (cur ? p.loc0 : p.loc1) + static_cast<long long>(s) * p.n;
+  const uint8_t* occ0 = p.occ + static_cast<long long>(s) * F * p.n;
+  const uint32_t* key0 = p.key + static_cast<long long>(s) * F * p.n;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  if (vec_ok) {
+    // Every frame's x shift is a multiple of 4 (and dims_x too): a thread
+    // folds 4 neighbouring chains at once, moving the 4 cells as one word
+    // (occupancy u32, keys uint4) and merging / counting them with the
+    // byte-SIMD helpers of K4.
+    const int ex4 = ex >> 2;
+    const long long ngroup = static_cast<long long>(ex4) * ey * ez;
+    for (long long base = static_cast<long long>(blockIdx.x) * blockDim.x; base < ngroup; base += stride) {
+      const long long i = base + threadIdx.x;
+      const bool active = i < ngroup;
+      const int iz = static_cast<int>(i / (static_cast<long long>(ex4) * ey));
+      const int rem = static_cast<int>(i - static_cast<long long>(iz) * ex4 * ey);
+      const int iy = rem / ex4;
+      const int gx = bx + 4 * (rem - iy * ex4), gy = by + iy, gz = bz + iz;
+      auto group_of = [&](int k, bool& in) {  // first cell of the group at c_{k-1}
+        const int cx = gx - Pc[k][0], cy = gy - Pc[k][1], cz = gz - Pc[k][2];
+        in = active && static_cast<unsigned>(cx) < static_cast<unsigned>(dx) &&
+             static_cast<unsigned>(cy) < static_cast<unsigned>(dy) && static_cast<unsigned>(cz) < static_cast<unsigned>(dz);
+        return cx + cy * dx + cz * dxy;
+      };
+      bool in_prev;
+      int pos_prev = group_of(0, in_prev);
+      uint32_t val = in_prev ? *reinterpret_cast<const uint32_t*>(src + pos_prev) : 0u;
+      for (int k0 = 0; k0 < F; k0 += U) {
+        bool in_c[U];
+        int pos[U];
+        uint32_t o[U];
+        uint4 kk[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) pos[u] = group_of(k0 + u + 1, in_c[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const bool in_r = u == 0 ? in_prev : in_c[u - 1];
+          const int r = u == 0 ? pos_prev : pos[u - 1];
+          const bool ld = k0 + u < F && in_c[u] && in_r;
+          const long long off = static_cast<long long>(k0 + u) * p.n + r;
+          o[u] = ld ? __ldcs(reinterpret_cast<const uint32_t*>(occ0 + off)) : 0u;
+          kk[u] = ld ? __ldcs(reinterpret_cast<const uint4*>(key0 + off)) : make_uint4(0u, 0u, 0u, 0u);
+        }
+        // per frame: Occupied / Free counts of this thread's 4 cells (each
+        // <= 4, so a warp sum fits a byte); two frames share one reduction
+        uint32_t packed[U / 2] = {};
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int k = k0 + u;
+          if (k >= F) break;
+          const bool in_r = u == 0 ? in_prev : in_c[u - 1];
+          if (in_c[u]) val = in_r ? merge4(val, o[u], kk[u], ep[k]) : 0u;  // shifted in: Unknown
+          const unsigned oc = in_c[u] ? count_occupied4(val) : 0u, fr = in_c[u] ? count_free4(val) : 0u;
+          packed[u >> 1] |= (oc | (fr << 8)) << (16 * (u & 1));
+        }
+        add_frame_counts<U>(packed, cnt, k0, F, lane);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (k0 + u < F) {
+            in_prev = in_c[u];
+            pos_prev = pos[u];
+          }
+        }
+      }
+      if (in_prev) *reinterpret_cast<uint32_t*>(dst + pos_prev) = val;
+    }
+  } else
+  for (long long base = static_cast<long long>(blockIdx.x) * blockDim.x; base < nchain; base += stride) {
+    const long long i = base + threadIdx.x;
+    const bool active = i < nchain;
+    const int iz = static_cast<int>(i / (static_cast<long long>(ex) * ey));
+    const int rem = static_cast<int>(i - static_cast<long long>(iz) * ex * ey);
+    const int iy = rem / ex;
+    const int gx = bx + rem - iy * ex, gy = by + iy, gz = bz + iz;
+    auto cell_of = [&](int k, bool& in) {  // c_{k-1} = g - P_{k-1}
+      const int cx = gx - Pc[k][0], cy = gy - Pc[k][1], cz = gz - Pc[k][2];
+      in = active && static_cast<unsigned>(cx) < static_cast<unsigned>(dx) &&
+           static_cast<unsigned>(cy) < static_cast<unsigned>(dy) && static_cast<unsigned>(cz) < static_cast<unsigned>(dz);
+      return cx + cy * dx + cz * dxy;
+    };
+    bool in_prev;
+    int pos_prev = cell_of(0, in_prev);
+    uint32_t val = in_prev ? src[pos_prev] : 0u;
+    for (int k0 = 0; k0 < F; k0 += U) {
+      // positions after frames k0..k0+U-1, then all their loads, then the merges
+      bool in_c[U];
+      int pos[U];
+      uint32_t o[U], kk[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) pos[u] = cell_of(k0 + u + 1, in_c[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool in_r = u == 0 ? in_prev : in_c[u - 1];
+        const int r = u == 0 ? pos_prev : pos[u - 1];
+        const bool ld = k0 + u < F && in_c[u] && in_r;
+        const long long off = static_cast<long long>(k0 + u) * p.n + r;
+        o[u] = ld ? __ldcs(occ0 + off) : 0u;
+        kk[u] = ld ? __ldcs(key0 + off) : 0u;
+      }
+      uint32_t packed[U / 2] = {};
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = k0 + u;
+        if (k >= F) break;
+        const bool in_r = u == 0 ? in_prev : in_c[u - 1];
+        if (in_c[u]) val = in_r ? merge_cell(val, decode_cell(o[u], kk[u], ep[k])) : 0u;  // shifted in: Unknown
+        const unsigned oc = in_c[u] && val == 2u ? 1u : 0u, fr = in_c[u] && val == 1u ? 1u : 0u;
+        packed[u >> 1] |= (oc | (fr << 8)) << (16 * (u & 1));
+      }
+      add_frame_counts<U>(packed, cnt, k0, F, lane);
+      // position after the group's last frame (F may end inside the group)
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (k0 + u < F) {
+          in_prev = in_c[u];
+          pos_prev = pos[u];
+        }
+      }
+    }
+    if (in_prev) dst[pos_prev] = static_cast<uint8_t>(val);
+  }
+  __syncthreads();
+  const unsigned long long t_end = global_ns();
+  for (int k = threadIdx.x; k < F; k += blockDim.x) {
+    Counters& c = p.counters[static_cast<long long>(s) * F + k];
+    if (cnt[k]) atomicAdd(&c.occupied, static_cast<unsigned long long>(cnt[k]));
+    if (cnt[kMaxFramesPerCall + k]) atomicAdd(&c.freed, static_cast<unsigned long long>(cnt[kMaxFramesPerCall + k]));
+    atomicMax(&c.t_end, t_end);
   }
 }
 

@@ -419,16 +419,21 @@ void launch_stages(vxm_ctx* c, bool cloud, bool capturing, int s0, int S, cudaSt
     if (npix % 4 == 0) {
       // staged quads + per-warp lists of valid pixels (u16, 4 per quad)
       const size_t smem = (sizeof(float4) + 4 * sizeof(uint16_t)) * kPopulateThreads * static_cast<size_t>(iters);
+      const bool clr = kp.key_fmt == vxm::kClearKeys;
       if (c->pop_compact)
-        vxm::populate_depth_tma_kernel<true><<<grid, kPopulateThreads, smem, st>>>(kp, iters);
+        (clr ? vxm::populate_depth_tma_kernel<true, true> : vxm::populate_depth_tma_kernel<true, false>)
+            <<<grid, kPopulateThreads, smem, st>>>(kp, iters);
       else
-        vxm::populate_depth_tma_kernel<false><<<grid, kPopulateThreads, smem, st>>>(kp, iters);
+        (clr ? vxm::populate_depth_tma_kernel<false, true> : vxm::populate_depth_tma_kernel<false, false>)
+            <<<grid, kPopulateThreads, smem, st>>>(kp, iters);
     } else {
-      vxm::populate_depth_kernel<<<grid, kPopulateThreads, 0, st>>>(kp, iters);
+      (kp.key_fmt == vxm::kClearKeys ? vxm::populate_depth_kernel<true> : vxm::populate_depth_kernel<false>)
+          <<<grid, kPopulateThreads, 0, st>>>(kp, iters);
     }
   } else {
     dim3 grid(static_cast<unsigned>(c->nsm * 4), S);
-    vxm::populate_cloud_kernel<<<grid, kPopulateThreads, 0, st>>>(kp);
+    (kp.key_fmt == vxm::kClearKeys ? vxm::populate_cloud_kernel<true> : vxm::populate_cloud_kernel<false>)
+        <<<grid, kPopulateThreads, 0, st>>>(kp);
   }
   VXM_CK(cudaGetLastError());
   if (kp.vox_inf > 0) {
@@ -469,7 +474,7 @@ void launch_merge_chain(vxm_ctx* c, const vxm::KParams& kp, int F, int streams, 
   if (kp.key_fmt == vxm::kClearKeys)
     VXM_CK(vxm::launch_pdl(vxm::merge_sequence_kernel<true>, grid, dim3(kMergeThreads), 0, st, kp, F));
   else
-    VXM_CK(vxm::launch_pdl(vxm::merge_sequence_kernel<false>, grid, dim3(kMergeThreads), 0, st, kp, F));
+    VXM_CK(vxm::launch_pdl(vxm::merge_sequence_epoch_kernel, grid, dim3(kMergeThreads), 0, st, kp, F));
   VXM_CK(cudaGetLastError());
 }
 
@@ -490,7 +495,7 @@ void launch_merge(vxm_ctx* c, const vxm::KParams& kp, int S, cudaStream_t st) {
     if (kp.key_fmt == vxm::kClearKeys)
       VXM_CK(vxm::launch_pdl(vxm::merge_shift_count_tma_kernel<true>, grid, dim3(kMergeThreads), smem, st, kp));
     else
-      VXM_CK(vxm::launch_pdl(vxm::merge_shift_count_tma_kernel<false>, grid, dim3(kMergeThreads), smem, st, kp));
+      VXM_CK(vxm::launch_pdl(vxm::merge_epoch_tma_kernel, grid, dim3(kMergeThreads), smem, st, kp));
   } else if (c->F == 1) {
     const long long rows = static_cast<long long>(kp.dy) * kp.dz;
     // one row per warp unless the batch fills the GPU several times over
@@ -502,7 +507,7 @@ void launch_merge(vxm_ctx* c, const vxm::KParams& kp, int S, cudaStream_t st) {
     if (kp.key_fmt == vxm::kClearKeys)
       VXM_CK(vxm::launch_pdl(vxm::merge_shift_count_kernel<true>, grid, dim3(kMergeThreads), 0, st, kp, rpw));
     else
-      VXM_CK(vxm::launch_pdl(vxm::merge_shift_count_kernel<false>, grid, dim3(kMergeThreads), 0, st, kp, rpw));
+      VXM_CK(vxm::launch_pdl(vxm::merge_epoch_kernel, grid, dim3(kMergeThreads), 0, st, kp, rpw));
     VXM_CK(cudaGetLastError());
   } else {
     launch_merge_chain(c, kp, c->F, S / c->F, st);
@@ -794,7 +799,9 @@ void run_frame(vxm_ctx* c, bool cloud, bool direct = false) {
       if (!g) g = capture_branch(c, s0, s1 - s0, bs);
       // the branch may start before ev[0] (recorded behind the previous
       // call's joins) fires: the frame time runs from the earliest branch start
+#ifndef VXM_NO_BSTART
       VXM_CK(cudaEventRecord(c->bstart[b], bs));
+#endif
       VXM_CK(cudaGraphLaunch(g, bs));
       VXM_CK(cudaEventRecord(c->ddone[b], bs));
       VXM_CK(cudaStreamWaitEvent(c->stream, c->ddone[b], 0));
@@ -878,7 +885,9 @@ void run_frame(vxm_ctx* c, bool cloud, bool direct = false) {
   }
   VXM_CK(cudaEventRecord(c->ev[5], c->stream));
   VXM_CK(cudaEventRecord(c->pp_free[c->pp], c->stream));  // its FrameParams may be overwritten
+#ifndef VXM_NO_BSTART
   c->desync_started = desync_call ? B : 0;
+#endif
   if (desync_call) {
     c->tail_pending = false;
   } else {
@@ -1207,12 +1216,14 @@ int vxm_create_multi(const vxm_config* cfg, int32_t n_streams, int32_t frames_pe
     kp.vh = c->bundle[2];
     kp.tiles_x = (kp.vw + 7) / 8;
     kp.tiles_y = (kp.vh + 3) / 4;
-    for (const void* fn : {reinterpret_cast<const void*>(vxm::merge_shift_count_tma_kernel<false>),
+    for (const void* fn : {reinterpret_cast<const void*>(vxm::merge_epoch_tma_kernel),
                            reinterpret_cast<const void*>(vxm::merge_shift_count_tma_kernel<true>)})
       VXM_CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(2 * vxm::merge_tma_smem_bytes(vxm::kMergeStageCells))));
-    for (const void* fn : {reinterpret_cast<const void*>(vxm::populate_depth_tma_kernel<true>),
-                           reinterpret_cast<const void*>(vxm::populate_depth_tma_kernel<false>)})
+    for (const void* fn : {reinterpret_cast<const void*>(vxm::populate_depth_tma_kernel<true, false>),
+                           reinterpret_cast<const void*>(vxm::populate_depth_tma_kernel<false, false>),
+                           reinterpret_cast<const void*>(vxm::populate_depth_tma_kernel<true, true>),
+                           reinterpret_cast<const void*>(vxm::populate_depth_tma_kernel<false, true>)})
       VXM_CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>((sizeof(float4) + 4 * sizeof(uint16_t)) * kPopulateThreads *
                                                    vxm::kPopMaxIters)));

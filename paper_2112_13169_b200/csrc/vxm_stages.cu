@@ -150,7 +150,7 @@ int vxm_populate_occupied(const vxm_grid_spec* grid, uint8_t* ms, const double* 
     kp.vox_inf = vox_inf;
     kp.counters = d_cnt.p;
     kp.frames = d_frame.p;
-    vxm::populate_cloud_kernel<<<dim3(blocks_for(static_cast<long long>(n), 256), 1), 256>>>(kp);
+    vxm::populate_cloud_kernel<false><<<dim3(blocks_for(static_cast<long long>(n), 256), 1), 256>>>(kp);
     VXM_SCK(cudaGetLastError());
     const bool generic = vox_inf > 0 && vxm::dilate_generic(vox_inf, kp.dx);
     DevBuf<uint32_t> d_bits(vox_inf > 0 && !generic

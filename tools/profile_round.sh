@@ -6,7 +6,7 @@ set -x
 mkdir -p gpurun_out
 TAG=${1:-r01}
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
-    --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 3 --latency-frames 5 --no-cpu-baseline \
+    --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 3 --no-extras --no-cpu-baseline \
     > gpurun_out/${TAG}_bench_under_ncu.log 2>&1
 for k in trace_bundle populate_depth dilate_rows dilate_tiles merge_shift; do
   ncu --set full --clock-control none --import-source on -k regex:$k -s 4 -c 1 -o gpurun_out/${TAG}_$k \
