@@ -780,6 +780,24 @@ __device__ __forceinline__ void ray_setup(const double* R, const double* start, 
   }
 }
 
+// The tmax update of a DDA step: only the chosen axis advances. Selected
+// addends (t + 0 == t for the other two: tmax >= 0) keep the three adds
+// unpredicated; VXM_PRED_ADDS (A/B) predicates the adds instead.
+#ifdef VXM_PRED_ADDS
+#define VXM_STEP_ADDS(E0, E1, E2)                 \
+  "@px add.rn.f64 %0, %0, " E0 ";\n\t"          \
+  "@py add.rn.f64 %1, %1, " E1 ";\n\t"          \
+  "@pz add.rn.f64 %2, %2, " E2 ";\n\t"
+#else
+#define VXM_STEP_ADDS(E0, E1, E2)                 \
+  "selp.f64 a0, " E0 ", 0d0000000000000000, px;\n\t" \
+  "selp.f64 a1, " E1 ", 0d0000000000000000, py;\n\t" \
+  "selp.f64 a2, " E2 ", 0d0000000000000000, pz;\n\t" \
+  "add.rn.f64 %0, %0, a0;\n\t"                  \
+  "add.rn.f64 %1, %1, a1;\n\t"                  \
+  "add.rn.f64 %2, %2, a2;\n\t"
+#endif
+
 // Two shapes (measured, tools/ab_time.sh): batches of frames run kChunk = 4
 // steps per chunk in 2-warp blocks held to 40 registers (48 warps per SM, a
 // few spilled values; 4-7% faster than one warp per block at 64 registers),
@@ -1017,12 +1035,7 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
               "and.pred py, q, npx;\n\t"
               "or.pred pz, px, py;\n\t"
               "not.pred pz, pz;\n\t"
-              "selp.f64 a0, %4, 0d0000000000000000, px;\n\t"
-              "selp.f64 a1, %5, 0d0000000000000000, py;\n\t"
-              "selp.f64 a2, %6, 0d0000000000000000, pz;\n\t"
-              "add.rn.f64 %0, %0, a0;\n\t"
-              "add.rn.f64 %1, %1, a1;\n\t"
-              "add.rn.f64 %2, %2, a2;\n\t"
+              VXM_STEP_ADDS("%4", "%5", "%6")
               "selp.b32 l, %8, %9, py;\n\t"
               "selp.b32 l, %7, l, px;\n\t"
               "add.s32 %3, %3, l;\n\t"
@@ -1057,12 +1070,7 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
             "or.pred ok, s0, s1;\n\t"
             "or.pred ok, ok, s2;\n\t"
             "selp.u32 %4, %4, 0, ok;\n\t"
-            "selp.f64 a0, %5, 0d0000000000000000, px;\n\t"
-            "selp.f64 a1, %6, 0d0000000000000000, py;\n\t"
-            "selp.f64 a2, %7, 0d0000000000000000, pz;\n\t"
-            "add.rn.f64 %0, %0, a0;\n\t"
-            "add.rn.f64 %1, %1, a1;\n\t"
-            "add.rn.f64 %2, %2, a2;\n\t"
+            VXM_STEP_ADDS("%5", "%6", "%7")
             "selp.b32 l, %12, %13, py;\n\t"
             "selp.b32 l, %11, l, px;\n\t"
             "add.s32 %3, %3, l;\n\t"

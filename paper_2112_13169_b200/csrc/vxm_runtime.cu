@@ -420,20 +420,19 @@ void launch_stages(vxm_ctx* c, bool cloud, bool capturing, int s0, int S, cudaSt
       // staged quads + per-warp lists of valid pixels (u16, 4 per quad)
       const size_t smem = (sizeof(float4) + 4 * sizeof(uint16_t)) * kPopulateThreads * static_cast<size_t>(iters);
       const bool clr = kp.key_fmt == vxm::kClearKeys;
-      if (c->pop_compact)
-        (clr ? vxm::populate_depth_tma_kernel<true, true> : vxm::populate_depth_tma_kernel<true, false>)
-            <<<grid, kPopulateThreads, smem, st>>>(kp, iters);
-      else
-        (clr ? vxm::populate_depth_tma_kernel<false, true> : vxm::populate_depth_tma_kernel<false, false>)
-            <<<grid, kPopulateThreads, smem, st>>>(kp, iters);
+      auto k1 = c->pop_compact ? (clr ? vxm::populate_depth_tma_kernel<true, true> : vxm::populate_depth_tma_kernel<true, false>)
+                               : (clr ? vxm::populate_depth_tma_kernel<false, true> : vxm::populate_depth_tma_kernel<false, false>);
+      VXM_CK(vxm::launch_ex(false, k1, grid, dim3(kPopulateThreads), smem, st, kp, iters));
     } else {
-      (kp.key_fmt == vxm::kClearKeys ? vxm::populate_depth_kernel<true> : vxm::populate_depth_kernel<false>)
-          <<<grid, kPopulateThreads, 0, st>>>(kp, iters);
+      VXM_CK(vxm::launch_ex(false, vxm::g_stage_priority,
+                            kp.key_fmt == vxm::kClearKeys ? vxm::populate_depth_kernel<true> : vxm::populate_depth_kernel<false>,
+                            grid, dim3(kPopulateThreads), 0, st, kp, iters));
     }
   } else {
     dim3 grid(static_cast<unsigned>(c->nsm * 4), S);
-    (kp.key_fmt == vxm::kClearKeys ? vxm::populate_cloud_kernel<true> : vxm::populate_cloud_kernel<false>)
-        <<<grid, kPopulateThreads, 0, st>>>(kp);
+    VXM_CK(vxm::launch_ex(false, vxm::g_stage_priority,
+                          kp.key_fmt == vxm::kClearKeys ? vxm::populate_cloud_kernel<true> : vxm::populate_cloud_kernel<false>,
+                          grid, dim3(kPopulateThreads), 0, st, kp));
   }
   VXM_CK(cudaGetLastError());
   if (kp.vox_inf > 0) {
