@@ -424,13 +424,13 @@ void launch_stages(vxm_ctx* c, bool cloud, bool capturing, int s0, int S, cudaSt
                                : (clr ? vxm::populate_depth_tma_kernel<false, true> : vxm::populate_depth_tma_kernel<false, false>);
       VXM_CK(vxm::launch_ex(false, k1, grid, dim3(kPopulateThreads), smem, st, kp, iters));
     } else {
-      VXM_CK(vxm::launch_ex(false, vxm::g_stage_priority,
+      VXM_CK(vxm::launch_ex(false,
                             kp.key_fmt == vxm::kClearKeys ? vxm::populate_depth_kernel<true> : vxm::populate_depth_kernel<false>,
                             grid, dim3(kPopulateThreads), 0, st, kp, iters));
     }
   } else {
     dim3 grid(static_cast<unsigned>(c->nsm * 4), S);
-    VXM_CK(vxm::launch_ex(false, vxm::g_stage_priority,
+    VXM_CK(vxm::launch_ex(false,
                           kp.key_fmt == vxm::kClearKeys ? vxm::populate_cloud_kernel<true> : vxm::populate_cloud_kernel<false>,
                           grid, dim3(kPopulateThreads), 0, st, kp));
   }
