@@ -752,6 +752,13 @@ __device__ __forceinline__ void ray_setup(const double* R, const double* start, 
   double d[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
+#ifdef VXM_EIGEN34_MATVEC
+    // Eigen 3.4's 3x3 * 3-vector: row 2 sums a0 + (a1 + a2) (see VoxmapEigenSubset.h)
+    if (a == 2) {
+      d[a] = dadd(dmul(R[3 * a], v0), dadd(dmul(R[3 * a + 1], v1), dmul(R[3 * a + 2], v2)));
+      continue;
+    }
+#endif
     d[a] = dadd(dadd(dmul(R[3 * a], v0), dmul(R[3 * a + 1], v1)), dmul(R[3 * a + 2], v2));
   }
   const double xs = static_cast<double>(xi), ys = static_cast<double>(yi),
@@ -1160,8 +1167,19 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
 
 // Launches K3 over `slots` frame slots in the shape that suits the batch.
 constexpr long long kSplitMaxRays = 32768;
+// batch K3 shape (A/B defines): kChunk 4, 2-warp blocks, 24 resident blocks
+// per SM (40 registers), no fast chunks
 #ifndef VXM_TB_MINB
-#define VXM_TB_MINB 24  // batch K3: 2-warp blocks at 40 registers (A/B define)
+#define VXM_TB_MINB 24
+#endif
+#ifndef VXM_TB_CHUNK
+#define VXM_TB_CHUNK 4
+#endif
+#ifndef VXM_TB_WARPS
+#define VXM_TB_WARPS 2
+#endif
+#ifndef VXM_TB_FAST
+#define VXM_TB_FAST false
 #endif
 
 // `batch` is the number of slots of the whole call (graph branches launch
@@ -1169,7 +1187,8 @@ constexpr long long kSplitMaxRays = 32768;
 inline void launch_trace(const KParams& kp, int slots, int batch, cudaStream_t st) {
   const int tiles = kp.tiles_x * kp.tiles_y;
   if (batch >= 8) {
-    launch_pdl(trace_bundle_kernel<4, 2, VXM_TB_MINB, true, false, false>, dim3((tiles + 1) / 2, slots), dim3(64), 0, st, kp);
+    launch_pdl(trace_bundle_kernel<VXM_TB_CHUNK, VXM_TB_WARPS, VXM_TB_MINB, true, VXM_TB_FAST, false>,
+               dim3((tiles + VXM_TB_WARPS - 1) / VXM_TB_WARPS, slots), dim3(32 * VXM_TB_WARPS), 0, st, kp);
   } else {
     if (static_cast<long long>(kp.vw) * kp.vh * batch <= kSplitMaxRays) {
       // few rays (the GPU far from full): 8x2 tiles, each ray walked as two

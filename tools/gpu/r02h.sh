@@ -1,0 +1,7 @@
+for rep in 1 2; do
+for lib in libvxm.so libvxm_c8.so libvxm_m20.so libvxm_w4.so libvxm_fast.so; do
+  echo "== $lib"
+  VXM_LIB_NAME=$lib timeout 300 python bench.py --no-extras --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('bench value', d['value'], 'stage', d['stage_ms_per_step'])"
+done
+done > gpurun_out/r02h_ab.txt 2>&1
+cat gpurun_out/r02h_ab.txt
