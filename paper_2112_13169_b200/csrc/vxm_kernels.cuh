@@ -873,9 +873,13 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   // occupancy byte, so either both write or neither does.
   // kTail: invalid cells only follow the end of the ray (the in-grid walk);
   // otherwise they can precede its entry into the grid (camera outside).
-  auto resolve_t = [&](const uint32_t (&cell)[kChunk], auto tail_tag) {
+  // Two phases: prefetch issues the chunk's occupancy loads and dedup masks,
+  // finish resolves the cells. (A software-pipelined walk that put the next
+  // chunk's steps between them was measured slower: at 40 registers it
+  // spills, at 64 the lower occupancy costs more than the latency it hides.)
+  auto prefetch_t = [&](const uint32_t (&cell)[kChunk], uint32_t (&o)[kChunk], uint32_t (&dup)[kChunk],
+                        auto tail_tag) {
     constexpr bool kTail = decltype(tail_tag)::value;
-    uint32_t o[kChunk];
 #pragma unroll
     for (int j = 0; j < kChunk; ++j) {
       // a lane whose ray has ended reads as "occupied": no write, no count
@@ -885,7 +889,6 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
     // the dedup first, for all cells of the chunk (it does not depend on the
     // loads, so its shuffle / match latency overlaps theirs): dup[j] != 0
     // when a higher lane makes the same cell in step j
-    uint32_t dup[kChunk];
 #pragma unroll
     for (int j = 0; j < kChunk; ++j) {
       if constexpr (kMatch) {
@@ -910,6 +913,10 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
             : "r"(cell[j]), "n"(kSplit ? 0x101f : 0x1f));  // kSplit: 16-lane segments (the halves)
       }
     }
+  };
+  auto finish_t = [&](const uint32_t (&cell)[kChunk], const uint32_t (&o)[kChunk], const uint32_t (&dup)[kChunk],
+                      auto tail_tag) {
+    constexpr bool kTail = decltype(tail_tag)::value;
 #pragma unroll
     for (int j = 0; j < kChunk; ++j) {
 // the per-cell resolve: predicates io (occupied) / w (write), the counters,
@@ -949,6 +956,11 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
 #undef VXM_RESOLVE_DECL
 #undef VXM_RESOLVE_BODY
     }
+  };
+  auto resolve_t = [&](const uint32_t (&cell)[kChunk], auto tail_tag) {
+    uint32_t o[kChunk], dup[kChunk];
+    prefetch_t(cell, o, dup, tail_tag);
+    finish_t(cell, o, dup, tail_tag);
   };
   auto resolve = [&](const uint32_t (&cell)[kChunk]) { resolve_t(cell, std::false_type{}); };
   // (kSplit: a near half's cells after its stop must not set its traced bit,
@@ -1025,35 +1037,8 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
     const double Mmin = fmin(fmin(M0, M1), M2);
     const double lim = dsub(Mmin, dadd(dmul(static_cast<double>(kChunk - 1), dmax),
                                        dmul(0x1p-40, dadd(fabs(Mmin), dmul(static_cast<double>(kChunk), dmax)))));
-    while (__any_sync(0xffffffffu, al != 0u)) {
-      if (kFast && __all_sync(0xffffffffu, !al || t0 < lim || t1 < lim || t2 < lim)) {
-        uint32_t cell[kChunk];
-#pragma unroll
-        for (int j = 0; j < kChunk; ++j) {
-          cell[j] = al ? uidx : 0xffffffffu;
-          asm("{\n\t"
-              ".reg .pred q, px, py, pz, npx;\n\t"
-              ".reg .f64 a0, a1, a2;\n\t"
-              ".reg .b32 l;\n\t"
-              "setp.le.f64 q, %0, %1;\n\t"
-              "setp.le.and.f64 px, %0, %2, q;\n\t"
-              "setp.le.f64 q, %1, %2;\n\t"
-              "not.pred npx, px;\n\t"
-              "and.pred py, q, npx;\n\t"
-              "or.pred pz, px, py;\n\t"
-              "not.pred pz, pz;\n\t"
-              VXM_STEP_ADDS("%4", "%5", "%6")
-              "selp.b32 l, %8, %9, py;\n\t"
-              "selp.b32 l, %7, l, px;\n\t"
-              "add.s32 %3, %3, l;\n\t"
-              "}"
-              : "+d"(t0), "+d"(t1), "+d"(t2), "+r"(uidx)
-              : "d"(e0), "d"(e1), "d"(e2), "r"(lin0), "r"(lin1), "r"(lin2));
-        }
-        resolve_tail(cell);
-        continue;
-      }
-      uint32_t cell[kChunk];
+    // kChunk exact steps (threshold tests included), their cells into cell[]
+    auto step_chunk = [&](uint32_t (&cell)[kChunk]) {
 #pragma unroll
       for (int j = 0; j < kChunk; ++j) {
         cell[j] = al ? uidx : 0xffffffffu;
@@ -1088,6 +1073,37 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
         // far half's first
         if (kSplit && !far_half && !al) cell[j] = 0xffffffffu;
       }
+    };
+    while (__any_sync(0xffffffffu, al != 0u)) {
+      if (kFast && __all_sync(0xffffffffu, !al || t0 < lim || t1 < lim || t2 < lim)) {
+        uint32_t cell[kChunk];
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) {
+          cell[j] = al ? uidx : 0xffffffffu;
+          asm("{\n\t"
+              ".reg .pred q, px, py, pz, npx;\n\t"
+              ".reg .f64 a0, a1, a2;\n\t"
+              ".reg .b32 l;\n\t"
+              "setp.le.f64 q, %0, %1;\n\t"
+              "setp.le.and.f64 px, %0, %2, q;\n\t"
+              "setp.le.f64 q, %1, %2;\n\t"
+              "not.pred npx, px;\n\t"
+              "and.pred py, q, npx;\n\t"
+              "or.pred pz, px, py;\n\t"
+              "not.pred pz, pz;\n\t"
+              VXM_STEP_ADDS("%4", "%5", "%6")
+              "selp.b32 l, %8, %9, py;\n\t"
+              "selp.b32 l, %7, l, px;\n\t"
+              "add.s32 %3, %3, l;\n\t"
+              "}"
+              : "+d"(t0), "+d"(t1), "+d"(t2), "+r"(uidx)
+              : "d"(e0), "d"(e1), "d"(e2), "r"(lin0), "r"(lin1), "r"(lin2));
+        }
+        resolve_tail(cell);
+        continue;
+      }
+      uint32_t cell[kChunk];
+      step_chunk(cell);
       resolve_tail(cell);
     }
     if constexpr (kSplit) {
