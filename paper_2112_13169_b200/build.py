@@ -27,7 +27,7 @@ NVFLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler",
 
 CU_SOURCES = ["vxm_unity.cu"]
 CU_INCLUDED = ["vxm_runtime.cu", "vxm_stages.cu"]
-CU_HEADERS = ["vxm_device.cuh", "vxm_kernels.cuh", "vxm_aux_kernels.cuh", "host/voxgrid_format.hpp"]
+CU_HEADERS = ["vxm_device.cuh", "vxm_kernels.cuh", "vxm_aux_kernels.cuh", "vxm_tuning.h", "host/voxgrid_format.hpp"]
 
 
 def _run(cmd, cwd=None):

@@ -11,6 +11,7 @@
 #include <type_traits>
 
 #include "vxm_device.cuh"
+#include "vxm_tuning.h"
 
 namespace vxm {
 
@@ -1183,20 +1184,7 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
 
 // Launches K3 over `slots` frame slots in the shape that suits the batch.
 constexpr long long kSplitMaxRays = 32768;
-// batch K3 shape (A/B defines): kChunk 4, 2-warp blocks, 24 resident blocks
-// per SM (40 registers), no fast chunks
-#ifndef VXM_TB_MINB
-#define VXM_TB_MINB 24
-#endif
-#ifndef VXM_TB_CHUNK
-#define VXM_TB_CHUNK 4
-#endif
-#ifndef VXM_TB_WARPS
-#define VXM_TB_WARPS 2
-#endif
-#ifndef VXM_TB_FAST
-#define VXM_TB_FAST false
-#endif
+// batch K3 shape: VXM_TB_* (vxm_tuning.h)
 
 // `batch` is the number of slots of the whole call (graph branches launch
 // shares of it concurrently, so the GPU is as full as the total says).

@@ -265,9 +265,6 @@ struct vxm_ctx {
   // FrameParams on the device, two buffers: the upload for the next call
   // (on param_stream) overlaps the graph of this one, and each buffer has
   // its own instance of every frame graph
-#ifndef VXM_PP
-#define VXM_PP 2
-#endif
   static constexpr int kPP = VXM_PP;
   vxm::FrameParams* frames_pp[kPP] = {nullptr, nullptr};
   int pp = 0;  // buffer of the current call
@@ -277,9 +274,6 @@ struct vxm_ctx {
   float* depth_dev = nullptr;
   // double-buffered staging for vxm_integrate_depth_async (created lazily)
   cudaStream_t copy_stream = nullptr;
-#ifndef VXM_BRANCHES
-#define VXM_BRANCHES 3
-#endif
   static constexpr int kBranches = VXM_BRANCHES;
   cudaStream_t side[kBranches] = {};  // streams of graph branches 1..
   cudaEvent_t fork[kBranches] = {}, join[kBranches] = {};

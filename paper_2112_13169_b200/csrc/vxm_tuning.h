@@ -1,0 +1,37 @@
+// Build-time tuning knobs of the kernels and the runtime, in one place. The
+// defaults are the measured optima on B200 (tools/ab_build.sh builds a
+// variant library with -D overrides; tools/quick_time.py / bench.py time it
+// with VXM_LIB_NAME=...). Product code never tests these names anywhere else.
+#pragma once
+
+// FrameParams device buffers (each with its own instance of every frame
+// graph): the upload for call k+1 runs while call k's graph executes. 3 and 4
+// measured no faster than 2.
+#ifndef VXM_PP
+#define VXM_PP 2
+#endif
+
+// Graph branches of a batch (equal shares of the streams, desynchronised
+// per-branch graphs): 3 beat 2, 4 and 6 (64 cfg2 streams: 2 branches -9%,
+// 4 branches -3%).
+#ifndef VXM_BRANCHES
+#define VXM_BRANCHES 3
+#endif
+
+// Batch ray-cast shape: kChunk steps per resolve, warps per block, resident
+// blocks per SM (which sets the register cap: 24 x 2 warps -> 40 registers),
+// fast (threshold-free) chunks. Measured alternatives, 64 cfg2 streams:
+// chunk 8 -25% frames/s, 20 blocks (48 registers) -2%, 4-warp blocks at 40
+// registers -1%, fast chunks -4%.
+#ifndef VXM_TB_CHUNK
+#define VXM_TB_CHUNK 4
+#endif
+#ifndef VXM_TB_WARPS
+#define VXM_TB_WARPS 2
+#endif
+#ifndef VXM_TB_MINB
+#define VXM_TB_MINB 24
+#endif
+#ifndef VXM_TB_FAST
+#define VXM_TB_FAST false
+#endif
