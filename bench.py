@@ -304,6 +304,18 @@ def profiled_traffic():
     return None, None
 
 
+def step_instructions():
+    """warp instructions of one batched cfg2 step (64 frames) from the committed
+    ncu capture (tools/summarize_profiles.py -> profiles/step_instructions.json)"""
+    f = ROOT / "profiles" / "step_instructions.json"
+    if f.exists():
+        try:
+            return json.loads(f.read_text())
+        except Exception:
+            pass
+    return None
+
+
 def pct(v, q):
     v = sorted(v)
     pos = q * (len(v) - 1)
@@ -535,6 +547,18 @@ def our_arm(args, world, rank, local):
     cl = clocks.summary()
     if cl:
         line["clocks"] = cl
+    # The step is instruction-issue bound (every kernel but the merge runs at
+    # 63-81% issue-active in ncu): its floor is the warp instructions of the
+    # five stages over the GPU's issue rate (SMs x 4 schedulers x SM clock).
+    si = step_instructions()
+    if si and S == 64 and si.get("total"):
+        props = torch.cuda.get_device_properties(dev)
+        mhz = (cl or {}).get("sm_mhz") or 1965
+        floor_ms = si["total"] / (props.multi_processor_count * 4 * mhz * 1e6) * 1e3
+        line["issue_roofline"] = {"bound": "warp-instruction issue", "warp_instructions_per_step": int(si["total"]),
+                                  "floor_ms_per_step": round(floor_ms, 4), "ms_per_step": round(ms / K, 4),
+                                  "frac": round(floor_ms / (ms / K), 4),
+                                  "source": si.get("source"), "per_kernel": si.get("warp_instructions")}
     if backend:
         line["dist_backend"] = backend
     wl_pool = wl

@@ -75,11 +75,16 @@ def kernel_section(tag, k):
         return f"### {k}\n\n(no capture{note})", None
     det = ncu_csv(["-i", str(rep), "--page", "details", "--csv"])
     out = [f"### {k}", "", "| metric | value | unit |", "|---|---|---|"]
+    vals = {}
     for r in det:
         if len(r) > 4 and r[-4] in KEEP:
             out.append(f"| {r[-4]} | {r[-2]} | {r[-3]} |")
+            if r[-4] == "Executed Instructions":
+                try:
+                    vals["executed_instructions"] = float(r[-2].replace(",", ""))
+                except ValueError:
+                    pass
     raw = ncu_csv(["-i", str(rep), "--page", "raw", "--csv"])
-    vals = {}
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
     if len(raw) >= 3:
         for key, unit, v in zip(raw[0], raw[1], raw[2]):
@@ -123,10 +128,13 @@ def main():
         md += ["```", gpu.read_text().strip(), "```", ""]
     md += ["## Launch list of the bench command", "", launch_table(tag), ""]
     traffic = alu = issue = None
+    step_instr = {}
     for k in ("trace_bundle", "populate_depth", "dilate_rows", "dilate_tiles", "merge_shift", "merge_sequence",
               "merge_tma"):
         sec, vals = kernel_section(tag, k)
         md += [sec, ""]
+        if vals and k in ("trace_bundle", "populate_depth", "dilate_rows", "dilate_tiles", "merge_shift"):
+            step_instr[k] = vals.get("executed_instructions")
         if k == "trace_bundle" and vals:
             try:
                 traffic = float(vals.get("dram__bytes_read.sum", 0)) + float(vals.get("dram__bytes_write.sum", 0))
@@ -141,6 +149,13 @@ def main():
              "alu_pipe_pct_of_peak": alu, "issue_active_pct": issue,
              "launch": "cfg2, 64 streams (one batched step)", "source": f"gpurun_out/{tag}_trace_bundle.ncu-rep"},
             indent=1))
+    if step_instr:
+        # warp instructions the batched cfg2 step executes (one single-branch
+        # launch of each stage over 64 frames; K5 publish is negligible):
+        # bench.py turns them into the step's issue floor
+        (OUT / "step_instructions.json").write_text(json.dumps(
+            {"tag": tag, "workload": "cfg2, 64 streams (one batched step)", "warp_instructions": step_instr,
+             "total": sum(v for v in step_instr.values() if v), "source": f"profiles/{tag}_kernels.md"}, indent=1))
     print((OUT / f"{tag}_kernels.md").read_text()[:3000])
 
 
