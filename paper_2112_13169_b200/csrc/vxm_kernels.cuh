@@ -36,7 +36,7 @@ __device__ __forceinline__ unsigned populate_point(const KParams& p, const doubl
     return 1u;  // counted in points_outside
   }
   const uint32_t idx = static_cast<uint32_t>(c[0]) + static_cast<uint32_t>(c[1]) * p.dx +
-                       static_cast<uint32_t>(c[2]) * static_cast<uint32_t>(p.dx * p.dy);
+                       static_cast<uint32_t>(c[2]) * (static_cast<uint32_t>(p.dx) * static_cast<uint32_t>(p.dy));
   target[idx] = mark;  // idempotent: every writer stores the same byte
   if (rowflag) {
     // a centre: the dilation only visits x-rows that hold one this frame
@@ -448,7 +448,8 @@ __global__ void __launch_bounds__(256) dilate_tiles_kernel(KParams p, int r_rt) 
   for (int i = threadIdx.x; i < H * H; i += blockDim.x) {
     const int hz = i / H, hy = i - hz * H;
     const int y = y0 - r + hy, z = z0 - r + hz;
-    const bool f = y >= 0 && y < p.dy && z >= 0 && z < p.dz && rf[z * p.dy + y] == e;
+    const bool f = y >= 0 && y < p.dy && z >= 0 && z < p.dz &&
+                   rf[static_cast<uint32_t>(z) * static_cast<uint32_t>(p.dy) + static_cast<uint32_t>(y)] == e;
     fl[i] = f ? 1 : 0;
     anyf = anyf || f;
   }
@@ -503,7 +504,7 @@ __global__ void __launch_bounds__(256) dilate_tiles_kernel(KParams p, int r_rt) 
       const int w = i & (WP - 1), row = i >> lg;
       const int hz = row / H, hy = row - hz * H;
       const int y = y0 - r + hy, z = z0 - r + hz;
-      bx[i] = fl[row] ? __ldg(plane + ((z * p.dy + y) << lg) + w) : 0u;
+      bx[i] = fl[row] ? __ldg(plane + ((static_cast<long long>(z) * p.dy + y) << lg) + w) : 0u;
     }
   }
   __syncthreads();
@@ -846,11 +847,15 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   if (blockIdx.x == 0 && threadIdx.x == 0) p.counters[s].t_trace = global_ns();
 
   const unsigned dx = p.dx, dy = p.dy, dz = p.dz;
-  const int dxy = p.dx * p.dy;
-  // linear-index increment of one step along each axis
-  const int lin0 = st.step[0], lin1 = st.step[1] * p.dx, lin2 = st.step[2] * dxy;
+  const uint32_t dxy = dx * dy;
+  // linear-index increment of one step along each axis; cell indices are
+  // uint32 (grids of fewer than 2^32 cells) in modular arithmetic, exact for
+  // every in-grid cell
+  const uint32_t lin0 = static_cast<uint32_t>(st.step[0]), lin1 = static_cast<uint32_t>(st.step[1]) * dx,
+                 lin2 = static_cast<uint32_t>(st.step[2]) * dxy;
   unsigned x = st.cur[0], y = st.cur[1], z = st.cur[2];
-  int idx = st.cur[0] + st.cur[1] * p.dx + st.cur[2] * dxy;
+  uint32_t idx = static_cast<uint32_t>(st.cur[0]) + static_cast<uint32_t>(st.cur[1]) * dx +
+                 static_cast<uint32_t>(st.cur[2]) * dxy;
   double t0 = st.tmax[0], t1 = st.tmax[1], t2 = st.tmax[2];
   const double stop = st.stop;
 
@@ -1248,7 +1253,7 @@ __device__ __forceinline__ void pp_visit(const KParams& p, const int* c, const i
     return;
   }
   const uint32_t idx = static_cast<uint32_t>(c[0]) + static_cast<uint32_t>(c[1]) * p.dx +
-                       static_cast<uint32_t>(c[2]) * static_cast<uint32_t>(p.dx * p.dy);
+                       static_cast<uint32_t>(c[2]) * (static_cast<uint32_t>(p.dx) * static_cast<uint32_t>(p.dy));
   if (occ[idx] != epoch) {
     // Free (every per-pixel write stores the same lowest-priority Free key)
     key[idx] = ray_key(p.key_fmt, epoch, -1);
@@ -2230,7 +2235,7 @@ __global__ void __launch_bounds__(256) merge_sequence_epoch_kernel(KParams p, in
   }
   __syncthreads();
   const int dx = p.dx, dy = p.dy, dz = p.dz;
-  const int dxy = dx * dy;
+  const uint32_t dxy = static_cast<uint32_t>(dx) * static_cast<uint32_t>(dy);  // (cells < 2^32)
   const int bx = f0->box_lo[0], by = f0->box_lo[1], bz = f0->box_lo[2];
   const int ex = f0->box_ext[0], ey = f0->box_ext[1], ez = f0->box_ext[2];
   const long long nchain = static_cast<long long>(ex) * ey * ez;
@@ -2254,18 +2259,19 @@ __global__ void __launch_bounds__(256) merge_sequence_epoch_kernel(KParams p, in
       const int rem = static_cast<int>(i - static_cast<long long>(iz) * ex4 * ey);
       const int iy = rem / ex4;
       const int gx = bx + 4 * (rem - iy * ex4), gy = by + iy, gz = bz + iz;
-      auto group_of = [&](int k, bool& in) {  // first cell of the group at c_{k-1}
+      auto group_of = [&](int k, bool& in) -> uint32_t {  // first cell of the group at c_{k-1}
         const int cx = gx - Pc[k][0], cy = gy - Pc[k][1], cz = gz - Pc[k][2];
         in = active && static_cast<unsigned>(cx) < static_cast<unsigned>(dx) &&
              static_cast<unsigned>(cy) < static_cast<unsigned>(dy) && static_cast<unsigned>(cz) < static_cast<unsigned>(dz);
-        return cx + cy * dx + cz * dxy;
+        return static_cast<uint32_t>(cx) + static_cast<uint32_t>(cy) * static_cast<uint32_t>(dx) +
+               static_cast<uint32_t>(cz) * dxy;
       };
       bool in_prev;
-      int pos_prev = group_of(0, in_prev);
+      uint32_t pos_prev = group_of(0, in_prev);
       uint32_t val = in_prev ? *reinterpret_cast<const uint32_t*>(src + pos_prev) : 0u;
       for (int k0 = 0; k0 < F; k0 += U) {
         bool in_c[U];
-        int pos[U];
+        uint32_t pos[U];
         uint32_t o[U];
         uint4 kk[U];
 #pragma unroll
@@ -2273,7 +2279,7 @@ __global__ void __launch_bounds__(256) merge_sequence_epoch_kernel(KParams p, in
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const bool in_r = u == 0 ? in_prev : in_c[u - 1];
-          const int r = u == 0 ? pos_prev : pos[u - 1];
+          const uint32_t r = u == 0 ? pos_prev : pos[u - 1];
           const bool ld = k0 + u < F && in_c[u] && in_r;
           const long long off = static_cast<long long>(k0 + u) * p.n + r;
           o[u] = ld ? __ldcs(reinterpret_cast<const uint32_t*>(occ0 + off)) : 0u;
@@ -2310,26 +2316,27 @@ __global__ void __launch_bounds__(256) merge_sequence_epoch_kernel(KParams p, in
     const int rem = static_cast<int>(i - static_cast<long long>(iz) * ex * ey);
     const int iy = rem / ex;
     const int gx = bx + rem - iy * ex, gy = by + iy, gz = bz + iz;
-    auto cell_of = [&](int k, bool& in) {  // c_{k-1} = g - P_{k-1}
+    auto cell_of = [&](int k, bool& in) -> uint32_t {  // c_{k-1} = g - P_{k-1}
       const int cx = gx - Pc[k][0], cy = gy - Pc[k][1], cz = gz - Pc[k][2];
       in = active && static_cast<unsigned>(cx) < static_cast<unsigned>(dx) &&
            static_cast<unsigned>(cy) < static_cast<unsigned>(dy) && static_cast<unsigned>(cz) < static_cast<unsigned>(dz);
-      return cx + cy * dx + cz * dxy;
+      return static_cast<uint32_t>(cx) + static_cast<uint32_t>(cy) * static_cast<uint32_t>(dx) +
+               static_cast<uint32_t>(cz) * dxy;
     };
     bool in_prev;
-    int pos_prev = cell_of(0, in_prev);
+    uint32_t pos_prev = cell_of(0, in_prev);
     uint32_t val = in_prev ? src[pos_prev] : 0u;
     for (int k0 = 0; k0 < F; k0 += U) {
       // positions after frames k0..k0+U-1, then all their loads, then the merges
       bool in_c[U];
-      int pos[U];
+      uint32_t pos[U];
       uint32_t o[U], kk[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) pos[u] = cell_of(k0 + u + 1, in_c[u]);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const bool in_r = u == 0 ? in_prev : in_c[u - 1];
-        const int r = u == 0 ? pos_prev : pos[u - 1];
+        const uint32_t r = u == 0 ? pos_prev : pos[u - 1];
         const bool ld = k0 + u < F && in_c[u] && in_r;
         const long long off = static_cast<long long>(k0 + u) * p.n + r;
         o[u] = ld ? __ldcs(occ0 + off) : 0u;
@@ -2402,7 +2409,7 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
   }
   __syncthreads();
   const int dx = p.dx, dy = p.dy, dz = p.dz;
-  const int dxy = dx * dy;
+  const uint32_t dxy = static_cast<uint32_t>(dx) * static_cast<uint32_t>(dy);  // (cells < 2^32)
   const int bx = f0->box_lo[0], by = f0->box_lo[1], bz = f0->box_lo[2];
   const int ex = f0->box_ext[0], ey = f0->box_ext[1], ez = f0->box_ext[2];
   const long long nchain = static_cast<long long>(ex) * ey * ez;
@@ -2429,18 +2436,19 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
       const int rem = static_cast<int>(i - static_cast<long long>(iz) * ex4 * ey);
       const int iy = rem / ex4;
       const int gx = bx + 4 * (rem - iy * ex4), gy = by + iy, gz = bz + iz;
-      auto group_of = [&](int k, bool& in) {  // first cell of the group at c_{k-1}
+      auto group_of = [&](int k, bool& in) -> uint32_t {  // first cell of the group at c_{k-1}
         const int cx = gx - Pc[k][0], cy = gy - Pc[k][1], cz = gz - Pc[k][2];
         in = active && static_cast<unsigned>(cx) < static_cast<unsigned>(dx) &&
              static_cast<unsigned>(cy) < static_cast<unsigned>(dy) && static_cast<unsigned>(cz) < static_cast<unsigned>(dz);
-        return cx + cy * dx + cz * dxy;
+        return static_cast<uint32_t>(cx) + static_cast<uint32_t>(cy) * static_cast<uint32_t>(dx) +
+               static_cast<uint32_t>(cz) * dxy;
       };
       bool in_prev;
-      int pos_prev = group_of(0, in_prev);
+      uint32_t pos_prev = group_of(0, in_prev);
       uint32_t val = in_prev ? *reinterpret_cast<const uint32_t*>(src + pos_prev) : 0u;
       for (int k0 = 0; k0 < F; k0 += U) {
         bool in_c[U];
-        int pos[U];
+        uint32_t pos[U];
         uint32_t o[U];
         uint4 kk[U];
 #pragma unroll
@@ -2448,7 +2456,7 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const bool in_r = u == 0 ? in_prev : in_c[u - 1];
-          const int r = u == 0 ? pos_prev : pos[u - 1];
+          const uint32_t r = u == 0 ? pos_prev : pos[u - 1];
           const bool ld = k0 + u < F && in_r && (kClear || in_c[u]);
           const long long off = static_cast<long long>(k0 + u) * p.n + r;
           o[u] = ld && !kClear ? __ldcs(reinterpret_cast<const uint32_t*>(occ0 + off)) : 0u;
@@ -2487,26 +2495,27 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
     const int rem = static_cast<int>(i - static_cast<long long>(iz) * ex * ey);
     const int iy = rem / ex;
     const int gx = bx + rem - iy * ex, gy = by + iy, gz = bz + iz;
-    auto cell_of = [&](int k, bool& in) {  // c_{k-1} = g - P_{k-1}
+    auto cell_of = [&](int k, bool& in) -> uint32_t {  // c_{k-1} = g - P_{k-1}
       const int cx = gx - Pc[k][0], cy = gy - Pc[k][1], cz = gz - Pc[k][2];
       in = active && static_cast<unsigned>(cx) < static_cast<unsigned>(dx) &&
            static_cast<unsigned>(cy) < static_cast<unsigned>(dy) && static_cast<unsigned>(cz) < static_cast<unsigned>(dz);
-      return cx + cy * dx + cz * dxy;
+      return static_cast<uint32_t>(cx) + static_cast<uint32_t>(cy) * static_cast<uint32_t>(dx) +
+               static_cast<uint32_t>(cz) * dxy;
     };
     bool in_prev;
-    int pos_prev = cell_of(0, in_prev);
+    uint32_t pos_prev = cell_of(0, in_prev);
     uint32_t val = in_prev ? src[pos_prev] : 0u;
     for (int k0 = 0; k0 < F; k0 += U) {
       // positions after frames k0..k0+U-1, then all their loads, then the merges
       bool in_c[U];
-      int pos[U];
+      uint32_t pos[U];
       uint32_t o[U], kk[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) pos[u] = cell_of(k0 + u + 1, in_c[u]);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const bool in_r = u == 0 ? in_prev : in_c[u - 1];
-        const int r = u == 0 ? pos_prev : pos[u - 1];
+        const uint32_t r = u == 0 ? pos_prev : pos[u - 1];
         const bool ld = k0 + u < F && in_r && (kClear || in_c[u]);
         const long long off = static_cast<long long>(k0 + u) * p.n + r;
         o[u] = ld && !kClear ? __ldcs(occ0 + off) : 0u;

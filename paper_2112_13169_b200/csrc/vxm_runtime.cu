@@ -1044,8 +1044,11 @@ void validate_config(const vxm_config& cfg) {
   if (!(cfg.depth > 0.0) || cfg.depth > cfg.camera.max_depth)
     throw InvalidArg{"PipelineConfig: depth must lie in (0, camera.max_depth]"};
   if (!(g.vox_size > 0.0)) throw InvalidArg{"vox_size must be positive"};
-  if (static_cast<long long>(g.dims[0]) * g.dims[1] * g.dims[2] >= (1LL << 31))
-    throw InvalidArg{"grid larger than 2^31 cells is not supported"};
+  // 32-bit cell indices (modular arithmetic, 0xFFFFFFFF is the tracer's
+  // "no cell"): up to 2^32 - 2 cells (a 4 GB grid), x-rows counted in int
+  if (static_cast<long long>(g.dims[0]) * g.dims[1] * g.dims[2] > 0xFFFFFFFELL ||
+      static_cast<long long>(g.dims[1]) * g.dims[2] >= (1LL << 31))
+    throw InvalidArg{"grids of more than 2^32 - 2 cells (or 2^31 x-rows) are not supported"};
 }
 
 }  // namespace

@@ -98,6 +98,9 @@ void check_grid(const vxm_grid_spec* g) {
   if (g->dims[0] < 1 || g->dims[1] < 1 || g->dims[2] < 1)
     throw StageError{VXM_EINVAL, "grid must be at least one voxel per axis"};
   if (!(g->vox_size > 0.0)) throw StageError{VXM_EINVAL, "vox_size must be positive"};
+  if (static_cast<long long>(g->dims[0]) * g->dims[1] * g->dims[2] > 0xFFFFFFFELL ||
+      static_cast<long long>(g->dims[1]) * g->dims[2] >= (1LL << 31))
+    throw StageError{VXM_EINVAL, "grids of more than 2^32 - 2 cells (or 2^31 x-rows) are not supported"};
 }
 
 void fill_pose(vxm::FrameParams& f, const vxm_pose& t) {

@@ -145,3 +145,28 @@ def test_clear_keys_batched_and_multi_frame(gpu_lib, S, F):
             _check(sb[i], sa[i], (call, i))
     for s in range(S):
         assert np.array_equal(a.local_grid(s)[0], b.local_grid(s)[0]), s
+
+
+def test_grid_beyond_2_31_cells(gpu_lib):
+    """A local grid of 2048 x 1024 x 1025 = 2,149,580,800 cells (> 2^31; the
+    reference accepts any size, proj/src/grid.cpp:17-42): 32-bit cell indices
+    in modular arithmetic cover grids of up to 2^32 - 2 cells. Rows of 2048
+    cells also take the generic dilation and the row-wise merge. Two frames,
+    the second recentring the grid, against the reference (which needs ~6 GB
+    of host memory here)."""
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 64, 48, 3.0)
+    grid = vm.GridSpec.create_centered(204.8, 102.4, 102.5, 0.1, (0.0, 0.0, 0.0))
+    assert grid.dims == (2048, 1024, 1025) and grid.cell_count() > 2 ** 31
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=1, depth=3.0)
+    gpu, orc = vm.MappingPipeline(cfg), oracle_pipeline(cfg)
+    boxes = np.array([[1.5, -2.0, -1.0, 1.8, 2.0, 1.0], [2.2, -0.5, -2.0, 2.5, 0.5, 0.5]])
+    for k, pos in enumerate([(0.0, 0.0, 0.0), (0.05, 0.27, -0.13)]):
+        pose = vm.look_along_x(pos)
+        depth = scenes.render(cam, pose, boxes)
+        sg, sr = gpu.integrate_depth(depth, pose), orc.integrate_depth(depth, pose)
+        _check(sg, sr, k)
+    assert sr["shifted"]
+    assert np.array_equal(gpu.local_grid()[0], orc.local_grid()[0])
+    with pytest.raises(ValueError, match="2\\^32"):
+        vm.MappingPipeline(vm.PipelineConfig(vm.GridSpec.create_centered(204.8, 204.8, 102.5, 0.1, (0, 0, 0)),
+                                             cam, vox_inf=0, depth=3.0))

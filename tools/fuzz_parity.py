@@ -4,7 +4,8 @@ camera sizes, vox_inf 0-5, depth limits, general rotations and robot motion
 (shifts along every axis, jumps), single streams and batches (desynchronised
 branches), compared frame by frame (stats) and grid by grid with the
 reference's Sequential pipeline. Prints one summary line per case and a total;
-exits non-zero on the first mismatch. Usage: python tools/fuzz_parity.py [seconds]"""
+exits non-zero on the first mismatch. A quarter of the cases run the
+large-bundle (clear) key format. Usage: python tools/fuzz_parity.py [seconds] [seed]"""
 import math, sys, time
 sys.path.insert(0, '.')
 import numpy as np
@@ -50,14 +51,16 @@ def main():
         poses = [[(rotation(rng, tilt), np.array([0.1 * s, 0.0, 0.0]) + k * step
                    + (np.array([0.0, 3.0, 0.0]) if k == n // 2 and rng.random() < 0.3 else 0.0))
                   for s in range(S)] for k in range(n)]
+        # the large-bundle key format on a quarter of the cases (VXM_FLAG_CLEAR_KEYS)
+        kflags = vm.N.FLAG_CLEAR_KEYS if rng.random() < 0.25 else 0
         desc = dict(vox=vox, dims=tuple(grid.dims), cam=(w, h), vox_inf=vox_inf, S=S, n=n, depth=round(depth_m, 3),
-                    per_pixel=tracer == vm.N.TRACER_PER_PIXEL)
+                    per_pixel=tracer == vm.N.TRACER_PER_PIXEL, clear_keys=bool(kflags))
         print(f"case {cases}: {desc}", flush=True)
         refs = [oracle_pipeline(cfg) for _ in range(S)]
         F = int(rng.choice([1, 1, 1, 2, 5, 33])) if S <= 3 else 1
         if F > 1:
             # multi-frame calls: frames_per_call consecutive frames of each stream
-            gpu = vm.MappingPipeline(cfg, n_streams=S, frames_per_call=F)
+            gpu = vm.MappingPipeline(cfg, n_streams=S, frames_per_call=F, flags=kflags)
             print(f"  frames_per_call {F}", flush=True)
             calls = max(1, n // 2)
             traj = [[(rotation(rng, tilt), np.array([0.1 * s, 0.0, 0.0]) + j * step) for j in range(calls * F)]
@@ -77,7 +80,7 @@ def main():
                                 sys.exit(1)
                 frames += S * F
         else:
-          gpu = vm.MappingPipeline(cfg, n_streams=S)
+          gpu = vm.MappingPipeline(cfg, n_streams=S, flags=kflags)
           path = str(rng.choice(["host", "device", "async"]))
           print(f"  path {path}", flush=True)
           keep = []
