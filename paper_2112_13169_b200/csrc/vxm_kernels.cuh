@@ -834,13 +834,19 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   const bool far_half = kSplit && lane >= 16;
   const int xi_idx = tx * 8 + (rl & 7);
   const int yi_idx = ty * (kSplit ? 2 : 4) + (rl >> 3);
-  const bool active = ty < (kSplit ? (p.vh + 1) / 2 : p.tiles_y) && xi_idx < p.vw && yi_idx < p.vh;
-  const uint32_t ray = static_cast<uint32_t>(yi_idx) * p.vw + xi_idx;  // row-major, y outer
+  if (ty >= (kSplit ? (p.vh + 1) / 2 : p.tiles_y)) return;  // a whole warp past the bundle (block rounding)
+  const bool active = xi_idx < p.vw && yi_idx < p.vh;
+  // Lanes past the bundle's edge (partial edge tiles) walk a clone of the
+  // edge ray, so that inside the grid every lane of a warp is live until its
+  // ray ends: the clone makes the same cells, occupancy reads and keys as its
+  // original (RED.max of equal keys, and the dedup keeps one of them), and
+  // its counters are not added.
+  const int xr = xi_idx < p.vw ? xi_idx : p.vw - 1, yr = yi_idx < p.vh ? yi_idx : p.vh - 1;
+  const uint32_t ray = static_cast<uint32_t>(yr) * p.vw + xr;  // row-major, y outer
   const uint32_t ray_key = vxm::ray_key(p.key_fmt, epoch, ray);  // | 1: UnknownTraced
 
-
   RayState st;
-  ray_setup(R, start, p.vs, p.ray_vs, xi_idx - (p.vw - 1) / 2, yi_idx - (p.vh - 1) / 2, p.vd, st);
+  ray_setup(R, start, p.vs, p.ray_vs, xr - (p.vw - 1) / 2, yr - (p.vh - 1) / 2, p.vd, st);
   // the ray setup above overlaps the tail of the populate/dilation kernels;
   // occupancy is read only from here on
   pdl_wait();
@@ -861,14 +867,15 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
 
   bool walking = active && !far_half;  // (outside the grid a split warp walks whole rays on its near lanes)
   bool entered = false;
-  uint32_t traced_bit = 0;
   unsigned freed = 0, traced = 0, skipped = 0;
 
-  // Lean resolve (inline PTX, no branches): per cell one predicated
-  // occupancy load, the write/traced counters (freed = writes - traced, summed
-  // at the end), the neighbour dedup through the shuffles' in-range
-  // predicates, and a predicated fire-and-forget RED.max on the key.
-  unsigned lw = 0, lt = 0;
+  // Lean resolve (inline PTX, no branches but the RED's): per cell one
+  // occupancy load, the write counter lw, the traced state carried in the
+  // key itself (kv = ray_key | traced), snap = lw at the first occupied cell
+  // (so traced writes = lw - snap at the end), the neighbour dedup through a
+  // mask, and a predicated fire-and-forget RED.max on the key.
+  uint32_t kv = ray_key;
+  unsigned lw = 0, snap = 0xffffffffu;
   const unsigned long long key_base = reinterpret_cast<unsigned long long>(key);
   uint32_t gt_mask;  // lanes above this one (higher ray indices)
   asm("mov.u32 %0, %%lanemask_gt;" : "=r"(gt_mask));
@@ -883,14 +890,20 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   // finish resolves the cells. (A software-pipelined walk that put the next
   // chunk's steps between them was measured slower: at 40 registers it
   // spills, at 64 the lower occupancy costs more than the latency it hides.)
+  // kLive: every cell of the chunk is valid (fast chunks: all lanes live).
   auto prefetch_t = [&](const uint32_t (&cell)[kChunk], uint32_t (&o)[kChunk], uint32_t (&dup)[kChunk],
-                        auto tail_tag) {
+                        auto tail_tag, auto live_tag) {
     constexpr bool kTail = decltype(tail_tag)::value;
+    constexpr bool kLive = decltype(live_tag)::value;
 #pragma unroll
     for (int j = 0; j < kChunk; ++j) {
       // a lane whose ray has ended reads as "occupied": no write, no count
-      // (its traced bit no longer matters)
-      o[j] = cell[j] != 0xffffffffu ? __ldg(occ + cell[j]) : (kTail ? epoch : 0u);
+      // (its traced state no longer matters; snap stays at or below its
+      // final write count)
+      if constexpr (kLive)
+        o[j] = __ldg(occ + cell[j]);
+      else
+        o[j] = cell[j] != 0xffffffffu ? __ldg(occ + cell[j]) : (kTail ? epoch : 0u);
     }
     // the dedup first, for all cells of the chunk (it does not depend on the
     // loads, so its shuffle / match latency overlaps theirs): dup[j] != 0
@@ -925,20 +938,20 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
     constexpr bool kTail = decltype(tail_tag)::value;
 #pragma unroll
     for (int j = 0; j < kChunk; ++j) {
-// the per-cell resolve: predicates io (occupied) / w (write), the counters,
-// the traced-bit state, ok = w and no higher-lane duplicate, the RED.max
+// the per-cell resolve: predicates io (occupied) / w (write), the write
+// count, snap, ok = w and no higher-lane duplicate, the RED.max of the key
+// as it stands (a written cell is never occupied, so the traced bit, set
+// after, cannot change at it), then the traced bit
 #define VXM_RESOLVE_BODY                   \
   "@w add.u32 %1, %1, 1;\n\t"            \
-  "@w add.u32 %2, %2, %0;\n\t"           \
-  "or.b32 kv, %6, %0;\n\t"               \
-  "selp.u32 %0, 1, %0, io;\n\t"          \
-  "setp.eq.and.u32 ok, %8, 0, w;\n\t"    \
+  "@io min.u32 %2, %2, %1;\n\t"          \
+  "setp.eq.and.u32 ok, %7, 0, w;\n\t"    \
   "mul.wide.u32 a, %3, 4;\n\t"           \
-  "add.u64 a, a, %7;\n\t"                \
-  "@ok red.relaxed.gpu.global.max.u32 [a], kv;\n\t"
+  "add.u64 a, a, %6;\n\t"                \
+  "@ok red.relaxed.gpu.global.max.u32 [a], %0;\n\t" \
+  "@io or.b32 %0, %0, 1;\n\t"
 #define VXM_RESOLVE_DECL                   \
   ".reg .pred v, io, w, ok;\n\t"         \
-  ".reg .b32 kv;\n\t"                    \
   ".reg .b64 a;\n\t"
 // kTail: the cell is valid or the ray has ended (o == epoch: no write)
 #define VXM_RESOLVE_HEAD_TAIL "setp.eq.u32 io|w, %4, %5;\n\t"
@@ -947,10 +960,10 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   "setp.ne.u32 v, %3, -1;\n\t"            \
   "setp.eq.and.u32 io, %4, %5, v;\n\t"    \
   "setp.ne.and.u32 w, %4, %5, v;\n\t"
-#define VXM_RESOLVE_ASM(HEAD)                                                                 \
-  asm volatile("{\n\t" VXM_RESOLVE_DECL HEAD VXM_RESOLVE_BODY "}"                            \
-               : "+r"(traced_bit), "+r"(lw), "+r"(lt)                                         \
-               : "r"(cell[j]), "r"(o[j]), "r"(epoch), "r"(ray_key), "l"(key_base), "r"(dup[j]) \
+#define VXM_RESOLVE_ASM(HEAD)                                                    \
+  asm volatile("{\n\t" VXM_RESOLVE_DECL HEAD VXM_RESOLVE_BODY "}"               \
+               : "+r"(kv), "+r"(lw), "+r"(snap)                                  \
+               : "r"(cell[j]), "r"(o[j]), "r"(epoch), "l"(key_base), "r"(dup[j]) \
                : "memory")
       if constexpr (kTail)
         VXM_RESOLVE_ASM(VXM_RESOLVE_HEAD_TAIL);
@@ -963,20 +976,22 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
 #undef VXM_RESOLVE_BODY
     }
   };
-  auto resolve_t = [&](const uint32_t (&cell)[kChunk], auto tail_tag) {
+  auto resolve_t = [&](const uint32_t (&cell)[kChunk], auto tail_tag, auto live_tag) {
     uint32_t o[kChunk], dup[kChunk];
-    prefetch_t(cell, o, dup, tail_tag);
+    prefetch_t(cell, o, dup, tail_tag, live_tag);
     finish_t(cell, o, dup, tail_tag);
   };
-  auto resolve = [&](const uint32_t (&cell)[kChunk]) { resolve_t(cell, std::false_type{}); };
+  auto resolve = [&](const uint32_t (&cell)[kChunk]) { resolve_t(cell, std::false_type{}, std::false_type{}); };
   // (kSplit: a near half's cells after its stop must not set its traced bit,
   // which the far half reads, so invalid cells take the general form)
   auto resolve_tail = [&](const uint32_t (&cell)[kChunk]) {
     if constexpr (kSplit)
-      resolve_t(cell, std::false_type{});
+      resolve_t(cell, std::false_type{}, std::false_type{});
     else
-      resolve_t(cell, std::true_type{});
+      resolve_t(cell, std::true_type{}, std::false_type{});
   };
+  // every cell valid (a fast chunk): the tail form without the invalid-cell loads
+  auto resolve_live = [&](const uint32_t (&cell)[kChunk]) { resolve_t(cell, std::true_type{}, std::true_type{}); };
 
   // The camera (every ray's start) is shared by the whole frame, so this
   // branch is uniform. Inside the grid the walk needs no per-cell bounds
@@ -1008,9 +1023,15 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
     double M0 = M[0], M1 = M[1], M2 = M[2];
     // tdelta of an axis the ray never steps along is +inf; that axis is never
     // chosen, and the selected-addend form below needs a finite value for it
-    const double e0 = st.step[0] ? st.tdelta[0] : 0.0, e1 = st.step[1] ? st.tdelta[1] : 0.0,
-                 e2 = st.step[2] ? st.tdelta[2] : 0.0;
-    uint32_t al = active ? 1u : 0u;
+    // (and clamped to a finite value: the fast chunks add m * tdelta with
+    // m in {0, 1}, which must leave t unchanged for m = 0; an axis whose
+    // tdelta overflows is never chosen before the walk ends, and when it is
+    // chosen at the walk's last step the sum no longer matters)
+    constexpr double kMaxFinite = 0x1.fffffffffffffp+1023;
+    const double e0 = st.step[0] ? fmin(st.tdelta[0], kMaxFinite) : 0.0,
+                 e1 = st.step[1] ? fmin(st.tdelta[1], kMaxFinite) : 0.0,
+                 e2 = st.step[2] ? fmin(st.tdelta[2], kMaxFinite) : 0.0;
+    uint32_t al = 1u;  // every lane (clones included) walks a ray inside the grid
     // kSplit: the steps whose chosen tmax is below tau = min(M) / 2 (none of
     // which can end the walk) are the near half; its lane walks them with
     // every threshold at tau. The far lane starts where they end: along each
@@ -1022,7 +1043,7 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
       const double tau = dmul(0.5, fmin(fmin(M0, M1), M2));
       if (!far_half) {
         M0 = M1 = M2 = tau;
-      } else if (active) {
+      } else {
         while (t0 < tau) { t0 = dadd(t0, e0); idx += lin0; }
         while (t1 < tau) { t1 = dadd(t1, e1); idx += lin1; }
         while (t2 < tau) { t2 = dadd(t2, e2); idx += lin2; }
@@ -1031,18 +1052,19 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
       }
     }
     uint32_t uidx = static_cast<uint32_t>(idx);
-    // Fast chunks (kFast): the walk can only end at a step whose chosen tmax (the
-    // current minimum) reaches min(M_a); the minimum grows by at most
-    // max(tdelta) per step, so while min(t) < lim = min(M) - (kChunk-1) *
-    // max(tdelta) (less a 2^-40 relative margin for the rounded adds) no
-    // step of the next chunk can end the walk and the threshold tests are
-    // skipped. The warp takes the fast form when all its live lanes qualify.
-    // Measured: 2-5% faster for a lone frame (8-step chunks, 72 registers);
-    // 2% slower in the 40-register batch kernel, which does not use it.
-    const double dmax = fmax(fmax(e0, e1), e2);
+    // Fast chunks (kFast): the walk ends at a step whose chosen tmax reaches
+    // its axis' threshold M_a >= min(M). Within the next kChunk steps every
+    // chosen tmax is at most min_a(t_a + (kChunk-1) tdelta_a): were axis b
+    // that minimum, each step takes the current minimum, which is at most
+    // b's current value, and b advances at most kChunk-1 times before the
+    // last step. So while that bound (an fma, one rounding; the walk's
+    // repeated adds stay within (kChunk+1) 2^-53 of it) is below lim =
+    // min(M)(1 - 2^-40), no step of the chunk can end the walk: the chunk
+    // runs without threshold tests, and with every lane live its cells are
+    // all valid (no invalid-cell handling in the resolve). The warp takes
+    // it when all lanes qualify (~80% of a cfg2 bundle's chunks).
     const double Mmin = fmin(fmin(M0, M1), M2);
-    const double lim = dsub(Mmin, dadd(dmul(static_cast<double>(kChunk - 1), dmax),
-                                       dmul(0x1p-40, dadd(fabs(Mmin), dmul(static_cast<double>(kChunk), dmax)))));
+    constexpr double kAhead = static_cast<double>(kChunk - 1);
     // kChunk exact steps (threshold tests included), their cells into cell[]
     auto step_chunk = [&](uint32_t (&cell)[kChunk]) {
 #pragma unroll
@@ -1080,24 +1102,35 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
         if (kSplit && !far_half && !al) cell[j] = 0xffffffffu;
       }
     };
-    while (__any_sync(0xffffffffu, al != 0u)) {
-      if (kFast && __all_sync(0xffffffffu, !al || t0 < lim || t1 < lim || t2 < lim)) {
+    // lim = -inf once the lane's walk has ended (set after the exact chunk
+    // it ends in), so the fast test needs no liveness term
+    double lim = dsub(Mmin, dmul(0x1p-40, fabs(Mmin)));
+    for (;;) {
+      // every lane live and no step of the next kChunk able to end its walk
+      if (kFast && __all_sync(0xffffffffu, __fma_rn(kAhead, e0, t0) < lim || __fma_rn(kAhead, e1, t1) < lim ||
+                                               __fma_rn(kAhead, e2, t2) < lim)) {
         uint32_t cell[kChunk];
 #pragma unroll
         for (int j = 0; j < kChunk; ++j) {
-          cell[j] = al ? uidx : 0xffffffffu;
+          cell[j] = uidx;
+          // the step without threshold tests: t_a = fma(m_a, e_a, t_a) with
+          // m_a = 1 on the chosen axis, 0 elsewhere (fma(1, e, t) = RN(t + e),
+          // fma(0, e, t) = t), one select of a high word per axis
           asm("{\n\t"
-              ".reg .pred q, px, py, pz, npx;\n\t"
-              ".reg .f64 a0, a1, a2;\n\t"
+              ".reg .pred q, px, py, pxy;\n\t"
+              ".reg .f64 m0, m1, m2;\n\t"
               ".reg .b32 l;\n\t"
               "setp.le.f64 q, %0, %1;\n\t"
               "setp.le.and.f64 px, %0, %2, q;\n\t"
               "setp.le.f64 q, %1, %2;\n\t"
-              "not.pred npx, px;\n\t"
-              "and.pred py, q, npx;\n\t"
-              "or.pred pz, px, py;\n\t"
-              "not.pred pz, pz;\n\t"
-              VXM_STEP_ADDS("%4", "%5", "%6")
+              "and.pred py, q, !px;\n\t"
+              "or.pred pxy, px, py;\n\t"
+              "selp.f64 m0, 0d3FF0000000000000, 0d0000000000000000, px;\n\t"
+              "selp.f64 m1, 0d3FF0000000000000, 0d0000000000000000, py;\n\t"
+              "selp.f64 m2, 0d0000000000000000, 0d3FF0000000000000, pxy;\n\t"
+              "fma.rn.f64 %0, m0, %4, %0;\n\t"
+              "fma.rn.f64 %1, m1, %5, %1;\n\t"
+              "fma.rn.f64 %2, m2, %6, %2;\n\t"
               "selp.b32 l, %8, %9, py;\n\t"
               "selp.b32 l, %7, l, px;\n\t"
               "add.s32 %3, %3, l;\n\t"
@@ -1105,28 +1138,31 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
               : "+d"(t0), "+d"(t1), "+d"(t2), "+r"(uidx)
               : "d"(e0), "d"(e1), "d"(e2), "r"(lin0), "r"(lin1), "r"(lin2));
         }
-        resolve_tail(cell);
+        resolve_live(cell);
         continue;
       }
+      if (!__any_sync(0xffffffffu, al != 0u)) break;
       uint32_t cell[kChunk];
       step_chunk(cell);
       resolve_tail(cell);
+      if (!al) lim = -__longlong_as_double(0x7ff0000000000000ll);
     }
     if constexpr (kSplit) {
       // The far half resolved its cells as if nothing before it were
       // occupied. If the near half met an occupied cell, the far half's writes
-      // before its own first occupied cell (lw - lt of them, all unoccupied)
-      // carry the traced bit: count them so and write their keys again with
-      // it (RED.max: the higher key wins), walking that prefix once more.
-      const uint32_t near_traced = __shfl_sync(0xffffffffu, traced_bit, lane & 15);
+      // before its own first occupied cell (min(snap, lw) of them, all
+      // unoccupied) carry the traced bit: count them so and write their keys
+      // again with it (RED.max: the higher key wins), walking that prefix once
+      // more. (A clone's original does this for it.)
+      const uint32_t near_traced = __shfl_sync(0xffffffffu, kv & 1u, lane & 15);
       if (far_half && active && near_traced) {
-        unsigned n = lw - lt;
-        lt = lw;
+        unsigned n = min(snap, lw);
+        snap = 0;
         double a0 = fs0, a1 = fs1, a2 = fs2;
         uint32_t u = fidx;
-        const uint32_t kv = ray_key | 1u;
+        const uint32_t kt = ray_key | 1u;
         for (; n > 0; --n) {
-          atomicMax(key + u, kv);
+          atomicMax(key + u, kt);
           const bool bx = a0 <= a1 && a0 <= a2;
           const bool by = !bx && a1 <= a2;
           if (bx) { a0 = dadd(a0, e0); u += lin0; }
@@ -1135,8 +1171,6 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
         }
       }
     }
-    freed += lw - lt;
-    traced += lt;
   } else {
   while (__any_sync(0xffffffffu, walking)) {
     uint32_t cell[kChunk];
@@ -1171,8 +1205,12 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
     }
     resolve(cell);
   }
-  freed += lw - lt;
-  traced += lt;
+  }
+  // writes before the first occupied cell free, the rest are traced; a
+  // clone's counts belong to its original
+  if (active) {
+    freed = min(snap, lw);
+    traced = lw - freed;
   }
   unsigned long long* slot = &p.counters[s].trace_slots[tile % kTraceSlots][0];
   const unsigned r_n = __reduce_add_sync(0xffffffffu, active && !far_half ? 1u : 0u);

@@ -19,10 +19,13 @@
 #endif
 
 // Batch ray-cast shape: kChunk steps per resolve, warps per block, resident
-// blocks per SM (which sets the register cap: 24 x 2 warps -> 40 registers),
+// blocks per SM (which sets the register cap: 20 x 2 warps -> 48 registers),
 // fast (threshold-free) chunks. Measured alternatives, 64 cfg2 streams:
-// chunk 8 -25% frames/s, 20 blocks (48 registers) -2%, 4-warp blocks at 40
-// registers -1%, fast chunks -4%.
+// chunk 8 -25% frames/s, 4-warp blocks at 40 registers -1%. Round 2: with
+// the per-axis fast-chunk bound, fma steps and live-lane resolves, fast
+// chunks are +5% (K3 146 -> 136 us per step) and 20 blocks (48 registers,
+// no spills) +0.5% over 24 (40 registers); before them fast chunks were -4%
+// and 20 blocks -2%.
 #ifndef VXM_TB_CHUNK
 #define VXM_TB_CHUNK 4
 #endif
@@ -30,8 +33,8 @@
 #define VXM_TB_WARPS 2
 #endif
 #ifndef VXM_TB_MINB
-#define VXM_TB_MINB 24
+#define VXM_TB_MINB 20
 #endif
 #ifndef VXM_TB_FAST
-#define VXM_TB_FAST false
+#define VXM_TB_FAST true
 #endif
