@@ -38,3 +38,8 @@
 #ifndef VXM_TB_FAST
 #define VXM_TB_FAST true
 #endif
+
+// Also measured for the fast chunks and not kept (same B200, 64 cfg2 streams,
+// within noise): each cell's occupancy load and dedup written right after the
+// step that makes it (ptxas schedules both forms alike), and the axis choice
+// from three independent compares (ptxas re-chains them).
