@@ -8,6 +8,7 @@
 // with -fmad=false as a second guard.
 #pragma once
 
+#include <cmath>
 #include <cstddef>
 #include <cstdint>
 
@@ -137,8 +138,28 @@ struct FrameParams {
   // frames 0..k) that some frame's grid covers (merge_sequence_kernel)
   int32_t box_lo[3];
   int32_t box_ext[3];
+  // per-frame constants of every ray's walk set-up (walk_ray,
+  // raytracer.hpp:80-98), computed once on the host with the same IEEE
+  // operations: the camera's cell floor(t_vc / vs) and the tmax numerators
+  // (cur + 1) vs - t_vc (positive directions) and cur vs - t_vc (negative)
+  int32_t cam_cell[3];
   uint32_t pad_;
+  double tnum_pos[3];
+  double tnum_neg[3];
 };
+
+// Fills FrameParams::cam_cell / tnum_* from f.trans and the walk's voxel
+// size (host side; the kernels read them instead of dividing per ray).
+inline void set_ray_consts(FrameParams& f, double vs) {
+  for (int a = 0; a < 3; ++a) {
+    const volatile double q = f.trans[a] / vs;  // (volatile: no contraction or reordering)
+    f.cam_cell[a] = static_cast<int>(std::floor(q));
+    const volatile double hp = static_cast<double>(f.cam_cell[a] + 1) * vs;
+    const volatile double hn = static_cast<double>(f.cam_cell[a]) * vs;
+    f.tnum_pos[a] = hp - f.trans[a];
+    f.tnum_neg[a] = hn - f.trans[a];
+  }
+}
 
 // Constant (per-context) launch parameters, passed by value.
 struct KParams {

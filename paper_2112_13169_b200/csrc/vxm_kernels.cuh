@@ -746,7 +746,7 @@ struct RayState {
 // golden vectors), |dir|^2 = (d0^2 + d1^2) + d2^2 (Eigen's vectorized redux).
 // gvs is generate_rays' vox_size (direction and max_dist), vs the grid's
 // (the walk): trace_bundle passes both (raytracer.cpp:100, 63-72).
-__device__ __forceinline__ void ray_setup(const double* R, const double* start, double vs,
+__device__ __forceinline__ void ray_setup(const double* R, const FrameParams* fp, double vs,
                                           double gvs, int xi, int yi, int vd, RayState& st) {
   const double v0 = dmul(static_cast<double>(xi), gvs);
   const double v1 = dmul(static_cast<double>(yi), gvs);
@@ -772,14 +772,16 @@ __device__ __forceinline__ void ray_setup(const double* R, const double* start, 
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     const double u = n2 > 0.0 ? ddiv(d[a], nrm) : d[a];
-    st.cur[a] = static_cast<int>(floor(ddiv(start[a], vs)));
+    // cur = floor(start / vs) and the numerators are per-frame constants
+    // (set_ray_consts, the same IEEE operations on the host)
+    st.cur[a] = fp->cam_cell[a];
     if (u > 0.0) {
       st.step[a] = 1;
-      st.tmax[a] = ddiv(dsub(dmul(static_cast<double>(st.cur[a] + 1), vs), start[a]), u);
+      st.tmax[a] = ddiv(fp->tnum_pos[a], u);
       st.tdelta[a] = ddiv(vs, u);
     } else if (u < 0.0) {
       st.step[a] = -1;
-      st.tmax[a] = ddiv(dsub(dmul(static_cast<double>(st.cur[a]), vs), start[a]), u);
+      st.tmax[a] = ddiv(fp->tnum_neg[a], u);
       st.tdelta[a] = ddiv(vs, -u);
     } else {
       st.step[a] = 0;
@@ -819,11 +821,9 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   const uint32_t epoch = fp->epoch;
   uint32_t* const key = fp->key_s;
   const uint8_t* const occ = fp->occ_s;
-  double R[9], start[3];
+  double R[9];
 #pragma unroll
   for (int i = 0; i < 9; ++i) R[i] = fp->rot[i];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) start[i] = fp->trans[i];
 
   const int lane = threadIdx.x & 31;
   const int tile = blockIdx.x * kTraceWarps + (threadIdx.x >> 5);
@@ -846,7 +846,7 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   const uint32_t ray_key = vxm::ray_key(p.key_fmt, epoch, ray);  // | 1: UnknownTraced
 
   RayState st;
-  ray_setup(R, start, p.vs, p.ray_vs, xr - (p.vw - 1) / 2, yr - (p.vh - 1) / 2, p.vd, st);
+  ray_setup(R, fp, p.vs, p.ray_vs, xr - (p.vw - 1) / 2, yr - (p.vh - 1) / 2, p.vd, st);
   // the ray setup above overlaps the tail of the populate/dilation kernels;
   // occupancy is read only from here on
   pdl_wait();
@@ -1000,26 +1000,22 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   if (x < dx && y < dy && z < dz) {
     // The walk ends at the first step whose chosen axis a has tmax_a >= M_a,
     // M_a = min(stop, E_a), where E_a is the exact tmax_a value of the step
-    // that would leave the grid along a (its rem_a-th step: the same
-    // repeated additions as the walk, done once here). So every step checks
-    // one threshold and nothing else; no per-step bounds or counters.
+    // that would leave the grid along a (its rem_a-th step). So every step
+    // checks one threshold and nothing else; no per-step bounds or counters.
     const int rem[3] = {st.step[0] > 0 ? static_cast<int>(dx - 1 - x) : static_cast<int>(x),
                         st.step[1] > 0 ? static_cast<int>(dy - 1 - y) : static_cast<int>(y),
                         st.step[2] > 0 ? static_cast<int>(dz - 1 - z) : static_cast<int>(z)};
+    // E_a need not be summed: the walk's tmax values along a are strictly
+    // increasing, T_a[k] ~ t_a + k tdelta_a, so "t_a >= E_a = T_a[rem_a]"
+    // holds exactly when "t_a >= V" for any V in (T_a[rem_a - 1], T_a[rem_a]];
+    // V = t_a + (rem_a - 1/2) tdelta_a is half a step away from both (the
+    // rounding of k repeated adds is ~k 2^-53 of T, far below half a step),
+    // and min(stop, V) decides every step exactly as min(stop, E_a) would.
     double M[3];
     const double tt[3] = {t0, t1, t2};
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      M[a] = stop;
-      // exit beyond the stop distance (with a 2^-30 margin on the estimate):
-      // the stop decides; otherwise sum exactly
-      if (st.step[a] != 0 &&
-          !(dadd(tt[a], dmul(static_cast<double>(rem[a]), st.tdelta[a])) > dmul(stop, 1.0 + 0x1p-30))) {
-        double e = tt[a];
-        for (int k = 0; k < rem[a]; ++k) e = dadd(e, st.tdelta[a]);
-        M[a] = fmin(stop, e);
-      }
-    }
+    for (int a = 0; a < 3; ++a)
+      M[a] = st.step[a] != 0 ? fmin(stop, dadd(tt[a], dmul(static_cast<double>(rem[a]) - 0.5, st.tdelta[a]))) : stop;
     double M0 = M[0], M1 = M[1], M2 = M[2];
     // tdelta of an axis the ray never steps along is +inf; that axis is never
     // chosen, and the selected-addend form below needs a finite value for it

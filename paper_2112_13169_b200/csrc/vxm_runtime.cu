@@ -655,6 +655,7 @@ void prepare_frames(vxm_ctx* c, const vxm_pose* poses, const float* depth_dev_ba
       }
       // the measurement grid takes the local grid's pre-shift origin (pipeline.cpp:84-85)
       camera_to_grid(poses[slot], org, f.rot, f.trans);
+      vxm::set_ray_consts(f, c->cfg.grid.vox_size);
       if (depth_dev_base) f.depth = depth_dev_base + frame_elems * slot;
       f.cur = c->cur[s] ^ static_cast<uint32_t>(range & 1);  // each chained range flips the buffers
       f.occ_s = c->occ + c->n * slot;

@@ -225,6 +225,7 @@ int vxm_trace_bundle(const vxm_grid_spec* grid, uint8_t* ms, const int32_t bundl
     DevBuf<vxm::FrameParams> d_frame(1);
     vxm::FrameParams f{};
     fill_pose(f, *t_vc);
+    vxm::set_ray_consts(f, kp.vs);
     f.epoch = kEpoch;
     f.occ_s = d_occ.p;
     f.key_s = d_key.p;
