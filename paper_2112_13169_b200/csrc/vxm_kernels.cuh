@@ -877,8 +877,13 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   uint32_t kv = ray_key;
   unsigned lw = 0, snap = 0xffffffffu;
   const unsigned long long key_base = reinterpret_cast<unsigned long long>(key);
-  uint32_t gt_mask;  // lanes above this one (higher ray indices)
-  asm("mov.u32 %0, %%lanemask_gt;" : "=r"(gt_mask));
+  // dedup bound: a cell is written when dup <= dup_max. With match.any, dup
+  // is the mask of lanes on the same cell and no higher lane (higher ray
+  // index) shares it exactly when dup <= lanemask_le (one compare instead of
+  // an AND and a compare); the shuffle form gives dup in {0, 1}, bound 0.
+  uint32_t dup_max = 0u;
+  if constexpr (kMatch) asm("mov.u32 %0, %%lanemask_le;" : "=r"(dup_max));
+
   // A write is dropped when a higher lane (higher ray index) makes the same
   // cell in the same step (measured: dropping the dedup after the first
   // chunks slows the kernel, the extra L2 atomics cost more than the check).
@@ -906,15 +911,14 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
         o[j] = cell[j] != 0xffffffffu ? __ldg(occ + cell[j]) : (kTail ? epoch : 0u);
     }
     // the dedup first, for all cells of the chunk (it does not depend on the
-    // loads, so its shuffle / match latency overlaps theirs): dup[j] != 0
-    // when a higher lane makes the same cell in step j
+    // loads, so its shuffle / match latency overlaps theirs): dup[j] >
+    // dup_max when a higher lane makes the same cell in step j
 #pragma unroll
     for (int j = 0; j < kChunk; ++j) {
       if constexpr (kMatch) {
         // the whole warp: only the highest lane of each distinct cell writes
         // (one match; batches, where instruction count decides)
         asm("match.any.sync.b32 %0, %1, -1;" : "=r"(dup[j]) : "r"(cell[j]));
-        dup[j] &= gt_mask;
       } else {
         // lane+1 and lane+8 (two shuffles; the lone-frame kernel, whose serial
         // chain favours short latency)
@@ -945,7 +949,7 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
 #define VXM_RESOLVE_BODY                   \
   "@w add.u32 %1, %1, 1;\n\t"            \
   "@io min.u32 %2, %2, %1;\n\t"          \
-  "setp.eq.and.u32 ok, %7, 0, w;\n\t"    \
+  "setp.le.and.u32 ok, %7, %8, w;\n\t"   \
   "mul.wide.u32 a, %3, 4;\n\t"           \
   "add.u64 a, a, %6;\n\t"                \
   "@ok red.relaxed.gpu.global.max.u32 [a], %0;\n\t" \
@@ -963,7 +967,7 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
 #define VXM_RESOLVE_ASM(HEAD)                                                    \
   asm volatile("{\n\t" VXM_RESOLVE_DECL HEAD VXM_RESOLVE_BODY "}"               \
                : "+r"(kv), "+r"(lw), "+r"(snap)                                  \
-               : "r"(cell[j]), "r"(o[j]), "r"(epoch), "l"(key_base), "r"(dup[j]) \
+               : "r"(cell[j]), "r"(o[j]), "r"(epoch), "l"(key_base), "r"(dup[j]), "r"(dup_max) \
                : "memory")
       if constexpr (kTail)
         VXM_RESOLVE_ASM(VXM_RESOLVE_HEAD_TAIL);
@@ -1103,8 +1107,24 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
     double lim = dsub(Mmin, dmul(0x1p-40, fabs(Mmin)));
     for (;;) {
       // every lane live and no step of the next kChunk able to end its walk
-      if (kFast && __all_sync(0xffffffffu, __fma_rn(kAhead, e0, t0) < lim || __fma_rn(kAhead, e1, t1) < lim ||
-                                               __fma_rn(kAhead, e2, t2) < lim)) {
+      // (PTX compares chained with or: left to ptxas, the three compares
+      // become an fmin with NaN handling, six more instructions per chunk)
+      uint32_t fast_ok = 0;
+      if constexpr (kFast)
+        asm("{\n\t"
+            ".reg .pred p;\n\t"
+            ".reg .f64 b;\n\t"
+            "fma.rn.f64 b, %1, %2, %3;\n\t"
+            "setp.lt.f64 p, b, %8;\n\t"
+            "fma.rn.f64 b, %1, %4, %5;\n\t"
+            "setp.lt.or.f64 p, b, %8, p;\n\t"
+            "fma.rn.f64 b, %1, %6, %7;\n\t"
+            "setp.lt.or.f64 p, b, %8, p;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t"
+            "}"
+            : "=r"(fast_ok)
+            : "d"(kAhead), "d"(e0), "d"(t0), "d"(e1), "d"(t1), "d"(e2), "d"(t2), "d"(lim));
+      if (kFast && __all_sync(0xffffffffu, fast_ok)) {
         uint32_t cell[kChunk];
 #pragma unroll
         for (int j = 0; j < kChunk; ++j) {
