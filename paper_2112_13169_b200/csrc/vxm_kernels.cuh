@@ -791,30 +791,13 @@ __device__ __forceinline__ void ray_setup(const double* R, const FrameParams* fp
   }
 }
 
-// The tmax update of a DDA step: only the chosen axis advances. Selected
-// addends (t + 0 == t for the other two: tmax >= 0) keep the three adds
-// unpredicated; VXM_PRED_ADDS (A/B) predicates the adds instead.
-#ifdef VXM_PRED_ADDS
-#define VXM_STEP_ADDS(E0, E1, E2)                 \
-  "@px add.rn.f64 %0, %0, " E0 ";\n\t"          \
-  "@py add.rn.f64 %1, %1, " E1 ";\n\t"          \
-  "@pz add.rn.f64 %2, %2, " E2 ";\n\t"
-#else
-#define VXM_STEP_ADDS(E0, E1, E2)                 \
-  "selp.f64 a0, " E0 ", 0d0000000000000000, px;\n\t" \
-  "selp.f64 a1, " E1 ", 0d0000000000000000, py;\n\t" \
-  "selp.f64 a2, " E2 ", 0d0000000000000000, pz;\n\t" \
-  "add.rn.f64 %0, %0, a0;\n\t"                  \
-  "add.rn.f64 %1, %1, a1;\n\t"                  \
-  "add.rn.f64 %2, %2, a2;\n\t"
-#endif
 
 // Two shapes (measured, tools/ab_time.sh): batches of frames run kChunk = 4
 // steps per chunk in 2-warp blocks held to 40 registers (48 warps per SM, a
 // few spilled values; 4-7% faster than one warp per block at 64 registers),
 // a lone frame (358 warps, GPU far from full) runs 8-step chunks at 64
 // registers, where per-warp latency decides.
-template <int kChunk, int kTraceWarps, int kMinBlocks, bool kMatch, bool kFast, bool kSplit>
+template <int kChunk, int kTraceWarps, int kMinBlocks, int kMatchMask, bool kFast, bool kSplit>
 __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_kernel(KParams p) {
   const int s = blockIdx.y;
   const FrameParams* fp = p.frames + s;
@@ -882,7 +865,7 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   // index) shares it exactly when dup <= lanemask_le (one compare instead of
   // an AND and a compare); the shuffle form gives dup in {0, 1}, bound 0.
   uint32_t dup_max = 0u;
-  if constexpr (kMatch) asm("mov.u32 %0, %%lanemask_le;" : "=r"(dup_max));
+  if constexpr (kMatchMask != 0) asm("mov.u32 %0, %%lanemask_le;" : "=r"(dup_max));
 
   // A write is dropped when a higher lane (higher ray index) makes the same
   // cell in the same step (measured: dropping the dedup after the first
@@ -915,9 +898,9 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
     // dup_max when a higher lane makes the same cell in step j
 #pragma unroll
     for (int j = 0; j < kChunk; ++j) {
-      if constexpr (kMatch) {
+      if ((kMatchMask >> j) & 1) {
         // the whole warp: only the highest lane of each distinct cell writes
-        // (one match; batches, where instruction count decides)
+        // (one match)
         asm("match.any.sync.b32 %0, %1, -1;" : "=r"(dup[j]) : "r"(cell[j]));
       } else {
         // lane+1 and lane+8 (two shuffles; the lone-frame kernel, whose serial
@@ -967,7 +950,8 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
 #define VXM_RESOLVE_ASM(HEAD)                                                    \
   asm volatile("{\n\t" VXM_RESOLVE_DECL HEAD VXM_RESOLVE_BODY "}"               \
                : "+r"(kv), "+r"(lw), "+r"(snap)                                  \
-               : "r"(cell[j]), "r"(o[j]), "r"(epoch), "l"(key_base), "r"(dup[j]), "r"(dup_max) \
+               : "r"(cell[j]), "r"(o[j]), "r"(epoch), "l"(key_base), "r"(dup[j]),                 \
+                 "r"(((kMatchMask >> j) & 1) ? dup_max : 0u)                                       \
                : "memory")
       if constexpr (kTail)
         VXM_RESOLVE_ASM(VXM_RESOLVE_HEAD_TAIL);
@@ -1090,7 +1074,13 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
             "or.pred ok, s0, s1;\n\t"
             "or.pred ok, ok, s2;\n\t"
             "selp.u32 %4, %4, 0, ok;\n\t"
-            VXM_STEP_ADDS("%5", "%6", "%7")
+            // t_a = fma(m_a, e_a, t_a), m_a in {0, 1} (as in the fast chunks)
+            "selp.f64 a0, 0d3FF0000000000000, 0d0000000000000000, px;\n\t"
+            "selp.f64 a1, 0d3FF0000000000000, 0d0000000000000000, py;\n\t"
+            "selp.f64 a2, 0d3FF0000000000000, 0d0000000000000000, pz;\n\t"
+            "fma.rn.f64 %0, a0, %5, %0;\n\t"
+            "fma.rn.f64 %1, a1, %6, %1;\n\t"
+            "fma.rn.f64 %2, a2, %7, %2;\n\t"
             "selp.b32 l, %12, %13, py;\n\t"
             "selp.b32 l, %11, l, px;\n\t"
             "add.s32 %3, %3, l;\n\t"
@@ -1250,17 +1240,24 @@ constexpr long long kSplitMaxRays = 32768;
 inline void launch_trace(const KParams& kp, int slots, int batch, cudaStream_t st) {
   const int tiles = kp.tiles_x * kp.tiles_y;
   if (batch >= 8) {
-    launch_pdl(trace_bundle_kernel<VXM_TB_CHUNK, VXM_TB_WARPS, VXM_TB_MINB, true, VXM_TB_FAST, false>,
-               dim3((tiles + VXM_TB_WARPS - 1) / VXM_TB_WARPS, slots), dim3(32 * VXM_TB_WARPS), 0, st, kp);
+    // dedup by match.any on every step for large bundles, on every other step
+    // (shuffles between) for small ones (VXM_TB_MATCH_* in vxm_tuning.h)
+    const dim3 grid((tiles + VXM_TB_WARPS - 1) / VXM_TB_WARPS, slots), block(32 * VXM_TB_WARPS);
+    if (static_cast<long long>(kp.vw) * kp.vh >= VXM_TB_MATCH_RAYS)
+      launch_pdl(trace_bundle_kernel<VXM_TB_CHUNK, VXM_TB_WARPS, VXM_TB_MINB, VXM_TB_MATCH_LARGE, VXM_TB_FAST, false>,
+                 grid, block, 0, st, kp);
+    else
+      launch_pdl(trace_bundle_kernel<VXM_TB_CHUNK, VXM_TB_WARPS, VXM_TB_MINB, VXM_TB_MATCH_SMALL, VXM_TB_FAST, false>,
+                 grid, block, 0, st, kp);
   } else {
     if (static_cast<long long>(kp.vw) * kp.vh * batch <= kSplitMaxRays) {
       // few rays (the GPU far from full): 8x2 tiles, each ray walked as two
       // halves by two lanes; measured -12% / -7% K3 time for a lone cfg2 /
       // cfg1 frame, +11% for a lone cfg3 frame (76k rays)
       const int tiles2 = kp.tiles_x * ((kp.vh + 1) / 2);
-      launch_pdl(trace_bundle_kernel<8, 1, 1, false, true, true>, dim3(tiles2, slots), dim3(32), 0, st, kp);
+      launch_pdl(trace_bundle_kernel<8, 1, 1, 0, true, true>, dim3(tiles2, slots), dim3(32), 0, st, kp);
     } else {
-      launch_pdl(trace_bundle_kernel<8, 1, 1, false, true, false>, dim3(tiles, slots), dim3(32), 0, st, kp);
+      launch_pdl(trace_bundle_kernel<8, 1, 1, 0, true, false>, dim3(tiles, slots), dim3(32), 0, st, kp);
     }
   }
 }

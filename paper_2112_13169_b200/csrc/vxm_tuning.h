@@ -38,6 +38,22 @@
 #ifndef VXM_TB_FAST
 #define VXM_TB_FAST true
 #endif
+// Batch ray-cast dedup per step of a chunk: bit j set = match.any over the
+// warp for step j, clear = the lane+1 / lane+8 neighbours by two shuffles.
+// Measured (K3 us per 64 frames, masks 0xF / 0x5 / 0x1 / 0x0): cfg2 (11,439
+// rays) 127.9 / 120.9 / 120.7 / 122.4, where match.any saturates the MIO
+// queue (ncu mio_throttle 15x cfg1's); cfg1 (19,239 rays) 186.4 / 194.6 /
+// 195 / 198.7; cfg3 (76k rays) 299 / 305 / 308 / 311. Bundles of at least
+// VXM_TB_MATCH_RAYS rays take the large mask.
+#ifndef VXM_TB_MATCH_LARGE
+#define VXM_TB_MATCH_LARGE 0xF
+#endif
+#ifndef VXM_TB_MATCH_SMALL
+#define VXM_TB_MATCH_SMALL 0x5
+#endif
+#ifndef VXM_TB_MATCH_RAYS
+#define VXM_TB_MATCH_RAYS 16384
+#endif
 
 // Also measured for the fast chunks and not kept (same B200, 64 cfg2 streams,
 // within noise): each cell's occupancy load and dedup written right after the

@@ -7,7 +7,7 @@ from paper_2112_13169_b200 import voxmap as vm
 from tests import scenes
 DEG = math.pi / 180
 which = sys.argv[1] if len(sys.argv) > 1 else "all"
-for name, vox_inf, dm, S, F in (("cfg1", 0, 6.5, 1, 1), ("cfg2", 2, 5.0, 1, 1), ("cfg2x64", 2, 5.0, 64, 1),
+for name, vox_inf, dm, S, F in (("cfg1", 0, 6.5, 1, 1), ("cfg1x64", 0, 6.5, 64, 1), ("cfg2", 2, 5.0, 1, 1), ("cfg2x64", 2, 5.0, 64, 1),
                                 ("seq64", 2, 5.0, 1, 64), ("cfg3x8", 0, 6.5, 8, 1)):
     if which != "all" and which != name:
         continue
