@@ -64,3 +64,9 @@
 // generic RED to a per-lane shared-memory word (no branch around the RED;
 // ptxas wraps every predicated RED in one): the generic atomics made the
 // batch ray cast 17% slower (130 -> 152 us per 64 cfg2 frames).
+
+// Also measured and not kept: capping the batch ray-cast blocks resident per
+// SM with dynamic shared memory so that the other branches' kernels fit
+// beside them (12 or 16 blocks instead of 20: 323k -> 267k / 286k frames/s,
+// the shared-memory carve-out also shrinks L1 for the occupancy loads), and 4
+// graph branches again after the round-2 ray cast (-2%).
