@@ -775,19 +775,17 @@ __device__ __forceinline__ void ray_setup(const double* R, const FrameParams* fp
     // cur = floor(start / vs) and the numerators are per-frame constants
     // (set_ray_consts, the same IEEE operations on the host)
     st.cur[a] = fp->cam_cell[a];
-    if (u > 0.0) {
-      st.step[a] = 1;
-      st.tmax[a] = ddiv(fp->tnum_pos[a], u);
-      st.tdelta[a] = ddiv(vs, u);
-    } else if (u < 0.0) {
-      st.step[a] = -1;
-      st.tmax[a] = ddiv(fp->tnum_neg[a], u);
-      st.tdelta[a] = ddiv(vs, -u);
-    } else {
-      st.step[a] = 0;
-      st.tmax[a] = __longlong_as_double(0x7ff0000000000000ll);
-      st.tdelta[a] = st.tmax[a];
-    }
+    // u > 0: tmax = tnum_pos / u, tdelta = vs / u; u < 0: tnum_neg / u and
+    // vs / -u; otherwise (0, NaN) both +inf. Written without branches (the
+    // signs of u differ within a warp, the divisions run once): vs / |u| is
+    // vs / u or vs / -u exactly, and the +inf select follows the divisions.
+    const bool pos = u > 0.0, neg = u < 0.0;
+    st.step[a] = pos ? 1 : (neg ? -1 : 0);
+    const double tm = ddiv(pos ? fp->tnum_pos[a] : fp->tnum_neg[a], u);
+    const double td = ddiv(vs, fabs(u));
+    const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+    st.tmax[a] = (pos || neg) ? tm : kInf;
+    st.tdelta[a] = (pos || neg) ? td : kInf;
   }
 }
 
