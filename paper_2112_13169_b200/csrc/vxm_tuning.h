@@ -70,3 +70,9 @@
 // beside them (12 or 16 blocks instead of 20: 323k -> 267k / 286k frames/s,
 // the shared-memory carve-out also shrinks L1 for the occupancy loads), and 4
 // graph branches again after the round-2 ray cast (-2%).
+
+// Also measured and not kept: finished rays parked on a per-slot sentinel
+// occupancy byte (always the frame's epoch) so that a warp keeps taking fast
+// chunks after its first lane ends: K3 115.5 -> 123 us per 64 cfg2 frames
+// (more chunks run with few live lanes, and the mutable step increments
+// spill at 48 registers).
