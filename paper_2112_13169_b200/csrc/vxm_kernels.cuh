@@ -280,7 +280,11 @@ __global__ void __launch_bounds__(256) populate_cloud_kernel(KParams p) {
 // dilates 8x8 tiles of bit rows along y and z in shared memory and writes the
 // Occupied bytes.
 // ---------------------------------------------------------------------------
+// (y, z) tile edge of the dilation (a power of two): 8 for batches, 4 for a
+// lone frame (more blocks for one frame: 30.7 -> 28.7 us per cfg2 frame; 16
+// and 4 measured slower for 64-stream batches, profiles/r02ad_dil_tile_ab.txt)
 constexpr int kDilT = 8;
+constexpr int kDilTLone = 4;
 
 // Word stride of a bit row: ceil(dx/32) rounded up to a power of two, so the
 // index arithmetic is shifts and masks.
@@ -409,11 +413,11 @@ __global__ void __launch_bounds__(256) dilate_rows_vec_kernel(KParams p, int r) 
 
 // Shared memory of K2b: the (8+2r)^2 halo bit rows and the y-dilated rows
 // (fused: also the packed, not yet x-dilated, halo rows).
-__host__ __device__ constexpr size_t dilate_smem_bytes(int r, int dx, bool fused = false) {
+__host__ __device__ constexpr size_t dilate_smem_bytes(int r, int dx, bool fused = false, int T = kDilT) {
   return sizeof(uint32_t) * static_cast<size_t>(dilate_row_words(dx)) *
-             (static_cast<size_t>(kDilT + 2 * r) * (kDilT + 2 * r) * (fused ? 2 : 1) +
-              static_cast<size_t>(kDilT) * (kDilT + 2 * r)) +
-         ((static_cast<size_t>(kDilT + 2 * r) * (kDilT + 2 * r) + 3) & ~static_cast<size_t>(3));  // row flags
+             (static_cast<size_t>(T + 2 * r) * (T + 2 * r) * (fused ? 2 : 1) +
+              static_cast<size_t>(T) * (T + 2 * r)) +
+         ((static_cast<size_t>(T + 2 * r) * (T + 2 * r) + 3) & ~static_cast<size_t>(3));  // row flags
 }
 
 // K2b: a block owns an 8x8 (y,z) tile of x-dilated bit rows, loads them with
@@ -422,7 +426,7 @@ __host__ __device__ constexpr size_t dilate_smem_bytes(int r, int dx, bool fused
 // kR > 0: radius fixed at compile time; kR == 0: radius at run time.
 // kFused: no K2a; the block packs and x-dilates its halo rows itself from the
 // centre bytes (dims_x % 4 == 0: 4-byte loads), one launch fewer.
-template <int kR, bool kFused, bool kClear>
+template <int kR, bool kFused, bool kClear, int kT = kDilT>
 __global__ void __launch_bounds__(256) dilate_tiles_kernel(KParams p, int r_rt) {
   pdl_wait();  // K1's centre bytes (fused) or K2a's bit rows
   extern __shared__ uint32_t bits[];
@@ -434,15 +438,15 @@ __global__ void __launch_bounds__(256) dilate_tiles_kernel(KParams p, int r_rt) 
   const int W = (p.dx + 31) >> 5;
   const int WP = dilate_row_words(p.dx);
   const int lg = __ffs(WP) - 1;
-  const int H = kDilT + 2 * r;
-  const int y0 = blockIdx.x * kDilT, z0 = blockIdx.y * kDilT;
+  const int H = kT + 2 * r;
+  const int y0 = blockIdx.x * kT, z0 = blockIdx.y * kT;
   const uint32_t dxy = static_cast<uint32_t>(p.dx) * p.dy;
   const uint32_t* plane = p.dbits + static_cast<long long>(s) * p.dy * p.dz * WP;
   uint32_t* bx = bits;                  // [H z][H y][WP]
-  uint32_t* by = bx + (H * H << lg);    // [H z][kDilT y][WP], y-dilated
+  uint32_t* by = bx + (H * H << lg);    // [H z][kT y][WP], y-dilated
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
 
-  uint8_t* fl = reinterpret_cast<uint8_t*>(by + ((H * kDilT) << lg));  // [H z][H y] row holds a centre
+  uint8_t* fl = reinterpret_cast<uint8_t*>(by + ((H * kT) << lg));  // [H z][H y] row holds a centre
   const uint8_t* rf = p.rowflag + static_cast<long long>(s) * p.dy * p.dz;
   bool anyf = false;
   for (int i = threadIdx.x; i < H * H; i += blockDim.x) {
@@ -508,9 +512,9 @@ __global__ void __launch_bounds__(256) dilate_tiles_kernel(KParams p, int r_rt) 
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < (H * kDilT) << lg; i += blockDim.x) {
+  for (int i = threadIdx.x; i < (H * kT) << lg; i += blockDim.x) {
     const int w = i & (WP - 1), yz = i >> lg;
-    const int y = yz & (kDilT - 1), hz = yz / kDilT;
+    const int y = yz & (kT - 1), hz = yz / kT;
     const uint32_t* col = bx + ((hz * H + y) << lg) + w;
     uint32_t d = 0;
 #pragma unroll
@@ -521,8 +525,8 @@ __global__ void __launch_bounds__(256) dilate_tiles_kernel(KParams p, int r_rt) 
     by[i] = d;
   }
   __syncthreads();
-  for (int row = warp; row < kDilT * kDilT; row += nw) {
-    const int z = row / kDilT, y = row & (kDilT - 1);
+  for (int row = warp; row < kT * kT; row += nw) {
+    const int z = row / kT, y = row & (kT - 1);
     const int gy = y0 + y, gz = z0 + z;
     if (gy >= p.dy || gz >= p.dz) continue;
     uint8_t* dst = occ + static_cast<uint32_t>(gy) * p.dx + static_cast<uint32_t>(gz) * dxy;
@@ -532,12 +536,12 @@ __global__ void __launch_bounds__(256) dilate_tiles_kernel(KParams p, int r_rt) 
       // have set are its own, so the rest of the word may become 0 (never an
       // epoch); the stage API restores pre-existing Occupied cells itself
       for (int x0 = lane * 4; x0 < p.dx; x0 += 128) {
-        const uint32_t* col = by + ((z * kDilT + y) << lg) + (x0 >> 5);
+        const uint32_t* col = by + ((z * kT + y) << lg) + (x0 >> 5);
         uint32_t d = 0;
 #pragma unroll
         for (int k = 0; k <= 2 * (kR > 0 ? kR : 16); ++k) {
           if (kR == 0 && k > 2 * r) break;
-          d |= col[(k * kDilT) << lg];
+          d |= col[(k * kT) << lg];
         }
         const uint32_t nib = (d >> (x0 & 31)) & 0xFu;
         if (nib) {
@@ -555,12 +559,12 @@ __global__ void __launch_bounds__(256) dilate_tiles_kernel(KParams p, int r_rt) 
       continue;
     }
     for (int w = 0; w < W; ++w) {
-      const uint32_t* col = by + ((z * kDilT + y) << lg) + w;
+      const uint32_t* col = by + ((z * kT + y) << lg) + w;
       uint32_t d = 0;
 #pragma unroll
       for (int k = 0; k <= 2 * (kR > 0 ? kR : 16); ++k) {
         if (kR == 0 && k > 2 * r) break;
-        d |= col[(k * kDilT) << lg];
+        d |= col[(k * kT) << lg];
       }
       const int x = (w << 5) + lane;
       if (x < p.dx && ((d >> lane) & 1u)) {
@@ -628,19 +632,26 @@ inline bool dilate_fused(int r, int dx) {
   return dx % 4 == 0 && dilate_smem_bytes(r, dx, true) <= 200 * 1024;
 }
 
-template <int kR, bool kClear>
-inline void launch_dilate_tiles_k(const KParams& kp, int r, bool fused, dim3 grid, cudaStream_t st) {
+template <int kR, bool kClear, int kT>
+inline void launch_dilate_tiles_k(const KParams& kp, int r, bool fused, cudaStream_t st, int streams) {
+  const dim3 grid((kp.dy + kT - 1) / kT, (kp.dz + kT - 1) / kT, streams);
   if (fused)
-    launch_pdl(dilate_tiles_kernel<kR, true, kClear>, grid, dim3(256), dilate_smem_bytes(r, kp.dx, true), st, kp, r);
+    launch_pdl(dilate_tiles_kernel<kR, true, kClear, kT>, grid, dim3(256), dilate_smem_bytes(r, kp.dx, true, kT), st,
+               kp, r);
   else
-    launch_pdl(dilate_tiles_kernel<kR, false, kClear>, grid, dim3(256), dilate_smem_bytes(r, kp.dx), st, kp, r);
+    launch_pdl(dilate_tiles_kernel<kR, false, kClear, kT>, grid, dim3(256), dilate_smem_bytes(r, kp.dx, false, kT),
+               st, kp, r);
 }
 template <int kR>
-inline void launch_dilate_tiles(const KParams& kp, int r, bool fused, dim3 grid, cudaStream_t st) {
-  if (kp.key_fmt == kClearKeys)
-    launch_dilate_tiles_k<kR, true>(kp, r, fused, grid, st);
-  else
-    launch_dilate_tiles_k<kR, false>(kp, r, fused, grid, st);
+inline void launch_dilate_tiles(const KParams& kp, int r, bool fused, cudaStream_t st, int streams) {
+  const bool lone = streams <= 2;
+  if (kp.key_fmt == kClearKeys) {
+    if (lone) launch_dilate_tiles_k<kR, true, kDilTLone>(kp, r, fused, st, streams);
+    else launch_dilate_tiles_k<kR, true, kDilT>(kp, r, fused, st, streams);
+  } else {
+    if (lone) launch_dilate_tiles_k<kR, false, kDilTLone>(kp, r, fused, st, streams);
+    else launch_dilate_tiles_k<kR, false, kDilT>(kp, r, fused, st, streams);
+  }
 }
 
 // the tile dilation's limits (radius, row length, shared memory)
@@ -672,13 +683,12 @@ inline void launch_dilate(const KParams& kp, int r, int streams, size_t /*smem*/
       launch_pdl(dilate_rows_kernel, dim3((rows + per_block - 1) / per_block, streams), dim3(256), 0, st, kp, r);
     }
   }
-  const dim3 grid((kp.dy + kDilT - 1) / kDilT, (kp.dz + kDilT - 1) / kDilT, streams);
   switch (r) {
-    case 1: launch_dilate_tiles<1>(kp, r, fused, grid, st); break;
-    case 2: launch_dilate_tiles<2>(kp, r, fused, grid, st); break;
-    case 3: launch_dilate_tiles<3>(kp, r, fused, grid, st); break;
-    case 4: launch_dilate_tiles<4>(kp, r, fused, grid, st); break;
-    default: launch_dilate_tiles<0>(kp, r, fused, grid, st); break;
+    case 1: launch_dilate_tiles<1>(kp, r, fused, st, streams); break;
+    case 2: launch_dilate_tiles<2>(kp, r, fused, st, streams); break;
+    case 3: launch_dilate_tiles<3>(kp, r, fused, st, streams); break;
+    case 4: launch_dilate_tiles<4>(kp, r, fused, st, streams); break;
+    default: launch_dilate_tiles<0>(kp, r, fused, st, streams); break;
   }
 }
 
@@ -686,11 +696,16 @@ inline void launch_dilate(const KParams& kp, int r, int streams, size_t /*smem*/
 template <bool kFused, bool kClear>
 inline cudaError_t dilate_set_smem_k(int bytes) {
   cudaError_t e = cudaSuccess;
-  const void* fns[5] = {reinterpret_cast<const void*>(dilate_tiles_kernel<0, kFused, kClear>),
-                        reinterpret_cast<const void*>(dilate_tiles_kernel<1, kFused, kClear>),
-                        reinterpret_cast<const void*>(dilate_tiles_kernel<2, kFused, kClear>),
-                        reinterpret_cast<const void*>(dilate_tiles_kernel<3, kFused, kClear>),
-                        reinterpret_cast<const void*>(dilate_tiles_kernel<4, kFused, kClear>)};
+  const void* fns[10] = {reinterpret_cast<const void*>(dilate_tiles_kernel<0, kFused, kClear>),
+                         reinterpret_cast<const void*>(dilate_tiles_kernel<1, kFused, kClear>),
+                         reinterpret_cast<const void*>(dilate_tiles_kernel<2, kFused, kClear>),
+                         reinterpret_cast<const void*>(dilate_tiles_kernel<3, kFused, kClear>),
+                         reinterpret_cast<const void*>(dilate_tiles_kernel<4, kFused, kClear>),
+                         reinterpret_cast<const void*>(dilate_tiles_kernel<0, kFused, kClear, kDilTLone>),
+                         reinterpret_cast<const void*>(dilate_tiles_kernel<1, kFused, kClear, kDilTLone>),
+                         reinterpret_cast<const void*>(dilate_tiles_kernel<2, kFused, kClear, kDilTLone>),
+                         reinterpret_cast<const void*>(dilate_tiles_kernel<3, kFused, kClear, kDilTLone>),
+                         reinterpret_cast<const void*>(dilate_tiles_kernel<4, kFused, kClear, kDilTLone>)};
   for (const void* f : fns) {
     const cudaError_t x = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (x != cudaSuccess) e = x;
