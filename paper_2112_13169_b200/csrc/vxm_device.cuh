@@ -148,6 +148,14 @@ struct FrameParams {
   double tnum_neg[3];
 };
 
+// The largest float not above m (exact test of a float depth against a
+// double range: (double)d > m  <=>  d > max_float_at_most(m)).
+inline float max_float_at_most(double m) {
+  float f = static_cast<float>(m);
+  if (static_cast<double>(f) > m) f = std::nextafter(f, -INFINITY);
+  return f;
+}
+
 // Fills FrameParams::cam_cell / tnum_* from f.trans and the walk's voxel
 // size (host side; the kernels read them instead of dividing per ray).
 inline void set_ray_consts(FrameParams& f, double vs) {
@@ -172,6 +180,8 @@ struct KParams {
   // camera
   int W, H;
   double max_depth;
+  float max_depth_f;  // the largest float <= max_depth: for a float depth d,
+                      // (double)d > max_depth exactly when d > max_depth_f
   const double* qx;   // ((u + 0.5) - cx) / fx per column (host glibc tan)
   const double* qy;   // ((v + 0.5) - cy) / fy per row
   // populate

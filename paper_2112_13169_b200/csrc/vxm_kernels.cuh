@@ -174,18 +174,22 @@ __global__ void __launch_bounds__(256) populate_depth_tma_kernel(KParams p, int 
     }
     const float d[4] = {cur.x, cur.y, cur.z, cur.w};
     bool ok[4];
-    unsigned b[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       // DepthImage::valid_depth (geometry.hpp:124): finite and > 0; then the
-      // max-depth cut on the promoted double (geometry.cpp:53-54).
-      ok[k] = q < nq && isfinite(d[k]) && d[k] > 0.0f && !(static_cast<double>(d[k]) > p.max_depth);
-      b[k] = __ballot_sync(0xffffffffu, ok[k]);
+      // max-depth cut on the promoted double (geometry.cpp:53-54). With
+      // max_depth_f the largest float <= max_depth, "d > 0 && d <= max_depth_f"
+      // is the same test (NaN and +inf fail the second compare).
+      ok[k] = q < nq && d[k] > 0.0f && d[k] <= p.max_depth_f;
     }
+    // most 128-pixel groups of a sparse frame hold no valid pixel
+    if (__any_sync(0xffffffffu, ok[0] || ok[1] || ok[2] || ok[3])) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (ok[k]) wl[nlist + __popc(b[k] & lt)] = static_cast<uint16_t>((it * T + threadIdx.x) * 4 + k);
-      nlist += __popc(b[k]);
+      for (int k = 0; k < 4; ++k) {
+        const unsigned b = __ballot_sync(0xffffffffu, ok[k]);
+        if (ok[k]) wl[nlist + __popc(b & lt)] = static_cast<uint16_t>((it * T + threadIdx.x) * 4 + k);
+        nlist += __popc(b);
+      }
     }
   }
   __syncwarp();

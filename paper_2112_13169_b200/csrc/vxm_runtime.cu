@@ -1207,6 +1207,7 @@ int vxm_create_multi(const vxm_config* cfg, int32_t n_streams, int32_t frames_pe
     kp.inv_vs = 1.0 / g.vox_size;
     kp.ray_vs = g.vox_size;
     kp.max_depth = cfg->camera.max_depth;
+    kp.max_depth_f = vxm::max_float_at_most(cfg->camera.max_depth);
     kp.vox_inf = cfg->vox_inf;
     kp.vd = c->bundle[0];
     kp.vw = c->bundle[1];

@@ -506,6 +506,33 @@ def test_pipeline_odd_frame_shapes_and_special_depths(gpu_lib, shape):
     _run_pair(cfg, frames)
 
 
+@pytest.mark.parametrize("max_depth", [5.0, 4.7, 6.3])
+def test_pipeline_compacting_k1_special_depths(gpu_lib, max_depth):
+    """The compacting, TMA-staged K1 (W*H % 4 == 0, sparse frames): its depth
+    test compares floats against the largest float <= max_depth, which must
+    equal the reference's double comparison (geometry.cpp:53-54) also when
+    max_depth is not a float; NaN, +-inf, zero, negative, subnormal depths and
+    the floats either side of max_depth."""
+    W, H = 96, 64
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, W, H, max_depth)
+    grid = vm.GridSpec.create_centered(8.0, 8.0, 3.0, 0.1, (0.0, 0.0, 0.0))
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=1, depth=min(max_depth, 4.5))
+    rng = np.random.default_rng(int(max_depth * 10))
+    m32 = np.float32(max_depth)
+    near = [np.nextafter(m32, np.float32(0)), m32, np.nextafter(m32, np.float32(100)),
+            np.nextafter(np.nextafter(m32, np.float32(100)), np.float32(100))]
+    special = np.array([np.nan, np.inf, -np.inf, -1.0, -0.0, 0.0, 1e-40] + near, dtype=np.float32)
+    frames = []
+    for k in range(6):
+        pose = vm.look_along_x((0.0, 0.11 * k, 0.0))
+        d = scenes.render(cam, pose, scenes.box_field_boxes(1)).copy()
+        d[rng.random(d.shape) < 0.6] = 0.0  # sparse: the host switches to the compacting K1
+        idx = rng.choice(d.size, 600, replace=False)
+        d.flat[idx] = special[rng.integers(0, special.size, idx.size)]
+        frames.append((d, pose))
+    _run_pair(cfg, frames)
+
+
 def test_per_pixel_tracer_branched_batch(gpu_lib):
     """TracerMode::PerPixelBaseline in a batch big enough for graph branches."""
     cam = vm.CameraModel(85 * DEG, 101 * DEG, 80, 60, 6.5)
