@@ -1494,7 +1494,7 @@ __device__ __forceinline__ uint32_t merge4(uint32_t l4, uint32_t o4, uint4 k4, u
 // K4, epoch-format keys (every bundle of up to 131,070 rays): merge4 decodes
 // occupancy bytes and keys; nothing is reset (keys of an older epoch read as
 // Unknown). The clear-format variant follows.
-__global__ void __launch_bounds__(256) merge_epoch_kernel(KParams p, int rows_per_warp) {
+__global__ void __launch_bounds__(256, VXM_MERGE_MINB) merge_epoch_kernel(KParams p, int rows_per_warp) {
   pdl_wait();  // K3's keys and counters
   const int s = blockIdx.y;
   if (blockIdx.x == 0 && threadIdx.x == 0) p.counters[s].t_merge = global_ns();
@@ -1574,17 +1574,19 @@ __global__ void __launch_bounds__(256) merge_epoch_kernel(KParams p, int rows_pe
       free_n += count_free16(out);
     }
   } else
-  if (vec && p.dx <= 128 && rows_per_warp == kRowsPerWarp) {
-    // A row is at most one 4-cell group per lane: issue the loads of all the
-    // warp's rows before resolving any, so each lane keeps kRowsPerWarp x 24 B
-    // in flight (the kernel is HBM-latency bound otherwise).
+  if (vec && p.dx <= 128 && rows_per_warp % kRowsPerWarp == 0) {
+    // A row is at most one 4-cell group per lane: issue the loads of
+    // kRowsPerWarp rows before resolving any, so each lane keeps
+    // kRowsPerWarp x 24 B in flight (the kernel is HBM-latency bound
+    // otherwise); a warp takes rows_per_warp / kRowsPerWarp such groups.
     const int x0 = lane * 4, sx = x0 + ox;
+    for (int g = 0; g < rows_per_warp; g += kRowsPerWarp) {
     uint32_t l4[kRowsPerWarp], o4[kRowsPerWarp], drow[kRowsPerWarp];
     uint4 k4[kRowsPerWarp];
     bool ok[kRowsPerWarp], in_row[kRowsPerWarp];
 #pragma unroll
     for (int rr = 0; rr < kRowsPerWarp; ++rr) {
-      const int row = warp_id * kRowsPerWarp + rr;
+      const int row = warp_id * rows_per_warp + g + rr;
       const int z = row / p.dy;
       const int y = row - z * p.dy;
       const int sy = y + oy, sz = z + oz;
@@ -1607,6 +1609,7 @@ __global__ void __launch_bounds__(256) merge_epoch_kernel(KParams p, int rows_pe
       occ_n += count_occupied4(out);
       free_n += count_free4(out);
       *reinterpret_cast<uint32_t*>(dst + drow[rr] + x0) = out;
+    }
     }
   } else
   for (int rr = 0; rr < rows_per_warp; ++rr) {

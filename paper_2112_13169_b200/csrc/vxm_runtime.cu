@@ -494,7 +494,8 @@ void launch_merge(vxm_ctx* c, const vxm::KParams& kp, int S, cudaStream_t st) {
     // one row per warp unless the batch fills the GPU several times over
     const long long warps = rows * c->nslots;  // the whole call (branches run concurrently)
     const long long fill = static_cast<long long>(c->nsm) * 64;
-    const int rpw = static_cast<int>(std::max(1LL, std::min<long long>(vxm::kRowsPerWarp, warps / fill)));
+    const long long rpw_max = warps / fill >= VXM_MERGE_RPW ? VXM_MERGE_RPW : vxm::kRowsPerWarp;
+    const int rpw = static_cast<int>(std::max(1LL, std::min<long long>(rpw_max, warps / fill)));
     const int rows_per_block = kMergeThreads / 32 * rpw;
     dim3 grid(static_cast<unsigned>((rows + rows_per_block - 1) / rows_per_block), S);
     if (kp.key_fmt == vxm::kClearKeys)

@@ -76,3 +76,18 @@
 // chunks after its first lane ends: K3 115.5 -> 123 us per 64 cfg2 frames
 // (more chunks run with few live lanes, and the mutable step increments
 // spill at 48 registers).
+
+// x-rows per warp of the direct-load K4 grid when the batch fills the GPU
+// many times over (a multiple of kRowsPerWarp = 4); the flat no-x-shift path
+// takes its 16-cell chunks over the same grid, so fewer warps amortise the
+// per-warp set-up and counter reduction (31% of K4's instructions at 4 rows
+// per warp) over more chunks. Measured, 64 cfg2 streams (K4 us / bench
+// frames/s): 4 rows 51 / 331k, 8 rows 51 / 333k, 16 rows 46 / 349k, 32 rows
+// 48 / 335k; a 48-register cap (VXM_MERGE_MINB 5) 44 / 349k.
+#ifndef VXM_MERGE_RPW
+#define VXM_MERGE_RPW 16
+#endif
+// resident blocks per SM the direct-load K4 is compiled for (register cap)
+#ifndef VXM_MERGE_MINB
+#define VXM_MERGE_MINB 1
+#endif

@@ -339,6 +339,28 @@ def test_batched_streams_equal_independent_pipelines(gpu_lib):
             assert np.array_equal(batch.local_grid(s)[0], singles[s].local_grid()[0]), (k, s)
 
 
+def test_large_batch_x_shifts(gpu_lib):
+    """A batch large enough for the merge grid's 16 rows per warp (32
+    streams of a 100x100x50 grid: four 4-row groups per warp in the row-path
+    K4, several 16-cell chunks per thread in the flat K4) with diagonal
+    motion, so frames shift along x (row path) and along y only (flat)."""
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 160, 120, 5.0)
+    grid = vm.GridSpec.create_centered(10.0, 10.0, 5.0, 0.1, (0.0, 0.0, 0.0))
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=2, depth=5.0)
+    S = 32
+    batch = vm.MappingPipeline(cfg, n_streams=S)
+    singles = [oracle_pipeline(cfg) for _ in range(S)]
+    for k in range(4):
+        poses = [vm.look_along_x((0.13 * k * (s % 3), 0.11 * k * (s % 4) - 0.2, 0.0)) for s in range(S)]
+        depth = np.stack([scenes.render(cam, poses[s], scenes.box_field_boxes(1 + s % 3)) for s in range(S)])
+        stats = batch.integrate_depth(depth, poses)
+        for s in range(S):
+            sr = singles[s].integrate_depth(depth[s], poses[s])
+            for key in ("occupied_count", "freed_count", "voxels_freed", "shift_offset", "origin"):
+                assert stats[s][key] == sr[key], (k, s, key)
+            assert np.array_equal(batch.local_grid(s)[0], singles[s].local_grid()[0]), (k, s)
+
+
 def test_pipeline_long_trajectory_wraps_epochs(gpu_lib):
     """cfg4-style moving robot over more frames than the 8-bit epoch holds
     (255), shifting by about one voxel per frame."""
