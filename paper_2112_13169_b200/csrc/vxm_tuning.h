@@ -87,7 +87,9 @@
 #ifndef VXM_MERGE_RPW
 #define VXM_MERGE_RPW 16
 #endif
-// resident blocks per SM the direct-load K4 is compiled for (register cap)
+// resident blocks per SM the direct-load K4 is compiled for (register cap):
+// 4 -> 64 registers; without a cap ptxas took 80 and K4 lost its rows-per-warp
+// gain (52 us, 324k frames/s); 5 -> 48 registers with a small spill (equal)
 #ifndef VXM_MERGE_MINB
-#define VXM_MERGE_MINB 1
+#define VXM_MERGE_MINB 4
 #endif
