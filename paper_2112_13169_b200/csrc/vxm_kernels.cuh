@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(256) populate_depth_kernel(KParams p, int iter
 constexpr int kPopMaxIters = 8;
 
 template <bool kCompact, bool kClear>
-__global__ void __launch_bounds__(256) populate_depth_tma_kernel(KParams p, int iters) {
+__global__ void __launch_bounds__(256, VXM_POP_MINB) populate_depth_tma_kernel(KParams p, int iters) {
   extern __shared__ float4 sq[];  // iters * blockDim.x quads
   __shared__ uint64_t bar[kPopMaxIters];
   const int s = blockIdx.y;

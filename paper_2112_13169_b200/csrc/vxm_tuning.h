@@ -93,3 +93,9 @@
 #ifndef VXM_MERGE_MINB
 #define VXM_MERGE_MINB 4
 #endif
+// resident blocks per SM the TMA-staged K1 is compiled for (register cap):
+// 4 -> 64 registers (uncapped: 77, 3 blocks per SM): +2% frames/s; 5 and 6
+// (48 / 40 registers) spill and slow K1 itself
+#ifndef VXM_POP_MINB
+#define VXM_POP_MINB 4
+#endif
