@@ -529,6 +529,29 @@ __global__ void __launch_bounds__(256) dilate_tiles_kernel(KParams p, int r_rt) 
     by[i] = d;
   }
   __syncthreads();
+  if (!kClear && nw == kT && (p.dx & 3) == 0 && p.dx <= 128) {
+    // one warp per y row of the tile (8 warps, 8x8 tile), walking its z
+    // column with running pointers; a lane owns one 4-cell group of the row
+    const int gy = y0 + warp, x0 = lane * 4;
+    if (gy < p.dy && x0 < p.dx) {
+      const int zs = kT << lg;
+      const uint32_t* col = by + (warp << lg) + (x0 >> 5);
+      uint8_t* dst = occ + static_cast<uint32_t>(gy) * p.dx + static_cast<uint32_t>(z0) * dxy + x0;
+      const int zn = min(kT, p.dz - z0);
+      const uint32_t ee = e * 0x01010101u;
+      for (int z = 0; z < zn; ++z, col += zs, dst += dxy) {
+        uint32_t d = 0;
+#pragma unroll
+        for (int k = 0; k <= 2 * (kR > 0 ? kR : 16); ++k) {
+          if (kR == 0 && k > 2 * r) break;
+          d |= col[k * zs];
+        }
+        const uint32_t nib = (d >> (x0 & 31)) & 0xFu;
+        if (nib) *reinterpret_cast<uint32_t*>(dst) = ee & (((nib * 0x00204081u) & 0x01010101u) * 0xFFu);
+      }
+    }
+    return;
+  }
   for (int row = warp; row < kT * kT; row += nw) {
     const int z = row / kT, y = row & (kT - 1);
     const int gy = y0 + y, gz = z0 + z;

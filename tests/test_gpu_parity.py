@@ -339,6 +339,28 @@ def test_batched_streams_equal_independent_pipelines(gpu_lib):
             assert np.array_equal(batch.local_grid(s)[0], singles[s].local_grid()[0]), (k, s)
 
 
+@pytest.mark.parametrize("vox_inf,extent", [(1, (6.0, 6.0, 3.0)), (3, (6.4, 5.0, 2.8)), (6, (9.6, 4.5, 3.0)),
+                                             (2, (6.2, 5.0, 2.0))])
+def test_batched_dilation_radii(gpu_lib, vox_inf, extent):
+    """The batch dilation (8x8 tiles; one warp per tile row walking its z
+    column when rows fit a warp) for compiled radii 1-4, the run-time radius
+    path (6) and a row length that is not a multiple of 4 (62 cells)."""
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 96, 72, 5.0)
+    grid = vm.GridSpec.create_centered(*extent, 0.1, (0.0, 0.0, 0.0))
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=vox_inf, depth=5.0)
+    S = 4
+    batch = vm.MappingPipeline(cfg, n_streams=S)
+    singles = [oracle_pipeline(cfg) for _ in range(S)]
+    for k in range(3):
+        poses = [vm.look_along_x((0.07 * k * s, 0.1 * k - 0.1 * s, 0.03 * s)) for s in range(S)]
+        depth = np.stack([scenes.render(cam, poses[s], scenes.box_field_boxes(1 + s)) for s in range(S)])
+        stats = batch.integrate_depth(depth, poses)
+        for s in range(S):
+            sr = singles[s].integrate_depth(depth[s], poses[s])
+            assert stats[s]["occupied_count"] == sr["occupied_count"], (k, s)
+            assert np.array_equal(batch.local_grid(s)[0], singles[s].local_grid()[0]), (k, s)
+
+
 def test_large_batch_x_shifts(gpu_lib):
     """A batch large enough for the merge grid's 16 rows per warp (32
     streams of a 100x100x50 grid: four 4-row groups per warp in the row-path
