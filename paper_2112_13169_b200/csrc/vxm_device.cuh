@@ -100,6 +100,7 @@ struct Counters {
   // them into vxm_stats::*_us without event nodes in the frame graph
   unsigned long long t_pop, t_trace, t_merge, t_end;
   unsigned long long trace_slots[32][4];  // K3 partials, folded by K4 (device only)
+  unsigned long long merge_done;          // K4 blocks finished (the last one publishes)
 };
 // The part of Counters the host reads back: K5 copies it into host-mapped
 // memory and clears the slot's Counters for the next frame.
@@ -197,6 +198,7 @@ struct KParams {
   uint8_t* dtmp;       // generic dilation (large radii / rows): 2 * n bytes per slot
   uint32_t* key;
   int key_fmt;         // KeyFmt
+  int k4_publish;      // K4's last block per slot publishes the counters (no K5)
   uint8_t* loc0;
   uint8_t* loc1;
   Counters* counters;

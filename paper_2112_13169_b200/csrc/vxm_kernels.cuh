@@ -1456,17 +1456,39 @@ constexpr int kRowsPerWarp = 4;
 // included, for the next frame (so the frame graph has neither a memset nor
 // a D2H copy node; a last-block check-in inside K4 cost its ~10k blocks more
 // than this launch).
-__global__ void __launch_bounds__(128) publish_counters_kernel(KParams p) {
-  pdl_wait();  // K4 complete
-  const int s = blockIdx.x;
+// K5's work for slot s: the counters into host-mapped memory, then cleared
+// (K3's partials included) for the next frame. Device function: K5 runs it in
+// one block per slot, or the last K4 block of a slot runs it (publish_when_last).
+__device__ __forceinline__ void publish_slot(const KParams& p, int s) {
   constexpr int kHead = sizeof(CountersHead) / sizeof(unsigned long long);
   constexpr int kParts = sizeof(Counters::trace_slots) / sizeof(unsigned long long);
   unsigned long long* c = reinterpret_cast<unsigned long long*>(p.counters + s);
   if (threadIdx.x < kHead) {
-    reinterpret_cast<unsigned long long*>(p.counters_out + s)[threadIdx.x] = c[threadIdx.x];
+    reinterpret_cast<unsigned long long*>(p.counters_out + s)[threadIdx.x] = __ldcg(c + threadIdx.x);
     c[threadIdx.x] = 0ull;
   }
   for (int i = threadIdx.x; i < kParts; i += blockDim.x) (&p.counters[s].trace_slots[0][0])[i] = 0ull;
+  if (threadIdx.x == 0) p.counters[s].merge_done = 0ull;
+}
+
+// End of a K4 block: the slot's last block to finish publishes its counters
+// (threadfence reduction: every block's counter atomics are ordered before its
+// increment of merge_done), so no K5 launch follows K4.
+__device__ __forceinline__ void publish_when_last(const KParams& p, int s) {
+  __shared__ unsigned last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(&p.counters[s].merge_done, 1ull) == gridDim.x - 1 ? 1u : 0u;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  publish_slot(p, s);
+}
+
+__global__ void __launch_bounds__(128) publish_counters_kernel(KParams p) {
+  pdl_wait();  // K4 complete
+  publish_slot(p, blockIdx.x);
 }
 
 // number of bytes of x (states 0..3) equal to 2 / to 1
@@ -1677,6 +1699,7 @@ __global__ void __launch_bounds__(256, VXM_MERGE_MINB) merge_epoch_kernel(KParam
   unsigned long long* dsts[2] = {&p.counters[s].occupied, &p.counters[s].freed};
   block_accumulate<2>(vals, dsts);  // ends after every warp's work (a block barrier)
   if (threadIdx.x == 0) atomicMax(&p.counters[s].t_end, global_ns());
+  if (p.k4_publish) publish_when_last(p, s);
 }
 
 // Clear-format keys of the source cells the shifted gather never reads

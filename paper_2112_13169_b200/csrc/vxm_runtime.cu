@@ -366,7 +366,7 @@ int merge_ranges(const vxm_ctx* c) {
 
 // The four stages for slots [s0, s0 + S) on stream `st` (kernel parameters
 // rebased to the first slot). `marks` records the stage-boundary events.
-void launch_merge(vxm_ctx* c, const vxm::KParams& kp, int S, cudaStream_t st);
+bool launch_merge(vxm_ctx* c, const vxm::KParams& kp, int S, cudaStream_t st);
 
 // K5 over S slots: counters -> host-mapped read-back, cleared for the next frame
 void launch_publish(const vxm::KParams& kp, int S, cudaStream_t st) {
@@ -448,8 +448,7 @@ void launch_stages(vxm_ctx* c, bool cloud, bool capturing, int s0, int S, cudaSt
   }
   mark(c->ev[3]);
   if (merge) {
-    launch_merge(c, kp, S, st);
-    launch_publish(kp, S, st);
+    if (!launch_merge(c, kp, S, st)) launch_publish(kp, S, st);
   }
   mark(c->ev[4]);
 }
@@ -471,7 +470,8 @@ void launch_merge_chain(vxm_ctx* c, const vxm::KParams& kp, int F, int streams, 
   VXM_CK(cudaGetLastError());
 }
 
-void launch_merge(vxm_ctx* c, const vxm::KParams& kp, int S, cudaStream_t st) {
+// Returns true when the K4 launched publishes the counters itself (no K5).
+bool launch_merge(vxm_ctx* c, const vxm::KParams& kp, int S, cudaStream_t st) {
   // Short rows whose cells move as words (dx % 4 == 0, dx <= 128: every
   // benchmark grid) take the direct-load K4 with four rows of loads in flight
   // per lane; it measured faster there than the TMA-staged K4 (57 vs 70 us for
@@ -498,14 +498,20 @@ void launch_merge(vxm_ctx* c, const vxm::KParams& kp, int S, cudaStream_t st) {
     const int rpw = static_cast<int>(std::max(1LL, std::min<long long>(rpw_max, warps / fill)));
     const int rows_per_block = kMergeThreads / 32 * rpw;
     dim3 grid(static_cast<unsigned>((rows + rows_per_block - 1) / rows_per_block), S);
-    if (kp.key_fmt == vxm::kClearKeys)
+    if (kp.key_fmt == vxm::kClearKeys) {
       VXM_CK(vxm::launch_pdl(vxm::merge_shift_count_kernel<true>, grid, dim3(kMergeThreads), 0, st, kp, rpw));
-    else
-      VXM_CK(vxm::launch_pdl(vxm::merge_epoch_kernel, grid, dim3(kMergeThreads), 0, st, kp, rpw));
+    } else {
+      vxm::KParams kq = kp;
+      kq.k4_publish = 1;
+      VXM_CK(vxm::launch_pdl(vxm::merge_epoch_kernel, grid, dim3(kMergeThreads), 0, st, kq, rpw));
+      VXM_CK(cudaGetLastError());
+      return true;
+    }
     VXM_CK(cudaGetLastError());
   } else {
     launch_merge_chain(c, kp, c->F, S / c->F, st);
   }
+  return false;
 }
 
 // One frame of every slot: the stages, optionally as graph branches over
@@ -569,8 +575,7 @@ void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
       VXM_CK(cudaStreamWaitEvent(c->stream, c->join[b], 0));
     }
     if (!by_stream && !chained) {
-      launch_merge(c, c->kp, c->nslots, c->stream);
-      launch_publish(c->kp, c->nslots, c->stream);
+      if (!launch_merge(c, c->kp, c->nslots, c->stream)) launch_publish(c->kp, c->nslots, c->stream);
     }
   } else {
     launch_stages(c, cloud, capturing, 0, c->nslots, c->stream, marks);
