@@ -1459,31 +1459,35 @@ constexpr int kRowsPerWarp = 4;
 // K5's work for slot s: the counters into host-mapped memory, then cleared
 // (K3's partials included) for the next frame. Device function: K5 runs it in
 // one block per slot, or the last K4 block of a slot runs it (publish_when_last).
-__device__ __forceinline__ void publish_slot(const KParams& p, int s) {
+// (threads t0 .. t0 + nt - 1 of the block take part)
+__device__ __forceinline__ void publish_slot(const KParams& p, int s, int t = threadIdx.x, int nt = blockDim.x) {
   constexpr int kHead = sizeof(CountersHead) / sizeof(unsigned long long);
   constexpr int kParts = sizeof(Counters::trace_slots) / sizeof(unsigned long long);
   unsigned long long* c = reinterpret_cast<unsigned long long*>(p.counters + s);
-  if (threadIdx.x < kHead) {
-    reinterpret_cast<unsigned long long*>(p.counters_out + s)[threadIdx.x] = __ldcg(c + threadIdx.x);
-    c[threadIdx.x] = 0ull;
+  if (t < kHead) {
+    reinterpret_cast<unsigned long long*>(p.counters_out + s)[t] = __ldcg(c + t);
+    c[t] = 0ull;
   }
-  for (int i = threadIdx.x; i < kParts; i += blockDim.x) (&p.counters[s].trace_slots[0][0])[i] = 0ull;
-  if (threadIdx.x == 0) p.counters[s].merge_done = 0ull;
+  for (int i = t; i < kParts; i += nt) (&p.counters[s].trace_slots[0][0])[i] = 0ull;
+  if (t == 0) p.counters[s].merge_done = 0ull;
 }
 
 // End of a K4 block: the slot's last block to finish publishes its counters
 // (threadfence reduction: every block's counter atomics are ordered before its
 // increment of merge_done), so no K5 launch follows K4.
+// Only warp 0 takes part (it made the block's counter atomics); the other
+// warps leave without waiting for the fence.
 __device__ __forceinline__ void publish_when_last(const KParams& p, int s) {
-  __shared__ unsigned last;
+  if (threadIdx.x >= 32) return;
+  unsigned last = 0;
   if (threadIdx.x == 0) {
     __threadfence();
     last = atomicAdd(&p.counters[s].merge_done, 1ull) == gridDim.x - 1 ? 1u : 0u;
   }
-  __syncthreads();
+  last = __shfl_sync(0xffffffffu, last, 0);
   if (!last) return;
   __threadfence();
-  publish_slot(p, s);
+  publish_slot(p, s, threadIdx.x, 32);
 }
 
 __global__ void __launch_bounds__(128) publish_counters_kernel(KParams p) {
