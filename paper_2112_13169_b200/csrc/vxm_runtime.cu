@@ -477,7 +477,7 @@ bool launch_merge(vxm_ctx* c, const vxm::KParams& kp, int S, cudaStream_t st) {
   // per lane; it measured faster there than the TMA-staged K4 (57 vs 70 us for
   // 64 cfg2 slots). Longer or odd rows take the TMA-staged K4 (57 vs 72 us for
   // 8 cfg3 slots of 200-cell rows).
-  const bool direct_vec = kp.dx % 4 == 0 && kp.dx <= 128;
+  const bool direct_vec = kp.dx % 4 == 0 && kp.dx <= VXM_MERGE_DIRECT_MAX_DX;
   if (c->F == 1 && !direct_vec && kp.dx <= vxm::kMergeTmaMaxDx && !(c->flags & VXM_FLAG_NO_TMA_MERGE)) {
     // groups of merge_tma_rows rows; each block pipelines several (two stages)
     const int rows = vxm::merge_tma_rows(kp.dx, kp.dy);

@@ -104,3 +104,11 @@
 // plane (no centre bytes, no pack phase in K2) with K5 clearing the plane for
 // the next frame: K2 no faster and the clearing stores in K5 lengthen every
 // branch's chain (355k -> 326k frames/s).
+
+// Longest x-row (cells, dx % 4 == 0) merged by the direct-load K4 (flat
+// chunks for frames without an x shift, per-row loops otherwise); longer or
+// odd rows take the TMA-staged K4. 1024 (round 2): 16 cfg3 streams (200-cell
+// rows) merge in 82 instead of 110 us, 35.5k -> 39.0k frames/s; 128 before.
+#ifndef VXM_MERGE_DIRECT_MAX_DX
+#define VXM_MERGE_DIRECT_MAX_DX 1024
+#endif

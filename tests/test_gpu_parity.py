@@ -8,6 +8,7 @@ import math
 import numpy as np
 import pytest
 
+from paper_2112_13169_b200 import _native as N
 from paper_2112_13169_b200 import voxmap as vm
 from tests import scenes
 from tests.oracle_api import have_ref, oracle_pipeline
@@ -359,6 +360,30 @@ def test_batched_dilation_radii(gpu_lib, vox_inf, extent):
             sr = singles[s].integrate_depth(depth[s], poses[s])
             assert stats[s]["occupied_count"] == sr["occupied_count"], (k, s)
             assert np.array_equal(batch.local_grid(s)[0], singles[s].local_grid()[0]), (k, s)
+
+
+@pytest.mark.parametrize("clear", [False, True], ids=["epoch_keys", "clear_keys"])
+def test_long_rows_direct_merge_x_shifts(gpu_lib, clear):
+    """Rows longer than 128 cells (200, 204) through the direct-load K4: flat
+    chunks for frames that shift only along y, the per-row loop for frames
+    that shift along x; both key formats."""
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 96, 72, 6.0)
+    for extent in ((20.0, 4.0, 2.0), (20.4, 3.0, 1.6)):
+        grid = vm.GridSpec.create_centered(*extent, 0.1, (0.0, 0.0, 0.0))
+        cfg = vm.PipelineConfig(grid, cam, vox_inf=1, depth=6.0)
+        S = 3
+        batch = vm.MappingPipeline(cfg, n_streams=S, flags=N.FLAG_CLEAR_KEYS if clear else 0)
+        singles = [oracle_pipeline(cfg) for _ in range(S)]
+        for k in range(4):
+            poses = [vm.look_along_x((0.23 * k * (s - 1), 0.12 * k, 0.0)) for s in range(S)]
+            depth = np.stack([scenes.render(cam, poses[s], scenes.box_field_boxes(1 + s)) for s in range(S)])
+            stats = batch.integrate_depth(depth, poses)
+            for s in range(S):
+                sr = singles[s].integrate_depth(depth[s], poses[s])
+                for key in ("occupied_count", "freed_count", "shift_offset"):
+                    assert stats[s][key] == sr[key], (extent, k, s, key)
+                assert np.array_equal(batch.local_grid(s)[0], singles[s].local_grid()[0]), (extent, k, s)
+        batch.close()
 
 
 def test_large_batch_x_shifts(gpu_lib):
