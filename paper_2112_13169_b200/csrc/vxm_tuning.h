@@ -112,3 +112,7 @@
 #ifndef VXM_MERGE_DIRECT_MAX_DX
 #define VXM_MERGE_DIRECT_MAX_DX 1024
 #endif
+
+// Also measured and not kept: the occupancy bytes of all slots in the
+// persisting L2 carve-out (access-policy window on every stream): ray cast
+// -2.5%, merge +3%, frames/s unchanged.
