@@ -101,7 +101,19 @@ struct Counters {
   unsigned long long t_pop, t_trace, t_merge, t_end;
   unsigned long long trace_slots[32][4];  // K3 partials, folded by K4 (device only)
   unsigned long long merge_done;          // K4 blocks finished (the last one publishes)
+  // K1: the smallest camera distance lower bound over this frame's points
+  // (float bits, atomicMin; +inf after each publish, 0 = unknown): the ray
+  // cast needs no occupancy reads for steps closer than that (minus the
+  // dilation radius)
+  unsigned int min_dist_bits;
+  unsigned int pad_;
 };
+
+// Per-warp min of a non-negative float, folded into *dst (as ordered bits).
+__device__ __forceinline__ void warp_min_dist(float v, unsigned int* dst) {
+  const unsigned b = __reduce_min_sync(0xffffffffu, __float_as_uint(v));
+  if ((threadIdx.x & 31) == 0 && b != 0x7F800000u) atomicMin(dst, b);
+}
 // The part of Counters the host reads back: K5 copies it into host-mapped
 // memory and clears the slot's Counters for the next frame.
 struct CountersHead {

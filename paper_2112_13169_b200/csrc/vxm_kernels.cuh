@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(256) populate_depth_kernel(KParams p, int iter
   const int npix = p.W * p.H;
 
   unsigned total = 0, outside = 0;
+  float mind = __uint_as_float(0x7F800000u);
   int first = ((blockIdx.x * iters) * blockDim.x + threadIdx.x) * 4;
   float4 next = first < npix ? load_quad(depth, first, npix) : make_float4(0.f, 0.f, 0.f, 0.f);
   for (int it = 0; it < iters && first < npix; ++it) {
@@ -97,11 +98,13 @@ __global__ void __launch_bounds__(256) populate_depth_kernel(KParams p, int iter
       const double D = static_cast<double>(d[k]);
       if (D > p.max_depth) continue;
       ++total;
+      mind = fminf(mind, d[k]);  // |point| >= its depth
       outside += populate_point<kClear>(p, R, t, target, rowflag, keys, mark, dmul(__ldg(p.qx + u), D),
                                 dmul(__ldg(p.qy + v), D), D);
     }
     first = nfirst;
   }
+  warp_min_dist(mind, &p.counters[s].min_dist_bits);
   unsigned vals[2] = {total, outside};
   unsigned long long* dst[2] = {&p.counters[s].points_total, &p.counters[s].points_outside};
   block_accumulate<2>(vals, dst);
@@ -153,6 +156,7 @@ __global__ void __launch_bounds__(256, VXM_POP_MINB) populate_depth_tma_kernel(K
   __syncthreads();  // barriers initialised before anyone waits on them
 
   unsigned total = 0, outside = 0;
+  float mind = __uint_as_float(0x7F800000u);
   if constexpr (kCompact) {
   // Each warp lists the valid pixels of its own quads (ballot positions, no
   // block barrier) and then transforms them 32 at a time, so no lane idles on
@@ -205,6 +209,7 @@ __global__ void __launch_bounds__(256, VXM_POP_MINB) populate_depth_tma_kernel(K
     v += (v + 1) * p.W <= pix ? 1 : 0;
     const int u = pix - v * p.W;
     const double D = static_cast<double>(spx[off]);
+    mind = fminf(mind, spx[off]);
     outside += populate_point<kClear>(p, R, t, target, rowflag, keys, mark, dmul(__ldg(p.qx + u), D),
                               dmul(__ldg(p.qy + v), D), D);
   }
@@ -234,11 +239,13 @@ __global__ void __launch_bounds__(256, VXM_POP_MINB) populate_depth_tma_kernel(K
       const double D = static_cast<double>(d[k]);
       if (D > p.max_depth) continue;
       ++total;
+      mind = fminf(mind, d[k]);
       outside += populate_point<kClear>(p, R, t, target, rowflag, keys, mark, dmul(__ldg(p.qx + u), D),
                                 dmul(__ldg(p.qy + v), D), D);
     }
   }
   }
+  warp_min_dist(mind, &p.counters[s].min_dist_bits);
   unsigned vals[2] = {total, outside};
   unsigned long long* dst[2] = {&p.counters[s].points_total, &p.counters[s].points_outside};
   warp_accumulate<2>(vals, dst);
@@ -264,13 +271,17 @@ __global__ void __launch_bounds__(256) populate_cloud_kernel(KParams p) {
   const long long n = fp->n_points;
   const double *xs = fp->xs, *ys = fp->ys, *zs = fp->zs;
   unsigned total = 0, outside = 0;
+  float mind = __uint_as_float(0x7F800000u);
   for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const double x = xs[i], y = ys[i], z = zs[i];
     if (!(isfinite(x) && isfinite(y) && isfinite(z))) continue;
     ++total;
+    // a lower bound of |point|, rounded down to a float
+    mind = fminf(mind, __double2float_rd(fmax(fabs(x), fmax(fabs(y), fabs(z)))));
     outside += populate_point<kClear>(p, R, t, target, rowflag, keys, mark, x, y, z);
   }
+  warp_min_dist(mind, &p.counters[s].min_dist_bits);
   unsigned vals[2] = {total, outside};
   unsigned long long* dst[2] = {&p.counters[s].points_total, &p.counters[s].points_outside};
   block_accumulate<2>(vals, dst);
@@ -874,6 +885,12 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   // occupancy is read only from here on
   pdl_wait();
   if (blockIdx.x == 0 && threadIdx.x == 0) p.counters[s].t_trace = global_ns();
+  // near field of the frame: every occupied cell lies at least near_dist from
+  // the camera (K1's smallest point distance bound, less the dilation radius
+  // plus one cell per axis, as a Euclidean length); 0 bits (not computed, e.g.
+  // a caller's grid with its own Occupied cells) leave it negative
+  const double near_dist = dsub(static_cast<double>(__uint_as_float(__ldcg(&p.counters[s].min_dist_bits))),
+                                dmul(1.7320508075688774 * (p.vox_inf + 2), p.vs));
 
   const unsigned dx = p.dx, dy = p.dy, dz = p.dz;
   const uint32_t dxy = dx * dy;
@@ -918,6 +935,32 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   // finish resolves the cells. (A software-pipelined walk that put the next
   // chunk's steps between them was measured slower: at 40 registers it
   // spills, at 64 the lower occupancy costs more than the latency it hides.)
+  // the dedup of step j's cell c: the value the resolve compares with
+  // dup_max (match mask, or 0/1 from the neighbour shuffles)
+  auto dedup = [&](uint32_t c, int j) -> uint32_t {
+    uint32_t d;
+    if ((kMatchMask >> j) & 1) {
+      // the whole warp: only the highest lane of each distinct cell writes
+      // (one match)
+      asm("match.any.sync.b32 %0, %1, -1;" : "=r"(d) : "r"(c));
+    } else {
+      // lane+1 and lane+8 (two shuffles; the lone-frame kernel, whose serial
+      // chain favours short latency)
+      asm("{\n\t"
+          ".reg .pred p1, p8, d1, d8;\n\t"
+          ".reg .b32 r1, r8;\n\t"
+          "shfl.sync.down.b32 r1|p1, %1, 1, %2, -1;\n\t"
+          "shfl.sync.down.b32 r8|p8, %1, 8, %2, -1;\n\t"
+          "setp.eq.and.u32 d1, r1, %1, p1;\n\t"
+          "setp.eq.and.u32 d8, r8, %1, p8;\n\t"
+          "or.pred d1, d1, d8;\n\t"
+          "selp.u32 %0, 1, 0, d1;\n\t"
+          "}"
+          : "=r"(d)
+          : "r"(c), "n"(kSplit ? 0x101f : 0x1f));  // kSplit: 16-lane segments (the halves)
+    }
+    return d;
+  };
   // kLive: every cell of the chunk is valid (fast chunks: all lanes live).
   auto prefetch_t = [&](const uint32_t (&cell)[kChunk], uint32_t (&o)[kChunk], uint32_t (&dup)[kChunk],
                         auto tail_tag, auto live_tag) {
@@ -937,28 +980,7 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
     // loads, so its shuffle / match latency overlaps theirs): dup[j] >
     // dup_max when a higher lane makes the same cell in step j
 #pragma unroll
-    for (int j = 0; j < kChunk; ++j) {
-      if ((kMatchMask >> j) & 1) {
-        // the whole warp: only the highest lane of each distinct cell writes
-        // (one match)
-        asm("match.any.sync.b32 %0, %1, -1;" : "=r"(dup[j]) : "r"(cell[j]));
-      } else {
-        // lane+1 and lane+8 (two shuffles; the lone-frame kernel, whose serial
-        // chain favours short latency)
-        asm("{\n\t"
-            ".reg .pred p1, p8, d1, d8;\n\t"
-            ".reg .b32 r1, r8;\n\t"
-            "shfl.sync.down.b32 r1|p1, %1, 1, %2, -1;\n\t"
-            "shfl.sync.down.b32 r8|p8, %1, 8, %2, -1;\n\t"
-            "setp.eq.and.u32 d1, r1, %1, p1;\n\t"
-            "setp.eq.and.u32 d8, r8, %1, p8;\n\t"
-            "or.pred d1, d1, d8;\n\t"
-            "selp.u32 %0, 1, 0, d1;\n\t"
-            "}"
-            : "=r"(dup[j])
-            : "r"(cell[j]), "n"(kSplit ? 0x101f : 0x1f));  // kSplit: 16-lane segments (the halves)
-      }
-    }
+    for (int j = 0; j < kChunk; ++j) dup[j] = dedup(cell[j], j);
   };
   auto finish_t = [&](const uint32_t (&cell)[kChunk], const uint32_t (&o)[kChunk], const uint32_t (&dup)[kChunk],
                       auto tail_tag) {
@@ -1135,55 +1157,84 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
     // lim = -inf once the lane's walk has ended (set after the exact chunk
     // it ends in), so the fast test needs no liveness term
     double lim = dsub(Mmin, dmul(0x1p-40, fabs(Mmin)));
-    for (;;) {
-      // every lane live and no step of the next kChunk able to end its walk
-      // (PTX compares chained with or: left to ptxas, the three compares
-      // become an fmin with NaN handling, six more instructions per chunk)
-      uint32_t fast_ok = 0;
-      if constexpr (kFast)
+    // the fast-chunk test against a limit: some axis of every lane has
+    // fma(kChunk-1, tdelta_a, t_a) below it (PTX compares chained with or:
+    // left to ptxas, the three compares become an fmin with NaN handling)
+    auto fast_test = [&](double lm) -> uint32_t {
+      uint32_t ok = 0;
+      asm("{\n\t"
+          ".reg .pred p;\n\t"
+          ".reg .f64 b;\n\t"
+          "fma.rn.f64 b, %1, %2, %3;\n\t"
+          "setp.lt.f64 p, b, %8;\n\t"
+          "fma.rn.f64 b, %1, %4, %5;\n\t"
+          "setp.lt.or.f64 p, b, %8, p;\n\t"
+          "fma.rn.f64 b, %1, %6, %7;\n\t"
+          "setp.lt.or.f64 p, b, %8, p;\n\t"
+          "selp.u32 %0, 1, 0, p;\n\t"
+          "}"
+          : "=r"(ok)
+          : "d"(kAhead), "d"(e0), "d"(t0), "d"(e1), "d"(t1), "d"(e2), "d"(t2), "d"(lm));
+      return ok;
+    };
+    // kChunk steps without threshold tests: t_a = fma(m_a, e_a, t_a) with
+    // m_a = 1 on the chosen axis, 0 elsewhere (fma(1, e, t) = RN(t + e),
+    // fma(0, e, t) = t), one select of a high word per axis
+    auto fast_steps = [&](uint32_t (&cell)[kChunk]) {
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) {
+        cell[j] = uidx;
         asm("{\n\t"
-            ".reg .pred p;\n\t"
-            ".reg .f64 b;\n\t"
-            "fma.rn.f64 b, %1, %2, %3;\n\t"
-            "setp.lt.f64 p, b, %8;\n\t"
-            "fma.rn.f64 b, %1, %4, %5;\n\t"
-            "setp.lt.or.f64 p, b, %8, p;\n\t"
-            "fma.rn.f64 b, %1, %6, %7;\n\t"
-            "setp.lt.or.f64 p, b, %8, p;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t"
+            ".reg .pred q, px, py, pxy;\n\t"
+            ".reg .f64 m0, m1, m2;\n\t"
+            ".reg .b32 l;\n\t"
+            "setp.le.f64 q, %0, %1;\n\t"
+            "setp.le.and.f64 px, %0, %2, q;\n\t"
+            "setp.le.f64 q, %1, %2;\n\t"
+            "and.pred py, q, !px;\n\t"
+            "or.pred pxy, px, py;\n\t"
+            "selp.f64 m0, 0d3FF0000000000000, 0d0000000000000000, px;\n\t"
+            "selp.f64 m1, 0d3FF0000000000000, 0d0000000000000000, py;\n\t"
+            "selp.f64 m2, 0d0000000000000000, 0d3FF0000000000000, pxy;\n\t"
+            "fma.rn.f64 %0, m0, %4, %0;\n\t"
+            "fma.rn.f64 %1, m1, %5, %1;\n\t"
+            "fma.rn.f64 %2, m2, %6, %2;\n\t"
+            "selp.b32 l, %8, %9, py;\n\t"
+            "selp.b32 l, %7, l, px;\n\t"
+            "add.s32 %3, %3, l;\n\t"
             "}"
-            : "=r"(fast_ok)
-            : "d"(kAhead), "d"(e0), "d"(t0), "d"(e1), "d"(t1), "d"(e2), "d"(t2), "d"(lim));
-      if (kFast && __all_sync(0xffffffffu, fast_ok)) {
+            : "+d"(t0), "+d"(t1), "+d"(t2), "+r"(uidx)
+            : "d"(e0), "d"(e1), "d"(e2), "r"(lin0), "r"(lin1), "r"(lin2));
+      }
+    };
+    if constexpr (kFast) {
+      // Near field: a step whose chosen tmax (the cell's exit) is below
+      // near_dist leaves a cell no occupied cell can be, so while the chunk
+      // bound is below min(lim, near_dist) for every lane the chunk needs no
+      // occupancy loads: every cell is written (untraced state unchanged),
+      // only the dedup and the RED remain.
+      const double lim_near = fmin(lim, near_dist);
+      while (__all_sync(0xffffffffu, fast_test(lim_near))) {
         uint32_t cell[kChunk];
+        fast_steps(cell);
 #pragma unroll
         for (int j = 0; j < kChunk; ++j) {
-          cell[j] = uidx;
-          // the step without threshold tests: t_a = fma(m_a, e_a, t_a) with
-          // m_a = 1 on the chosen axis, 0 elsewhere (fma(1, e, t) = RN(t + e),
-          // fma(0, e, t) = t), one select of a high word per axis
-          asm("{\n\t"
-              ".reg .pred q, px, py, pxy;\n\t"
-              ".reg .f64 m0, m1, m2;\n\t"
-              ".reg .b32 l;\n\t"
-              "setp.le.f64 q, %0, %1;\n\t"
-              "setp.le.and.f64 px, %0, %2, q;\n\t"
-              "setp.le.f64 q, %1, %2;\n\t"
-              "and.pred py, q, !px;\n\t"
-              "or.pred pxy, px, py;\n\t"
-              "selp.f64 m0, 0d3FF0000000000000, 0d0000000000000000, px;\n\t"
-              "selp.f64 m1, 0d3FF0000000000000, 0d0000000000000000, py;\n\t"
-              "selp.f64 m2, 0d0000000000000000, 0d3FF0000000000000, pxy;\n\t"
-              "fma.rn.f64 %0, m0, %4, %0;\n\t"
-              "fma.rn.f64 %1, m1, %5, %1;\n\t"
-              "fma.rn.f64 %2, m2, %6, %2;\n\t"
-              "selp.b32 l, %8, %9, py;\n\t"
-              "selp.b32 l, %7, l, px;\n\t"
-              "add.s32 %3, %3, l;\n\t"
-              "}"
-              : "+d"(t0), "+d"(t1), "+d"(t2), "+r"(uidx)
-              : "d"(e0), "d"(e1), "d"(e2), "r"(lin0), "r"(lin1), "r"(lin2));
+          const uint32_t dup = dedup(cell[j], j);
+          asm volatile("{\n\t.reg .pred ok;\n\t.reg .b64 a;\n\t"
+                       "setp.le.u32 ok, %1, %2;\n\t"
+                       "mul.wide.u32 a, %0, 4;\n\t"
+                       "add.u64 a, a, %3;\n\t"
+                       "@ok red.relaxed.gpu.global.max.u32 [a], %4;\n\t}"
+                       :: "r"(cell[j]), "r"(dup), "r"(((kMatchMask >> j) & 1) ? dup_max : 0u), "l"(key_base), "r"(kv)
+                       : "memory");
         }
+        lw += kChunk;
+      }
+    }
+    for (;;) {
+      if (kFast && __all_sync(0xffffffffu, fast_test(lim))) {
+        uint32_t cell[kChunk];
+        fast_steps(cell);
         resolve_live(cell);
         continue;
       }
@@ -1469,7 +1520,10 @@ __device__ __forceinline__ void publish_slot(const KParams& p, int s, int t = th
     c[t] = 0ull;
   }
   for (int i = t; i < kParts; i += nt) (&p.counters[s].trace_slots[0][0])[i] = 0ull;
-  if (t == 0) p.counters[s].merge_done = 0ull;
+  if (t == 0) {
+    p.counters[s].merge_done = 0ull;
+    p.counters[s].min_dist_bits = 0x7F800000u;
+  }
 }
 
 // End of a K4 block: the slot's last block to finish publishes its counters
