@@ -43,6 +43,16 @@ dbatch = vm.MappingPipeline(cfg, n_streams=S)
 for k in range(4):
     dbatch.integrate_depth(depth, poses)
 movers.append(dbatch)
+# round 2: a batch large enough for the 16-rows-per-warp K4 with its
+# last-block counter publish (32 streams of a 100x100x50 grid), near-field
+# ray-cast chunks (surfaces beyond the near field), y and x shifts
+gbig = vm.GridSpec.create_centered(10.0, 10.0, 5.0, 0.1, (0.0, 0.0, 0.0))
+cam2 = vm.CameraModel(85 * DEG, 101 * DEG, 96, 72, 5.0)
+big = vm.MappingPipeline(vm.PipelineConfig(gbig, cam2, vox_inf=2, depth=5.0), n_streams=32)
+for k in range(3):
+    ps = [vm.look_along_x((0.13 * k * (s % 2), 0.11 * k, 0.0)) for s in range(32)]
+    big.integrate_depth(vm.render_depth(cam2, ps, boxes), ps)
+movers.append(big)
 print("sanitize case done", sb[0]["freed_count"])
 for p in [batch, one, seq] + movers:
     p.close()
