@@ -2376,7 +2376,7 @@ __device__ __forceinline__ void add_frame_counts(const uint32_t (&packed)[U / 2]
   }
 }
 
-__global__ void __launch_bounds__(256) merge_sequence_epoch_kernel(KParams p, int F) {
+__global__ void __launch_bounds__(256, VXM_SEQ_MINB) merge_sequence_epoch_kernel(KParams p, int F) {
   pdl_wait();  // K3's keys and counters
   constexpr int U = 4;  // frames whose loads are issued together
   __shared__ unsigned cnt[2 * kMaxFramesPerCall];           // occupied, then freed, per frame
