@@ -457,9 +457,11 @@ def our_arm(args, world, rank, local):
     branches = pipe.graph_branches
     d = W.dims(vm, c)
     # K1 populate, K2 dilation when vox_inf > 0 (one fused tile kernel when dims_x % 4 == 0, else K2a rows +
-    # K2b tiles), K3 trace, K4 merge, K5 publish, per branch
+    # K2b tiles), K3 trace, K4 merge, per branch; K5 (counter publish) only when K4 is not the direct-load
+    # epoch-key merge (rows of more than 1024 cells or not a multiple of 4), which publishes from its last block
     k2 = 0 if c["vox_inf"] == 0 else (1 if d[0] % 4 == 0 else 2)
-    kernels_per_step = (4 + k2) * branches
+    k5 = 0 if (d[0] % 4 == 0 and d[0] <= 1024) else 1
+    kernels_per_step = (3 + k2 + k5) * branches
     dev_grids, dev_origins = final_state(vm, pipe, S)
     pipe.close()
 
