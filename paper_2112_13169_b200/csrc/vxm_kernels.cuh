@@ -1511,19 +1511,24 @@ constexpr int kRowsPerWarp = 4;
 // (K3's partials included) for the next frame. Device function: K5 runs it in
 // one block per slot, or the last K4 block of a slot runs it (publish_when_last).
 // (threads t0 .. t0 + nt - 1 of the block take part)
-__device__ __forceinline__ void publish_slot(const KParams& p, int s, int t = threadIdx.x, int nt = blockDim.x) {
+// clears slot s's counters for the next frame (threads t of nt)
+__device__ __forceinline__ void publish_slot_clear(const KParams& p, int s, int t, int nt) {
   constexpr int kHead = sizeof(CountersHead) / sizeof(unsigned long long);
   constexpr int kParts = sizeof(Counters::trace_slots) / sizeof(unsigned long long);
   unsigned long long* c = reinterpret_cast<unsigned long long*>(p.counters + s);
-  if (t < kHead) {
-    reinterpret_cast<unsigned long long*>(p.counters_out + s)[t] = __ldcg(c + t);
-    c[t] = 0ull;
-  }
+  if (t < kHead) c[t] = 0ull;
   for (int i = t; i < kParts; i += nt) (&p.counters[s].trace_slots[0][0])[i] = 0ull;
   if (t == 0) {
     p.counters[s].merge_done = 0ull;
     p.counters[s].min_dist_bits = 0x7F800000u;
   }
+}
+__device__ __forceinline__ void publish_slot(const KParams& p, int s, int t = threadIdx.x, int nt = blockDim.x) {
+  constexpr int kHead = sizeof(CountersHead) / sizeof(unsigned long long);
+  unsigned long long* c = reinterpret_cast<unsigned long long*>(p.counters + s);
+  if (t < kHead) reinterpret_cast<unsigned long long*>(p.counters_out + s)[t] = __ldcg(c + t);
+  __syncwarp();  // (t < 32 here: the copies precede the clearing)
+  publish_slot_clear(p, s, t, nt);
 }
 
 // End of a K4 block: the slot's last block to finish publishes its counters
@@ -1542,6 +1547,67 @@ __device__ __forceinline__ void publish_when_last(const KParams& p, int s) {
   if (!last) return;
   __threadfence();
   publish_slot(p, s, threadIdx.x, 32);
+}
+
+// The packed publish of K4 (grids below 2^24 cells, fewer than 2^16 blocks per
+// slot): each block adds (1 << 48 | freed << 24 | occupied) to merge_done; the
+// block that brings the count to gridDim.x holds the totals in the returned
+// value, folds K3's partials (written by the previous kernel, so visible) and
+// publishes. Only block 0 fences (so that its t_merge stamp is visible first).
+__device__ __forceinline__ void publish_packed(const KParams& p, int s, unsigned occ_n, unsigned free_n) {
+  __shared__ unsigned long long part[2][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  const unsigned o = __reduce_add_sync(0xffffffffu, occ_n), f = __reduce_add_sync(0xffffffffu, free_n);
+  if (lane == 0) {
+    part[0][warp] = o;
+    part[1][warp] = f;
+  }
+  __syncthreads();
+  if (warp != 0) return;
+  unsigned long long bo = lane < nw ? part[0][lane] : 0ull, bf = lane < nw ? part[1][lane] : 0ull;
+#pragma unroll
+  for (int k = 16; k > 0; k >>= 1) {
+    bo += __shfl_down_sync(0xffffffffu, bo, k);
+    bf += __shfl_down_sync(0xffffffffu, bf, k);
+  }
+  unsigned long long tot = 0;
+  unsigned last = 0;
+  if (lane == 0) {
+    if (blockIdx.x == 0) __threadfence();
+    const unsigned long long add = (1ull << 48) | (bf << 24) | bo;
+    tot = atomicAdd(&p.counters[s].merge_done, add) + add;
+    last = (tot >> 48) == gridDim.x ? 1u : 0u;
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return;
+  tot = __shfl_sync(0xffffffffu, tot, 0);
+  __threadfence();  // (acquire side: block 0's t_merge)
+  Counters& c = p.counters[s];
+  unsigned long long v[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    v[i] = __ldcg(&c.trace_slots[lane][i]);
+#pragma unroll
+    for (int k = 16; k > 0; k >>= 1) v[i] += __shfl_down_sync(0xffffffffu, v[i], k);
+  }
+  if (lane == 0) {
+    CountersHead h;
+    h.points_total = __ldcg(&c.points_total);
+    h.points_outside = __ldcg(&c.points_outside);
+    h.rays_traced = v[0];
+    h.voxels_freed = v[1];
+    h.voxels_traced = v[2];
+    h.voxels_skipped = v[3];
+    h.occupied = tot & 0xFFFFFFull;
+    h.freed = (tot >> 24) & 0xFFFFFFull;
+    h.t_pop = __ldcg(&c.t_pop);
+    h.t_trace = __ldcg(&c.t_trace);
+    h.t_merge = __ldcg(&c.t_merge);
+    h.t_end = global_ns();
+    p.counters_out[s] = h;
+  }
+  __syncwarp();
+  publish_slot_clear(p, s, lane, 32);
 }
 
 __global__ void __launch_bounds__(128) publish_counters_kernel(KParams p) {
@@ -1615,7 +1681,12 @@ __global__ void __launch_bounds__(256, VXM_MERGE_MINB) merge_epoch_kernel(KParam
   const int rows = p.dy * p.dz;
   const uint32_t dxy = static_cast<uint32_t>(p.dx) * p.dy;
 
-  if (blockIdx.x == 0 && threadIdx.x < 32) fold_trace_slots(p.counters[s]);
+  // packed publish (k4_publish, grids of fewer than 2^24 cells): the block counts
+  // travel in one 64-bit atomic with the block count and the last block folds
+  // K3's partials itself, so no block waits on a fence except block 0 (its
+  // t_merge stamp)
+  const bool packed = p.k4_publish && p.n < (1LL << 24) && gridDim.x < 65536u;
+  if (!packed && blockIdx.x == 0 && threadIdx.x < 32) fold_trace_slots(p.counters[s]);
 
   unsigned occ_n = 0, free_n = 0;
   const bool vec = (p.dx & 3) == 0 && (ox & 3) == 0;
@@ -1752,6 +1823,10 @@ __global__ void __launch_bounds__(256, VXM_MERGE_MINB) merge_epoch_kernel(KParam
         }
       }
     }
+  }
+  if (packed) {
+    publish_packed(p, s, occ_n, free_n);
+    return;
   }
   unsigned vals[2] = {occ_n, free_n};
   unsigned long long* dsts[2] = {&p.counters[s].occupied, &p.counters[s].freed};
