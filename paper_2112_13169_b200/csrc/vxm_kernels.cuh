@@ -886,11 +886,15 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   pdl_wait();
   if (blockIdx.x == 0 && threadIdx.x == 0) p.counters[s].t_trace = global_ns();
   // near field of the frame: every occupied cell lies at least near_dist from
-  // the camera (K1's smallest point distance bound, less the dilation radius
-  // plus one cell per axis, as a Euclidean length); 0 bits (not computed, e.g.
-  // a caller's grid with its own Occupied cells) leave it negative
-  const double near_dist = dsub(static_cast<double>(__uint_as_float(__ldcg(&p.counters[s].min_dist_bits))),
-                                dmul(1.7320508075688774 * (p.vox_inf + 2), p.vs));
+  // the camera. A point P of the frame has |P| >= d (its depth; K1's bound),
+  // its grid-frame image is within (1 +- 2e-6)|P| of the camera (R^T R is
+  // within 1e-6 of I, pose_valid), and every cell of its dilated cube lies
+  // within sqrt(3) (vox_inf + 1) vs of it; 1e-5 relative and 1e-6 m absolute
+  // cover the rounding. 0 bits (not computed, e.g. a caller's grid with its
+  // own Occupied cells) leave it negative.
+  const double near_dist =
+      dsub(dmul(static_cast<double>(__uint_as_float(__ldcg(&p.counters[s].min_dist_bits))), 1.0 - 1e-5),
+           dadd(dmul(1.7320508075688774 * (p.vox_inf + 1) * (1.0 + 1e-9), p.vs), 1e-6));
 
   const unsigned dx = p.dx, dy = p.dy, dz = p.dz;
   const uint32_t dxy = dx * dy;
