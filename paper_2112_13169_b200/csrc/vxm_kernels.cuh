@@ -848,7 +848,7 @@ __device__ __forceinline__ void ray_setup(const double* R, const FrameParams* fp
 // few spilled values; 4-7% faster than one warp per block at 64 registers),
 // a lone frame (358 warps, GPU far from full) runs 8-step chunks at 64
 // registers, where per-warp latency decides.
-template <int kChunk, int kTraceWarps, int kMinBlocks, int kMatchMask, bool kFast, bool kSplit>
+template <int kChunk, int kTraceWarps, int kMinBlocks, int kMatchMask, bool kFast, bool kSplit, int kNearMask = kMatchMask>
 __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_kernel(KParams p) {
   const int s = blockIdx.y;
   const FrameParams* fp = p.frames + s;
@@ -926,7 +926,7 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   // index) shares it exactly when dup <= lanemask_le (one compare instead of
   // an AND and a compare); the shuffle form gives dup in {0, 1}, bound 0.
   uint32_t dup_max = 0u;
-  if constexpr (kMatchMask != 0) asm("mov.u32 %0, %%lanemask_le;" : "=r"(dup_max));
+  if constexpr ((kMatchMask | kNearMask) != 0) asm("mov.u32 %0, %%lanemask_le;" : "=r"(dup_max));
 
   // A write is dropped when a higher lane (higher ray index) makes the same
   // cell in the same step (measured: dropping the dedup after the first
@@ -941,9 +941,9 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   // spills, at 64 the lower occupancy costs more than the latency it hides.)
   // the dedup of step j's cell c: the value the resolve compares with
   // dup_max (match mask, or 0/1 from the neighbour shuffles)
-  auto dedup = [&](uint32_t c, int j) -> uint32_t {
+  auto dedup = [&](uint32_t c, int j, int mask = kMatchMask) -> uint32_t {
     uint32_t d;
-    if ((kMatchMask >> j) & 1) {
+    if ((mask >> j) & 1) {
       // the whole warp: only the highest lane of each distinct cell writes
       // (one match)
       asm("match.any.sync.b32 %0, %1, -1;" : "=r"(d) : "r"(c));
@@ -1223,13 +1223,13 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
         fast_steps(cell);
 #pragma unroll
         for (int j = 0; j < kChunk; ++j) {
-          const uint32_t dup = dedup(cell[j], j);
+          const uint32_t dup = dedup(cell[j], j, kNearMask);
           asm volatile("{\n\t.reg .pred ok;\n\t.reg .b64 a;\n\t"
                        "setp.le.u32 ok, %1, %2;\n\t"
                        "mul.wide.u32 a, %0, 4;\n\t"
                        "add.u64 a, a, %3;\n\t"
                        "@ok red.relaxed.gpu.global.max.u32 [a], %4;\n\t}"
-                       :: "r"(cell[j]), "r"(dup), "r"(((kMatchMask >> j) & 1) ? dup_max : 0u), "l"(key_base), "r"(kv)
+                       :: "r"(cell[j]), "r"(dup), "r"(((kNearMask >> j) & 1) ? dup_max : 0u), "l"(key_base), "r"(kv)
                        : "memory");
         }
         lw += kChunk;
@@ -1339,10 +1339,10 @@ inline void launch_trace(const KParams& kp, int slots, int batch, cudaStream_t s
     // (shuffles between) for small ones (VXM_TB_MATCH_* in vxm_tuning.h)
     const dim3 grid((tiles + VXM_TB_WARPS - 1) / VXM_TB_WARPS, slots), block(32 * VXM_TB_WARPS);
     if (static_cast<long long>(kp.vw) * kp.vh >= VXM_TB_MATCH_RAYS)
-      launch_pdl(trace_bundle_kernel<VXM_TB_CHUNK, VXM_TB_WARPS, VXM_TB_MINB, VXM_TB_MATCH_LARGE, VXM_TB_FAST, false>,
+      launch_pdl(trace_bundle_kernel<VXM_TB_CHUNK, VXM_TB_WARPS, VXM_TB_MINB, VXM_TB_MATCH_LARGE, VXM_TB_FAST, false, VXM_TB_NEAR_MATCH_LARGE>,
                  grid, block, 0, st, kp);
     else
-      launch_pdl(trace_bundle_kernel<VXM_TB_CHUNK, VXM_TB_WARPS, VXM_TB_MINB, VXM_TB_MATCH_SMALL, VXM_TB_FAST, false>,
+      launch_pdl(trace_bundle_kernel<VXM_TB_CHUNK, VXM_TB_WARPS, VXM_TB_MINB, VXM_TB_MATCH_SMALL, VXM_TB_FAST, false, VXM_TB_NEAR_MATCH_SMALL>,
                  grid, block, 0, st, kp);
   } else {
     if (static_cast<long long>(kp.vw) * kp.vh * batch <= kSplitMaxRays) {
