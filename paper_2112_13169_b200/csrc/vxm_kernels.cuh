@@ -763,24 +763,26 @@ inline cudaError_t dilate_set_smem(int bytes) {
 // (proj/src/raytracer.cpp:35-61) + walk_ray (proj/include/voxmap/raytracer.hpp:
 // 76-118) + traverse_ray (raytracer.cpp:63-96). One thread per ray; a warp
 // owns an 8x4 tile of end-plane targets so that its rays stay spatially
-// coherent, and a block is one warp so no warp waits on another.
+// coherent (lanes past the bundle's edge walk a clone of the edge ray).
 //
 // The walk runs in chunks of kChunk DDA steps: (A) the chunk's cell indices
 // are computed (they do not depend on grid contents), (B) their occupancy
 // bytes are loaded together through the read-only path, (C) the chunk is
-// resolved in order with predicated, branch-free PTX. Inside the grid each
-// step only compares the chosen axis' tmax with a per-axis threshold
-// min(stop, E_a), E_a being the exact tmax at which the walk would leave the
-// grid along a (summed once per ray with the walk's own additions), so there
-// are no per-step bounds tests or step counters. ncu (profiles/) showed the
-// kernel issue- and ALU-pipe bound, so the step and the resolve are written to
-// minimise instructions per visit. The Sequential last-writer rule is a
+// resolved in order with predicated PTX. Inside the grid each step only
+// compares the chosen axis' tmax with a per-axis threshold min(stop, E_a),
+// E_a the tmax at which the walk would leave the grid along a (decided by a
+// value half a step below it), so there are no per-step bounds tests or step
+// counters; chunks that provably cannot end any lane's walk skip even that
+// (fast chunks), and chunks closer to the camera than any Occupied cell of
+// the frame skip the occupancy loads (near field). ncu (profiles/) shows the
+// kernel issue-bound, so the step and the resolve are written to minimise
+// instructions per visit. The Sequential last-writer rule is a
 // fire-and-forget RED.max on the cell key; before issuing it a lane drops its
 // write when a higher lane (a higher ray index) writes the same cell in the
 // same step, which removes most same-address traffic near the camera: over
-// the whole warp with one match.any in the batch kernel, against lane+1 and
-// lane+8 with two shuffles in the lone-frame kernel (shorter latency).
-// Counters go to 32 per-stream slots (one RED per warp each), summed by K4.
+// the whole warp with match.any, or against lane+1 and lane+8 with two
+// shuffles (per step of a chunk, kMatchMask / kNearMask). Counters go to 32
+// per-stream slots (one RED per warp each), summed by K4.
 // ---------------------------------------------------------------------------
 
 constexpr int kTraceSlots = 32;
@@ -844,10 +846,10 @@ __device__ __forceinline__ void ray_setup(const double* R, const FrameParams* fp
 
 
 // Two shapes (measured, tools/ab_time.sh): batches of frames run kChunk = 4
-// steps per chunk in 2-warp blocks held to 40 registers (48 warps per SM, a
-// few spilled values; 4-7% faster than one warp per block at 64 registers),
-// a lone frame (358 warps, GPU far from full) runs 8-step chunks at 64
-// registers, where per-warp latency decides.
+// steps per chunk in 2-warp blocks held to 48 registers (40 warps per SM;
+// vxm_tuning.h), a lone frame (358 warps, GPU far from full) runs 8-step
+// chunks in one-warp blocks at 64-80 registers, where per-warp latency
+// decides, with each ray walked as two halves (kSplit) when it has few rays.
 template <int kChunk, int kTraceWarps, int kMinBlocks, int kMatchMask, bool kFast, bool kSplit, int kNearMask = kMatchMask>
 __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_kernel(KParams p) {
   const int s = blockIdx.y;
