@@ -214,7 +214,13 @@ __global__ void __launch_bounds__(256, VXM_POP_MINB) populate_depth_tma_kernel(K
                               dmul(__ldg(p.qy + v), D), D);
   }
   } else {
-  for (int it = 0; it < iters; ++it) {
+  // the thread's first pixel (u0, v0) advances by 4T pixels per tile: one
+  // division for the first tile, then a carry
+  int v0 = (q0 * 4 + threadIdx.x * 4) / p.W;
+  int u0 = q0 * 4 + threadIdx.x * 4 - v0 * p.W;
+  const int du = (4 * T) % p.W, dv = (4 * T) / p.W;
+  for (int it = 0; it < iters; ++it, u0 += du, v0 += dv) {
+    if (u0 >= p.W) { u0 -= p.W; ++v0; }
     const int q = q0 + it * T + threadIdx.x;
     if (q0 + it * T >= nq) break;
     float4 cur;
@@ -226,18 +232,15 @@ __global__ void __launch_bounds__(256, VXM_POP_MINB) populate_depth_tma_kernel(K
     }
     if (q >= nq) continue;
     const float d[4] = {cur.x, cur.y, cur.z, cur.w};
-    const int first = q * 4;
-    const int v0 = first / p.W;
-    const int u0 = first - v0 * p.W;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       int u = u0 + k, v = v0;
       if (u >= p.W) { u -= p.W; ++v; }  // a row boundary inside the quad
       // DepthImage::valid_depth (geometry.hpp:124): finite and > 0; then the
-      // max-depth cut on the promoted double (geometry.cpp:53-54).
-      if (!(isfinite(d[k]) && d[k] > 0.0f)) continue;
+      // max-depth cut on the promoted double (geometry.cpp:53-54), as two
+      // float compares against the largest float <= max_depth
+      if (!(d[k] > 0.0f && d[k] <= p.max_depth_f)) continue;
       const double D = static_cast<double>(d[k]);
-      if (D > p.max_depth) continue;
       ++total;
       mind = fminf(mind, d[k]);
       outside += populate_point<kClear>(p, R, t, target, rowflag, keys, mark, dmul(__ldg(p.qx + u), D),
