@@ -2439,30 +2439,40 @@ __global__ void __launch_bounds__(256) merge_shift_count_tma_kernel(KParams p) {
 constexpr int kMaxFramesPerCall = 64;
 
 // Warp sums of per-frame Occupied / Free counts packed as bytes (frame k0+u:
-// byte pair u&1 of word u>>1; every warp sum is <= 128), added by lane 0 into
-// the block's per-frame counters (32-bit shared atomics: [k] occupied,
-// [kMaxFramesPerCall + k] freed).
+// byte pair u&1 of word u>>1; every warp sum is <= 128), accumulated by the
+// lane of each frame and added into the block's per-frame counters (32-bit
+// shared atomics: [k] occupied, [kMaxFramesPerCall + k] freed) at the end.
 template <int U>
-__device__ __forceinline__ void add_frame_counts(const uint32_t (&packed)[U / 2], unsigned* cnt, int k0, int F,
-                                                 int lane) {
+__device__ __forceinline__ void add_frame_counts(const uint32_t (&packed)[U / 2], uint32_t (&acc)[4], int k0, int lane) {
+  // Each warp sum lands in the lane of its frame (lane k & 31, frames k and
+  // k + 1 of a pair share a half of the 64), flushed once per thread by
+  // flush_frame_counts instead of shared atomics every group.
 #pragma unroll
   for (int h = 0; h < U / 2; ++h) {
     const uint32_t sum = __reduce_add_sync(0xffffffffu, packed[h]);
-    if (lane == 0 && sum) {
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int k = k0 + 2 * h + q;
-        const uint32_t half = (sum >> (16 * q)) & 0xffffu;
-        if (k < F && (half & 0xffu)) atomicAdd(&cnt[k], half & 0xffu);
-        if (k < F && (half >> 8)) atomicAdd(&cnt[kMaxFramesPerCall + k], half >> 8);
-      }
+    const int fk = k0 + 2 * h;  // even: fk and fk + 1 in the same half
+    const uint32_t mine = lane == (fk & 31) ? sum : (lane == ((fk + 1) & 31) ? sum >> 16 : 0u);
+    if (fk < 32) {
+      acc[0] += mine & 0xffu;
+      acc[1] += (mine >> 8) & 0xffu;
+    } else {
+      acc[2] += mine & 0xffu;
+      acc[3] += (mine >> 8) & 0xffu;
     }
   }
 }
 
+// the lane accumulators of add_frame_counts into the block's shared counts
+__device__ __forceinline__ void flush_frame_counts(const uint32_t (&acc)[4], unsigned* cnt, int lane) {
+  if (acc[0]) atomicAdd(&cnt[lane], acc[0]);
+  if (acc[1]) atomicAdd(&cnt[kMaxFramesPerCall + lane], acc[1]);
+  if (acc[2]) atomicAdd(&cnt[32 + lane], acc[2]);
+  if (acc[3]) atomicAdd(&cnt[kMaxFramesPerCall + 32 + lane], acc[3]);
+}
+
 __global__ void __launch_bounds__(256, VXM_SEQ_MINB) merge_sequence_epoch_kernel(KParams p, int F) {
   pdl_wait();  // K3's keys and counters
-  constexpr int U = 4;  // frames whose loads are issued together
+  constexpr int U = VXM_SEQ_U;  // frames whose loads are issued together
   __shared__ unsigned cnt[2 * kMaxFramesPerCall];           // occupied, then freed, per frame
   __shared__ int Pc[kMaxFramesPerCall + U][3];              // P_{k-1} at index k
   __shared__ uint32_t ep[kMaxFramesPerCall];
@@ -2504,6 +2514,7 @@ __global__ void __launch_bounds__(256, VXM_SEQ_MINB) merge_sequence_epoch_kernel
   const uint8_t* occ0 = p.occ + static_cast<long long>(s) * F * p.n;
   const uint32_t* key0 = p.key + static_cast<long long>(s) * F * p.n;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  uint32_t acc[4] = {0u, 0u, 0u, 0u};  // per-frame Occupied / Free counts, see add_frame_counts
   if (vec_ok) {
     // Every frame's x shift is a multiple of 4 (and dims_x too): a thread
     // folds 4 neighbouring chains at once, moving the 4 cells as one word
@@ -2528,6 +2539,8 @@ __global__ void __launch_bounds__(256, VXM_SEQ_MINB) merge_sequence_epoch_kernel
       bool in_prev;
       uint32_t pos_prev = group_of(0, in_prev);
       uint32_t val = in_prev ? *reinterpret_cast<const uint32_t*>(src + pos_prev) : 0u;
+      auto og = occ0;  // slabs of frame k0 (advanced one frame per load pair)
+      auto kg = key0;
       for (int k0 = 0; k0 < F; k0 += U) {
         bool in_c[U];
         uint32_t pos[U];
@@ -2540,9 +2553,12 @@ __global__ void __launch_bounds__(256, VXM_SEQ_MINB) merge_sequence_epoch_kernel
           const bool in_r = u == 0 ? in_prev : in_c[u - 1];
           const uint32_t r = u == 0 ? pos_prev : pos[u - 1];
           const bool ld = k0 + u < F && in_c[u] && in_r;
-          const long long off = static_cast<long long>(k0 + u) * p.n + r;
-          o[u] = ld ? __ldcs(reinterpret_cast<const uint32_t*>(occ0 + off)) : 0u;
-          kk[u] = ld ? __ldcs(reinterpret_cast<const uint4*>(key0 + off)) : make_uint4(0u, 0u, 0u, 0u);
+          const auto oa = og + r;
+          const auto ka = kg + r;
+          og += p.n;
+          kg += p.n;
+          o[u] = ld ? __ldcs(reinterpret_cast<const uint32_t*>(oa)) : 0u;
+          kk[u] = ld ? __ldcs(reinterpret_cast<const uint4*>(ka)) : make_uint4(0u, 0u, 0u, 0u);
         }
         // per frame: Occupied / Free counts of this thread's 4 cells (each
         // <= 4, so a warp sum fits a byte); two frames share one reduction
@@ -2556,7 +2572,7 @@ __global__ void __launch_bounds__(256, VXM_SEQ_MINB) merge_sequence_epoch_kernel
           const unsigned oc = in_c[u] ? count_occupied4(val) : 0u, fr = in_c[u] ? count_free4(val) : 0u;
           packed[u >> 1] |= (oc | (fr << 8)) << (16 * (u & 1));
         }
-        add_frame_counts<U>(packed, cnt, k0, F, lane);
+        add_frame_counts<U>(packed, acc, k0, lane);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           if (k0 + u < F) {
@@ -2585,6 +2601,8 @@ __global__ void __launch_bounds__(256, VXM_SEQ_MINB) merge_sequence_epoch_kernel
     bool in_prev;
     uint32_t pos_prev = cell_of(0, in_prev);
     uint32_t val = in_prev ? src[pos_prev] : 0u;
+    auto og = occ0;  // slabs of frame k0 (advanced one frame per load pair)
+    auto kg = key0;
     for (int k0 = 0; k0 < F; k0 += U) {
       // positions after frames k0..k0+U-1, then all their loads, then the merges
       bool in_c[U];
@@ -2597,9 +2615,12 @@ __global__ void __launch_bounds__(256, VXM_SEQ_MINB) merge_sequence_epoch_kernel
         const bool in_r = u == 0 ? in_prev : in_c[u - 1];
         const uint32_t r = u == 0 ? pos_prev : pos[u - 1];
         const bool ld = k0 + u < F && in_c[u] && in_r;
-        const long long off = static_cast<long long>(k0 + u) * p.n + r;
-        o[u] = ld ? __ldcs(occ0 + off) : 0u;
-        kk[u] = ld ? __ldcs(key0 + off) : 0u;
+        const auto oa = og + r;
+        const auto ka = kg + r;
+        og += p.n;
+        kg += p.n;
+        o[u] = ld ? __ldcs(oa) : 0u;
+        kk[u] = ld ? __ldcs(ka) : 0u;
       }
       uint32_t packed[U / 2] = {};
 #pragma unroll
@@ -2611,7 +2632,7 @@ __global__ void __launch_bounds__(256, VXM_SEQ_MINB) merge_sequence_epoch_kernel
         const unsigned oc = in_c[u] && val == 2u ? 1u : 0u, fr = in_c[u] && val == 1u ? 1u : 0u;
         packed[u >> 1] |= (oc | (fr << 8)) << (16 * (u & 1));
       }
-      add_frame_counts<U>(packed, cnt, k0, F, lane);
+      add_frame_counts<U>(packed, acc, k0, lane);
       // position after the group's last frame (F may end inside the group)
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -2623,6 +2644,7 @@ __global__ void __launch_bounds__(256, VXM_SEQ_MINB) merge_sequence_epoch_kernel
     }
     if (in_prev) dst[pos_prev] = static_cast<uint8_t>(val);
   }
+  flush_frame_counts(acc, cnt, lane);
   __syncthreads();
   const unsigned long long t_end = global_ns();
   for (int k = threadIdx.x; k < F; k += blockDim.x) {
@@ -2636,7 +2658,7 @@ __global__ void __launch_bounds__(256, VXM_SEQ_MINB) merge_sequence_epoch_kernel
 template <bool kClear>
 __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
   pdl_wait();  // K3's keys and counters
-  constexpr int U = 4;  // frames whose loads are issued together
+  constexpr int U = VXM_SEQ_U;  // frames whose loads are issued together
   __shared__ unsigned cnt[2 * kMaxFramesPerCall];           // occupied, then freed, per frame
   __shared__ int Pc[kMaxFramesPerCall + U][3];              // P_{k-1} at index k
   __shared__ uint32_t ep[kMaxFramesPerCall];
@@ -2681,6 +2703,7 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
   // so all F slots end all-Unknown
   uint32_t* key0 = p.key + static_cast<long long>(s) * F * p.n;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  uint32_t acc[4] = {0u, 0u, 0u, 0u};  // per-frame Occupied / Free counts, see add_frame_counts
   if (vec_ok) {
     // Every frame's x shift is a multiple of 4 (and dims_x too): a thread
     // folds 4 neighbouring chains at once, moving the 4 cells as one word
@@ -2705,6 +2728,8 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
       bool in_prev;
       uint32_t pos_prev = group_of(0, in_prev);
       uint32_t val = in_prev ? *reinterpret_cast<const uint32_t*>(src + pos_prev) : 0u;
+      auto og = occ0;  // slabs of frame k0 (advanced one frame per load pair)
+      auto kg = key0;
       for (int k0 = 0; k0 < F; k0 += U) {
         bool in_c[U];
         uint32_t pos[U];
@@ -2717,10 +2742,13 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
           const bool in_r = u == 0 ? in_prev : in_c[u - 1];
           const uint32_t r = u == 0 ? pos_prev : pos[u - 1];
           const bool ld = k0 + u < F && in_r && (kClear || in_c[u]);
-          const long long off = static_cast<long long>(k0 + u) * p.n + r;
-          o[u] = ld && !kClear ? __ldcs(reinterpret_cast<const uint32_t*>(occ0 + off)) : 0u;
-          kk[u] = ld ? __ldcs(reinterpret_cast<const uint4*>(key0 + off)) : make_uint4(0u, 0u, 0u, 0u);
-          if (kClear && ld && touched4(kk[u])) *reinterpret_cast<uint4*>(key0 + off) = make_uint4(0u, 0u, 0u, 0u);
+          const auto oa = og + r;
+          const auto ka = kg + r;
+          og += p.n;
+          kg += p.n;
+          o[u] = ld && !kClear ? __ldcs(reinterpret_cast<const uint32_t*>(oa)) : 0u;
+          kk[u] = ld ? __ldcs(reinterpret_cast<const uint4*>(ka)) : make_uint4(0u, 0u, 0u, 0u);
+          if (kClear && ld && touched4(kk[u])) *reinterpret_cast<uint4*>(ka) = make_uint4(0u, 0u, 0u, 0u);
         }
         // per frame: Occupied / Free counts of this thread's 4 cells (each
         // <= 4, so a warp sum fits a byte); two frames share one reduction
@@ -2735,7 +2763,7 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
           const unsigned oc = in_c[u] ? count_occupied4(val) : 0u, fr = in_c[u] ? count_free4(val) : 0u;
           packed[u >> 1] |= (oc | (fr << 8)) << (16 * (u & 1));
         }
-        add_frame_counts<U>(packed, cnt, k0, F, lane);
+        add_frame_counts<U>(packed, acc, k0, lane);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           if (k0 + u < F) {
@@ -2764,6 +2792,8 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
     bool in_prev;
     uint32_t pos_prev = cell_of(0, in_prev);
     uint32_t val = in_prev ? src[pos_prev] : 0u;
+    auto og = occ0;  // slabs of frame k0 (advanced one frame per load pair)
+    auto kg = key0;
     for (int k0 = 0; k0 < F; k0 += U) {
       // positions after frames k0..k0+U-1, then all their loads, then the merges
       bool in_c[U];
@@ -2776,10 +2806,13 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
         const bool in_r = u == 0 ? in_prev : in_c[u - 1];
         const uint32_t r = u == 0 ? pos_prev : pos[u - 1];
         const bool ld = k0 + u < F && in_r && (kClear || in_c[u]);
-        const long long off = static_cast<long long>(k0 + u) * p.n + r;
-        o[u] = ld && !kClear ? __ldcs(occ0 + off) : 0u;
-        kk[u] = ld ? __ldcs(key0 + off) : 0u;
-        if (kClear && kk[u]) key0[off] = 0u;
+        const auto oa = og + r;
+        const auto ka = kg + r;
+        og += p.n;
+        kg += p.n;
+        o[u] = ld && !kClear ? __ldcs(oa) : 0u;
+        kk[u] = ld ? __ldcs(ka) : 0u;
+        if (kClear && kk[u]) *ka = 0u;
       }
       uint32_t packed[U / 2] = {};
 #pragma unroll
@@ -2792,7 +2825,7 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
         const unsigned oc = in_c[u] && val == 2u ? 1u : 0u, fr = in_c[u] && val == 1u ? 1u : 0u;
         packed[u >> 1] |= (oc | (fr << 8)) << (16 * (u & 1));
       }
-      add_frame_counts<U>(packed, cnt, k0, F, lane);
+      add_frame_counts<U>(packed, acc, k0, lane);
       // position after the group's last frame (F may end inside the group)
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -2804,6 +2837,7 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
     }
     if (in_prev) dst[pos_prev] = static_cast<uint8_t>(val);
   }
+  flush_frame_counts(acc, cnt, lane);
   __syncthreads();
   const unsigned long long t_end = global_ns();
   for (int k = threadIdx.x; k < F; k += blockDim.x) {

@@ -131,3 +131,8 @@
 #ifndef VXM_SEQ_MINB
 #define VXM_SEQ_MINB 5
 #endif
+
+// frames of a chain whose loads the multi-frame merge issues together (even)
+#ifndef VXM_SEQ_U
+#define VXM_SEQ_U 4
+#endif
