@@ -2470,6 +2470,39 @@ __device__ __forceinline__ void flush_frame_counts(const uint32_t (&acc)[4], uns
   if (acc[3]) atomicAdd(&cnt[kMaxFramesPerCall + 32 + lane], acc[3]);
 }
 
+// Warp 0 of a chain-merge block: the cumulative shifts P_{k-1} of the F
+// frames (Pc[k], Pc[0] = 0; entries past F repeat P_{F-1}) and their epochs,
+// two frames per lane and one warp scan instead of a serial loop over F in
+// one thread; *vec_ok = every x shift (and dims_x) is a multiple of 4.
+__device__ __forceinline__ void chain_prefix(const FrameParams* f0, int F, int dx, int (*Pc)[3], uint32_t* ep,
+                                             int* vec_ok, int lane) {
+  static_assert(kMaxFramesPerCall <= 64, "two frames per lane");
+  const int k = 2 * lane;
+  int a0[3] = {0, 0, 0}, a1[3] = {0, 0, 0}, t[3];
+  if (k < F) {
+    for (int a = 0; a < 3; ++a) a0[a] = f0[k].off[a];
+    ep[k] = f0[k].epoch;
+  }
+  if (k + 1 < F) {
+    for (int a = 0; a < 3; ++a) a1[a] = f0[k + 1].off[a];
+    ep[k + 1] = f0[k + 1].epoch;
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    t[a] = a0[a] + a1[a];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, t[a], d);
+      if (lane >= d) t[a] += v;
+    }
+    Pc[k + 1][a] = t[a] - a1[a];  // P_k
+    Pc[k + 2][a] = t[a];          // P_{k+1}
+  }
+  if (lane == 0) Pc[0][0] = Pc[0][1] = Pc[0][2] = 0;
+  const bool aligned = __all_sync(0xffffffffu, ((t[0] - a1[0]) & 3) == 0 && (t[0] & 3) == 0);
+  if (lane == 0) *vec_ok = aligned && (dx & 3) == 0 ? 1 : 0;
+}
+
 __global__ void __launch_bounds__(256, VXM_SEQ_MINB) merge_sequence_epoch_kernel(KParams p, int F) {
   pdl_wait();  // K3's keys and counters
   constexpr int U = VXM_SEQ_U;  // frames whose loads are issued together
@@ -2485,19 +2518,7 @@ __global__ void __launch_bounds__(256, VXM_SEQ_MINB) merge_sequence_epoch_kernel
   }
   for (int k = threadIdx.x; k < 2 * kMaxFramesPerCall; k += blockDim.x) cnt[k] = 0u;
   __shared__ int vec_ok;
-  if (threadIdx.x == 0) {
-    int P[3] = {0, 0, 0};
-    bool aligned = (p.dx & 3) == 0;
-    for (int k = 0; k <= F; ++k) {
-      for (int a = 0; a < 3; ++a) Pc[k][a] = P[a];
-      aligned = aligned && (P[0] & 3) == 0;
-      if (k < F) {
-        for (int a = 0; a < 3; ++a) P[a] += f0[k].off[a];
-        ep[k] = f0[k].epoch;
-      }
-    }
-    vec_ok = aligned ? 1 : 0;
-  }
+  if (threadIdx.x < 32) chain_prefix(f0, F, p.dx, Pc, ep, &vec_ok, lane);
   if (blockIdx.x == 0) {
     // fold the trace counters of every frame slot of this stream (one warp each)
     for (int k = threadIdx.x >> 5; k < F; k += blockDim.x >> 5) fold_trace_slots(p.counters[static_cast<long long>(s) * F + k]);
@@ -2508,6 +2529,9 @@ __global__ void __launch_bounds__(256, VXM_SEQ_MINB) merge_sequence_epoch_kernel
   const int bx = f0->box_lo[0], by = f0->box_lo[1], bz = f0->box_lo[2];
   const int ex = f0->box_ext[0], ey = f0->box_ext[1], ez = f0->box_ext[2];
   const long long nchain = static_cast<long long>(ex) * ey * ez;
+  // blocks past the work (the grid is sized for the largest box) leave
+  // before the counters: no idle t_end atomics on the frame slots
+  if (blockIdx.x > 0 && static_cast<long long>(blockIdx.x) * blockDim.x >= (vec_ok ? (nchain >> 2) : nchain)) return;
   const uint32_t cur = f0->cur;
   const uint8_t* src = (cur ? p.loc1 : p.loc0) + static_cast<long long>(s) * p.n;
   uint8_t* dst = (cur ? p.loc0 : p.loc1) + static_cast<long long>(s) * p.n;
@@ -2671,19 +2695,7 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
   }
   for (int k = threadIdx.x; k < 2 * kMaxFramesPerCall; k += blockDim.x) cnt[k] = 0u;
   __shared__ int vec_ok;
-  if (threadIdx.x == 0) {
-    int P[3] = {0, 0, 0};
-    bool aligned = (p.dx & 3) == 0;
-    for (int k = 0; k <= F; ++k) {
-      for (int a = 0; a < 3; ++a) Pc[k][a] = P[a];
-      aligned = aligned && (P[0] & 3) == 0;
-      if (k < F) {
-        for (int a = 0; a < 3; ++a) P[a] += f0[k].off[a];
-        ep[k] = f0[k].epoch;
-      }
-    }
-    vec_ok = aligned ? 1 : 0;
-  }
+  if (threadIdx.x < 32) chain_prefix(f0, F, p.dx, Pc, ep, &vec_ok, lane);
   if (blockIdx.x == 0) {
     // fold the trace counters of every frame slot of this stream (one warp each)
     for (int k = threadIdx.x >> 5; k < F; k += blockDim.x >> 5) fold_trace_slots(p.counters[static_cast<long long>(s) * F + k]);
@@ -2694,6 +2706,9 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
   const int bx = f0->box_lo[0], by = f0->box_lo[1], bz = f0->box_lo[2];
   const int ex = f0->box_ext[0], ey = f0->box_ext[1], ez = f0->box_ext[2];
   const long long nchain = static_cast<long long>(ex) * ey * ez;
+  // blocks past the work (the grid is sized for the largest box) leave
+  // before the counters: no idle t_end atomics on the frame slots
+  if (blockIdx.x > 0 && static_cast<long long>(blockIdx.x) * blockDim.x >= (vec_ok ? (nchain >> 2) : nchain)) return;
   const uint32_t cur = f0->cur;
   const uint8_t* src = (cur ? p.loc1 : p.loc0) + static_cast<long long>(s) * p.n;
   uint8_t* dst = (cur ? p.loc0 : p.loc1) + static_cast<long long>(s) * p.n;
