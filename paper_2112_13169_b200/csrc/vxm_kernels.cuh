@@ -2470,6 +2470,26 @@ __device__ __forceinline__ void flush_frame_counts(const uint32_t (&acc)[4], uns
   if (acc[3]) atomicAdd(&cnt[kMaxFramesPerCall + 32 + lane], acc[3]);
 }
 
+// End of a chain-merge block (k4_publish): the stream's last participating
+// block (block 0 and every block that did not leave early) publishes its F
+// frame slots, one warp per slot, so no K5 follows on the chain of ranges.
+// Threadfence reduction: each thread's counter atomics are fenced before the
+// block's arrival on merge_done of the stream's first slot.
+__device__ __forceinline__ void chain_publish_when_last(const KParams& p, int s, int F, long long work) {
+  __shared__ unsigned last;
+  const long long nact = max(1LL, min(static_cast<long long>(gridDim.x), (work + blockDim.x - 1) / blockDim.x));
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0)
+    last = atomicAdd(&p.counters[static_cast<long long>(s) * F].merge_done, 1ull) ==
+                   static_cast<unsigned long long>(nact - 1) ? 1u : 0u;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int k = threadIdx.x >> 5; k < F; k += blockDim.x >> 5)
+    publish_slot(p, s * F + k, threadIdx.x & 31, 32);
+}
+
 // Warp 0 of a chain-merge block: the cumulative shifts P_{k-1} of the F
 // frames (Pc[k], Pc[0] = 0; entries past F repeat P_{F-1}) and their epochs,
 // two frames per lane and one warp scan instead of a serial loop over F in
@@ -2503,7 +2523,7 @@ __device__ __forceinline__ void chain_prefix(const FrameParams* f0, int F, int d
   if (lane == 0) *vec_ok = aligned && (dx & 3) == 0 ? 1 : 0;
 }
 
-__global__ void __launch_bounds__(256, VXM_SEQ_MINB) merge_sequence_epoch_kernel(KParams p, int F) {
+__global__ void __launch_bounds__(VXM_SEQ_THREADS, VXM_SEQ_MINB * 256 / VXM_SEQ_THREADS) merge_sequence_epoch_kernel(KParams p, int F) {
   pdl_wait();  // K3's keys and counters
   constexpr int U = VXM_SEQ_U;  // frames whose loads are issued together
   __shared__ unsigned cnt[2 * kMaxFramesPerCall];           // occupied, then freed, per frame
@@ -2677,10 +2697,11 @@ __global__ void __launch_bounds__(256, VXM_SEQ_MINB) merge_sequence_epoch_kernel
     if (cnt[kMaxFramesPerCall + k]) atomicAdd(&c.freed, static_cast<unsigned long long>(cnt[kMaxFramesPerCall + k]));
     atomicMax(&c.t_end, t_end);
   }
+  if (p.k4_publish) chain_publish_when_last(p, s, F, vec_ok ? (nchain >> 2) : nchain);
 }
 
 template <bool kClear>
-__global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
+__global__ void __launch_bounds__(VXM_SEQ_THREADS) merge_sequence_kernel(KParams p, int F) {
   pdl_wait();  // K3's keys and counters
   constexpr int U = VXM_SEQ_U;  // frames whose loads are issued together
   __shared__ unsigned cnt[2 * kMaxFramesPerCall];           // occupied, then freed, per frame
@@ -2861,6 +2882,7 @@ __global__ void __launch_bounds__(256) merge_sequence_kernel(KParams p, int F) {
     if (cnt[kMaxFramesPerCall + k]) atomicAdd(&c.freed, static_cast<unsigned long long>(cnt[kMaxFramesPerCall + k]));
     atomicMax(&c.t_end, t_end);
   }
+  if (p.k4_publish) chain_publish_when_last(p, s, F, vec_ok ? (nchain >> 2) : nchain);
 }
 
 }  // namespace vxm

@@ -456,18 +456,23 @@ void launch_stages(vxm_ctx* c, bool cloud, bool capturing, int s0, int S, cudaSt
 // K4 for S slots of rebased parameters: merge + shift + counts (F == 1), or
 // the chain kernel over S / F streams (F > 1).
 // K4' over `streams` streams of F frames each (kp rebased to the first)
-void launch_merge_chain(vxm_ctx* c, const vxm::KParams& kp, int F, int streams, cudaStream_t st) {
+// Returns true: the chain kernel publishes the counters itself (no K5).
+bool launch_merge_chain(vxm_ctx* c, const vxm::KParams& kp_in, int F, int streams, cudaStream_t st) {
+  vxm::KParams kp = kp_in;
+  kp.k4_publish = 1;
   // chains of F frames per stream; the chain box varies per call, so the
   // launch covers it with a fixed grid-stride shape
   const long long chains = c->n * 2;
-  const long long blocks = std::min<long long>((chains + kMergeThreads - 1) / kMergeThreads,
-                                               std::max<long long>(1, c->nsm * 8LL / streams));
+  constexpr int kChainThreads = VXM_SEQ_THREADS;
+  const long long blocks = std::min<long long>((chains + kChainThreads - 1) / kChainThreads,
+                                               std::max<long long>(1, c->nsm * (2048LL / kChainThreads) / streams));
   dim3 grid(static_cast<unsigned>(std::max<long long>(1, blocks)), streams);
   if (kp.key_fmt == vxm::kClearKeys)
-    VXM_CK(vxm::launch_pdl(vxm::merge_sequence_kernel<true>, grid, dim3(kMergeThreads), 0, st, kp, F));
+    VXM_CK(vxm::launch_pdl(vxm::merge_sequence_kernel<true>, grid, dim3(kChainThreads), 0, st, kp, F));
   else
-    VXM_CK(vxm::launch_pdl(vxm::merge_sequence_epoch_kernel, grid, dim3(kMergeThreads), 0, st, kp, F));
+    VXM_CK(vxm::launch_pdl(vxm::merge_sequence_epoch_kernel, grid, dim3(kChainThreads), 0, st, kp, F));
   VXM_CK(cudaGetLastError());
+  return true;
 }
 
 // Returns true when the K4 launched publishes the counters itself (no K5).
@@ -495,7 +500,7 @@ bool launch_merge(vxm_ctx* c, const vxm::KParams& kp, int S, cudaStream_t st) {
     const long long warps = rows * c->nslots;  // the whole call (branches run concurrently)
     const long long fill = static_cast<long long>(c->nsm) * 64;
     const long long rpw_max = warps / fill >= VXM_MERGE_RPW ? VXM_MERGE_RPW : vxm::kRowsPerWarp;
-    const int rpw = static_cast<int>(std::max(1LL, std::min<long long>(rpw_max, warps / fill)));
+    const int rpw = static_cast<int>(std::max<long long>(VXM_MERGE_RPW_MIN, std::min<long long>(rpw_max, warps / fill)));
     const int rows_per_block = kMergeThreads / 32 * rpw;
     dim3 grid(static_cast<unsigned>((rows + rows_per_block - 1) / rows_per_block), S);
     if (kp.key_fmt == vxm::kClearKeys) {
@@ -509,7 +514,7 @@ bool launch_merge(vxm_ctx* c, const vxm::KParams& kp, int S, cudaStream_t st) {
     }
     VXM_CK(cudaGetLastError());
   } else {
-    launch_merge_chain(c, kp, c->F, S / c->F, st);
+    return launch_merge_chain(c, kp, c->F, S / c->F, st);
   }
   return false;
 }
@@ -565,8 +570,7 @@ void launch_frame(vxm_ctx* c, bool cloud, bool capturing) {
         kp.counters_out += s0;
         kp.occ += c->n * s0;
         kp.key += c->n * s0;
-        launch_merge_chain(c, kp, s1 - s0, 1, bs);
-        launch_publish(kp, s1 - s0, bs);
+        if (!launch_merge_chain(c, kp, s1 - s0, 1, bs)) launch_publish(kp, s1 - s0, bs);
         if (b + 1 < B) VXM_CK(cudaEventRecord(c->chain[b], bs));
       }
     }
@@ -844,8 +848,7 @@ void run_frame(vxm_ctx* c, bool cloud, bool direct = false) {
       kp.counters_out += s0;
       kp.occ += c->n * s0;
       kp.key += c->n * s0;
-      launch_merge_chain(c, kp, s1 - s0, 1, bs);
-      launch_publish(kp, s1 - s0, bs);
+      if (!launch_merge_chain(c, kp, s1 - s0, 1, bs)) launch_publish(kp, s1 - s0, bs);
       VXM_CK(cudaEventRecord(c->chain[b], bs));
       VXM_CK(cudaEventRecord(c->ddone[b], bs));
       VXM_CK(cudaStreamWaitEvent(c->stream, c->ddone[b], 0));

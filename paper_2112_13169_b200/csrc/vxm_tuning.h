@@ -118,6 +118,12 @@
 // chunks for frames without an x shift, per-row loops otherwise); longer or
 // odd rows take the TMA-staged K4. 1024 (round 2): 16 cfg3 streams (200-cell
 // rows) merge in 82 instead of 110 us, 35.5k -> 39.0k frames/s; 128 before.
+// fewest rows per warp of K4 (a lone frame's slot fills the GPU less than once;
+// 4 -> a quarter of the blocks: lone cfg1/cfg2/cfg3 frames unchanged, r02br)
+#ifndef VXM_MERGE_RPW_MIN
+#define VXM_MERGE_RPW_MIN 1
+#endif
+
 #ifndef VXM_MERGE_DIRECT_MAX_DX
 #define VXM_MERGE_DIRECT_MAX_DX 1024
 #endif
@@ -132,7 +138,15 @@
 #define VXM_SEQ_MINB 5
 #endif
 
-// frames of a chain whose loads the multi-frame merge issues together (even)
+// frames of a chain whose loads the multi-frame merge issues together (even;
+// 8 at 64 registers: merge 70 -> 79 us, r02bn/r02bp)
+// threads per block of the multi-frame merge (VXM_SEQ_MINB counts 256-thread
+// blocks' worth of residency; 128: cfg1 64-frame merge 70.6 -> 66.6 us but
+// cfg3 89 -> 91 us, calls unchanged within noise, r02bp)
+#ifndef VXM_SEQ_THREADS
+#define VXM_SEQ_THREADS 256
+#endif
+
 #ifndef VXM_SEQ_U
 #define VXM_SEQ_U 4
 #endif
