@@ -53,6 +53,16 @@ for k in range(3):
     ps = [vm.look_along_x((0.13 * k * (s % 2), 0.11 * k, 0.0)) for s in range(32)]
     big.integrate_depth(vm.render_depth(cam2, ps, boxes), ps)
 movers.append(big)
+# chain merges with their in-kernel counter publish: one stream of 33 frames
+# (three chained frame ranges) and 3 streams x 8 frames whose x shifts are
+# multiples of 4 cells (the word-wise chains)
+seq33 = vm.MappingPipeline(cfg, frames_per_call=33)
+ps = [vm.look_along_x((0.0, 0.05 * (j % 12), 0.0)) for j in range(33)]
+seq33.integrate_depth(vm.render_depth(cam, ps, boxes), ps)
+seq3 = vm.MappingPipeline(cfg, n_streams=3, frames_per_call=8)
+ps = [vm.look_along_x((0.4 * (j % 3), 0.1 * s, 0.0)) for s in range(3) for j in range(8)]
+seq3.integrate_depth(vm.render_depth(cam, ps, boxes), ps)
+movers += [seq33, seq3]
 print("sanitize case done", sb[0]["freed_count"])
 for p in [batch, one, seq] + movers:
     p.close()
