@@ -47,6 +47,59 @@ __device__ __forceinline__ unsigned populate_point(const KParams& p, const doubl
   return 0u;
 }
 
+// N points at once (the dense depth kernel): every point's transform and
+// fast voxel coordinates first, branch-free, so that the N fp64 dependency
+// chains interleave; then per valid point the bounds test and the stores of
+// populate_point. Points whose floor the fast path cannot decide (rare) are
+// left to the caller (bit k of *pend), so no call to the exact division sits
+// in the loop (its call frame made ptxas spill the batch's registers).
+template <bool kClear, int N>
+__device__ __forceinline__ unsigned populate_points(const KParams& p, const double* R, const double* t,
+                                                    uint8_t* target, uint8_t* rowflag, uint32_t* keys, uint8_t mark,
+                                                    const double (&x)[N], const double (&y)[N], const double (&z)[N],
+                                                    const bool (&ok)[N], uint32_t* pend) {
+  int c[N][3];
+  bool fast[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    fast[k] = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      double acc = t[a];
+      acc = dadd(acc, dmul(R[3 * a + 0], x[k]));
+      acc = dadd(acc, dmul(R[3 * a + 1], y[k]));
+      acc = dadd(acc, dmul(R[3 * a + 2], z[k]));
+      bool f;
+      c[k][a] = voxel_coord_fast(acc, p.inv_vs, f);
+      fast[k] = fast[k] && f;
+    }
+  }
+  unsigned outside = 0;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    if (!ok[k]) continue;
+    if (!fast[k]) {
+      *pend |= 1u << k;
+      continue;
+    }
+    if (static_cast<unsigned>(c[k][0]) >= static_cast<unsigned>(p.dx) ||
+        static_cast<unsigned>(c[k][1]) >= static_cast<unsigned>(p.dy) ||
+        static_cast<unsigned>(c[k][2]) >= static_cast<unsigned>(p.dz)) {
+      ++outside;
+      continue;
+    }
+    const uint32_t idx = static_cast<uint32_t>(c[k][0]) + static_cast<uint32_t>(c[k][1]) * p.dx +
+                         static_cast<uint32_t>(c[k][2]) * (static_cast<uint32_t>(p.dx) * static_cast<uint32_t>(p.dy));
+    target[idx] = mark;
+    if (rowflag) {
+      rowflag[static_cast<uint32_t>(c[k][1]) + static_cast<uint32_t>(c[k][2]) * p.dy] = mark;
+    } else if constexpr (kClear) {
+      keys[idx] = kClearOccupied;
+    }
+  }
+  return outside;
+}
+
 // Depth quads (4 pixels, one 16-byte streaming load) per thread; a block
 // walks `iters` consecutive 256-quad tiles of one stream's frame and loads
 // tile i+1 before resolving tile i, so the HBM latency of a batched launch
@@ -201,24 +254,68 @@ __global__ void __launch_bounds__(256, VXM_POP_MINB) populate_depth_tma_kernel(K
   const int pix0 = q0 * 4;
   const float invW = 1.0f / static_cast<float>(p.W);
   total += lane == 0 ? static_cast<unsigned>(nlist) : 0u;
-  for (int i = lane; i < nlist; i += 32) {
-    const int off = wl[i];
+  auto pixel_uv = [&](int off, int& u, int& v) {
     const int pix = pix0 + off;
-    int v = static_cast<int>((static_cast<float>(pix) + 0.5f) * invW);  // pix / W, corrected below
+    v = static_cast<int>((static_cast<float>(pix) + 0.5f) * invW);  // pix / W, corrected below
     v -= v * p.W > pix ? 1 : 0;
     v += (v + 1) * p.W <= pix ? 1 : 0;
-    const int u = pix - v * p.W;
+    u = pix - v * p.W;
+  };
+#if VXM_POP_CBATCH
+  // VXM_POP_CBATCH list entries per lane at a time (interleaved fp64 chains);
+  // entry 32 j + lane whose floor the fast path cannot decide sets bit j of
+  // `pending` (a warp lists at most iters * 128 <= 1024 pixels, so j < 32)
+  constexpr int B = VXM_POP_CBATCH;
+  uint32_t pending = 0;
+  for (int i0 = 0; i0 < nlist; i0 += 32 * B) {
+    double X[B], Y[B], Z[B];
+    bool ok[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int i = i0 + 32 * b + lane;
+      ok[b] = i < nlist;
+      const int off = ok[b] ? wl[i] : 0;
+      int u, v;
+      pixel_uv(off, u, v);
+      const float dk = spx[off];
+      const double D = static_cast<double>(ok[b] ? dk : 0.0f);
+      mind = ok[b] ? fminf(mind, dk) : mind;
+      X[b] = dmul(__ldg(p.qx + u), D);
+      Y[b] = dmul(__ldg(p.qy + v), D);
+      Z[b] = D;
+    }
+    uint32_t pm = 0;
+    outside += populate_points<kClear, B>(p, R, t, target, rowflag, keys, mark, X, Y, Z, ok, &pm);
+    pending |= pm << (i0 >> 5);
+  }
+  while (pending) {
+    const int j = __ffs(pending) - 1;
+    pending &= pending - 1;
+    const int off = wl[32 * j + lane];
+    int u, v;
+    pixel_uv(off, u, v);
+    const double D = static_cast<double>(spx[off]);
+    outside += populate_point<kClear>(p, R, t, target, rowflag, keys, mark, dmul(__ldg(p.qx + u), D),
+                              dmul(__ldg(p.qy + v), D), D);
+  }
+#else
+  for (int i = lane; i < nlist; i += 32) {
+    const int off = wl[i];
+    int u, v;
+    pixel_uv(off, u, v);
     const double D = static_cast<double>(spx[off]);
     mind = fminf(mind, spx[off]);
     outside += populate_point<kClear>(p, R, t, target, rowflag, keys, mark, dmul(__ldg(p.qx + u), D),
                               dmul(__ldg(p.qy + v), D), D);
   }
+#endif
   } else {
   // the thread's first pixel (u0, v0) advances by 4T pixels per tile: one
   // division for the first tile, then a carry
   int v0 = (q0 * 4 + threadIdx.x * 4) / p.W;
   int u0 = q0 * 4 + threadIdx.x * 4 - v0 * p.W;
   const int du = (4 * T) % p.W, dv = (4 * T) / p.W;
+  uint32_t pending = 0;  // bit 4 it + k: pixel k of tile it needs the exact division (iters <= 8)
   for (int it = 0; it < iters; ++it, u0 += du, v0 += dv) {
     if (u0 >= p.W) { u0 -= p.W; ++v0; }
     const int q = q0 + it * T + threadIdx.x;
@@ -232,6 +329,40 @@ __global__ void __launch_bounds__(256, VXM_POP_MINB) populate_depth_tma_kernel(K
     }
     if (q >= nq) continue;
     const float d[4] = {cur.x, cur.y, cur.z, cur.w};
+#if VXM_POP_BATCH
+    double X[4], Y[4], Z[4];
+    bool ok[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int u = u0 + k, v = v0;
+      if (u >= p.W) { u -= p.W; ++v; }  // a row boundary inside the quad
+      // DepthImage::valid_depth (geometry.hpp:124): finite and > 0; then the
+      // max-depth cut on the promoted double (geometry.cpp:53-54), as two
+      // float compares against the largest float <= max_depth
+      ok[k] = d[k] > 0.0f && d[k] <= p.max_depth_f;
+      const double D = static_cast<double>(ok[k] ? d[k] : 0.0f);
+      total += ok[k] ? 1u : 0u;
+      mind = ok[k] ? fminf(mind, d[k]) : mind;
+      X[k] = dmul(__ldg(p.qx + u), D);
+      Y[k] = dmul(__ldg(p.qy + v), D);
+      Z[k] = D;
+    }
+#pragma unroll
+    for (int h = 0; h < 4; h += VXM_POP_BATCH) {
+      double x[VXM_POP_BATCH], y[VXM_POP_BATCH], z[VXM_POP_BATCH];
+      bool o[VXM_POP_BATCH];
+#pragma unroll
+      for (int k = 0; k < VXM_POP_BATCH; ++k) {
+        x[k] = X[h + k];
+        y[k] = Y[h + k];
+        z[k] = Z[h + k];
+        o[k] = ok[h + k];
+      }
+      uint32_t pm = 0;
+      outside += populate_points<kClear, VXM_POP_BATCH>(p, R, t, target, rowflag, keys, mark, x, y, z, o, &pm);
+      pending |= pm << (4 * it + h);
+    }
+#else
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       int u = u0 + k, v = v0;
@@ -246,6 +377,21 @@ __global__ void __launch_bounds__(256, VXM_POP_MINB) populate_depth_tma_kernel(K
       outside += populate_point<kClear>(p, R, t, target, rowflag, keys, mark, dmul(__ldg(p.qx + u), D),
                                 dmul(__ldg(p.qy + v), D), D);
     }
+#endif
+  }
+  // the pixels the fast floor could not decide, through populate_point (the
+  // exact division); the depth is still in shared memory (or re-read)
+  while (pending) {
+    const int b = __ffs(pending) - 1;
+    pending &= pending - 1;
+    const int it = b >> 2, k = b & 3;
+    const int q = q0 + it * T + threadIdx.x;
+    const float dk = aligned ? reinterpret_cast<const float*>(sq + it * T + threadIdx.x)[k] : depth[q * 4 + k];
+    const int pix = q * 4 + k;
+    const int v = pix / p.W, u = pix - v * p.W;
+    const double D = static_cast<double>(dk);
+    outside += populate_point<kClear>(p, R, t, target, rowflag, keys, mark, dmul(__ldg(p.qx + u), D),
+                              dmul(__ldg(p.qy + v), D), D);
   }
   }
   warp_min_dist(mind, &p.counters[s].min_dist_bits);

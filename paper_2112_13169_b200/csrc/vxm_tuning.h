@@ -118,6 +118,19 @@
 // chunks for frames without an x shift, per-row loops otherwise); longer or
 // odd rows take the TMA-staged K4. 1024 (round 2): 16 cfg3 streams (200-cell
 // rows) merge in 82 instead of 110 us, 35.5k -> 39.0k frames/s; 128 before.
+// K1 dense path: pixels of a quad transformed VXM_POP_BATCH at a time
+// (interleaved fp64 chains; 0: one after another). r02bt, cfg1 x64 frames/s:
+// 0 230.0k, 2 237.8k, 4 239.2k; K1+K2 88.6 -> 78.3 -> 76.3 us
+#ifndef VXM_POP_BATCH
+#define VXM_POP_BATCH 4
+#endif
+
+// K1 compacting path: list entries per lane transformed together (0: one at a
+// time). r02bu, cfg2 x64 K1+K2 stage: 0 57.1 us, 2 55.8 us, 4 56.8 us
+#ifndef VXM_POP_CBATCH
+#define VXM_POP_CBATCH 2
+#endif
+
 // fewest rows per warp of K4 (a lone frame's slot fills the GPU less than once;
 // 4 -> a quarter of the blocks: lone cfg1/cfg2/cfg3 frames unchanged, r02br)
 #ifndef VXM_MERGE_RPW_MIN

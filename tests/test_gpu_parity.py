@@ -295,6 +295,28 @@ def test_pipeline_cfg1_cfg2_640x480(gpu_lib, vox_inf, depth_m):
     _run_pair(cfg, frames)
 
 
+@pytest.mark.parametrize("vox_inf", [0, 2])
+def test_dense_k1_points_on_voxel_faces(gpu_lib, vox_inf):
+    """Dense frames (every pixel valid: the dense K1 path) of walls at depths
+    that are whole multiples of the voxel size, so one coordinate of each of
+    their points lies exactly on a voxel face: the fast floor cannot decide
+    there and the deferred exact division (after the tile loop) must, for
+    pixels of every tile a thread holds."""
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 640, 480, 6.5)
+    grid = vm.GridSpec.create_centered(10.0, 10.0, 5.0, 0.1, (0.0, 0.0, 0.0))
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=vox_inf, depth=6.5)
+    rng = np.random.default_rng(7 + vox_inf)
+    frames = []
+    for k, walls in enumerate(((2.0,), (1.5, 3.0), (0.5, 2.5, 4.0, 6.0))):
+        d = np.empty((480, 640), np.float32)
+        for rows, w in zip(np.array_split(np.arange(480), len(walls)), walls):
+            d[rows] = w
+        idx = rng.choice(d.size, 2000, replace=False)
+        d.flat[idx] = rng.uniform(0.3, 6.0, idx.size).astype(np.float32)
+        frames.append((d, vm.look_along_x((0.0, 0.1 * k, 0.0))))
+    _run_pair(cfg, frames)
+
+
 def test_pipeline_cloud_entry_point(gpu_lib):
     cam = vm.CameraModel(85 * DEG, 101 * DEG, 160, 120, 6.5)
     grid = vm.GridSpec.create_centered(6.0, 6.0, 3.0, 0.15, (0.0, 0.0, 0.0))
