@@ -290,8 +290,30 @@ __device__ __noinline__ int voxel_coord_exact(double acc, double vs) {
 // fraction tests read the high words, so the fast path costs four fp64
 // operations and a few integer compares. Otherwise (near an integer, zero,
 // large, NaN) the exact division runs.
-// The fast path alone: ok = false when the exact division must decide.
-__device__ __forceinline__ int voxel_coord_fast(double acc, double inv_vs, bool& ok) {
+// Near an integer (where the fast path declines: points on voxel faces, e.g.
+// axis-aligned walls, land within a few ulps of one) the floor is still
+// decided without the division: with k = rint(q), |Q - k| < 2^-15 for the
+// exact quotient Q = acc / vs, so floor(RN(Q)) is k or k - 1, and RN(Q) >= k
+// iff Q >= k - d/2, d = k - nextafter(k, -inf) (a tie rounds to k: an integer
+// below 2^29 has an even significand), i.e. iff acc - k vs >= -(d/2) vs.
+// r = fma(-k, vs, acc) and hv = RN((d/2) vs) (d/2 is exact) are each within
+// 2^-53 of their exact values, so the sign of e = r + hv is that of the exact
+// expression whenever |e| > 2^-49 (|r| + hv). Otherwise (a quotient at a
+// rounding midpoint), k == 0 (d/2 underflows) or NaN: ok = false.
+__device__ __forceinline__ int voxel_coord_near(double acc, double q, double vs, bool& ok) {
+  const double k = rint(q);
+  const long long kb = __double_as_longlong(k);
+  const double pk = __longlong_as_double(k > 0.0 ? kb - 1 : kb + 1);  // nextafter(k, -inf), k != 0
+  const double hv = dmul(dmul(dsub(k, pk), 0.5), vs);
+  const double r = __fma_rn(-k, vs, acc);
+  const double e = dadd(r, hv);
+  ok = k != 0.0 && fabs(e) > dmul(dadd(fabs(r), hv), 0x1p-49);
+  return static_cast<int>(k) - (e < 0.0 ? 1 : 0);
+}
+
+// The fast path alone (then the near-integer test): ok = false when the exact
+// division must decide.
+__device__ __forceinline__ int voxel_coord_fast(double acc, double vs, double inv_vs, bool& ok) {
   constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
   const double q = dmul(acc, inv_vs);
   const double t = __dadd_rd(q, kMagic);
@@ -302,17 +324,20 @@ __device__ __forceinline__ int voxel_coord_fast(double acc, double inv_vs, bool&
   return __double2loint(t);
 }
 
-__device__ __forceinline__ int voxel_coord(double acc, double vs, double inv_vs) {
-  constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+// fast path, else the near-integer test, else (ok = false) the division decides
+__device__ __forceinline__ int voxel_coord_fast_near(double acc, double vs, double inv_vs, bool& ok) {
+  const int c = voxel_coord_fast(acc, vs, inv_vs, ok);
+  if (ok) return c;
   const double q = dmul(acc, inv_vs);
-  const double t = __dadd_rd(q, kMagic);   // floor(q) + kMagic
-  const double n = dsub(t, kMagic);        // floor(q)
-  const double frac = dsub(q, n);          // in [0, 1]
   const uint32_t qhi = static_cast<uint32_t>(__double2hiint(q)) & 0x7fffffffu;
-  const uint32_t fhi = static_cast<uint32_t>(__double2hiint(frac));
-  // |q| < 2^29, frac > 2^-16 (hi word above 0x3EF00000), frac < 1 - 2^-16
-  if (qhi < 0x41C00000u && fhi > 0x3EF00000u && fhi < 0x3FEFFFE0u) return __double2loint(t);
-  return voxel_coord_exact(acc, vs);
+  if (qhi >= 0x41C00000u) return 0;  // |q| >= 2^29 (or NaN): the clamp and NaN rules of the exact path
+  return voxel_coord_near(acc, q, vs, ok);
+}
+
+__device__ __forceinline__ int voxel_coord(double acc, double vs, double inv_vs) {
+  bool ok;
+  const int c = voxel_coord_fast_near(acc, vs, inv_vs, ok);
+  return ok ? c : voxel_coord_exact(acc, vs);
 }
 
 // p_v[a] = ((t[a] + R[3a]x) + R[3a+1]y) + R[3a+2]z   (kernels_scalar.cpp:27-30)

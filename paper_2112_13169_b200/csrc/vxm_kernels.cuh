@@ -70,7 +70,7 @@ __device__ __forceinline__ unsigned populate_points(const KParams& p, const doub
       acc = dadd(acc, dmul(R[3 * a + 1], y[k]));
       acc = dadd(acc, dmul(R[3 * a + 2], z[k]));
       bool f;
-      c[k][a] = voxel_coord_fast(acc, p.inv_vs, f);
+      c[k][a] = voxel_coord_fast(acc, p.vs, p.inv_vs, f);
       fast[k] = fast[k] && f;
     }
   }
@@ -267,7 +267,8 @@ __global__ void __launch_bounds__(256, VXM_POP_MINB) populate_depth_tma_kernel(K
   // `pending` (a warp lists at most iters * 128 <= 1024 pixels, so j < 32)
   constexpr int B = VXM_POP_CBATCH;
   uint32_t pending = 0;
-  for (int i0 = 0; i0 < nlist; i0 += 32 * B) {
+  int i0 = 0;
+  for (; i0 < nlist; i0 += 32 * B) {
     double X[B], Y[B], Z[B];
     bool ok[B];
 #pragma unroll
@@ -287,6 +288,20 @@ __global__ void __launch_bounds__(256, VXM_POP_MINB) populate_depth_tma_kernel(K
     uint32_t pm = 0;
     outside += populate_points<kClear, B>(p, R, t, target, rowflag, keys, mark, X, Y, Z, ok, &pm);
     pending |= pm << (i0 >> 5);
+    // many deferred points (voxel faces): the rest one at a time, as the dense path
+    if (__popc(__ballot_sync(0xffffffffu, pm != 0u)) > VXM_POP_SERIAL_LANES) {
+      i0 += 32 * B;
+      break;
+    }
+  }
+  for (int i = i0 + lane; i < nlist; i += 32) {
+    const int off = wl[i];
+    int u, v;
+    pixel_uv(off, u, v);
+    const double D = static_cast<double>(spx[off]);
+    mind = fminf(mind, spx[off]);
+    outside += populate_point<kClear>(p, R, t, target, rowflag, keys, mark, dmul(__ldg(p.qx + u), D),
+                              dmul(__ldg(p.qy + v), D), D);
   }
   while (pending) {
     const int j = __ffs(pending) - 1;
@@ -316,6 +331,7 @@ __global__ void __launch_bounds__(256, VXM_POP_MINB) populate_depth_tma_kernel(K
   int u0 = q0 * 4 + threadIdx.x * 4 - v0 * p.W;
   const int du = (4 * T) % p.W, dv = (4 * T) / p.W;
   uint32_t pending = 0;  // bit 4 it + k: pixel k of tile it needs the exact division (iters <= 8)
+  bool serial = false;   // (warp-uniform) the rest of the tiles one pixel at a time
   for (int it = 0; it < iters; ++it, u0 += du, v0 += dv) {
     if (u0 >= p.W) { u0 -= p.W; ++v0; }
     const int q = q0 + it * T + threadIdx.x;
@@ -330,6 +346,7 @@ __global__ void __launch_bounds__(256, VXM_POP_MINB) populate_depth_tma_kernel(K
     if (q >= nq) continue;
     const float d[4] = {cur.x, cur.y, cur.z, cur.w};
 #if VXM_POP_BATCH
+    if (!serial) {
     double X[4], Y[4], Z[4];
     bool ok[4];
 #pragma unroll
@@ -362,7 +379,16 @@ __global__ void __launch_bounds__(256, VXM_POP_MINB) populate_depth_tma_kernel(K
       outside += populate_points<kClear, VXM_POP_BATCH>(p, R, t, target, rowflag, keys, mark, x, y, z, o, &pm);
       pending |= pm << (4 * it + h);
     }
-#else
+    // Points on voxel faces (axis-aligned walls and floors, e.g. a corridor)
+    // are deferred almost all: a warp whose tile deferred pixels on more than
+    // VXM_POP_SERIAL_LANES lanes takes the rest of its tiles one pixel at a
+    // time with the near-integer floor inline (populate_point), which costs
+    // less there than the batch plus the deferred pass.
+    serial = __popc(__ballot_sync(__activemask(), ((pending >> (4 * it)) & 0xFu) != 0u)) > VXM_POP_SERIAL_LANES;
+    continue;
+    }
+#endif
+    {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       int u = u0 + k, v = v0;
@@ -377,7 +403,7 @@ __global__ void __launch_bounds__(256, VXM_POP_MINB) populate_depth_tma_kernel(K
       outside += populate_point<kClear>(p, R, t, target, rowflag, keys, mark, dmul(__ldg(p.qx + u), D),
                                 dmul(__ldg(p.qy + v), D), D);
     }
-#endif
+    }
   }
   // the pixels the fast floor could not decide, through populate_point (the
   // exact division); the depth is still in shared memory (or re-read)

@@ -125,6 +125,14 @@
 #define VXM_POP_BATCH 4
 #endif
 
+// K1 dense path: a warp whose batched tile deferred pixels on more than this
+// many lanes (points on voxel faces) takes its remaining tiles one pixel at a
+// time (r02by: the batch with deferral alone ran the corridor trajectory at
+// 174k frames/s vs 209k one pixel at a time; box scenes the other way round)
+#ifndef VXM_POP_SERIAL_LANES
+#define VXM_POP_SERIAL_LANES 8
+#endif
+
 // K1 compacting path: list entries per lane transformed together (0: one at a
 // time). r02bu, cfg2 x64 K1+K2 stage: 0 57.1 us, 2 55.8 us, 4 56.8 us
 #ifndef VXM_POP_CBATCH

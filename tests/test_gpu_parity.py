@@ -295,19 +295,20 @@ def test_pipeline_cfg1_cfg2_640x480(gpu_lib, vox_inf, depth_m):
     _run_pair(cfg, frames)
 
 
-@pytest.mark.parametrize("vox_inf", [0, 2])
-def test_dense_k1_points_on_voxel_faces(gpu_lib, vox_inf):
-    """Dense frames (every pixel valid: the dense K1 path) of walls at depths
-    that are whole multiples of the voxel size, so one coordinate of each of
-    their points lies exactly on a voxel face: the fast floor cannot decide
-    there and the deferred exact division (after the tile loop) must, for
-    pixels of every tile a thread holds."""
-    cam = vm.CameraModel(85 * DEG, 101 * DEG, 640, 480, 6.5)
+@pytest.mark.parametrize("vox_inf,depth_m", [(0, 6.5), (2, 6.5), (1, 2.2)])
+def test_k1_points_on_voxel_faces(gpu_lib, vox_inf, depth_m):
+    """Frames of walls at depths that are whole multiples of the voxel size,
+    so one coordinate of each of their points lies (within rounding) on a
+    voxel face: the fast floor declines there and the near-integer floor or
+    the division decides, in the batched K1 (deferred pass), the warps that
+    switch to one pixel at a time, and (depth 2.2 m: most walls beyond it) the
+    compacting K1."""
+    cam = vm.CameraModel(85 * DEG, 101 * DEG, 640, 480, depth_m)
     grid = vm.GridSpec.create_centered(10.0, 10.0, 5.0, 0.1, (0.0, 0.0, 0.0))
-    cfg = vm.PipelineConfig(grid, cam, vox_inf=vox_inf, depth=6.5)
+    cfg = vm.PipelineConfig(grid, cam, vox_inf=vox_inf, depth=depth_m)
     rng = np.random.default_rng(7 + vox_inf)
     frames = []
-    for k, walls in enumerate(((2.0,), (1.5, 3.0), (0.5, 2.5, 4.0, 6.0))):
+    for k, walls in enumerate(((2.0,), (1.5, 3.0), (0.5, 2.5, 4.0, 6.0), (2.0, 4.0, 6.0), (1.0, 2.1, 3.0))):
         d = np.empty((480, 640), np.float32)
         for rows, w in zip(np.array_split(np.arange(480), len(walls)), walls):
             d[rows] = w
