@@ -106,7 +106,11 @@ struct Counters {
   // cast needs no occupancy reads for steps closer than that (minus the
   // dilation radius)
   unsigned int min_dist_bits;
-  unsigned int pad_;
+  // K1 (dense depth): warps of this slot's K1 that found their first tile
+  // face-heavy (low half, this frame; moved to the high half at the publish),
+  // read by the next K1 of the slot to start such warps one pixel at a time.
+  // A hint only: every mode gives the same result.
+  unsigned int pop_faces;
 };
 
 // Per-warp min of a non-negative float, folded into *dst (as ordered bits).
@@ -324,33 +328,42 @@ __device__ __forceinline__ int voxel_coord_fast(double acc, double vs, double in
   return __double2loint(t);
 }
 
-// fast path, else the near-integer test, else (ok = false) the division decides
-__device__ __forceinline__ int voxel_coord_fast_near(double acc, double vs, double inv_vs, bool& ok) {
-  const int c = voxel_coord_fast(acc, vs, inv_vs, ok);
-  if (ok) return c;
+// where the fast path declined: the near-integer test, else the division
+__device__ __forceinline__ int voxel_coord_slow(double acc, double vs, double inv_vs) {
   const double q = dmul(acc, inv_vs);
   const uint32_t qhi = static_cast<uint32_t>(__double2hiint(q)) & 0x7fffffffu;
-  if (qhi >= 0x41C00000u) return 0;  // |q| >= 2^29 (or NaN): the clamp and NaN rules of the exact path
-  return voxel_coord_near(acc, q, vs, ok);
+  if (qhi < 0x41C00000u) {  // (|q| >= 2^29 or NaN: the clamp and NaN rules of the exact path)
+    bool ok;
+    const int c = voxel_coord_near(acc, q, vs, ok);
+    if (ok) return c;
+  }
+  return voxel_coord_exact(acc, vs);
 }
 
 __device__ __forceinline__ int voxel_coord(double acc, double vs, double inv_vs) {
   bool ok;
-  const int c = voxel_coord_fast_near(acc, vs, inv_vs, ok);
-  return ok ? c : voxel_coord_exact(acc, vs);
+  const int c = voxel_coord_fast(acc, vs, inv_vs, ok);
+  return ok ? c : voxel_coord_slow(acc, vs, inv_vs);
 }
 
 // p_v[a] = ((t[a] + R[3a]x) + R[3a+1]y) + R[3a+2]z   (kernels_scalar.cpp:27-30)
+// (slow: set when a coordinate needed more than the fast floor)
 __device__ __forceinline__ void transform_voxelize(const double* R, const double* t, double x,
                                                    double y, double z, double vs,
-                                                   double inv_vs, int* c) {
+                                                   double inv_vs, int* c, bool* slow = nullptr) {
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     double acc = t[a];
     acc = dadd(acc, dmul(R[3 * a + 0], x));
     acc = dadd(acc, dmul(R[3 * a + 1], y));
     acc = dadd(acc, dmul(R[3 * a + 2], z));
-    c[a] = voxel_coord(acc, vs, inv_vs);
+    bool ok;
+    int f = voxel_coord_fast(acc, vs, inv_vs, ok);
+    if (!ok) {
+      if (slow) *slow = true;
+      f = voxel_coord_slow(acc, vs, inv_vs);
+    }
+    c[a] = f;
   }
 }
 

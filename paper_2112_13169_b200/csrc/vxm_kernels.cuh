@@ -27,9 +27,9 @@ template <bool kClear>
 __device__ __forceinline__ unsigned populate_point(const KParams& p, const double* R,
                                                    const double* t, uint8_t* target,
                                                    uint8_t* rowflag, uint32_t* keys, uint8_t mark, double x,
-                                                   double y, double z) {
+                                                   double y, double z, bool* slow = nullptr) {
   int c[3];
-  transform_voxelize(R, t, x, y, z, p.vs, p.inv_vs, c);
+  transform_voxelize(R, t, x, y, z, p.vs, p.inv_vs, c, slow);
   if (static_cast<unsigned>(c[0]) >= static_cast<unsigned>(p.dx) ||
       static_cast<unsigned>(c[1]) >= static_cast<unsigned>(p.dy) ||
       static_cast<unsigned>(c[2]) >= static_cast<unsigned>(p.dz)) {
@@ -331,7 +331,12 @@ __global__ void __launch_bounds__(256, VXM_POP_MINB) populate_depth_tma_kernel(K
   int u0 = q0 * 4 + threadIdx.x * 4 - v0 * p.W;
   const int du = (4 * T) % p.W, dv = (4 * T) / p.W;
   uint32_t pending = 0;  // bit 4 it + k: pixel k of tile it needs the exact division (iters <= 8)
-  bool serial = false;   // (warp-uniform) the rest of the tiles one pixel at a time
+  // (warp-uniform) the rest of the tiles one pixel at a time: from the start
+  // when most warps of the slot's previous K1 found face-heavy tiles
+  const uint32_t hint = __ldcg(&p.counters[s].pop_faces) >> 16;
+  bool serial = 100u * hint > VXM_POP_HINT_PCT * gridDim.x * (blockDim.x >> 5);
+  bool faces = false;  // this warp's first tile was face-heavy
+  bool lane_slow = false;  // (serial, first tile) a pixel of this lane took the slow floor
   for (int it = 0; it < iters; ++it, u0 += du, v0 += dv) {
     if (u0 >= p.W) { u0 -= p.W; ++v0; }
     const int q = q0 + it * T + threadIdx.x;
@@ -385,10 +390,12 @@ __global__ void __launch_bounds__(256, VXM_POP_MINB) populate_depth_tma_kernel(K
     // time with the near-integer floor inline (populate_point), which costs
     // less there than the batch plus the deferred pass.
     serial = __popc(__ballot_sync(__activemask(), ((pending >> (4 * it)) & 0xFu) != 0u)) > VXM_POP_SERIAL_LANES;
+    faces = faces || (it == 0 && serial);
     continue;
     }
 #endif
     {
+    bool* slow = it == 0 ? &lane_slow : nullptr;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       int u = u0 + k, v = v0;
@@ -401,10 +408,12 @@ __global__ void __launch_bounds__(256, VXM_POP_MINB) populate_depth_tma_kernel(K
       ++total;
       mind = fminf(mind, d[k]);
       outside += populate_point<kClear>(p, R, t, target, rowflag, keys, mark, dmul(__ldg(p.qx + u), D),
-                                dmul(__ldg(p.qy + v), D), D);
+                                dmul(__ldg(p.qy + v), D), D, slow);
     }
+    if (it == 0) faces = __popc(__ballot_sync(__activemask(), lane_slow)) > VXM_POP_SERIAL_LANES;
     }
   }
+  if (faces && (threadIdx.x & 31) == 0) atomicAdd(&p.counters[s].pop_faces, 1u);
   // the pixels the fast floor could not decide, through populate_point (the
   // exact division); the depth is still in shared memory (or re-read)
   while (pending) {
@@ -1702,6 +1711,7 @@ __device__ __forceinline__ void publish_slot_clear(const KParams& p, int s, int 
   if (t == 0) {
     p.counters[s].merge_done = 0ull;
     p.counters[s].min_dist_bits = 0x7F800000u;
+    p.counters[s].pop_faces = (p.counters[s].pop_faces & 0xFFFFu) << 16;
   }
 }
 __device__ __forceinline__ void publish_slot(const KParams& p, int s, int t = threadIdx.x, int nt = blockDim.x) {

@@ -133,6 +133,12 @@
 #define VXM_POP_SERIAL_LANES 8
 #endif
 
+// ... and every warp starts one pixel at a time when more than this percentage
+// of the warps of the slot's previous K1 found face-heavy first tiles
+#ifndef VXM_POP_HINT_PCT
+#define VXM_POP_HINT_PCT 75
+#endif
+
 // K1 compacting path: list entries per lane transformed together (0: one at a
 // time). r02bu, cfg2 x64 K1+K2 stage: 0 57.1 us, 2 55.8 us, 4 56.8 us
 #ifndef VXM_POP_CBATCH
