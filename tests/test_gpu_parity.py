@@ -98,6 +98,35 @@ def test_transform_voxelize_clamp_band_and_near_integers(gpu_lib):
         assert np.array_equal(g, w)
 
 
+@pytest.mark.parametrize("vs", [0.05, 0.07, 0.1, 0.15, 0.2, 0.3])
+def test_transform_voxelize_near_integer_quotients(gpu_lib, vs):
+    """Coordinates within a few ulps of whole multiples of the voxel size and
+    of the points where acc / vs rounds across an integer (k - ulp/2): the
+    near-integer floor (remainder sign, no division) against the reference's
+    floor(acc / vs), positive and negative, up to 2^28 cells."""
+    rng = np.random.default_rng(int(vs * 1000))
+    k = np.concatenate([np.arange(-40, 41), rng.integers(-2**28, 2**28, 300),
+                        2.0 ** np.arange(1, 29), -(2.0 ** np.arange(1, 29))]).astype(np.float64)
+    below = np.nextafter(k, -np.inf)
+    bases = [k * vs, ((k + below) / 2) * vs]  # multiples, and the rounding midpoints below k
+    xs = []
+    for b in bases:
+        for j in range(-6, 7):
+            v = b.copy()
+            step = np.inf if j > 0 else -np.inf
+            for _ in range(abs(j)):
+                v = np.nextafter(v, step)
+            xs.append(v)
+    xs = np.concatenate(xs)
+    zs = np.zeros(xs.size)
+    for t0 in (0.0, 0.25, -3.5):
+        t = np.array([t0, 0.0, 0.0])
+        got = vm.kernel_transform_voxelize(xs, zs, zs, np.eye(3), t, vs)
+        want = ref.transform_voxelize(xs, zs, zs, np.eye(3), t, vs)
+        for g, w in zip(got, want):
+            assert np.array_equal(g, w), (vs, t0, int((g != w).sum()))
+
+
 @pytest.mark.parametrize("n", [0, 1, 3, 4, 5, 33, 4097])
 def test_transform_voxelize_random_rotations(gpu_lib, n):
     rng = np.random.default_rng(41 + n)
