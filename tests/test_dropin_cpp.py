@@ -65,8 +65,25 @@ def test_reference_acceptance_reproduces_recorded_run():
     exe = Path(__file__).resolve().parent.parent / "oracle" / "_ref" / "acceptance"
     if not exe.exists():
         pytest.skip("oracle/_ref not built")
-    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=900)
     strip = lambda s: [re.sub(r" \(\d+\.\d+ s\)", "", ln) for ln in s.strip().splitlines()]  # noqa: E731
     want = strip((Path(__file__).resolve().parent / "golden" / "acceptance_recorded.txt").read_text())
-    assert strip(r.stdout) == want
+    # criteria 8 (log-log slope of wall times) and 10 (a 3x wall-time ratio)
+    # measure this host's timings, so a busy host can flip their verdict: their
+    # text must match with either verdict, every other line exactly (a few runs
+    # are tried for the exact recorded output first)
+    timed = ("] 8: ", "] 10: ")
+    untag = lambda ln: re.sub(r"^\[(PASS|FAIL)\] ", "", ln)  # noqa: E731
+    for _ in range(3):
+        r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=900)
+        got = strip(r.stdout)
+        if got == want:
+            break
     assert r.returncode == 1  # the recorded run fails criterion 9 too
+    assert len(got) == len(want)
+    for g, w in zip(got[:-1], want[:-1]):
+        if any(t in w for t in timed):
+            assert untag(g) == untag(w), (g, w)
+        else:
+            assert g == w, (g, w)
+    extra = sum(1 for g in got if g.startswith("[FAIL]") and any(t in g for t in timed))
+    assert got[-1] == f"acceptance: {1 + extra} of 12 criteria failed", got[-1]
