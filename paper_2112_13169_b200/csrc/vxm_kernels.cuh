@@ -1513,14 +1513,14 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
 }
 
 // Launches K3 over `slots` frame slots in the shape that suits the batch.
-constexpr long long kSplitMaxRays = 32768;
+constexpr long long kSplitMaxRays = VXM_TB_SPLIT_MAX_RAYS;
 // batch K3 shape: VXM_TB_* (vxm_tuning.h)
 
 // `batch` is the number of slots of the whole call (graph branches launch
 // shares of it concurrently, so the GPU is as full as the total says).
 inline void launch_trace(const KParams& kp, int slots, int batch, cudaStream_t st) {
   const int tiles = kp.tiles_x * kp.tiles_y;
-  if (batch >= 8) {
+  if (batch >= VXM_TB_BATCH_MIN) {
     // dedup by match.any on every step for large bundles, on every other step
     // (shuffles between) for small ones (VXM_TB_MATCH_* in vxm_tuning.h)
     const dim3 grid((tiles + VXM_TB_WARPS - 1) / VXM_TB_WARPS, slots), block(32 * VXM_TB_WARPS);

@@ -32,6 +32,18 @@
 #ifndef VXM_TB_WARPS
 #define VXM_TB_WARPS 2
 #endif
+// K3 shape by the call's slots: the batch kernel from VXM_TB_BATCH_MIN slots,
+// below that the one-warp kernel, each ray as two halves while the call has at
+// most VXM_TB_SPLIT_MAX_RAYS rays. r02cg (graph ms per call): batch kernel from
+// 16 slots: cfg2 x8 0.0486 -> 0.0509, cfg1 x8 0.0573 -> 0.0615; split up to 64k
+// rays: cfg2 x4 0.0430 -> 0.0451; both kept as they are
+#ifndef VXM_TB_BATCH_MIN
+#define VXM_TB_BATCH_MIN 8
+#endif
+#ifndef VXM_TB_SPLIT_MAX_RAYS
+#define VXM_TB_SPLIT_MAX_RAYS 32768
+#endif
+
 #ifndef VXM_TB_MINB
 #define VXM_TB_MINB 20
 #endif
