@@ -1421,6 +1421,38 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
         lw += kChunk;
       }
     }
+    // (the one-warp kernel only: in the 48-register batch kernel the extra
+    // code lengthened the all-live fast chunk, r02ch)
+    constexpr bool kTailFast = VXM_TB_TAIL_FAST && kTraceWarps == 1;
+    if constexpr (kTailFast) {
+    // Once some lanes' walks have ended (only an exact chunk ends one), their
+    // lim is +inf, so they never block a fast chunk: the warp's tail takes
+    // fast chunks whenever its live lanes qualify, with the ended lanes' cells
+    // masked (they keep stepping; an invalid cell reads as occupied: no write,
+    // no count) instead of exact chunks to the end of its longest ray.
+    bool all_live = true;  // (warp-uniform)
+    for (;;) {
+      if (kFast && __all_sync(0xffffffffu, fast_test(lim))) {
+        uint32_t cell[kChunk];
+        fast_steps(cell);
+        if (all_live) {
+          resolve_live(cell);
+        } else {
+#pragma unroll
+          for (int j = 0; j < kChunk; ++j) cell[j] = al ? cell[j] : 0xffffffffu;
+          resolve_tail(cell);
+        }
+        continue;
+      }
+      uint32_t cell[kChunk];
+      step_chunk(cell);
+      resolve_tail(cell);
+      if (!al) lim = __longlong_as_double(0x7ff0000000000000ll);
+      const unsigned live = __ballot_sync(0xffffffffu, al != 0u);
+      if (!live) break;
+      all_live = live == 0xffffffffu;
+    }
+    } else {
     for (;;) {
       if (kFast && __all_sync(0xffffffffu, fast_test(lim))) {
         uint32_t cell[kChunk];
@@ -1433,6 +1465,7 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
       step_chunk(cell);
       resolve_tail(cell);
       if (!al) lim = -__longlong_as_double(0x7ff0000000000000ll);
+    }
     }
     if constexpr (kSplit) {
       // The far half resolved its cells as if nothing before it were

@@ -32,6 +32,14 @@
 #ifndef VXM_TB_WARPS
 #define VXM_TB_WARPS 2
 #endif
+// K3 (one-warp kernel of lone frames / small calls): fast chunks in the warp's
+// tail with the ended lanes masked (1) or exact chunks from the first ended
+// lane on (0). r02ch: lone cfg2 27.8 -> 27.2 us, cfg1 26.2 -> 25.7, cfg3 53.3
+// -> 52.5; in the batch kernel it cost 1-3% (not used there)
+#ifndef VXM_TB_TAIL_FAST
+#define VXM_TB_TAIL_FAST 1
+#endif
+
 // K3 shape by the call's slots: the batch kernel from VXM_TB_BATCH_MIN slots,
 // below that the one-warp kernel, each ray as two halves while the call has at
 // most VXM_TB_SPLIT_MAX_RAYS rays. r02cg (graph ms per call): batch kernel from
