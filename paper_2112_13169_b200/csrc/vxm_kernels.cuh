@@ -1453,6 +1453,36 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
       all_live = live == 0xffffffffu;
     }
     } else {
+#if VXM_TB_TAIL_FAST_BATCH
+    // the batch kernel: the all-live fast loop as below, and the masked fast
+    // chunk tried only where the tail would take an exact chunk (lim2 = lim of
+    // the live lanes, +inf for the ended ones)
+    double lim2 = lim;
+    for (;;) {
+      if (kFast && __all_sync(0xffffffffu, fast_test(lim))) {
+        uint32_t cell[kChunk];
+        fast_steps(cell);
+        resolve_live(cell);
+        continue;
+      }
+      if (!__any_sync(0xffffffffu, al != 0u)) break;
+      if (kFast && __all_sync(0xffffffffu, fast_test(lim2))) {
+        uint32_t cell[kChunk];
+        fast_steps(cell);
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) cell[j] = al ? cell[j] : 0xffffffffu;
+        resolve_tail(cell);
+        continue;
+      }
+      uint32_t cell[kChunk];
+      step_chunk(cell);
+      resolve_tail(cell);
+      if (!al) {
+        lim = -__longlong_as_double(0x7ff0000000000000ll);
+        lim2 = __longlong_as_double(0x7ff0000000000000ll);
+      }
+    }
+#else
     for (;;) {
       if (kFast && __all_sync(0xffffffffu, fast_test(lim))) {
         uint32_t cell[kChunk];
@@ -1466,6 +1496,7 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
       resolve_tail(cell);
       if (!al) lim = -__longlong_as_double(0x7ff0000000000000ll);
     }
+#endif
     }
     if constexpr (kSplit) {
       // The far half resolved its cells as if nothing before it were

@@ -40,6 +40,13 @@
 #define VXM_TB_TAIL_FAST 1
 #endif
 
+// K3 batch kernel: the masked tail fast chunk tried where an exact chunk would
+// run (r02cj: trace 109.1 -> 110.2 us per 64 cfg2 frames, cfg1 x64 -1.4%: the
+// second fast test per tail chunk costs more than the exact chunks it saves)
+#ifndef VXM_TB_TAIL_FAST_BATCH
+#define VXM_TB_TAIL_FAST_BATCH 0
+#endif
+
 // K3 shape by the call's slots: the batch kernel from VXM_TB_BATCH_MIN slots,
 // below that the one-warp kernel, each ray as two halves while the call has at
 // most VXM_TB_SPLIT_MAX_RAYS rays. r02cg (graph ms per call): batch kernel from
