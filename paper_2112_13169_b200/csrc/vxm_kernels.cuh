@@ -1350,7 +1350,7 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
     // the fast-chunk test against a limit: some axis of every lane has
     // fma(kChunk-1, tdelta_a, t_a) below it (PTX compares chained with or:
     // left to ptxas, the three compares become an fmin with NaN handling)
-    auto fast_test = [&](double lm) -> uint32_t {
+    auto fast_test = [&](double lm, double ahead = static_cast<double>(kChunk - 1)) -> uint32_t {
       uint32_t ok = 0;
       asm("{\n\t"
           ".reg .pred p;\n\t"
@@ -1364,9 +1364,12 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
           "selp.u32 %0, 1, 0, p;\n\t"
           "}"
           : "=r"(ok)
-          : "d"(kAhead), "d"(e0), "d"(t0), "d"(e1), "d"(t1), "d"(e2), "d"(t2), "d"(lm));
+          : "d"(ahead), "d"(e0), "d"(t0), "d"(e1), "d"(t1), "d"(e2), "d"(t2), "d"(lm));
       return ok;
     };
+    // two chunks under one test (the same bound with 2 kChunk - 1 steps ahead)
+    constexpr bool kFast2 = VXM_TB_FAST2 && kTraceWarps > 1;
+    constexpr double kAhead2 = static_cast<double>(2 * kChunk - 1);
     // kChunk steps without threshold tests: t_a = fma(m_a, e_a, t_a) with
     // m_a = 1 on the chosen axis, 0 elsewhere (fma(1, e, t) = RN(t + e),
     // fma(0, e, t) = t), one select of a high word per axis
@@ -1404,7 +1407,10 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
       // occupancy loads: every cell is written (untraced state unchanged),
       // only the dedup and the RED remain.
       const double lim_near = fmin(lim, near_dist);
-      while (__all_sync(0xffffffffu, fast_test(lim_near))) {
+      int near_reps = 1;  // chunks per test: 2 while the two-chunk bound holds
+      if constexpr (kFast2) near_reps = __all_sync(0xffffffffu, fast_test(lim_near, kAhead2)) ? 2 : 1;
+      while (near_reps == 2 || __all_sync(0xffffffffu, fast_test(lim_near))) {
+        for (int rep = 0; rep < near_reps; ++rep) {
         uint32_t cell[kChunk];
         fast_steps(cell);
 #pragma unroll
@@ -1419,6 +1425,8 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
                        : "memory");
         }
         lw += kChunk;
+        }
+        if constexpr (kFast2) near_reps = __all_sync(0xffffffffu, fast_test(lim_near, kAhead2)) ? 2 : 1;
       }
     }
     // (the one-warp kernel only: in the 48-register batch kernel the extra
@@ -1484,6 +1492,15 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
     }
 #else
     for (;;) {
+      if (kFast2 && __all_sync(0xffffffffu, fast_test(lim, kAhead2))) {
+#pragma unroll 1
+        for (int rep = 0; rep < 2; ++rep) {
+          uint32_t cell[kChunk];
+          fast_steps(cell);
+          resolve_live(cell);
+        }
+        continue;
+      }
       if (kFast && __all_sync(0xffffffffu, fast_test(lim))) {
         uint32_t cell[kChunk];
         fast_steps(cell);

@@ -47,6 +47,14 @@
 #define VXM_TB_TAIL_FAST_BATCH 0
 #endif
 
+// K3 batch kernel: two fast chunks under one chunk-bound test (2 kChunk - 1
+// steps ahead) while it holds (r02cm: trace 109.4 -> 111.0 us per 64 cfg2
+// frames, cfg1 x64 -1.3%: the rep loop costs what the saved tests do, and the
+// looser bound sends more chunks to the single-chunk test)
+#ifndef VXM_TB_FAST2
+#define VXM_TB_FAST2 0
+#endif
+
 // K3 shape by the call's slots: the batch kernel from VXM_TB_BATCH_MIN slots,
 // below that the one-warp kernel, each ray as two halves while the call has at
 // most VXM_TB_SPLIT_MAX_RAYS rays. r02cg (graph ms per call): batch kernel from
