@@ -1982,11 +1982,43 @@ __global__ void __launch_bounds__(256, VXM_MERGE_MINB) merge_epoch_kernel(KParam
     };
     const bool aligned = (delta & 15) == 0;
     const uint32_t nch = static_cast<uint32_t>(p.n >> 4);
+#if VXM_MERGE_INCR
+    // the chunk's (x, y, z) advanced by the grid stride with carries (one
+    // division pair for the first chunk and one for the stride) instead of
+    // two division pairs per chunk; the chunk's last cell is in the same row
+    // or the next one (dx >= 16)
+    const uint32_t ch0 = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+    uint32_t cz = div_small(ch0 << 4, dxy, inv_dxy), cy, cx;
+    cy = div_small((ch0 << 4) - cz * dxy, dx, inv_dx);
+    cx = (ch0 << 4) - cz * dxy - cy * dx;
+    const uint32_t S = stride << 4;
+    const uint32_t sz = S / dxy, sy = (S - sz * dxy) / dx, sx = S - sz * dxy - sy * dx;
+    const int dyi = p.dy;
+    for (uint32_t ch = ch0; ch < nch; ch += stride) {
+      const uint32_t c = ch << 4;
+      const int sc = static_cast<int>(c) + delta;
+      uint32_t out[4] = {0u, 0u, 0u, 0u};
+      const bool row0 = static_cast<int>(cy) >= ylo && static_cast<int>(cy) < yhi && static_cast<int>(cz) >= zlo &&
+                        static_cast<int>(cz) < zhi;
+      // the row of cell c + 15
+      int ey = static_cast<int>(cy), ez = static_cast<int>(cz);
+      if (cx + 15 >= dx) {
+        if (++ey == dyi) { ey = 0; ++ez; }
+      }
+      const bool row1 = ey >= ylo && ey < yhi && ez >= zlo && ez < zhi;
+      cx += sx;
+      cy += sy;
+      cz += sz;
+      if (cx >= dx) { cx -= dx; ++cy; }
+      if (cy >= static_cast<uint32_t>(dyi)) { cy -= dyi; ++cz; }
+      if (row0 && row1) {
+#else
     for (uint32_t ch = blockIdx.x * blockDim.x + threadIdx.x; ch < nch; ch += gridDim.x * blockDim.x) {
       const uint32_t c = ch << 4;
       const int sc = static_cast<int>(c) + delta;
       uint32_t out[4] = {0u, 0u, 0u, 0u};
       if (valid(c) && valid(c + 15)) {
+#endif
         uint32_t l[4], o[4];
         if (aligned) {
           const uint4 L = __ldcs(reinterpret_cast<const uint4*>(src + sc));

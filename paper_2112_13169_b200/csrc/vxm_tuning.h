@@ -180,6 +180,13 @@
 #define VXM_POP_CBATCH 2
 #endif
 
+// K4 flat path: chunk coordinates advanced by the grid stride (1) or two
+// division pairs per chunk (0). r02cn: merge stage 45.1 -> 43.0 us per 64 cfg2
+// frames (quick_time), bench 46.9 -> 45.6 us and +0.6% frames/s
+#ifndef VXM_MERGE_INCR
+#define VXM_MERGE_INCR 1
+#endif
+
 // fewest rows per warp of K4 (a lone frame's slot fills the GPU less than once;
 // 4 -> a quarter of the blocks: lone cfg1/cfg2/cfg3 frames unchanged, r02br)
 #ifndef VXM_MERGE_RPW_MIN
