@@ -1918,6 +1918,19 @@ __device__ __forceinline__ unsigned count_free16(const uint32_t (&x)[4]) {
 // merge of 4 packed cells: local l4, occupancy o4 (epoch bytes), 4 epoch keys.
 // States are 0..3 per byte, so "== 0" and "== 3" are two-bit tests.
 __device__ __forceinline__ uint32_t merge4(uint32_t l4, uint32_t o4, uint4 k4, uint32_t epoch) {
+#if VXM_MERGE4_PRMT
+  // the four keys' bytes 3, 2 and 0 gathered into one word each (byte i =
+  // key i's byte): a key is this frame's iff byte 3 == epoch >> 6 and the top
+  // six bits of byte 2 == epoch & 63 (epoch << 18, 14 bits); bit 0 of byte 0
+  // is its traced bit
+  static_assert(kKeyShift == 18, "byte layout of the epoch keys");
+  const uint32_t b3 = __byte_perm(__byte_perm(k4.x, k4.y, 0x0073), __byte_perm(k4.z, k4.w, 0x0073), 0x5410);
+  const uint32_t b2 = __byte_perm(__byte_perm(k4.x, k4.y, 0x0062), __byte_perm(k4.z, k4.w, 0x0062), 0x5410);
+  const uint32_t b0 = __byte_perm(__byte_perm(k4.x, k4.y, 0x0040), __byte_perm(k4.z, k4.w, 0x0040), 0x5410);
+  const uint32_t e3 = ((epoch >> 6) & 0xffu) * 0x01010101u, e2 = ((epoch & 63u) << 2) * 0x01010101u;
+  const uint32_t valid = zero_bytes((b3 ^ e3) | ((b2 & 0xfcfcfcfcu) ^ e2));  // 0xff per key of this frame
+  uint32_t m4 = valid & (0x01010101u | ((b0 << 1) & 0x02020202u));            // 1 or 3
+#else
   const uint32_t kk[4] = {k4.x, k4.y, k4.z, k4.w};
   uint32_t m4 = 0;
 #pragma unroll
@@ -1925,6 +1938,7 @@ __device__ __forceinline__ uint32_t merge4(uint32_t l4, uint32_t o4, uint4 k4, u
     const uint32_t v = (kk[i] >> kKeyShift) == epoch ? (1u | ((kk[i] & 1u) << 1)) : 0u;  // 1 or 3
     m4 |= v << (8 * i);
   }
+#endif
   const uint32_t occm = zero_bytes(o4 ^ (epoch * 0x01010101u));  // 0xff where Occupied
   m4 = (m4 & ~occm) | (0x02020202u & occm);
   const uint32_t keep = (((m4 | (m4 >> 1)) & 0x01010101u) ^ 0x01010101u) * 0xffu;  // m == 0

@@ -187,6 +187,13 @@
 #define VXM_MERGE_INCR 1
 #endif
 
+// K4 / chain merges: the four keys of a word decoded with byte permutes (1)
+// or one by one (0). r02cq: K4 flat loop 620 -> 572 SASS instructions, bench
+// merge stage 45.6 -> 44.7 us per 64 cfg2 frames, frames/s +0.2-0.9%
+#ifndef VXM_MERGE4_PRMT
+#define VXM_MERGE4_PRMT 1
+#endif
+
 // fewest rows per warp of K4 (a lone frame's slot fills the GPU less than once;
 // 4 -> a quarter of the blocks: lone cfg1/cfg2/cfg3 frames unchanged, r02br)
 #ifndef VXM_MERGE_RPW_MIN
