@@ -224,6 +224,10 @@ struct KParams {
 
 // 0xff in every byte of x that is zero, 0x00 elsewhere (exact, no carries
 // across bytes: each byte's low 7 bits + 0x7f stays within the byte).
+// 0x80 in every byte of x that is zero, 0 elsewhere
+__device__ __forceinline__ uint32_t zero_bytes_msb(uint32_t x) {
+  return ((((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x) & 0x80808080u) ^ 0x80808080u;
+}
 __device__ __forceinline__ uint32_t zero_bytes(uint32_t x) {
   const uint32_t nonzero = (((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x) & 0x80808080u;
   return ((nonzero ^ 0x80808080u) >> 7) * 0xffu;

@@ -579,7 +579,7 @@ __global__ void __launch_bounds__(256) dilate_rows_vec_kernel(KParams p, int r) 
     const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const uint32_t hit = zero_bytes(w4[i] ^ ee) & 0x80808080u;  // 0x80 per matching byte
+      const uint32_t hit = zero_bytes_msb(w4[i] ^ ee);  // 0x80 per matching byte
       m |= ((hit * 0x00204081u) >> 28) << (4 * i);
     }
   }
@@ -676,7 +676,7 @@ __global__ void __launch_bounds__(256) dilate_tiles_kernel(KParams p, int r_rt) 
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           if (q < nq) {
-            const uint32_t hit = zero_bytes(__ldg(src + q) ^ ee) & 0x80808080u;  // 0x80 per centre byte
+            const uint32_t hit = zero_bytes_msb(__ldg(src + q) ^ ee);  // 0x80 per centre byte
             m |= ((hit * 0x00204081u) >> 28) << (4 * q);
           }
         }
