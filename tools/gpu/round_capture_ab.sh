@@ -1,0 +1,11 @@
+mkdir -p gpurun_out
+T=r02ct
+timeout 1200 bash tools/profile_round.sh $T > gpurun_out/${T}_profile.log 2>&1
+AB=gpurun_out/r02cu_knobs_ab.txt
+for rep in 1 2; do
+for lib in libvxm.so libvxm_minb16.so libvxm_minb24.so libvxm_br4.so libvxm_rpw8.so; do
+  echo "== $lib" >> $AB
+  VXM_LIB_NAME=$lib QT_CONFIGS=cfg2:64,cfg1:64 timeout 200 python tools/quick_time.py 2>&1 | grep -A1 x64 >> $AB
+  VXM_LIB_NAME=$lib timeout 200 python bench.py --no-extras --no-cpu-baseline --steps 50 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('$lib bench value', d['value'], d.get('stage_ms_per_step'))" >> $AB
+done
+done
