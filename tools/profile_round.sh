@@ -18,5 +18,5 @@ done
 ncu --set full --clock-control none --import-source on -k regex:merge_sequence_epoch -s 2 -c 1 -o gpurun_out/${TAG}_merge_sequence \
     python tools/prof_frames.py seq64 > gpurun_out/${TAG}_merge_sequence.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:merge_epoch_tma -s 2 -c 1 -o gpurun_out/${TAG}_merge_tma \
-    python tools/prof_frames.py cfg3x8 > gpurun_out/${TAG}_merge_tma.log 2>&1
+    python tools/prof_frames.py odd8 > gpurun_out/${TAG}_merge_tma.log 2>&1
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem --format=csv > gpurun_out/${TAG}_gpu.txt
