@@ -36,14 +36,73 @@ struct StageError {
                        std::string(#call) + ": " + cudaGetErrorString(e_)};              \
   } while (0)
 
-// RAII device buffer.
+// Per-thread, per-device cache of stage scratch blocks. Every stage call runs
+// on its thread's default stream and ends in a synchronous download (or a
+// device synchronize), so a block released at the end of one call is idle
+// and the next call on the thread reuses it: no cudaMalloc/cudaFree per call
+// (the reference's stage functions allocate nothing on the device). Blocks
+// are rounded up to powers of two; at most kScratchKeep bytes stay cached.
+struct ScratchBlock {
+  int dev;
+  void* p;
+  size_t bytes;
+  bool used;
+};
+constexpr size_t kScratchKeep = size_t(1) << 31;
+struct ScratchCache {
+  std::vector<ScratchBlock> blocks;
+  size_t kept = 0;
+  ~ScratchCache() {
+    for (auto& b : blocks) cudaFree(b.p);  // thread exit; fails harmlessly at process teardown
+  }
+  void* acquire(size_t bytes) {
+    int dev = 0;
+    VXM_SCK(cudaGetDevice(&dev));
+    ScratchBlock* best = nullptr;
+    for (auto& b : blocks)
+      if (!b.used && b.dev == dev && b.bytes >= bytes && (!best || b.bytes < best->bytes)) best = &b;
+    if (best) {
+      best->used = true;
+      return best->p;
+    }
+    size_t cap = 256;
+    while (cap < bytes) cap <<= 1;
+    void* p = nullptr;
+    if (cudaMalloc(&p, cap) != cudaSuccess) {  // drop the idle blocks and retry once
+      cudaGetLastError();
+      trim(0);
+      VXM_SCK(cudaMalloc(&p, cap));
+    }
+    blocks.push_back({dev, p, cap, true});
+    kept += cap;
+    return p;
+  }
+  void release(void* p) {
+    for (auto& b : blocks)
+      if (b.p == p) b.used = false;
+    trim(kScratchKeep);
+  }
+  void trim(size_t keep) {
+    for (size_t i = blocks.size(); i-- > 0 && kept > keep;)
+      if (!blocks[i].used) {
+        cudaFree(blocks[i].p);
+        kept -= blocks[i].bytes;
+        blocks.erase(blocks.begin() + static_cast<long>(i));
+      }
+  }
+};
+thread_local ScratchCache g_scratch;
+
+// RAII device buffer from the scratch cache.
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
   explicit DevBuf(size_t n) {
-    if (n) VXM_SCK(cudaMalloc(&p, sizeof(T) * n));
+    if (n) p = static_cast<T*>(g_scratch.acquire(sizeof(T) * n));
   }
-  ~DevBuf() { cudaFree(p); }
+  ~DevBuf() {
+    if (p) g_scratch.release(p);
+  }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
 };

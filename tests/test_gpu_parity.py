@@ -61,6 +61,28 @@ def test_merge_matches_reference_any_size_and_alignment(gpu_lib, n, offset):
     assert np.array_equal(loc, want)
 
 
+def test_stage_calls_reuse_scratch(gpu_lib):
+    # stage entry points draw their device buffers from a per-thread cache
+    # (no cudaMalloc/cudaFree per call): many calls of varying sizes stay
+    # bit-exact and leave the device's free memory where the first call left it
+    import torch
+
+    rng = np.random.default_rng(5)
+    sizes = [int(x) for x in rng.integers(1, 300_000, 40)]
+    vm.kernel_merge(np.zeros(300_000, np.uint8), np.zeros(300_000, np.uint8))
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    for n in sizes * 3:
+        loc = rng.integers(0, 4, n, dtype=np.uint8)
+        ms = rng.integers(0, 4, n, dtype=np.uint8)
+        want = loc.copy()
+        ref.merge(want, ms.copy())
+        vm.kernel_merge(loc, ms)
+        assert np.array_equal(loc, want), n
+    free1 = torch.cuda.mem_get_info()[0]
+    assert free0 - free1 < 64 << 20, (free0, free1)
+
+
 def test_transform_voxelize_known_answers(gpu_lib):
     # proj/tests/test_kernels.cpp:63-87: floor semantics and the +-1e9 clamp
     xs = np.array([0.05, 0.15, -0.05, 1e12, -1e12, 0.0])
