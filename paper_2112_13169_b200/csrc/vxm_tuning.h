@@ -80,6 +80,11 @@
 // queue (ncu mio_throttle 15x cfg1's); cfg1 (19,239 rays) 186.4 / 194.6 /
 // 195 / 198.7; cfg3 (76k rays) 299 / 305 / 308 / 311. Bundles of at least
 // VXM_TB_MATCH_RAYS rays take the large mask.
+// Re-swept at the final round-2 state (profiles/r02cu_knobs_ab.txt,
+// r02cx_knobs_ab.txt; bench frames/s at 50 steps, two reps, default 380k):
+// 16 / 24 K3 blocks per SM 365k / 370k, 4 branches 369k, 8 merge rows per
+// warp 364-368k, small-bundle mask 0x1 / 0x4 367-373k / 377-378k, near mask
+// 0x5 378-380k, K4 at 5 blocks per SM 379k: the defaults stay.
 #ifndef VXM_TB_MATCH_LARGE
 #define VXM_TB_MATCH_LARGE 0xF
 #endif
