@@ -2061,7 +2061,11 @@ __global__ void __launch_bounds__(256, VXM_MERGE_MINB) merge_epoch_kernel(KParam
           }
         }
       }
+#if VXM_MERGE_STCS
+      __stcs(reinterpret_cast<uint4*>(dst + c), make_uint4(out[0], out[1], out[2], out[3]));
+#else
       *reinterpret_cast<uint4*>(dst + c) = make_uint4(out[0], out[1], out[2], out[3]);
+#endif
       occ_n += count_occupied16(out);
       free_n += count_free16(out);
     }
@@ -2289,7 +2293,11 @@ __global__ void __launch_bounds__(256) merge_shift_count_kernel(KParams p, int r
           }
         }
       }
+#if VXM_MERGE_STCS
+      __stcs(reinterpret_cast<uint4*>(dst + c), make_uint4(out[0], out[1], out[2], out[3]));
+#else
       *reinterpret_cast<uint4*>(dst + c) = make_uint4(out[0], out[1], out[2], out[3]);
+#endif
       occ_n += count_occupied16(out);
       free_n += count_free16(out);
     }

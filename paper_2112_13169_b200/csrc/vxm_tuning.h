@@ -139,6 +139,13 @@
 // resident blocks per SM the direct-load K4 is compiled for (register cap):
 // 4 -> 64 registers; without a cap ptxas took 80 and K4 lost its rows-per-warp
 // gain (52 us, 324k frames/s); 5 -> 48 registers with a small spill (equal)
+// flat K4: the merged local grid stored with the streaming hint (it is read
+// again only by the next frame's K4) instead of a plain store. r02da, three
+// alternating reps, bench frames/s at 50 steps: 379.7k / 380.2k / 381.0k ->
+// 381.1k / 380.8k / 381.6k; cfg1 x64 234.6-235.2k -> 235.5-235.7k (kept)
+#ifndef VXM_MERGE_STCS
+#define VXM_MERGE_STCS 1
+#endif
 #ifndef VXM_MERGE_MINB
 #define VXM_MERGE_MINB 4
 #endif
