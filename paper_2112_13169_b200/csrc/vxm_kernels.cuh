@@ -198,7 +198,11 @@ __global__ void __launch_bounds__(256, VXM_POP_MINB) populate_depth_tma_kernel(K
       if (start >= nq) break;
       const uint32_t bytes = static_cast<uint32_t>(min(T, nq - start)) * 16u;
       mbar_expect_tx(&bar[i], bytes);
+#if VXM_POP_EVICT_FIRST
+      bulk_g2s_stream(sq + i * T, depth + static_cast<long long>(start) * 4, bytes, &bar[i]);
+#else
       bulk_g2s(sq + i * T, depth + static_cast<long long>(start) * 4, bytes, &bar[i]);
+#endif
     }
   }
   double R[9], t[3];

@@ -152,6 +152,14 @@
 // resident blocks per SM the TMA-staged K1 is compiled for (register cap):
 // 4 -> 64 registers (uncapped: 77, 3 blocks per SM): +2% frames/s; 5 and 6
 // (48 / 40 registers) spill and slow K1 itself
+// K1: the depth tiles' bulk copies carry an L2 evict-first policy (each
+// frame is read once) so they do not displace the occupancy bytes and keys
+// the other branches' kernels work on. r02dc, three alternating reps, bench
+// frames/s at 50 steps: 381.5k / 381.8k / 381.4k -> 383.4k / 383.5k / 384.5k,
+// populate+dilate 55.6 -> 54.7 us per 64 cfg2 frames (kept)
+#ifndef VXM_POP_EVICT_FIRST
+#define VXM_POP_EVICT_FIRST 1
+#endif
 #ifndef VXM_POP_MINB
 #define VXM_POP_MINB 4
 #endif
