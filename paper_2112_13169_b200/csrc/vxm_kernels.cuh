@@ -1111,6 +1111,15 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   uint32_t kv = ray_key;
   unsigned lw = 0, snap = 0xffffffffu;
   const unsigned long long key_base = reinterpret_cast<unsigned long long>(key);
+#if VXM_TB_RED_HINT
+  unsigned long long kpol;  // L2 evict-last on the keys K4 reads next
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(kpol));
+#define VXM_RED_MAX(V, P) "@ok red.relaxed.gpu.global.max.L2::cache_hint.u32 [a], " V ", " P ";\n\t"
+#define VXM_RED_POL , "l"(kpol)
+#else
+#define VXM_RED_MAX(V, P) "@ok red.relaxed.gpu.global.max.u32 [a], " V ";\n\t"
+#define VXM_RED_POL
+#endif
   // dedup bound: a cell is written when dup <= dup_max. With match.any, dup
   // is the mask of lanes on the same cell and no higher lane (higher ray
   // index) shares it exactly when dup <= lanemask_le (one compare instead of
@@ -1191,7 +1200,7 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   "setp.le.and.u32 ok, %7, %8, w;\n\t"   \
   "mul.wide.u32 a, %3, 4;\n\t"           \
   "add.u64 a, a, %6;\n\t"                \
-  "@ok red.relaxed.gpu.global.max.u32 [a], %0;\n\t" \
+  VXM_RED_MAX("%0", "%9") \
   "@io or.b32 %0, %0, 1;\n\t"
 #define VXM_RESOLVE_DECL                   \
   ".reg .pred v, io, w, ok;\n\t"         \
@@ -1207,7 +1216,7 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
   asm volatile("{\n\t" VXM_RESOLVE_DECL HEAD VXM_RESOLVE_BODY "}"               \
                : "+r"(kv), "+r"(lw), "+r"(snap)                                  \
                : "r"(cell[j]), "r"(o[j]), "r"(epoch), "l"(key_base), "r"(dup[j]),                 \
-                 "r"(((kMatchMask >> j) & 1) ? dup_max : 0u)                                       \
+                 "r"(((kMatchMask >> j) & 1) ? dup_max : 0u) VXM_RED_POL                           \
                : "memory")
       if constexpr (kTail)
         VXM_RESOLVE_ASM(VXM_RESOLVE_HEAD_TAIL);
@@ -1424,8 +1433,9 @@ __global__ void __launch_bounds__(32 * kTraceWarps, kMinBlocks) trace_bundle_ker
                        "setp.le.u32 ok, %1, %2;\n\t"
                        "mul.wide.u32 a, %0, 4;\n\t"
                        "add.u64 a, a, %3;\n\t"
-                       "@ok red.relaxed.gpu.global.max.u32 [a], %4;\n\t}"
+                       VXM_RED_MAX("%4", "%5") "}"
                        :: "r"(cell[j]), "r"(dup), "r"(((kNearMask >> j) & 1) ? dup_max : 0u), "l"(key_base), "r"(kv)
+                          VXM_RED_POL
                        : "memory");
         }
         lw += kChunk;

@@ -67,6 +67,13 @@
 #define VXM_TB_SPLIT_MAX_RAYS 32768
 #endif
 
+// K3: the key REDs carry an L2 evict-last policy (K4 reads the keys next).
+// r02de, three alternating reps: graph frames/s cfg2 x64 +0.4%, cfg1 x64
+// +0.2%, bench value inconclusive (380.9k / 383.4k / 382.5k against 383.5k /
+// 377.4k / 315.9k with an outlier): within noise, kept off
+#ifndef VXM_TB_RED_HINT
+#define VXM_TB_RED_HINT 0
+#endif
 #ifndef VXM_TB_MINB
 #define VXM_TB_MINB 20
 #endif
