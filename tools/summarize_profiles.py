@@ -122,7 +122,7 @@ def main():
           "dram__bytes_write.sum --clock-control none` of `bench.py --steps 2 --warmup 3` (cold-cache and "
           "serialised: compare shares, not absolutes). Per-kernel sections = `ncu --set full` of one launch in a "
           "batched cfg2 step (64 streams); merge_sequence from one 64-frame call of a single moving stream; "
-          "merge_tma (the TMA-staged K4 of rows longer than 128 cells) from a batched cfg3 step (8 streams).", ""]
+          "merge_tma (the TMA-staged K4 of rows that are not word-aligned or longer than 1024 cells) from 8 cfg2 frames on a 101x100x50 grid.", ""]
     gpu = RAW / f"{tag}_gpu.txt"
     if gpu.exists():
         md += ["```", gpu.read_text().strip(), "```", ""]
